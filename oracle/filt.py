@@ -1,0 +1,74 @@
+"""Cone (linear-decay) filter (oracle).  P:50 §2.4: weights "decaying linearly
+with distance up to a specified filter radius (rmin)"; H stored sparse, applied
+by sparse matrix multiplication.  SPEC S:183-216.
+
+H_ij = max(0, rmin - ||c_i - c_j||) for ||c_i - c_j|| < rmin (R#12), centroids
+(ex+.5, ey+.5, ez+.5); Hs_i = sum_j H_ij over in-domain j (R#13, truncated at
+the boundary).  Modes (R#10, R#11):
+  0 density filter      xPhys = (H x)/Hs (passive forced 0); dc~ = H(dc/Hs); dv~ = H(dv/Hs)
+  1 sensitivity filter  dc~_i = sum_j H_ij x_j dc_j / (Hs_i max(gamma, x_i)), gamma = 1e-3
+  2 plain               dc~ = (H dc)/Hs
+"""
+import numpy as np
+import scipy.sparse as sp
+
+GAMMA = 1e-3
+
+
+def filter_matrix(nelx, nely, nelz, rmin):
+    """H (CSR, symmetric) by enumerating every lattice offset of the box
+    |d| <= ceil(rmin) and keeping d < rmin; plus Hs = H 1."""
+    n_el = nelx * nely * nelz
+    ez, ex, ey = np.meshgrid(np.arange(nelz), np.arange(nelx), np.arange(nely), indexing="ij")
+    ex, ey, ez = ex.ravel(), ey.ravel(), ez.ravel()
+    e = np.arange(n_el)
+    R = int(np.ceil(rmin))
+    rows, cols, vals = [], [], []
+    for dz in range(-R, R + 1):
+        for dx in range(-R, R + 1):
+            for dy in range(-R, R + 1):
+                d = np.sqrt(float(dx * dx + dy * dy + dz * dz))
+                if not d < rmin:
+                    continue
+                jx, jy, jz = ex + dx, ey + dy, ez + dz
+                ok = (jx >= 0) & (jx < nelx) & (jy >= 0) & (jy < nely) & (jz >= 0) & (jz < nelz)
+                j = jz * nelx * nely + jx * nely + jy
+                rows.append(e[ok])
+                cols.append(j[ok])
+                vals.append(np.full(int(ok.sum()), rmin - d))
+    H = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n_el, n_el)).tocsr()
+    Hs = np.asarray(H.sum(axis=1)).ravel()
+    return H, Hs
+
+
+def filter_matrix_allpairs(centroids, rmin):
+    """Dense O(N^2) all-pairs H (brute force cross-check)."""
+    d = np.sqrt(((centroids[:, None, :] - centroids[None, :, :]) ** 2).sum(-1))
+    return np.where(d < rmin, rmin - d, 0.0)
+
+
+def apply_filter(H, Hs, mode, what, v, x=None, passive=None):
+    """One filter application.
+    what = "x"  : physical densities from design variables (mode 0), else identity
+    what = "dc" : filtered sensitivities
+    what = "dv" : filtered volume sensitivities
+    """
+    if what == "x":
+        if mode != 0:
+            return v.copy()
+        out = (H @ v) / Hs
+        if passive is not None:
+            out[np.asarray(passive) != 0] = 0.0
+        return out
+    if mode == 0:
+        return H @ (v / Hs)
+    if mode == 1:
+        if what == "dv":
+            return v.copy()
+        return (H @ (x * v)) / (Hs * np.maximum(GAMMA, x))
+    if mode == 2:
+        if what == "dv":
+            return v.copy()
+        return (H @ v) / Hs
+    raise ValueError(mode)
