@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the matrix-free SIMP hot path (BASELINE.json metric: seconds per
+SIMP iteration; PCG matvec GDOF/s; % of HBM roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A "step" is one SIMP iteration (modulus, PCG solve,
+sensitivities, filter, OC) of BASELINE config --config (default 4: the
+512x256x256 cantilever, 101.6 M DOF, fp64) with all inputs resident in HBM.
+Steps continue the optimisation (x evolves), so W warm-up + K timed steps of
+config 4 are its 5 BASELINE iterations.  N > 1: launched by torchrun, one rank
+per GPU, x-slab decomposition with NCCL (strong scaling).  Prints ONE JSON
+line on rank 0.  See DESIGN.md "Measurement" for every number's definition.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = dict(hbm_gbs=6650.0)   # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle as it stands, on a bounded x-slab sample of the
+# same workload, extrapolated to one full SIMP iteration.
+# ---------------------------------------------------------------------------
+def oracle_sample(p, n_cg, slab=8):
+    import oracle
+    from workloads import cantilever_fixed, random_vector
+    nelx, nely, nelz = p["nelx"], p["nely"], p["nelz"]
+    sx = min(slab, nelx)
+    n_el_s = sx * nely * nelz
+    KE = oracle.element_stiffness(p["nu"])
+    x = np.full(n_el_s, p["volfrac"])
+    E = p["Emin"] + x ** p["penal"] * (p["E0"] - p["Emin"])
+    fx = cantilever_fixed(sx, nely, nelz)
+    pv = random_vector(3 * (sx + 1) * (nely + 1) * (nelz + 1), seed=1)
+    t0 = time.perf_counter()
+    q = oracle.matvec_elementwise(sx, nely, nelz, KE, E, pv, fx)
+    t_mv = time.perf_counter() - t0
+    # one Jacobi-PCG iteration = matvec + 3 axpy + 2 dots + 1 scaling (numpy)
+    t0 = time.perf_counter()
+    r = pv.copy(); z = r * 0.5; pp = z.copy(); uu = np.zeros_like(r)
+    a = (r @ z) / (pp @ q); uu += a * pp; r -= a * q; z = 0.5 * r; pp = z + 0.3 * pp
+    t_vec = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    edof = oracle.edof_matrix(sx, nely, nelz)
+    ce = oracle.element_energies(q, KE, edof)
+    _, c, dc, dv = oracle.sensitivities(x, ce, p["penal"], p["E0"], p["Emin"])
+    t_sens = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    H, Hs = oracle.filter_matrix(sx, nely, nelz, p["rmin"])
+    dcf = oracle.apply_filter(H, Hs, 0, "dc", dc)
+    dvf = oracle.apply_filter(H, Hs, 0, "dv", dv)
+    t_filt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    xn, lam, V, npass = oracle.oc_update(x, dcf, dvf, p["volfrac"], p["move"], p["oc_tol"],
+                                         p["oc_lmax"], 0, H, Hs)
+    oracle.apply_filter(H, Hs, 0, "x", xn)
+    t_oc = time.perf_counter() - t0
+    scale = (nelx * nely * nelz) / n_el_s
+    est = n_cg * (t_mv + t_vec) * scale + (t_sens + t_filt + t_oc) * scale
+    sample = (f"oracle on an x-slab of {sx}x{nely}x{nelz} elements ({n_el_s} el): element-loop "
+              f"matvec {t_mv:.2f}s + PCG vector ops {t_vec:.2f}s, ce/dc {t_sens:.2f}s, filter "
+              f"{t_filt:.2f}s, OC ({npass} passes) {t_oc:.2f}s; scaled x{scale:.0f} to the full "
+              f"grid with N_cg={n_cg} PCG iterations per SIMP iteration")
+    return est, sample, (t_mv + t_vec + t_sens + t_filt + t_oc)
+
+
+def cores_used():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, cfg_p, world, rank):
+    """--impl reference: the oracle as it stands."""
+    if rank != 0:
+        return
+    n_cg = args.ref_ncg
+    if n_cg is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", f"ncg_cfg{args.config}.json")) as fh:
+                n_cg = int(json.load(fh)["cg_iters_per_simp_iteration"])
+        except Exception:
+            n_cg = int(round(6.6 * cfg_p["nelx"]))
+    vals, sample = [], ""
+    for i in range(args.warmup + args.steps):
+        est, sample, wall = oracle_sample(cfg_p, n_cg, slab=args.ref_slab)
+        if i >= args.warmup:
+            vals.append(est)
+    v = float(np.mean(vals))
+    line = {"impl": "reference", "metric": "s per SIMP iteration", "value": v,
+            "unit": "s/iteration", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, cfg_p, world),
+            "cpu_baseline": {"value": v, "unit": "s/iteration", "cores": cores_used(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "s/iteration", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, p, world):
+    n_nd = (p["nelx"] + 1) * (p["nely"] + 1) * (p["nelz"] + 1)
+    return {"workload": f"BASELINE config {args.config}: cantilever {p['nelx']}x{p['nely']}x{p['nelz']} "
+                        f"Hex8, fp64, volfrac {p['volfrac']}, rmin {p['rmin']}, PCG rtol {p['cg_rtol']}",
+            "nelx": p["nelx"], "nely": p["nely"], "nelz": p["nelz"], "n_dof": 3 * n_nd,
+            "filter": "density (mode 0)", "parallelism": f"x-slab{world}",
+            "l2": "inputs larger than L2 (one DOF vector = %.0f MB)" % (3 * n_nd * 8 / 1e6)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--matvec-reps", type=int, default=50)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-ncg", type=int, default=None)
+    ap.add_argument("--ref-slab", type=int, default=8)
+    args = ap.parse_args()
+
+    from workloads import make_problem
+    world, rank, local = dist_env()
+    p, f, fx, pas = make_problem(args.config)
+
+    if args.impl == "reference":
+        run_reference(args, p, world, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    pg = None
+    if world > 1:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = td
+    from paper_2504_05604_b200 import topo
+    if world > 1:
+        obj = [topo.nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(obj, src=0)
+        dist = dict(mode=topo.TOPO_DIST_NCCL, rank=rank, world=world, device=local, nccl_id=obj[0])
+
+    stream = torch.cuda.Stream()
+    pr = topo.Problem(p, f, fx, pas, dist=dist)
+    pr.set_stream(stream.cuda_stream)
+    n_dof = pr.count("ndof")
+    n_el = pr.count("nel")
+    n_nd = pr.count("nodes")
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    def max_over_ranks(v):
+        if pg is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up SIMP iterations (untimed) ----
+    cg_warm = []
+    for _ in range(args.warmup):
+        pr.optimize(1)
+        cg_warm.append(pr.timings()["cg_iters"])
+
+    # ---- timed SIMP iterations (device-resident inputs) ----
+    pr.profile(True)
+    l0 = pr.timings()["kernel_launches"]
+    cg_timed, phase = [], []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                c_hist, _, _ = pr.optimize(1)
+                t = pr.timings()
+                cg_timed.append(t["cg_iters"])
+                phase.append({k: t[k] for k in ("ms_efield", "ms_solve", "ms_sens", "ms_filter", "ms_oc")})
+            e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    launches = pr.timings()["kernel_launches"] - l0
+    mv_ms, mv_samples = pr.kernel_time()
+    pr.profile(False)
+    clocks = clk.summary()
+    s_per_iter = ms_total / 1e3 / args.steps
+
+    # ---- standalone matvec GDOF/s (device-resident, CUDA events on the stream) ----
+    from workloads import random_vector
+    pr.matvec_load(random_vector(3 * n_nd, seed=1))
+    pr.matvec_run(3)
+    torch.cuda.synchronize()
+    barrier()
+    with torch.cuda.stream(stream):
+        m0 = torch.cuda.Event(enable_timing=True)
+        m1 = torch.cuda.Event(enable_timing=True)
+        m0.record(stream)
+        pr.matvec_run(args.matvec_reps)
+        m1.record(stream)
+    torch.cuda.synchronize()
+    mv_standalone_ms = max_over_ranks(m0.elapsed_time(m1) / args.matvec_reps)
+    gdofs = n_dof / (mv_standalone_ms * 1e-3) / 1e9
+
+    # ---- end-to-end through the C ABI with pinned host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        x_host = torch.empty(n_el, dtype=torch.float64, pin_memory=True).numpy()
+        x_out = torch.empty(n_el, dtype=torch.float64, pin_memory=True).numpy()
+        x_host[:] = pr.get("x")
+        torch.cuda.synchronize()
+        barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            pr.filter("x", x_host, want=False)          # H2D design variables, xPhys = H x / Hs
+            c_e2e, _, _ = pr.optimize(1, x_out=x_out)    # one SIMP iteration, D2H x and c
+            x_host[:] = x_out
+        torch.cuda.synchronize()
+        w1 = time.perf_counter()
+        e2e_s = max_over_ranks((w1 - w0) / args.e2e_steps)
+        e2e = {"value": e2e_s, "unit": "s/iteration", "h2d_bytes_per_step": 8 * n_el,
+               "d2h_bytes_per_step": 8 * n_el + 8}
+
+    peaks, peaks_src = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    # dominant kernel: the PCG matvec k_matvec<true>; algorithmic bytes per launch
+    # = read p (24 B/node) + E (8 B/el) + write q (24 B/node)  [SURVEY §8(d): 16 B/DOF + 8 B/el]
+    own_el = n_el // world
+    own_nd = n_nd // world
+    mv_bytes = 48 * own_nd + 8 * own_el
+    achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "kernel": "k_matvec<true> (PCG q = K p, fused p.q)", "samples": mv_samples,
+            "mean_ms": mv_ms, "bytes_per_launch": mv_bytes, "peak_source": peaks_src}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_cg = int(np.mean(cg_timed))
+        est, sample, wall = oracle_sample(p, n_cg)
+        cpu = {"value": est, "unit": "s/iteration", "cores": 1, "kind": "oracle",
+               "sample": sample + f" (wall {wall:.1f}s; SciPy sparse kernels single-threaded)"}
+        try:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", f"ncg_cfg{args.config}.json"), "w") as fh:
+                json.dump({"cg_iters_per_simp_iteration": n_cg, "per_step": cg_timed}, fh)
+        except Exception:
+            pass
+
+    if rank == 0:
+        line = {"metric": "s per SIMP iteration", "value": s_per_iter, "unit": "s/iteration",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_total / args.steps, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload_config(args, p, world),
+                "matvec_gdofs": gdofs, "matvec_ms": mv_standalone_ms,
+                "cg_iters_per_step": cg_timed, "cg_iters_warmup": cg_warm,
+                "ms_per_cg_iter": [ph["ms_solve"] / max(1, n) for ph, n in zip(phase, cg_timed)],
+                "phase_ms": phase, "c_last": float(c_hist[-1]),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    pr.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

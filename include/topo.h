@@ -1,0 +1,244 @@
+/*
+ * topo.h -- C ABI of the B200-native matrix-free SIMP hot path
+ * (PyTopo3D, arXiv 2504.05604; PAPER.md = "P:line", SPEC.md = "S:line").
+ *
+ * One call per step of the paper's optimisation loop (§2.5):
+ *   topo_init         problem statement: grid, material, loads, supports,
+ *                     passive (obstacle) regions              P:42 §2.2, §2.3
+ *   topo_set_density  design variables x (pseudo-densities)   P:45 §2.3
+ *   topo_solve        K(x) u = f, matrix-free EbE Jacobi-PCG  P:42 §2.2
+ *   topo_sensitivity  ce = u_e^T KE u_e, c, dc                P:47 §2.3
+ *   topo_filter       rmin cone filter (density / sensitivity) P:50 §2.4
+ *   topo_oc_step      OC bisection with move limits            P:44-47 §2.3
+ *   topo_optimize     the whole loop for n_iter iterations      P:53 §2.5
+ *
+ * Conventions
+ *  - Every call returns int: TOPO_OK (0) or a TOPO_E* code.  No call throws,
+ *    aborts or exits.  topo_last_error(ctx) has a one-line explanation.
+ *  - Arithmetic is IEEE binary64 throughout (the BASELINE configs say fp64).
+ *  - Host arrays use the EXTERNAL numbering of SPEC S:45:
+ *        node    n(ix,iy,iz) = iz*(nelx+1)*(nely+1) + ix*(nely+1) + iy
+ *        element e(ex,ey,ez) = ez*nelx*nely + ex*nely + ey
+ *        DOFs of node n: 3n, 3n+1, 3n+2 = (ux, uy, uz)
+ *    The device layout is private (x-slab SoA).
+ *  - Ownership: the caller owns every host buffer.  Inputs are copied before
+ *    the call returns and never retained.  Outputs go to caller-allocated
+ *    buffers of the documented length; a NULL output is skipped.  The context
+ *    owns all device memory until topo_destroy.
+ *  - Multi-GPU (x-slabs): with dist->mode == TOPO_DIST_NCCL each rank passes
+ *    GLOBAL-size inputs; outputs are written only for that rank's owned
+ *    elements [ex_begin, ex_end) x all y,z (and the matching node planes);
+ *    entries of other ranks are left untouched (gathering is the caller's job).
+ *    TOPO_DIST_LOOPBACK runs `world` slabs in ONE process on one GPU (tests
+ *    the partition and halo logic); outputs are then complete.
+ *  - Threading: one context per thread; distinct contexts are independent.
+ *  - Call order: init -> [set_density] -> solve -> sensitivity -> filter(dc)
+ *    -> oc_step.  A call whose inputs are not ready returns TOPO_ESTATE.
+ */
+#ifndef TOPO_H
+#define TOPO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes (mapped from SPEC's error kinds) ---------- */
+#define TOPO_OK              0
+#define TOPO_EINVAL          1  /* bad dims/params, load on a fixed DOF */
+#define TOPO_ENOCONV         2  /* PCG hit cg_max_iter (S:138 SingularSystem)               */
+#define TOPO_EBREAKDOWN      3  /* PCG p^T K p <= 0 or non-finite                           */
+#define TOPO_EUNCONSTRAINED  4  /* no fixed DOF (S:138 InsufficientConstraints)             */
+#define TOPO_EBISECT         5  /* volume target unreachable in [0, oc_lmax]         */
+#define TOPO_EALLPASSIVE     6  /* no design element                                */
+#define TOPO_ECUDA           7
+#define TOPO_ENCCL           8
+#define TOPO_ENOMEM          9
+#define TOPO_ESTATE         10  /* call order / missing input                               */
+
+/* ---- filter modes (§2.4; reading R#10) -------------------- */
+#define TOPO_FILTER_DENSITY     0  /* xPhys = H x / Hs ; dc~ = H(dc/Hs) ; dv~ = H(dv/Hs)     */
+#define TOPO_FILTER_SENSITIVITY 1  /* dc~_i = sum_j H_ij x_j dc_j / (Hs_i max(1e-3, x_i))   */
+#define TOPO_FILTER_PLAIN       2  /* dc~ = H dc / Hs                                       */
+
+/* topo_filter `what` */
+#define TOPO_FILTER_X   0   /* design variables -> physical densities                */
+#define TOPO_FILTER_DC  1   /* raw sensitivities -> filtered sensitivities            */
+
+/* topo_get fields.  Element fields are [n_el], node fields [3*n_nd] (DOF
+ * interleaved, like u) unless noted.                                        */
+#define TOPO_FIELD_U        0  /* displacements [3*n_nd]                         */
+#define TOPO_FIELD_X        1  /* design variables [n_el]                        */
+#define TOPO_FIELD_XPHYS    2  /* physical densities [n_el]                      */
+#define TOPO_FIELD_E        3  /* SIMP modulus E_e [n_el]                        */
+#define TOPO_FIELD_CE       4  /* element energies u_e^T KE u_e [n_el]           */
+#define TOPO_FIELD_DC       5  /* raw sensitivities [n_el]                       */
+#define TOPO_FIELD_DCF      6  /* filtered sensitivities [n_el]                  */
+#define TOPO_FIELD_DVF      7  /* filtered volume sensitivities [n_el]           */
+#define TOPO_FIELD_XNEW     8  /* last OC result [n_el]                          */
+#define TOPO_FIELD_HS       9  /* filter row sums Hs [n_el]                      */
+#define TOPO_FIELD_INVDIAG 10  /* Jacobi inverse diagonal per DOF [3*n_nd], 0 on fixed */
+#define TOPO_FIELD_R       11  /* PCG recursive residual [3*n_nd]               */
+
+/* distribution modes */
+#define TOPO_DIST_SINGLE   0
+#define TOPO_DIST_NCCL     1
+#define TOPO_DIST_LOOPBACK 2
+
+typedef struct topo_ctx topo_ctx;    /* opaque; owns all device state */
+
+/* Problem parameters.  Fill with topo_params_default first. */
+typedef struct {
+  int32_t nelx, nely, nelz;   /* elements per axis, >= 1; unit cubes           */
+  double  volfrac;            /* 0 < volfrac < 1: target mean density over design elements  */
+  double  penal;              /* SIMP exponent p >= 1 ("commonly p = 3")              */
+  double  rmin;               /* filter radius in element lengths, 0 < rmin <= 6     */
+  double  E0, Emin;           /* 0 < Emin < E0                                       */
+  double  nu;                 /* Poisson ratio 0 <= nu < 0.5                        */
+  double  move;               /* OC move limit 0 < move <= 1 ("standard move limits")  */
+  int32_t filter_mode;        /* TOPO_FILTER_*                                              */
+  double  cg_rtol;            /* stop when ||r|| <= cg_rtol ||f_free|| (then true residual) */
+  int64_t cg_max_iter;        /* <= 0 -> 10 * n_dof                                  */
+  int32_t cg_warm_start;      /* 1: start PCG from the previous u                            */
+  double  oc_tol;             /* bisection stops when (l2-l1)/(l1+l2) <= oc_tol              */
+  double  oc_lmax;            /* initial bracket [0, oc_lmax]                                */
+  int32_t deterministic;      /* reductions are always fixed-order; kept for the ABI */
+  int32_t cg_check_every;     /* PCG iterations per CUDA-graph batch between host polls; <=0 auto */
+} topo_params;
+
+typedef struct {
+  int32_t mode;               /* TOPO_DIST_SINGLE / _NCCL / _LOOPBACK                       */
+  int32_t rank, world;        /* NCCL: this rank, #ranks; LOOPBACK: world = #slabs          */
+  int32_t device;             /* CUDA device ordinal of this rank                            */
+  const uint8_t *nccl_id;     /* NCCL: 128-byte ncclUniqueId broadcast by the caller         */
+} topo_dist;
+
+typedef struct {
+  int64_t iters;              /* PCG iterations of the last solve                            */
+  double  rel_res;            /* recursive ||r||/||f_free|| at exit                          */
+  double  true_rel_res;       /* ||f - K u||/||f_free|| recomputed at exit                   */
+  double  ms;                 /* device time of the solve (CUDA events)                      */
+  int32_t replacements;       /* residual replacements performed                             */
+} topo_solve_info;
+
+typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulative counters  */
+  double  ms_efield, ms_solve, ms_sens, ms_filter, ms_oc, ms_total;
+  int64_t cg_iters;
+  int32_t oc_passes;
+  double  c, fu, volume, change, lambda;
+  int64_t kernel_launches;    /* cumulative count of this library's kernel launches          */
+  int64_t cg_iters_total;     /* cumulative PCG iterations                                   */
+} topo_timings;
+
+/* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,
+ * move 0.2, density filter, cg_rtol 1e-8, oc_tol 1e-10, oc_lmax 1e9). */
+void topo_params_default(topo_params *p);
+
+/* Create a context.  load: [3*n_nd] nodal forces (must be 0 on fixed DOFs).
+ * fixed: [3*n_nd] 0/1 Dirichlet mask (u = 0 where 1, elimination).
+ * passive: [n_el] 0/1 non-design (void) mask or NULL.
+ * dist: NULL -> one GPU (current device).  Errors: EINVAL, EUNCONSTRAINED,
+ * EALLPASSIVE, ENOMEM, ECUDA, ENCCL.  On error *out is NULL.              */
+int topo_init(const topo_params *p, const double *load, const uint8_t *fixed,
+              const uint8_t *passive, const topo_dist *dist, topo_ctx **out);
+
+/* Bind the CUDA stream (cudaStream_t as void*) every later call launches
+ * on.  NULL/0 -> the context's own non-blocking stream.                    */
+int topo_set_stream(topo_ctx *ctx, void *stream);
+
+/* Owned element range along x of this rank: [ex_begin, ex_end).           */
+int topo_owned_range(const topo_ctx *ctx, int32_t *ex_begin, int32_t *ex_end);
+
+/* Design variables x [n_el] (host).  NULL -> volfrac on design, 0 on passive.
+ * Passive entries are forced to 0.  Sets xPhys = x (reading R#18: the first
+ * iteration is unfiltered).                                                 */
+int topo_set_density(topo_ctx *ctx, const double *x);
+
+/* Set physical densities directly (xPhys, [n_el]); passive forced to 0.    */
+int topo_set_xphys(topo_ctx *ctx, const double *xphys);
+
+/* Solve K(xPhys) u = f on free DOFs (Jacobi-PCG, matrix-free).  Computes
+ * E = Emin + xPhys^p (E0-Emin) first.  u: [3*n_nd] output or NULL.
+ * Errors: ENOCONV, EBREAKDOWN (u keeps the last iterate).                   */
+int topo_solve(topo_ctx *ctx, double *u, topo_solve_info *info);
+
+/* After topo_solve: ce_e = u_e^T KE u_e, c = sum_e E_e ce_e,
+ * dc_e = -p xPhys^(p-1) (E0-Emin) ce_e (0 on passive).  c: scalar out.
+ * ce, dc: [n_el] or NULL.                                                   */
+int topo_sensitivity(topo_ctx *ctx, double *c, double *ce, double *dc);
+
+/* One filter application.  what = TOPO_FILTER_DC: in = raw dc [n_el] (NULL ->
+ * the context's dc from topo_sensitivity), out = dc~ [n_el] or NULL; also
+ * prepares dv~.  what = TOPO_FILTER_X: in = x [n_el] (NULL -> current x),
+ * out = xPhys [n_el] or NULL, and the context's xPhys is replaced.          */
+int topo_filter(topo_ctx *ctx, int32_t what, const double *in, double *out);
+
+/* OC bisection on the context's x, dc~, dv~ (after topo_filter(DC)).
+ * xnew: [n_el] or NULL.  Scalars: final lambda (last lmid), change =
+ * max |xnew - x| over design elements, volume = mean design xPhys(xnew)
+ * (mode 0) / mean design xnew (modes 1, 2).  Then x <- xnew and
+ * xPhys <- filter(x).  Errors: EBISECT.                                      */
+int topo_oc_step(topo_ctx *ctx, double *xnew, double *lambda, double *change, double *volume);
+
+/* The loop: n_iter x (solve, sensitivity, filter, oc).  c_hist [n_iter]
+ * (compliance of the design entering each iteration), x_out [n_el] final
+ * design, n_done iterations completed (partial on error).
+ * change_tol > 0 stops early when change < change_tol.                      */
+int topo_optimize(topo_ctx *ctx, int32_t n_iter, double change_tol, double *c_hist,
+                  double *x_out, int32_t *n_done);
+
+/* q = K(E) p with the Dirichlet mask (q = 0 on fixed DOFs, p read as 0
+ * there), using the current E (topo_solve / topo_update_modulus).  Host
+ * p, q: [3*n_nd].  Test / GDOF-s hook.                                      */
+int topo_apply_K(topo_ctx *ctx, const double *p, double *q);
+
+/* Recompute E (and the Jacobi diagonal) from the current xPhys.            */
+int topo_update_modulus(topo_ctx *ctx);
+
+/* Benchmark hooks (device-resident operands).  topo_matvec_load copies a
+ * host p [3*n_nd] into the internal matvec operand; topo_matvec_run launches
+ * `reps` back-to-back matvec kernels on the bound stream (no host sync).   */
+int topo_matvec_load(topo_ctx *ctx, const double *p);
+int topo_matvec_run(topo_ctx *ctx, int32_t reps);
+
+/* Read a field (TOPO_FIELD_*) in external numbering.                        */
+int topo_get(topo_ctx *ctx, int32_t field, double *out);
+
+int topo_get_timings(const topo_ctx *ctx, topo_timings *t);
+
+/* Live kernel timing inside the timed region: when enabled, the PCG driver
+ * brackets one matvec launch per CUDA-graph batch with CUDA events on the
+ * bound stream.  topo_kernel_time returns the mean matvec duration (ms) and
+ * the number of samples since the last reset.                               */
+int topo_profile(topo_ctx *ctx, int32_t enable);
+int topo_kernel_time(topo_ctx *ctx, double *mean_ms, int64_t *samples);
+
+/* The element stiffness the library uses (24x24 row-major, unit cube,
+ * E = 1, 2x2x2 Gauss; "pre-computed").  No context needed.    */
+int topo_element_stiffness(double nu, double *ke576);
+
+/* Number of layout/grid facts for tests: n_dof, n_el, owned nodes, etc.    */
+int64_t topo_count(const topo_ctx *ctx, int32_t what);
+#define TOPO_COUNT_NDOF        0
+#define TOPO_COUNT_NEL         1
+#define TOPO_COUNT_NODES       2
+#define TOPO_COUNT_DESIGN      3
+#define TOPO_COUNT_STENCIL     4   /* filter stencil points                   */
+#define TOPO_COUNT_DEVICE_BYTES 5  /* device memory held by the context        */
+
+/* NCCL mode helper: fill a 128-byte ncclUniqueId (rank 0 calls it and
+ * broadcasts the bytes, e.g. with torch.distributed).  ENCCL if libnccl.so.2
+ * cannot be loaded.                                                          */
+int topo_nccl_unique_id(uint8_t *out128);
+
+const char *topo_last_error(const topo_ctx *ctx);
+const char *topo_strerror(int code);
+const char *topo_version(void);
+void topo_destroy(topo_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPO_H */

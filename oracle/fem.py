@@ -136,3 +136,35 @@ def true_residual(K, u, f, fixed):
     free = np.asarray(fixed) == 0
     r = (f - K @ np.where(free, u, 0.0))[free]
     return float(np.linalg.norm(r) / np.linalg.norm(f[free]))
+
+
+def matvec_rows(nelx, nely, nelz, KE, E, p, fixed, nodes):
+    """Rows q_n (3 per node) of the masked operator for a list of node ids,
+    by brute force over each node's (up to 8) elements.  For sampled parity
+    checks on grids whose full matvec is too large for the oracle."""
+    from .mesh import LOCAL_NODES
+    fx = np.asarray(fixed) != 0
+    pm = np.where(fx, 0.0, p)
+    nxy = (nelx + 1) * (nely + 1)
+    out = np.zeros((len(nodes), 3))
+    for k, n in enumerate(nodes):
+        iz, rem = divmod(int(n), nxy)
+        ix, iy = divmod(rem, nely + 1)
+        for ez in (iz - 1, iz):
+            for ex in (ix - 1, ix):
+                for ey in (iy - 1, iy):
+                    if not (0 <= ex < nelx and 0 <= ey < nely and 0 <= ez < nelz):
+                        continue
+                    e = ez * nelx * nely + ex * nely + ey
+                    dofs = []
+                    ln = None
+                    for a, (dx, dy, dz) in enumerate(LOCAL_NODES):
+                        m = (ez + dz) * nxy + (ex + dx) * (nely + 1) + (ey + dy)
+                        if m == n:
+                            ln = a
+                        dofs += [3 * m, 3 * m + 1, 3 * m + 2]
+                    out[k] += E[e] * (KE[3 * ln:3 * ln + 3] @ pm[dofs])
+        for c in range(3):
+            if fx[3 * n + c]:
+                out[k, c] = 0.0
+    return out

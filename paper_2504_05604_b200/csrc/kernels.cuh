@@ -1,0 +1,565 @@
+// sm_100a kernels of the SIMP hot path.
+// fp64 throughout; no tensor cores (tcgen05 has no f64 kind).
+#pragma once
+#include "common.cuh"
+
+namespace topo {
+
+constexpr int kMaxStencil = 1331;      // (2R+1)^3 for R <= 5 (rmin <= 6)
+__constant__ double c_KE[576];          // element stiffness, row-major 24x24
+__constant__ int4 c_st_off[kMaxStencil];  // filter stencil offsets (dx, dy, dz, -)
+__constant__ double c_st_w[kMaxStencil];  // rmin - |d|
+
+struct Material { double E0, Emin, penal, kd; };
+
+// local index of the element corner (a,b,c) in SPEC S:45 order
+__host__ __device__ constexpr int lidx(int a, int b, int c) {
+  return 4 * c + (b ? (a ? 2 : 3) : (a ? 1 : 0));
+}
+
+__device__ __forceinline__ bool decode_node(const Geo& g, long long i, int& ix, int& iy, int& iz) {
+  const long long pl = i / g.nplane;
+  const int rem = (int)(i - pl * g.nplane);
+  const int zs = rem / g.NY, ys = rem - zs * g.NY;
+  ix = (int)pl - 1 + g.ex0;
+  iy = ys - 1;
+  iz = zs - 1;
+  return (ys >= 1) & (ys <= g.nely + 1) & (zs >= 1) & (zs <= g.nelz + 1);
+}
+__device__ __forceinline__ bool decode_elem(const Geo& g, long long i, int& ex, int& ey, int& ez) {
+  const long long pl = i / g.eplane;
+  const int rem = (int)(i - pl * g.eplane);
+  const int zs = rem / g.EY, ys = rem - zs * g.EY;
+  ex = (int)pl - g.H + g.ex0;
+  ey = ys - 1;
+  ez = zs - 1;
+  return (ys >= 1) & (ys <= g.nely) & (zs >= 1) & (zs <= g.nelz);
+}
+
+// ===========================================================================
+// A1  SIMP modulus  E_e = Emin + xPhys_e^p (E0 - Emin)          (§2.3)
+//     over every in-domain element of the local array (owned + halos).
+// ===========================================================================
+__global__ void k_efield(Geo g, Material m, const double* __restrict__ xphys,
+                         double* __restrict__ E) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez) || ex < 0 || ex >= g.nelx) continue;
+    E[i] = m.Emin + pow(xphys[i], m.penal) * (m.E0 - m.Emin);
+  }
+}
+
+// Jacobi inverse diagonal per DOF: 1/(kd * sum_{e ni n} E_e), 0 on fixed DOFs.
+// diag(K) is one scalar per node because every KE_ii = (lambda+4mu)/9.
+__global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
+                          const uint8_t* __restrict__ fixm, double* __restrict__ invd) {
+  const long long b = g.nplane, e = (long long)(g.nown + 1) * g.nplane;
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    if (!decode_node(g, i, ix, iy, iz)) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d)
+      s += E[elem_idx(g, ix - 1 + (d & 1), iy - 1 + ((d >> 1) & 1), iz - 1 + (d >> 2))];
+    const double v = 1.0 / (m.kd * s);
+    const uint8_t fm = fixm[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) invd[c * g.ncomp + i] = (fm >> c) & 1 ? 0.0 : v;
+  }
+}
+
+// ===========================================================================
+// A2  EbE matvec  q_n = sum_{e ni n} E_e KE[ln,:] p_e, q = 0 on fixed DOFs.
+// Node-centric gather: each thread owns one node, loops over its 27
+// neighbours once (3 loads each) and accumulates the 8 element row-blocks;
+// all KE indices are compile-time constants (constant-bank operands).
+// ===========================================================================
+template <bool kDot>
+__global__ void __launch_bounds__(kBlock)
+k_matvec(Geo g, DevState* st, int gate, const double* __restrict__ E,
+         const double* __restrict__ p, const uint8_t* __restrict__ fixm,
+         double* __restrict__ q, double* partials, unsigned int* counter, int finish) {
+  if (gate && st->done) return;
+  const long long b0 = g.nplane, e0 = (long long)(g.nown + 1) * g.nplane;
+  double dot = 0.0;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    if (!decode_node(g, i, ix, iy, iz)) continue;
+    double s[8][3];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s[e][0] = s[e][1] = s[e][2] = 0.0;
+#pragma unroll
+    for (int oz = -1; oz <= 1; ++oz)
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox)
+#pragma unroll
+        for (int oy = -1; oy <= 1; ++oy) {
+          const long long j = i + ox * g.nplane + oz * g.NY + oy;
+          const double p0 = p[j], p1 = p[j + g.ncomp], p2 = p[j + 2 * g.ncomp];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int dx = e & 1, dy = (e >> 1) & 1, dz = e >> 2;
+            const int a = ox + 1 - dx, bb = oy + 1 - dy, c = oz + 1 - dz;
+            if (a < 0 || a > 1 || bb < 0 || bb > 1 || c < 0 || c > 1) continue;
+            const int ln = lidx(1 - dx, 1 - dy, 1 - dz), lm = lidx(a, bb, c);
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) {
+              const int r = (3 * ln + ci) * 24 + 3 * lm;
+              s[e][ci] = fma(c_KE[r + 0], p0, s[e][ci]);
+              s[e][ci] = fma(c_KE[r + 1], p1, s[e][ci]);
+              s[e][ci] = fma(c_KE[r + 2], p2, s[e][ci]);
+            }
+          }
+        }
+    double qv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const double Ee = E[elem_idx(g, ix - 1 + (e & 1), iy - 1 + ((e >> 1) & 1), iz - 1 + (e >> 2))];
+#pragma unroll
+      for (int ci = 0; ci < 3; ++ci) qv[ci] = fma(Ee, s[e][ci], qv[ci]);
+    }
+    const uint8_t fm = fixm[i];
+#pragma unroll
+    for (int ci = 0; ci < 3; ++ci) {
+      const double v = (fm >> ci) & 1 ? 0.0 : qv[ci];
+      q[i + ci * g.ncomp] = v;
+      if (kDot) dot = fma(p[i + ci * g.ncomp], v, dot);
+    }
+  }
+  if (kDot) {
+    __shared__ double tot[1];
+    double v[1] = {dot};
+    if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) {
+      if (finish) {
+        st->pq = tot[0];
+        if (!(tot[0] > 0.0) || !isfinite(tot[0])) {
+          st->status = 3;
+          st->done = 1;
+        } else {
+          st->alpha = st->rz / tot[0];
+        }
+      } else {
+        st->sums[0] = tot[0];
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// A3/A4  PCG vector kernels over the owned node planes (pads are zero and
+// stay zero).  SoA: component stride ncomp.
+// ===========================================================================
+// p = M^{-1} r + beta p   (beta = 0 on a fresh start)
+__global__ void k_pupdate(Geo g, DevState* st, const double* __restrict__ r,
+                          const double* __restrict__ invd, double* __restrict__ p) {
+  if (st->done) return;
+  const double beta = st->fresh ? 0.0 : st->beta;
+  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
+    p[i] = fma(beta, p[i], invd[i] * r[i]);
+  }
+}
+
+__device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, double rr) {
+  st->beta = rz_new / st->rz;
+  st->rz = rz_new;
+  st->rr = rr;
+  st->it += 1;
+  st->fresh = 0;
+  if (!isfinite(rr) || !isfinite(rz_new)) {
+    st->status = 3;
+    st->done = 1;
+  } else if (rr <= st->tol2 * st->bb) {
+    st->done = 1;
+  } else if (st->it >= st->max_it) {
+    st->status = 2;
+    st->done = 1;
+  }
+}
+
+// u += alpha p ; r -= alpha q ; partial (r M^{-1} r, r r)
+__global__ void __launch_bounds__(kBlock)
+k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
+         const double* __restrict__ p, const double* __restrict__ q,
+         const double* __restrict__ invd, double* partials, unsigned int* counter, int finish) {
+  if (st->done) return;
+  const double alpha = st->alpha;
+  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  double rz = 0.0, rr = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
+    u[i] = fma(alpha, p[i], u[i]);
+    const double rv = fma(-alpha, q[i], r[i]);
+    r[i] = rv;
+    rz = fma(rv * invd[i], rv, rz);
+    rr = fma(rv, rv, rr);
+  }
+  __shared__ double tot[2];
+  double v[2] = {rz, rr};
+  if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
+    if (finish) cg_finish_update(st, tot[0], tot[1]);
+    else { st->sums[0] = tot[0]; st->sums[1] = tot[1]; }
+  }
+}
+
+// Multi-slab finish kernels (after the allreduce of st->sums).
+__global__ void k_finish_alpha(DevState* st) {
+  if (st->done) return;
+  const double pq = st->sums[0];
+  st->pq = pq;
+  if (!(pq > 0.0) || !isfinite(pq)) { st->status = 3; st->done = 1; }
+  else st->alpha = st->rz / pq;
+}
+__global__ void k_finish_update(DevState* st) {
+  if (st->done) return;
+  cg_finish_update(st, st->sums[0], st->sums[1]);
+}
+
+// r = f - q (masked by construction: q and f are 0 on fixed DOFs); partial
+// (r M^{-1} r, r r).  Used at PCG start and for the true-residual check.
+__global__ void __launch_bounds__(kBlock)
+k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __restrict__ q,
+           const double* __restrict__ invd, double* __restrict__ r, int write_r,
+           double* partials, unsigned int* counter) {
+  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  double rz = 0.0, rr = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
+    const double rv = f[i] - q[i];
+    if (write_r) r[i] = rv;
+    rz = fma(rv * invd[i], rv, rz);
+    rr = fma(rv, rv, rr);
+  }
+  __shared__ double tot[2];
+  double v[2] = {rz, rr};
+  if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
+    st->sums[0] = tot[0];
+    st->sums[1] = tot[1];
+  }
+}
+
+// generic dot over owned node planes: sums[slot] = a . b
+__global__ void __launch_bounds__(kBlock)
+k_dot(Geo g, DevState* st, const double* __restrict__ a, const double* __restrict__ b,
+      int slot, double* partials, unsigned int* counter) {
+  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  double s = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
+    s = fma(a[i], b[i], s);
+  }
+  __shared__ double tot[1];
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) st->sums[slot] = tot[0];
+}
+
+// ===========================================================================
+// A5  ce = u_e^T KE u_e ; dc = -p xPhys^(p-1)(E0-Emin) ce (0 on passive);
+//     partial c = sum E ce.                                     (§2.3)
+// ===========================================================================
+__global__ void __launch_bounds__(kBlock)
+k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
+       const double* __restrict__ E, const double* __restrict__ xphys,
+       const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
+       double* partials, unsigned int* counter) {
+  const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
+  double csum = 0.0;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez)) continue;
+    double ue[24];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const int cx = (a == 1 || a == 2 || a == 5 || a == 6), cy = (a == 2 || a == 3 || a == 6 || a == 7),
+                cz = a >= 4;
+      const long long n = node_idx(g, ex + cx, ey + cy, ez + cz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ue[3 * a + c] = u[n + c * g.ncomp];
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < 24; ++r) {
+      double t = 0.0;
+#pragma unroll
+      for (int c = 0; c < 24; ++c) t = fma(c_KE[r * 24 + c], ue[c], t);
+      s = fma(ue[r], t, s);
+    }
+    ce[i] = s;
+    const double xp = xphys[i];
+    dc[i] = passive[i] ? 0.0 : -m.penal * pow(xp, m.penal - 1.0) * (m.E0 - m.Emin) * s;
+    csum = fma(E[i], s, csum);
+  }
+  __shared__ double tot[1];
+  double v[1] = {csum};
+  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) st->sums[0] = tot[0];
+}
+
+// ===========================================================================
+// A6  rmin cone filter (§2.4), truncated at the domain boundary.
+// out_i = post_i * sum_j H_ij val_j over in-domain j of the stencil.
+// ===========================================================================
+enum FiltMode { F_HS = 0, F_X0 = 1, F_DIV = 2, F_XDC = 3, F_PLAIN = 4 };
+//  F_HS   : out = sum H                                  (row sums Hs)
+//  F_X0   : out = (sum H a)/Hs, passive -> 0             (density filter of x)
+//  F_DIV  : out = sum H (a/b)                             (H(dc/Hs), H(dv/Hs))
+//  F_XDC  : out = (sum H a b)/(Hs max(1e-3, a_i))         (sensitivity filter, a=x, b=dc)
+//  F_PLAIN: out = (sum H a)/Hs                            (plain)
+template <int MODE>
+__global__ void __launch_bounds__(kBlock)
+k_filter(Geo g, int nst, const double* __restrict__ a, const double* __restrict__ b,
+         const double* __restrict__ hs, const uint8_t* __restrict__ passive,
+         double* __restrict__ out, int all_local) {
+  // all_local: evaluate on every in-domain local element (Hs incl. halos), else owned only
+  const long long b0 = all_local ? 0 : (long long)g.H * g.eplane;
+  const long long e0 = all_local ? g.nelloc : (long long)(g.H + g.nex) * g.eplane;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez) || ex < 0 || ex >= g.nelx) continue;
+    double s = 0.0;
+    for (int k = 0; k < nst; ++k) {
+      const int4 o = c_st_off[k];
+      const int jx = ex + o.x, jy = ey + o.y, jz = ez + o.z;
+      if (jx < 0 || jx >= g.nelx || jy < 0 || jy >= g.nely || jz < 0 || jz >= g.nelz) continue;
+      const long long j = i + (long long)o.x * g.eplane + (long long)o.z * g.EY + o.y;
+      double v;
+      if (MODE == F_HS) v = 1.0;
+      else if (MODE == F_DIV) v = a[j] / b[j];
+      else if (MODE == F_XDC) v = a[j] * b[j];
+      else v = a[j];
+      s = fma(c_st_w[k], v, s);
+    }
+    double r;
+    if (MODE == F_HS || MODE == F_DIV) r = s;
+    else if (MODE == F_XDC) r = s / (hs[i] * fmax(1e-3, a[i]));
+    else r = s / hs[i];
+    if (MODE == F_X0 && passive[i]) r = 0.0;
+    out[i] = r;
+  }
+}
+
+// ===========================================================================
+// A7  OC bisection (§2.3).  One pass evaluates xnew(lmid) and the
+// volume V(lmid): mode 0 uses V = sum_j dv~_j xnew_j (= sum_{i in D} xPhys_i,
+// H symmetric), modes 1/2 V = sum_{j in D} xnew_j.
+// ===========================================================================
+__device__ __forceinline__ double oc_candidate(double x, double dcf, double dvf, double lmid,
+                                              double move) {
+  const double cand = x * sqrt(fmax(0.0, -dcf / (dvf * lmid)));
+  return fmax(0.0, fmax(x - move, fmin(1.0, fmin(x + move, cand))));
+}
+
+__device__ __forceinline__ void oc_finish_pass(DevState* st, double vol) {
+  st->vol = vol;
+  if (vol > st->target) st->l1 = st->lmid;
+  else st->l2 = st->lmid;
+  st->oc_pass += 1;
+  st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > st->oc_tol) ? 1 : 0;
+  if (st->oc_active) st->lmid = 0.5 * (st->l2 + st->l1);
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_oc_pass(Geo g, DevState* st, double move, int mode, const double* __restrict__ x,
+          const double* __restrict__ dcf, const double* __restrict__ dvf,
+          const uint8_t* __restrict__ passive, double* partials, unsigned int* counter,
+          int finish) {
+  if (!st->oc_active) return;
+  const double lmid = st->lmid;
+  const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
+  double vol = 0.0;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez) || passive[i]) continue;
+    const double xn = oc_candidate(x[i], dcf[i], dvf[i], lmid, move);
+    vol += (mode == 0) ? dvf[i] * xn : xn;
+  }
+  __shared__ double tot[1];
+  double v[1] = {vol};
+  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) {
+    if (finish) oc_finish_pass(st, tot[0]);
+    else st->sums[0] = tot[0];
+  }
+}
+__global__ void k_oc_finish(DevState* st) {
+  if (!st->oc_active) return;
+  oc_finish_pass(st, st->sums[0]);
+}
+
+// final: xnew at the last evaluated lmid (l from the last pass), change =
+// max |xnew - x| over design elements, design-volume sum of xnew.
+__global__ void __launch_bounds__(kBlock)
+k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x,
+           const double* __restrict__ dcf, const double* __restrict__ dvf,
+           const uint8_t* __restrict__ passive, double* __restrict__ xnew, double* partials,
+           unsigned int* counter) {
+  const double lmid = st->lmid;   // not advanced after the last pass (oc_active == 0)
+  const int any = st->oc_pass > 0;
+  const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
+  double chg = 0.0, vsum = 0.0;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez)) continue;
+    if (passive[i]) { xnew[i] = 0.0; continue; }
+    const double xo = x[i];
+    const double xn = any ? oc_candidate(xo, dcf[i], dvf[i], lmid, move) : xo;
+    xnew[i] = xn;
+    chg = fmax(chg, fabs(xn - xo));
+    vsum += xn;
+  }
+  __shared__ double tot[2];
+  double v[2] = {vsum, chg};
+  if (grid_reduce<2, 1>(v, partials, counter, tot) && threadIdx.x == 0) {
+    st->sums[2] = tot[0];
+    st->sums[3] = tot[1];
+  }
+}
+
+// sum over owned design elements of a field (volume of xPhys)
+__global__ void __launch_bounds__(kBlock)
+k_design_sum(Geo g, DevState* st, const double* __restrict__ a, const uint8_t* __restrict__ passive,
+             int slot, double* partials, unsigned int* counter) {
+  const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
+  double s = 0.0;
+  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
+       i += (long long)gridDim.x * blockDim.x) {
+    int ex, ey, ez;
+    if (!decode_elem(g, i, ex, ey, ez) || passive[i]) continue;
+    s += a[i];
+  }
+  __shared__ double tot[1];
+  double v[1] = {s};
+  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) st->sums[slot] = tot[0];
+}
+
+// ---------------------------------------------------------------------------
+// Layout kernels: external (host order) <-> internal, for the owned range.
+// ---------------------------------------------------------------------------
+// nodes: ext[3*n + c] (n over owned node planes) <-> SoA internal
+__global__ void k_nodes_in(Geo g, const double* __restrict__ ext, double* __restrict__ in, int ix0,
+                           int nix) {
+  const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    // k enumerates the external sub-block in external order (iz, ix, iy)
+    const int iy = (int)(k % (g.nely + 1));
+    const long long t = k / (g.nely + 1);
+    const int ixr = (int)(t % nix), iz = (int)(t / nix);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) in[i + c * g.ncomp] = ext[3 * k + c];
+  }
+}
+__global__ void k_nodes_out(Geo g, const double* __restrict__ in, double* __restrict__ ext, int ix0,
+                            int nix) {
+  const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int iy = (int)(k % (g.nely + 1));
+    const long long t = k / (g.nely + 1);
+    const int ixr = (int)(t % nix), iz = (int)(t / nix);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ext[3 * k + c] = in[i + c * g.ncomp];
+  }
+}
+// elements: ext[(ez*nex + exr)*nely + ey] for the owned x range
+__global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __restrict__ in) {
+  const long long tot = (long long)g.nex * g.nelz * g.nely;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int ey = (int)(k % g.nely);
+    const long long t = k / g.nely;
+    const int exr = (int)(t % g.nex), ez = (int)(t / g.nex);
+    in[elem_idx(g, g.ex0 + exr, ey, ez)] = ext[k];
+  }
+}
+__global__ void k_elems_out(Geo g, const double* __restrict__ in, double* __restrict__ ext) {
+  const long long tot = (long long)g.nex * g.nelz * g.nely;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int ey = (int)(k % g.nely);
+    const long long t = k / g.nely;
+    const int exr = (int)(t % g.nex), ez = (int)(t / g.nex);
+    ext[k] = in[elem_idx(g, g.ex0 + exr, ey, ez)];
+  }
+}
+
+// loopback allreduce: dst[g]->sums[k] = sum_g src ... (fixed slab order)
+struct StatePtrs { DevState* s[16]; };
+__global__ void k_slab_allreduce(StatePtrs sp, int nslab, int k0, int nk, int maxmask) {
+  // thread t owns slot k0+t: reads it on every slab, then writes it back
+  const int k = k0 + threadIdx.x;
+  if (threadIdx.x >= nk) return;
+  double a = sp.s[0]->sums[k];
+  const bool mx = (maxmask >> threadIdx.x) & 1;
+  for (int s = 1; s < nslab; ++s) {
+    const double v = sp.s[s]->sums[k];
+    a = mx ? fmax(a, v) : a + v;
+  }
+  for (int s = 0; s < nslab; ++s) sp.s[s]->sums[k] = a;
+}
+
+}  // namespace topo
+
+namespace topo {
+// ---------------------------------------------------------------------------
+// small state / utility kernels
+// ---------------------------------------------------------------------------
+__global__ void k_cg_init(DevState* st, double tol2, double bb, long long max_it) {
+  st->tol2 = tol2;
+  st->bb = bb;
+  st->max_it = max_it;
+  st->it = 0;
+  st->status = 0;
+  st->fresh = 1;
+  st->done = 0;
+  st->alpha = st->beta = 0.0;
+}
+// after k_residual(write_r) + allreduce: rz, rr from sums; restart semantics
+__global__ void k_cg_start(DevState* st) {
+  st->rz = st->sums[0];
+  st->rr = st->sums[1];
+  st->fresh = 1;
+  st->status = 0;
+  st->done = (st->rr <= st->tol2 * st->bb) ? 1 : 0;
+}
+__global__ void k_oc_init(DevState* st, double lmax, double target, double tol) {
+  st->l1 = 0.0;
+  st->l2 = lmax;
+  st->target = target;
+  st->oc_tol = tol;
+  st->oc_pass = 0;
+  st->vol = 0.0;
+  st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > tol) ? 1 : 0;
+  st->lmid = 0.5 * (st->l2 + st->l1);
+}
+// zero the fixed DOFs of a node vector (owned planes)
+__global__ void k_mask_fixed(Geo g, const uint8_t* __restrict__ fixm, double* __restrict__ v) {
+  const long long b = g.nplane, e = (long long)(g.nown + 1) * g.nplane;
+  for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint8_t fm = fixm[i];
+    if (!fm) continue;
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if ((fm >> c) & 1) v[i + c * g.ncomp] = 0.0;
+  }
+}
+// force passive elements to 0 over the whole local element array
+__global__ void k_apply_passive(Geo g, const uint8_t* __restrict__ passive, double* __restrict__ a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
+       i += (long long)gridDim.x * blockDim.x)
+    if (passive[i]) a[i] = 0.0;
+}
+}  // namespace topo

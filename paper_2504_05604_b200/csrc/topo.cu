@@ -1,0 +1,1300 @@
+// libtopo: C-ABI implementation of the matrix-free SIMP hot path on B200.
+// See include/topo.h for the contract and DESIGN.md for the design.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/topo.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace topo {
+void build_element_stiffness(double nu, double* ke);  // ke_host.cpp
+}
+using namespace topo;
+
+// ---------------------------------------------------------------------------
+// Minimal NCCL binding, resolved with dlopen at init time (NCCL mode only),
+// so the library loads on machines without libnccl.
+// ---------------------------------------------------------------------------
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclFloat64 = 8 };
+enum { ncclSum = 0, ncclMax = 2 };
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* cands[] = {"libnccl.so.2", "libnccl.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+    for (const char* c : cands) {
+      h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+#define LD(name, sym) name = reinterpret_cast<decltype(name)>(dlsym(h, sym)); if (!name) { err = "missing " sym; return false; }
+    LD(GetUniqueId, "ncclGetUniqueId");
+    LD(CommInitRank, "ncclCommInitRank");
+    LD(CommDestroy, "ncclCommDestroy");
+    LD(AllReduce, "ncclAllReduce");
+    LD(Send, "ncclSend");
+    LD(Recv, "ncclRecv");
+    LD(GroupStart, "ncclGroupStart");
+    LD(GroupEnd, "ncclGroupEnd");
+    LD(GetErrorString, "ncclGetErrorString");
+#undef LD
+    return true;
+  }
+};
+NcclApi g_nccl;
+
+struct TopoError {
+  int code;
+  std::string msg;
+};
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+struct Slab {
+  Geo g{};
+  // node vectors: 3*ncomp doubles each (SoA)
+  double *u = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *f = nullptr, *invd = nullptr,
+         *w = nullptr;
+  uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
+  // element arrays: nelloc each
+  double *E = nullptr, *x = nullptr, *xphys = nullptr, *dc = nullptr, *dcf = nullptr,
+         *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ce = nullptr, *xnew = nullptr;
+  uint8_t* passive = nullptr;
+  double* partials = nullptr;
+  unsigned int* counter = nullptr;
+  DevState* st = nullptr;
+  double* stage = nullptr;   // staging for layout transforms
+  size_t stage_n = 0;
+};
+
+struct topo_ctx {
+  topo_params prm{};
+  int mode = TOPO_DIST_SINGLE, rank = 0, world = 1, device = 0;
+  std::vector<Slab> slabs;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
+  ncclComm_t comm = nullptr;
+  double ke[576];
+  double kd = 0.0;
+  std::vector<int4> st_off;
+  std::vector<double> st_w;
+  int R = 0;
+  long long n_design = 0;   // global design-element count
+  double bb = 0.0;          // ||f_free||^2
+  // state flags
+  bool has_E = false, has_u = false, has_sens = false, has_dcf = false, has_dvf = false;
+  // pinned mirror of slab 0's DevState
+  DevState* hstate = nullptr;
+  // CUDA graphs (PCG batch, OC batch)
+  cudaGraphExec_t cg_exec = nullptr;
+  int cg_batch = 0;
+  long long cg_batch_launches = 0;
+  bool cg_profiled_graph = false;
+  cudaGraphExec_t oc_exec = nullptr;
+  int oc_batch = 16;
+  long long oc_batch_launches = 0;
+  // profiling
+  bool profile = false;
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  double prof_ms = 0.0;
+  long long prof_n = 0;
+  // phase events
+  cudaEvent_t ev[8] = {};
+  topo_timings tim{};
+  long long launches = 0;
+  std::string err;
+  size_t dev_bytes = 0;
+};
+
+namespace {
+
+const topo_ctx* g_const_owner = nullptr;   // whose KE / stencil is in constant memory
+
+int set_err(topo_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return set_err(ctx, TOPO_ECUDA, "%s failed: %s (%s:%d)", #call,                 \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+  } while (0)
+#define CK(call)                        \
+  do {                                  \
+    int rc_ = (call);                   \
+    if (rc_ != TOPO_OK) return rc_;     \
+  } while (0)
+#define NC(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != 0)                                                                      \
+      return set_err(ctx, TOPO_ENCCL, "%s failed: %s", #call, g_nccl.GetErrorString(r_)); \
+  } while (0)
+
+inline int grid_for(long long n) {
+  long long b = (n + kBlock - 1) / kBlock;
+  if (b < 1) b = 1;
+  if (b > kMaxGridBlocks) b = kMaxGridBlocks;
+  return (int)b;
+}
+
+// --- launch helpers (count launches) ----------------------------------------
+#define LAUNCH(ctx, kern, grid, ...)                                      \
+  do {                                                                    \
+    kern<<<(grid), kBlock, 0, (ctx)->stream>>>(__VA_ARGS__);              \
+    (ctx)->launches++;                                                    \
+  } while (0)
+
+int check_launch(topo_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return TOPO_OK;
+}
+
+int ensure_constants(topo_ctx* ctx) {
+  if (g_const_owner == ctx) return TOPO_OK;
+  CU(cudaMemcpyToSymbolAsync(c_KE, ctx->ke, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->st_off.empty()) {
+    CU(cudaMemcpyToSymbolAsync(c_st_off, ctx->st_off.data(), sizeof(int4) * ctx->st_off.size(), 0,
+                               cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyToSymbolAsync(c_st_w, ctx->st_w.data(), sizeof(double) * ctx->st_w.size(), 0,
+                               cudaMemcpyHostToDevice, ctx->stream));
+  }
+  g_const_owner = ctx;
+  return TOPO_OK;
+}
+
+Material material(const topo_ctx* ctx) {
+  return Material{ctx->prm.E0, ctx->prm.Emin, ctx->prm.penal, ctx->kd};
+}
+
+// ---------------------------------------------------------------------------
+// Communication across slabs (loopback: in-process copies; NCCL: send/recv)
+// ---------------------------------------------------------------------------
+int allreduce(topo_ctx* ctx, int k0, int nk, int maxmask) {
+  const int W = ctx->world;
+  if (W == 1) return TOPO_OK;
+  if (ctx->mode == TOPO_DIST_LOOPBACK) {
+    StatePtrs sp{};
+    for (int s = 0; s < W; ++s) sp.s[s] = ctx->slabs[s].st;
+    k_slab_allreduce<<<1, 32, 0, ctx->stream>>>(sp, W, k0, nk, maxmask);
+    ctx->launches++;
+    return check_launch(ctx);
+  }
+  DevState* st = ctx->slabs[0].st;
+  // contiguous runs of sum / max slots
+  int k = 0;
+  while (k < nk) {
+    const bool mx = (maxmask >> k) & 1;
+    int e = k;
+    while (e < nk && (((maxmask >> e) & 1) != 0) == mx) ++e;
+    NC(g_nccl.AllReduce(st->sums + k0 + k, st->sums + k0 + k, (size_t)(e - k), ncclFloat64,
+                        mx ? ncclMax : ncclSum, ctx->comm, ctx->stream));
+    k = e;
+  }
+  return TOPO_OK;
+}
+
+// node planes of a 3-component vector: owned boundary planes -> neighbours' ghosts
+int exchange_nodes(topo_ctx* ctx, double* Slab::*field) {
+  const int W = ctx->world;
+  if (W == 1) return TOPO_OK;
+  if (ctx->mode == TOPO_DIST_LOOPBACK) {
+    for (int s = 0; s < W; ++s) {
+      Slab& a = ctx->slabs[s];
+      const size_t bytes = sizeof(double) * a.g.nplane;
+      for (int c = 0; c < 3; ++c) {
+        double* v = a.*field + c * a.g.ncomp;
+        if (s > 0) {
+          Slab& l = ctx->slabs[s - 1];
+          CU(cudaMemcpyAsync(l.*field + c * l.g.ncomp + (l.g.nown + 1) * l.g.nplane, v + a.g.nplane,
+                             bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        if (s < W - 1) {
+          Slab& rr = ctx->slabs[s + 1];
+          CU(cudaMemcpyAsync(rr.*field + c * rr.g.ncomp, v + a.g.nown * a.g.nplane, bytes,
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+      }
+    }
+    return TOPO_OK;
+  }
+  Slab& a = ctx->slabs[0];
+  const size_t n = a.g.nplane;
+  NC(g_nccl.GroupStart());
+  for (int c = 0; c < 3; ++c) {
+    double* v = a.*field + c * a.g.ncomp;
+    if (ctx->rank > 0) {
+      NC(g_nccl.Send(v + a.g.nplane, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
+      NC(g_nccl.Recv(v, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
+    }
+    if (ctx->rank < W - 1) {
+      NC(g_nccl.Send(v + a.g.nown * a.g.nplane, n, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->stream));
+      NC(g_nccl.Recv(v + (a.g.nown + 1) * a.g.nplane, n, ncclFloat64, ctx->rank + 1, ctx->comm,
+                     ctx->stream));
+    }
+  }
+  NC(g_nccl.GroupEnd());
+  return TOPO_OK;
+}
+
+// k element planes each side: owned boundary planes -> neighbours' halos
+int exchange_elems(topo_ctx* ctx, double* Slab::*field, int k) {
+  const int W = ctx->world;
+  if (W == 1 || k <= 0) return TOPO_OK;
+  if (ctx->mode == TOPO_DIST_LOOPBACK) {
+    for (int s = 0; s < W; ++s) {
+      Slab& a = ctx->slabs[s];
+      const size_t bytes = sizeof(double) * a.g.eplane * k;
+      double* v = a.*field;
+      if (s > 0) {
+        Slab& l = ctx->slabs[s - 1];
+        CU(cudaMemcpyAsync(l.*field + (l.g.H + l.g.nex) * l.g.eplane, v + a.g.H * a.g.eplane, bytes,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+      if (s < W - 1) {
+        Slab& rr = ctx->slabs[s + 1];
+        CU(cudaMemcpyAsync(rr.*field + (rr.g.H - k) * rr.g.eplane,
+                           v + (a.g.H + a.g.nex - k) * a.g.eplane, bytes, cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+      }
+    }
+    return TOPO_OK;
+  }
+  Slab& a = ctx->slabs[0];
+  const size_t n = a.g.eplane * k;
+  double* v = a.*field;
+  NC(g_nccl.GroupStart());
+  if (ctx->rank > 0) {
+    NC(g_nccl.Send(v + a.g.H * a.g.eplane, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
+    NC(g_nccl.Recv(v + (a.g.H - k) * a.g.eplane, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
+  }
+  if (ctx->rank < W - 1) {
+    NC(g_nccl.Send(v + (a.g.H + a.g.nex - k) * a.g.eplane, n, ncclFloat64, ctx->rank + 1, ctx->comm,
+                   ctx->stream));
+    NC(g_nccl.Recv(v + (a.g.H + a.g.nex) * a.g.eplane, n, ncclFloat64, ctx->rank + 1, ctx->comm,
+                   ctx->stream));
+  }
+  NC(g_nccl.GroupEnd());
+  return TOPO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host <-> device layout transfers (external numbering on the host side)
+// ---------------------------------------------------------------------------
+// owned node planes [ix0, ix0+nix) of slab s
+void slab_node_range(const Slab& s, int& ix0, int& nix) {
+  ix0 = s.g.ex0;
+  nix = s.g.nown;
+}
+
+int upload_nodes(topo_ctx* ctx, const double* host, double* Slab::*field) {
+  const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
+  std::vector<double> tmp;
+  for (Slab& s : ctx->slabs) {
+    int ix0, nix;
+    slab_node_range(s, ix0, nix);
+    const size_t row = (size_t)nix * (nely + 1) * 3;   // one iz layer of the sub-block
+    const double* src;
+    if (ctx->world == 1) {
+      src = host;
+    } else {
+      tmp.resize(row * (nelz + 1));
+      for (int iz = 0; iz <= nelz; ++iz)
+        memcpy(&tmp[iz * row], host + 3 * ((size_t)iz * (nelx + 1) * (nely + 1) + (size_t)ix0 * (nely + 1)),
+               sizeof(double) * row);
+      src = tmp.data();
+    }
+    CU(cudaMemcpyAsync(s.stage, src, sizeof(double) * row * (nelz + 1), cudaMemcpyHostToDevice, ctx->stream));
+    LAUNCH(ctx, k_nodes_in, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.stage, s.*field, ix0, nix);
+    CK(check_launch(ctx));
+    if (ctx->world > 1) CU(cudaStreamSynchronize(ctx->stream));   // tmp reuse
+  }
+  return TOPO_OK;
+}
+
+int download_nodes(topo_ctx* ctx, double* Slab::*field, double* host) {
+  const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
+  std::vector<double> tmp;
+  for (Slab& s : ctx->slabs) {
+    int ix0, nix;
+    slab_node_range(s, ix0, nix);
+    const size_t row = (size_t)nix * (nely + 1) * 3;
+    LAUNCH(ctx, k_nodes_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.*field, s.stage, ix0, nix);
+    CK(check_launch(ctx));
+    if (ctx->world == 1) {
+      CU(cudaMemcpyAsync(host, s.stage, sizeof(double) * row * (nelz + 1), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    } else {
+      tmp.resize(row * (nelz + 1));
+      CU(cudaMemcpyAsync(tmp.data(), s.stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      for (int iz = 0; iz <= nelz; ++iz)
+        memcpy(host + 3 * ((size_t)iz * (nelx + 1) * (nely + 1) + (size_t)ix0 * (nely + 1)), &tmp[iz * row],
+               sizeof(double) * row);
+    }
+  }
+  return TOPO_OK;
+}
+
+int upload_elems(topo_ctx* ctx, const double* host, double* Slab::*field) {
+  const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
+  std::vector<double> tmp;
+  for (Slab& s : ctx->slabs) {
+    const size_t row = (size_t)s.g.nex * nely;
+    const double* src;
+    if (ctx->world == 1) {
+      src = host;
+    } else {
+      tmp.resize(row * nelz);
+      for (int ez = 0; ez < nelz; ++ez)
+        memcpy(&tmp[ez * row], host + (size_t)ez * nelx * nely + (size_t)s.g.ex0 * nely, sizeof(double) * row);
+      src = tmp.data();
+    }
+    CU(cudaMemcpyAsync(s.stage, src, sizeof(double) * row * nelz, cudaMemcpyHostToDevice, ctx->stream));
+    LAUNCH(ctx, k_elems_in, grid_for((long long)row * nelz), s.g, s.stage, s.*field);
+    CK(check_launch(ctx));
+    if (ctx->world > 1) CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return TOPO_OK;
+}
+
+int download_elems(topo_ctx* ctx, double* Slab::*field, double* host) {
+  const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
+  std::vector<double> tmp;
+  for (Slab& s : ctx->slabs) {
+    const size_t row = (size_t)s.g.nex * nely;
+    LAUNCH(ctx, k_elems_out, grid_for((long long)row * nelz), s.g, s.*field, s.stage);
+    CK(check_launch(ctx));
+    if (ctx->world == 1) {
+      CU(cudaMemcpyAsync(host, s.stage, sizeof(double) * row * nelz, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    } else {
+      tmp.resize(row * nelz);
+      CU(cudaMemcpyAsync(tmp.data(), s.stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      for (int ez = 0; ez < nelz; ++ez)
+        memcpy(host + (size_t)ez * nelx * nely + (size_t)s.g.ex0 * nely, &tmp[ez * row], sizeof(double) * row);
+    }
+  }
+  return TOPO_OK;
+}
+
+// Fill a local element array (incl. halos) from a global host array of bytes.
+void fill_local_elems_u8(const topo_ctx* ctx, const Slab& s, const uint8_t* glob, std::vector<uint8_t>& loc) {
+  const Geo& g = s.g;
+  loc.assign(g.nelloc, 0);
+  for (int exl = 0; exl < g.NEXL; ++exl) {
+    const int ex = exl - g.H + g.ex0;
+    if (ex < 0 || ex >= g.nelx) continue;
+    for (int ez = 0; ez < g.nelz; ++ez)
+      for (int ey = 0; ey < g.nely; ++ey)
+        loc[elem_idx(g, ex, ey, ez)] = glob ? glob[(size_t)ez * g.nelx * g.nely + (size_t)ex * g.nely + ey] : 0;
+  }
+}
+
+int sync_state(topo_ctx* ctx) {
+  CU(cudaMemcpyAsync(ctx->hstate, ctx->slabs[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Phase pieces
+// ---------------------------------------------------------------------------
+int update_modulus(topo_ctx* ctx) {
+  CK(ensure_constants(ctx));
+  const Material m = material(ctx);
+  for (Slab& s : ctx->slabs) {
+    LAUNCH(ctx, k_efield, grid_for(s.g.nelloc), s.g, m, s.xphys, s.E);
+    LAUNCH(ctx, k_invdiag, grid_for((long long)s.g.nown * s.g.nplane), s.g, m, s.E, s.fixm, s.invd);
+  }
+  CK(check_launch(ctx));
+  ctx->has_E = true;
+  return TOPO_OK;
+}
+
+// q = K p for every slab (p ghosts exchanged first)
+int matvec_all(topo_ctx* ctx, double* Slab::*pin, double* Slab::*qout) {
+  CK(exchange_nodes(ctx, pin));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_matvec<false>, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, 0, s.E, s.*pin,
+           s.fixm, s.*qout, s.partials, s.counter, 0);
+  return check_launch(ctx);
+}
+
+// residual r(or w) = f - K u ; sums[0,1] = (rz, rr) allreduced
+int residual(topo_ctx* ctx, bool write_r) {
+  CK(matvec_all(ctx, &Slab::u, &Slab::q));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_residual, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.r,
+           write_r ? 1 : 0, s.partials, s.counter);
+  CK(check_launch(ctx));
+  return allreduce(ctx, 0, 2, 0);
+}
+
+// enqueue one PCG iteration
+int enqueue_cg_iter(topo_ctx* ctx, bool prof_here) {
+  const int W = ctx->world;
+  const int fin = (W == 1) ? 1 : 0;
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_pupdate, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.r, s.invd, s.p);
+  CK(exchange_nodes(ctx, &Slab::p));
+  if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_matvec<true>, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, 1, s.E, s.p, s.fixm,
+           s.q, s.partials, s.counter, fin);
+  if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
+  if (!fin) {
+    CK(allreduce(ctx, 0, 1, 0));
+    for (Slab& s : ctx->slabs) { k_finish_alpha<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+  }
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_update, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.u, s.r, s.p, s.q, s.invd,
+           s.partials, s.counter, fin);
+  if (!fin) {
+    CK(allreduce(ctx, 0, 2, 0));
+    for (Slab& s : ctx->slabs) { k_finish_update<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+  }
+  return check_launch(ctx);
+}
+
+int build_cg_graph(topo_ctx* ctx) {
+  if (ctx->cg_exec && ctx->cg_profiled_graph == ctx->profile) return TOPO_OK;
+  if (ctx->cg_exec) { cudaGraphExecDestroy(ctx->cg_exec); ctx->cg_exec = nullptr; }
+  cudaGraph_t graph;
+  const long long l0 = ctx->launches;
+  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = TOPO_OK;
+  for (int i = 0; i < ctx->cg_batch && rc == TOPO_OK; ++i) rc = enqueue_cg_iter(ctx, ctx->profile && i == 0);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != TOPO_OK) return rc;
+  if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&ctx->cg_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  ctx->cg_batch_launches = ctx->launches - l0;
+  ctx->launches = l0;
+  ctx->cg_profiled_graph = ctx->profile;
+  return TOPO_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// A4  PCG driver.  Batches of cg_batch iterations run as one CUDA graph; the
+// device flag `done` turns the rest of a batch into no-ops, so the host
+// polls once per batch.  After convergence of the recursive residual the
+// true residual f - K u is checked; if it fails, r is replaced and PCG
+// restarts.
+// ---------------------------------------------------------------------------
+int do_solve(topo_ctx* ctx, topo_solve_info* info) {
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  CK(exchange_nodes(ctx, &Slab::invd));   // (ghost invd unused by v1 kernels; kept consistent)
+  const topo_params& P = ctx->prm;
+  const long long n_dof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+  const long long maxit = P.cg_max_iter > 0 ? P.cg_max_iter : 10 * n_dof;
+  CU(cudaEventRecord(ctx->ev[6], ctx->stream));
+  if (!P.cg_warm_start || !ctx->has_u || ctx->bb == 0.0)
+    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
+  for (Slab& s : ctx->slabs) {
+    k_cg_init<<<1, 1, 0, ctx->stream>>>(s.st, P.cg_rtol * P.cg_rtol, ctx->bb, maxit);
+    ctx->launches++;
+  }
+  CK(residual(ctx, true));
+  for (Slab& s : ctx->slabs) { k_cg_start<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+  CK(check_launch(ctx));
+  CK(build_cg_graph(ctx));
+  int replacements = 0, rc = TOPO_OK;
+  double rr_true = 0.0;
+  DevState& h = *ctx->hstate;
+  CK(sync_state(ctx));
+  long long it_prev = h.it;
+  while (true) {
+    if (!h.done) {
+      CU(cudaGraphLaunch(ctx->cg_exec, ctx->stream));
+      ctx->launches += ctx->cg_batch_launches;
+      CK(sync_state(ctx));
+      if (ctx->profile && h.it > it_prev) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->pe0, ctx->pe1) == cudaSuccess) {
+          ctx->prof_ms += ms;
+          ctx->prof_n++;
+        }
+      }
+      it_prev = h.it;
+      continue;
+    }
+    if (h.status == 2) { rc = set_err(ctx, TOPO_ENOCONV, "PCG: no convergence in %lld iterations", h.it); break; }
+    if (h.status == 3) { rc = set_err(ctx, TOPO_EBREAKDOWN, "PCG breakdown at iteration %lld", h.it); break; }
+    CK(residual(ctx, false));
+    CK(sync_state(ctx));
+    rr_true = h.sums[1];
+    if (rr_true <= h.tol2 * h.bb) break;
+    if (replacements >= 20) { rc = set_err(ctx, TOPO_ENOCONV, "PCG: true residual stagnates"); break; }
+    ++replacements;
+    CK(residual(ctx, true));
+    for (Slab& s : ctx->slabs) { k_cg_start<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+    CK(sync_state(ctx));
+    if (h.done) {   // replaced residual already small (true residual above was not) -> done
+      rr_true = h.rr;
+      break;
+    }
+  }
+  CU(cudaEventRecord(ctx->ev[7], ctx->stream));
+  CU(cudaEventSynchronize(ctx->ev[7]));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+  ctx->tim.cg_iters = h.it;
+  ctx->tim.cg_iters_total += h.it;
+  if (info) {
+    info->iters = h.it;
+    info->rel_res = ctx->bb > 0 ? std::sqrt(h.rr / ctx->bb) : 0.0;
+    info->true_rel_res = ctx->bb > 0 ? std::sqrt(rr_true / ctx->bb) : 0.0;
+    info->ms = ms;
+    info->replacements = replacements;
+  }
+  ctx->has_u = true;
+  ctx->has_sens = ctx->has_dcf = false;
+  return rc;
+}
+
+// A5: ce, dc, c = sum E ce, f^T u
+int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
+  if (!ctx->has_u) return set_err(ctx, TOPO_ESTATE, "topo_sensitivity before topo_solve");
+  CK(ensure_constants(ctx));
+  CK(exchange_nodes(ctx, &Slab::u));
+  const Material m = material(ctx);
+  for (Slab& s : ctx->slabs) {
+    LAUNCH(ctx, k_sens, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
+           s.passive, s.ce, s.dc, s.partials, s.counter);
+    LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.u, 1, s.partials, s.counter);
+  }
+  CK(check_launch(ctx));
+  CK(allreduce(ctx, 0, 2, 0));
+  CK(sync_state(ctx));
+  if (c_out) *c_out = ctx->hstate->sums[0];
+  if (fu_out) *fu_out = ctx->hstate->sums[1];
+  ctx->tim.c = ctx->hstate->sums[0];
+  ctx->tim.fu = ctx->hstate->sums[1];
+  ctx->has_sens = true;
+  return TOPO_OK;
+}
+
+// A6 on dc: dc~ (and dv~ once)
+int do_filter_dc(topo_ctx* ctx) {
+  CK(ensure_constants(ctx));
+  const int mode = ctx->prm.filter_mode, nst = (int)ctx->st_off.size();
+  CK(exchange_elems(ctx, &Slab::dc, ctx->R));
+  for (Slab& s : ctx->slabs) {
+    const int gr = grid_for((long long)s.g.nex * s.g.eplane);
+    if (mode == TOPO_FILTER_DENSITY)
+      LAUNCH(ctx, k_filter<F_DIV>, gr, s.g, nst, s.dc, s.hs, s.hs, s.passive, s.dcf, 0);
+    else if (mode == TOPO_FILTER_SENSITIVITY)
+      LAUNCH(ctx, k_filter<F_XDC>, gr, s.g, nst, s.x, s.dc, s.hs, s.passive, s.dcf, 0);
+    else
+      LAUNCH(ctx, k_filter<F_PLAIN>, gr, s.g, nst, s.dc, s.dc, s.hs, s.passive, s.dcf, 0);
+    if (!ctx->has_dvf) {
+      if (mode == TOPO_FILTER_DENSITY)
+        LAUNCH(ctx, k_filter<F_DIV>, gr, s.g, nst, s.dv, s.hs, s.hs, s.passive, s.dvf, 0);
+      else
+        CU(cudaMemcpyAsync(s.dvf, s.dv, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+  }
+  CK(check_launch(ctx));
+  ctx->has_dvf = true;
+  ctx->has_dcf = true;
+  return TOPO_OK;
+}
+
+// A6 on x: xPhys = filter(x) (mode 0) or x
+int do_filter_x(topo_ctx* ctx) {
+  CK(ensure_constants(ctx));
+  const int nst = (int)ctx->st_off.size();
+  if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY) {
+    for (Slab& s : ctx->slabs)
+      LAUNCH(ctx, k_filter<F_X0>, grid_for((long long)s.g.nex * s.g.eplane), s.g, nst, s.x, s.x, s.hs,
+             s.passive, s.xphys, 0);
+    CK(check_launch(ctx));
+    CK(exchange_elems(ctx, &Slab::xphys, ctx->slabs[0].g.H));
+  } else {
+    for (Slab& s : ctx->slabs)
+      CU(cudaMemcpyAsync(s.xphys, s.x, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  ctx->has_E = false;
+  return TOPO_OK;
+}
+
+int build_oc_graph(topo_ctx* ctx) {
+  if (ctx->oc_exec) return TOPO_OK;
+  const int W = ctx->world, fin = (W == 1) ? 1 : 0;
+  cudaGraph_t graph;
+  const long long l0 = ctx->launches;
+  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = TOPO_OK;
+  for (int i = 0; i < ctx->oc_batch && rc == TOPO_OK; ++i) {
+    for (Slab& s : ctx->slabs)
+      LAUNCH(ctx, k_oc_pass, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, ctx->prm.move,
+             ctx->prm.filter_mode, s.x, s.dcf, s.dvf, s.passive, s.partials, s.counter, fin);
+    if (!fin) {
+      rc = allreduce(ctx, 0, 1, 0);
+      for (Slab& s : ctx->slabs) { k_oc_finish<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+    }
+  }
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+  if (rc != TOPO_OK) return rc;
+  if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "OC graph capture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&ctx->oc_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "OC graph instantiate: %s", cudaGetErrorString(e));
+  ctx->oc_batch_launches = ctx->launches - l0;
+  ctx->launches = l0;
+  return TOPO_OK;
+}
+
+// A7: bisection, final xnew, x <- xnew, xPhys <- filter(x)
+int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
+  if (!ctx->has_dcf) return set_err(ctx, TOPO_ESTATE, "topo_oc_step before topo_filter(DC)");
+  CK(ensure_constants(ctx));
+  const topo_params& P = ctx->prm;
+  for (Slab& s : ctx->slabs) {
+    k_oc_init<<<1, 1, 0, ctx->stream>>>(s.st, P.oc_lmax, P.volfrac * (double)ctx->n_design, P.oc_tol);
+    ctx->launches++;
+  }
+  CK(check_launch(ctx));
+  CK(build_oc_graph(ctx));
+  DevState& h = *ctx->hstate;
+  CK(sync_state(ctx));
+  int guard = 0;
+  while (h.oc_active) {
+    CU(cudaGraphLaunch(ctx->oc_exec, ctx->stream));
+    ctx->launches += ctx->oc_batch_launches;
+    CK(sync_state(ctx));
+    if (++guard > 4096 / ctx->oc_batch) return set_err(ctx, TOPO_EBISECT, "OC bisection did not terminate");
+  }
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_oc_final, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.dcf, s.dvf,
+           s.passive, s.xnew, s.partials, s.counter);
+  CK(check_launch(ctx));
+  CK(allreduce(ctx, 2, 2, 0x2));
+  for (Slab& s : ctx->slabs)
+    CU(cudaMemcpyAsync(s.x, s.xnew, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(exchange_elems(ctx, &Slab::x, ctx->slabs[0].g.H));
+  CK(do_filter_x(ctx));
+  double vol;
+  if (P.filter_mode == TOPO_FILTER_DENSITY) {
+    for (Slab& s : ctx->slabs)
+      LAUNCH(ctx, k_design_sum, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, s.xphys, s.passive, 4,
+             s.partials, s.counter);
+    CK(check_launch(ctx));
+    CK(allreduce(ctx, 4, 1, 0));
+    CK(sync_state(ctx));
+    vol = h.sums[4];
+  } else {
+    CK(sync_state(ctx));
+    vol = h.sums[2];
+  }
+  const double lam = h.lmid, chg = h.sums[3];
+  if (lambda) *lambda = lam;
+  if (change) *change = chg;
+  if (volume) *volume = vol / (double)ctx->n_design;
+  ctx->tim.lambda = lam;
+  ctx->tim.change = chg;
+  ctx->tim.volume = vol / (double)ctx->n_design;
+  ctx->tim.oc_passes = h.oc_pass;
+  ctx->has_sens = ctx->has_dcf = false;
+  return TOPO_OK;
+}
+
+int alloc_slab(topo_ctx* ctx, Slab& s) {
+  const Geo& g = s.g;
+  auto al = [&](void** p, size_t bytes) -> int {
+    CU(cudaMalloc(p, bytes));
+    CU(cudaMemsetAsync(*p, 0, bytes, ctx->stream));
+    ctx->dev_bytes += bytes;
+    return TOPO_OK;
+  };
+  const size_t nb = sizeof(double) * 3 * g.ncomp, eb = sizeof(double) * g.nelloc;
+  double** nv[] = {&s.u, &s.r, &s.p, &s.q, &s.f, &s.invd, &s.w};
+  for (double** v : nv) CK(al((void**)v, nb));
+  CK(al((void**)&s.fixm, g.ncomp));
+  double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew};
+  for (double** v : ev) CK(al((void**)v, eb));
+  CK(al((void**)&s.passive, g.nelloc));
+  CK(al((void**)&s.partials, sizeof(double) * 8 * kMaxGridBlocks));
+  CK(al((void**)&s.counter, sizeof(unsigned int) * 4));
+  CK(al((void**)&s.st, sizeof(DevState)));
+  s.stage_n = std::max((size_t)3 * (g.nown) * (g.nely + 1) * (g.nelz + 1), (size_t)g.nex * g.nely * g.nelz);
+  CK(al((void**)&s.stage, sizeof(double) * s.stage_n));
+  return TOPO_OK;
+}
+
+void free_ctx(topo_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (Slab& s : ctx->slabs) {
+    void* ptrs[] = {s.u, s.r, s.p, s.q, s.f, s.invd, s.w, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
+                    s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  if (ctx->cg_exec) cudaGraphExecDestroy(ctx->cg_exec);
+  if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
+  if (ctx->pe0) cudaEventDestroy(ctx->pe0);
+  if (ctx->pe1) cudaEventDestroy(ctx->pe1);
+  for (cudaEvent_t e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->hstate) cudaFreeHost(ctx->hstate);
+  if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (g_const_owner == ctx) g_const_owner = nullptr;
+  delete ctx;
+}
+
+int validate(topo_ctx* ctx, const topo_params* p) {
+  if (!p) return set_err(ctx, TOPO_EINVAL, "params is NULL");
+  if (p->nelx < 1 || p->nely < 1 || p->nelz < 1)
+    return set_err(ctx, TOPO_EINVAL, "grid dimensions must be >= 1 (got %d x %d x %d)", p->nelx, p->nely, p->nelz);
+  if ((double)(p->nelx + 1) * (p->nely + 1) * (p->nelz + 1) * 3 > 2.0e9)
+    return set_err(ctx, TOPO_EINVAL, "grid too large for one context");
+  if (!(p->volfrac > 0 && p->volfrac < 1)) return set_err(ctx, TOPO_EINVAL, "volfrac must be in (0,1)");
+  if (!(p->penal >= 1)) return set_err(ctx, TOPO_EINVAL, "penal must be >= 1");
+  if (!(p->rmin > 0 && p->rmin <= 6)) return set_err(ctx, TOPO_EINVAL, "rmin must be in (0, 6]");
+  if (!(p->Emin > 0 && p->Emin < p->E0)) return set_err(ctx, TOPO_EINVAL, "need 0 < Emin < E0");
+  if (!(p->nu >= 0 && p->nu < 0.5)) return set_err(ctx, TOPO_EINVAL, "nu must be in [0, 0.5)");
+  if (!(p->move > 0 && p->move <= 1)) return set_err(ctx, TOPO_EINVAL, "move must be in (0, 1]");
+  if (p->filter_mode < 0 || p->filter_mode > 2) return set_err(ctx, TOPO_EINVAL, "filter_mode must be 0, 1 or 2");
+  if (!(p->cg_rtol > 0 && p->cg_rtol < 1)) return set_err(ctx, TOPO_EINVAL, "cg_rtol must be in (0,1)");
+  if (!(p->oc_tol > 0) || !(p->oc_lmax > 0)) return set_err(ctx, TOPO_EINVAL, "oc_tol, oc_lmax must be > 0");
+  return TOPO_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+void topo_params_default(topo_params* p) {
+  if (!p) return;
+  memset(p, 0, sizeof *p);
+  p->nelx = p->nely = p->nelz = 1;
+  p->volfrac = 0.3;
+  p->penal = 3.0;
+  p->rmin = 1.5;
+  p->E0 = 1.0;
+  p->Emin = 1e-9;
+  p->nu = 0.3;
+  p->move = 0.2;
+  p->filter_mode = TOPO_FILTER_DENSITY;
+  p->cg_rtol = 1e-8;
+  p->cg_max_iter = 0;
+  p->cg_warm_start = 1;
+  p->oc_tol = 1e-10;
+  p->oc_lmax = 1e9;
+  p->deterministic = 1;
+  p->cg_check_every = 0;
+}
+
+const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }
+
+const char* topo_strerror(int code) {
+  switch (code) {
+    case TOPO_OK: return "ok";
+    case TOPO_EINVAL: return "invalid argument";
+    case TOPO_ENOCONV: return "PCG did not converge";
+    case TOPO_EBREAKDOWN: return "PCG breakdown";
+    case TOPO_EUNCONSTRAINED: return "no fixed DOFs (rigid-body modes)";
+    case TOPO_EBISECT: return "OC bisection failure";
+    case TOPO_EALLPASSIVE: return "no design elements";
+    case TOPO_ECUDA: return "CUDA error";
+    case TOPO_ENCCL: return "NCCL error";
+    case TOPO_ENOMEM: return "out of memory";
+    case TOPO_ESTATE: return "call out of order";
+    default: return "unknown error";
+  }
+}
+
+const char* topo_last_error(const topo_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+int topo_element_stiffness(double nu, double* ke576) {
+  if (!ke576 || !(nu >= 0 && nu < 0.5)) return TOPO_EINVAL;
+  build_element_stiffness(nu, ke576);
+  return TOPO_OK;
+}
+
+int topo_nccl_unique_id(uint8_t* out128) {
+  std::string err;
+  if (!out128 || !g_nccl.load(err)) return TOPO_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return TOPO_ENCCL;
+  memcpy(out128, id.internal, 128);
+  return TOPO_OK;
+}
+
+int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, const uint8_t* passive,
+              const topo_dist* dist, topo_ctx** out) {
+  if (!out) return TOPO_EINVAL;
+  *out = nullptr;
+  topo_ctx* ctx = new topo_ctx();
+  int rc = validate(ctx, p);
+  if (rc == TOPO_OK && (!load || !fixed)) rc = set_err(ctx, TOPO_EINVAL, "load and fixed are required");
+  if (rc != TOPO_OK) { delete ctx; return rc; }
+  ctx->prm = *p;
+  const int nelx = p->nelx, nely = p->nely, nelz = p->nelz;
+  const long long nn = (long long)(nelx + 1) * (nely + 1) * (nelz + 1), ne = (long long)nelx * nely * nelz;
+  // --- problem checks on the host (global inputs) ---
+  long long nfix = 0;
+  for (long long i = 0; i < 3 * nn; ++i) {
+    if (fixed[i]) {
+      ++nfix;
+      if (load[i] != 0.0) {
+        rc = set_err(ctx, TOPO_EINVAL, "load on fixed DOF %lld", i);
+        break;
+      }
+    }
+    if (!std::isfinite(load[i])) { rc = set_err(ctx, TOPO_EINVAL, "non-finite load"); break; }
+  }
+  if (rc == TOPO_OK && nfix == 0) rc = set_err(ctx, TOPO_EUNCONSTRAINED, "no fixed DOFs");
+  long long nd = ne;
+  if (passive) {
+    nd = 0;
+    for (long long e = 0; e < ne; ++e) nd += passive[e] ? 0 : 1;
+  }
+  if (rc == TOPO_OK && nd == 0) rc = set_err(ctx, TOPO_EALLPASSIVE, "every element is passive");
+  ctx->n_design = nd;
+  // --- distribution ---
+  if (dist) {
+    ctx->mode = dist->mode;
+    ctx->rank = dist->rank;
+    ctx->world = dist->world;
+    ctx->device = dist->device;
+  } else {
+    cudaGetDevice(&ctx->device);
+  }
+  if (rc == TOPO_OK && (ctx->world < 1 || ctx->world > 16 || ctx->rank < 0 || ctx->rank >= ctx->world))
+    rc = set_err(ctx, TOPO_EINVAL, "bad rank/world");
+  if (rc == TOPO_OK && ctx->mode == TOPO_DIST_SINGLE && ctx->world != 1)
+    rc = set_err(ctx, TOPO_EINVAL, "TOPO_DIST_SINGLE needs world == 1");
+  // --- KE and filter stencil (host precompute) ---
+  build_element_stiffness(p->nu, ctx->ke);
+  ctx->kd = ctx->ke[0];
+  {
+    const int B = (int)std::ceil(p->rmin);
+    int R = 0;
+    for (int dz = -B; dz <= B; ++dz)
+      for (int dx = -B; dx <= B; ++dx)
+        for (int dy = -B; dy <= B; ++dy) {
+          const double d = std::sqrt((double)(dx * dx + dy * dy + dz * dz));
+          if (!(d < p->rmin)) continue;
+          ctx->st_off.push_back(make_int4(dx, dy, dz, 0));
+          ctx->st_w.push_back(p->rmin - d);
+          R = std::max(R, std::max(std::abs(dx), std::max(std::abs(dy), std::abs(dz))));
+        }
+    ctx->R = R;
+    if ((int)ctx->st_off.size() > kMaxStencil) rc = set_err(ctx, TOPO_EINVAL, "filter stencil too large");
+  }
+  const int H = std::max(1, ctx->R);
+  // slab partition: owned elements [ex0, ex1)
+  const int W = ctx->world;
+  for (int s = 0; s < W && rc == TOPO_OK; ++s) {
+    const int ex0 = (int)((long long)s * nelx / W), ex1 = (int)((long long)(s + 1) * nelx / W);
+    if (ex1 - ex0 < std::max(1, W > 1 ? ctx->R : 1))
+      rc = set_err(ctx, TOPO_EINVAL, "slab %d has %d element planes; need >= filter radius %d", s, ex1 - ex0, ctx->R);
+  }
+  if (rc != TOPO_OK) { delete ctx; return rc; }
+  if (cudaSetDevice(ctx->device) != cudaSuccess) { delete ctx; return TOPO_ECUDA; }
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return TOPO_ECUDA; }
+  ctx->stream = ctx->own_stream;
+  if (cudaMallocHost(&ctx->hstate, sizeof(DevState)) != cudaSuccess) { free_ctx(ctx); return TOPO_ENOMEM; }
+  memset(ctx->hstate, 0, sizeof(DevState));
+  cudaEventCreate(&ctx->pe0);
+  cudaEventCreate(&ctx->pe1);
+  for (cudaEvent_t& e : ctx->ev) cudaEventCreate(&e);
+  if (ctx->mode == TOPO_DIST_NCCL && W > 1) {
+    std::string err;
+    if (!g_nccl.load(err)) { rc = set_err(ctx, TOPO_ENCCL, "%s", err.c_str()); free_ctx(ctx); return rc; }
+    if (!dist->nccl_id) { free_ctx(ctx); return TOPO_EINVAL; }
+    ncclUniqueId id;
+    memcpy(id.internal, dist->nccl_id, 128);
+    ncclResult_t r = g_nccl.CommInitRank(&ctx->comm, W, id, ctx->rank);
+    if (r != 0) { rc = set_err(ctx, TOPO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); free_ctx(ctx); return rc; }
+  }
+  // local slabs
+  const int s_begin = (ctx->mode == TOPO_DIST_NCCL) ? ctx->rank : 0;
+  const int s_end = (ctx->mode == TOPO_DIST_NCCL) ? ctx->rank + 1 : W;
+  for (int s = s_begin; s < s_end; ++s) {
+    Slab sl;
+    Geo& g = sl.g;
+    g.nelx = nelx; g.nely = nely; g.nelz = nelz;
+    g.ex0 = (int)((long long)s * nelx / W);
+    g.ex1 = (int)((long long)(s + 1) * nelx / W);
+    g.nex = g.ex1 - g.ex0;
+    g.nown = g.nex + (s == W - 1 ? 1 : 0);
+    g.NY = ((nely + 3) + 3) / 4 * 4;
+    g.NZ = nelz + 3;
+    g.NXL = g.nown + 2;
+    g.nplane = (long long)g.NY * g.NZ;
+    g.ncomp = (long long)g.NXL * g.nplane;
+    g.H = H;
+    g.EY = ((nely + 2) + 3) / 4 * 4;
+    g.EZ = nelz + 2;
+    g.NEXL = g.nex + 2 * H;
+    g.eplane = (long long)g.EY * g.EZ;
+    g.nelloc = (long long)g.NEXL * g.eplane;
+    ctx->slabs.push_back(sl);
+  }
+  for (Slab& s : ctx->slabs) {
+    rc = alloc_slab(ctx, s);
+    if (rc != TOPO_OK) { int r2 = rc; free_ctx(ctx); return r2 == TOPO_ECUDA ? TOPO_ENOMEM : r2; }
+  }
+  // --- inputs ---
+  std::vector<uint8_t> loc8;
+  std::vector<double> locd;
+  for (Slab& s : ctx->slabs) {
+    const Geo& g = s.g;
+    // fixed-DOF bit mask on the owned node planes
+    loc8.assign(g.ncomp, 0);
+    for (int ix = g.ex0; ix < g.ex0 + g.nown; ++ix)
+      for (int iz = 0; iz <= nelz; ++iz)
+        for (int iy = 0; iy <= nely; ++iy) {
+          const long long n = (long long)iz * (nelx + 1) * (nely + 1) + (long long)ix * (nely + 1) + iy;
+          loc8[node_idx(g, ix, iy, iz)] = (fixed[3 * n] ? 1 : 0) | (fixed[3 * n + 1] ? 2 : 0) | (fixed[3 * n + 2] ? 4 : 0);
+        }
+    if (cudaMemcpy(s.fixm, loc8.data(), g.ncomp, cudaMemcpyHostToDevice) != cudaSuccess) { free_ctx(ctx); return TOPO_ECUDA; }
+    // passive mask and dv (1 on design) over the whole local element array
+    fill_local_elems_u8(ctx, s, passive, loc8);
+    if (cudaMemcpy(s.passive, loc8.data(), g.nelloc, cudaMemcpyHostToDevice) != cudaSuccess) { free_ctx(ctx); return TOPO_ECUDA; }
+    locd.assign(g.nelloc, 0.0);
+    std::vector<double> locx(g.nelloc, 0.0);
+    for (int exl = 0; exl < g.NEXL; ++exl) {
+      const int ex = exl - g.H + g.ex0;
+      if (ex < 0 || ex >= nelx) continue;
+      for (int ez = 0; ez < nelz; ++ez)
+        for (int ey = 0; ey < nely; ++ey) {
+          const long long i = elem_idx(g, ex, ey, ez);
+          const bool des = !loc8[i];
+          locd[i] = des ? 1.0 : 0.0;
+          locx[i] = des ? p->volfrac : 0.0;
+        }
+    }
+    if (cudaMemcpy(s.dv, locd.data(), sizeof(double) * g.nelloc, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(s.x, locx.data(), sizeof(double) * g.nelloc, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(s.xphys, locx.data(), sizeof(double) * g.nelloc, cudaMemcpyHostToDevice) != cudaSuccess) {
+      free_ctx(ctx);
+      return TOPO_ECUDA;
+    }
+  }
+  rc = upload_nodes(ctx, load, &Slab::f);
+  if (rc == TOPO_OK) rc = ensure_constants(ctx);
+  if (rc == TOPO_OK) {
+    // ||f_free||^2 and filter row sums Hs (all local in-domain elements)
+    for (Slab& s : ctx->slabs) {
+      LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.f, 0, s.partials, s.counter);
+      LAUNCH(ctx, k_filter<F_HS>, grid_for(s.g.nelloc), s.g, (int)ctx->st_off.size(), s.hs, s.hs, s.hs,
+             s.passive, s.hs, 1);
+    }
+    rc = check_launch(ctx);
+  }
+  if (rc == TOPO_OK) rc = allreduce(ctx, 0, 1, 0);
+  if (rc == TOPO_OK) rc = sync_state(ctx);
+  if (rc != TOPO_OK) { free_ctx(ctx); return rc; }
+  ctx->bb = ctx->hstate->sums[0];
+  // PCG batch size between host polls: ~ a few ms of device work
+  {
+    const long long ndof = 3 * nn;
+    int b = p->cg_check_every;
+    if (b <= 0) b = (int)std::min<long long>(64, std::max<long long>(8, 20000000LL / std::max<long long>(ndof, 1)));
+    ctx->cg_batch = b;
+  }
+  *out = ctx;
+  return TOPO_OK;
+}
+
+int topo_set_stream(topo_ctx* ctx, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->own_stream;
+  if (s != ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    ctx->stream = s;
+    if (ctx->cg_exec) { cudaGraphExecDestroy(ctx->cg_exec); ctx->cg_exec = nullptr; }
+    if (ctx->oc_exec) { cudaGraphExecDestroy(ctx->oc_exec); ctx->oc_exec = nullptr; }
+    g_const_owner = nullptr;
+  }
+  return TOPO_OK;
+}
+
+int topo_owned_range(const topo_ctx* ctx, int32_t* ex_begin, int32_t* ex_end) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ex_begin) *ex_begin = ctx->slabs.front().g.ex0;
+  if (ex_end) *ex_end = ctx->slabs.back().g.ex1;
+  return TOPO_OK;
+}
+
+static int set_x_common(topo_ctx* ctx, const double* x, bool also_xphys) {
+  if (x) {
+    CK(upload_elems(ctx, x, &Slab::x));
+  } else {
+    for (Slab& s : ctx->slabs) {
+      // x = volfrac * dv  (dv = 1 on design, 0 elsewhere)
+      std::vector<double> h(s.g.nelloc);
+      CU(cudaMemcpy(h.data(), s.dv, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToHost));
+      for (double& v : h) v *= ctx->prm.volfrac;
+      CU(cudaMemcpy(s.x, h.data(), sizeof(double) * s.g.nelloc, cudaMemcpyHostToDevice));
+    }
+  }
+  for (Slab& s : ctx->slabs) LAUNCH(ctx, k_apply_passive, grid_for(s.g.nelloc), s.g, s.passive, s.x);
+  CK(check_launch(ctx));
+  CK(exchange_elems(ctx, &Slab::x, ctx->slabs[0].g.H));
+  if (also_xphys)
+    for (Slab& s : ctx->slabs)
+      CU(cudaMemcpyAsync(s.xphys, s.x, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
+  ctx->has_E = false;
+  ctx->has_sens = ctx->has_dcf = false;
+  return TOPO_OK;
+}
+
+int topo_set_density(topo_ctx* ctx, const double* x) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(set_x_common(ctx, x, true));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+int topo_set_xphys(topo_ctx* ctx, const double* xphys) {
+  if (!ctx || !xphys) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(upload_elems(ctx, xphys, &Slab::xphys));
+  for (Slab& s : ctx->slabs) LAUNCH(ctx, k_apply_passive, grid_for(s.g.nelloc), s.g, s.passive, s.xphys);
+  CK(check_launch(ctx));
+  CK(exchange_elems(ctx, &Slab::xphys, ctx->slabs[0].g.H));
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->has_E = false;
+  return TOPO_OK;
+}
+
+int topo_update_modulus(topo_ctx* ctx) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(update_modulus(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+int topo_solve(topo_ctx* ctx, double* u, topo_solve_info* info) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  CK(update_modulus(ctx));
+  CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  int rc = do_solve(ctx, info);
+  if (u) CK(download_nodes(ctx, &Slab::u, u));
+  return rc;
+}
+
+int topo_sensitivity(topo_ctx* ctx, double* c, double* ce, double* dc) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(do_sensitivity(ctx, c, nullptr));
+  if (ce) CK(download_elems(ctx, &Slab::ce, ce));
+  if (dc) CK(download_elems(ctx, &Slab::dc, dc));
+  return TOPO_OK;
+}
+
+int topo_filter(topo_ctx* ctx, int32_t what, const double* in, double* out) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  if (what == TOPO_FILTER_DC) {
+    if (in) {
+      CK(upload_elems(ctx, in, &Slab::dc));
+      ctx->has_sens = true;
+    }
+    if (!ctx->has_sens) return set_err(ctx, TOPO_ESTATE, "topo_filter(DC) before topo_sensitivity");
+    CK(do_filter_dc(ctx));
+    if (out) CK(download_elems(ctx, &Slab::dcf, out));
+    return TOPO_OK;
+  }
+  if (what == TOPO_FILTER_X) {
+    if (in) CK(set_x_common(ctx, in, false));
+    CK(do_filter_x(ctx));
+    if (out) CK(download_elems(ctx, &Slab::xphys, out));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return TOPO_OK;
+  }
+  return set_err(ctx, TOPO_EINVAL, "topo_filter: bad `what`");
+}
+
+int topo_oc_step(topo_ctx* ctx, double* xnew, double* lambda, double* change, double* volume) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(do_oc(ctx, lambda, change, volume));
+  if (xnew) CK(download_elems(ctx, &Slab::x, xnew));
+  return TOPO_OK;
+}
+
+int topo_optimize(topo_ctx* ctx, int32_t n_iter, double change_tol, double* c_hist, double* x_out,
+                  int32_t* n_done) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  if (n_done) *n_done = 0;
+  int rc = TOPO_OK;
+  for (int it = 0; it < n_iter; ++it) {
+    cudaEvent_t* ev = ctx->ev;
+    CU(cudaEventRecord(ev[0], ctx->stream));
+    CK(update_modulus(ctx));
+    CU(cudaEventRecord(ev[1], ctx->stream));
+    rc = do_solve(ctx, nullptr);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[2], ctx->stream));
+    double c = 0.0, fu = 0.0;
+    rc = do_sensitivity(ctx, &c, &fu);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[3], ctx->stream));
+    rc = do_filter_dc(ctx);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[4], ctx->stream));
+    double lam, chg, vol;
+    rc = do_oc(ctx, &lam, &chg, &vol);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[5], ctx->stream));
+    CU(cudaEventSynchronize(ev[5]));
+    float t[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
+    ctx->tim.ms_efield = t[0];
+    ctx->tim.ms_solve = t[1];
+    ctx->tim.ms_sens = t[2];
+    ctx->tim.ms_filter = t[3];   // dc filter; the x filter is inside ms_oc
+    ctx->tim.ms_oc = t[4];
+    ctx->tim.ms_total = t[0] + t[1] + t[2] + t[3] + t[4];
+    if (c_hist) c_hist[it] = c;
+    if (n_done) *n_done = it + 1;
+    if (change_tol > 0 && chg < change_tol) break;
+  }
+  if (x_out) CK(download_elems(ctx, &Slab::x, x_out));
+  return rc;
+}
+
+int topo_apply_K(topo_ctx* ctx, const double* p, double* q) {
+  if (!ctx || !p) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(topo_matvec_load(ctx, p));
+  CK(topo_matvec_run(ctx, 1));
+  if (q) CK(download_nodes(ctx, &Slab::q, q));
+  return TOPO_OK;
+}
+
+int topo_matvec_load(topo_ctx* ctx, const double* p) {
+  if (!ctx || !p) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  CK(upload_nodes(ctx, p, &Slab::w));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.w);
+  CK(check_launch(ctx));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+int topo_matvec_run(topo_ctx* ctx, int32_t reps) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  for (int i = 0; i < reps; ++i) CK(matvec_all(ctx, &Slab::w, &Slab::q));
+  return TOPO_OK;
+}
+
+int topo_get(topo_ctx* ctx, int32_t field, double* out) {
+  if (!ctx || !out) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  switch (field) {
+    case TOPO_FIELD_U: return download_nodes(ctx, &Slab::u, out);
+    case TOPO_FIELD_X: return download_elems(ctx, &Slab::x, out);
+    case TOPO_FIELD_XPHYS: return download_elems(ctx, &Slab::xphys, out);
+    case TOPO_FIELD_E: return download_elems(ctx, &Slab::E, out);
+    case TOPO_FIELD_CE: return download_elems(ctx, &Slab::ce, out);
+    case TOPO_FIELD_DC: return download_elems(ctx, &Slab::dc, out);
+    case TOPO_FIELD_DCF: return download_elems(ctx, &Slab::dcf, out);
+    case TOPO_FIELD_DVF: return download_elems(ctx, &Slab::dvf, out);
+    case TOPO_FIELD_XNEW: return download_elems(ctx, &Slab::xnew, out);
+    case TOPO_FIELD_HS: return download_elems(ctx, &Slab::hs, out);
+    case TOPO_FIELD_INVDIAG: return download_nodes(ctx, &Slab::invd, out);
+    case TOPO_FIELD_R: return download_nodes(ctx, &Slab::r, out);
+    default: return set_err(ctx, TOPO_EINVAL, "unknown field %d", field);
+  }
+}
+
+int topo_get_timings(const topo_ctx* ctx, topo_timings* t) {
+  if (!ctx || !t) return TOPO_EINVAL;
+  *t = ctx->tim;
+  t->kernel_launches = ctx->launches;
+  return TOPO_OK;
+}
+
+int topo_profile(topo_ctx* ctx, int32_t enable) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->profile = enable != 0;
+  ctx->prof_ms = 0.0;
+  ctx->prof_n = 0;
+  return TOPO_OK;
+}
+
+int topo_kernel_time(topo_ctx* ctx, double* mean_ms, int64_t* samples) {
+  if (!ctx) return TOPO_EINVAL;
+  if (mean_ms) *mean_ms = ctx->prof_n ? ctx->prof_ms / ctx->prof_n : 0.0;
+  if (samples) *samples = ctx->prof_n;
+  return TOPO_OK;
+}
+
+int64_t topo_count(const topo_ctx* ctx, int32_t what) {
+  if (!ctx) return -1;
+  const topo_params& P = ctx->prm;
+  switch (what) {
+    case TOPO_COUNT_NDOF: return 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+    case TOPO_COUNT_NEL: return (long long)P.nelx * P.nely * P.nelz;
+    case TOPO_COUNT_NODES: return (long long)(P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+    case TOPO_COUNT_DESIGN: return ctx->n_design;
+    case TOPO_COUNT_STENCIL: return (long long)ctx->st_off.size();
+    case TOPO_COUNT_DEVICE_BYTES: return (long long)ctx->dev_bytes;
+    default: return -1;
+  }
+}
+
+void topo_destroy(topo_ctx* ctx) { free_ctx(ctx); }
+
+}  // extern "C"

@@ -156,3 +156,16 @@ def test_true_residual_of_direct_solve():
     K = assemble(*dims, KE, E)
     f, fixed = cantilever_load(*dims), cantilever_fixed(*dims)
     assert true_residual(K, solve_direct(K, f, fixed), f, fixed) < 1e-10
+
+
+def test_matvec_rows_equals_csr():
+    dims = (6, 5, 4)
+    KE = element_stiffness(NU)
+    E = random_density(120, seed=8)
+    K = assemble(*dims, KE, E)
+    fixed = cantilever_fixed(*dims)
+    p = random_vector(K.shape[0], seed=2)
+    q = matvec_free(K, p, fixed)
+    from oracle import matvec_rows
+    nodes = np.arange(0, K.shape[0] // 3, 7)
+    assert np.allclose(matvec_rows(*dims, KE, E, p, fixed, nodes), q.reshape(-1, 3)[nodes], rtol=0, atol=1e-14)
