@@ -305,15 +305,16 @@ def main():
 
     peaks, peaks_src = load_peaks()
     hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-    # dominant kernel: the PCG matvec k_matvec<true>; algorithmic bytes per launch
-    # = read p (24 B/node) + E (8 B/el) + write q (24 B/node)  [SURVEY §8(d): 16 B/DOF + 8 B/el]
+    # dominant kernel: the fused PCG matvec k_mv_wht<fused,dot>; algorithmic bytes per
+    # launch = read r (24 B/node), M^-1 (8 B/node), p_old (24 B/node), fixed mask (1 B/node),
+    # E (8 B/el); write p_new (24 B/node), q (24 B/node)  -> 105 B/node + 8 B/el
     own_el = n_el // world
     own_nd = n_nd // world
-    mv_bytes = 48 * own_nd + 8 * own_el
+    mv_bytes = 105 * own_nd + 8 * own_el
     achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": (achieved / hbm) if achieved else None, "traffic": None,
-            "kernel": "k_matvec<true> (PCG q = K p, fused p.q)", "samples": mv_samples,
+            "kernel": "k_mv_wht<fused,dot> (p = M^-1 r + beta p; q = K p; p.q)", "samples": mv_samples,
             "mean_ms": mv_ms, "bytes_per_launch": mv_bytes, "peak_source": peaks_src}
 
     cpu = None

@@ -72,3 +72,26 @@ def apply_filter(H, Hs, mode, what, v, x=None, passive=None):
             return v.copy()
         return (H @ v) / Hs
     raise ValueError(mode)
+
+
+def filter_rows(nelx, nely, nelz, rmin, rows):
+    """Rows of H for a list of element ids, by brute force over the offset box
+    (for sampled checks on grids whose H does not fit).  Returns a list of
+    (cols, weights) and the row sums Hs[rows]."""
+    R = int(np.ceil(rmin))
+    out, hs = [], []
+    for e in rows:
+        ez, rem = divmod(int(e), nelx * nely)
+        ex, ey = divmod(rem, nely)
+        cols, w = [], []
+        for dz in range(-R, R + 1):
+            for dx in range(-R, R + 1):
+                for dy in range(-R, R + 1):
+                    d = np.sqrt(float(dx * dx + dy * dy + dz * dz))
+                    jx, jy, jz = ex + dx, ey + dy, ez + dz
+                    if d < rmin and 0 <= jx < nelx and 0 <= jy < nely and 0 <= jz < nelz:
+                        cols.append(jz * nelx * nely + jx * nely + jy)
+                        w.append(rmin - d)
+        out.append((np.array(cols), np.array(w)))
+        hs.append(float(np.sum(w)))
+    return out, np.array(hs)

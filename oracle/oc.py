@@ -26,6 +26,16 @@ def sensitivities(xPhys, ce, penal, E0, Emin, passive=None):
     return E, c, dc, dv
 
 
+def oc_xnew(x, dc_f, dv_f, lmid, move, passive=None):
+    """xnew(lmid) on design elements, 0 on passive (R15-R17)."""
+    D = np.ones(x.shape, dtype=bool) if passive is None else (np.asarray(passive) == 0)
+    xs = np.zeros_like(x)
+    xd, dcd, dvd = x[D], dc_f[D], dv_f[D]
+    cand = xd * np.sqrt(np.maximum(0.0, -dcd / (dvd * lmid)))
+    xs[D] = np.maximum(0.0, np.maximum(xd - move, np.minimum(1.0, np.minimum(xd + move, cand))))
+    return xs
+
+
 def oc_update(x, dc_f, dv_f, volfrac, move, tol, lmax, mode, H=None, Hs=None, passive=None,
               trace=None):
     """Returns (xnew, lmid_last, V_last, n_passes).  Literal bisection loop."""
@@ -35,11 +45,7 @@ def oc_update(x, dc_f, dv_f, volfrac, move, tol, lmax, mode, H=None, Hs=None, pa
     xnew, lmid, V, n = x.copy(), None, None, 0
     while (l2 - l1) / (l1 + l2) > tol:
         lmid = 0.5 * (l2 + l1)
-        xs = np.zeros_like(x)
-        xd, dcd, dvd = x[D], dc_f[D], dv_f[D]
-        cand = xd * np.sqrt(np.maximum(0.0, -dcd / (dvd * lmid)))
-        xs[D] = np.maximum(0.0, np.maximum(xd - move, np.minimum(1.0, np.minimum(xd + move, cand))))
-        xnew = xs
+        xnew = oc_xnew(x, dc_f, dv_f, lmid, move, passive)
         if mode == 0:
             xp = (H @ xnew) / Hs
             V = float(np.sum(xp[D]))

@@ -77,9 +77,15 @@ __device__ __forceinline__ void warp_sum(double (&v)[K]) {
     for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
 }
 
+__device__ __forceinline__ int flat_tid() { return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z); }
+__device__ __forceinline__ int flat_nthreads() { return blockDim.x * blockDim.y * blockDim.z; }
+__device__ __forceinline__ unsigned flat_bid() { return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); }
+__device__ __forceinline__ unsigned flat_nblocks() { return gridDim.x * gridDim.y * gridDim.z; }
+
 template <int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double (*sh)[32]) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tid = flat_tid();
+  const int lane = tid & 31, wid = tid >> 5, nw = flat_nthreads() >> 5;
   warp_sum<K>(v);
   __syncthreads();
   if (lane == 0)
@@ -93,7 +99,8 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double (*sh)[32]) {
 
 // Max-reduction variant for a single value.
 __device__ __forceinline__ double block_max(double v, double* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tid = flat_tid();
+  const int lane = tid & 31, wid = tid >> 5, nw = flat_nthreads() >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
@@ -105,17 +112,21 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   return v;
 }
 
-// `partials` holds K*gridDim.x doubles; `counter` must be 0 on entry and is
-// reset by the last block.  `nmax` (K2 > K) entries are max-reduced.
+// Deterministic grid reduction over a 1-3D grid of 1-3D blocks (blocks are a
+// multiple of 32 threads).  `partials` holds K*nblocks doubles; `counter`
+// must be 0 on entry and is reset by the last block.  The last KMAX of the K
+// values are max-reduced, the others summed.  Returns true in every thread of
+// the last block; `out_sh[k]` (shared) then holds the totals.
 template <int K, int KMAX = 0>
 __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* counter,
                             double* out_sh) {
   __shared__ double sh[K > 0 ? K : 1][32];
   __shared__ bool am_last;
+  const int tid = flat_tid(), nth = flat_nthreads();
+  const unsigned bid = flat_bid(), nb = flat_nblocks();
   double vs[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) vs[k] = v[k];
-  // sum part
   {
     double t[K];
 #pragma unroll
@@ -126,12 +137,12 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
   }
 #pragma unroll
   for (int k = K - KMAX; k < K; ++k) vs[k] = block_max(vs[k], &sh[0][0]);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) partials[(size_t)k * gridDim.x + blockIdx.x] = vs[k];
+    for (int k = 0; k < K; ++k) partials[(size_t)k * nb + bid] = vs[k];
     __threadfence();
     unsigned int prev = atomicAdd(counter, 1u);
-    am_last = (prev == gridDim.x - 1);
+    am_last = (prev == nb - 1);
   }
   __syncthreads();
   if (!am_last) return false;
@@ -140,8 +151,8 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double a = (k < K - KMAX) ? 0.0 : -1.0e300;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-      double pv = __ldcg(&partials[(size_t)k * gridDim.x + b]);
+    for (unsigned b = tid; b < nb; b += nth) {
+      double pv = __ldcg(&partials[(size_t)k * nb + b]);
       a = (k < K - KMAX) ? a + pv : fmax(a, pv);
     }
     t[k] = a;
@@ -156,7 +167,7 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
   }
 #pragma unroll
   for (int k = K - KMAX; k < K; ++k) t[k] = block_max(t[k], &sh[0][0]);
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) out_sh[k] = t[k];
     *counter = 0u;

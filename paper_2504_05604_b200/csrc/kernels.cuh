@@ -50,7 +50,7 @@ __global__ void k_efield(Geo g, Material m, const double* __restrict__ xphys,
   }
 }
 
-// Jacobi inverse diagonal per DOF: 1/(kd * sum_{e ni n} E_e), 0 on fixed DOFs.
+// Jacobi inverse diagonal per node: 1/(kd * sum_{e ni n} E_e).
 // diag(K) is one scalar per node because every KE_ii = (lambda+4mu)/9.
 __global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
                           const uint8_t* __restrict__ fixm, double* __restrict__ invd) {
@@ -63,88 +63,8 @@ __global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
 #pragma unroll
     for (int d = 0; d < 8; ++d)
       s += E[elem_idx(g, ix - 1 + (d & 1), iy - 1 + ((d >> 1) & 1), iz - 1 + (d >> 2))];
-    const double v = 1.0 / (m.kd * s);
-    const uint8_t fm = fixm[i];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) invd[c * g.ncomp + i] = (fm >> c) & 1 ? 0.0 : v;
-  }
-}
-
-// ===========================================================================
-// A2  EbE matvec  q_n = sum_{e ni n} E_e KE[ln,:] p_e, q = 0 on fixed DOFs.
-// Node-centric gather: each thread owns one node, loops over its 27
-// neighbours once (3 loads each) and accumulates the 8 element row-blocks;
-// all KE indices are compile-time constants (constant-bank operands).
-// ===========================================================================
-template <bool kDot>
-__global__ void __launch_bounds__(kBlock)
-k_matvec(Geo g, DevState* st, int gate, const double* __restrict__ E,
-         const double* __restrict__ p, const uint8_t* __restrict__ fixm,
-         double* __restrict__ q, double* partials, unsigned int* counter, int finish) {
-  if (gate && st->done) return;
-  const long long b0 = g.nplane, e0 = (long long)(g.nown + 1) * g.nplane;
-  double dot = 0.0;
-  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
-       i += (long long)gridDim.x * blockDim.x) {
-    int ix, iy, iz;
-    if (!decode_node(g, i, ix, iy, iz)) continue;
-    double s[8][3];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) s[e][0] = s[e][1] = s[e][2] = 0.0;
-#pragma unroll
-    for (int oz = -1; oz <= 1; ++oz)
-#pragma unroll
-      for (int ox = -1; ox <= 1; ++ox)
-#pragma unroll
-        for (int oy = -1; oy <= 1; ++oy) {
-          const long long j = i + ox * g.nplane + oz * g.NY + oy;
-          const double p0 = p[j], p1 = p[j + g.ncomp], p2 = p[j + 2 * g.ncomp];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int dx = e & 1, dy = (e >> 1) & 1, dz = e >> 2;
-            const int a = ox + 1 - dx, bb = oy + 1 - dy, c = oz + 1 - dz;
-            if (a < 0 || a > 1 || bb < 0 || bb > 1 || c < 0 || c > 1) continue;
-            const int ln = lidx(1 - dx, 1 - dy, 1 - dz), lm = lidx(a, bb, c);
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-              const int r = (3 * ln + ci) * 24 + 3 * lm;
-              s[e][ci] = fma(c_KE[r + 0], p0, s[e][ci]);
-              s[e][ci] = fma(c_KE[r + 1], p1, s[e][ci]);
-              s[e][ci] = fma(c_KE[r + 2], p2, s[e][ci]);
-            }
-          }
-        }
-    double qv[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const double Ee = E[elem_idx(g, ix - 1 + (e & 1), iy - 1 + ((e >> 1) & 1), iz - 1 + (e >> 2))];
-#pragma unroll
-      for (int ci = 0; ci < 3; ++ci) qv[ci] = fma(Ee, s[e][ci], qv[ci]);
-    }
-    const uint8_t fm = fixm[i];
-#pragma unroll
-    for (int ci = 0; ci < 3; ++ci) {
-      const double v = (fm >> ci) & 1 ? 0.0 : qv[ci];
-      q[i + ci * g.ncomp] = v;
-      if (kDot) dot = fma(p[i + ci * g.ncomp], v, dot);
-    }
-  }
-  if (kDot) {
-    __shared__ double tot[1];
-    double v[1] = {dot};
-    if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) {
-      if (finish) {
-        st->pq = tot[0];
-        if (!(tot[0] > 0.0) || !isfinite(tot[0])) {
-          st->status = 3;
-          st->done = 1;
-        } else {
-          st->alpha = st->rz / tot[0];
-        }
-      } else {
-        st->sums[0] = tot[0];
-      }
-    }
+    // one scalar per node (r is exactly 0 on fixed DOFs, so no mask is needed)
+    invd[i] = 1.0 / (m.kd * s);
   }
 }
 
@@ -152,19 +72,6 @@ k_matvec(Geo g, DevState* st, int gate, const double* __restrict__ E,
 // A3/A4  PCG vector kernels over the owned node planes (pads are zero and
 // stay zero).  SoA: component stride ncomp.
 // ===========================================================================
-// p = M^{-1} r + beta p   (beta = 0 on a fresh start)
-__global__ void k_pupdate(Geo g, DevState* st, const double* __restrict__ r,
-                          const double* __restrict__ invd, double* __restrict__ p) {
-  if (st->done) return;
-  const double beta = st->fresh ? 0.0 : st->beta;
-  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
-    p[i] = fma(beta, p[i], invd[i] * r[i]);
-  }
-}
-
 __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, double rr) {
   st->beta = rz_new / st->rz;
   st->rz = rz_new;
@@ -182,23 +89,39 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
   }
 }
 
-// u += alpha p ; r -= alpha q ; partial (r M^{-1} r, r r)
+// u += alpha p ; r -= alpha q ; partial (r M^{-1} r, r r).  double2 over
+// pairs of nodes of the owned planes (pads are zero and stay zero).
 __global__ void __launch_bounds__(kBlock)
 k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
          const double* __restrict__ p, const double* __restrict__ q,
          const double* __restrict__ invd, double* partials, unsigned int* counter, int finish) {
   if (st->done) return;
   const double alpha = st->alpha;
-  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  const long long b0 = g.nplane, npair = (long long)g.nown * g.nplane / 2;
   double rz = 0.0, rr = 0.0;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
-    u[i] = fma(alpha, p[i], u[i]);
-    const double rv = fma(-alpha, q[i], r[i]);
-    r[i] = rv;
-    rz = fma(rv * invd[i], rv, rz);
-    rr = fma(rv, rv, rr);
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < npair;
+       j += (long long)gridDim.x * blockDim.x) {
+    const long long i = b0 + 2 * j;
+    const double2 iv = *reinterpret_cast<const double2*>(invd + i);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long k = i + c * g.ncomp;
+      double2 uu = *reinterpret_cast<const double2*>(u + k);
+      const double2 pp = *reinterpret_cast<const double2*>(p + k);
+      double2 rv = *reinterpret_cast<const double2*>(r + k);
+      const double2 qq = *reinterpret_cast<const double2*>(q + k);
+      uu.x = fma(alpha, pp.x, uu.x);
+      uu.y = fma(alpha, pp.y, uu.y);
+      rv.x = fma(-alpha, qq.x, rv.x);
+      rv.y = fma(-alpha, qq.y, rv.y);
+      *reinterpret_cast<double2*>(u + k) = uu;
+      *reinterpret_cast<double2*>(r + k) = rv;
+      s0 = fma(rv.x, rv.x, s0);
+      s1 = fma(rv.y, rv.y, s1);
+    }
+    rz = fma(s0, iv.x, fma(s1, iv.y, rz));
+    rr += s0 + s1;
   }
   __shared__ double tot[2];
   double v[2] = {rz, rr};
@@ -229,13 +152,18 @@ k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __re
            double* partials, unsigned int* counter) {
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   double rz = 0.0, rr = 0.0;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x) {
-    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
-    const double rv = f[i] - q[i];
-    if (write_r) r[i] = rv;
-    rz = fma(rv * invd[i], rv, rz);
-    rr = fma(rv, rv, rr);
+    const long long i = b0 + k;
+    double s = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double rv = f[i + c * g.ncomp] - q[i + c * g.ncomp];
+      if (write_r) r[i + c * g.ncomp] = rv;
+      s = fma(rv, rv, s);
+    }
+    rz = fma(s, invd[i], rz);
+    rr += s;
   }
   __shared__ double tot[2];
   double v[2] = {rz, rr};
@@ -474,6 +402,21 @@ __global__ void k_nodes_out(Geo g, const double* __restrict__ in, double* __rest
   }
 }
 // elements: ext[(ez*nex + exr)*nely + ey] for the owned x range
+// per-node scalar (Jacobi inverse diagonal) -> per-DOF external array, 0 on fixed DOFs
+__global__ void k_invd_out(Geo g, const double* __restrict__ in, const uint8_t* __restrict__ fixm,
+                           double* __restrict__ ext, int ix0, int nix) {
+  const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int iy = (int)(k % (g.nely + 1));
+    const long long t = k / (g.nely + 1);
+    const int ixr = (int)(t % nix), iz = (int)(t / nix);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+    const uint8_t fm = fixm[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) ext[3 * k + c] = (fm >> c) & 1 ? 0.0 : in[i];
+  }
+}
 __global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __restrict__ in) {
   const long long tot = (long long)g.nex * g.nelz * g.nely;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;

@@ -1,5 +1,7 @@
 // libtopo: C-ABI implementation of the matrix-free SIMP hot path on B200.
 // See include/topo.h for the contract and DESIGN.md for the design.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -7,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -14,9 +17,11 @@
 #include "../../include/topo.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include "matvec_wht.cuh"
 
 namespace topo {
 void build_element_stiffness(double nu, double* ke);  // ke_host.cpp
+bool wht_constants(const double* ke, double out[8], double tol);
 }
 using namespace topo;
 
@@ -78,8 +83,9 @@ struct TopoError {
 struct Slab {
   Geo g{};
   // node vectors: 3*ncomp doubles each (SoA)
-  double *u = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *f = nullptr, *invd = nullptr,
+  double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
          *w = nullptr;
+  double* invd = nullptr;    // per node (1 component): 1/(kd sum E)
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
   double *E = nullptr, *x = nullptr, *xphys = nullptr, *dc = nullptr, *dcf = nullptr,
@@ -90,6 +96,8 @@ struct Slab {
   DevState* st = nullptr;
   double* stage = nullptr;   // staging for layout transforms
   size_t stage_n = 0;
+  // TMA descriptors of the matvec operands (built at init; pointers never change)
+  CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E;
 };
 
 struct topo_ctx {
@@ -100,6 +108,8 @@ struct topo_ctx {
   ncclComm_t comm = nullptr;
   double ke[576];
   double kd = 0.0;
+  WhtK wht{};
+  int tz = 8;               // z extent of a matvec CTA (threads 32 x tz)
   std::vector<int4> st_off;
   std::vector<double> st_w;
   int R = 0;
@@ -128,6 +138,8 @@ struct topo_ctx {
   long long launches = 0;
   std::string err;
   size_t dev_bytes = 0;
+  bool debug = false;        // TOPO_DEBUG_SYNC=1: no graphs, sync + check after every kernel
+  int sticky = TOPO_OK;
 };
 
 namespace {
@@ -171,13 +183,22 @@ inline int grid_for(long long n) {
 }
 
 // --- launch helpers (count launches) ----------------------------------------
+void debug_sync(topo_ctx* ctx, const char* name) {
+  if (!ctx->debug || ctx->sticky) return;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) ctx->sticky = set_err(ctx, TOPO_ECUDA, "kernel %s: %s", name, cudaGetErrorString(e));
+}
+
 #define LAUNCH(ctx, kern, grid, ...)                                      \
   do {                                                                    \
     kern<<<(grid), kBlock, 0, (ctx)->stream>>>(__VA_ARGS__);              \
     (ctx)->launches++;                                                    \
+    debug_sync((ctx), #kern);                                             \
   } while (0)
 
 int check_launch(topo_ctx* ctx) {
+  if (ctx->sticky) return ctx->sticky;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
   return TOPO_OK;
@@ -186,6 +207,7 @@ int check_launch(topo_ctx* ctx) {
 int ensure_constants(topo_ctx* ctx) {
   if (g_const_owner == ctx) return TOPO_OK;
   CU(cudaMemcpyToSymbolAsync(c_KE, ctx->ke, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyToSymbolAsync(c_wht, &ctx->wht, sizeof(WhtK), 0, cudaMemcpyHostToDevice, ctx->stream));
   if (!ctx->st_off.empty()) {
     CU(cudaMemcpyToSymbolAsync(c_st_off, ctx->st_off.data(), sizeof(int4) * ctx->st_off.size(), 0,
                                cudaMemcpyHostToDevice, ctx->stream));
@@ -228,14 +250,14 @@ int allreduce(topo_ctx* ctx, int k0, int nk, int maxmask) {
 }
 
 // node planes of a 3-component vector: owned boundary planes -> neighbours' ghosts
-int exchange_nodes(topo_ctx* ctx, double* Slab::*field) {
+int exchange_nodes(topo_ctx* ctx, double* Slab::*field, int ncomp = 3) {
   const int W = ctx->world;
   if (W == 1) return TOPO_OK;
   if (ctx->mode == TOPO_DIST_LOOPBACK) {
     for (int s = 0; s < W; ++s) {
       Slab& a = ctx->slabs[s];
       const size_t bytes = sizeof(double) * a.g.nplane;
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < ncomp; ++c) {
         double* v = a.*field + c * a.g.ncomp;
         if (s > 0) {
           Slab& l = ctx->slabs[s - 1];
@@ -254,7 +276,7 @@ int exchange_nodes(topo_ctx* ctx, double* Slab::*field) {
   Slab& a = ctx->slabs[0];
   const size_t n = a.g.nplane;
   NC(g_nccl.GroupStart());
-  for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < ncomp; ++c) {
     double* v = a.*field + c * a.g.ncomp;
     if (ctx->rank > 0) {
       NC(g_nccl.Send(v + a.g.nplane, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
@@ -369,6 +391,25 @@ int download_nodes(topo_ctx* ctx, double* Slab::*field, double* host) {
   return TOPO_OK;
 }
 
+int download_invd(topo_ctx* ctx, double* host) {
+  const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
+  std::vector<double> tmp;
+  for (Slab& s : ctx->slabs) {
+    int ix0, nix;
+    slab_node_range(s, ix0, nix);
+    const size_t row = (size_t)nix * (nely + 1) * 3;
+    LAUNCH(ctx, k_invd_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.invd, s.fixm, s.stage, ix0, nix);
+    CK(check_launch(ctx));
+    tmp.resize(row * (nelz + 1));
+    CU(cudaMemcpyAsync(tmp.data(), s.stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int iz = 0; iz <= nelz; ++iz)
+      memcpy(host + 3 * ((size_t)iz * (nelx + 1) * (nely + 1) + (size_t)ix0 * (nely + 1)), &tmp[iz * row],
+             sizeof(double) * row);
+  }
+  return TOPO_OK;
+}
+
 int upload_elems(topo_ctx* ctx, const double* host, double* Slab::*field) {
   const int nelx = ctx->prm.nelx, nely = ctx->prm.nely, nelz = ctx->prm.nelz;
   std::vector<double> tmp;
@@ -446,47 +487,138 @@ int update_modulus(topo_ctx* ctx) {
   return TOPO_OK;
 }
 
-// q = K p for every slab (p ghosts exchanged first)
-int matvec_all(topo_ctx* ctx, double* Slab::*pin, double* Slab::*qout) {
-  CK(exchange_nodes(ctx, pin));
-  for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_matvec<false>, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, 0, s.E, s.*pin,
-           s.fixm, s.*qout, s.partials, s.counter, 0);
+// launch geometry of the WHT matvec for one slab: (gy, gz, gx) CTAs of 32 x tz
+struct MvGrid { dim3 grid, block; int CX; };
+MvGrid mv_grid(const topo_ctx* ctx, const Geo& g) {
+  const int tz = ctx->tz;
+  const int gy = (g.nely + 1 + 30) / 31, gz = (g.nelz + 1 + tz - 2) / (tz - 1);
+  const long long tiles = (long long)gy * gz;
+  const long long target = 148LL * (tz <= 8 ? 2 : 1) * 8;   // ~8 waves of resident CTAs
+  long long gx = (target + tiles - 1) / tiles;
+  gx = std::max(1LL, std::min<long long>(gx, (g.nown + 3) / 4));   // >= 4 planes per chunk
+  const int CX = (int)((g.nown + gx - 1) / gx);
+  gx = (g.nown + CX - 1) / CX;
+  return MvGrid{dim3(gy, gz, (unsigned)gx), dim3(32, tz, 1), CX};
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encode(topo_ctx* ctx) {
+  if (g_encode) return TOPO_OK;
+  cudaDriverEntryPointQueryResult qr;
+  CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_encode, cudaEnableDefault, &qr));
+  if (qr != cudaDriverEntryPointSuccess || !g_encode)
+    return set_err(ctx, TOPO_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  return TOPO_OK;
+}
+
+// rank-4 {NY, NZ, NXL, ncomp} (ncomp = 3) or rank-3 {NY, NZ, NXL} (ncomp = 1) node map
+int map_nodes(topo_ctx* ctx, CUtensorMap* m, double* ptr, const Geo& g, int ncomp) {
+  const cuuint64_t dims[4] = {(cuuint64_t)g.NY, (cuuint64_t)g.NZ, (cuuint64_t)g.NXL, 3};
+  const cuuint64_t strides[3] = {(cuuint64_t)g.NY * 8, (cuuint64_t)g.nplane * 8, (cuuint64_t)g.ncomp * 8};
+  const cuuint32_t box[4] = {34, (cuuint32_t)ctx->tz + 1, 1, 3};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, ncomp == 3 ? 4 : 3, ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(ctx, TOPO_ECUDA, "cuTensorMapEncodeTiled(nodes) failed: %d", (int)r);
+  return TOPO_OK;
+}
+
+int map_elems(topo_ctx* ctx, CUtensorMap* m, double* ptr, const Geo& g) {
+  const cuuint64_t dims[3] = {(cuuint64_t)g.EY, (cuuint64_t)g.EZ, (cuuint64_t)g.NEXL};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.EY * 8, (cuuint64_t)g.eplane * 8};
+  const cuuint32_t box[3] = {34, (cuuint32_t)ctx->tz, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(ctx, TOPO_ECUDA, "cuTensorMapEncodeTiled(elems) failed: %d", (int)r);
+  return TOPO_OK;
+}
+
+int build_maps(topo_ctx* ctx, Slab& s) {
+  CK(get_encode(ctx));
+  CK(map_nodes(ctx, &s.m_r, s.r, s.g, 3));
+  CK(map_nodes(ctx, &s.m_u, s.u, s.g, 3));
+  CK(map_nodes(ctx, &s.m_w, s.w, s.g, 3));
+  CK(map_nodes(ctx, &s.m_p0, s.p0, s.g, 3));
+  CK(map_nodes(ctx, &s.m_p1, s.p1, s.g, 3));
+  CK(map_nodes(ctx, &s.m_invd, s.invd, s.g, 1));
+  CK(map_elems(ctx, &s.m_E, s.E, s.g));
+  return TOPO_OK;
+}
+
+template <int TZ, bool kFused, bool kDot>
+int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish) {
+  static bool attr_set = false;
+  const int smem = MvSmem<TZ>::bytes(kFused);
+  if (!attr_set) {
+    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kFused, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set = true;
+  }
+  const MvGrid m = mv_grid(ctx, s.g);
+  k_mv_wht<TZ, kFused, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, s.fixm, pnew, q,
+                                                                     s.partials, s.counter, finish);
+  ctx->launches++;
+  debug_sync(ctx, kFused ? "k_mv_wht<fused>" : "k_mv_wht<plain>");
   return check_launch(ctx);
 }
 
-// residual r(or w) = f - K u ; sums[0,1] = (rz, rr) allreduced
+template <bool kFused, bool kDot>
+int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CUtensorMap* pold, double* pnew,
+              double* q, int finish) {
+  MvMaps maps;
+  maps.vin = vin;
+  maps.pold = pold ? *pold : vin;
+  maps.invd = s.m_invd;
+  maps.E = s.m_E;
+  if (ctx->tz == 16) return launch_mv_t<16, kFused, kDot>(ctx, s, gate, maps, pnew, q, finish);
+  return launch_mv_t<8, kFused, kDot>(ctx, s, gate, maps, pnew, q, finish);
+}
+
+// q = K v for every slab (v ghosts exchanged first; v must be 0 on fixed DOFs)
+int matvec_all(topo_ctx* ctx, double* Slab::*pin, CUtensorMap Slab::*pmap, double* Slab::*qout) {
+  CK(exchange_nodes(ctx, pin));
+  for (Slab& s : ctx->slabs) CK((launch_mv<false, false>(ctx, s, 0, s.*pmap, nullptr, nullptr, s.*qout, 0)));
+  return check_launch(ctx);
+}
+
+// residual r = f - K u ; sums[0,1] = (rz, rr) allreduced; r ghosts refreshed
 int residual(topo_ctx* ctx, bool write_r) {
-  CK(matvec_all(ctx, &Slab::u, &Slab::q));
+  CK(matvec_all(ctx, &Slab::u, &Slab::m_u, &Slab::q));
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_residual, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.r,
+    LAUNCH(ctx, k_residual, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.r,
            write_r ? 1 : 0, s.partials, s.counter);
   CK(check_launch(ctx));
+  if (write_r) CK(exchange_nodes(ctx, &Slab::r));
   return allreduce(ctx, 0, 2, 0);
 }
 
-// enqueue one PCG iteration
-int enqueue_cg_iter(topo_ctx* ctx, bool prof_here) {
+// enqueue one PCG iteration; `parity` selects the p ping-pong direction
+int enqueue_cg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   const int W = ctx->world;
   const int fin = (W == 1) ? 1 : 0;
-  for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_pupdate, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.r, s.invd, s.p);
-  CK(exchange_nodes(ctx, &Slab::p));
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
-  for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_matvec<true>, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, 1, s.E, s.p, s.fixm,
-           s.q, s.partials, s.counter, fin);
+  for (Slab& s : ctx->slabs) {
+    const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
+    double* pnew = parity ? s.p0 : s.p1;
+    CK((launch_mv<true, true>(ctx, s, 1, s.m_r, pold, pnew, s.q, fin)));
+  }
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
   if (!fin) {
     CK(allreduce(ctx, 0, 1, 0));
     for (Slab& s : ctx->slabs) { k_finish_alpha<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
   }
-  for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_update, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.u, s.r, s.p, s.q, s.invd,
-           s.partials, s.counter, fin);
+  for (Slab& s : ctx->slabs) {
+    double* pnew = parity ? s.p0 : s.p1;
+    LAUNCH(ctx, k_update, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pnew, s.q,
+           s.invd, s.partials, s.counter, fin);
+  }
   if (!fin) {
     CK(allreduce(ctx, 0, 2, 0));
     for (Slab& s : ctx->slabs) { k_finish_update<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+    CK(exchange_nodes(ctx, &Slab::r));
   }
   return check_launch(ctx);
 }
@@ -498,7 +630,7 @@ int build_cg_graph(topo_ctx* ctx) {
   const long long l0 = ctx->launches;
   CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   int rc = TOPO_OK;
-  for (int i = 0; i < ctx->cg_batch && rc == TOPO_OK; ++i) rc = enqueue_cg_iter(ctx, ctx->profile && i == 0);
+  for (int i = 0; i < ctx->cg_batch && rc == TOPO_OK; ++i) rc = enqueue_cg_iter(ctx, ctx->profile && i == 0, i & 1);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != TOPO_OK) return rc;
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -522,7 +654,7 @@ int build_cg_graph(topo_ctx* ctx) {
 int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
-  CK(exchange_nodes(ctx, &Slab::invd));   // (ghost invd unused by v1 kernels; kept consistent)
+  CK(exchange_nodes(ctx, &Slab::invd, 1));   // ghost planes feed the fused p-update
   const topo_params& P = ctx->prm;
   const long long n_dof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
   const long long maxit = P.cg_max_iter > 0 ? P.cg_max_iter : 10 * n_dof;
@@ -536,7 +668,7 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   CK(residual(ctx, true));
   for (Slab& s : ctx->slabs) { k_cg_start<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
   CK(check_launch(ctx));
-  CK(build_cg_graph(ctx));
+  if (!ctx->debug) CK(build_cg_graph(ctx));
   int replacements = 0, rc = TOPO_OK;
   double rr_true = 0.0;
   DevState& h = *ctx->hstate;
@@ -544,8 +676,12 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   long long it_prev = h.it;
   while (true) {
     if (!h.done) {
-      CU(cudaGraphLaunch(ctx->cg_exec, ctx->stream));
-      ctx->launches += ctx->cg_batch_launches;
+      if (ctx->debug) {
+        for (int i = 0; i < ctx->cg_batch; ++i) CK(enqueue_cg_iter(ctx, false, i & 1));
+      } else {
+        CU(cudaGraphLaunch(ctx->cg_exec, ctx->stream));
+        ctx->launches += ctx->cg_batch_launches;
+      }
       CK(sync_state(ctx));
       if (ctx->profile && h.it > it_prev) {
         float ms = 0.f;
@@ -657,22 +793,26 @@ int do_filter_x(topo_ctx* ctx) {
   return TOPO_OK;
 }
 
-int build_oc_graph(topo_ctx* ctx) {
-  if (ctx->oc_exec) return TOPO_OK;
+int enqueue_oc_batch(topo_ctx* ctx) {
   const int W = ctx->world, fin = (W == 1) ? 1 : 0;
-  cudaGraph_t graph;
-  const long long l0 = ctx->launches;
-  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  int rc = TOPO_OK;
-  for (int i = 0; i < ctx->oc_batch && rc == TOPO_OK; ++i) {
+  for (int i = 0; i < ctx->oc_batch; ++i) {
     for (Slab& s : ctx->slabs)
       LAUNCH(ctx, k_oc_pass, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, ctx->prm.move,
              ctx->prm.filter_mode, s.x, s.dcf, s.dvf, s.passive, s.partials, s.counter, fin);
     if (!fin) {
-      rc = allreduce(ctx, 0, 1, 0);
+      CK(allreduce(ctx, 0, 1, 0));
       for (Slab& s : ctx->slabs) { k_oc_finish<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
     }
   }
+  return check_launch(ctx);
+}
+
+int build_oc_graph(topo_ctx* ctx) {
+  if (ctx->oc_exec) return TOPO_OK;
+  cudaGraph_t graph;
+  const long long l0 = ctx->launches;
+  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_oc_batch(ctx);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != TOPO_OK) return rc;
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "OC graph capture: %s", cudaGetErrorString(e));
@@ -694,13 +834,17 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
     ctx->launches++;
   }
   CK(check_launch(ctx));
-  CK(build_oc_graph(ctx));
+  if (!ctx->debug) CK(build_oc_graph(ctx));
   DevState& h = *ctx->hstate;
   CK(sync_state(ctx));
   int guard = 0;
   while (h.oc_active) {
-    CU(cudaGraphLaunch(ctx->oc_exec, ctx->stream));
-    ctx->launches += ctx->oc_batch_launches;
+    if (ctx->debug) {
+      CK(enqueue_oc_batch(ctx));
+    } else {
+      CU(cudaGraphLaunch(ctx->oc_exec, ctx->stream));
+      ctx->launches += ctx->oc_batch_launches;
+    }
     CK(sync_state(ctx));
     if (++guard > 4096 / ctx->oc_batch) return set_err(ctx, TOPO_EBISECT, "OC bisection did not terminate");
   }
@@ -747,13 +891,16 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
     return TOPO_OK;
   };
   const size_t nb = sizeof(double) * 3 * g.ncomp, eb = sizeof(double) * g.nelloc;
-  double** nv[] = {&s.u, &s.r, &s.p, &s.q, &s.f, &s.invd, &s.w};
+  double** nv[] = {&s.u, &s.r, &s.p0, &s.p1, &s.q, &s.f, &s.w};
   for (double** v : nv) CK(al((void**)v, nb));
+  CK(al((void**)&s.invd, sizeof(double) * g.ncomp));
   CK(al((void**)&s.fixm, g.ncomp));
   double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew};
   for (double** v : ev) CK(al((void**)v, eb));
   CK(al((void**)&s.passive, g.nelloc));
-  CK(al((void**)&s.partials, sizeof(double) * 8 * kMaxGridBlocks));
+  const MvGrid mg = mv_grid(ctx, g);
+  const size_t nbmax = std::max<size_t>(kMaxGridBlocks, (size_t)mg.grid.x * mg.grid.y * mg.grid.z);
+  CK(al((void**)&s.partials, sizeof(double) * 8 * nbmax));
   CK(al((void**)&s.counter, sizeof(unsigned int) * 4));
   CK(al((void**)&s.st, sizeof(DevState)));
   s.stage_n = std::max((size_t)3 * (g.nown) * (g.nely + 1) * (g.nelz + 1), (size_t)g.nex * g.nely * g.nelz);
@@ -766,7 +913,7 @@ void free_ctx(topo_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
-    void* ptrs[] = {s.u, s.r, s.p, s.q, s.f, s.invd, s.w, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
+    void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -914,6 +1061,12 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   build_element_stiffness(p->nu, ctx->ke);
   ctx->kd = ctx->ke[0];
   {
+    double w[8];
+    if (!wht_constants(ctx->ke, w, 1e-13) && rc == TOPO_OK)
+      rc = set_err(ctx, TOPO_EINVAL, "KE lacks the Walsh-Hadamard block structure");
+    ctx->wht = WhtK{w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]};
+  }
+  {
     const int B = (int)std::ceil(p->rmin);
     int R = 0;
     for (int dz = -B; dz <= B; ++dz)
@@ -929,6 +1082,8 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
     if ((int)ctx->st_off.size() > kMaxStencil) rc = set_err(ctx, TOPO_EINVAL, "filter stencil too large");
   }
   const int H = std::max(1, ctx->R);
+  if (const char* e = getenv("TOPO_TZ")) ctx->tz = atoi(e) == 16 ? 16 : 8;   // matvec CTA shape (tuning)
+  if (const char* e = getenv("TOPO_DEBUG_SYNC")) ctx->debug = atoi(e) != 0;
   // slab partition: owned elements [ex0, ex1)
   const int W = ctx->world;
   for (int s = 0; s < W && rc == TOPO_OK; ++s) {
@@ -980,6 +1135,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   }
   for (Slab& s : ctx->slabs) {
     rc = alloc_slab(ctx, s);
+    if (rc == TOPO_OK) rc = build_maps(ctx, s);
     if (rc != TOPO_OK) { int r2 = rc; free_ctx(ctx); return r2 == TOPO_ECUDA ? TOPO_ENOMEM : r2; }
   }
   // --- inputs ---
@@ -1039,7 +1195,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
     const long long ndof = 3 * nn;
     int b = p->cg_check_every;
     if (b <= 0) b = (int)std::min<long long>(64, std::max<long long>(8, 20000000LL / std::max<long long>(ndof, 1)));
-    ctx->cg_batch = b;
+    ctx->cg_batch = (b + 1) / 2 * 2;   // even: the p ping-pong returns to p0 after a batch
   }
   *out = ctx;
   return TOPO_OK;
@@ -1235,7 +1391,7 @@ int topo_matvec_run(topo_ctx* ctx, int32_t reps) {
   cudaSetDevice(ctx->device);
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
-  for (int i = 0; i < reps; ++i) CK(matvec_all(ctx, &Slab::w, &Slab::q));
+  for (int i = 0; i < reps; ++i) CK(matvec_all(ctx, &Slab::w, &Slab::m_w, &Slab::q));
   return TOPO_OK;
 }
 
@@ -1253,7 +1409,7 @@ int topo_get(topo_ctx* ctx, int32_t field, double* out) {
     case TOPO_FIELD_DVF: return download_elems(ctx, &Slab::dvf, out);
     case TOPO_FIELD_XNEW: return download_elems(ctx, &Slab::xnew, out);
     case TOPO_FIELD_HS: return download_elems(ctx, &Slab::hs, out);
-    case TOPO_FIELD_INVDIAG: return download_nodes(ctx, &Slab::invd, out);
+    case TOPO_FIELD_INVDIAG: return download_invd(ctx, out);
     case TOPO_FIELD_R: return download_nodes(ctx, &Slab::r, out);
     default: return set_err(ctx, TOPO_EINVAL, "unknown field %d", field);
   }

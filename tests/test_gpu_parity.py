@@ -46,6 +46,8 @@ SMALL = [
     ((37, 13, 5), 2.5, (18.0, 6.0, 3.0)),  # ragged, obstacle, R = 2
     ((23, 9, 7), 3.0, None),             # R = 2, 93-point stencil, odd sizes
     ((9, 3, 2), 4.0, None),              # R = 3 wider than parts of the grid
+    ((10, 45, 9), 1.5, None),            # 2 x 2 y-z matvec tiles (odd tile origins), ragged
+    ((7, 66, 15), 2.5, (3.0, 30.0, 5.0)),  # 3 x 3 tiles, obstacle
 ]
 
 

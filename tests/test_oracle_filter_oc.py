@@ -155,3 +155,15 @@ def test_oc_move_clamp_and_passive_and_volume():
         tr = sorted(trace)
         assert all(tr[i][1] >= tr[i + 1][1] - 1e-12 for i in range(len(tr) - 1))
         assert npass == len(trace) and npass > 30
+
+
+def test_filter_rows_equal_matrix():
+    dims, rmin = (7, 6, 5), 2.5
+    H, Hs = filter_matrix(*dims, rmin)
+    from oracle import filter_rows
+    rows = [0, 17, 100, 209]
+    rr, hs = filter_rows(*dims, rmin, rows)
+    for (cols, w), i in zip(rr, rows):
+        row = H.getrow(i)
+        assert dict(zip(cols.tolist(), w.tolist())) == pytest.approx(dict(zip(row.indices.tolist(), row.data.tolist())))
+    assert np.allclose(hs, Hs[rows], rtol=1e-15)
