@@ -148,6 +148,14 @@ int topo_init(const topo_params *p, const double *load, const uint8_t *fixed,
  * on.  NULL/0 -> the context's own non-blocking stream.                    */
 int topo_set_stream(topo_ctx *ctx, void *stream);
 
+/* x-slab partition without a context (host only, no GPU): rank `rank` of
+ * `world` owns elements [ex_begin, ex_end) = [rank*nelx/world,
+ * (rank+1)*nelx/world) (integer division) and node planes [ex_begin, ex_end)
+ * plus ix = nelx on the last rank.  EINVAL if a slab would be thinner than
+ * max(1, R), R = filter radius ceil(rmin)-1 (halo from one neighbour only). */
+int topo_partition(int32_t nelx, double rmin, int32_t world, int32_t rank, int32_t *ex_begin,
+                   int32_t *ex_end);
+
 /* Owned element range along x of this rank: [ex_begin, ex_end).           */
 int topo_owned_range(const topo_ctx *ctx, int32_t *ex_begin, int32_t *ex_end);
 

@@ -53,7 +53,8 @@ struct DevState {
   int done;         // 1 -> PCG kernels are no-ops
   int status;       // 0 ok, 2 ENOCONV, 3 EBREAKDOWN
   int fresh;        // 1 -> next p-update uses beta = 0 (start / restart)
-  int pad0;
+  int pending;      // 1 -> u lacks alpha_prev * p (applied by the next odd update or a flush)
+  double alpha_prev;
   // OC bisection
   double l1, l2, lmid, target, vol, oc_tol;
   int oc_active, oc_pass;

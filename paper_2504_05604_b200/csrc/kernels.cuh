@@ -72,7 +72,13 @@ __global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
 // A3/A4  PCG vector kernels over the owned node planes (pads are zero and
 // stay zero).  SoA: component stride ncomp.
 // ===========================================================================
-__device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, double rr) {
+__device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, double rr, int even) {
+  if (even) {                 // u update deferred: the next (odd) update applies both steps
+    st->alpha_prev = st->alpha;
+    st->pending = 1;
+  } else {
+    st->pending = 0;
+  }
   st->beta = rz_new / st->rz;
   st->rz = rz_new;
   st->rr = rr;
@@ -89,33 +95,43 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
   }
 }
 
-// u += alpha p ; r -= alpha q ; partial (r M^{-1} r, r r).  double2 over
-// pairs of nodes of the owned planes (pads are zero and stay zero).
+// PCG vector update, u updated every other iteration:
+//   even slot (kU = false): r -= alpha q                            (u pending)
+//   odd slot  (kU = true) : u += alpha_prev p_prev + alpha p ; r -= alpha q
+// r is 0 on fixed DOFs (q comes unmasked from the matvec); partial
+// (r M^{-1} r, r r).  double2 over pairs of nodes of the owned planes (pads
+// are zero and stay zero).  Saves one read+write of u every second iteration.
+template <bool kU>
 __global__ void __launch_bounds__(kBlock)
 k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
-         const double* __restrict__ p, const double* __restrict__ q,
-         const double* __restrict__ invd, double* partials, unsigned int* counter, int finish) {
+         const double* __restrict__ pprev, const double* __restrict__ p, const double* __restrict__ q,
+         const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* partials,
+         unsigned int* counter, int finish) {
   if (st->done) return;
-  const double alpha = st->alpha;
+  const double alpha = st->alpha, alpha_prev = kU ? st->alpha_prev : 0.0;
   const long long b0 = g.nplane, npair = (long long)g.nown * g.nplane / 2;
   double rz = 0.0, rr = 0.0;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < npair;
        j += (long long)gridDim.x * blockDim.x) {
     const long long i = b0 + 2 * j;
     const double2 iv = *reinterpret_cast<const double2*>(invd + i);
+    const uchar2 fm = *reinterpret_cast<const uchar2*>(fixm + i);
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long k = i + c * g.ncomp;
-      double2 uu = *reinterpret_cast<const double2*>(u + k);
-      const double2 pp = *reinterpret_cast<const double2*>(p + k);
+      if (kU) {
+        double2 uu = *reinterpret_cast<const double2*>(u + k);
+        const double2 p0 = *reinterpret_cast<const double2*>(pprev + k);
+        const double2 pp = *reinterpret_cast<const double2*>(p + k);
+        uu.x = fma(alpha, pp.x, fma(alpha_prev, p0.x, uu.x));
+        uu.y = fma(alpha, pp.y, fma(alpha_prev, p0.y, uu.y));
+        *reinterpret_cast<double2*>(u + k) = uu;
+      }
       double2 rv = *reinterpret_cast<const double2*>(r + k);
       const double2 qq = *reinterpret_cast<const double2*>(q + k);
-      uu.x = fma(alpha, pp.x, uu.x);
-      uu.y = fma(alpha, pp.y, uu.y);
-      rv.x = fma(-alpha, qq.x, rv.x);
-      rv.y = fma(-alpha, qq.y, rv.y);
-      *reinterpret_cast<double2*>(u + k) = uu;
+      rv.x = (fm.x >> c) & 1 ? 0.0 : fma(-alpha, qq.x, rv.x);
+      rv.y = (fm.y >> c) & 1 ? 0.0 : fma(-alpha, qq.y, rv.y);
       *reinterpret_cast<double2*>(r + k) = rv;
       s0 = fma(rv.x, rv.x, s0);
       s1 = fma(rv.y, rv.y, s1);
@@ -126,10 +142,21 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
   __shared__ double tot[2];
   double v[2] = {rz, rr};
   if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
-    if (finish) cg_finish_update(st, tot[0], tot[1]);
+    if (finish) cg_finish_update(st, tot[0], tot[1], kU ? 0 : 1);
     else { st->sums[0] = tot[0]; st->sums[1] = tot[1]; }
   }
 }
+
+// u += alpha_prev p (the deferred half-step) when the solve stops after an even slot
+__global__ void k_flush_u(Geo g, double alpha_prev, double* __restrict__ u, const double* __restrict__ p) {
+  const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long c = k / n, i = b0 + (k - c * n) + c * g.ncomp;
+    u[i] = fma(alpha_prev, p[i], u[i]);
+  }
+}
+__global__ void k_clear_pending(DevState* st) { st->pending = 0; }
 
 // Multi-slab finish kernels (after the allreduce of st->sums).
 __global__ void k_finish_alpha(DevState* st) {
@@ -139,26 +166,27 @@ __global__ void k_finish_alpha(DevState* st) {
   if (!(pq > 0.0) || !isfinite(pq)) { st->status = 3; st->done = 1; }
   else st->alpha = st->rz / pq;
 }
-__global__ void k_finish_update(DevState* st) {
+__global__ void k_finish_update(DevState* st, int even) {
   if (st->done) return;
-  cg_finish_update(st, st->sums[0], st->sums[1]);
+  cg_finish_update(st, st->sums[0], st->sums[1], even);
 }
 
-// r = f - q (masked by construction: q and f are 0 on fixed DOFs); partial
+// r = f - q, 0 on fixed DOFs (q arrives unmasked from the matvec); partial
 // (r M^{-1} r, r r).  Used at PCG start and for the true-residual check.
 __global__ void __launch_bounds__(kBlock)
 k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __restrict__ q,
-           const double* __restrict__ invd, double* __restrict__ r, int write_r,
-           double* partials, unsigned int* counter) {
+           const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* __restrict__ r,
+           int write_r, double* partials, unsigned int* counter) {
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   double rz = 0.0, rr = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x) {
     const long long i = b0 + k;
+    const uint8_t fm = fixm[i];
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double rv = f[i + c * g.ncomp] - q[i + c * g.ncomp];
+      const double rv = (fm >> c) & 1 ? 0.0 : f[i + c * g.ncomp] - q[i + c * g.ncomp];
       if (write_r) r[i + c * g.ncomp] = rv;
       s = fma(rv, rv, s);
     }
@@ -460,6 +488,8 @@ namespace topo {
 // small state / utility kernels
 // ---------------------------------------------------------------------------
 __global__ void k_cg_init(DevState* st, double tol2, double bb, long long max_it) {
+  st->pending = 0;
+  st->alpha_prev = 0.0;
   st->tol2 = tol2;
   st->bb = bb;
   st->max_it = max_it;

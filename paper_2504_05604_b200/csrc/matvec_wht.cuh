@@ -44,41 +44,40 @@ __device__ __forceinline__ void wht4(const double v[4], double G[4]) {
   G[3] = d0 - d1;
 }
 
-// Q = E * B * P  (P, Q indexed [c][m], m = mx + 2 my + 4 mz)
+// Q = E * B * P  (P, Q indexed [c][m], m = mx + 2 my + 4 mz).  E is folded
+// into the 8 block constants (8 DMUL) instead of scaling the 21 outputs.
 __device__ __forceinline__ void wht_block(const double P[3][8], double Ee, double Q[3][8]) {
   const WhtK& K = c_wht;
+  const double k0 = Ee * K.k0, o0 = Ee * K.o0, k7 = Ee * K.k7, o7 = Ee * K.o7;
+  const double a = Ee * K.a, b = Ee * K.b, r = Ee * K.r, s = Ee * K.s;
   double t;
-  t = K.o0 * (P[0][1] + P[1][2] + P[2][4]);
-  Q[0][1] = fma(K.k0, P[0][1], t);
-  Q[1][2] = fma(K.k0, P[1][2], t);
-  Q[2][4] = fma(K.k0, P[2][4], t);
-  t = K.o7 * (P[0][6] + P[1][5] + P[2][3]);
-  Q[0][6] = fma(K.k7, P[0][6], t);
-  Q[1][5] = fma(K.k7, P[1][5], t);
-  Q[2][3] = fma(K.k7, P[2][3], t);
+  t = o0 * (P[0][1] + P[1][2] + P[2][4]);
+  Q[0][1] = fma(k0, P[0][1], t);
+  Q[1][2] = fma(k0, P[1][2], t);
+  Q[2][4] = fma(k0, P[2][4], t);
+  t = o7 * (P[0][6] + P[1][5] + P[2][3]);
+  Q[0][6] = fma(k7, P[0][6], t);
+  Q[1][5] = fma(k7, P[1][5], t);
+  Q[2][3] = fma(k7, P[2][3], t);
   Q[0][0] = Q[1][0] = Q[2][0] = 0.0;   // rigid translations carry no energy
-  Q[1][3] = fma(K.a, P[1][3], K.b * P[2][5]);
-  Q[2][5] = fma(K.b, P[1][3], K.a * P[2][5]);
-  Q[0][3] = fma(K.a, P[0][3], K.b * P[2][6]);
-  Q[2][6] = fma(K.b, P[0][3], K.a * P[2][6]);
-  Q[0][5] = fma(K.a, P[0][5], K.b * P[1][6]);
-  Q[1][6] = fma(K.b, P[0][5], K.a * P[1][6]);
-  t = K.r * (P[0][2] + P[1][1]);
+  Q[1][3] = fma(a, P[1][3], b * P[2][5]);
+  Q[2][5] = fma(b, P[1][3], a * P[2][5]);
+  Q[0][3] = fma(a, P[0][3], b * P[2][6]);
+  Q[2][6] = fma(b, P[0][3], a * P[2][6]);
+  Q[0][5] = fma(a, P[0][5], b * P[1][6]);
+  Q[1][6] = fma(b, P[0][5], a * P[1][6]);
+  t = r * (P[0][2] + P[1][1]);
   Q[0][2] = t;
   Q[1][1] = t;
-  Q[2][7] = K.s * P[2][7];
-  t = K.r * (P[0][4] + P[2][1]);
+  Q[2][7] = s * P[2][7];
+  t = r * (P[0][4] + P[2][1]);
   Q[0][4] = t;
   Q[2][1] = t;
-  Q[1][7] = K.s * P[1][7];
-  t = K.r * (P[1][4] + P[2][2]);
+  Q[1][7] = s * P[1][7];
+  t = r * (P[1][4] + P[2][2]);
   Q[1][4] = t;
   Q[2][2] = t;
-  Q[0][7] = K.s * P[0][7];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int m = 1; m < 8; ++m) Q[c][m] *= Ee;
+  Q[0][7] = s * P[0][7];
 }
 
 // Tensor maps of one matvec launch (TMA descriptors, kernel-parameter space).
@@ -89,7 +88,7 @@ struct MvMaps {
   CUtensorMap E;      // 3D {EY, EZ, NEXL}
 };
 
-constexpr int kMvStages = 4;
+constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
 template <int TZ> struct MvSmem {
   static constexpr int YW = 34;                                   // 33 nodes, box width padded to 16 B
   static constexpr int V = 3 * (TZ + 1) * YW * 8;                 // bytes of one 3-component node tile
@@ -97,19 +96,20 @@ template <int TZ> struct MvSmem {
   static constexpr int EB = TZ * YW * 8;                          // element tile (box width 34 as well)
   static constexpr int VA = (V + 127) / 128 * 128, IA = (I + 127) / 128 * 128, EA = (EB + 127) / 128 * 128;
   __host__ __device__ static constexpr int stage(bool fused) { return fused ? 2 * VA + IA + EA : VA + EA; }
-  __host__ __device__ static constexpr int bytes(bool fused) { return kMvStages * stage(fused) + 128; }
+  // raw stages + 3 rotating p-planes (pre-pass output) + alignment slack
+  __host__ __device__ static constexpr int bytes(bool fused) { return kMvStages * stage(fused) + 3 * VA + 128; }
 };
 
 template <int TZ, bool kFused, bool kDot>
 __global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? 2 : 1))
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
-         const uint8_t* __restrict__ fixm, double* __restrict__ pnew, double* __restrict__ q,
+         double* __restrict__ pnew, double* __restrict__ q,
          double* partials, unsigned int* counter, int finish) {
   if (gate && st->done) return;
   using L = MvSmem<TZ>;
   const double beta = (kFused && !st->fresh) ? st->beta : 0.0;
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ double xch[2][TZ][32][3];
+  __shared__ double xch[2][3][TZ][32];   // lanes contiguous: conflict-free
   __shared__ __align__(8) uint64_t full[kMvStages];
 
   const int ty = threadIdx.x, tz = threadIdx.y;
@@ -124,11 +124,17 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   const int xe = min(xs + CX, xend_slab);
   const bool first_chunk = chunk == 0, last_chunk = (xe == xend_slab);
   const bool owned = ty >= 1 && tz >= 1 && iyb <= g.nely && izb <= g.nelz;
-  const long long ob = (long long)(izb + 1) * g.NY + (iyb + 1);
-  const long long ncomp = g.ncomp, nplane = g.nplane;
+  // 32-bit in-array offsets (init validates 3*ncomp < 2^31)
+  const int ob = (izb + 1) * g.NY + (iyb + 1);
+  const int ncomp = (int)g.ncomp, nplane = (int)g.nplane;
   const int nunits = xe - xs + 2;           // node planes xs-1 .. xe
+  // running output pointers at the base node (advanced by nplane per step)
+  double* qp = q + (size_t)(xs - g.ex0 + 1) * nplane + ob;
 
   auto slot = [&](int s) { return dsm + s * L::stage(kFused); };
+  double* pbuf = reinterpret_cast<double*>(dsm + kMvStages * L::stage(kFused));   // [3][3][TZ+1][YW]
+  constexpr int PB = L::VA / 8;                                                      // doubles per p-plane
+  constexpr int CS = (TZ + 1) * L::YW;                                               // component stride
   auto issue = [&](int t) {                 // unit t: node plane j = xs-1+t, element plane j-1
     const int s = t % kMvStages;
     unsigned char* b = slot(s);
@@ -154,113 +160,149 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   if (leader)
     for (int t = 0; t < min(kMvStages, nunits); ++t) issue(t);
 
-  // corners (k = ay + 2 az) of this thread's element column from unit t; returns E_e
-  auto consume = [&](int t, double v[3][4], double pb[3]) -> double {
+  // Pre-pass of unit t: p = M^{-1} r + beta p_old once per node of the (TZ+1) x 34
+  // tile plane into p-plane t%3 (plain variant: copy), owner nodes write p to
+  // global; returns this thread's E_e for element plane j-1.  The raw stage is
+  // fully consumed here.
+  // Pre-pass node mapping (fixed per thread): nodes tid and tid + 32*TZ of the tile plane
+  const int tid = tz * 32 + ty;
+  constexpr int NPN = (CS + 32 * TZ - 1) / (32 * TZ);       // nodes per thread (2 for TZ = 8)
+  int pn_idx[NPN];
+  long long pn_off[NPN];                                      // global offset in a plane, -1 if not owned
+#pragma unroll
+  for (int u = 0; u < NPN; ++u) {
+    const int n = tid + u * 32 * TZ;
+    pn_idx[u] = n < CS ? n : -1;
+    pn_off[u] = -1;
+    if (n < CS) {
+      const int row = n / L::YW, col = n - row * L::YW;
+      const int cty = col - yoff, iy = yb + col - 1, iz = z0 + row - 1;
+      if (cty >= 1 && cty <= 31 && row >= 1 && row <= TZ - 1 && iy <= g.nely && iz <= g.nelz)
+        pn_off[u] = (long long)(z0 + row) * g.NY + (yb + col);
+    }
+  }
+  // Pre-pass of unit t: p = M^{-1} r + beta p_old once per node of the (TZ+1) x 34
+  // tile plane into p-plane t%3 (plain variant: copy), owner nodes write p to
+  // global; returns this thread's E_e for element plane j-1.  The raw stage is
+  // fully consumed here.
+  auto prepass = [&](int t) -> double {
     const int s = t % kMvStages;
     mbar_wait(&full[s], (uint32_t)((t / kMvStages) & 1));
     const double* sv = reinterpret_cast<const double*>(slot(s));
     const double* sp = reinterpret_cast<const double*>(slot(s) + L::VA);
     const double* si = reinterpret_cast<const double*>(slot(s) + 2 * L::VA);
     const double* se = reinterpret_cast<const double*>(slot(s) + (kFused ? 2 * L::VA + L::IA : L::VA));
+    double* pb = pbuf + (t % 3) * PB;
+    const bool wr_plane = kFused && ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
+    double* pplane = pnew + (size_t)(xs + t - g.ex0) * nplane;     // node plane j = xs-1+t
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int o = (tz + (k >> 1)) * L::YW + ty + yoff + (k & 1);
-      const double iv = kFused ? si[o] : 1.0;
+    for (int u = 0; u < NPN; ++u) {
+      const int n = pn_idx[u];
+      if (n < 0) continue;
+      double v[3];
+      if (kFused) {
+        const double iv = si[n];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int oc = c * (TZ + 1) * L::YW + o;
-        v[c][k] = kFused ? fma(beta, sp[oc], iv * sv[oc]) : sv[oc];
+        for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], iv * sv[c * CS + n]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];
       }
-    }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) pb[c] = v[c][0];
-    if (kFused) {
-      const int j = xs - 1 + t;
-      if (owned && ((j >= xs && j < xe) || (j == xs - 1 && first_chunk) || (j == xe && last_chunk))) {
-        const long long i = (long long)(j - g.ex0 + 1) * nplane + ob;
+      for (int c = 0; c < 3; ++c) pb[c * CS + n] = v[c];
+      if (wr_plane && pn_off[u] >= 0) {
+        double* o = pplane + pn_off[u];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) pnew[i + c * ncomp] = v[c][0];
+        for (int c = 0; c < 3; ++c) o[(size_t)c * ncomp] = v[c];
       }
     }
     return t > 0 ? se[tz * L::YW + ty + yoff] : 0.0;
   };
-  auto release = [&](int t) {               // all threads have read unit t (caller synced)
+  // corners (k = ay + 2 az) of this thread's element column in p-plane t%3
+  auto corners_wht = [&](int t, double G[3][4]) {
+    const double* pb = pbuf + (t % 3) * PB;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = pb[c * CS + (tz + (k >> 1)) * L::YW + ty + yoff + (k & 1)];
+      wht4(v, G[c]);
+    }
+  };
+  auto release = [&](int t) {               // all threads are past the pre-pass of unit t
     if (leader && t + kMvStages < nunits) {
       fence_proxy_async();
       issue(t + kMvStages);
     }
   };
 
-  double G0[3][4], A[3][4], pb_prev[3];
-  {
-    double v[3][4];
-    consume(0, v, pb_prev);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) wht4(v[c], G0[c]);
-    __syncthreads();
-    release(0);
-  }
+  double G0[3][4], A[3][4];
+  double Ecur = 0.0;
+  prepass(0);
+  if (nunits > 1) Ecur = prepass(1);
+  __syncthreads();
+  release(0);
+  if (nunits > 1) release(1);
+  corners_wht(0, G0);
   double dot = 0.0;
-  int buf = 0;
   for (int t = 1; t < nunits; ++t) {
     const int ex = xs - 2 + t;              // element plane of this step (node planes ex, ex+1)
-    double v[3][4], pb[3], G1[3][4];
-    const double Ee = consume(t, v, pb);
+    (void)ex;
+    double G1[3][4];
+    corners_wht(t, G1);
+    const double Ee = Ecur;
+    if (t + 1 < nunits) Ecur = prepass(t + 1);
+    double Q[3][8];
+    {
+      double P[3][8];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) wht4(v[c], G1[c]);
-    double P[3][8], Q[3][8];
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        P[c][2 * k] = G0[c][k] + G1[c][k];
-        P[c][2 * k + 1] = G0[c][k] - G1[c][k];
-      }
-    wht_block(P, Ee, Q);
-    if (ex >= xs) {
-      // complete node plane ex: A (from element ex-1) + R0 (element ex)
-      double C[3][4];
+        for (int k = 0; k < 4; ++k) {
+          P[c][2 * k] = G0[c][k] + G1[c][k];
+          P[c][2 * k + 1] = G0[c][k] - G1[c][k];
+        }
+      wht_block(P, Ee, Q);
+    }
+    if (t >= 2) {                           // ex >= xs: complete node plane ex
+      const int buf = t & 1;
+      double S[3], pbase[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double Ac[4];
+        double Ac[4], C[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) Ac[k] = A[c][k] + (Q[c][2 * k] + Q[c][2 * k + 1]);
-        wht4(Ac, C[c]);
-      }
-      // y-z neighbourhood: owner(ty,tz) = C0(ty,tz) + C1(ty-1,tz) + C2(ty,tz-1) + C3(ty-1,tz-1)
-      double S[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const double T = C[c][2] + __shfl_up_sync(0xffffffffu, C[c][3], 1);
-        S[c] = C[c][0] + __shfl_up_sync(0xffffffffu, C[c][1], 1);
-        xch[buf][tz][ty][c] = T;
+        wht4(Ac, C);
+        // y-z neighbourhood: owner(ty,tz) = C0(ty,tz) + C1(ty-1,tz) + C2(ty,tz-1) + C3(ty-1,tz-1)
+        xch[buf][c][tz][ty] = C[2] + __shfl_up_sync(0xffffffffu, C[3], 1);
+        S[c] = C[0] + __shfl_up_sync(0xffffffffu, C[1], 1);
+        // p at the owner's node of plane ex (p-plane (t-1)%3 is rewritten only after this barrier)
+        pbase[c] = kDot ? pbuf[((t - 1) % 3) * PB + c * CS + tz * L::YW + ty + yoff] : 0.0;
       }
       __syncthreads();
-      release(t);
       if (owned) {
-        const long long i = (long long)(ex - g.ex0 + 1) * nplane + ob;
-        const uint8_t fm = fixm[i];
+        // q is NOT masked here: the fixed-DOF mask is applied by the consumers
+        // (k_update, k_residual, k_mask_fixed); p is exactly 0 on fixed DOFs, so
+        // p.q is unaffected.  Keeps a latency-bound byte load off this loop.
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double qv = (fm >> c) & 1 ? 0.0 : S[c] + xch[buf][tz - 1][ty][c];
-          q[i + c * ncomp] = qv;
-          if (kDot) dot = fma(pb_prev[c], qv, dot);
+          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          qp[c * ncomp] = qv;
+          if (kDot) dot = fma(pbase[c], qv, dot);
         }
       }
-      buf ^= 1;
+      qp += nplane;
     } else {
       __syncthreads();
-      release(t);
     }
+    if (t + 1 < nunits) release(t + 1);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         A[c][k] = Q[c][2 * k] - Q[c][2 * k + 1];   // R1: element ex -> node plane ex+1
         G0[c][k] = G1[c][k];
       }
-      pb_prev[c] = pb[c];
-    }
   }
 
   if (kDot) {

@@ -558,7 +558,7 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
-  k_mv_wht<TZ, kFused, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, s.fixm, pnew, q,
+  k_mv_wht<TZ, kFused, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
                                                                      s.partials, s.counter, finish);
   ctx->launches++;
   debug_sync(ctx, kFused ? "k_mv_wht<fused>" : "k_mv_wht<plain>");
@@ -588,8 +588,8 @@ int matvec_all(topo_ctx* ctx, double* Slab::*pin, CUtensorMap Slab::*pmap, doubl
 int residual(topo_ctx* ctx, bool write_r) {
   CK(matvec_all(ctx, &Slab::u, &Slab::m_u, &Slab::q));
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_residual, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.r,
-           write_r ? 1 : 0, s.partials, s.counter);
+    LAUNCH(ctx, k_residual, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.fixm,
+           s.r, write_r ? 1 : 0, s.partials, s.counter);
   CK(check_launch(ctx));
   if (write_r) CK(exchange_nodes(ctx, &Slab::r));
   return allreduce(ctx, 0, 2, 0);
@@ -612,15 +612,33 @@ int enqueue_cg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   }
   for (Slab& s : ctx->slabs) {
     double* pnew = parity ? s.p0 : s.p1;
-    LAUNCH(ctx, k_update, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pnew, s.q,
-           s.invd, s.partials, s.counter, fin);
+    double* pprev = parity ? s.p1 : s.p0;
+    if (parity)
+      LAUNCH(ctx, k_update<true>, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev, pnew,
+             s.q, s.invd, s.fixm, s.partials, s.counter, fin);
+    else
+      LAUNCH(ctx, k_update<false>, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev, pnew,
+             s.q, s.invd, s.fixm, s.partials, s.counter, fin);
   }
   if (!fin) {
     CK(allreduce(ctx, 0, 2, 0));
-    for (Slab& s : ctx->slabs) { k_finish_update<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
+    for (Slab& s : ctx->slabs) { k_finish_update<<<1, 1, 0, ctx->stream>>>(s.st, parity ? 0 : 1); ctx->launches++; }
     CK(exchange_nodes(ctx, &Slab::r));
   }
   return check_launch(ctx);
+}
+
+// apply the deferred u half-step (even-slot exit); p of an even slot lives in p1
+int flush_u(topo_ctx* ctx) {
+  DevState& h = *ctx->hstate;
+  if (!h.pending) return TOPO_OK;
+  for (Slab& s : ctx->slabs) {
+    LAUNCH(ctx, k_flush_u, grid_for(3LL * s.g.nown * s.g.nplane), s.g, h.alpha_prev, s.u, s.p1);
+    k_clear_pending<<<1, 1, 0, ctx->stream>>>(s.st);
+    ctx->launches++;
+  }
+  CK(check_launch(ctx));
+  return sync_state(ctx);
 }
 
 int build_cg_graph(topo_ctx* ctx) {
@@ -693,6 +711,7 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
       it_prev = h.it;
       continue;
     }
+    CK(flush_u(ctx));
     if (h.status == 2) { rc = set_err(ctx, TOPO_ENOCONV, "PCG: no convergence in %lld iterations", h.it); break; }
     if (h.status == 3) { rc = set_err(ctx, TOPO_EBREAKDOWN, "PCG breakdown at iteration %lld", h.it); break; }
     CK(residual(ctx, false));
@@ -935,8 +954,8 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (!p) return set_err(ctx, TOPO_EINVAL, "params is NULL");
   if (p->nelx < 1 || p->nely < 1 || p->nelz < 1)
     return set_err(ctx, TOPO_EINVAL, "grid dimensions must be >= 1 (got %d x %d x %d)", p->nelx, p->nely, p->nelz);
-  if ((double)(p->nelx + 1) * (p->nely + 1) * (p->nelz + 1) * 3 > 2.0e9)
-    return set_err(ctx, TOPO_EINVAL, "grid too large for one context");
+  if ((double)(p->nelx + 4) * (p->nely + 7) * (p->nelz + 3) * 3 > 2.0e9)
+    return set_err(ctx, TOPO_EINVAL, "grid too large for one context (32-bit in-slab offsets)");
   if (!(p->volfrac > 0 && p->volfrac < 1)) return set_err(ctx, TOPO_EINVAL, "volfrac must be in (0,1)");
   if (!(p->penal >= 1)) return set_err(ctx, TOPO_EINVAL, "penal must be >= 1");
   if (!(p->rmin > 0 && p->rmin <= 6)) return set_err(ctx, TOPO_EINVAL, "rmin must be in (0, 6]");
@@ -1201,6 +1220,18 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   return TOPO_OK;
 }
 
+int topo_partition(int32_t nelx, double rmin, int32_t world, int32_t rank, int32_t* ex_begin, int32_t* ex_end) {
+  if (nelx < 1 || world < 1 || rank < 0 || rank >= world || !(rmin > 0)) return TOPO_EINVAL;
+  const int R = std::max(0, (int)std::ceil(rmin) - 1);
+  for (int s = 0; s < world; ++s) {
+    const int a = (int)((long long)s * nelx / world), b = (int)((long long)(s + 1) * nelx / world);
+    if (b - a < std::max(1, world > 1 ? R : 1)) return TOPO_EINVAL;
+  }
+  if (ex_begin) *ex_begin = (int)((long long)rank * nelx / world);
+  if (ex_end) *ex_end = (int)((long long)(rank + 1) * nelx / world);
+  return TOPO_OK;
+}
+
 int topo_set_stream(topo_ctx* ctx, void* stream) {
   if (!ctx) return TOPO_EINVAL;
   cudaStream_t s = stream ? (cudaStream_t)stream : ctx->own_stream;
@@ -1370,6 +1401,9 @@ int topo_apply_K(topo_ctx* ctx, const double* p, double* q) {
   cudaSetDevice(ctx->device);
   CK(topo_matvec_load(ctx, p));
   CK(topo_matvec_run(ctx, 1));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.q);
+  CK(check_launch(ctx));
   if (q) CK(download_nodes(ctx, &Slab::q, q));
   return TOPO_OK;
 }

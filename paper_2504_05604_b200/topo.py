@@ -29,7 +29,7 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            "topo_oc_step", "topo_optimize", "topo_apply_K", "topo_update_modulus",
            "topo_matvec_load", "topo_matvec_run", "topo_get", "topo_get_timings", "topo_profile",
            "topo_kernel_time", "topo_element_stiffness", "topo_count", "topo_last_error",
-           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id"]
+           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition"]
 
 
 class topo_params(C.Structure):
@@ -96,6 +96,7 @@ def _load():
         "topo_version": (C.c_char_p, []),
         "topo_destroy": (None, [ctxp]),
         "topo_nccl_unique_id": (I, [U8]),
+        "topo_partition": (I, [C.c_int32, C.c_double, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -136,6 +137,15 @@ def nccl_unique_id():
     if rc:
         raise TopoError(rc, "topo_nccl_unique_id")
     return bytes(buf)
+
+
+def partition(nelx, rmin, world, rank):
+    """Owned element range [ex0, ex1) of `rank` (host-only, no GPU)."""
+    a, b = C.c_int32(), C.c_int32()
+    rc = _lib.topo_partition(int(nelx), float(rmin), int(world), int(rank), C.byref(a), C.byref(b))
+    if rc:
+        raise TopoError(rc, "topo_partition")
+    return a.value, b.value
 
 
 def make_params(p):
