@@ -189,7 +189,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="default: --steps")
     ap.add_argument("--matvec-reps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-ncg", type=int, default=None)
@@ -197,6 +197,8 @@ def main():
     args = ap.parse_args()
 
     from workloads import make_problem
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     world, rank, local = dist_env()
     p, f, fx, pas = make_problem(args.config)
 
@@ -243,6 +245,7 @@ def main():
         cg_warm.append(pr.timings()["cg_iters"])
 
     # ---- timed SIMP iterations (device-resident inputs) ----
+    pr.snapshot()          # the e2e leg below replays exactly these iterations
     pr.profile(True)
     l0 = pr.timings()["kernel_launches"]
     cg_timed, phase = [], []
@@ -287,6 +290,7 @@ def main():
     # ---- end-to-end through the C ABI with pinned host buffers ----
     e2e = None
     if args.e2e_steps > 0:
+        pr.restore()       # same design and warm start as the first timed step
         x_host = torch.empty(n_el, dtype=torch.float64, pin_memory=True).numpy()
         x_out = torch.empty(n_el, dtype=torch.float64, pin_memory=True).numpy()
         x_host[:] = pr.get("x")
@@ -321,7 +325,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_cg = int(np.mean(cg_timed))
         est, sample, wall = oracle_sample(p, n_cg)
-        cpu = {"value": est, "unit": "s/iteration", "cores": 1, "kind": "oracle",
+        cpu = {"value": est, "unit": "s/iteration", "cores": cores_used(), "kind": "oracle",
                "sample": sample + f" (wall {wall:.1f}s; SciPy sparse kernels single-threaded)"}
         try:
             os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -211,6 +211,14 @@ int topo_update_modulus(topo_ctx *ctx);
 int topo_matvec_load(topo_ctx *ctx, const double *p);
 int topo_matvec_run(topo_ctx *ctx, int32_t reps);
 
+/* Device-side checkpoint of the optimiser state (design x, xPhys and the
+ * displacement u used as PCG warm start): topo_snapshot copies it into
+ * context-owned backup buffers (allocated on first use), topo_restore copies
+ * it back.  Used by bench.py to time the same SIMP iterations twice (device-
+ * resident and end-to-end); also a cheap checkpoint/resume.                  */
+int topo_snapshot(topo_ctx *ctx);
+int topo_restore(topo_ctx *ctx);
+
 /* Read a field (TOPO_FIELD_*) in external numbering.                        */
 int topo_get(topo_ctx *ctx, int32_t field, double *out);
 

@@ -102,7 +102,7 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
 // (r M^{-1} r, r r).  double2 over pairs of nodes of the owned planes (pads
 // are zero and stay zero).  Saves one read+write of u every second iteration.
 template <bool kU>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 2)
 k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
          const double* __restrict__ pprev, const double* __restrict__ p, const double* __restrict__ q,
          const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* partials,
@@ -110,34 +110,57 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
   if (st->done) return;
   const double alpha = st->alpha, alpha_prev = kU ? st->alpha_prev : 0.0;
   const long long b0 = g.nplane, npair = (long long)g.nown * g.nplane / 2;
+  const long long nc = g.ncomp;
   double rz = 0.0, rr = 0.0;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < npair;
-       j += (long long)gridDim.x * blockDim.x) {
-    const long long i = b0 + 2 * j;
-    const double2 iv = *reinterpret_cast<const double2*>(invd + i);
-    const uchar2 fm = *reinterpret_cast<const uchar2*>(fixm + i);
-    double s0 = 0.0, s1 = 0.0;
+  constexpr int UN = kU ? 1 : 2;            // pairs per thread per trip: all loads issued first
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; j0 < npair; j0 += UN * stride) {
+    double2 rv[UN][3], qq[UN][3], uu[UN][3], p0[UN][3], pp[UN][3], iv[UN];
+    uchar2 fm[UN];
+    bool ok[UN];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const long long k = i + c * g.ncomp;
-      if (kU) {
-        double2 uu = *reinterpret_cast<const double2*>(u + k);
-        const double2 p0 = *reinterpret_cast<const double2*>(pprev + k);
-        const double2 pp = *reinterpret_cast<const double2*>(p + k);
-        uu.x = fma(alpha, pp.x, fma(alpha_prev, p0.x, uu.x));
-        uu.y = fma(alpha, pp.y, fma(alpha_prev, p0.y, uu.y));
-        *reinterpret_cast<double2*>(u + k) = uu;
+    for (int w = 0; w < UN; ++w) {
+      const long long j = j0 + w * stride;
+      ok[w] = j < npair;
+      const long long i = b0 + 2 * (ok[w] ? j : j0);
+      iv[w] = *reinterpret_cast<const double2*>(invd + i);
+      fm[w] = *reinterpret_cast<const uchar2*>(fixm + i);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const long long k = i + c * nc;
+        rv[w][c] = *reinterpret_cast<const double2*>(r + k);
+        qq[w][c] = *reinterpret_cast<const double2*>(q + k);
+        if (kU) {
+          uu[w][c] = *reinterpret_cast<const double2*>(u + k);
+          p0[w][c] = *reinterpret_cast<const double2*>(pprev + k);
+          pp[w][c] = *reinterpret_cast<const double2*>(p + k);
+        }
       }
-      double2 rv = *reinterpret_cast<const double2*>(r + k);
-      const double2 qq = *reinterpret_cast<const double2*>(q + k);
-      rv.x = (fm.x >> c) & 1 ? 0.0 : fma(-alpha, qq.x, rv.x);
-      rv.y = (fm.y >> c) & 1 ? 0.0 : fma(-alpha, qq.y, rv.y);
-      *reinterpret_cast<double2*>(r + k) = rv;
-      s0 = fma(rv.x, rv.x, s0);
-      s1 = fma(rv.y, rv.y, s1);
     }
-    rz = fma(s0, iv.x, fma(s1, iv.y, rz));
-    rr += s0 + s1;
+#pragma unroll
+    for (int w = 0; w < UN; ++w) {
+      if (!ok[w]) continue;
+      const long long i = b0 + 2 * (j0 + w * stride);
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const long long k = i + c * nc;
+        if (kU) {
+          double2 un;
+          un.x = fma(alpha, pp[w][c].x, fma(alpha_prev, p0[w][c].x, uu[w][c].x));
+          un.y = fma(alpha, pp[w][c].y, fma(alpha_prev, p0[w][c].y, uu[w][c].y));
+          *reinterpret_cast<double2*>(u + k) = un;
+        }
+        double2 rn;
+        rn.x = (fm[w].x >> c) & 1 ? 0.0 : fma(-alpha, qq[w][c].x, rv[w][c].x);
+        rn.y = (fm[w].y >> c) & 1 ? 0.0 : fma(-alpha, qq[w][c].y, rv[w][c].y);
+        *reinterpret_cast<double2*>(r + k) = rn;
+        s0 = fma(rn.x, rn.x, s0);
+        s1 = fma(rn.y, rn.y, s1);
+      }
+      rz = fma(s0, iv[w].x, fma(s1, iv[w].y, rz));
+      rr += s0 + s1;
+    }
   }
   __shared__ double tot[2];
   double v[2] = {rz, rr};

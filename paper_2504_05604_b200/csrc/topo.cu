@@ -96,6 +96,7 @@ struct Slab {
   DevState* st = nullptr;
   double* stage = nullptr;   // staging for layout transforms
   size_t stage_n = 0;
+  double *u_b = nullptr, *x_b = nullptr, *xphys_b = nullptr;   // snapshot buffers
   // TMA descriptors of the matvec operands (built at init; pointers never change)
   CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E;
 };
@@ -139,6 +140,7 @@ struct topo_ctx {
   std::string err;
   size_t dev_bytes = 0;
   bool debug = false;        // TOPO_DEBUG_SYNC=1: no graphs, sync + check after every kernel
+  bool snap_has_u = false, has_snap = false;
   int sticky = TOPO_OK;
 };
 
@@ -933,7 +935,8 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
-                    s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage};
+                    s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
+                    s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -1426,6 +1429,43 @@ int topo_matvec_run(topo_ctx* ctx, int32_t reps) {
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
   for (int i = 0; i < reps; ++i) CK(matvec_all(ctx, &Slab::w, &Slab::m_w, &Slab::q));
+  return TOPO_OK;
+}
+
+int topo_snapshot(topo_ctx* ctx) {
+  if (!ctx) return TOPO_EINVAL;
+  cudaSetDevice(ctx->device);
+  for (Slab& s : ctx->slabs) {
+    const size_t nb = sizeof(double) * 3 * s.g.ncomp, eb = sizeof(double) * s.g.nelloc;
+    if (!s.u_b) {
+      CU(cudaMalloc(&s.u_b, nb));
+      CU(cudaMalloc(&s.x_b, eb));
+      CU(cudaMalloc(&s.xphys_b, eb));
+      ctx->dev_bytes += nb + 2 * eb;
+    }
+    CU(cudaMemcpyAsync(s.u_b, s.u, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.x_b, s.x, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.xphys_b, s.xphys, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->snap_has_u = ctx->has_u;
+  ctx->has_snap = true;
+  return TOPO_OK;
+}
+
+int topo_restore(topo_ctx* ctx) {
+  if (!ctx) return TOPO_EINVAL;
+  if (!ctx->has_snap) return set_err(ctx, TOPO_ESTATE, "topo_restore without topo_snapshot");
+  cudaSetDevice(ctx->device);
+  for (Slab& s : ctx->slabs) {
+    const size_t nb = sizeof(double) * 3 * s.g.ncomp, eb = sizeof(double) * s.g.nelloc;
+    CU(cudaMemcpyAsync(s.u, s.u_b, nb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.x, s.x_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(s.xphys, s.xphys_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->has_u = ctx->snap_has_u;
+  ctx->has_E = ctx->has_sens = ctx->has_dcf = false;
   return TOPO_OK;
 }
 

@@ -29,7 +29,7 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            "topo_oc_step", "topo_optimize", "topo_apply_K", "topo_update_modulus",
            "topo_matvec_load", "topo_matvec_run", "topo_get", "topo_get_timings", "topo_profile",
            "topo_kernel_time", "topo_element_stiffness", "topo_count", "topo_last_error",
-           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition"]
+           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition", "topo_snapshot", "topo_restore"]
 
 
 class topo_params(C.Structure):
@@ -96,6 +96,8 @@ def _load():
         "topo_version": (C.c_char_p, []),
         "topo_destroy": (None, [ctxp]),
         "topo_nccl_unique_id": (I, [U8]),
+        "topo_snapshot": (I, [ctxp]),
+        "topo_restore": (I, [ctxp]),
         "topo_partition": (I, [C.c_int32, C.c_double, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
@@ -287,6 +289,12 @@ class Problem:
 
     def matvec_run(self, reps=1):
         self._check(_lib.topo_matvec_run(self._ctx, int(reps)), "topo_matvec_run")
+
+    def snapshot(self):
+        self._check(_lib.topo_snapshot(self._ctx), "topo_snapshot")
+
+    def restore(self):
+        self._check(_lib.topo_restore(self._ctx), "topo_restore")
 
     def get(self, field):
         n = 3 * self.n_nd if field in NODE_FIELDS else self.n_el

@@ -246,3 +246,17 @@ def test_single_element_and_tiny(topo):
         with topo.Problem(p, f, fx) as pr:
             c, x, nd = pr.optimize(3)
         assert_rel(c, ro["c"], 1e-6, f"c {dims}")
+
+
+def test_snapshot_restore_bitwise_determinism(topo):
+    """S:446 determinism: replaying the same SIMP iterations from a device
+    snapshot gives bit-identical compliance histories and designs (all
+    reductions are fixed-order)."""
+    p, f, fx, pas = make_problem(1)
+    with topo.Problem(p, f, fx, pas) as pr:
+        pr.optimize(3)
+        pr.snapshot()
+        c1, x1, _ = pr.optimize(4)
+        pr.restore()
+        c2, x2, _ = pr.optimize(4)
+    assert np.array_equal(c1, c2) and np.array_equal(x1, x2)
