@@ -82,6 +82,21 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic(cfg, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the fused matvec from the
+    newest committed ncu --set full capture (profiles/), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_cfg%d.json" % cfg)))
+    if not files or world != 1:
+        return None
+    try:
+        d = json.load(open(files[-1]))
+        k = next(v for n, v in d.items() if n.startswith("k_mv_wht"))
+        return (k["dram_read_GB"] + k["dram_write_GB"]) * 1e9
+    except Exception:
+        return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -316,8 +331,11 @@ def main():
     own_nd = n_nd // world
     mv_bytes = 105 * own_nd + 8 * own_el
     achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+    traffic = ncu_traffic(args.config, world)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+            "traffic_source": "profiles/r*_ncu_cfg%d.json (ncu --set full, one launch)" % args.config
+            if traffic else None,
             "kernel": "k_mv_wht<fused,dot> (p = M^-1 r + beta p; q = K p; p.q)", "samples": mv_samples,
             "mean_ms": mv_ms, "bytes_per_launch": mv_bytes, "peak_source": peaks_src}
 

@@ -260,3 +260,16 @@ def test_snapshot_restore_bitwise_determinism(topo):
         pr.restore()
         c2, x2, _ = pr.optimize(4)
     assert np.array_equal(c1, c2) and np.array_equal(x1, x2)
+
+
+def test_paper_protocol_parity(topo):
+    """The paper's own benchmark protocol (32x16x16, rmin 4 -> 251-point
+    stencil, point load, sensitivity filter): first 5 iterations vs oracle."""
+    p, f, fx, pas = make_problem("paper")
+    ro = oracle.run_optimization(p, f, fx, pas, n_iter=5)
+    with topo.Problem(p, f, fx, pas) as pr:
+        c, x, nd = pr.optimize(5)
+        xphys = pr.get("xphys")
+        assert pr.count("stencil") == 251
+    assert_rel(c, ro["c"], 1e-6, "c history (paper protocol)")
+    assert_rel(xphys, ro["xPhys"], 1e-6, "xPhys (paper protocol)")

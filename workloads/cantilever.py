@@ -28,6 +28,15 @@ CONFIGS = {
 }
 
 
+# The paper's own benchmark protocol (§3, §4.2; SURVEY
+# §8(f) NEXT f1): 32x16x16 cantilever, volfrac 0.2, penal 3.0, rmin 4.0,
+# 200 iterations, left face fixed, a vertical point load at the centre of the
+# free end's bottom edge, the paper's sensitivity filter.  The
+# solve tolerance stands in for the paper's direct solver.
+PAPER_PROTOCOL = dict(nelx=32, nely=16, nelz=16, volfrac=0.2, rmin=4.0, n_iter=200, cg_rtol=1e-10,
+                      obstacle=None, filter_mode=1, load="point")
+
+
 def config_params(cfg, **over):
     """Full parameter dict of a config (common values + config values + overrides)."""
     p = dict(COMMON)
@@ -115,11 +124,23 @@ def random_vector(n, seed=1):
     return np.random.default_rng(seed).standard_normal(n)
 
 
+def point_load(nelx, nely, nelz):
+    """f_y = -1 on the node at the centre of the free end's bottom edge:
+    (ix, iy, iz) = (nelx, 0, nelz // 2)  (P:59 "vertical point load ... at the
+    center of the free end's bottom edge"; vertical = -y as in the configs)."""
+    f = np.zeros(3 * n_nodes(nelx, nely, nelz))
+    f[3 * node_id(nelx, nely, nelz, nelx, 0, nelz // 2) + 1] = -1.0
+    return f
+
+
 def make_problem(cfg, **over):
-    """(params, f, fixed, passive-or-None) for a BASELINE config index or a dict."""
+    """(params, f, fixed, passive-or-None) for a BASELINE config index, "paper"
+    (the paper's benchmark protocol) or a dict."""
+    if cfg == "paper":
+        cfg = PAPER_PROTOCOL
     p = config_params(cfg, **over)
     nelx, nely, nelz = p["nelx"], p["nely"], p["nelz"]
-    f = cantilever_load(nelx, nely, nelz)
+    f = point_load(nelx, nely, nelz) if p.get("load") == "point" else cantilever_load(nelx, nely, nelz)
     fixed = cantilever_fixed(nelx, nely, nelz)
     passive = None
     if p.get("obstacle"):
