@@ -14,6 +14,8 @@ It follows the paper's own CPU pipeline (PAPER.md = P:line):
   filt       cone filter H, Hs (brute force)         P:50 §2.4
   oc         OC bisection with move limits, passive  P:47 §2.3; S:282
   loop       top3d loop                              P:53 §2.5; S:292
+  mg         geometric multigrid preconditioner      SURVEY §8(f) f2 (P:104, P:115);
+             (Galerkin, damped Jacobi, V-cycle)      readings M1-M6 in DESIGN.md
 Arithmetic is fp64 throughout.  Readings where the paper is silent are listed in
 DESIGN.md ("Readings") and cited as R#n below.
 
@@ -30,3 +32,4 @@ from .fem import (assemble, solve, solve_direct, solve_jacobi_cg, compliance_fu,
 from .filt import filter_matrix, filter_matrix_allpairs, apply_filter, filter_rows  # noqa: F401
 from .oc import oc_update, oc_xnew, sensitivities  # noqa: F401
 from .loop import run_optimization  # noqa: F401
+from . import mg  # noqa: F401

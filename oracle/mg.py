@@ -1,0 +1,227 @@
+"""Geometric multigrid preconditioner for the K(x)u = f solve (oracle).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Why: SURVEY §8(f) NEXT f2 -- "matrix-free geometric multigrid preconditioner on
+the hex-grid hierarchy, replacing Jacobi"; the paper names the solve as the
+dominant cost (Table 1 "Solve" 67.8 %) and scalability of
+the solver as future work (§4.3).  The paper gives no multigrid
+algorithm, so this module writes out the textbook one (DESIGN.md readings
+M1-M6), each step in plain NumPy/SciPy, no blocking or fusion:
+
+  M1 hierarchy   nested Hex8 grids, coarse element = 2x2x2 fine elements,
+                 n_c = ceil(n/2) per axis (an odd axis gets a half-empty last
+                 coarse element; its outer node is a plain coarse node)
+  M2 transfer    P = trilinear interpolation (per axis: even fine node 2j <- coarse
+                 j; odd fine node 2j+1 <- (j, j+1) with weights 1/2, 1/2),
+                 restriction = P^T
+  M3 operators   Galerkin: K_{l+1} = P^T K_l P (unmasked); the level operator
+                 acts on free DOFs only (A_l = K_l[free, free])
+  M4 coarse BCs  coarse DOF (j, c) fixed iff the fine node at min(2j, n) (per
+                 axis: the coarse node's position, clamped into the fine grid) has
+                 DOF c fixed.  The hierarchy is only built while property Q holds:
+                 every fixed fine DOF interpolates from fixed coarse DOFs only.
+                 Under Q, P^T K P restricted to free coarse DOFs IS the Galerkin
+                 operator of the free-DOF problem (pinned in tests)
+  M5 smoother    damped Jacobi x <- x + w D^-1 (b - A x), nu pre- and nu
+                 post-smoothing steps (symmetric V-cycle -> SPD preconditioner)
+  M6 coarsest    exact solve (dense Cholesky) on the coarsest level; coarsening
+                 stops at the first level with <= coarse_max DOFs
+The outer Krylov method is the same PCG as solve_jacobi_cg (stopping on the
+true residual), with z = V(r) instead of z = D^-1 r.
+"""
+import numpy as np
+import scipy.linalg as sla
+import scipy.sparse as sp
+
+
+def coarse_dims(nelx, nely, nelz):
+    """M1: coarse grid of ceil(n/2) elements per axis."""
+    return (nelx + 1) // 2, (nely + 1) // 2, (nelz + 1) // 2
+
+
+def prolongation_1d(n):
+    """M2 along one axis: (n+1) fine nodes x (ceil(n/2)+1) coarse nodes."""
+    nc = (n + 1) // 2
+    P = np.zeros((n + 1, nc + 1))
+    for i in range(n + 1):
+        if i % 2 == 0:
+            P[i, i // 2] = 1.0
+        else:
+            P[i, (i - 1) // 2] = 0.5
+            P[i, (i + 1) // 2] = 0.5
+    return P
+
+
+def prolongation(nelx, nely, nelz):
+    """M2: DOF-level trilinear interpolation P [3 n_nd_fine, 3 n_nd_coarse] in the
+    SPEC S:45 numbering (node = iz (nx+1)(ny+1) + ix (ny+1) + iy, DOF 3n + c):
+    node-level P = Pz (x) Px (x) Py, DOF-level = P_node (x) I_3."""
+    Px, Py, Pz = (sp.csr_matrix(prolongation_1d(n)) for n in (nelx, nely, nelz))
+    Pn = sp.kron(Pz, sp.kron(Px, Py))
+    P = sp.kron(Pn, sp.identity(3)).tocsr()
+    P.eliminate_zeros()                 # kron keeps explicit zeros; the sparsity pattern is used (Q)
+    return P
+
+
+def prolongation_loops(nelx, nely, nelz):
+    """Same matrix by explicit enumeration of fine nodes (brute-force check)."""
+    cx, cy, cz = coarse_dims(nelx, nely, nelz)
+    w1 = [prolongation_1d(n) for n in (nelx, nely, nelz)]
+    rows, cols, vals = [], [], []
+    for iz in range(nelz + 1):
+        for ix in range(nelx + 1):
+            for iy in range(nely + 1):
+                n = iz * (nelx + 1) * (nely + 1) + ix * (nely + 1) + iy
+                for jz in range(cz + 1):
+                    for jx in range(cx + 1):
+                        for jy in range(cy + 1):
+                            w = w1[0][ix, jx] * w1[1][iy, jy] * w1[2][iz, jz]
+                            if w == 0.0:
+                                continue
+                            m = jz * (cx + 1) * (cy + 1) + jx * (cy + 1) + jy
+                            for c in range(3):
+                                rows.append(3 * n + c)
+                                cols.append(3 * m + c)
+                                vals.append(w)
+    nf = 3 * (nelx + 1) * (nely + 1) * (nelz + 1)
+    nc = 3 * (cx + 1) * (cy + 1) * (cz + 1)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(nf, nc))
+
+
+def coarse_fixed(nelx, nely, nelz, fixed):
+    """M4: coarse DOF (j, c) fixed iff fine node min(2j, n) (per axis) has DOF c fixed."""
+    cx, cy, cz = coarse_dims(nelx, nely, nelz)
+    fixed = np.asarray(fixed)
+    out = np.zeros(3 * (cx + 1) * (cy + 1) * (cz + 1), dtype=np.uint8)
+    for jz in range(cz + 1):
+        for jx in range(cx + 1):
+            for jy in range(cy + 1):
+                ix, iy, iz = min(2 * jx, nelx), min(2 * jy, nely), min(2 * jz, nelz)
+                n = iz * (nelx + 1) * (nely + 1) + ix * (nely + 1) + iy
+                m = jz * (cx + 1) * (cy + 1) + jx * (cy + 1) + jy
+                out[3 * m:3 * m + 3] = fixed[3 * n:3 * n + 3]
+    return out
+
+
+def property_q(P, fixed_f, fixed_c):
+    """M4: True iff every fixed fine DOF receives interpolation weight only from
+    fixed coarse DOFs (then masking commutes with the Galerkin product)."""
+    rows = np.flatnonzero(np.asarray(fixed_f) != 0)
+    sub = P[rows].tocoo()
+    return not np.any(np.asarray(fixed_c)[sub.col] == 0)
+
+
+def n_levels(nelx, nely, nelz, coarse_max=1000):
+    """M6: number of levels: coarsen until a level has <= coarse_max DOFs (or
+    the grid cannot shrink any more)."""
+    dims, L = (nelx, nely, nelz), 1
+    while 3 * (dims[0] + 1) * (dims[1] + 1) * (dims[2] + 1) > coarse_max:
+        nd = coarse_dims(*dims)
+        if nd == dims:
+            break
+        dims, L = nd, L + 1
+    return L
+
+
+def hierarchy(K, fixed, dims, n_lev=None, coarse_max=1000):
+    """Levels [dict(dims, K, fixed, P (to the next-coarser level))], fine first (M1-M4)."""
+    if n_lev is None:
+        n_lev = n_levels(*dims, coarse_max=coarse_max)
+    levels = [dict(dims=tuple(dims), K=K.tocsr(), fixed=np.asarray(fixed, dtype=np.uint8))]
+    for _ in range(n_lev - 1):
+        lv = levels[-1]
+        P = prolongation(*lv["dims"])
+        fc = coarse_fixed(*lv["dims"], lv["fixed"])
+        if not property_q(P, lv["fixed"], fc):
+            break                       # M4: stop coarsening where Q fails
+        lv["P"] = P
+        Kc = (P.T @ lv["K"] @ P).tocsr()
+        levels.append(dict(dims=coarse_dims(*lv["dims"]), K=Kc, fixed=fc))
+    return levels
+
+
+def level_operator(lv):
+    """A_l on the free DOFs, its diagonal and the free index set (M3)."""
+    free = np.flatnonzero(lv["fixed"] == 0)
+    A = lv["K"][free][:, free].tocsr()
+    return A, A.diagonal(), free
+
+
+def vcycle(levels, b, omega=0.6, nu=2, _l=0, _ops=None):
+    """One V-cycle z = V(b) for a full-length level-_l vector b (0 on fixed DOFs).
+    M5/M6; textbook recursion (Briggs, Henson, McCormick, "A Multigrid Tutorial",
+    V-cycle scheme), written out without fusion."""
+    if _ops is None:
+        _ops = [level_operator(lv) for lv in levels]
+        for k, lv in enumerate(levels):
+            if k == len(levels) - 1:
+                lv["chol"] = sla.cho_factor(_ops[k][0].toarray())
+    A, d, free = _ops[_l]
+    lv = levels[_l]
+    bf = b[free]
+    if _l == len(levels) - 1:
+        xf = sla.cho_solve(lv["chol"], bf)
+    else:
+        xf = np.zeros_like(bf)
+        for _ in range(nu):
+            xf = xf + omega * (bf - A @ xf) / d
+        r = np.zeros_like(b)
+        r[free] = bf - A @ xf
+        rc = lv["P"].T @ r
+        rc[levels[_l + 1]["fixed"] != 0] = 0.0
+        ec = vcycle(levels, rc, omega, nu, _l + 1, _ops)
+        xf = xf + (lv["P"] @ ec)[free]
+        for _ in range(nu):
+            xf = xf + omega * (bf - A @ xf) / d
+    x = np.zeros_like(b)
+    x[free] = xf
+    return x
+
+
+def solve_mgcg(K, f, fixed, dims, rtol=1e-10, omega=0.6, nu=2, coarse_max=1000,
+               max_iter=10000, u0=None):
+    """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
+    TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""
+    levels = hierarchy(K, fixed, dims, coarse_max=coarse_max)
+    ops = [level_operator(lv) for lv in levels]
+    levels[-1]["chol"] = sla.cho_factor(ops[-1][0].toarray())
+    A, _, free = ops[0]
+    fx = np.asarray(fixed) != 0
+    nb = np.linalg.norm(f[~fx])
+    u = np.zeros(K.shape[0]) if u0 is None else np.where(fx, 0.0, u0)
+    if nb == 0.0:
+        return np.zeros(K.shape[0]), 0
+
+    def M(r):
+        return vcycle(levels, r, omega, nu, 0, ops)
+
+    def res(u):
+        r = np.zeros_like(u)
+        r[free] = f[free] - A @ u[free]
+        return r
+    r = res(u)
+    z = M(r)
+    p = z.copy()
+    rz = r @ z
+    it = 0
+    while it < max_iter:
+        if np.linalg.norm(r) <= rtol * nb:
+            rt = res(u)
+            if np.linalg.norm(rt) <= rtol * nb:
+                break
+            r = rt
+            z = M(r)
+            p = z.copy()
+            rz = r @ z
+        q = np.zeros_like(p)
+        q[free] = A @ p[free]
+        alpha = rz / (p @ q)
+        u = u + alpha * p
+        r = r - alpha * q
+        z = M(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+        it += 1
+    return u, it

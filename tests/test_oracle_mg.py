@@ -1,0 +1,173 @@
+"""Pins for oracle.mg (geometric multigrid) against
+closed forms, brute force and invariants -- not against the oracle itself.
+
+* P by explicit enumeration; P reproduces linear fields exactly (trilinear
+  interpolation is exact for them, also with a half-empty last coarse element)
+* Galerkin P^T K P of a 2x2x2 fine grid = the coarse (h = 2) Hex8 element
+  matrix integrated octant by octant with the octant's modulus (FE subspace
+  property; independent Gauss quadrature, no P, no assembly)
+* uniform modulus: Galerkin coarse operator = rediscretisation with 2 KE
+* coarse fixed DOFs of the cantilever = the x = 0 face at every level; property
+  Q holds; under Q masking commutes with the Galerkin product
+* V-cycle is a symmetric positive definite operator; 1-level V-cycle = exact
+  solve; MG-PCG reaches the direct solution (readings M1-M6)
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+from oracle import mg
+from oracle.ke import constitutive, strain_displacement
+from oracle.mesh import LOCAL_NODES
+from workloads import make_problem
+from workloads.cantilever import cantilever_fixed, cantilever_load
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (3, 2, 1), (4, 3, 2), (5, 5, 3)])
+def test_prolongation_matches_enumeration(dims):
+    a = mg.prolongation(*dims)
+    b = mg.prolongation_loops(*dims)
+    assert a.shape == b.shape
+    assert abs(a - b).max() == 0.0
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2), (3, 2, 1), (5, 4, 3), (6, 1, 2)])
+def test_prolongation_reproduces_linear_fields(dims):
+    nx, ny, nz = dims
+    cx, cy, cz = mg.coarse_dims(*dims)
+    P = mg.prolongation(*dims)
+    A = np.array([[0.3, -1.2, 0.7], [2.0, 0.1, -0.4], [-0.5, 0.9, 1.1]])
+    t = np.array([0.25, -0.5, 1.5])
+
+    def field(nxx, nyy, nzz, h):
+        v = np.zeros(3 * (nxx + 1) * (nyy + 1) * (nzz + 1))
+        for iz in range(nzz + 1):
+            for ix in range(nxx + 1):
+                for iy in range(nyy + 1):
+                    n = iz * (nxx + 1) * (nyy + 1) + ix * (nyy + 1) + iy
+                    v[3 * n:3 * n + 3] = A @ (h * np.array([ix, iy, iz])) + t
+        return v
+    # coarse node j sits at fine position 2j (outside the grid for the last node of an odd axis)
+    assert np.max(np.abs(P @ field(cx, cy, cz, 2.0) - field(nx, ny, nz, 1.0))) < 1e-13
+
+
+def _coarse_element_by_quadrature(E_oct, nu):
+    """24x24 stiffness of a cube of edge 2 whose 8 octants have moduli E_oct[cx,cy,cz]:
+    sum over octants of E * h * int_oct B^T D B (reference coordinates, 2x2x2 Gauss per
+    octant; exact for the trilinear integrand).  Independent of P and of assembly."""
+    D = constitutive(1.0, nu)
+    g = (0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0))
+    K = np.zeros((24, 24))
+    for cz in (0, 1):
+        for cx in (0, 1):
+            for cy in (0, 1):
+                for a in g:
+                    for b in g:
+                        for c in g:
+                            B = strain_displacement((cx + a) / 2, (cy + b) / 2, (cz + c) / 2)
+                            K += E_oct[cx, cy, cz] * 2.0 * (1.0 / 64.0) * (B.T @ D @ B)
+    return K
+
+
+def test_galerkin_equals_octant_quadrature():
+    nu = 0.3
+    KE = oracle.element_stiffness(nu)
+    rng = np.random.default_rng(5)
+    E = rng.uniform(1e-3, 1.0, 8)                      # fine elements, external order (ez, ex, ey)
+    K = oracle.assemble(2, 2, 2, KE, E)
+    P = mg.prolongation(2, 2, 2)
+    Kc = (P.T @ K @ P).toarray()                       # 8 coarse nodes, SPEC numbering
+    E_oct = np.zeros((2, 2, 2))
+    for ez in range(2):
+        for ex in range(2):
+            for ey in range(2):
+                E_oct[ex, ey, ez] = E[ez * 4 + ex * 2 + ey]
+    Kq = _coarse_element_by_quadrature(E_oct, nu)      # local node order
+    # coarse node n(jx,jy,jz) = jz*4 + jx*2 + jy; local corner a at (dx,dy,dz)
+    perm = []
+    for (dx, dy, dz) in LOCAL_NODES:
+        n = dz * 4 + dx * 2 + dy
+        perm += [3 * n, 3 * n + 1, 3 * n + 2]
+    assert np.max(np.abs(Kc[np.ix_(perm, perm)] - Kq)) < 1e-13 * np.max(np.abs(Kq))
+
+
+@pytest.mark.parametrize("dims", [(4, 2, 2), (6, 4, 2)])
+def test_galerkin_uniform_is_rediscretisation(dims):
+    KE = oracle.element_stiffness(0.3)
+    n_el = dims[0] * dims[1] * dims[2]
+    K = oracle.assemble(*dims, KE, np.ones(n_el))
+    P = mg.prolongation(*dims)
+    cd = mg.coarse_dims(*dims)
+    Kc = oracle.assemble(*cd, 2.0 * KE, np.ones(cd[0] * cd[1] * cd[2]))
+    d = (P.T @ K @ P - Kc).toarray()
+    assert np.max(np.abs(d)) < 1e-13
+
+
+@pytest.mark.parametrize("dims", [(30, 10, 2), (60, 20, 4), (120, 40, 20), (7, 5, 3)])
+def test_cantilever_coarse_fixed_is_face_and_property_q(dims):
+    fx = cantilever_fixed(*dims)
+    cur = dims
+    for _ in range(6):
+        cd = mg.coarse_dims(*cur)
+        fc = mg.coarse_fixed(*cur, fx)
+        assert np.array_equal(fc, cantilever_fixed(*cd))      # the x = 0 face, all DOFs
+        assert mg.property_q(mg.prolongation(*cur), fx, fc)
+        cur, fx = cd, fc
+
+
+def test_masked_galerkin_identity_under_q():
+    dims = (6, 4, 2)
+    p, f, fx, _ = make_problem(dict(nelx=6, nely=4, nelz=2, volfrac=0.3, rmin=1.5, n_iter=1,
+                                    cg_rtol=1e-10, obstacle=None))
+    KE = oracle.element_stiffness(0.3)
+    E = np.random.default_rng(2).uniform(1e-9, 1.0, 48)
+    K = oracle.assemble(*dims, KE, E)
+    P = mg.prolongation(*dims)
+    fc = mg.coarse_fixed(*dims, fx)
+    ff, cf = np.flatnonzero(fx == 0), np.flatnonzero(fc == 0)
+    A1 = (P.T @ K @ P)[cf][:, cf]
+    Pm = P[ff][:, cf]
+    A2 = Pm.T @ K[ff][:, ff] @ Pm
+    assert abs(A1 - A2).max() < 1e-14
+
+
+def _evolved_case(cfg=1, n_iter=6):
+    p, f, fx, pas = make_problem(cfg)
+    r = oracle.run_optimization(p, f, fx, pas, n_iter=n_iter, solver="direct", record=True)
+    rec = r["records"][-1]
+    E = p["Emin"] + rec["xPhys"] ** p["penal"] * (p["E0"] - p["Emin"])
+    KE = oracle.element_stiffness(p["nu"])
+    dims = (p["nelx"], p["nely"], p["nelz"])
+    return oracle.assemble(*dims, KE, E), f, fx, dims, rec["u"]
+
+
+def test_vcycle_symmetric_positive_definite():
+    K, f, fx, dims, _ = _evolved_case(1, 4)
+    lv = mg.hierarchy(K, fx, dims)
+    assert len(lv) == 3
+    rng = np.random.default_rng(3)
+    free = fx == 0
+    b1 = np.where(free, rng.standard_normal(len(f)), 0.0)
+    b2 = np.where(free, rng.standard_normal(len(f)), 0.0)
+    v1, v2 = mg.vcycle(lv, b1), mg.vcycle(lv, b2)
+    assert abs(b1 @ v2 - b2 @ v1) <= 1e-12 * abs(b1 @ v2)
+    assert b1 @ v1 > 0 and b2 @ v2 > 0
+    assert np.all(v1[~free] == 0.0)
+
+
+def test_vcycle_one_level_is_exact_solve():
+    K, f, fx, dims, u = _evolved_case(0, 3)
+    lv = mg.hierarchy(K, fx, dims, n_lev=1)
+    z = mg.vcycle(lv, np.where(fx == 0, f, 0.0))
+    assert np.linalg.norm(z - u) <= 1e-9 * np.linalg.norm(u)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_mgcg_reaches_direct_solution(cfg):
+    K, f, fx, dims, u = _evolved_case(cfg, 8)
+    um, it = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10)
+    _, itj = oracle.solve_jacobi_cg(K, f, fx, rtol=1e-10)
+    assert np.linalg.norm(um - u) <= 1e-8 * np.linalg.norm(u)
+    assert oracle.true_residual(K, um, f, fx) <= 1e-10
+    assert it < itj / 5                                        # the point of f2
