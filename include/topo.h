@@ -6,7 +6,8 @@
  *   topo_init         problem statement: grid, material, loads, supports,
  *                     passive (obstacle) regions              P:42 §2.2, §2.3
  *   topo_set_density  design variables x (pseudo-densities)   P:45 §2.3
- *   topo_solve        K(x) u = f, matrix-free EbE Jacobi-PCG  P:42 §2.2
+ *   topo_solve        K(x) u = f, matrix-free EbE PCG          P:42 §2.2
+ *                     (Jacobi or geometric-multigrid preconditioner)
  *   topo_sensitivity  ce = u_e^T KE u_e, c, dc                P:47 §2.3
  *   topo_filter       rmin cone filter (density / sensitivity) P:50 §2.4
  *   topo_oc_step      OC bisection with move limits            P:44-47 §2.3
@@ -106,7 +107,24 @@ typedef struct {
   double  oc_lmax;            /* initial bracket [0, oc_lmax]                                */
   int32_t deterministic;      /* reductions are always fixed-order; kept for the ABI */
   int32_t cg_check_every;     /* PCG iterations per CUDA-graph batch between host polls; <=0 auto */
+  /* Preconditioner of the PCG solve (readings M1-M6).
+   * TOPO_PRECOND_JACOBI: z = D^-1 r with the on-the-fly diagonal.
+   * TOPO_PRECOND_MG: one V-cycle of geometric multigrid on the nested Hex8 grids
+   *   (trilinear transfer, Galerkin coarse operators, damped-Jacobi smoothing,
+   *   exact coarsest solve).  Single slab only (world == 1); EINVAL at init if
+   *   the hierarchy cannot be built (fewer than 2 levels, or coarse Dirichlet
+   *   DOFs that do not cover the fine ones: property Q of reading M4).
+   * TOPO_PRECOND_AUTO (default): MG where it can be built, else Jacobi.         */
+  int32_t precond;
+  int32_t mg_nu;              /* damped-Jacobi sweeps before and after the coarse correction (>= 1) */
+  double  mg_omega;           /* theta in (0, 2): level-l Jacobi weight w_l = theta / lam_l, lam_l the
+                                 Rayleigh quotient of D^-1 A_l after 8 power steps (default 1.6)   */
+  int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (<= 4096) */
 } topo_params;
+
+#define TOPO_PRECOND_JACOBI 0
+#define TOPO_PRECOND_MG     1
+#define TOPO_PRECOND_AUTO   2
 
 typedef struct {
   int32_t mode;               /* TOPO_DIST_SINGLE / _NCCL / _LOOPBACK                       */
@@ -121,6 +139,8 @@ typedef struct {
   double  true_rel_res;       /* ||f - K u||/||f_free|| recomputed at exit                   */
   double  ms;                 /* device time of the solve (CUDA events)                      */
   int32_t replacements;       /* residual replacements performed                             */
+  int32_t precond;            /* preconditioner used: TOPO_PRECOND_JACOBI or TOPO_PRECOND_MG  */
+  int32_t mg_levels;          /* multigrid levels (0 with Jacobi)                            */
 } topo_solve_info;
 
 typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulative counters  */
@@ -130,6 +150,8 @@ typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulativ
   double  c, fu, volume, change, lambda;
   int64_t kernel_launches;    /* cumulative count of this library's kernel launches          */
   int64_t cg_iters_total;     /* cumulative PCG iterations                                   */
+  int32_t mg_fallbacks;       /* solves where the multigrid PCG broke down and was redone with
+                                 the Jacobi preconditioner (cumulative)                        */
 } topo_timings;
 
 /* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,
@@ -167,7 +189,8 @@ int topo_set_density(topo_ctx *ctx, const double *x);
 /* Set physical densities directly (xPhys, [n_el]); passive forced to 0.    */
 int topo_set_xphys(topo_ctx *ctx, const double *xphys);
 
-/* Solve K(xPhys) u = f on free DOFs (Jacobi-PCG, matrix-free).  Computes
+/* Solve K(xPhys) u = f on free DOFs (PCG, matrix-free; preconditioner per
+ * topo_params.precond).  Computes
  * E = Emin + xPhys^p (E0-Emin) first.  u: [3*n_nd] output or NULL.
  * Errors: ENOCONV, EBREAKDOWN (u keeps the last iterate).                   */
 int topo_solve(topo_ctx *ctx, double *u, topo_solve_info *info);
@@ -234,6 +257,18 @@ int topo_kernel_time(topo_ctx *ctx, double *mean_ms, int64_t *samples);
 /* The element stiffness the library uses (24x24 row-major, unit cube,
  * E = 1, 2x2x2 Gauss; "pre-computed").  No context needed.    */
 int topo_element_stiffness(double nu, double *ke576);
+
+/* Multigrid test hooks.  topo_mg_levels: *n_levels = L (0
+ * if the context solves with Jacobi) and the element counts dims[3*l ..
+ * 3*l+2] = (nelx_l, nely_l, nelz_l) for l < L (dims may be NULL; room for 16
+ * levels).  topo_mg_apply: y = A_l x on level l (external numbering of level
+ * l's grid, [3*(nelx_l+1)(nely_l+1)(nelz_l+1)], x read as 0 on fixed DOFs, y = 0
+ * there), A_0 = K(E), A_{l+1} = P^T A_l P (Galerkin).  topo_mg_vcycle: z = V(b)
+ * for a fine-level b [3*n_nd] (one V-cycle, the PCG preconditioner).  Both use
+ * the current E (recomputed from xPhys if stale).  ESTATE without multigrid. */
+int topo_mg_levels(topo_ctx *ctx, int32_t *n_levels, int32_t *dims);
+int topo_mg_apply(topo_ctx *ctx, int32_t level, const double *x, double *y);
+int topo_mg_vcycle(topo_ctx *ctx, const double *b, double *z);
 
 /* Number of layout/grid facts for tests: n_dof, n_el, owned nodes, etc.    */
 int64_t topo_count(const topo_ctx *ctx, int32_t what);

@@ -23,8 +23,12 @@ M1-M6), each step in plain NumPy/SciPy, no blocking or fusion:
                  every fixed fine DOF interpolates from fixed coarse DOFs only.
                  Under Q, P^T K P restricted to free coarse DOFs IS the Galerkin
                  operator of the free-DOF problem (pinned in tests)
-  M5 smoother    damped Jacobi x <- x + w D^-1 (b - A x), nu pre- and nu
+  M5 smoother    damped Jacobi x <- x + w_l D^-1 (b - A x), nu pre- and nu
                  post-smoothing steps (symmetric V-cycle -> SPD preconditioner)
+                 with w_l = theta / lam_l, lam_l = Rayleigh quotient of D^-1 A_l
+                 after k power steps from a fixed hash-generated start vector
+                 (lam_l <= lam_max: a fixed w would diverge where lam_max(D^-1 A)
+                 exceeds 2/w, which random densities reach: lam_max ~ 4.7)
   M6 coarsest    exact solve (dense Cholesky) on the coarsest level; coarsening
                  stops at the first level with <= coarse_max DOFs
 The outer Krylov method is the same PCG as solve_jacobi_cg (stopping on the
@@ -148,10 +152,45 @@ def level_operator(lv):
     return A, A.diagonal(), free
 
 
-def vcycle(levels, b, omega=0.6, nu=2, _l=0, _ops=None):
+def start_vector(n_dof, fixed):
+    """M5: deterministic start vector of the power steps: DOF k (external
+    numbering of its level) gets 2 u - 1, u = (splitmix64(k) >> 11) / 2^53;
+    0 on fixed DOFs.  Integer arithmetic, so any implementation reproduces it."""
+    M = (1 << 64) - 1
+    v = np.zeros(n_dof)
+    for k in range(n_dof):
+        z = (k + 0x9E3779B97F4A7C15) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        z = z ^ (z >> 31)
+        v[k] = 2.0 * ((z >> 11) * 2.0 ** -53) - 1.0
+    v[np.asarray(fixed) != 0] = 0.0
+    return v
+
+
+def lambda_estimate(lv, k=8):
+    """M5: lam = (v^T A v) / (v^T D v) after v <- D^-1 A v applied k times
+    (power method on D^-1 A, no normalisation needed for k this small)."""
+    A, d, free = level_operator(lv)
+    v = start_vector(lv["K"].shape[0], lv["fixed"])[free]
+    for _ in range(k):
+        v = (A @ v) / d
+    return float((v @ (A @ v)) / (v @ (d * v)))
+
+
+def smoother_weights(levels, theta=1.6, k=8):
+    """w_l = theta / lam_l on every level but the coarsest (M5)."""
+    for lv in levels[:-1]:
+        lv["lam"] = lambda_estimate(lv, k)
+        lv["omega"] = theta / lv["lam"]
+    return levels
+
+
+def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
     """One V-cycle z = V(b) for a full-length level-_l vector b (0 on fixed DOFs).
     M5/M6; textbook recursion (Briggs, Henson, McCormick, "A Multigrid Tutorial",
-    V-cycle scheme), written out without fusion."""
+    V-cycle scheme), written out without fusion.  omega None -> each level's
+    lv["omega"] (smoother_weights), else one fixed weight on every level."""
     if _ops is None:
         _ops = [level_operator(lv) for lv in levels]
         for k, lv in enumerate(levels):
@@ -160,12 +199,13 @@ def vcycle(levels, b, omega=0.6, nu=2, _l=0, _ops=None):
     A, d, free = _ops[_l]
     lv = levels[_l]
     bf = b[free]
+    w = lv.get("omega") if omega is None else omega
     if _l == len(levels) - 1:
         xf = sla.cho_solve(lv["chol"], bf)
     else:
         xf = np.zeros_like(bf)
         for _ in range(nu):
-            xf = xf + omega * (bf - A @ xf) / d
+            xf = xf + w * (bf - A @ xf) / d
         r = np.zeros_like(b)
         r[free] = bf - A @ xf
         rc = lv["P"].T @ r
@@ -173,17 +213,17 @@ def vcycle(levels, b, omega=0.6, nu=2, _l=0, _ops=None):
         ec = vcycle(levels, rc, omega, nu, _l + 1, _ops)
         xf = xf + (lv["P"] @ ec)[free]
         for _ in range(nu):
-            xf = xf + omega * (bf - A @ xf) / d
+            xf = xf + w * (bf - A @ xf) / d
     x = np.zeros_like(b)
     x[free] = xf
     return x
 
 
-def solve_mgcg(K, f, fixed, dims, rtol=1e-10, omega=0.6, nu=2, coarse_max=1000,
-               max_iter=10000, u0=None):
+def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
+               max_iter=10000, u0=None, power_steps=8):
     """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
     TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""
-    levels = hierarchy(K, fixed, dims, coarse_max=coarse_max)
+    levels = smoother_weights(hierarchy(K, fixed, dims, coarse_max=coarse_max), theta, power_steps)
     ops = [level_operator(lv) for lv in levels]
     levels[-1]["chol"] = sla.cho_factor(ops[-1][0].toarray())
     A, _, free = ops[0]
@@ -194,7 +234,7 @@ def solve_mgcg(K, f, fixed, dims, rtol=1e-10, omega=0.6, nu=2, coarse_max=1000,
         return np.zeros(K.shape[0]), 0
 
     def M(r):
-        return vcycle(levels, r, omega, nu, 0, ops)
+        return vcycle(levels, r, None, nu, 0, ops)
 
     def res(u):
         r = np.zeros_like(u)

@@ -72,6 +72,10 @@ __global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
 // A3/A4  PCG vector kernels over the owned node planes (pads are zero and
 // stay zero).  SoA: component stride ncomp.
 // ===========================================================================
+// kMG: beta and rz (= r.z) come from the V-cycle's last sweep (k_mg_jacobi<2>),
+// so only the iteration count, the pending-u bookkeeping and the stopping test
+// are updated here.
+template <bool kMG = false>
 __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, double rr, int even) {
   if (even) {                 // u update deferred: the next (odd) update applies both steps
     st->alpha_prev = st->alpha;
@@ -79,8 +83,10 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
   } else {
     st->pending = 0;
   }
-  st->beta = rz_new / st->rz;
-  st->rz = rz_new;
+  if (!kMG) {
+    st->beta = rz_new / st->rz;
+    st->rz = rz_new;
+  }
   st->rr = rr;
   st->it += 1;
   st->fresh = 0;
@@ -101,7 +107,7 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
 // r is 0 on fixed DOFs (q comes unmasked from the matvec); partial
 // (r M^{-1} r, r r).  double2 over pairs of nodes of the owned planes (pads
 // are zero and stay zero).  Saves one read+write of u every second iteration.
-template <bool kU>
+template <bool kU, bool kMG>
 __global__ void __launch_bounds__(kBlock, 2)
 k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
          const double* __restrict__ pprev, const double* __restrict__ p, const double* __restrict__ q,
@@ -123,7 +129,7 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
       const long long j = j0 + w * stride;
       ok[w] = j < npair;
       const long long i = b0 + 2 * (ok[w] ? j : j0);
-      iv[w] = *reinterpret_cast<const double2*>(invd + i);
+      if (!kMG) iv[w] = *reinterpret_cast<const double2*>(invd + i);
       fm[w] = *reinterpret_cast<const uchar2*>(fixm + i);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -158,14 +164,14 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
         s0 = fma(rn.x, rn.x, s0);
         s1 = fma(rn.y, rn.y, s1);
       }
-      rz = fma(s0, iv[w].x, fma(s1, iv[w].y, rz));
+      if (!kMG) rz = fma(s0, iv[w].x, fma(s1, iv[w].y, rz));
       rr += s0 + s1;
     }
   }
   __shared__ double tot[2];
   double v[2] = {rz, rr};
   if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
-    if (finish) cg_finish_update(st, tot[0], tot[1], kU ? 0 : 1);
+    if (finish) cg_finish_update<kMG>(st, tot[0], tot[1], kU ? 0 : 1);
     else { st->sums[0] = tot[0]; st->sums[1] = tot[1]; }
   }
 }

@@ -23,9 +23,12 @@
 // (z).  Every output node is written by exactly one thread; sums are in a
 // fixed order (deterministic).
 //
-// kFused: p_new = M^{-1} r + beta p_old is computed while loading (Jacobi
-// preconditioner + PCG direction update, A3/A4), written once by the owner,
-// and the matvec runs on p_new; p_old / p_new are ping-pong buffers.
+// kPre (PCG direction update fused into the load, A3/A4; p_new is written
+// once by the owner and the matvec runs on it; p_old / p_new are ping-pong):
+//   kPre = 0: plain q = K v
+//   kPre = 1: p_new = M^{-1} r + beta p_old   (Jacobi preconditioner, vin = r)
+//   kPre = 2: p_new = z + beta p_old          (z = V(r) from the multigrid
+//             preconditioner already in HBM, vin = z; no M^{-1} stream)
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
@@ -95,17 +98,20 @@ template <int TZ> struct MvSmem {
   static constexpr int I = (TZ + 1) * YW * 8;                     // one scalar node tile
   static constexpr int EB = TZ * YW * 8;                          // element tile (box width 34 as well)
   static constexpr int VA = (V + 127) / 128 * 128, IA = (I + 127) / 128 * 128, EA = (EB + 127) / 128 * 128;
-  __host__ __device__ static constexpr int stage(bool fused) { return fused ? 2 * VA + IA + EA : VA + EA; }
+  __host__ __device__ static constexpr int stage(int pre) { return pre == 1 ? 2 * VA + IA + EA : pre == 2 ? 2 * VA + EA : VA + EA; }
+  // offset of the element tile inside a stage
+  __host__ __device__ static constexpr int eoff(int pre) { return pre == 1 ? 2 * VA + IA : pre == 2 ? 2 * VA : VA; }
   // raw stages + 3 rotating p-planes (pre-pass output) + alignment slack
-  __host__ __device__ static constexpr int bytes(bool fused) { return kMvStages * stage(fused) + 3 * VA + 128; }
+  __host__ __device__ static constexpr int bytes(int pre) { return kMvStages * stage(pre) + 3 * VA + 128; }
 };
 
-template <int TZ, bool kFused, bool kDot>
+template <int TZ, int kPre, bool kDot>
 __global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? 2 : 1))
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
          double* __restrict__ pnew, double* __restrict__ q,
          double* partials, unsigned int* counter, int finish) {
   if (gate && st->done) return;
+  constexpr bool kFused = kPre != 0;
   using L = MvSmem<TZ>;
   const double beta = (kFused && !st->fresh) ? st->beta : 0.0;
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -131,8 +137,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   // running output pointers at the base node (advanced by nplane per step)
   double* qp = q + (size_t)(xs - g.ex0 + 1) * nplane + ob;
 
-  auto slot = [&](int s) { return dsm + s * L::stage(kFused); };
-  double* pbuf = reinterpret_cast<double*>(dsm + kMvStages * L::stage(kFused));   // [3][3][TZ+1][YW]
+  auto slot = [&](int s) { return dsm + s * L::stage(kPre); };
+  double* pbuf = reinterpret_cast<double*>(dsm + kMvStages * L::stage(kPre));   // [3][3][TZ+1][YW]
   constexpr int PB = L::VA / 8;                                                      // doubles per p-plane
   constexpr int CS = (TZ + 1) * L::YW;                                               // component stride
   auto issue = [&](int t) {                 // unit t: node plane j = xs-1+t, element plane j-1
@@ -140,19 +146,18 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     unsigned char* b = slot(s);
     const int j = xs - 1 + t;
     const int ixl = j - g.ex0 + 1;
-    const uint32_t bytes = (kFused ? 2 * L::V + L::I : L::V) + (t > 0 ? L::EB : 0);
+    const uint32_t bytes = (kPre == 1 ? 2 * L::V + L::I : kPre == 2 ? 2 * L::V : L::V) + (t > 0 ? L::EB : 0);
     mbar_arrive_expect_tx(&full[s], bytes);
     tma_load_4d(b, &maps.vin, &full[s], yb, z0, ixl, 0);
-    if (kFused) {
-      tma_load_4d(b + L::VA, &maps.pold, &full[s], yb, z0, ixl, 0);
-      tma_load_3d(b + 2 * L::VA, &maps.invd, &full[s], yb, z0, ixl);
-    }
-    if (t > 0) tma_load_3d(b + (kFused ? 2 * L::VA + L::IA : L::VA), &maps.E, &full[s], yb, z0, j - 1 - g.ex0 + g.H);
+    if (kFused) tma_load_4d(b + L::VA, &maps.pold, &full[s], yb, z0, ixl, 0);
+    if (kPre == 1) tma_load_3d(b + 2 * L::VA, &maps.invd, &full[s], yb, z0, ixl);
+    if (t > 0) tma_load_3d(b + L::eoff(kPre), &maps.E, &full[s], yb, z0, j - 1 - g.ex0 + g.H);
   };
   if (leader) {
     tma_prefetch_desc(&maps.vin);
     tma_prefetch_desc(&maps.E);
-    if (kFused) { tma_prefetch_desc(&maps.pold); tma_prefetch_desc(&maps.invd); }
+    if (kFused) tma_prefetch_desc(&maps.pold);
+    if (kPre == 1) tma_prefetch_desc(&maps.invd);
     for (int s = 0; s < kMvStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
@@ -191,7 +196,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     const double* sv = reinterpret_cast<const double*>(slot(s));
     const double* sp = reinterpret_cast<const double*>(slot(s) + L::VA);
     const double* si = reinterpret_cast<const double*>(slot(s) + 2 * L::VA);
-    const double* se = reinterpret_cast<const double*>(slot(s) + (kFused ? 2 * L::VA + L::IA : L::VA));
+    const double* se = reinterpret_cast<const double*>(slot(s) + L::eoff(kPre));
     double* pb = pbuf + (t % 3) * PB;
     const bool wr_plane = kFused && ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
     double* pplane = pnew + (size_t)(xs + t - g.ex0) * nplane;     // node plane j = xs-1+t
@@ -200,10 +205,13 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       const int n = pn_idx[u];
       if (n < 0) continue;
       double v[3];
-      if (kFused) {
+      if (kPre == 1) {
         const double iv = si[n];
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], iv * sv[c * CS + n]);
+      } else if (kPre == 2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], sv[c * CS + n]);
       } else {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];

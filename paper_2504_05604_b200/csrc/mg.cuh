@@ -1,0 +1,511 @@
+// Geometric multigrid preconditioner kernels (DESIGN.md
+// readings M1-M6).  fp64, deterministic (every output written by one thread,
+// fixed summation order; no atomics).
+//
+// Level 0 is the fine slab (W = 1, layout of common.cuh); levels l >= 1 use the
+// same padded node layout: node (ix,iy,iz) at ((ix+1)*NZ + iz+1)*NY + iy+1,
+// components SoA with stride ncomp, zero pads / ghost planes.  Element
+// matrices of stored levels are SoA: K[(r*24 + s) * nel + e], e = (ex*nz +
+// ez)*ny + ey, r,s local DOFs in SPEC S:45 corner order.
+//
+// Transfer (M2): P = trilinear interpolation, per axis fine node 2j <- coarse j,
+// 2j+1 <- (j, j+1) with weights 1/2; restriction = P^T.  Coarse operators
+// (M3): Galerkin P^T K P.  Smoother (M5): damped Jacobi.  Coarsest (M6):
+// explicit inverse by Gauss-Jordan (SPD, no pivoting), applied as a dense
+// matvec.
+#pragma once
+#include "common.cuh"
+
+namespace topo {
+
+struct LvGeo {
+  int nx, ny, nz;         // elements per axis
+  int NY;                 // y pitch (nodes)
+  long long nplane;       // NY * NZ
+  long long ncomp;        // component stride
+  __host__ __device__ long long n(int ix, int iy, int iz) const {
+    return (long long)(ix + 1) * nplane + (long long)(iz + 1) * NY + (iy + 1);
+  }
+  __host__ __device__ long long nodes() const { return (long long)(nx + 1) * (ny + 1) * (nz + 1); }
+  __host__ __device__ long long nel() const { return (long long)nx * ny * nz; }
+};
+
+// node k of the (nx+1)(ny+1)(nz+1) enumeration, iy fastest (coalesced)
+__device__ __forceinline__ void lv_decode(const LvGeo& L, long long k, int& ix, int& iy, int& iz) {
+  iy = (int)(k % (L.ny + 1));
+  const long long t = k / (L.ny + 1);
+  iz = (int)(t % (L.nz + 1));
+  ix = (int)(t / (L.nz + 1));
+}
+
+__constant__ double c_mg_diag8[8 * 24];       // diag of M_c (level-1 Galerkin from fine E)
+__constant__ signed char c_mg_nzA[8][8][8];   // child c, parent corner R -> child corners A with w != 0
+__constant__ double c_mg_nzW[8][8][8];
+__constant__ int c_mg_nzN[8][8];
+
+__host__ __device__ constexpr int mg_lidx(int a, int b, int c) { return 4 * c + (b ? (a ? 2 : 3) : (a ? 1 : 0)); }
+__device__ __forceinline__ int corner_dx(int a) { return (a == 1 || a == 2 || a == 5 || a == 6) ? 1 : 0; }
+__device__ __forceinline__ int corner_dy(int a) { return (a == 2 || a == 3 || a == 6 || a == 7) ? 1 : 0; }
+__device__ __forceinline__ int corner_dz(int a) { return a >= 4 ? 1 : 0; }
+
+#define MG_GATE(st) \
+  if ((st) && (st)->done) return;
+
+// ---------------------------------------------------------------------------
+// Restriction  bC = mask_C( P^T mask_F(v) ),  v = bF - qF (kResid) or bF.
+// Thread per coarse node; gathers the 3x3x3 fine neighbourhood of node 2j.
+// ---------------------------------------------------------------------------
+template <bool kResid>
+__global__ void __launch_bounds__(kBlock)
+k_mg_restrict(LvGeo F, LvGeo Cg, const double* __restrict__ bF, const double* __restrict__ qF,
+              const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, double* __restrict__ bC,
+              const DevState* st) {
+  MG_GATE(st);
+  const long long tot = Cg.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int jx, jy, jz;
+    lv_decode(Cg, k, jx, jy, jz);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int iz = 2 * jz + dz;
+      if (iz < 0 || iz > F.nz) continue;
+      const double wz = dz ? 0.5 : 1.0;
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int ix = 2 * jx + dx;
+        if (ix < 0 || ix > F.nx) continue;
+        const double wxz = wz * (dx ? 0.5 : 1.0);
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int iy = 2 * jy + dy;
+          if (iy < 0 || iy > F.ny) continue;
+          const double w = wxz * (dy ? 0.5 : 1.0);
+          const long long i = F.n(ix, iy, iz);
+          const uint8_t fm = fixF[i];
+          double v0 = bF[i], v1 = bF[i + F.ncomp], v2 = bF[i + 2 * F.ncomp];
+          if (kResid) {
+            v0 -= qF[i];
+            v1 -= qF[i + F.ncomp];
+            v2 -= qF[i + 2 * F.ncomp];
+          }
+          if (!(fm & 1)) s0 = fma(w, v0, s0);
+          if (!(fm & 2)) s1 = fma(w, v1, s1);
+          if (!(fm & 4)) s2 = fma(w, v2, s2);
+        }
+      }
+    }
+    const long long j = Cg.n(jx, jy, jz);
+    const uint8_t fc = fixC[j];
+    bC[j] = (fc & 1) ? 0.0 : s0;
+    bC[j + Cg.ncomp] = (fc & 2) ? 0.0 : s1;
+    bC[j + 2 * Cg.ncomp] = (fc & 4) ? 0.0 : s2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Prolongation  xF (+)= mask_F( P eC ).  Thread per fine node (<= 8 sources).
+// ---------------------------------------------------------------------------
+template <bool kAdd>
+__global__ void __launch_bounds__(kBlock)
+k_mg_prolong(LvGeo F, LvGeo Cg, const double* __restrict__ eC, const uint8_t* __restrict__ fixF,
+             double* __restrict__ xF, const DevState* st) {
+  MG_GATE(st);
+  const long long tot = F.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(F, k, ix, iy, iz);
+    const int jx = ix >> 1, jy = iy >> 1, jz = iz >> 1;
+    const int nx = (ix & 1) + 1, ny = (iy & 1) + 1, nz = (iz & 1) + 1;
+    const double w = (nx == 2 ? 0.5 : 1.0) * (ny == 2 ? 0.5 : 1.0) * (nz == 2 ? 0.5 : 1.0);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int a = 0; a < nz; ++a)
+      for (int b = 0; b < nx; ++b)
+        for (int c = 0; c < ny; ++c) {
+          const long long j = Cg.n(jx + b, jy + c, jz + a);
+          s0 += eC[j];
+          s1 += eC[j + Cg.ncomp];
+          s2 += eC[j + 2 * Cg.ncomp];
+        }
+    const long long i = F.n(ix, iy, iz);
+    const uint8_t fm = fixF[i];
+    const double v[3] = {(fm & 1) ? 0.0 : w * s0, (fm & 2) ? 0.0 : w * s1, (fm & 4) ? 0.0 : w * s2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long o = i + c * F.ncomp;
+      xF[o] = kAdd ? xF[o] + v[c] : v[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Damped Jacobi (M5) on one level.  q = A x comes from the operator kernel
+// (unmasked at level 0, masked at coarse levels; masking happens here).
+// The weight w_l = theta / lam_l lives in device memory (set by the setup's
+// power steps, k_mg_rayleigh).
+//   MODE 0: x = w D^-1 b                      (first sweep from x = 0)
+//   MODE 1: x = x + w D^-1 (b - q)
+//   MODE 2: MODE 1 and rho = b . x_new (PCG: b = r, x = z = V(r)); the last
+//           block sets beta = rho / rho_old (0 on a fresh start), rz = rho.
+// kNodeD: D^-1 is one scalar per node (level 0: KE_ii constant), else per DOF.
+// ---------------------------------------------------------------------------
+template <int MODE, bool kNodeD>
+__global__ void __launch_bounds__(kBlock)
+k_mg_jacobi(LvGeo L, const double* __restrict__ b, const double* __restrict__ q,
+            const double* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
+            double* __restrict__ x, DevState* st, int gate, double* partials, unsigned int* counter) {
+  if (gate && st->done) return;
+  const double omega = *omp;
+  const long long tot = L.nodes();
+  double dot = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+    const double dn = kNodeD ? invd[i] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long o = i + c * L.ncomp;
+      const double d = kNodeD ? dn : invd[o];
+      const double bv = b[o];
+      double xn;
+      if ((fm >> c) & 1) xn = 0.0;
+      else if (MODE == 0) xn = omega * d * bv;
+      else xn = fma(omega * d, bv - q[o], x[o]);
+      x[o] = xn;
+      if (MODE == 2) dot = fma(bv, xn, dot);
+    }
+  }
+  if (MODE == 2) {
+    __shared__ double tot_sh[1];
+    double v[1] = {dot};
+    if (grid_reduce<1>(v, partials, counter, tot_sh) && threadIdx.x == 0) {
+      const double rho = tot_sh[0];
+      if (!(rho > 0.0) || !isfinite(rho)) {
+        st->status = 3;
+        st->done = 1;
+      } else {
+        st->beta = st->fresh ? 0.0 : rho / st->rz;
+        st->rz = rho;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Smoother weights (M5): power steps v <- D^-1 A v from a fixed start vector,
+// then w_l = theta (v^T D v) / (v^T A v) = theta / lam_l.
+// Start vector: DOF k of the level's external numbering (3 n + c) gets
+// 2 u - 1, u = (splitmix64(k) >> 11) 2^-53; 0 on fixed DOFs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double mg_hash_unit(unsigned long long k) {
+  unsigned long long z = k + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, double* __restrict__ v) {
+  const long long tot = L.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    const unsigned long long ext = ((unsigned long long)iz * (L.nx + 1) + ix) * (L.ny + 1) + iy;
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : mg_hash_unit(3 * ext + c);
+  }
+}
+
+template <bool kNodeD>
+__global__ void __launch_bounds__(kBlock)
+k_mg_rayleigh(LvGeo L, const double* __restrict__ v, const double* __restrict__ t, const double* __restrict__ invd,
+              const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out, double* partials,
+              unsigned int* counter) {
+  const long long tot = L.nodes();
+  double vt = 0.0, vdv = 0.0;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if ((fm >> c) & 1) continue;
+      const long long o = i + c * L.ncomp;
+      const double vv = v[o];
+      vt = fma(vv, t[o], vt);
+      vdv = fma(vv * vv, 1.0 / (kNodeD ? invd[i] : invd[o]), vdv);
+    }
+  }
+  __shared__ double tot_sh[2];
+  double r[2] = {vt, vdv};
+  if (grid_reduce<2>(r, partials, counter, tot_sh) && threadIdx.x == 0) *om_out = theta * tot_sh[1] / tot_sh[0];
+}
+
+// ---------------------------------------------------------------------------
+// Stored-level operator q = mask(A x) (node-centric gather over the <= 8
+// elements of each node; each element matrix is read once in total).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const double* __restrict__ x,
+               const uint8_t* __restrict__ fix, double* __restrict__ q, const DevState* st) {
+  MG_GATE(st);
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy) {
+          const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+          if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+          const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+          const int a = mg_lidx(1 - dx, 1 - dy, 1 - dz);
+          double xe[24];
+#pragma unroll
+          for (int bb = 0; bb < 8; ++bb) {
+            const long long n = L.n(ex + corner_dx(bb), ey + corner_dy(bb), ez + corner_dz(bb));
+#pragma unroll
+            for (int c = 0; c < 3; ++c) xe[3 * bb + c] = x[n + c * L.ncomp];
+          }
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const double* row = K + (long long)((3 * a + i) * 24) * nel + e;
+            double s = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < 24; ++cc) s = fma(row[(long long)cc * nel], xe[cc], s);
+            acc[i] += s;
+          }
+        }
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) q[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : acc[c];
+  }
+}
+
+// Inverse diagonal of a stored level (0 on fixed DOFs).
+__global__ void __launch_bounds__(kBlock)
+k_mg_diag_asm(LvGeo L, const double* __restrict__ K, const uint8_t* __restrict__ fix, double* __restrict__ invd) {
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy) {
+          const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+          if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+          const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+          const int a = mg_lidx(1 - dx, 1 - dy, 1 - dz);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[c] += K[(long long)((3 * a + c) * 25) * nel + e];
+        }
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : 1.0 / acc[c];
+  }
+}
+
+// Inverse diagonal of level 1 straight from the fine moduli (level 1 applied
+// matrix-free as P^T K P): diag = sum_e sum_c E_c diag(M_c).
+__global__ void __launch_bounds__(kBlock)
+k_mg_diag_l1(Geo g, LvGeo L, const double* __restrict__ E, const uint8_t* __restrict__ fix,
+             double* __restrict__ invd) {
+  const long long tot = L.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy) {
+          const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+          if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+          const int a = mg_lidx(1 - dx, 1 - dy, 1 - dz);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int fx = 2 * ex + (c & 1), fy = 2 * ey + ((c >> 1) & 1), fz = 2 * ez + (c >> 2);
+            if (fx >= g.nelx || fy >= g.nely || fz >= g.nelz) continue;
+            const double Ef = E[elem_idx(g, fx, fy, fz)];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) acc[i] = fma(Ef, c_mg_diag8[24 * c + 3 * a + i], acc[i]);
+          }
+        }
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : 1.0 / acc[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Element matrices of level log2(S) straight from the fine moduli:
+//   K_e[k] = sum_f E_f tab[f][k],  f = fx + S fy + S^2 fz over the S^3 fine
+// elements of e (E = 0 outside the fine domain).  Thread per element; the
+// table is staged through shared memory in chunks of kCh entries.
+// ---------------------------------------------------------------------------
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __restrict__ tab,
+              double* __restrict__ K) {
+  constexpr int NT = S * S * S, kCh = 32;
+  __shared__ double tb[NT][kCh];
+  const long long nel = L.nel();
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double Ef[NT];
+  if (e < nel) {
+    const int ey = (int)(e % L.ny);
+    const long long t = e / L.ny;
+    const int ez = (int)(t % L.nz), ex = (int)(t / L.nz);
+#pragma unroll
+    for (int f = 0; f < NT; ++f) {
+      const int fx = S * ex + f % S, fy = S * ey + (f / S) % S, fz = S * ez + f / (S * S);
+      Ef[f] = (fx < g.nelx && fy < g.nely && fz < g.nelz) ? E[elem_idx(g, fx, fy, fz)] : 0.0;
+    }
+  }
+  for (int k0 = 0; k0 < 576; k0 += kCh) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < NT * kCh; t += blockDim.x) tb[t / kCh][t % kCh] = tab[(t / kCh) * 576 + k0 + t % kCh];
+    __syncthreads();
+    if (e < nel) {
+      for (int kk = 0; kk < kCh; ++kk) {
+        double s = 0.0;
+#pragma unroll
+        for (int f = 0; f < NT; ++f) s = fma(Ef[f], tb[f][kk], s);
+        K[(long long)(k0 + kk) * nel + e] = s;
+      }
+    }
+  }
+}
+
+// Element matrices of level l+1 from the stored level l (Galerkin per child):
+//   KC_e[3R+i][3S+j] = sum_c sum_{A,B} w[c][A][R] KF_child(c)[3A+i][3B+j] w[c][B][S]
+// Thread per (entry, coarse element), element fastest.
+__global__ void __launch_bounds__(kBlock)
+k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __restrict__ KC) {
+  const long long nelC = Cg.nel(), nelF = F.nel();
+  const long long tot = 576 * nelC;
+  for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < tot;
+       id += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(id / nelC);
+    const long long e = id - (long long)k * nelC;
+    const int r = k / 24, s = k % 24, R = r / 3, i = r % 3, Sn = s / 3, j = s % 3;
+    const int ey = (int)(e % Cg.ny);
+    const long long t = e / Cg.ny;
+    const int ez = (int)(t % Cg.nz), ex = (int)(t / Cg.nz);
+    double acc = 0.0;
+    for (int c = 0; c < 8; ++c) {
+      const int fx = 2 * ex + (c & 1), fy = 2 * ey + ((c >> 1) & 1), fz = 2 * ez + (c >> 2);
+      if (fx >= F.nx || fy >= F.ny || fz >= F.nz) continue;
+      const long long fe = ((long long)fx * F.nz + fz) * F.ny + fy;
+      const int na = c_mg_nzN[c][R], nb = c_mg_nzN[c][Sn];
+      for (int ia = 0; ia < na; ++ia) {
+        const int A = c_mg_nzA[c][R][ia];
+        const double wa = c_mg_nzW[c][R][ia];
+        double sb = 0.0;
+        for (int ib = 0; ib < nb; ++ib) {
+          const int B = c_mg_nzA[c][Sn][ib];
+          sb = fma(c_mg_nzW[c][Sn][ib], KF[(long long)((3 * A + i) * 24 + 3 * B + j) * nelF + fe], sb);
+        }
+        acc = fma(wa, sb, acc);
+      }
+    }
+    KC[id] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarsest level (M6): dense matrix over free DOFs, Gauss-Jordan inverse,
+// dense solve.
+// ---------------------------------------------------------------------------
+// dmap[level idx of DOF] = dense index or -1 (fixed / pad).  Thread per node:
+// it owns (zeroes and fills) its rows; no atomics.
+__global__ void __launch_bounds__(kBlock)
+k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ dmap, int n,
+                double* __restrict__ A) {
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    int rows[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      rows[c] = dmap[i + c * L.ncomp];
+      if (rows[c] >= 0)
+        for (int j = 0; j < n; ++j) A[(long long)rows[c] * n + j] = 0.0;
+    }
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy) {
+          const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+          if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+          const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+          const int a = mg_lidx(1 - dx, 1 - dy, 1 - dz);
+          for (int bb = 0; bb < 8; ++bb) {
+            const long long nb = L.n(ex + corner_dx(bb), ey + corner_dy(bb), ez + corner_dz(bb));
+            for (int cj = 0; cj < 3; ++cj) {
+              const int col = dmap[nb + cj * L.ncomp];
+              if (col < 0) continue;
+#pragma unroll
+              for (int ci = 0; ci < 3; ++ci)
+                if (rows[ci] >= 0)
+                  A[(long long)rows[ci] * n + col] += K[(long long)((3 * a + ci) * 24 + 3 * bb + cj) * nel + e];
+            }
+          }
+        }
+  }
+}
+
+// One Gauss-Jordan pivot step (in place on SPD, no pivoting), ping-pong:
+//   out_kk = 1/p, out_kj = a_kj/p, out_ik = -a_ik/p, out_ij = a_ij - a_ik a_kj / p.
+// After steps k = 0..n-1 the buffer holds A^-1.
+__global__ void __launch_bounds__(kBlock)
+k_mg_gj_step(const double* __restrict__ a, double* __restrict__ o, int n, int k) {
+  const long long tot = (long long)n * n;
+  const double p = a[(long long)k * n + k], ip = 1.0 / p;
+  for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < tot;
+       id += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(id / n), j = (int)(id - (long long)i * n);
+    double v;
+    if (i == k && j == k) v = ip;
+    else if (i == k) v = a[id] * ip;
+    else if (j == k) v = -a[id] * ip;
+    else v = a[id] - a[(long long)i * n + k] * a[(long long)k * n + j] * ip;
+    o[id] = v;
+  }
+}
+
+// x[imap[r]] = sum_j Ainv[r][j] b[imap[j]]  (warp per row, fixed lane order)
+__global__ void __launch_bounds__(kBlock)
+k_mg_coarse_solve(const double* __restrict__ Ainv, int n, const long long* __restrict__ imap,
+                  const double* __restrict__ b, double* __restrict__ x, const DevState* st) {
+  MG_GATE(st);
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < n; r += nwarp) {
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(Ainv[(long long)r * n + j], b[imap[j]], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[imap[r]] = s;
+  }
+}
+
+}  // namespace topo

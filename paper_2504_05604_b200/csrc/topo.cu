@@ -18,10 +18,13 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "matvec_wht.cuh"
+#include "mg.cuh"
 
 namespace topo {
 void build_element_stiffness(double nu, double* ke);  // ke_host.cpp
 bool wht_constants(const double* ke, double out[8], double tol);
+void mg_child_weights(double w[8][8][8]);            // mg_host.cpp
+void mg_galerkin_tables(const double* ke, double* tab8, double* tab64, double* diag8);
 }
 using namespace topo;
 
@@ -84,7 +87,7 @@ struct Slab {
   Geo g{};
   // node vectors: 3*ncomp doubles each (SoA)
   double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
-         *w = nullptr;
+         *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
   double* invd = nullptr;    // per node (1 component): 1/(kd sum E)
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
@@ -98,7 +101,17 @@ struct Slab {
   size_t stage_n = 0;
   double *u_b = nullptr, *x_b = nullptr, *xphys_b = nullptr;   // snapshot buffers
   // TMA descriptors of the matvec operands (built at init; pointers never change)
-  CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E;
+  CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z;
+};
+
+// One coarse multigrid level (l >= 1, M1-M6).
+struct MgLevel {
+  LvGeo L{};
+  double *x = nullptr, *b = nullptr, *t = nullptr, *invd = nullptr;   // 3*ncomp each
+  double* K = nullptr;          // stored element matrices [576][nel] (stored levels)
+  uint8_t* fixm = nullptr;      // per node: bit c = DOF c fixed
+  std::vector<uint8_t> hfix;    // host copy, external node order
+  bool stored = false;
 };
 
 struct topo_ctx {
@@ -121,10 +134,10 @@ struct topo_ctx {
   // pinned mirror of slab 0's DevState
   DevState* hstate = nullptr;
   // CUDA graphs (PCG batch, OC batch)
-  cudaGraphExec_t cg_exec = nullptr;
+  cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};   // PCG batch graphs: [0] Jacobi, [1] multigrid
   int cg_batch = 0;
-  long long cg_batch_launches = 0;
-  bool cg_profiled_graph = false;
+  long long cg_batch_launches[2] = {0, 0};
+  bool cg_profiled_graph[2] = {false, false};
   cudaGraphExec_t oc_exec = nullptr;
   int oc_batch = 16;
   long long oc_batch_launches = 0;
@@ -142,6 +155,18 @@ struct topo_ctx {
   bool debug = false;        // TOPO_DEBUG_SYNC=1: no graphs, sync + check after every kernel
   bool snap_has_u = false, has_snap = false;
   int sticky = TOPO_OK;
+  // geometric multigrid (level 0 = the fine slab; mg[0] unused)
+  bool mg_on = false, mg_ready = false;
+  std::vector<MgLevel> mg;
+  double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr, *mg_A1 = nullptr;
+  double mg_diag8[8 * 24];
+  int mg_n = 0;                      // free DOFs of the coarsest level
+  int* mg_dmap = nullptr;            // coarsest: level DOF index -> dense index or -1
+  long long* mg_imap = nullptr;      // coarsest: dense index -> level DOF index
+  double* mg_om = nullptr;           // [17]: smoother weight per level; [16] = 1.0
+  cudaGraphExec_t mg_setup_exec = nullptr;
+  long long mg_setup_launches = 0;
+  int mg_batch = 2;
 };
 
 namespace {
@@ -210,6 +235,26 @@ int ensure_constants(topo_ctx* ctx) {
   if (g_const_owner == ctx) return TOPO_OK;
   CU(cudaMemcpyToSymbolAsync(c_KE, ctx->ke, sizeof(double) * 576, 0, cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaMemcpyToSymbolAsync(c_wht, &ctx->wht, sizeof(WhtK), 0, cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->mg_on) {
+    double w[8][8][8];
+    mg_child_weights(w);
+    signed char nzA[8][8][8] = {};
+    double nzW[8][8][8] = {};
+    int nzN[8][8] = {};
+    for (int c = 0; c < 8; ++c)
+      for (int R = 0; R < 8; ++R)
+        for (int A = 0; A < 8; ++A)
+          if (w[c][A][R] != 0.0) {
+            nzA[c][R][nzN[c][R]] = (signed char)A;
+            nzW[c][R][nzN[c][R]] = w[c][A][R];
+            nzN[c][R]++;
+          }
+    CU(cudaMemcpyToSymbolAsync(c_mg_diag8, ctx->mg_diag8, sizeof(ctx->mg_diag8), 0, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyToSymbolAsync(c_mg_nzA, nzA, sizeof nzA, 0, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyToSymbolAsync(c_mg_nzW, nzW, sizeof nzW, 0, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyToSymbolAsync(c_mg_nzN, nzN, sizeof nzN, 0, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));   // host staging arrays go out of scope
+  }
   if (!ctx->st_off.empty()) {
     CU(cudaMemcpyToSymbolAsync(c_st_off, ctx->st_off.data(), sizeof(int4) * ctx->st_off.size(), 0,
                                cudaMemcpyHostToDevice, ctx->stream));
@@ -486,6 +531,7 @@ int update_modulus(topo_ctx* ctx) {
   }
   CK(check_launch(ctx));
   ctx->has_E = true;
+  ctx->mg_ready = false;
   return TOPO_OK;
 }
 
@@ -548,26 +594,27 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   CK(map_nodes(ctx, &s.m_p1, s.p1, s.g, 3));
   CK(map_nodes(ctx, &s.m_invd, s.invd, s.g, 1));
   CK(map_elems(ctx, &s.m_E, s.E, s.g));
+  CK(map_nodes(ctx, &s.m_z, s.z, s.g, 3));
   return TOPO_OK;
 }
 
-template <int TZ, bool kFused, bool kDot>
+template <int TZ, int kPre, bool kDot>
 int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish) {
   static bool attr_set = false;
-  const int smem = MvSmem<TZ>::bytes(kFused);
+  const int smem = MvSmem<TZ>::bytes(kPre);
   if (!attr_set) {
-    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kFused, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
-  k_mv_wht<TZ, kFused, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
-                                                                     s.partials, s.counter, finish);
+  k_mv_wht<TZ, kPre, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
+                                                                   s.partials, s.counter, finish);
   ctx->launches++;
-  debug_sync(ctx, kFused ? "k_mv_wht<fused>" : "k_mv_wht<plain>");
+  debug_sync(ctx, kPre == 1 ? "k_mv_wht<jacobi-fused>" : kPre == 2 ? "k_mv_wht<mg-fused>" : "k_mv_wht<plain>");
   return check_launch(ctx);
 }
 
-template <bool kFused, bool kDot>
+template <int kPre, bool kDot>
 int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CUtensorMap* pold, double* pnew,
               double* q, int finish) {
   MvMaps maps;
@@ -575,14 +622,14 @@ int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CU
   maps.pold = pold ? *pold : vin;
   maps.invd = s.m_invd;
   maps.E = s.m_E;
-  if (ctx->tz == 16) return launch_mv_t<16, kFused, kDot>(ctx, s, gate, maps, pnew, q, finish);
-  return launch_mv_t<8, kFused, kDot>(ctx, s, gate, maps, pnew, q, finish);
+  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot>(ctx, s, gate, maps, pnew, q, finish);
+  return launch_mv_t<8, kPre, kDot>(ctx, s, gate, maps, pnew, q, finish);
 }
 
 // q = K v for every slab (v ghosts exchanged first; v must be 0 on fixed DOFs)
 int matvec_all(topo_ctx* ctx, double* Slab::*pin, CUtensorMap Slab::*pmap, double* Slab::*qout) {
   CK(exchange_nodes(ctx, pin));
-  for (Slab& s : ctx->slabs) CK((launch_mv<false, false>(ctx, s, 0, s.*pmap, nullptr, nullptr, s.*qout, 0)));
+  for (Slab& s : ctx->slabs) CK((launch_mv<0, false>(ctx, s, 0, s.*pmap, nullptr, nullptr, s.*qout, 0)));
   return check_launch(ctx);
 }
 
@@ -605,7 +652,7 @@ int enqueue_cg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   for (Slab& s : ctx->slabs) {
     const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
     double* pnew = parity ? s.p0 : s.p1;
-    CK((launch_mv<true, true>(ctx, s, 1, s.m_r, pold, pnew, s.q, fin)));
+    CK((launch_mv<1, true>(ctx, s, 1, s.m_r, pold, pnew, s.q, fin)));
   }
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
   if (!fin) {
@@ -616,11 +663,11 @@ int enqueue_cg_iter(topo_ctx* ctx, bool prof_here, int parity) {
     double* pnew = parity ? s.p0 : s.p1;
     double* pprev = parity ? s.p1 : s.p0;
     if (parity)
-      LAUNCH(ctx, k_update<true>, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev, pnew,
-             s.q, s.invd, s.fixm, s.partials, s.counter, fin);
+      LAUNCH(ctx, (k_update<true, false>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
+             pnew, s.q, s.invd, s.fixm, s.partials, s.counter, fin);
     else
-      LAUNCH(ctx, k_update<false>, grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev, pnew,
-             s.q, s.invd, s.fixm, s.partials, s.counter, fin);
+      LAUNCH(ctx, (k_update<false, false>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
+             pnew, s.q, s.invd, s.fixm, s.partials, s.counter, fin);
   }
   if (!fin) {
     CK(allreduce(ctx, 0, 2, 0));
@@ -643,23 +690,390 @@ int flush_u(topo_ctx* ctx) {
   return sync_state(ctx);
 }
 
-int build_cg_graph(topo_ctx* ctx) {
-  if (ctx->cg_exec && ctx->cg_profiled_graph == ctx->profile) return TOPO_OK;
-  if (ctx->cg_exec) { cudaGraphExecDestroy(ctx->cg_exec); ctx->cg_exec = nullptr; }
+int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity);
+
+int build_cg_graph(topo_ctx* ctx, int mg) {
+  if (ctx->cg_exec[mg] && ctx->cg_profiled_graph[mg] == ctx->profile) return TOPO_OK;
+  if (ctx->cg_exec[mg]) { cudaGraphExecDestroy(ctx->cg_exec[mg]); ctx->cg_exec[mg] = nullptr; }
   cudaGraph_t graph;
   const long long l0 = ctx->launches;
   CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   int rc = TOPO_OK;
-  for (int i = 0; i < ctx->cg_batch && rc == TOPO_OK; ++i) rc = enqueue_cg_iter(ctx, ctx->profile && i == 0, i & 1);
+  const int nb = mg ? ctx->mg_batch : ctx->cg_batch;
+  for (int i = 0; i < nb && rc == TOPO_OK; ++i)
+    rc = mg ? enqueue_mg_iter(ctx, ctx->profile && i == 0, i & 1)
+            : enqueue_cg_iter(ctx, ctx->profile && i == 0, i & 1);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != TOPO_OK) return rc;
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "graph capture: %s", cudaGetErrorString(e));
-  e = cudaGraphInstantiate(&ctx->cg_exec, graph, 0);
+  e = cudaGraphInstantiate(&ctx->cg_exec[mg], graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
-  ctx->cg_batch_launches = ctx->launches - l0;
+  ctx->cg_batch_launches[mg] = ctx->launches - l0;
   ctx->launches = l0;
-  ctx->cg_profiled_graph = ctx->profile;
+  ctx->cg_profiled_graph[mg] = ctx->profile;
+  return TOPO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Geometric multigrid preconditioner (M1-M6).
+// Level 0 is the fine slab (W = 1); level 1 is applied matrix-free as
+// P^T K(E) P through the fine WHT matvec unless it is the coarsest level;
+// levels >= 2 (and a coarsest level 1) store Galerkin element matrices; the
+// coarsest level is solved with an explicit Gauss-Jordan inverse.
+// ---------------------------------------------------------------------------
+LvGeo lv0(const topo_ctx* ctx) {
+  const Geo& g = ctx->slabs[0].g;
+  return LvGeo{g.nelx, g.nely, g.nelz, g.NY, g.nplane, g.ncomp};
+}
+const LvGeo& lvg(const topo_ctx* ctx, int l) { return ctx->mg[l].L; }
+
+// Hierarchy on the host (init): dims, coarse Dirichlet masks (M4: the node at the
+// clamped position min(2j, n) decides), property Q, allocations, coarsest maps.
+int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
+  const topo_params& P = ctx->prm;
+  ctx->mg_on = false;
+  if (P.precond == TOPO_PRECOND_JACOBI) return TOPO_OK;
+  if (ctx->world != 1 || ctx->slabs.size() != 1) {
+    if (P.precond == TOPO_PRECOND_MG) return set_err(ctx, TOPO_EINVAL, "multigrid needs a single slab (world == 1)");
+    return TOPO_OK;
+  }
+  struct H { int nx, ny, nz; std::vector<uint8_t> fix; };
+  std::vector<H> hs;
+  {
+    H h{P.nelx, P.nely, P.nelz, {}};
+    const long long nn = (long long)(h.nx + 1) * (h.ny + 1) * (h.nz + 1);
+    h.fix.resize(nn);
+    for (long long n = 0; n < nn; ++n)
+      h.fix[n] = (fixed[3 * n] ? 1 : 0) | (fixed[3 * n + 1] ? 2 : 0) | (fixed[3 * n + 2] ? 4 : 0);
+    hs.push_back(std::move(h));
+  }
+  while (true) {
+    const H& f = hs.back();
+    if (3LL * (f.nx + 1) * (f.ny + 1) * (f.nz + 1) <= P.mg_coarse_max) break;
+    H c{(f.nx + 1) / 2, (f.ny + 1) / 2, (f.nz + 1) / 2, {}};
+    if (c.nx == f.nx && c.ny == f.ny && c.nz == f.nz) break;
+    auto fid = [&](int ix, int iy, int iz) { return (long long)iz * (f.nx + 1) * (f.ny + 1) + (long long)ix * (f.ny + 1) + iy; };
+    auto cid = [&](int ix, int iy, int iz) { return (long long)iz * (c.nx + 1) * (c.ny + 1) + (long long)ix * (c.ny + 1) + iy; };
+    c.fix.assign((size_t)(c.nx + 1) * (c.ny + 1) * (c.nz + 1), 0);
+    for (int jz = 0; jz <= c.nz; ++jz)
+      for (int jx = 0; jx <= c.nx; ++jx)
+        for (int jy = 0; jy <= c.ny; ++jy)
+          c.fix[cid(jx, jy, jz)] = f.fix[fid(std::min(2 * jx, f.nx), std::min(2 * jy, f.ny), std::min(2 * jz, f.nz))];
+    bool q_ok = true;   // property Q: fixed fine DOFs interpolate from fixed coarse DOFs only
+    for (int iz = 0; iz <= f.nz && q_ok; ++iz)
+      for (int ix = 0; ix <= f.nx && q_ok; ++ix)
+        for (int iy = 0; iy <= f.ny && q_ok; ++iy) {
+          const uint8_t m = f.fix[fid(ix, iy, iz)];
+          if (!m) continue;
+          for (int a = 0; a <= (iz & 1); ++a)
+            for (int b = 0; b <= (ix & 1); ++b)
+              for (int d = 0; d <= (iy & 1); ++d)
+                if (m & ~c.fix[cid((ix >> 1) + b, (iy >> 1) + d, (iz >> 1) + a)]) q_ok = false;
+        }
+    if (!q_ok) break;
+    hs.push_back(std::move(c));
+  }
+  const int L = (int)hs.size();
+  long long nfree_c = 0;
+  for (uint8_t m : hs.back().fix) nfree_c += 3 - __builtin_popcount(m & 7);
+  const char* why = L < 2 ? "fewer than 2 levels (grid too small, or coarse Dirichlet DOFs violate property Q)"
+                  : nfree_c > 4096 ? "coarsest level has more than 4096 free DOFs" : nullptr;
+  if (why) {
+    if (P.precond == TOPO_PRECOND_MG) return set_err(ctx, TOPO_EINVAL, "multigrid hierarchy: %s", why);
+    return TOPO_OK;
+  }
+  if (L > 16) return set_err(ctx, TOPO_EINVAL, "multigrid: more than 16 levels");
+  ctx->mg_on = true;
+  ctx->mg.resize(L);
+  auto al = [&](void** p, size_t bytes) -> int {
+    CU(cudaMalloc(p, bytes));
+    CU(cudaMemsetAsync(*p, 0, bytes, ctx->stream));
+    ctx->dev_bytes += bytes;
+    return TOPO_OK;
+  };
+  for (int l = 1; l < L; ++l) {
+    MgLevel& m = ctx->mg[l];
+    const H& h = hs[l];
+    m.L = LvGeo{h.nx, h.ny, h.nz, h.ny + 3, (long long)(h.ny + 3) * (h.nz + 3), 0};
+    m.L.ncomp = (long long)(h.nx + 3) * m.L.nplane;
+    m.hfix = h.fix;
+    m.stored = (l >= 2) || (L == 2);
+    CK(al((void**)&m.x, sizeof(double) * 3 * m.L.ncomp));
+    CK(al((void**)&m.b, sizeof(double) * 3 * m.L.ncomp));
+    CK(al((void**)&m.t, sizeof(double) * 3 * m.L.ncomp));
+    CK(al((void**)&m.invd, sizeof(double) * 3 * m.L.ncomp));
+    CK(al((void**)&m.fixm, m.L.ncomp));
+    if (m.stored) CK(al((void**)&m.K, sizeof(double) * 576 * m.L.nel()));
+    std::vector<uint8_t> lay(m.L.ncomp, 0);
+    for (int iz = 0; iz <= h.nz; ++iz)
+      for (int ix = 0; ix <= h.nx; ++ix)
+        for (int iy = 0; iy <= h.ny; ++iy)
+          lay[m.L.n(ix, iy, iz)] = h.fix[(long long)iz * (h.nx + 1) * (h.ny + 1) + (long long)ix * (h.ny + 1) + iy];
+    CU(cudaMemcpy(m.fixm, lay.data(), m.L.ncomp, cudaMemcpyHostToDevice));
+  }
+  // coarsest dense maps
+  {
+    const MgLevel& m = ctx->mg[L - 1];
+    const H& h = hs[L - 1];
+    std::vector<int> dmap(3 * m.L.ncomp, -1);
+    std::vector<long long> imap;
+    for (int iz = 0; iz <= h.nz; ++iz)
+      for (int ix = 0; ix <= h.nx; ++ix)
+        for (int iy = 0; iy <= h.ny; ++iy) {
+          const uint8_t fm = h.fix[(long long)iz * (h.nx + 1) * (h.ny + 1) + (long long)ix * (h.ny + 1) + iy];
+          for (int c = 0; c < 3; ++c) {
+            if ((fm >> c) & 1) continue;
+            const long long li = m.L.n(ix, iy, iz) + c * m.L.ncomp;
+            dmap[li] = (int)imap.size();
+            imap.push_back(li);
+          }
+        }
+    ctx->mg_n = (int)imap.size();
+    CK(al((void**)&ctx->mg_dmap, sizeof(int) * dmap.size()));
+    CK(al((void**)&ctx->mg_imap, sizeof(long long) * std::max<size_t>(1, imap.size())));
+    CU(cudaMemcpy(ctx->mg_dmap, dmap.data(), sizeof(int) * dmap.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->mg_imap, imap.data(), sizeof(long long) * imap.size(), cudaMemcpyHostToDevice));
+    const size_t nn = (size_t)ctx->mg_n * ctx->mg_n;
+    CK(al((void**)&ctx->mg_A0, sizeof(double) * std::max<size_t>(1, nn)));
+    CK(al((void**)&ctx->mg_A1, sizeof(double) * std::max<size_t>(1, nn)));
+  }
+  {
+    std::vector<double> om(17, 1.0);
+    CK(al((void**)&ctx->mg_om, sizeof(double) * 17));
+    CU(cudaMemcpy(ctx->mg_om, om.data(), sizeof(double) * 17, cudaMemcpyHostToDevice));
+  }
+  // Galerkin tables
+  {
+    std::vector<double> t8(8 * 576), t64(64 * 576);
+    mg_galerkin_tables(ctx->ke, t8.data(), t64.data(), ctx->mg_diag8);
+    CK(al((void**)&ctx->mg_tab8, sizeof(double) * t8.size()));
+    CK(al((void**)&ctx->mg_tab64, sizeof(double) * t64.size()));
+    CU(cudaMemcpy(ctx->mg_tab8, t8.data(), sizeof(double) * t8.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->mg_tab64, t64.data(), sizeof(double) * t64.size(), cudaMemcpyHostToDevice));
+  }
+  {
+    const long long ndof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+    int b = P.cg_check_every > 0 ? P.cg_check_every : (int)std::min<long long>(16, std::max<long long>(2, 4000000LL / ndof));
+    ctx->mg_batch = (b + 1) / 2 * 2;
+  }
+  return TOPO_OK;
+}
+
+constexpr int kMgPowerSteps = 8;   // power steps of the smoother-weight estimate (M5)
+int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin);
+int mg_apply(topo_ctx* ctx, int l, int gate);
+
+double* mg_Ainv(const topo_ctx* ctx) { return (ctx->mg_n % 2 == 0) ? ctx->mg_A0 : ctx->mg_A1; }
+
+// Per-design setup: level-1 diagonal, Galerkin element matrices, coarsest inverse.
+int enqueue_mg_setup(topo_ctx* ctx) {
+  Slab& s = ctx->slabs[0];
+  const int L = (int)ctx->mg.size();
+  for (int l = 1; l < L; ++l) {
+    MgLevel& m = ctx->mg[l];
+    const long long nn = m.L.nodes(), ne = m.L.nel();
+    if (l == 1 && !m.stored) {
+      LAUNCH(ctx, k_mg_diag_l1, grid_for(nn), s.g, m.L, s.E, m.fixm, m.invd);
+      continue;
+    }
+    if (l == 1) {
+      k_mg_asm_fine<2><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(s.g, m.L, s.E, ctx->mg_tab8, m.K);
+      ctx->launches++;
+    } else if (l == 2 && !ctx->mg[1].stored) {
+      k_mg_asm_fine<4><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(s.g, m.L, s.E, ctx->mg_tab64, m.K);
+      ctx->launches++;
+    } else {
+      const MgLevel& f = ctx->mg[l - 1];
+      LAUNCH(ctx, k_mg_asm_galerkin, grid_for(576 * ne), f.L, f.K, m.L, m.K);
+    }
+    debug_sync(ctx, "k_mg_asm");
+    LAUNCH(ctx, k_mg_diag_asm, grid_for(nn), m.L, m.K, m.fixm, m.invd);
+  }
+  // smoother weights w_l = theta / lam_l (M5): kMgPowerSteps power steps per level
+  const double* one = ctx->mg_om + 16;
+  for (int l = 0; l < L - 1; ++l) {
+    if (l == 0) {
+      const LvGeo F = lv0(ctx);
+      const int gF = grid_for(F.nodes());
+      LAUNCH(ctx, k_mg_start_vec, gF, F, s.fixm, s.z);
+      for (int k = 0; k < kMgPowerSteps; ++k) {
+        CK(mg_mv0(ctx, 0, s.m_z));
+        LAUNCH(ctx, (k_mg_jacobi<0, true>), gF, F, s.q, s.q, s.invd, s.fixm, one, s.z, s.st, 0, s.partials, s.counter);
+      }
+      CK(mg_mv0(ctx, 0, s.m_z));
+      LAUNCH(ctx, k_mg_rayleigh<true>, gF, F, s.z, s.q, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om, s.partials,
+             s.counter);
+    } else {
+      MgLevel& m = ctx->mg[l];
+      const int gL = grid_for(m.L.nodes());
+      LAUNCH(ctx, k_mg_start_vec, gL, m.L, m.fixm, m.x);
+      for (int k = 0; k < kMgPowerSteps; ++k) {
+        CK(mg_apply(ctx, l, 0));
+        LAUNCH(ctx, (k_mg_jacobi<0, false>), gL, m.L, m.t, m.t, m.invd, m.fixm, one, m.x, s.st, 0, s.partials,
+               s.counter);
+      }
+      CK(mg_apply(ctx, l, 0));
+      LAUNCH(ctx, k_mg_rayleigh<false>, gL, m.L, m.x, m.t, m.invd, m.fixm, ctx->prm.mg_omega, ctx->mg_om + l,
+             s.partials, s.counter);
+    }
+  }
+  const MgLevel& c = ctx->mg[L - 1];
+  const int n = ctx->mg_n;
+  LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, n, ctx->mg_A0);
+  for (int k = 0; k < n; ++k) {
+    const double* a = (k % 2 == 0) ? ctx->mg_A0 : ctx->mg_A1;
+    double* o = (k % 2 == 0) ? ctx->mg_A1 : ctx->mg_A0;
+    LAUNCH(ctx, k_mg_gj_step, grid_for((long long)n * n), a, o, n, k);
+  }
+  return check_launch(ctx);
+}
+
+int mg_setup(topo_ctx* ctx) {
+  if (!ctx->mg_on || ctx->mg_ready) return TOPO_OK;
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  if (ctx->debug) {
+    CK(enqueue_mg_setup(ctx));
+  } else {
+    if (!ctx->mg_setup_exec) {
+      cudaGraph_t graph;
+      const long long l0 = ctx->launches;
+      CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = enqueue_mg_setup(ctx);
+      cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+      if (rc != TOPO_OK) return rc;
+      if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "MG setup capture: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&ctx->mg_setup_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "MG setup instantiate: %s", cudaGetErrorString(e));
+      ctx->mg_setup_launches = ctx->launches - l0;
+      ctx->launches = l0;
+    }
+    CU(cudaGraphLaunch(ctx->mg_setup_exec, ctx->stream));
+    ctx->launches += ctx->mg_setup_launches;
+  }
+  ctx->mg_ready = true;
+  return TOPO_OK;
+}
+
+// fine plain matvec q = K v (v = z or w), gated by the PCG state
+int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin) {
+  Slab& s = ctx->slabs[0];
+  return launch_mv<0, false>(ctx, s, gate, vin, nullptr, nullptr, s.q, 0);
+}
+
+// t_l = A_l x_l on a coarse level (stored: element matrices; level 1: P^T K P)
+int mg_apply(topo_ctx* ctx, int l, int gate) {
+  Slab& s = ctx->slabs[0];
+  MgLevel& m = ctx->mg[l];
+  const DevState* gst = gate ? s.st : nullptr;
+  if (m.stored) {
+    LAUNCH(ctx, k_mg_apply_asm, grid_for(m.L.nodes()), m.L, m.K, m.x, m.fixm, m.t, gst);
+    return check_launch(ctx);
+  }
+  const LvGeo F = lv0(ctx);
+  LAUNCH(ctx, k_mg_prolong<false>, grid_for(F.nodes()), F, m.L, m.x, s.fixm, s.w, gst);
+  CK(mg_mv0(ctx, gate, s.m_w));
+  LAUNCH(ctx, k_mg_restrict<false>, grid_for(m.L.nodes()), F, m.L, s.q, s.q, s.fixm, m.fixm, m.t, gst);
+  return check_launch(ctx);
+}
+
+// One V-cycle on level l (level 0: b = r, x = z; `dot`: the last fine sweep
+// computes rho = r.z and beta for the PCG).
+int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
+  Slab& s = ctx->slabs[0];
+  const int L = (int)ctx->mg.size(), nu = ctx->prm.mg_nu;
+  const DevState* gst = gate ? s.st : nullptr;
+  const double* om = ctx->mg_om + l;
+  if (l == L - 1) {
+    const MgLevel& c = ctx->mg[l];
+    LAUNCH(ctx, k_mg_coarse_solve, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_imap, c.b, c.x, gst);
+    return check_launch(ctx);
+  }
+  MgLevel& n1 = ctx->mg[l + 1];
+  if (l == 0) {
+    const LvGeo F = lv0(ctx);
+    const int gF = grid_for(F.nodes());
+    LAUNCH(ctx, (k_mg_jacobi<0, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+    for (int k = 1; k < nu; ++k) {
+      CK(mg_mv0(ctx, gate, s.m_z));
+      LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+    }
+    CK(mg_mv0(ctx, gate, s.m_z));
+    LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), F, n1.L, s.r, s.q, s.fixm, n1.fixm, n1.b, gst);
+    CK(enqueue_vcycle(ctx, 1, gate, false));
+    LAUNCH(ctx, k_mg_prolong<true>, gF, F, n1.L, n1.x, s.fixm, s.z, gst);
+    for (int k = 1; k <= nu; ++k) {
+      CK(mg_mv0(ctx, gate, s.m_z));
+      if (dot && k == nu)
+        LAUNCH(ctx, (k_mg_jacobi<2, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+      else
+        LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+    }
+    return check_launch(ctx);
+  }
+  MgLevel& m = ctx->mg[l];
+  const int gL = grid_for(m.L.nodes());
+  LAUNCH(ctx, (k_mg_jacobi<0, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+  for (int k = 1; k < nu; ++k) {
+    CK(mg_apply(ctx, l, gate));
+    LAUNCH(ctx, (k_mg_jacobi<1, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+  }
+  CK(mg_apply(ctx, l, gate));
+  LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), m.L, n1.L, m.b, m.t, m.fixm, n1.fixm, n1.b, gst);
+  CK(enqueue_vcycle(ctx, l + 1, gate, false));
+  LAUNCH(ctx, k_mg_prolong<true>, gL, m.L, n1.L, n1.x, m.fixm, m.x, gst);
+  for (int k = 1; k <= nu; ++k) {
+    CK(mg_apply(ctx, l, gate));
+    LAUNCH(ctx, (k_mg_jacobi<1, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+  }
+  return check_launch(ctx);
+}
+
+// one MG-PCG iteration: z = V(r) (rho, beta) ; p = z + beta p ; q = K p ; alpha ; u, r update
+int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
+  Slab& s = ctx->slabs[0];
+  CK(enqueue_vcycle(ctx, 0, 1, true));
+  if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
+  const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
+  double* pnew = parity ? s.p0 : s.p1;
+  double* pprev = parity ? s.p1 : s.p0;
+  CK((launch_mv<2, true>(ctx, s, 1, s.m_z, pold, pnew, s.q, 1)));
+  if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
+  if (parity)
+    LAUNCH(ctx, (k_update<true, true>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
+           pnew, s.q, s.invd, s.fixm, s.partials, s.counter, 1);
+  else
+    LAUNCH(ctx, (k_update<false, true>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
+           pnew, s.q, s.invd, s.fixm, s.partials, s.counter, 1);
+  return check_launch(ctx);
+}
+
+// host <-> level-l vectors in external numbering (test hooks)
+int mg_upload(topo_ctx* ctx, int l, const double* host, double* dev) {
+  const MgLevel& m = ctx->mg[l];
+  const LvGeo& L = m.L;
+  std::vector<double> lay(3 * L.ncomp, 0.0);
+  long long n = 0;
+  for (int iz = 0; iz <= L.nz; ++iz)
+    for (int ix = 0; ix <= L.nx; ++ix)
+      for (int iy = 0; iy <= L.ny; ++iy, ++n)
+        for (int c = 0; c < 3; ++c)
+          lay[L.n(ix, iy, iz) + c * L.ncomp] = ((m.hfix[n] >> c) & 1) ? 0.0 : host[3 * n + c];
+  CU(cudaMemcpy(dev, lay.data(), sizeof(double) * lay.size(), cudaMemcpyHostToDevice));
+  return TOPO_OK;
+}
+int mg_download(topo_ctx* ctx, int l, const double* dev, double* host) {
+  const LvGeo& L = ctx->mg[l].L;
+  std::vector<double> lay(3 * L.ncomp);
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaMemcpy(lay.data(), dev, sizeof(double) * lay.size(), cudaMemcpyDeviceToHost));
+  long long n = 0;
+  for (int iz = 0; iz <= L.nz; ++iz)
+    for (int ix = 0; ix <= L.nx; ++ix)
+      for (int iy = 0; iy <= L.ny; ++iy, ++n)
+        for (int c = 0; c < 3; ++c) host[3 * n + c] = lay[L.n(ix, iy, iz) + c * L.ncomp];
   return TOPO_OK;
 }
 
@@ -671,16 +1085,11 @@ int build_cg_graph(topo_ctx* ctx) {
 // true residual f - K u is checked; if it fails, r is replaced and PCG
 // restarts.
 // ---------------------------------------------------------------------------
-int do_solve(topo_ctx* ctx, topo_solve_info* info) {
-  CK(ensure_constants(ctx));
-  if (!ctx->has_E) CK(update_modulus(ctx));
-  CK(exchange_nodes(ctx, &Slab::invd, 1));   // ghost planes feed the fused p-update
+// One PCG pass (Jacobi or multigrid preconditioner) from the current u.
+int solve_pass(topo_ctx* ctx, int mg, int* replacements_out, double* rr_true_out) {
   const topo_params& P = ctx->prm;
   const long long n_dof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
   const long long maxit = P.cg_max_iter > 0 ? P.cg_max_iter : 10 * n_dof;
-  CU(cudaEventRecord(ctx->ev[6], ctx->stream));
-  if (!P.cg_warm_start || !ctx->has_u || ctx->bb == 0.0)
-    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
   for (Slab& s : ctx->slabs) {
     k_cg_init<<<1, 1, 0, ctx->stream>>>(s.st, P.cg_rtol * P.cg_rtol, ctx->bb, maxit);
     ctx->launches++;
@@ -688,7 +1097,7 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   CK(residual(ctx, true));
   for (Slab& s : ctx->slabs) { k_cg_start<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
   CK(check_launch(ctx));
-  if (!ctx->debug) CK(build_cg_graph(ctx));
+  if (!ctx->debug) CK(build_cg_graph(ctx, mg));
   int replacements = 0, rc = TOPO_OK;
   double rr_true = 0.0;
   DevState& h = *ctx->hstate;
@@ -697,10 +1106,11 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   while (true) {
     if (!h.done) {
       if (ctx->debug) {
-        for (int i = 0; i < ctx->cg_batch; ++i) CK(enqueue_cg_iter(ctx, false, i & 1));
+        const int nb = mg ? ctx->mg_batch : ctx->cg_batch;
+        for (int i = 0; i < nb; ++i) CK(mg ? enqueue_mg_iter(ctx, false, i & 1) : enqueue_cg_iter(ctx, false, i & 1));
       } else {
-        CU(cudaGraphLaunch(ctx->cg_exec, ctx->stream));
-        ctx->launches += ctx->cg_batch_launches;
+        CU(cudaGraphLaunch(ctx->cg_exec[mg], ctx->stream));
+        ctx->launches += ctx->cg_batch_launches[mg];
       }
       CK(sync_state(ctx));
       if (ctx->profile && h.it > it_prev) {
@@ -730,18 +1140,49 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
       break;
     }
   }
+  *replacements_out = replacements;
+  *rr_true_out = rr_true;
+  return rc;
+}
+
+int do_solve(topo_ctx* ctx, topo_solve_info* info) {
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  CK(exchange_nodes(ctx, &Slab::invd, 1));   // ghost planes feed the fused p-update
+  CK(mg_setup(ctx));                         // multigrid: smoother weights, Galerkin levels, coarsest inverse
+  const topo_params& P = ctx->prm;
+  CU(cudaEventRecord(ctx->ev[6], ctx->stream));
+  if (!P.cg_warm_start || !ctx->has_u || ctx->bb == 0.0)
+    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
+  int mg = ctx->mg_on ? 1 : 0, replacements = 0;
+  double rr_true = 0.0;
+  long long iters = 0;
+  int rc = solve_pass(ctx, mg, &replacements, &rr_true);
+  iters = ctx->hstate->it;
+  if (rc == TOPO_EBREAKDOWN && mg) {
+    // multigrid breakdown (an indefinite V-cycle): redo this solve with the
+    // Jacobi preconditioner from u = 0 (both GPU paths; counted in timings)
+    ctx->tim.mg_fallbacks++;
+    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
+    mg = 0;
+    rc = solve_pass(ctx, 0, &replacements, &rr_true);
+    iters += ctx->hstate->it;
+  }
+  DevState& h = *ctx->hstate;
   CU(cudaEventRecord(ctx->ev[7], ctx->stream));
   CU(cudaEventSynchronize(ctx->ev[7]));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
-  ctx->tim.cg_iters = h.it;
-  ctx->tim.cg_iters_total += h.it;
+  ctx->tim.cg_iters = iters;
+  ctx->tim.cg_iters_total += iters;
   if (info) {
-    info->iters = h.it;
+    info->iters = iters;
     info->rel_res = ctx->bb > 0 ? std::sqrt(h.rr / ctx->bb) : 0.0;
     info->true_rel_res = ctx->bb > 0 ? std::sqrt(rr_true / ctx->bb) : 0.0;
     info->ms = ms;
     info->replacements = replacements;
+    info->precond = mg ? TOPO_PRECOND_MG : TOPO_PRECOND_JACOBI;
+    info->mg_levels = ctx->mg_on ? (int)ctx->mg.size() : 0;
   }
   ctx->has_u = true;
   ctx->has_sens = ctx->has_dcf = false;
@@ -912,7 +1353,7 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
     return TOPO_OK;
   };
   const size_t nb = sizeof(double) * 3 * g.ncomp, eb = sizeof(double) * g.nelloc;
-  double** nv[] = {&s.u, &s.r, &s.p0, &s.p1, &s.q, &s.f, &s.w};
+  double** nv[] = {&s.u, &s.r, &s.p0, &s.p1, &s.q, &s.f, &s.w, &s.z};
   for (double** v : nv) CK(al((void**)v, nb));
   CK(al((void**)&s.invd, sizeof(double) * g.ncomp));
   CK(al((void**)&s.fixm, g.ncomp));
@@ -934,13 +1375,25 @@ void free_ctx(topo_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
-    void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
+    void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
-  if (ctx->cg_exec) cudaGraphExecDestroy(ctx->cg_exec);
+  for (MgLevel& m : ctx->mg) {
+    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.fixm};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  {
+    void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_A0, ctx->mg_A1, ctx->mg_dmap, ctx->mg_imap, ctx->mg_om};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+  if (ctx->mg_setup_exec) cudaGraphExecDestroy(ctx->mg_setup_exec);
+  for (cudaGraphExec_t g : ctx->cg_exec)
+    if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
   if (ctx->pe0) cudaEventDestroy(ctx->pe0);
   if (ctx->pe1) cudaEventDestroy(ctx->pe1);
@@ -968,6 +1421,11 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (p->filter_mode < 0 || p->filter_mode > 2) return set_err(ctx, TOPO_EINVAL, "filter_mode must be 0, 1 or 2");
   if (!(p->cg_rtol > 0 && p->cg_rtol < 1)) return set_err(ctx, TOPO_EINVAL, "cg_rtol must be in (0,1)");
   if (!(p->oc_tol > 0) || !(p->oc_lmax > 0)) return set_err(ctx, TOPO_EINVAL, "oc_tol, oc_lmax must be > 0");
+  if (p->precond < 0 || p->precond > 2) return set_err(ctx, TOPO_EINVAL, "precond must be 0, 1 or 2");
+  if (p->mg_nu < 1 || p->mg_nu > 8) return set_err(ctx, TOPO_EINVAL, "mg_nu must be in [1, 8]");
+  if (!(p->mg_omega > 0 && p->mg_omega < 2)) return set_err(ctx, TOPO_EINVAL, "mg_omega must be in (0, 2)");
+  if (p->mg_coarse_max < 24 || p->mg_coarse_max > 4096)
+    return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be in [24, 4096]");
   return TOPO_OK;
 }
 
@@ -997,6 +1455,10 @@ void topo_params_default(topo_params* p) {
   p->oc_lmax = 1e9;
   p->deterministic = 1;
   p->cg_check_every = 0;
+  p->precond = TOPO_PRECOND_AUTO;
+  p->mg_nu = 1;
+  p->mg_omega = 1.6;
+  p->mg_coarse_max = 1000;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }
@@ -1198,6 +1660,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
     }
   }
   rc = upload_nodes(ctx, load, &Slab::f);
+  if (rc == TOPO_OK) rc = mg_build(ctx, fixed);
   if (rc == TOPO_OK) rc = ensure_constants(ctx);
   if (rc == TOPO_OK) {
     // ||f_free||^2 and filter row sums Hs (all local in-domain elements)
@@ -1241,7 +1704,9 @@ int topo_set_stream(topo_ctx* ctx, void* stream) {
   if (s != ctx->stream) {
     cudaStreamSynchronize(ctx->stream);
     ctx->stream = s;
-    if (ctx->cg_exec) { cudaGraphExecDestroy(ctx->cg_exec); ctx->cg_exec = nullptr; }
+    for (cudaGraphExec_t& g : ctx->cg_exec)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+    if (ctx->mg_setup_exec) { cudaGraphExecDestroy(ctx->mg_setup_exec); ctx->mg_setup_exec = nullptr; }
     if (ctx->oc_exec) { cudaGraphExecDestroy(ctx->oc_exec); ctx->oc_exec = nullptr; }
     g_const_owner = nullptr;
   }
@@ -1523,6 +1988,46 @@ int64_t topo_count(const topo_ctx* ctx, int32_t what) {
     case TOPO_COUNT_DEVICE_BYTES: return (long long)ctx->dev_bytes;
     default: return -1;
   }
+}
+
+int topo_mg_levels(topo_ctx* ctx, int32_t* n_levels, int32_t* dims) {
+  if (!ctx || !n_levels) return TOPO_EINVAL;
+  const int L = ctx->mg_on ? (int)ctx->mg.size() : 0;
+  *n_levels = L;
+  if (dims)
+    for (int l = 0; l < L; ++l) {
+      const LvGeo g = l == 0 ? lv0(ctx) : ctx->mg[l].L;
+      dims[3 * l] = g.nx;
+      dims[3 * l + 1] = g.ny;
+      dims[3 * l + 2] = g.nz;
+    }
+  return TOPO_OK;
+}
+
+int topo_mg_apply(topo_ctx* ctx, int32_t level, const double* x, double* y) {
+  if (!ctx || !x || !y) return TOPO_EINVAL;
+  if (!ctx->mg_on) return set_err(ctx, TOPO_ESTATE, "topo_mg_apply: context has no multigrid hierarchy");
+  if (level < 0 || level >= (int)ctx->mg.size()) return set_err(ctx, TOPO_EINVAL, "topo_mg_apply: bad level %d", level);
+  cudaSetDevice(ctx->device);
+  CK(mg_setup(ctx));
+  if (level == 0) return topo_apply_K(ctx, x, y);
+  MgLevel& m = ctx->mg[level];
+  CK(mg_upload(ctx, level, x, m.x));
+  CK(mg_apply(ctx, level, 0));
+  return mg_download(ctx, level, m.t, y);
+}
+
+int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
+  if (!ctx || !b || !z) return TOPO_EINVAL;
+  if (!ctx->mg_on) return set_err(ctx, TOPO_ESTATE, "topo_mg_vcycle: context has no multigrid hierarchy");
+  cudaSetDevice(ctx->device);
+  CK(mg_setup(ctx));
+  CK(upload_nodes(ctx, b, &Slab::r));
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.r);
+  CK(check_launch(ctx));
+  CK(enqueue_vcycle(ctx, 0, 0, false));
+  return download_nodes(ctx, &Slab::z, z);
 }
 
 void topo_destroy(topo_ctx* ctx) { free_ctx(ctx); }

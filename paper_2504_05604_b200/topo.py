@@ -21,6 +21,8 @@ TOPO_FILTER_X, TOPO_FILTER_DC = 0, 1
 FIELDS = dict(u=0, x=1, xphys=2, E=3, ce=4, dc=5, dcf=6, dvf=7, xnew=8, hs=9, invdiag=10, r=11)
 NODE_FIELDS = {"u", "invdiag", "r"}
 TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK = 0, 1, 2
+TOPO_PRECOND_JACOBI, TOPO_PRECOND_MG, TOPO_PRECOND_AUTO = 0, 1, 2
+PRECOND = dict(jacobi=0, mg=1, auto=2)
 COUNTS = dict(ndof=0, nel=1, nodes=2, design=3, stencil=4, device_bytes=5)
 
 # Every symbol include/topo.h declares (checked by tests/test_abi.py).
@@ -29,7 +31,8 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            "topo_oc_step", "topo_optimize", "topo_apply_K", "topo_update_modulus",
            "topo_matvec_load", "topo_matvec_run", "topo_get", "topo_get_timings", "topo_profile",
            "topo_kernel_time", "topo_element_stiffness", "topo_count", "topo_last_error",
-           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition", "topo_snapshot", "topo_restore"]
+           "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition", "topo_snapshot", "topo_restore",
+           "topo_mg_levels", "topo_mg_apply", "topo_mg_vcycle"]
 
 
 class topo_params(C.Structure):
@@ -38,7 +41,9 @@ class topo_params(C.Structure):
                 ("E0", C.c_double), ("Emin", C.c_double), ("nu", C.c_double), ("move", C.c_double),
                 ("filter_mode", C.c_int32), ("cg_rtol", C.c_double), ("cg_max_iter", C.c_int64),
                 ("cg_warm_start", C.c_int32), ("oc_tol", C.c_double), ("oc_lmax", C.c_double),
-                ("deterministic", C.c_int32), ("cg_check_every", C.c_int32)]
+                ("deterministic", C.c_int32), ("cg_check_every", C.c_int32),
+                ("precond", C.c_int32), ("mg_nu", C.c_int32), ("mg_omega", C.c_double),
+                ("mg_coarse_max", C.c_int32)]
 
 
 class topo_dist(C.Structure):
@@ -48,7 +53,8 @@ class topo_dist(C.Structure):
 
 class topo_solve_info(C.Structure):
     _fields_ = [("iters", C.c_int64), ("rel_res", C.c_double), ("true_rel_res", C.c_double),
-                ("ms", C.c_double), ("replacements", C.c_int32)]
+                ("ms", C.c_double), ("replacements", C.c_int32), ("precond", C.c_int32),
+                ("mg_levels", C.c_int32)]
 
 
 class topo_timings(C.Structure):
@@ -57,7 +63,7 @@ class topo_timings(C.Structure):
                 ("cg_iters", C.c_int64), ("oc_passes", C.c_int32), ("c", C.c_double),
                 ("fu", C.c_double), ("volume", C.c_double), ("change", C.c_double),
                 ("lambda_", C.c_double), ("kernel_launches", C.c_int64),
-                ("cg_iters_total", C.c_int64)]
+                ("cg_iters_total", C.c_int64), ("mg_fallbacks", C.c_int32)]
 
 
 def _load():
@@ -99,6 +105,9 @@ def _load():
         "topo_snapshot": (I, [ctxp]),
         "topo_restore": (I, [ctxp]),
         "topo_partition": (I, [C.c_int32, C.c_double, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)]),
+        "topo_mg_levels": (I, [ctxp, P(C.c_int32), P(C.c_int32)]),
+        "topo_mg_apply": (I, [ctxp, C.c_int32, D, D]),
+        "topo_mg_vcycle": (I, [ctxp, D, D]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -155,10 +164,13 @@ def make_params(p):
     prm = topo_params()
     _lib.topo_params_default(C.byref(prm))
     for k in ("nelx", "nely", "nelz", "filter_mode", "cg_warm_start", "deterministic",
-              "cg_check_every"):
+              "cg_check_every", "mg_nu", "mg_coarse_max"):
         if k in p:
             setattr(prm, k, int(p[k]))
-    for k in ("volfrac", "penal", "rmin", "E0", "Emin", "nu", "move", "cg_rtol", "oc_tol", "oc_lmax"):
+    if "precond" in p:
+        prm.precond = PRECOND[p["precond"]] if isinstance(p["precond"], str) else int(p["precond"])
+    for k in ("volfrac", "penal", "rmin", "E0", "Emin", "nu", "move", "cg_rtol", "oc_tol", "oc_lmax",
+              "mg_omega"):
         if k in p:
             setattr(prm, k, float(p[k]))
     if "cg_max_iter" in p:
@@ -243,7 +255,8 @@ class Problem:
         info = topo_solve_info()
         self._check(_lib.topo_solve(self._ctx, _dp(u), C.byref(info)), "topo_solve")
         return u, dict(iters=info.iters, rel_res=info.rel_res, true_rel_res=info.true_rel_res,
-                       ms=info.ms, replacements=info.replacements)
+                       ms=info.ms, replacements=info.replacements,
+                       precond={0: "jacobi", 1: "mg"}[info.precond], mg_levels=info.mg_levels)
 
     def sensitivity(self, want=True):
         c = C.c_double()
@@ -316,6 +329,28 @@ class Problem:
         m, n = C.c_double(), C.c_int64()
         self._check(_lib.topo_kernel_time(self._ctx, C.byref(m), C.byref(n)), "topo_kernel_time")
         return m.value, n.value
+
+    def mg_levels(self):
+        """[(nelx_l, nely_l, nelz_l)] of the multigrid hierarchy ([] with Jacobi)."""
+        n = C.c_int32()
+        dims = np.zeros(48, dtype=np.int32)
+        self._check(_lib.topo_mg_levels(self._ctx, C.byref(n),
+                                        dims.ctypes.data_as(C.POINTER(C.c_int32))), "topo_mg_levels")
+        return [tuple(int(v) for v in dims[3 * l:3 * l + 3]) for l in range(n.value)]
+
+    def mg_apply(self, level, x):
+        """y = A_level x on multigrid level `level` (external numbering of that grid)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros_like(x)
+        self._check(_lib.topo_mg_apply(self._ctx, int(level), _dp(x), _dp(y)), "topo_mg_apply")
+        return y
+
+    def mg_vcycle(self, b):
+        """z = V(b): one multigrid V-cycle on a fine-level vector."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        z = np.zeros(3 * self.n_nd)
+        self._check(_lib.topo_mg_vcycle(self._ctx, _dp(b), _dp(z)), "topo_mg_vcycle")
+        return z
 
     def count(self, what):
         return int(_lib.topo_count(self._ctx, COUNTS[what]))

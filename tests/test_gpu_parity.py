@@ -91,9 +91,10 @@ def test_matvec_parity(topo, case):
 
 
 @pytest.mark.parametrize("case", SMALL[:3])
-def test_solve_parity_random_density(topo, case):
+@pytest.mark.parametrize("precond", ["jacobi", "mg"])
+def test_solve_parity_random_density(topo, case, precond):
     """Config 1's standalone solve on x ~ U[0.01, 1] (seed 0), plus others."""
-    p, f, fx, pas = _problem(*case)
+    p, f, fx, pas = _problem(*case, precond=precond)
     dims = (p["nelx"], p["nely"], p["nelz"])
     x = _xfield(np.prod(dims), pas, seed=0)
     KE = oracle.element_stiffness(p["nu"])
@@ -160,9 +161,10 @@ def test_sens_filter_oc_parity(topo, case, mode):
 @pytest.mark.parametrize("cfg,n_iter", [(0, 20), (1, 10)])
 @pytest.mark.parametrize("mode", [0, 1])
 def test_loop_parity_configs(topo, cfg, n_iter, mode):
-    """BASELINE configs 0/1: c history (fixed n_iter) within 1e-6 relative,
-    volume within 1e-6, final design within 1e-6."""
-    p, f, fx, pas = make_problem(cfg, filter_mode=mode)
+    """BASELINE configs 0/1 with the north_star Jacobi-PCG: c history (fixed
+    n_iter) within 1e-6 relative, volume within 1e-6, final design within 1e-6.
+    (The multigrid variant: tests/test_gpu_mg.py.)"""
+    p, f, fx, pas = make_problem(cfg, filter_mode=mode, precond="jacobi")
     ro = oracle.run_optimization(p, f, fx, pas, n_iter=n_iter)
     with topo.Problem(p, f, fx, pas) as pr:
         c, x, nd = pr.optimize(n_iter)
@@ -196,7 +198,7 @@ def test_loopback_slabs_match_single(topo, W):
     """x-slab decomposition (W slabs on one GPU, in-process halo copies):
     identical problem, results equal W = 1 to rounding, and the oracle."""
     dims, obst = (37, 13, 5), (18.0, 6.0, 3.0)
-    p, f, fx, pas = _problem(dims, 2.5, obst)
+    p, f, fx, pas = _problem(dims, 2.5, obst, precond="jacobi")
     x0 = _xfield(int(np.prod(dims)), pas, seed=5)
     pv = random_vector(3 * 38 * 14 * 6, seed=1)
     outs = []
@@ -230,10 +232,11 @@ def test_zero_load_and_errors(topo):
         with pytest.raises(topo.TopoError) as e:
             pr.sensitivity()
         assert e.value.code == topo.TOPO_ESTATE
-    with topo.Problem(dict(p, cg_max_iter=5), f, fx) as pr:
-        with pytest.raises(topo.TopoError) as e:
-            pr.solve()
-        assert e.value.code == topo.TOPO_ENOCONV
+    for pc, mx in (("jacobi", 5), ("mg", 1)):
+        with topo.Problem(dict(p, cg_max_iter=mx, precond=pc), f, fx) as pr:
+            with pytest.raises(topo.TopoError) as e:
+                pr.solve()
+            assert e.value.code == topo.TOPO_ENOCONV
 
 
 def test_single_element_and_tiny(topo):

@@ -144,7 +144,7 @@ def _evolved_case(cfg=1, n_iter=6):
 
 def test_vcycle_symmetric_positive_definite():
     K, f, fx, dims, _ = _evolved_case(1, 4)
-    lv = mg.hierarchy(K, fx, dims)
+    lv = mg.smoother_weights(mg.hierarchy(K, fx, dims))
     assert len(lv) == 3
     rng = np.random.default_rng(3)
     free = fx == 0
@@ -171,3 +171,38 @@ def test_mgcg_reaches_direct_solution(cfg):
     assert np.linalg.norm(um - u) <= 1e-8 * np.linalg.norm(u)
     assert oracle.true_residual(K, um, f, fx) <= 1e-10
     assert it < itj / 5                                        # the point of f2
+
+
+def test_start_vector_is_splitmix64():
+    """Known splitmix64 outputs (seed-free counter form, increment 0x9E3779B97F4A7C15):
+    the first output for state 0 is 0xE220A8397B1DCDAF."""
+    v = mg.start_vector(2, [0, 0])
+    u0 = (0xE220A8397B1DCDAF >> 11) * 2.0 ** -53
+    assert v[0] == 2.0 * u0 - 1.0
+    assert np.all(mg.start_vector(6, [0, 1, 0, 0, 1, 0])[[1, 4]] == 0.0)
+
+
+@pytest.mark.parametrize("seed", [0, 2])
+def test_lambda_estimate_bounds(seed):
+    """Rayleigh quotient <= lam_max(D^-1 A) <= element bound lam_max(KE)/KE_ii
+    (x^T A x = sum_e x_e^T E_e KE x_e <= lam(KE)/kd x^T D x), and the damped
+    smoother it sets is convergent: w lam_max < 2 for theta = 1.6."""
+    import scipy.sparse as sps
+    import scipy.sparse.linalg as spla
+    from workloads import random_density
+    dims = (12, 6, 4)
+    fx = cantilever_fixed(*dims)
+    KE = oracle.element_stiffness(0.3)
+    E = 1e-9 + random_density(int(np.prod(dims)), seed=seed) ** 3
+    K = oracle.assemble(*dims, KE, E)
+    lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=200))
+    bound = np.linalg.eigvalsh(KE).max() / KE[0, 0]
+    for l in lv[:-1]:
+        A, d, _ = mg.level_operator(l)
+        Dm = sps.diags(1.0 / np.sqrt(d))
+        lam_max = spla.eigsh(Dm @ A @ Dm, k=1, which="LA", return_eigenvectors=False)[0]
+        assert l["lam"] <= lam_max * (1 + 1e-12)
+        assert l["omega"] * lam_max < 2.0
+    A0, d0, _ = mg.level_operator(lv[0])
+    Dm = sps.diags(1.0 / np.sqrt(d0))
+    assert spla.eigsh(Dm @ A0 @ Dm, k=1, which="LA", return_eigenvectors=False)[0] <= bound + 1e-12
