@@ -29,6 +29,8 @@
 //   kPre = 1: p_new = M^{-1} r + beta p_old   (Jacobi preconditioner, vin = r)
 //   kPre = 2: p_new = z + beta p_old          (z = V(r) from the multigrid
 //             preconditioner already in HBM, vin = z; no M^{-1} stream)
+//   kPre = 3: p_new = w M^{-1} b               (first damped-Jacobi sweep of the
+//             multigrid V-cycle from x = 0, w = *scale; vin = b)
 #pragma once
 #include "common.cuh"
 #include "tma.cuh"
@@ -49,8 +51,13 @@ __device__ __forceinline__ void wht4(const double v[4], double G[4]) {
 
 // Q = E * B * P  (P, Q indexed [c][m], m = mx + 2 my + 4 mz).  E is folded
 // into the 8 block constants (8 DMUL) instead of scaling the 21 outputs.
+__constant__ WhtK c_wht1;   // Lambda^-1 B Lambda^-1, Lambda = diag(2^|m|): level-1 multigrid (mg.cuh)
+
+__device__ __forceinline__ void wht_block_k(const WhtK& K, const double P[3][8], double Ee, double Q[3][8]);
 __device__ __forceinline__ void wht_block(const double P[3][8], double Ee, double Q[3][8]) {
-  const WhtK& K = c_wht;
+  wht_block_k(c_wht, P, Ee, Q);
+}
+__device__ __forceinline__ void wht_block_k(const WhtK& K, const double P[3][8], double Ee, double Q[3][8]) {
   const double k0 = Ee * K.k0, o0 = Ee * K.o0, k7 = Ee * K.k7, o7 = Ee * K.o7;
   const double a = Ee * K.a, b = Ee * K.b, r = Ee * K.r, s = Ee * K.s;
   double t;
@@ -91,6 +98,14 @@ struct MvMaps {
   CUtensorMap E;      // 3D {EY, EZ, NEXL}
 };
 
+// kEpi = 1 epilogue operands (multigrid post-smoothing fused into the matvec):
+// out = mask(v + w M^-1 (b - K v)) and rho = b . out, with b = r of the PCG.
+struct MvEpi {
+  const double* b;          // 3 * ncomp
+  const double* invd;       // per node
+  const uint8_t* fixm;      // per node
+};
+
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
 template <int TZ> struct MvSmem {
   static constexpr int YW = 34;                                   // 33 nodes, box width padded to 16 B
@@ -98,22 +113,27 @@ template <int TZ> struct MvSmem {
   static constexpr int I = (TZ + 1) * YW * 8;                     // one scalar node tile
   static constexpr int EB = TZ * YW * 8;                          // element tile (box width 34 as well)
   static constexpr int VA = (V + 127) / 128 * 128, IA = (I + 127) / 128 * 128, EA = (EB + 127) / 128 * 128;
-  __host__ __device__ static constexpr int stage(int pre) { return pre == 1 ? 2 * VA + IA + EA : pre == 2 ? 2 * VA + EA : VA + EA; }
-  // offset of the element tile inside a stage
-  __host__ __device__ static constexpr int eoff(int pre) { return pre == 1 ? 2 * VA + IA : pre == 2 ? 2 * VA : VA; }
+  // stage = [vin][p_old (pre 1,2)][M^-1 (pre 1,3)][E]
+  __host__ __device__ static constexpr int ioff(int pre) { return pre == 1 ? 2 * VA : VA; }
+  __host__ __device__ static constexpr int eoff(int pre) {
+    return VA + (pre == 1 || pre == 2 ? VA : 0) + (pre == 1 || pre == 3 ? IA : 0);
+  }
+  __host__ __device__ static constexpr int stage(int pre) { return eoff(pre) + EA; }
   // raw stages + 3 rotating p-planes (pre-pass output) + alignment slack
   __host__ __device__ static constexpr int bytes(int pre) { return kMvStages * stage(pre) + 3 * VA + 128; }
 };
 
-template <int TZ, int kPre, bool kDot>
+template <int TZ, int kPre, bool kDot, int kEpi>
 __global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? 2 : 1))
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
          double* __restrict__ pnew, double* __restrict__ q,
-         double* partials, unsigned int* counter, int finish) {
+         double* partials, unsigned int* counter, int finish, const double* __restrict__ scale, MvEpi epi) {
   if (gate && st->done) return;
   constexpr bool kFused = kPre != 0;
+  constexpr bool kInvd = kPre == 1 || kPre == 3;
   using L = MvSmem<TZ>;
-  const double beta = (kFused && !st->fresh) ? st->beta : 0.0;
+  const double beta = (kPre == 1 || kPre == 2) && !st->fresh ? st->beta : 0.0;
+  const double wsc = (kPre == 3 || kEpi == 1) ? *scale : 1.0;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ double xch[2][3][TZ][32];   // lanes contiguous: conflict-free
   __shared__ __align__(8) uint64_t full[kMvStages];
@@ -146,18 +166,18 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     unsigned char* b = slot(s);
     const int j = xs - 1 + t;
     const int ixl = j - g.ex0 + 1;
-    const uint32_t bytes = (kPre == 1 ? 2 * L::V + L::I : kPre == 2 ? 2 * L::V : L::V) + (t > 0 ? L::EB : 0);
+    const uint32_t bytes = L::V + (kPre == 1 || kPre == 2 ? L::V : 0) + (kInvd ? L::I : 0) + (t > 0 ? L::EB : 0);
     mbar_arrive_expect_tx(&full[s], bytes);
     tma_load_4d(b, &maps.vin, &full[s], yb, z0, ixl, 0);
-    if (kFused) tma_load_4d(b + L::VA, &maps.pold, &full[s], yb, z0, ixl, 0);
-    if (kPre == 1) tma_load_3d(b + 2 * L::VA, &maps.invd, &full[s], yb, z0, ixl);
+    if (kPre == 1 || kPre == 2) tma_load_4d(b + L::VA, &maps.pold, &full[s], yb, z0, ixl, 0);
+    if (kInvd) tma_load_3d(b + L::ioff(kPre), &maps.invd, &full[s], yb, z0, ixl);
     if (t > 0) tma_load_3d(b + L::eoff(kPre), &maps.E, &full[s], yb, z0, j - 1 - g.ex0 + g.H);
   };
   if (leader) {
     tma_prefetch_desc(&maps.vin);
     tma_prefetch_desc(&maps.E);
-    if (kFused) tma_prefetch_desc(&maps.pold);
-    if (kPre == 1) tma_prefetch_desc(&maps.invd);
+    if (kPre == 1 || kPre == 2) tma_prefetch_desc(&maps.pold);
+    if (kInvd) tma_prefetch_desc(&maps.invd);
     for (int s = 0; s < kMvStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
@@ -195,7 +215,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     mbar_wait(&full[s], (uint32_t)((t / kMvStages) & 1));
     const double* sv = reinterpret_cast<const double*>(slot(s));
     const double* sp = reinterpret_cast<const double*>(slot(s) + L::VA);
-    const double* si = reinterpret_cast<const double*>(slot(s) + 2 * L::VA);
+    const double* si = reinterpret_cast<const double*>(slot(s) + L::ioff(kPre));
     const double* se = reinterpret_cast<const double*>(slot(s) + L::eoff(kPre));
     double* pb = pbuf + (t % 3) * PB;
     const bool wr_plane = kFused && ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
@@ -212,6 +232,10 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       } else if (kPre == 2) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], sv[c * CS + n]);
+      } else if (kPre == 3) {
+        const double iv = wsc * si[n];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = iv * sv[c * CS + n];
       } else {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];
@@ -246,6 +270,19 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
 
   double G0[3][4], A[3][4];
   double Ecur = 0.0;
+  // kEpi: the owner's epilogue operands (b, M^-1, mask) for the next node plane it
+  // writes are loaded one x-step ahead, so the global loads overlap the compute
+  double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0;
+  uint8_t efm = 0;
+  auto epi_load = [&](long long go) {
+    if (kEpi == 1 && owned) {
+      efm = epi.fixm[go];
+      einv = epi.invd[go];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
+    }
+  };
+  if (nunits > 2) epi_load(qp - q);
   prepass(0);
   if (nunits > 1) Ecur = prepass(1);
   __syncthreads();
@@ -285,10 +322,10 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         xch[buf][c][tz][ty] = C[2] + __shfl_up_sync(0xffffffffu, C[3], 1);
         S[c] = C[0] + __shfl_up_sync(0xffffffffu, C[1], 1);
         // p at the owner's node of plane ex (p-plane (t-1)%3 is rewritten only after this barrier)
-        pbase[c] = kDot ? pbuf[((t - 1) % 3) * PB + c * CS + tz * L::YW + ty + yoff] : 0.0;
+        pbase[c] = (kDot || kEpi) ? pbuf[((t - 1) % 3) * PB + c * CS + tz * L::YW + ty + yoff] : 0.0;
       }
       __syncthreads();
-      if (owned) {
+      if (owned && kEpi == 0) {
         // q is NOT masked here: the fixed-DOF mask is applied by the consumers
         // (k_update, k_residual, k_mask_fixed); p is exactly 0 on fixed DOFs, so
         // p.q is unaffected.  Keeps a latency-bound byte load off this loop.
@@ -298,8 +335,19 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
           qp[c * ncomp] = qv;
           if (kDot) dot = fma(pbase[c], qv, dot);
         }
+      } else if (owned) {
+        // damped-Jacobi sweep on the owner's node: out = v + w D^-1 (b - K v)
+        const double wd = wsc * einv;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          const double zn = ((efm >> c) & 1) ? 0.0 : fma(wd, eb[c] - qv, pbase[c]);
+          qp[c * ncomp] = zn;
+          dot = fma(eb[c], zn, dot);
+        }
       }
       qp += nplane;
+      if (t + 1 < nunits) epi_load(qp - q);
     } else {
       __syncthreads();
     }
@@ -313,7 +361,20 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       }
   }
 
-  if (kDot) {
+  if (kEpi == 1) {
+    __shared__ double tot[1];
+    double vv[1] = {dot};
+    if (grid_reduce<1>(vv, partials, counter, tot) && leader) {
+      const double rho = tot[0];
+      if (!(rho > 0.0) || !isfinite(rho)) {
+        st->status = 3;
+        st->done = 1;
+      } else {
+        st->beta = st->fresh ? 0.0 : rho / st->rz;
+        st->rz = rho;
+      }
+    }
+  } else if (kDot) {
     __shared__ double tot[1];
     double vv[1] = {dot};
     if (grid_reduce<1>(vv, partials, counter, tot) && leader) {

@@ -15,6 +15,7 @@
 // matvec.
 #pragma once
 #include "common.cuh"
+#include "matvec_wht.cuh"
 
 namespace topo {
 
@@ -30,12 +31,15 @@ struct LvGeo {
   __host__ __device__ long long nel() const { return (long long)nx * ny * nz; }
 };
 
-// node k of the (nx+1)(ny+1)(nz+1) enumeration, iy fastest (coalesced)
+// node k of the (nx+1)(ny+1)(nz+1) enumeration, iy fastest (coalesced); 32-bit
+// arithmetic (init validates node counts < 2^31)
 __device__ __forceinline__ void lv_decode(const LvGeo& L, long long k, int& ix, int& iy, int& iz) {
-  iy = (int)(k % (L.ny + 1));
-  const long long t = k / (L.ny + 1);
-  iz = (int)(t % (L.nz + 1));
-  ix = (int)(t / (L.nz + 1));
+  const unsigned kk = (unsigned)k, ny1 = (unsigned)(L.ny + 1), nz1 = (unsigned)(L.nz + 1);
+  const unsigned t = kk / ny1;
+  iy = (int)(kk - t * ny1);
+  const unsigned u = t / nz1;
+  iz = (int)(t - u * nz1);
+  ix = (int)u;
 }
 
 __constant__ double c_mg_diag8[8 * 24];       // diag of M_c (level-1 Galerkin from fine E)
@@ -426,6 +430,199 @@ k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __re
       }
     }
     KC[id] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Level 1 matrix-free: y = P^T K(E) P x, element by element in the Walsh
+// domain.  With H the unnormalised +-1 transform of the 8 corners (natural
+// index k = ax + 2 ay + 4 az, entry (-1)^{popcount(m & k)}) and KE = H^T B H
+// (B block-diagonal, wht_block), the Galerkin element matrix of a coarse
+// element is K1_e = H^T [ sum_c E_c T_c^T B T_c ] H, where T_c = H P_c H^-1
+// is, per axis, [[1, s/2], [0, 1/2]] on (sum, difference) pairs (s = +1 for
+// the lower child, -1 for the upper).  ~1650 flops per coarse element instead
+// of a fine matvec on P x plus two transfers.  Two phases for determinism:
+// phase 1 writes each element's 24 outputs, phase 2 sums them per node.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void fwht8(double v[8]) {
+#pragma unroll
+  for (int b = 1; b < 8; b <<= 1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (!(k & b)) {
+        const double u = v[k], w = v[k | b];
+        v[k] = u + w;
+        v[k | b] = u - w;
+      }
+}
+
+constexpr int kL1Block = 128;
+__global__ void __launch_bounds__(kL1Block, 3)
+k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const double* __restrict__ x,
+             double* __restrict__ Y, const DevState* st) {
+  MG_GATE(st);
+  const long long nel = L.nel();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
+       e += (long long)gridDim.x * blockDim.x) {
+    const unsigned ee = (unsigned)e, ny = (unsigned)L.ny, nz = (unsigned)L.nz;
+    const unsigned t = ee / ny, ey = ee - t * ny, ex = t / nz, ez = t - ex * nz;
+    double W[3][8], Yh[3][8], Ech[8];
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch)     // child moduli first: independent loads off the compute chain
+      Ech[ch] = E[elem_idx(g, 2 * ex + (ch & 1), 2 * ey + ((ch >> 1) & 1), 2 * ez + (ch >> 2))];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long n = L.n(ex + (k & 1), ey + ((k >> 1) & 1), ez + (k >> 2));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        W[c][k] = x[n + c * L.ncomp];
+        Yh[c][k] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht8(W[c]);
+    // T_c = Lambda^-1 T''_c with T''_c = [[1, s/2], [0, 1]] per axis, so
+    // T_c^T B T_c = T''_c^T (Lambda^-1 B Lambda^-1) T''_c: one FMA per pair each way
+    // and the rescaled block constants c_wht1.
+#pragma unroll 1
+    for (int ch = 0; ch < 8; ++ch) {
+      double Ec = Ech[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (no local memory)
+      if (Ec == 0.0) continue;                                  // child outside the fine domain
+      double P[3][8], Q[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) P[c][m] = W[c][m];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double hs = ((ch >> d) & 1) ? -0.5 : 0.5;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int m = 0; m < 8; ++m)
+            if (!((m >> d) & 1)) P[c][m] = fma(hs, P[c][m | (1 << d)], P[c][m]);
+      }
+      wht_block_k(c_wht1, P, Ec, Q);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double hs = ((ch >> d) & 1) ? -0.5 : 0.5;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int m = 0; m < 8; ++m)
+            if (!((m >> d) & 1)) Q[c][m | (1 << d)] = fma(hs, Q[c][m], Q[c][m | (1 << d)]);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) Yh[c][m] += Q[c][m];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      fwht8(Yh[c]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Y[(long long)(3 * k + c) * nel + e] = Yh[c][k];
+    }
+  }
+}
+
+// phase 2: q_i = mask( sum over the <= 8 elements of i of Y[corner of i] )
+__global__ void __launch_bounds__(kBlock)
+k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict__ fix, double* __restrict__ q,
+               const DevState* st) {
+  MG_GATE(st);
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+      const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+      if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+      const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+      const int kc = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+      a0 += Y[(long long)(3 * kc) * nel + e];
+      a1 += Y[(long long)(3 * kc + 1) * nel + e];
+      a2 += Y[(long long)(3 * kc + 2) * nel + e];
+    }
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+    q[i] = (fm & 1) ? 0.0 : a0;
+    q[i + L.ncomp] = (fm & 2) ? 0.0 : a1;
+    q[i + 2 * L.ncomp] = (fm & 4) ? 0.0 : a2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stored levels are applied through an assembled 27-point block stencil
+// S[(b*9 + ci*3 + cj) * ncomp + i] (b = (dx+1) + 3(dy+1) + 9(dz+1), node
+// layout index i): 243 doubles per node instead of 576 per element, and no
+// element gathers.  Out-of-domain neighbours have zero blocks; pads of x are 0.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock)
+k_mg_stencil(LvGeo L, const double* __restrict__ K, double* __restrict__ S) {
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    for (int b = 0; b < 27; ++b) {
+      const int bx = b % 3 - 1, by = (b / 3) % 3 - 1, bz = b / 9 - 1;
+      double blk[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int dz = 0; dz < 2; ++dz)
+        for (int dx = 0; dx < 2; ++dx)
+          for (int dy = 0; dy < 2; ++dy) {
+            const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+            if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+            const int ax = 1 - dx, ay = 1 - dy, az = 1 - dz;          // corner of node i in e
+            const int cx = ax + bx, cy = ay + by, cz = az + bz;        // corner of node i + b
+            if (cx < 0 || cx > 1 || cy < 0 || cy > 1 || cz < 0 || cz > 1) continue;
+            const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+            const int a = mg_lidx(ax, ay, az), c = mg_lidx(cx, cy, cz);
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+              for (int cj = 0; cj < 3; ++cj) blk[ci * 3 + cj] += K[(long long)((3 * a + ci) * 24 + 3 * c + cj) * nel + e];
+          }
+#pragma unroll
+      for (int t = 0; t < 9; ++t) S[(long long)(b * 9 + t) * L.ncomp + i] = blk[t];
+    }
+  }
+}
+
+// q = mask(A x) through the stencil; thread per node, 27 neighbour 3-vectors.
+__global__ void __launch_bounds__(kBlock)
+k_mg_apply_st(LvGeo L, const double* __restrict__ S, const double* __restrict__ x,
+              const uint8_t* __restrict__ fix, double* __restrict__ q, const DevState* st) {
+  MG_GATE(st);
+  const long long tot = L.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const long long i = L.n(ix, iy, iz);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll 3
+    for (int b = 0; b < 27; ++b) {
+      // b = (dx+1) + 3 (dy+1) + 9 (dz+1); layout: x -> nplane, z -> NY, y -> 1
+      const long long j = i + (long long)(b % 3 - 1) * L.nplane + (long long)((b / 3) % 3 - 1) +
+                          (long long)(b / 9 - 1) * L.NY;
+      const double x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
+      const double* sb = S + (long long)(b * 9) * L.ncomp + i;
+      a0 = fma(sb[0], x0, fma(sb[L.ncomp], x1, fma(sb[2 * L.ncomp], x2, a0)));
+      a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, fma(sb[5 * L.ncomp], x2, a1)));
+      a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, fma(sb[8 * L.ncomp], x2, a2)));
+    }
+    const uint8_t fm = fix[i];
+    q[i] = (fm & 1) ? 0.0 : a0;
+    q[i + L.ncomp] = (fm & 2) ? 0.0 : a1;
+    q[i + 2 * L.ncomp] = (fm & 4) ? 0.0 : a2;
   }
 }
 

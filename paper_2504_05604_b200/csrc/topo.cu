@@ -109,6 +109,8 @@ struct MgLevel {
   LvGeo L{};
   double *x = nullptr, *b = nullptr, *t = nullptr, *invd = nullptr;   // 3*ncomp each
   double* K = nullptr;          // stored element matrices [576][nel] (stored levels)
+  double* S = nullptr;          // 27-point block stencil [243][ncomp] (stored levels that are smoothed)
+  double* Y = nullptr;          // level 1 matrix-free: per-element outputs [24][nel]
   uint8_t* fixm = nullptr;      // per node: bit c = DOF c fixed
   std::vector<uint8_t> hfix;    // host copy, external node order
   bool stored = false;
@@ -123,6 +125,7 @@ struct topo_ctx {
   double ke[576];
   double kd = 0.0;
   WhtK wht{};
+  WhtK wht1{};              // level-1 multigrid: block constants scaled by Lambda^-1 . Lambda^-1
   int tz = 8;               // z extent of a matvec CTA (threads 32 x tz)
   std::vector<int4> st_off;
   std::vector<double> st_w;
@@ -249,6 +252,10 @@ int ensure_constants(topo_ctx* ctx) {
             nzW[c][R][nzN[c][R]] = w[c][A][R];
             nzN[c][R]++;
           }
+    const WhtK& w0 = ctx->wht;
+    const WhtK w1{w0.k0 / 4, w0.o0 / 4, w0.k7 / 16, w0.o7 / 16, w0.a / 16, w0.b / 16, w0.r / 4, w0.s / 64};
+    ctx->wht1 = w1;
+    CU(cudaMemcpyToSymbolAsync(c_wht1, &ctx->wht1, sizeof(WhtK), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_diag8, ctx->mg_diag8, sizeof(ctx->mg_diag8), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzA, nzA, sizeof nzA, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzW, nzW, sizeof nzW, 0, cudaMemcpyHostToDevice, ctx->stream));
@@ -598,32 +605,35 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   return TOPO_OK;
 }
 
-template <int TZ, int kPre, bool kDot>
-int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish) {
+template <int TZ, int kPre, bool kDot, int kEpi>
+int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish,
+                const double* scale) {
   static bool attr_set = false;
   const int smem = MvSmem<TZ>::bytes(kPre);
   if (!attr_set) {
-    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
-  k_mv_wht<TZ, kPre, kDot><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
-                                                                   s.partials, s.counter, finish);
+  const MvEpi epi{s.r, s.invd, s.fixm};
+  k_mv_wht<TZ, kPre, kDot, kEpi><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
+                                                                         s.partials, s.counter, finish, scale, epi);
   ctx->launches++;
-  debug_sync(ctx, kPre == 1 ? "k_mv_wht<jacobi-fused>" : kPre == 2 ? "k_mv_wht<mg-fused>" : "k_mv_wht<plain>");
+  debug_sync(ctx, kPre == 1 ? "k_mv_wht<jacobi-fused>" : kPre == 2 ? "k_mv_wht<mg-fused>"
+                  : kPre == 3 ? "k_mv_wht<mg-presmooth>" : "k_mv_wht<plain>");
   return check_launch(ctx);
 }
 
-template <int kPre, bool kDot>
+template <int kPre, bool kDot, int kEpi = 0>
 int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CUtensorMap* pold, double* pnew,
-              double* q, int finish) {
+              double* q, int finish, const double* scale = nullptr) {
   MvMaps maps;
   maps.vin = vin;
   maps.pold = pold ? *pold : vin;
   maps.invd = s.m_invd;
   maps.E = s.m_E;
-  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot>(ctx, s, gate, maps, pnew, q, finish);
-  return launch_mv_t<8, kPre, kDot>(ctx, s, gate, maps, pnew, q, finish);
+  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot, kEpi>(ctx, s, gate, maps, pnew, q, finish, scale);
+  return launch_mv_t<8, kPre, kDot, kEpi>(ctx, s, gate, maps, pnew, q, finish, scale);
 }
 
 // q = K v for every slab (v ghosts exchanged first; v must be 0 on fixed DOFs)
@@ -805,6 +815,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CK(al((void**)&m.invd, sizeof(double) * 3 * m.L.ncomp));
     CK(al((void**)&m.fixm, m.L.ncomp));
     if (m.stored) CK(al((void**)&m.K, sizeof(double) * 576 * m.L.nel()));
+    if (m.stored && l < L - 1) CK(al((void**)&m.S, sizeof(double) * 243 * m.L.ncomp));
+    if (!m.stored) CK(al((void**)&m.Y, sizeof(double) * 24 * m.L.nel()));
     std::vector<uint8_t> lay(m.L.ncomp, 0);
     for (int iz = 0; iz <= h.nz; ++iz)
       for (int ix = 0; ix <= h.nx; ++ix)
@@ -889,6 +901,7 @@ int enqueue_mg_setup(topo_ctx* ctx) {
     }
     debug_sync(ctx, "k_mg_asm");
     LAUNCH(ctx, k_mg_diag_asm, grid_for(nn), m.L, m.K, m.fixm, m.invd);
+    if (m.S) LAUNCH(ctx, k_mg_stencil, grid_for(nn), m.L, m.K, m.S);
   }
   // smoother weights w_l = theta / lam_l (M5): kMgPowerSteps power steps per level
   const double* one = ctx->mg_om + 16;
@@ -963,24 +976,29 @@ int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin) {
   return launch_mv<0, false>(ctx, s, gate, vin, nullptr, nullptr, s.q, 0);
 }
 
-// t_l = A_l x_l on a coarse level (stored: element matrices; level 1: P^T K P)
+// t_l = A_l x_l on a coarse level (stored: block stencil; level 1: P^T K P matrix-free)
 int mg_apply(topo_ctx* ctx, int l, int gate) {
   Slab& s = ctx->slabs[0];
   MgLevel& m = ctx->mg[l];
   const DevState* gst = gate ? s.st : nullptr;
   if (m.stored) {
-    LAUNCH(ctx, k_mg_apply_asm, grid_for(m.L.nodes()), m.L, m.K, m.x, m.fixm, m.t, gst);
+    if (m.S) LAUNCH(ctx, k_mg_apply_st, grid_for(m.L.nodes()), m.L, m.S, m.x, m.fixm, m.t, gst);
+    else LAUNCH(ctx, k_mg_apply_asm, grid_for(m.L.nodes()), m.L, m.K, m.x, m.fixm, m.t, gst);   // coarsest (test hook)
     return check_launch(ctx);
   }
-  const LvGeo F = lv0(ctx);
-  LAUNCH(ctx, k_mg_prolong<false>, grid_for(F.nodes()), F, m.L, m.x, s.fixm, s.w, gst);
-  CK(mg_mv0(ctx, gate, s.m_w));
-  LAUNCH(ctx, k_mg_restrict<false>, grid_for(m.L.nodes()), F, m.L, s.q, s.q, s.fixm, m.fixm, m.t, gst);
+  // level 1: P^T K(E) P matrix-free in the Walsh domain (two deterministic phases)
+  {
+    const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
+    k_mg_l1_elem<<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, m.x, m.Y, gst);
+    ctx->launches++;
+    debug_sync(ctx, "k_mg_l1_elem");
+  }
+  LAUNCH(ctx, k_mg_l1_gather, grid_for(m.L.nodes()), m.L, m.Y, m.fixm, m.t, gst);
   return check_launch(ctx);
 }
 
-// One V-cycle on level l (level 0: b = r, x = z; `dot`: the last fine sweep
-// computes rho = r.z and beta for the PCG).
+// One V-cycle on level l (level 0: b = r; the result lands in s.w and the last
+// fine sweep also sets rho = r.V(r) and beta for the PCG; `dot` is unused).
 int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size(), nu = ctx->prm.mg_nu;
@@ -995,22 +1013,22 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
   if (l == 0) {
     const LvGeo F = lv0(ctx);
     const int gF = grid_for(F.nodes());
-    LAUNCH(ctx, (k_mg_jacobi<0, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+    // first sweep from z = 0 fused into the matvec's load: z = w D^-1 r, q = K z
+    CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
+    for (int k = 1; k < nu; ++k) {
+      LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+      CK(mg_mv0(ctx, gate, s.m_z));
+    }
+    LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), F, n1.L, s.r, s.q, s.fixm, n1.fixm, n1.b, gst);
+    CK(enqueue_vcycle(ctx, 1, gate, false));
+    LAUNCH(ctx, k_mg_prolong<true>, gF, F, n1.L, n1.x, s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
       CK(mg_mv0(ctx, gate, s.m_z));
       LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
     }
-    CK(mg_mv0(ctx, gate, s.m_z));
-    LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), F, n1.L, s.r, s.q, s.fixm, n1.fixm, n1.b, gst);
-    CK(enqueue_vcycle(ctx, 1, gate, false));
-    LAUNCH(ctx, k_mg_prolong<true>, gF, F, n1.L, n1.x, s.fixm, s.z, gst);
-    for (int k = 1; k <= nu; ++k) {
-      CK(mg_mv0(ctx, gate, s.m_z));
-      if (dot && k == nu)
-        LAUNCH(ctx, (k_mg_jacobi<2, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
-      else
-        LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
-    }
+    // last sweep fused into the matvec epilogue: w = z + w D^-1 (r - K z) (the
+    // V-cycle result lives in s.w), rho = r.w and beta for the PCG
+    CK((launch_mv<0, false, 1>(ctx, s, gate, s.m_z, nullptr, nullptr, s.w, 0, om)));
     return check_launch(ctx);
   }
   MgLevel& m = ctx->mg[l];
@@ -1039,7 +1057,7 @@ int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
   double* pnew = parity ? s.p0 : s.p1;
   double* pprev = parity ? s.p1 : s.p0;
-  CK((launch_mv<2, true>(ctx, s, 1, s.m_z, pold, pnew, s.q, 1)));
+  CK((launch_mv<2, true>(ctx, s, 1, s.m_w, pold, pnew, s.q, 1)));   // p = V(r) + beta p, V(r) in s.w
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
   if (parity)
     LAUNCH(ctx, (k_update<true, true>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
@@ -1382,7 +1400,7 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   for (MgLevel& m : ctx->mg) {
-    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.fixm};
+    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.fixm};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -2027,7 +2045,7 @@ int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
     LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.r);
   CK(check_launch(ctx));
   CK(enqueue_vcycle(ctx, 0, 0, false));
-  return download_nodes(ctx, &Slab::z, z);
+  return download_nodes(ctx, &Slab::w, z);   // the V-cycle result (last sweep fused into the matvec)
 }
 
 void topo_destroy(topo_ctx* ctx) { free_ctx(ctx); }
