@@ -82,19 +82,20 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(cfg, world):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the fused matvec from the
-    newest committed ncu --set full capture (profiles/), or None."""
+def ncu_traffic(cfg, world, keys):
+    """sum over `keys` of dram__bytes_read.sum + dram__bytes_write.sum (one launch
+    each) from the newest committed ncu --set full capture that has them
+    (profiles/r*_ncu_cfg<cfg>*.json), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_cfg%d.json" % cfg)))
-    if not files or world != 1:
+    if world != 1:
         return None
-    try:
-        d = json.load(open(files[-1]))
-        k = next(v for n, v in d.items() if n.startswith("k_mv_wht"))
-        return (k["dram_read_GB"] + k["dram_write_GB"]) * 1e9
-    except Exception:
-        return None
+    for fn in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_cfg%d*.json" % cfg)), reverse=True):
+        try:
+            d = json.load(open(fn))
+            return sum((d[k]["dram_read_GB"] + d[k]["dram_write_GB"]) * 1e9 for k in keys), os.path.basename(fn)
+        except Exception:
+            continue
+    return None
 
 
 def dist_env():
@@ -209,13 +210,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-ncg", type=int, default=None)
     ap.add_argument("--ref-slab", type=int, default=8)
+    ap.add_argument("--precond", default="auto", choices=["auto", "mg", "jacobi"],
+                    help="PCG preconditioner (auto: geometric multigrid on one GPU, Jacobi on x-slabs)")
+    ap.add_argument("--mg-coarse-max", type=int, default=0, help="coarsest MG level DOF bound (0 = library auto)")
     args = ap.parse_args()
 
     from workloads import make_problem
     if args.e2e_steps is None:
         args.e2e_steps = args.steps
     world, rank, local = dist_env()
-    p, f, fx, pas = make_problem(args.config)
+    p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max)
 
     if args.impl == "reference":
         run_reference(args, p, world, rank)
@@ -282,6 +286,9 @@ def main():
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     launches = pr.timings()["kernel_launches"] - l0
     mv_ms, mv_samples = pr.kernel_time()
+    kt = [pr.kernel_time_k(k) for k in range(3)]
+    mg_levels = pr.mg_levels()
+    use_mg = bool(mg_levels) and pr.timings()["mg_fallbacks"] == 0
     pr.profile(False)
     clocks = clk.summary()
     s_per_iter = ms_total / 1e3 / args.steps
@@ -324,20 +331,40 @@ def main():
 
     peaks, peaks_src = load_peaks()
     hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-    # dominant kernel: the fused PCG matvec k_mv_wht<fused,dot>; algorithmic bytes per
-    # launch = read r (24 B/node), M^-1 (8 B/node), p_old (24 B/node), fixed mask (1 B/node),
-    # E (8 B/el); write p_new (24 B/node), q (24 B/node)  -> 105 B/node + 8 B/el
     own_el = n_el // world
     own_nd = n_nd // world
-    mv_bytes = 105 * own_nd + 8 * own_el
-    achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
-    traffic = ncu_traffic(args.config, world)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-            "traffic_source": "profiles/r*_ncu_cfg%d.json (ncu --set full, one launch)" % args.config
-            if traffic else None,
-            "kernel": "k_mv_wht<fused,dot> (p = M^-1 r + beta p; q = K p; p.q)", "samples": mv_samples,
-            "mean_ms": mv_ms, "bytes_per_launch": mv_bytes, "peak_source": peaks_src}
+    if use_mg:
+        # dominant kernel: the TMA-fed WHT matvec k_mv_wht, three variants per
+        # MG-PCG iteration, algorithmic bytes per launch:
+        #   <2,1,0> PCG   p = V(r) + beta p, q = K p, p.q : read V(r) 24 + p_old 24, write p 24 + q 24 B/node
+        #   <3,0,0> pre   z = w D^-1 r, q = K z          : read r 24 + D^-1 8, write z 24 + q 24 B/node
+        #   <0,0,1> post  z + w D^-1 (r - K z), r.(..)   : read z 24 + r 24 + D^-1 8 + mask 1, write 24 B/node
+        # each + E (8 B/el)
+        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,0>", 80, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
+        per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
+                "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
+               for n, b, t in var]
+        tot_b = sum(v["bytes_per_launch"] for v in per)
+        tot_ms = sum(v["mean_ms"] for v in per)
+        achieved = tot_b / (tot_ms * 1e-3) / 1e9 if tot_ms > 0 else None
+        tr = ncu_traffic(args.config, world, [v["kernel"] for v in per])
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": tr[0] if tr else None,
+                "traffic_source": (f"profiles/{tr[1]} (ncu --set full, one launch of each variant)" if tr else None),
+                "kernel": "k_mv_wht (3 variants per MG-PCG iteration; bytes and time summed)",
+                "bytes_per_launch": tot_b, "mean_ms": tot_ms, "variants": per, "peak_source": peaks_src}
+    else:
+        # dominant kernel: the fused PCG matvec k_mv_wht<8,1,1,0>; algorithmic bytes per
+        # launch = read r (24 B/node), M^-1 (8 B/node), p_old (24 B/node), fixed mask (1 B/node),
+        # E (8 B/el); write p_new (24 B/node), q (24 B/node)  -> 105 B/node + 8 B/el
+        mv_bytes = 105 * own_nd + 8 * own_el
+        achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
+        tr = ncu_traffic(args.config, world, ["k_mv_wht<8,1,1>"])
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": tr[0] if tr else None,
+                "traffic_source": f"profiles/{tr[1]} (ncu --set full, one launch)" if tr else None,
+                "kernel": "k_mv_wht<8,1,1,0> (p = M^-1 r + beta p; q = K p; p.q)", "samples": mv_samples,
+                "mean_ms": mv_ms, "bytes_per_launch": mv_bytes, "peak_source": peaks_src}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -357,7 +384,9 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_total / args.steps, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload_config(args, p, world),
+                "config": dict(workload_config(args, p, world),
+                               precond="multigrid" if use_mg else "jacobi",
+                               mg_levels=[list(d) for d in mg_levels] if use_mg else None),
                 "matvec_gdofs": gdofs, "matvec_ms": mv_standalone_ms,
                 "cg_iters_per_step": cg_timed, "cg_iters_warmup": cg_warm,
                 "ms_per_cg_iter": [ph["ms_solve"] / max(1, n) for ph, n in zip(phase, cg_timed)],

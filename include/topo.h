@@ -118,8 +118,10 @@ typedef struct {
   int32_t precond;
   int32_t mg_nu;              /* damped-Jacobi sweeps before and after the coarse correction (>= 1) */
   double  mg_omega;           /* theta in (0, 2): level-l Jacobi weight w_l = theta / lam_l, lam_l the
-                                 Rayleigh quotient of D^-1 A_l after 8 power steps (default 1.6)   */
-  int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (<= 4096) */
+                                 Rayleigh quotient of D^-1 A_l after 8 power steps (default 1.4: the
+                                 8-step estimate is 0.80-0.95 of lam_max, so w lam_max <= 1.75)   */
+  int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (24..8192;
+                                 0 = auto: min(5000, max(1000, n_dof / 2000)))                     */
 } topo_params;
 
 #define TOPO_PRECOND_JACOBI 0
@@ -253,6 +255,11 @@ int topo_get_timings(const topo_ctx *ctx, topo_timings *t);
  * the number of samples since the last reset.                               */
 int topo_profile(topo_ctx *ctx, int32_t enable);
 int topo_kernel_time(topo_ctx *ctx, double *mean_ms, int64_t *samples);
+/* Same for the fine-level matvec variants of a multigrid PCG iteration:
+ * which = 0: the PCG matvec (as topo_kernel_time); 1: the V-cycle's first sweep
+ * fused into the matvec (z = w D^-1 r, q = K z); 2: its last sweep fused into the
+ * matvec epilogue (z + w D^-1 (r - K z), rho).                                */
+int topo_kernel_time_k(topo_ctx *ctx, int32_t which, double *mean_ms, int64_t *samples);
 
 /* The element stiffness the library uses (24x24 row-major, unit cube,
  * E = 1, 2x2x2 Gauss; "pre-computed").  No context needed.    */

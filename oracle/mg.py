@@ -28,7 +28,8 @@ M1-M6), each step in plain NumPy/SciPy, no blocking or fusion:
                  with w_l = theta / lam_l, lam_l = Rayleigh quotient of D^-1 A_l
                  after k power steps from a fixed hash-generated start vector
                  (lam_l <= lam_max: a fixed w would diverge where lam_max(D^-1 A)
-                 exceeds 2/w, which random densities reach: lam_max ~ 4.7)
+                 exceeds 2/w, which random densities reach: lam_max ~ 4.7).  8 steps
+                 estimate 0.80-0.95 of lam_max, so theta = 1.4 keeps w lam_max <= 1.75
   M6 coarsest    exact solve (dense Cholesky) on the coarsest level; coarsening
                  stops at the first level with <= coarse_max DOFs
 The outer Krylov method is the same PCG as solve_jacobi_cg (stopping on the
@@ -178,7 +179,7 @@ def lambda_estimate(lv, k=8):
     return float((v @ (A @ v)) / (v @ (d * v)))
 
 
-def smoother_weights(levels, theta=1.6, k=8):
+def smoother_weights(levels, theta=1.4, k=8):
     """w_l = theta / lam_l on every level but the coarsest (M5)."""
     for lv in levels[:-1]:
         lv["lam"] = lambda_estimate(lv, k)
@@ -219,7 +220,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
     return x
 
 
-def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
+def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.4, nu=1, coarse_max=1000,
                max_iter=10000, u0=None, power_steps=8):
     """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
     TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""

@@ -333,71 +333,117 @@ k_filter(Geo g, int nst, const double* __restrict__ a, const double* __restrict_
 }
 
 // ===========================================================================
-// A7  OC bisection (§2.3).  One pass evaluates xnew(lmid) and the
-// volume V(lmid): mode 0 uses V = sum_j dv~_j xnew_j (= sum_{i in D} xPhys_i,
-// H symmetric), modes 1/2 V = sum_{j in D} xnew_j.
+// A7  OC bisection (§2.3).  xnew(lambda) = max(0, x-m, min(1, x+m,
+// x sqrt(max(0, -dc~/(dv~ lambda))))); mode 0 volume V = sum_j dv~_j xnew_j
+// (= sum_{i in D} xPhys_i, H symmetric; R26), modes 1/2 V = sum_{j in D}
+// xnew_j.
+//  * k_oc_prep stores A = x sqrt(max(0, -dc~/dv~)) once (0 on passive elements
+//    and pads), so a candidate is A / sqrt(lambda) and a pass needs no division,
+//    square root, index decode or passive mask (x = A = 0 there gives xnew = 0).
+//  * One pass evaluates the 7 midpoints of the next 3 bisection levels (heap
+//    order) and the last block walks the tree exactly as the sequential loop
+//    would (same lmid arithmetic, same strict V > target test, stop on the
+//    bracket tolerance), so ~80 passes become ~27.
 // ===========================================================================
-__device__ __forceinline__ double oc_candidate(double x, double dcf, double dvf, double lmid,
-                                              double move) {
-  const double cand = x * sqrt(fmax(0.0, -dcf / (dvf * lmid)));
-  return fmax(0.0, fmax(x - move, fmin(1.0, fmin(x + move, cand))));
+constexpr int kOcCand = 7;
+
+__device__ __forceinline__ double oc_xnew(double x, double A, double s, double move) {
+  return fmax(0.0, fmax(x - move, fmin(1.0, fmin(x + move, A * s))));
 }
 
-__device__ __forceinline__ void oc_finish_pass(DevState* st, double vol) {
-  st->vol = vol;
-  if (vol > st->target) st->l1 = st->lmid;
-  else st->l2 = st->lmid;
-  st->oc_pass += 1;
-  st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > st->oc_tol) ? 1 : 0;
-  if (st->oc_active) st->lmid = 0.5 * (st->l2 + st->l1);
+// heap-ordered midpoints lam[1..7] of 3 bisection levels below the bracket [l1, l2]
+__device__ __forceinline__ void oc_tree(double l1, double l2, double lam[kOcCand + 1]) {
+  double a[kOcCand + 1], b[kOcCand + 1];
+  a[1] = l1;
+  b[1] = l2;
+#pragma unroll
+  for (int k = 1; k <= kOcCand; ++k) {
+    lam[k] = 0.5 * (b[k] + a[k]);
+    if (2 * k <= kOcCand) {
+      a[2 * k] = a[k];          // V <= target: l2 = lmid
+      b[2 * k] = lam[k];
+      a[2 * k + 1] = lam[k];    // V > target: l1 = lmid
+      b[2 * k + 1] = b[k];
+    }
+  }
+}
+
+__device__ __forceinline__ void oc_walk(DevState* st, const double* V) {
+  double lam[kOcCand + 1];
+  oc_tree(st->l1, st->l2, lam);
+  int k = 1;
+  for (int lvl = 0; lvl < 3 && st->oc_active; ++lvl) {
+    st->lmid = lam[k];
+    st->vol = V[k - 1];
+    if (V[k - 1] > st->target) {
+      st->l1 = lam[k];
+      k = 2 * k + 1;
+    } else {
+      st->l2 = lam[k];
+      k = 2 * k;
+    }
+    st->oc_pass += 1;
+    st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > st->oc_tol) ? 1 : 0;
+  }
 }
 
 __global__ void __launch_bounds__(kBlock)
-k_oc_pass(Geo g, DevState* st, double move, int mode, const double* __restrict__ x,
-          const double* __restrict__ dcf, const double* __restrict__ dvf,
-          const uint8_t* __restrict__ passive, double* partials, unsigned int* counter,
-          int finish) {
-  if (!st->oc_active) return;
-  const double lmid = st->lmid;
+k_oc_prep(Geo g, const double* __restrict__ x, const double* __restrict__ dcf, const double* __restrict__ dvf,
+          const uint8_t* __restrict__ passive, double* __restrict__ A) {
   const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
-  double vol = 0.0;
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
        i += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
-    if (!decode_elem(g, i, ex, ey, ez) || passive[i]) continue;
-    const double xn = oc_candidate(x[i], dcf[i], dvf[i], lmid, move);
-    vol += (mode == 0) ? dvf[i] * xn : xn;
+    const bool ok = decode_elem(g, i, ex, ey, ez) && !passive[i];
+    A[i] = ok ? x[i] * sqrt(fmax(0.0, -dcf[i] / dvf[i])) : 0.0;
   }
-  __shared__ double tot[1];
-  double v[1] = {vol};
-  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) {
-    if (finish) oc_finish_pass(st, tot[0]);
-    else st->sums[0] = tot[0];
+}
+
+template <int MODE0>
+__global__ void __launch_bounds__(kBlock)
+k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const double* __restrict__ A,
+          const double* __restrict__ dvf, double* partials, unsigned int* counter, int finish) {
+  if (!st->oc_active) return;
+  double lam[kOcCand + 1], sc[kOcCand], vol[kOcCand];
+  oc_tree(st->l1, st->l2, lam);
+#pragma unroll
+  for (int k = 0; k < kOcCand; ++k) {
+    sc[k] = 1.0 / sqrt(lam[k + 1]);
+    vol[k] = 0.0;
+  }
+  const unsigned b0 = (unsigned)(g.H * g.eplane), e0 = (unsigned)((g.H + g.nex) * g.eplane);
+  for (unsigned i = b0 + blockIdx.x * blockDim.x + threadIdx.x; i < e0; i += gridDim.x * blockDim.x) {
+    const double xv = x[i], av = A[i], dv = MODE0 ? dvf[i] : 1.0;
+    // lambda-independent clamp bounds: xnew = min(hi, max(lo, A s)) (= oc_xnew exactly)
+    const double lo = fmax(0.0, xv - move), hi = fmin(1.0, xv + move);
+#pragma unroll
+    for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv, fmin(hi, fmax(lo, av * sc[k])), vol[k]);
+  }
+  __shared__ double tot[kOcCand];
+  if (grid_reduce<kOcCand>(vol, partials, counter, tot) && threadIdx.x == 0) {
+    if (finish) oc_walk(st, tot);
+    else
+      for (int k = 0; k < kOcCand; ++k) st->sums[k] = tot[k];
   }
 }
 __global__ void k_oc_finish(DevState* st) {
   if (!st->oc_active) return;
-  oc_finish_pass(st, st->sums[0]);
+  oc_walk(st, st->sums);
 }
 
-// final: xnew at the last evaluated lmid (l from the last pass), change =
-// max |xnew - x| over design elements, design-volume sum of xnew.
+// final: xnew at the last evaluated lmid, change = max |xnew - x| over design
+// elements, design-volume sum of xnew (passive elements and pads give 0).
 __global__ void __launch_bounds__(kBlock)
-k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x,
-           const double* __restrict__ dcf, const double* __restrict__ dvf,
-           const uint8_t* __restrict__ passive, double* __restrict__ xnew, double* partials,
-           unsigned int* counter) {
-  const double lmid = st->lmid;   // not advanced after the last pass (oc_active == 0)
+k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const double* __restrict__ A,
+           double* __restrict__ xnew, double* partials, unsigned int* counter) {
+  const double lmid = st->lmid;   // the last evaluated midpoint
   const int any = st->oc_pass > 0;
-  const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
+  const double sc = any ? 1.0 / sqrt(lmid) : 0.0;
+  const unsigned b0 = (unsigned)(g.H * g.eplane), e0 = (unsigned)((g.H + g.nex) * g.eplane);
   double chg = 0.0, vsum = 0.0;
-  for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
-       i += (long long)gridDim.x * blockDim.x) {
-    int ex, ey, ez;
-    if (!decode_elem(g, i, ex, ey, ez)) continue;
-    if (passive[i]) { xnew[i] = 0.0; continue; }
+  for (unsigned i = b0 + blockIdx.x * blockDim.x + threadIdx.x; i < e0; i += gridDim.x * blockDim.x) {
     const double xo = x[i];
-    const double xn = any ? oc_candidate(xo, dcf[i], dvf[i], lmid, move) : xo;
+    const double xn = any ? oc_xnew(xo, A[i], sc, move) : xo;
     xnew[i] = xn;
     chg = fmax(chg, fabs(xn - xo));
     vsum += xn;

@@ -98,8 +98,9 @@ struct MvMaps {
   CUtensorMap E;      // 3D {EY, EZ, NEXL}
 };
 
-// kEpi = 1 epilogue operands (multigrid post-smoothing fused into the matvec):
-// out = mask(v + w M^-1 (b - K v)) and rho = b . out, with b = r of the PCG.
+// Epilogue operands (multigrid V-cycle, b = r of the PCG):
+//   kEpi = 1: out = mask(v + w M^-1 (b - K v)) and rho = b . out (last sweep)
+//   kEpi = 2: out = mask(b - K v)  (the residual the restriction reads)
 struct MvEpi {
   const double* b;          // 3 * ncomp
   const double* invd;       // per node
@@ -275,9 +276,9 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0;
   uint8_t efm = 0;
   auto epi_load = [&](long long go) {
-    if (kEpi == 1 && owned) {
+    if (kEpi != 0 && owned) {
       efm = epi.fixm[go];
-      einv = epi.invd[go];
+      if (kEpi == 1) einv = epi.invd[go];
 #pragma unroll
       for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
     }
@@ -334,6 +335,12 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
           const double qv = S[c] + xch[buf][c][tz - 1][ty];
           qp[c * ncomp] = qv;
           if (kDot) dot = fma(pbase[c], qv, dot);
+        }
+      } else if (owned && kEpi == 2) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          qp[c * ncomp] = ((efm >> c) & 1) ? 0.0 : eb[c] - qv;
         }
       } else if (owned) {
         // damped-Jacobi sweep on the owner's node: out = v + w D^-1 (b - K v)

@@ -633,7 +633,7 @@ k_mg_apply_st(LvGeo L, const double* __restrict__ S, const double* __restrict__ 
 // dmap[level idx of DOF] = dense index or -1 (fixed / pad).  Thread per node:
 // it owns (zeroes and fills) its rows; no atomics.
 __global__ void __launch_bounds__(kBlock)
-k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ dmap, int n,
+k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ dmap, int ld,
                 double* __restrict__ A) {
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -641,13 +641,9 @@ k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ d
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
     const long long i = L.n(ix, iy, iz);
-    int rows[3];
+    int rows[3];   // (A is zeroed beforehand; each row is owned by one thread)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      rows[c] = dmap[i + c * L.ncomp];
-      if (rows[c] >= 0)
-        for (int j = 0; j < n; ++j) A[(long long)rows[c] * n + j] = 0.0;
-    }
+    for (int c = 0; c < 3; ++c) rows[c] = dmap[i + c * L.ncomp];
     for (int dz = 0; dz < 2; ++dz)
       for (int dx = 0; dx < 2; ++dx)
         for (int dy = 0; dy < 2; ++dy) {
@@ -663,11 +659,90 @@ k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ d
 #pragma unroll
               for (int ci = 0; ci < 3; ++ci)
                 if (rows[ci] >= 0)
-                  A[(long long)rows[ci] * n + col] += K[(long long)((3 * a + ci) * 24 + 3 * bb + cj) * nel + e];
+                  A[(long long)rows[ci] * ld + col] += K[(long long)((3 * a + ci) * 24 + 3 * bb + cj) * nel + e];
             }
           }
         }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Blocked Gauss-Jordan inverse of the coarsest matrix (column-major, n_pad =
+// multiple of kGjB, padding = identity).  Step k over the block K:
+//   P = A_KK^-1 ; R = P A_K,: (R_:,K = 0) ; C = A_:,K (C_K,: = 0)
+//   A -= C R (rank-kGjB update, cuBLAS DGEMM) ; A_:,K = -C P (DGEMM) ;
+//   A_K,: = R ; A_KK = P.
+// The scalar step (kGjB = 1) is a_kk = 1/p, a_kj = a_kj/p, a_ik = -a_ik/p,
+// a_ij -= a_ik a_kj / p; SPD needs no pivoting (pivots are Schur-complement
+// diagonals).
+// ---------------------------------------------------------------------------
+constexpr int kGjB = 64;
+
+// P = inverse of the b x b diagonal block at (k0, k0) by scalar Gauss-Jordan in
+// shared memory (one CTA)
+__global__ void __launch_bounds__(1024)
+k_gj_block_inv(const double* __restrict__ A, int ld, int k0, double* __restrict__ P) {
+  extern __shared__ double sb[];           // [kGjB][kGjB] column-major
+  __shared__ double col[kGjB], row[kGjB];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int t = tid; t < kGjB * kGjB; t += nt) {
+    const int i = t % kGjB, j = t / kGjB;
+    sb[t] = A[(long long)(k0 + j) * ld + k0 + i];
+  }
+  __syncthreads();
+  for (int k = 0; k < kGjB; ++k) {
+    if (tid < kGjB) {
+      col[tid] = sb[k * kGjB + tid];       // a_ik
+      row[tid] = sb[tid * kGjB + k];       // a_kj
+    }
+    __syncthreads();
+    const double ip = 1.0 / col[k];
+    for (int t = tid; t < kGjB * kGjB; t += nt) {
+      const int i = t % kGjB, j = t / kGjB;
+      double v;
+      if (i == k && j == k) v = ip;
+      else if (i == k) v = row[j] * ip;
+      else if (j == k) v = -col[i] * ip;
+      else v = sb[t] - col[i] * row[j] * ip;
+      sb[t] = v;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < kGjB * kGjB; t += nt) P[t] = sb[t];
+}
+
+// C = A_:,K with rows K zeroed (n_pad x b, column-major)
+__global__ void __launch_bounds__(kBlock)
+k_gj_take_col(const double* __restrict__ A, int ld, int k0, double* __restrict__ C) {
+  const long long tot = (long long)ld * kGjB;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % ld), j = (int)(t / ld);
+    C[t] = (i >= k0 && i < k0 + kGjB) ? 0.0 : A[(long long)(k0 + j) * ld + i];
+  }
+}
+
+// R_:,K = 0 (R is b x n_pad column-major)
+__global__ void k_gj_zero_rk(double* __restrict__ R, int k0) {
+  for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < kGjB * kGjB; t += gridDim.x * blockDim.x) {
+    const int i = t % kGjB, j = t / kGjB;
+    R[(long long)(k0 + j) * kGjB + i] = 0.0;
+  }
+}
+
+// A_K,: = R, then A_KK = P
+__global__ void __launch_bounds__(kBlock)
+k_gj_put_row(double* __restrict__ A, int ld, int k0, const double* __restrict__ R, const double* __restrict__ P) {
+  const long long tot = (long long)ld * kGjB;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % kGjB), j = (int)(t / kGjB);
+    A[(long long)j * ld + k0 + i] = (j >= k0 && j < k0 + kGjB) ? P[(j - k0) * kGjB + i] : R[t];
+  }
+}
+
+// identity on the padding rows/columns [n, n_pad)
+__global__ void k_gj_pad(double* __restrict__ A, int n, int ld) {
+  for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < ld - n; t += gridDim.x * blockDim.x)
+    A[(long long)(n + t) * ld + n + t] = 1.0;
 }
 
 // One Gauss-Jordan pivot step (in place on SPD, no pivoting), ping-pong:
@@ -691,14 +766,14 @@ k_mg_gj_step(const double* __restrict__ a, double* __restrict__ o, int n, int k)
 
 // x[imap[r]] = sum_j Ainv[r][j] b[imap[j]]  (warp per row, fixed lane order)
 __global__ void __launch_bounds__(kBlock)
-k_mg_coarse_solve(const double* __restrict__ Ainv, int n, const long long* __restrict__ imap,
+k_mg_coarse_solve(const double* __restrict__ Ainv, int n, int ld, const long long* __restrict__ imap,
                   const double* __restrict__ b, double* __restrict__ x, const DevState* st) {
   MG_GATE(st);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
   for (int r = warp; r < n; r += nwarp) {
     double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(Ainv[(long long)r * n + j], b[imap[j]], s);
+    for (int j = lane; j < n; j += 32) s = fma(Ainv[(long long)r * ld + j], b[imap[j]], s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) x[imap[r]] = s;

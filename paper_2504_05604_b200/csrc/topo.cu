@@ -74,6 +74,40 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
+// Minimal cuBLAS binding (dlopen): only DGEMM, for the rank-kGjB updates of the
+// blocked Gauss-Jordan inverse of the coarsest multigrid matrix (a plain
+// library GEMM; every other step runs in this library's kernels).
+typedef struct cublasContext* cublasHandle_t;
+struct CublasApi {
+  void* h = nullptr;
+  int (*Create)(cublasHandle_t*) = nullptr;
+  int (*Destroy)(cublasHandle_t) = nullptr;
+  int (*SetStream)(cublasHandle_t, cudaStream_t) = nullptr;
+  int (*SetWorkspace)(cublasHandle_t, void*, size_t) = nullptr;
+  int (*Dgemm)(cublasHandle_t, int, int, int, int, int, const double*, const double*, int, const double*, int,
+               const double*, double*, int) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* cands[] = {"libcublas.so.12", "libcublas.so",
+                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12"};
+    for (const char* c : cands) {
+      h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { err = "cannot dlopen libcublas.so.12"; return false; }
+#define LD(name, sym) name = reinterpret_cast<decltype(name)>(dlsym(h, sym)); if (!name) { err = "missing " sym; return false; }
+    LD(Create, "cublasCreate_v2");
+    LD(Destroy, "cublasDestroy_v2");
+    LD(SetStream, "cublasSetStream_v2");
+    LD(SetWorkspace, "cublasSetWorkspace_v2");
+    LD(Dgemm, "cublasDgemm_v2");
+#undef LD
+    return true;
+  }
+};
+CublasApi g_cublas;
+constexpr int CUBLAS_OP_N_ = 0;
+
 struct TopoError {
   int code;
   std::string msg;
@@ -92,7 +126,8 @@ struct Slab {
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
   double *E = nullptr, *x = nullptr, *xphys = nullptr, *dc = nullptr, *dcf = nullptr,
-         *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ce = nullptr, *xnew = nullptr;
+         *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ce = nullptr, *xnew = nullptr,
+         *oca = nullptr;   // OC: A = x sqrt(max(0, -dc~/dv~))
   uint8_t* passive = nullptr;
   double* partials = nullptr;
   unsigned int* counter = nullptr;
@@ -142,13 +177,19 @@ struct topo_ctx {
   long long cg_batch_launches[2] = {0, 0};
   bool cg_profiled_graph[2] = {false, false};
   cudaGraphExec_t oc_exec = nullptr;
-  int oc_batch = 16;
+  int oc_batch = 14;                 // passes (3 bisection levels each) per OC graph launch
   long long oc_batch_launches = 0;
   // profiling
   bool profile = false;
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
   double prof_ms = 0.0;
   long long prof_n = 0;
+  // multigrid V-cycle fine matvecs (pre-smoothing kPre=3, post-smoothing kEpi=1):
+  // pe[0..1] and pe[2..3] bracket them in the first iteration of each batch
+  cudaEvent_t pe[4] = {};
+  double prof_ms_k[3] = {0, 0, 0};
+  long long prof_n_k[3] = {0, 0, 0};
+  bool prof_capture = false;   // set while enqueueing the profiled iteration
   // phase events
   cudaEvent_t ev[8] = {};
   topo_timings tim{};
@@ -161,7 +202,10 @@ struct topo_ctx {
   // geometric multigrid (level 0 = the fine slab; mg[0] unused)
   bool mg_on = false, mg_ready = false;
   std::vector<MgLevel> mg;
-  double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr, *mg_A1 = nullptr;
+  double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
+  double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
+  int mg_npad = 0;                   // coarsest dense size rounded up to kGjB
+  cublasHandle_t cublas = nullptr;
   double mg_diag8[8 * 24];
   int mg_n = 0;                      // free DOFs of the coarsest level
   int* mg_dmap = nullptr;            // coarsest: level DOF index -> dense index or -1
@@ -750,6 +794,12 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   }
   struct H { int nx, ny, nz; std::vector<uint8_t> fix; };
   std::vector<H> hs;
+  // coarsest size: explicit, or auto = min(5000, max(1000, n_dof / 2000)) DOFs
+  // (a larger exact coarse solve cuts MG-PCG iterations; its dense inverse is
+  // only worth it on large grids)
+  const long long ndof0 = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+  const long long coarse_max = P.mg_coarse_max > 0 ? P.mg_coarse_max
+                                                   : std::min<long long>(5000, std::max<long long>(1000, ndof0 / 2000));
   {
     H h{P.nelx, P.nely, P.nelz, {}};
     const long long nn = (long long)(h.nx + 1) * (h.ny + 1) * (h.nz + 1);
@@ -760,7 +810,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   }
   while (true) {
     const H& f = hs.back();
-    if (3LL * (f.nx + 1) * (f.ny + 1) * (f.nz + 1) <= P.mg_coarse_max) break;
+    if (3LL * (f.nx + 1) * (f.ny + 1) * (f.nz + 1) <= coarse_max) break;
     H c{(f.nx + 1) / 2, (f.ny + 1) / 2, (f.nz + 1) / 2, {}};
     if (c.nx == f.nx && c.ny == f.ny && c.nz == f.nz) break;
     auto fid = [&](int ix, int iy, int iz) { return (long long)iz * (f.nx + 1) * (f.ny + 1) + (long long)ix * (f.ny + 1) + iy; };
@@ -788,7 +838,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   long long nfree_c = 0;
   for (uint8_t m : hs.back().fix) nfree_c += 3 - __builtin_popcount(m & 7);
   const char* why = L < 2 ? "fewer than 2 levels (grid too small, or coarse Dirichlet DOFs violate property Q)"
-                  : nfree_c > 4096 ? "coarsest level has more than 4096 free DOFs" : nullptr;
+                  : nfree_c > 8192 ? "coarsest level has more than 8192 free DOFs" : nullptr;
   if (why) {
     if (P.precond == TOPO_PRECOND_MG) return set_err(ctx, TOPO_EINVAL, "multigrid hierarchy: %s", why);
     return TOPO_OK;
@@ -846,9 +896,19 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CK(al((void**)&ctx->mg_imap, sizeof(long long) * std::max<size_t>(1, imap.size())));
     CU(cudaMemcpy(ctx->mg_dmap, dmap.data(), sizeof(int) * dmap.size(), cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->mg_imap, imap.data(), sizeof(long long) * imap.size(), cudaMemcpyHostToDevice));
-    const size_t nn = (size_t)ctx->mg_n * ctx->mg_n;
-    CK(al((void**)&ctx->mg_A0, sizeof(double) * std::max<size_t>(1, nn)));
-    CK(al((void**)&ctx->mg_A1, sizeof(double) * std::max<size_t>(1, nn)));
+    ctx->mg_npad = (ctx->mg_n + kGjB - 1) / kGjB * kGjB;
+    const size_t np = (size_t)ctx->mg_npad;
+    CK(al((void**)&ctx->mg_A0, sizeof(double) * np * np));
+    CK(al((void**)&ctx->mg_C, sizeof(double) * np * kGjB));
+    CK(al((void**)&ctx->mg_R, sizeof(double) * np * kGjB));
+    CK(al((void**)&ctx->mg_P, sizeof(double) * kGjB * kGjB));
+    const size_t ws = 32u << 20;
+    CK(al((void**)&ctx->mg_ws, ws));
+    std::string err;
+    if (!g_cublas.load(err)) return set_err(ctx, TOPO_ECUDA, "%s", err.c_str());
+    if (g_cublas.Create(&ctx->cublas) != 0) return set_err(ctx, TOPO_ECUDA, "cublasCreate failed");
+    if (g_cublas.SetWorkspace(ctx->cublas, ctx->mg_ws, ws) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetWorkspace failed");
+    CU(cudaFuncSetAttribute(k_gj_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjB * kGjB * 8));
   }
   {
     std::vector<double> om(17, 1.0);
@@ -876,7 +936,7 @@ constexpr int kMgPowerSteps = 8;   // power steps of the smoother-weight estimat
 int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin);
 int mg_apply(topo_ctx* ctx, int l, int gate);
 
-double* mg_Ainv(const topo_ctx* ctx) { return (ctx->mg_n % 2 == 0) ? ctx->mg_A0 : ctx->mg_A1; }
+double* mg_Ainv(const topo_ctx* ctx) { return ctx->mg_A0; }
 
 // Per-design setup: level-1 diagonal, Galerkin element matrices, coarsest inverse.
 int enqueue_mg_setup(topo_ctx* ctx) {
@@ -933,11 +993,30 @@ int enqueue_mg_setup(topo_ctx* ctx) {
   }
   const MgLevel& c = ctx->mg[L - 1];
   const int n = ctx->mg_n;
-  LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, n, ctx->mg_A0);
-  for (int k = 0; k < n; ++k) {
-    const double* a = (k % 2 == 0) ? ctx->mg_A0 : ctx->mg_A1;
-    double* o = (k % 2 == 0) ? ctx->mg_A1 : ctx->mg_A0;
-    LAUNCH(ctx, k_mg_gj_step, grid_for((long long)n * n), a, o, n, k);
+  const int np = ctx->mg_npad;
+  double* A = ctx->mg_A0;
+  CU(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)np * np, ctx->stream));
+  LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, np, A);
+  if (np > n) LAUNCH(ctx, k_gj_pad, 1, A, n, np);
+  // blocked Gauss-Jordan (mg.cuh): A <- A^-1 in place
+  if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
+  const double d_one = 1.0, d_mone = -1.0, d_zero = 0.0;
+  for (int k0 = 0; k0 < np; k0 += kGjB) {
+    k_gj_block_inv<<<1, 1024, kGjB * kGjB * 8, ctx->stream>>>(A, np, k0, ctx->mg_P);
+    ctx->launches++;
+    // R = P A_K,:  (b x np)
+    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, kGjB, np, kGjB, &d_one, ctx->mg_P, kGjB, A + k0, np,
+                       &d_zero, ctx->mg_R, kGjB) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (row panel) failed");
+    k_gj_zero_rk<<<64, kBlock, 0, ctx->stream>>>(ctx->mg_R, k0);
+    ctx->launches++;
+    LAUNCH(ctx, k_gj_take_col, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_C);
+    // A -= C R  (rows/columns K untouched: C_K,: = 0, R_:,K = 0)
+    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, np, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_R, kGjB,
+                       &d_one, A, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (update) failed");
+    // A_:,K = -C P
+    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, kGjB, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_P, kGjB,
+                       &d_zero, A + (size_t)k0 * np, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (column panel) failed");
+    LAUNCH(ctx, k_gj_put_row, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
   }
   return check_launch(ctx);
 }
@@ -1006,20 +1085,26 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
   const double* om = ctx->mg_om + l;
   if (l == L - 1) {
     const MgLevel& c = ctx->mg[l];
-    LAUNCH(ctx, k_mg_coarse_solve, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_imap, c.b, c.x, gst);
+    LAUNCH(ctx, k_mg_coarse_solve, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_npad, ctx->mg_imap, c.b,
+           c.x, gst);
     return check_launch(ctx);
   }
   MgLevel& n1 = ctx->mg[l + 1];
   if (l == 0) {
     const LvGeo F = lv0(ctx);
     const int gF = grid_for(F.nodes());
-    // first sweep from z = 0 fused into the matvec's load: z = w D^-1 r, q = K z
-    CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
+    // first sweep from z = 0 fused into the matvec's load: z = w D^-1 r, and
+    // (nu = 1) the epilogue writes the residual r - K z for the restriction
+    if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[0], ctx->stream, cudaEventRecordExternal));
+    if (nu == 1) CK((launch_mv<3, false, 2>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
+    else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
+    if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
       LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
-      CK(mg_mv0(ctx, gate, s.m_z));
+      if (k < nu - 1) CK(mg_mv0(ctx, gate, s.m_z));
+      else CK((launch_mv<0, false, 2>(ctx, s, gate, s.m_z, nullptr, nullptr, s.q, 0, om)));
     }
-    LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), F, n1.L, s.r, s.q, s.fixm, n1.fixm, n1.b, gst);
+    LAUNCH(ctx, k_mg_restrict<false>, grid_for(n1.L.nodes()), F, n1.L, s.q, s.q, s.fixm, n1.fixm, n1.b, gst);
     CK(enqueue_vcycle(ctx, 1, gate, false));
     LAUNCH(ctx, k_mg_prolong<true>, gF, F, n1.L, n1.x, s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
@@ -1028,7 +1113,9 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
     }
     // last sweep fused into the matvec epilogue: w = z + w D^-1 (r - K z) (the
     // V-cycle result lives in s.w), rho = r.w and beta for the PCG
+    if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[2], ctx->stream, cudaEventRecordExternal));
     CK((launch_mv<0, false, 1>(ctx, s, gate, s.m_z, nullptr, nullptr, s.w, 0, om)));
+    if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[3], ctx->stream, cudaEventRecordExternal));
     return check_launch(ctx);
   }
   MgLevel& m = ctx->mg[l];
@@ -1052,7 +1139,10 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
 // one MG-PCG iteration: z = V(r) (rho, beta) ; p = z + beta p ; q = K p ; alpha ; u, r update
 int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   Slab& s = ctx->slabs[0];
-  CK(enqueue_vcycle(ctx, 0, 1, true));
+  ctx->prof_capture = prof_here;
+  const int rcv = enqueue_vcycle(ctx, 0, 1, true);
+  ctx->prof_capture = false;
+  CK(rcv);
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
   const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
   double* pnew = parity ? s.p0 : s.p1;
@@ -1137,6 +1227,12 @@ int solve_pass(topo_ctx* ctx, int mg, int* replacements_out, double* rr_true_out
           ctx->prof_ms += ms;
           ctx->prof_n++;
         }
+        if (mg)
+          for (int k = 0; k < 2; ++k)
+            if (cudaEventElapsedTime(&ms, ctx->pe[2 * k], ctx->pe[2 * k + 1]) == cudaSuccess) {
+              ctx->prof_ms_k[1 + k] += ms;
+              ctx->prof_n_k[1 + k]++;
+            }
       }
       it_prev = h.it;
       continue;
@@ -1276,11 +1372,15 @@ int do_filter_x(topo_ctx* ctx) {
 int enqueue_oc_batch(topo_ctx* ctx) {
   const int W = ctx->world, fin = (W == 1) ? 1 : 0;
   for (int i = 0; i < ctx->oc_batch; ++i) {
-    for (Slab& s : ctx->slabs)
-      LAUNCH(ctx, k_oc_pass, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, ctx->prm.move,
-             ctx->prm.filter_mode, s.x, s.dcf, s.dvf, s.passive, s.partials, s.counter, fin);
+    for (Slab& s : ctx->slabs) {
+      const int gr = grid_for((long long)s.g.nex * s.g.eplane);
+      if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY)
+        LAUNCH(ctx, k_oc_pass<1>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
+      else
+        LAUNCH(ctx, k_oc_pass<0>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
+    }
     if (!fin) {
-      CK(allreduce(ctx, 0, 1, 0));
+      CK(allreduce(ctx, 0, kOcCand, 0));
       for (Slab& s : ctx->slabs) { k_oc_finish<<<1, 1, 0, ctx->stream>>>(s.st); ctx->launches++; }
     }
   }
@@ -1312,6 +1412,7 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   for (Slab& s : ctx->slabs) {
     k_oc_init<<<1, 1, 0, ctx->stream>>>(s.st, P.oc_lmax, P.volfrac * (double)ctx->n_design, P.oc_tol);
     ctx->launches++;
+    LAUNCH(ctx, k_oc_prep, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.x, s.dcf, s.dvf, s.passive, s.oca);
   }
   CK(check_launch(ctx));
   if (!ctx->debug) CK(build_oc_graph(ctx));
@@ -1329,8 +1430,8 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
     if (++guard > 4096 / ctx->oc_batch) return set_err(ctx, TOPO_EBISECT, "OC bisection did not terminate");
   }
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_oc_final, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.dcf, s.dvf,
-           s.passive, s.xnew, s.partials, s.counter);
+    LAUNCH(ctx, k_oc_final, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.xnew,
+           s.partials, s.counter);
   CK(check_launch(ctx));
   CK(allreduce(ctx, 2, 2, 0x2));
   for (Slab& s : ctx->slabs)
@@ -1375,7 +1476,7 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   for (double** v : nv) CK(al((void**)v, nb));
   CK(al((void**)&s.invd, sizeof(double) * g.ncomp));
   CK(al((void**)&s.fixm, g.ncomp));
-  double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew};
+  double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew, &s.oca};
   for (double** v : ev) CK(al((void**)v, eb));
   CK(al((void**)&s.passive, g.nelloc));
   const MvGrid mg = mv_grid(ctx, g);
@@ -1393,7 +1494,7 @@ void free_ctx(topo_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
-    void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf,
+    void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
@@ -1405,16 +1506,20 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   {
-    void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_A0, ctx->mg_A1, ctx->mg_dmap, ctx->mg_imap, ctx->mg_om};
+    void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_A0, ctx->mg_C, ctx->mg_R, ctx->mg_P, ctx->mg_ws,
+                    ctx->mg_dmap, ctx->mg_imap, ctx->mg_om};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
   if (ctx->mg_setup_exec) cudaGraphExecDestroy(ctx->mg_setup_exec);
+  if (ctx->cublas) g_cublas.Destroy(ctx->cublas);
   for (cudaGraphExec_t g : ctx->cg_exec)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
   if (ctx->pe0) cudaEventDestroy(ctx->pe0);
   if (ctx->pe1) cudaEventDestroy(ctx->pe1);
+  for (cudaEvent_t e : ctx->pe)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->hstate) cudaFreeHost(ctx->hstate);
@@ -1442,8 +1547,8 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (p->precond < 0 || p->precond > 2) return set_err(ctx, TOPO_EINVAL, "precond must be 0, 1 or 2");
   if (p->mg_nu < 1 || p->mg_nu > 8) return set_err(ctx, TOPO_EINVAL, "mg_nu must be in [1, 8]");
   if (!(p->mg_omega > 0 && p->mg_omega < 2)) return set_err(ctx, TOPO_EINVAL, "mg_omega must be in (0, 2)");
-  if (p->mg_coarse_max < 24 || p->mg_coarse_max > 4096)
-    return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be in [24, 4096]");
+  if (p->mg_coarse_max != 0 && (p->mg_coarse_max < 24 || p->mg_coarse_max > 8192))
+    return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be 0 (auto) or in [24, 8192]");
   return TOPO_OK;
 }
 
@@ -1475,8 +1580,8 @@ void topo_params_default(topo_params* p) {
   p->cg_check_every = 0;
   p->precond = TOPO_PRECOND_AUTO;
   p->mg_nu = 1;
-  p->mg_omega = 1.6;
-  p->mg_coarse_max = 1000;
+  p->mg_omega = 1.4;
+  p->mg_coarse_max = 0;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }
@@ -1601,6 +1706,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   memset(ctx->hstate, 0, sizeof(DevState));
   cudaEventCreate(&ctx->pe0);
   cudaEventCreate(&ctx->pe1);
+  for (cudaEvent_t& e : ctx->pe) cudaEventCreate(&e);
   for (cudaEvent_t& e : ctx->ev) cudaEventCreate(&e);
   if (ctx->mode == TOPO_DIST_NCCL && W > 1) {
     std::string err;
@@ -1984,6 +2090,7 @@ int topo_profile(topo_ctx* ctx, int32_t enable) {
   ctx->profile = enable != 0;
   ctx->prof_ms = 0.0;
   ctx->prof_n = 0;
+  for (int k = 0; k < 3; ++k) ctx->prof_ms_k[k] = 0.0, ctx->prof_n_k[k] = 0;
   return TOPO_OK;
 }
 
@@ -1991,6 +2098,14 @@ int topo_kernel_time(topo_ctx* ctx, double* mean_ms, int64_t* samples) {
   if (!ctx) return TOPO_EINVAL;
   if (mean_ms) *mean_ms = ctx->prof_n ? ctx->prof_ms / ctx->prof_n : 0.0;
   if (samples) *samples = ctx->prof_n;
+  return TOPO_OK;
+}
+
+int topo_kernel_time_k(topo_ctx* ctx, int32_t which, double* mean_ms, int64_t* samples) {
+  if (!ctx || which < 0 || which > 2) return TOPO_EINVAL;
+  if (which == 0) return topo_kernel_time(ctx, mean_ms, samples);
+  if (mean_ms) *mean_ms = ctx->prof_n_k[which] ? ctx->prof_ms_k[which] / ctx->prof_n_k[which] : 0.0;
+  if (samples) *samples = ctx->prof_n_k[which];
   return TOPO_OK;
 }
 

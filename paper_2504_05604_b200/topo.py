@@ -32,7 +32,7 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            "topo_matvec_load", "topo_matvec_run", "topo_get", "topo_get_timings", "topo_profile",
            "topo_kernel_time", "topo_element_stiffness", "topo_count", "topo_last_error",
            "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition", "topo_snapshot", "topo_restore",
-           "topo_mg_levels", "topo_mg_apply", "topo_mg_vcycle"]
+           "topo_mg_levels", "topo_mg_apply", "topo_mg_vcycle", "topo_kernel_time_k"]
 
 
 class topo_params(C.Structure):
@@ -108,6 +108,7 @@ def _load():
         "topo_mg_levels": (I, [ctxp, P(C.c_int32), P(C.c_int32)]),
         "topo_mg_apply": (I, [ctxp, C.c_int32, D, D]),
         "topo_mg_vcycle": (I, [ctxp, D, D]),
+        "topo_kernel_time_k": (I, [ctxp, C.c_int32, D, P(C.c_int64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -351,6 +352,13 @@ class Problem:
         z = np.zeros(3 * self.n_nd)
         self._check(_lib.topo_mg_vcycle(self._ctx, _dp(b), _dp(z)), "topo_mg_vcycle")
         return z
+
+    def kernel_time_k(self, which):
+        """(mean ms, samples) of matvec variant `which` (0 PCG, 1 MG pre-sweep, 2 MG post-sweep)."""
+        m, n = C.c_double(), C.c_int64()
+        self._check(_lib.topo_kernel_time_k(self._ctx, int(which), C.byref(m), C.byref(n)),
+                    "topo_kernel_time_k")
+        return m.value, n.value
 
     def count(self, what):
         return int(_lib.topo_count(self._ctx, COUNTS[what]))

@@ -94,7 +94,7 @@ def test_mg_vcycle_parity(topo, dims, obst, nu):
 def test_mg_solve_parity(topo, dims, obst):
     p, f, fx, pas, x, K = _case(dims, obst, seed=2)
     uo = oracle.solve_direct(K, f, fx)
-    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=1)
+    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.4, nu=1)
     its = {}
     for pc in ("jacobi", "mg"):
         with topo.Problem(dict(p, precond=pc), f, fx, pas) as pr:

@@ -186,7 +186,7 @@ def test_start_vector_is_splitmix64():
 def test_lambda_estimate_bounds(seed):
     """Rayleigh quotient <= lam_max(D^-1 A) <= element bound lam_max(KE)/KE_ii
     (x^T A x = sum_e x_e^T E_e KE x_e <= lam(KE)/kd x^T D x), and the damped
-    smoother it sets is convergent: w lam_max < 2 for theta = 1.6."""
+    smoother it sets is convergent: w lam_max < 2 for theta = 1.4."""
     import scipy.sparse as sps
     import scipy.sparse.linalg as spla
     from workloads import random_density
