@@ -337,10 +337,11 @@ def main():
         # dominant kernel: the TMA-fed WHT matvec k_mv_wht, three variants per
         # MG-PCG iteration, algorithmic bytes per launch:
         #   <2,1,0> PCG   p = V(r) + beta p, q = K p, p.q : read V(r) 24 + p_old 24, write p 24 + q 24 B/node
-        #   <3,0,0> pre   z = w D^-1 r, q = K z          : read r 24 + D^-1 8, write z 24 + q 24 B/node
+        #   <3,0,2> pre   z = w D^-1 r, res = r - K z    : read r 24 + D^-1 8 (TMA) + r 24 + mask 1
+        #                                                  (epilogue), write z 24 + res 24 B/node
         #   <0,0,1> post  z + w D^-1 (r - K z), r.(..)   : read z 24 + r 24 + D^-1 8 + mask 1, write 24 B/node
         # each + E (8 B/el)
-        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,0>", 80, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
+        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 105, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
         per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
                 "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
                for n, b, t in var]

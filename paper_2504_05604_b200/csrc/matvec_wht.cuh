@@ -101,6 +101,7 @@ struct MvMaps {
 // Epilogue operands (multigrid V-cycle, b = r of the PCG):
 //   kEpi = 1: out = mask(v + w M^-1 (b - K v)) and rho = b . out (last sweep)
 //   kEpi = 2: out = mask(b - K v)  (the residual the restriction reads)
+//   kEpi = 3: out = mask(K v)      (power steps of the smoother-weight estimate)
 struct MvEpi {
   const double* b;          // 3 * ncomp
   const double* invd;       // per node
@@ -279,8 +280,9 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     if (kEpi != 0 && owned) {
       efm = epi.fixm[go];
       if (kEpi == 1) einv = epi.invd[go];
+      if (kEpi == 1 || kEpi == 2)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
+        for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
     }
   };
   if (nunits > 2) epi_load(qp - q);
@@ -336,11 +338,11 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
           qp[c * ncomp] = qv;
           if (kDot) dot = fma(pbase[c], qv, dot);
         }
-      } else if (owned && kEpi == 2) {
+      } else if (owned && (kEpi == 2 || kEpi == 3)) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double qv = S[c] + xch[buf][c][tz - 1][ty];
-          qp[c * ncomp] = ((efm >> c) & 1) ? 0.0 : eb[c] - qv;
+          qp[c * ncomp] = ((efm >> c) & 1) ? 0.0 : (kEpi == 2 ? eb[c] - qv : qv);
         }
       } else if (owned) {
         // damped-Jacobi sweep on the owner's node: out = v + w D^-1 (b - K v)

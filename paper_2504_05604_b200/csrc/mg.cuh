@@ -46,6 +46,7 @@ __constant__ double c_mg_diag8[8 * 24];       // diag of M_c (level-1 Galerkin f
 __constant__ signed char c_mg_nzA[8][8][8];   // child c, parent corner R -> child corners A with w != 0
 __constant__ double c_mg_nzW[8][8][8];
 __constant__ int c_mg_nzN[8][8];
+__constant__ unsigned short c_mg_upair[300];  // upper triangle (r <= s) of a 24x24 element matrix: r*24+s
 
 __host__ __device__ constexpr int mg_lidx(int a, int b, int c) { return 4 * c + (b ? (a ? 2 : 3) : (a ? 1 : 0)); }
 __device__ __forceinline__ int corner_dx(int a) { return (a == 1 || a == 2 || a == 5 || a == 6) ? 1 : 0; }
@@ -382,16 +383,22 @@ k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __rest
       Ef[f] = (fx < g.nelx && fy < g.nely && fz < g.nelz) ? E[elem_idx(g, fx, fy, fz)] : 0.0;
     }
   }
-  for (int k0 = 0; k0 < 576; k0 += kCh) {
+  // symmetric: the 300 upper-triangle entries, each written to (r, s) and (s, r)
+  for (int u0 = 0; u0 < 300; u0 += kCh) {
     __syncthreads();
-    for (int t = threadIdx.x; t < NT * kCh; t += blockDim.x) tb[t / kCh][t % kCh] = tab[(t / kCh) * 576 + k0 + t % kCh];
+    for (int t = threadIdx.x; t < NT * kCh; t += blockDim.x) {
+      const int u = u0 + t % kCh;
+      tb[t / kCh][t % kCh] = u < 300 ? tab[(t / kCh) * 576 + c_mg_upair[u]] : 0.0;
+    }
     __syncthreads();
     if (e < nel) {
-      for (int kk = 0; kk < kCh; ++kk) {
+      for (int kk = 0; kk < kCh && u0 + kk < 300; ++kk) {
         double s = 0.0;
 #pragma unroll
         for (int f = 0; f < NT; ++f) s = fma(Ef[f], tb[f][kk], s);
-        K[(long long)(k0 + kk) * nel + e] = s;
+        const int rs = c_mg_upair[u0 + kk], r = rs / 24, c = rs % 24;
+        K[(long long)rs * nel + e] = s;
+        K[(long long)(c * 24 + r) * nel + e] = s;
       }
     }
   }
@@ -403,11 +410,12 @@ k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __rest
 __global__ void __launch_bounds__(kBlock)
 k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __restrict__ KC) {
   const long long nelC = Cg.nel(), nelF = F.nel();
-  const long long tot = 576 * nelC;
+  const long long tot = 300 * nelC;      // symmetric: upper triangle, mirrored on write
   for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < tot;
        id += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(id / nelC);
-    const long long e = id - (long long)k * nelC;
+    const int u = (int)(id / nelC);
+    const long long e = id - (long long)u * nelC;
+    const int k = c_mg_upair[u];
     const int r = k / 24, s = k % 24, R = r / 3, i = r % 3, Sn = s / 3, j = s % 3;
     const int ey = (int)(e % Cg.ny);
     const long long t = e / Cg.ny;
@@ -429,7 +437,8 @@ k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __re
         acc = fma(wa, sb, acc);
       }
     }
-    KC[id] = acc;
+    KC[(long long)k * nelC + e] = acc;
+    KC[(long long)(s * 24 + r) * nelC + e] = acc;
   }
 }
 
@@ -529,9 +538,11 @@ k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const double* __restr
 }
 
 // phase 2: q_i = mask( sum over the <= 8 elements of i of Y[corner of i] )
+// (kScale: q_i = D^-1 mask(sum), the next power step's vector)
+template <bool kScale>
 __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict__ fix, double* __restrict__ q,
-               const DevState* st) {
+               const DevState* st, const double* __restrict__ invd) {
   MG_GATE(st);
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -552,6 +563,11 @@ k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict_
     }
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
+    if (kScale) {   // invd is 0 on fixed DOFs
+      a0 *= invd[i];
+      a1 *= invd[i + L.ncomp];
+      a2 *= invd[i + 2 * L.ncomp];
+    }
     q[i] = (fm & 1) ? 0.0 : a0;
     q[i + L.ncomp] = (fm & 2) ? 0.0 : a1;
     q[i + 2 * L.ncomp] = (fm & 4) ? 0.0 : a2;

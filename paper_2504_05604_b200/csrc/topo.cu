@@ -136,7 +136,7 @@ struct Slab {
   size_t stage_n = 0;
   double *u_b = nullptr, *x_b = nullptr, *xphys_b = nullptr;   // snapshot buffers
   // TMA descriptors of the matvec operands (built at init; pointers never change)
-  CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z;
+  CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z, m_q;
 };
 
 // One coarse multigrid level (l >= 1, M1-M6).
@@ -304,6 +304,10 @@ int ensure_constants(topo_ctx* ctx) {
     CU(cudaMemcpyToSymbolAsync(c_mg_nzA, nzA, sizeof nzA, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzW, nzW, sizeof nzW, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzN, nzN, sizeof nzN, 0, cudaMemcpyHostToDevice, ctx->stream));
+    unsigned short up[300];
+    for (int r = 0, u = 0; r < 24; ++r)
+      for (int c = r; c < 24; ++c) up[u++] = (unsigned short)(r * 24 + c);
+    CU(cudaMemcpyToSymbolAsync(c_mg_upair, up, sizeof up, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));   // host staging arrays go out of scope
   }
   if (!ctx->st_off.empty()) {
@@ -646,6 +650,7 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   CK(map_nodes(ctx, &s.m_invd, s.invd, s.g, 1));
   CK(map_elems(ctx, &s.m_E, s.E, s.g));
   CK(map_nodes(ctx, &s.m_z, s.z, s.g, 3));
+  CK(map_nodes(ctx, &s.m_q, s.q, s.g, 3));
   return TOPO_OK;
 }
 
@@ -933,6 +938,16 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 }
 
 constexpr int kMgPowerSteps = 8;   // power steps of the smoother-weight estimate (M5)
+
+// level-1 phase 1 (Walsh-domain Galerkin per coarse element), 128-thread CTAs
+int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst) {
+  Slab& s = ctx->slabs[0];
+  const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
+  k_mg_l1_elem<<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, m.x, m.Y, gst);
+  ctx->launches++;
+  debug_sync(ctx, "k_mg_l1_elem");
+  return check_launch(ctx);
+}
 int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin);
 int mg_apply(topo_ctx* ctx, int l, int gate);
 
@@ -957,7 +972,7 @@ int enqueue_mg_setup(topo_ctx* ctx) {
       ctx->launches++;
     } else {
       const MgLevel& f = ctx->mg[l - 1];
-      LAUNCH(ctx, k_mg_asm_galerkin, grid_for(576 * ne), f.L, f.K, m.L, m.K);
+      LAUNCH(ctx, k_mg_asm_galerkin, grid_for(300 * ne), f.L, f.K, m.L, m.K);
     }
     debug_sync(ctx, "k_mg_asm");
     LAUNCH(ctx, k_mg_diag_asm, grid_for(nn), m.L, m.K, m.fixm, m.invd);
@@ -969,19 +984,27 @@ int enqueue_mg_setup(topo_ctx* ctx) {
     if (l == 0) {
       const LvGeo F = lv0(ctx);
       const int gF = grid_for(F.nodes());
+      // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
+      // masked products K v ping-pong between q and w
       LAUNCH(ctx, k_mg_start_vec, gF, F, s.fixm, s.z);
-      for (int k = 0; k < kMgPowerSteps; ++k) {
-        CK(mg_mv0(ctx, 0, s.m_z));
-        LAUNCH(ctx, (k_mg_jacobi<0, true>), gF, F, s.q, s.q, s.invd, s.fixm, one, s.z, s.st, 0, s.partials, s.counter);
+      CK((launch_mv<0, false, 3>(ctx, s, 0, s.m_z, nullptr, nullptr, s.q, 0, one)));
+      for (int k = 1; k <= kMgPowerSteps; ++k) {
+        const bool odd = k & 1;
+        CK((launch_mv<3, false, 3>(ctx, s, 0, odd ? s.m_q : s.m_w, nullptr, s.z, odd ? s.w : s.q, 0, one)));
       }
-      CK(mg_mv0(ctx, 0, s.m_z));
-      LAUNCH(ctx, k_mg_rayleigh<true>, gF, F, s.z, s.q, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om, s.partials,
+      double* tlast = (kMgPowerSteps & 1) ? s.w : s.q;
+      LAUNCH(ctx, k_mg_rayleigh<true>, gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om, s.partials,
              s.counter);
     } else {
       MgLevel& m = ctx->mg[l];
       const int gL = grid_for(m.L.nodes());
       LAUNCH(ctx, k_mg_start_vec, gL, m.L, m.fixm, m.x);
       for (int k = 0; k < kMgPowerSteps; ++k) {
+        if (!m.stored) {   // level 1: x <- D^-1 (A x) in the gather phase
+          CK(launch_l1_elem(ctx, m, nullptr));
+          LAUNCH(ctx, k_mg_l1_gather<true>, gL, m.L, m.Y, m.fixm, m.x, nullptr, m.invd);
+          continue;
+        }
         CK(mg_apply(ctx, l, 0));
         LAUNCH(ctx, (k_mg_jacobi<0, false>), gL, m.L, m.t, m.t, m.invd, m.fixm, one, m.x, s.st, 0, s.partials,
                s.counter);
@@ -1066,13 +1089,8 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
     return check_launch(ctx);
   }
   // level 1: P^T K(E) P matrix-free in the Walsh domain (two deterministic phases)
-  {
-    const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
-    k_mg_l1_elem<<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, m.x, m.Y, gst);
-    ctx->launches++;
-    debug_sync(ctx, "k_mg_l1_elem");
-  }
-  LAUNCH(ctx, k_mg_l1_gather, grid_for(m.L.nodes()), m.L, m.Y, m.fixm, m.t, gst);
+  CK(launch_l1_elem(ctx, m, gst));
+  LAUNCH(ctx, k_mg_l1_gather<false>, grid_for(m.L.nodes()), m.L, m.Y, m.fixm, m.t, gst, nullptr);
   return check_launch(ctx);
 }
 
