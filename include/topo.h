@@ -122,6 +122,9 @@ typedef struct {
                                  8-step estimate is 0.80-0.95 of lam_max, so w lam_max <= 1.75)   */
   int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (24..8192;
                                  0 = auto: min(5000, max(1000, n_dof / 2000)))                     */
+  int32_t mg_fp32;            /* 1 (default): multigrid levels >= 1 (vectors, stencils, level-1 Galerkin
+                                 operator) in fp32 -- mixed precision: the fine level,
+                                 the PCG and every result stay fp64; 0: the whole V-cycle in fp64   */
 } topo_params;
 
 #define TOPO_PRECOND_JACOBI 0

@@ -37,7 +37,8 @@
 
 namespace topo {
 
-struct WhtK { double k0, o0, k7, o7, a, b, r, s; };
+template <typename T> struct WhtKT { T k0, o0, k7, o7, a, b, r, s; };
+using WhtK = WhtKT<double>;
 __constant__ WhtK c_wht;
 
 __device__ __forceinline__ void wht4(const double v[4], double G[4]) {
@@ -51,16 +52,20 @@ __device__ __forceinline__ void wht4(const double v[4], double G[4]) {
 
 // Q = E * B * P  (P, Q indexed [c][m], m = mx + 2 my + 4 mz).  E is folded
 // into the 8 block constants (8 DMUL) instead of scaling the 21 outputs.
-__constant__ WhtK c_wht1;   // Lambda^-1 B Lambda^-1, Lambda = diag(2^|m|): level-1 multigrid (mg.cuh)
+// Lambda^-1 B Lambda^-1, Lambda = diag(2^|m|): level-1 multigrid (mg.cuh), fp64 and fp32
+__constant__ WhtK c_wht1;
+__constant__ WhtKT<float> c_wht1f;
 
-__device__ __forceinline__ void wht_block_k(const WhtK& K, const double P[3][8], double Ee, double Q[3][8]);
+template <typename T>
+__device__ __forceinline__ void wht_block_k(const WhtKT<T>& K, const T P[3][8], T Ee, T Q[3][8]);
 __device__ __forceinline__ void wht_block(const double P[3][8], double Ee, double Q[3][8]) {
-  wht_block_k(c_wht, P, Ee, Q);
+  wht_block_k<double>(c_wht, P, Ee, Q);
 }
-__device__ __forceinline__ void wht_block_k(const WhtK& K, const double P[3][8], double Ee, double Q[3][8]) {
-  const double k0 = Ee * K.k0, o0 = Ee * K.o0, k7 = Ee * K.k7, o7 = Ee * K.o7;
-  const double a = Ee * K.a, b = Ee * K.b, r = Ee * K.r, s = Ee * K.s;
-  double t;
+template <typename T>
+__device__ __forceinline__ void wht_block_k(const WhtKT<T>& K, const T P[3][8], T Ee, T Q[3][8]) {
+  const T k0 = Ee * K.k0, o0 = Ee * K.o0, k7 = Ee * K.k7, o7 = Ee * K.o7;
+  const T a = Ee * K.a, b = Ee * K.b, r = Ee * K.r, s = Ee * K.s;
+  T t;
   t = o0 * (P[0][1] + P[1][2] + P[2][4]);
   Q[0][1] = fma(k0, P[0][1], t);
   Q[1][2] = fma(k0, P[1][2], t);
@@ -69,7 +74,7 @@ __device__ __forceinline__ void wht_block_k(const WhtK& K, const double P[3][8],
   Q[0][6] = fma(k7, P[0][6], t);
   Q[1][5] = fma(k7, P[1][5], t);
   Q[2][3] = fma(k7, P[2][3], t);
-  Q[0][0] = Q[1][0] = Q[2][0] = 0.0;   // rigid translations carry no energy
+  Q[0][0] = Q[1][0] = Q[2][0] = T(0);   // rigid translations carry no energy
   Q[1][3] = fma(a, P[1][3], b * P[2][5]);
   Q[2][5] = fma(b, P[1][3], a * P[2][5]);
   Q[0][3] = fma(a, P[0][3], b * P[2][6]);

@@ -60,10 +60,10 @@ __device__ __forceinline__ int corner_dz(int a) { return a >= 4 ? 1 : 0; }
 // Restriction  bC = mask_C( P^T mask_F(v) ),  v = bF - qF (kResid) or bF.
 // Thread per coarse node; gathers the 3x3x3 fine neighbourhood of node 2j.
 // ---------------------------------------------------------------------------
-template <bool kResid>
+template <bool kResid, typename TF, typename TC>
 __global__ void __launch_bounds__(kBlock)
-k_mg_restrict(LvGeo F, LvGeo Cg, const double* __restrict__ bF, const double* __restrict__ qF,
-              const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, double* __restrict__ bC,
+k_mg_restrict(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict__ qF,
+              const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, TC* __restrict__ bC,
               const DevState* st) {
   MG_GATE(st);
   const long long tot = Cg.nodes();
@@ -87,7 +87,7 @@ k_mg_restrict(LvGeo F, LvGeo Cg, const double* __restrict__ bF, const double* __
           const double w = wxz * (dy ? 0.5 : 1.0);
           const long long i = F.n(ix, iy, iz);
           const uint8_t fm = fixF[i];
-          double v0 = bF[i], v1 = bF[i + F.ncomp], v2 = bF[i + 2 * F.ncomp];
+          double v0 = (double)bF[i], v1 = (double)bF[i + F.ncomp], v2 = (double)bF[i + 2 * F.ncomp];
           if (kResid) {
             v0 -= qF[i];
             v1 -= qF[i + F.ncomp];
@@ -101,19 +101,19 @@ k_mg_restrict(LvGeo F, LvGeo Cg, const double* __restrict__ bF, const double* __
     }
     const long long j = Cg.n(jx, jy, jz);
     const uint8_t fc = fixC[j];
-    bC[j] = (fc & 1) ? 0.0 : s0;
-    bC[j + Cg.ncomp] = (fc & 2) ? 0.0 : s1;
-    bC[j + 2 * Cg.ncomp] = (fc & 4) ? 0.0 : s2;
+    bC[j] = (TC)((fc & 1) ? 0.0 : s0);
+    bC[j + Cg.ncomp] = (TC)((fc & 2) ? 0.0 : s1);
+    bC[j + 2 * Cg.ncomp] = (TC)((fc & 4) ? 0.0 : s2);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Prolongation  xF (+)= mask_F( P eC ).  Thread per fine node (<= 8 sources).
 // ---------------------------------------------------------------------------
-template <bool kAdd>
+template <bool kAdd, typename TC, typename TF>
 __global__ void __launch_bounds__(kBlock)
-k_mg_prolong(LvGeo F, LvGeo Cg, const double* __restrict__ eC, const uint8_t* __restrict__ fixF,
-             double* __restrict__ xF, const DevState* st) {
+k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
+             TF* __restrict__ xF, const DevState* st) {
   MG_GATE(st);
   const long long tot = F.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -128,9 +128,9 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const double* __restrict__ eC, const uint8_t* __
       for (int b = 0; b < nx; ++b)
         for (int c = 0; c < ny; ++c) {
           const long long j = Cg.n(jx + b, jy + c, jz + a);
-          s0 += eC[j];
-          s1 += eC[j + Cg.ncomp];
-          s2 += eC[j + 2 * Cg.ncomp];
+          s0 += (double)eC[j];
+          s1 += (double)eC[j + Cg.ncomp];
+          s2 += (double)eC[j + 2 * Cg.ncomp];
         }
     const long long i = F.n(ix, iy, iz);
     const uint8_t fm = fixF[i];
@@ -138,7 +138,7 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const double* __restrict__ eC, const uint8_t* __
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long o = i + c * F.ncomp;
-      xF[o] = kAdd ? xF[o] + v[c] : v[c];
+      xF[o] = (TF)(kAdd ? (double)xF[o] + v[c] : v[c]);
     }
   }
 }
@@ -154,11 +154,11 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const double* __restrict__ eC, const uint8_t* __
 //           block sets beta = rho / rho_old (0 on a fresh start), rz = rho.
 // kNodeD: D^-1 is one scalar per node (level 0: KE_ii constant), else per DOF.
 // ---------------------------------------------------------------------------
-template <int MODE, bool kNodeD>
+template <int MODE, bool kNodeD, typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_jacobi(LvGeo L, const double* __restrict__ b, const double* __restrict__ q,
-            const double* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
-            double* __restrict__ x, DevState* st, int gate, double* partials, unsigned int* counter) {
+k_mg_jacobi(LvGeo L, const T* __restrict__ b, const T* __restrict__ q,
+            const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
+            T* __restrict__ x, DevState* st, int gate, double* partials, unsigned int* counter) {
   if (gate && st->done) return;
   const double omega = *omp;
   const long long tot = L.nodes();
@@ -169,17 +169,17 @@ k_mg_jacobi(LvGeo L, const double* __restrict__ b, const double* __restrict__ q,
     lv_decode(L, k, ix, iy, iz);
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
-    const double dn = kNodeD ? invd[i] : 0.0;
+    const double dn = kNodeD ? (double)invd[i] : 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long o = i + c * L.ncomp;
-      const double d = kNodeD ? dn : invd[o];
-      const double bv = b[o];
+      const double d = kNodeD ? dn : (double)invd[o];
+      const double bv = (double)b[o];
       double xn;
       if ((fm >> c) & 1) xn = 0.0;
       else if (MODE == 0) xn = omega * d * bv;
-      else xn = fma(omega * d, bv - q[o], x[o]);
-      x[o] = xn;
+      else xn = fma(omega * d, bv - (double)q[o], (double)x[o]);
+      x[o] = (T)xn;
       if (MODE == 2) dot = fma(bv, xn, dot);
     }
   }
@@ -213,8 +213,9 @@ __device__ __forceinline__ double mg_hash_unit(unsigned long long k) {
   return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, double* __restrict__ v) {
+k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, T* __restrict__ v) {
   const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -224,13 +225,13 @@ k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, double* __restrict__ v)
     const unsigned long long ext = ((unsigned long long)iz * (L.nx + 1) + ix) * (L.ny + 1) + iy;
     const uint8_t fm = fix[i];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) v[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : mg_hash_unit(3 * ext + c);
+    for (int c = 0; c < 3; ++c) v[i + c * L.ncomp] = (T)(((fm >> c) & 1) ? 0.0 : mg_hash_unit(3 * ext + c));
   }
 }
 
-template <bool kNodeD>
+template <bool kNodeD, typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_rayleigh(LvGeo L, const double* __restrict__ v, const double* __restrict__ t, const double* __restrict__ invd,
+k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T* __restrict__ invd,
               const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out, double* partials,
               unsigned int* counter) {
   const long long tot = L.nodes();
@@ -245,9 +246,9 @@ k_mg_rayleigh(LvGeo L, const double* __restrict__ v, const double* __restrict__ 
     for (int c = 0; c < 3; ++c) {
       if ((fm >> c) & 1) continue;
       const long long o = i + c * L.ncomp;
-      const double vv = v[o];
-      vt = fma(vv, t[o], vt);
-      vdv = fma(vv * vv, 1.0 / (kNodeD ? invd[i] : invd[o]), vdv);
+      const double vv = (double)v[o];
+      vt = fma(vv, (double)t[o], vt);
+      vdv = fma(vv * vv, 1.0 / (double)(kNodeD ? invd[i] : invd[o]), vdv);
     }
   }
   __shared__ double tot_sh[2];
@@ -259,9 +260,10 @@ k_mg_rayleigh(LvGeo L, const double* __restrict__ v, const double* __restrict__ 
 // Stored-level operator q = mask(A x) (node-centric gather over the <= 8
 // elements of each node; each element matrix is read once in total).
 // ---------------------------------------------------------------------------
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const double* __restrict__ x,
-               const uint8_t* __restrict__ fix, double* __restrict__ q, const DevState* st) {
+k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const T* __restrict__ x,
+               const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
   MG_GATE(st);
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -281,7 +283,7 @@ k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const double* __restrict__
           for (int bb = 0; bb < 8; ++bb) {
             const long long n = L.n(ex + corner_dx(bb), ey + corner_dy(bb), ez + corner_dz(bb));
 #pragma unroll
-            for (int c = 0; c < 3; ++c) xe[3 * bb + c] = x[n + c * L.ncomp];
+            for (int c = 0; c < 3; ++c) xe[3 * bb + c] = (double)x[n + c * L.ncomp];
           }
 #pragma unroll
           for (int i = 0; i < 3; ++i) {
@@ -295,13 +297,14 @@ k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const double* __restrict__
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) q[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : acc[c];
+    for (int c = 0; c < 3; ++c) q[i + c * L.ncomp] = (T)(((fm >> c) & 1) ? 0.0 : acc[c]);
   }
 }
 
 // Inverse diagonal of a stored level (0 on fixed DOFs).
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_diag_asm(LvGeo L, const double* __restrict__ K, const uint8_t* __restrict__ fix, double* __restrict__ invd) {
+k_mg_diag_asm(LvGeo L, const double* __restrict__ K, const uint8_t* __restrict__ fix, T* __restrict__ invd) {
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -321,15 +324,16 @@ k_mg_diag_asm(LvGeo L, const double* __restrict__ K, const uint8_t* __restrict__
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : 1.0 / acc[c];
+    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = (T)(((fm >> c) & 1) ? 0.0 : 1.0 / acc[c]);
   }
 }
 
 // Inverse diagonal of level 1 straight from the fine moduli (level 1 applied
 // matrix-free as P^T K P): diag = sum_e sum_c E_c diag(M_c).
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_diag_l1(Geo g, LvGeo L, const double* __restrict__ E, const uint8_t* __restrict__ fix,
-             double* __restrict__ invd) {
+             T* __restrict__ invd) {
   const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -354,7 +358,7 @@ k_mg_diag_l1(Geo g, LvGeo L, const double* __restrict__ E, const uint8_t* __rest
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = ((fm >> c) & 1) ? 0.0 : 1.0 / acc[c];
+    for (int c = 0; c < 3; ++c) invd[i + c * L.ncomp] = (T)(((fm >> c) & 1) ? 0.0 : 1.0 / acc[c]);
   }
 }
 
@@ -453,39 +457,45 @@ k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __re
 // of a fine matvec on P x plus two transfers.  Two phases for determinism:
 // phase 1 writes each element's 24 outputs, phase 2 sums them per node.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void fwht8(double v[8]) {
+template <typename T>
+__device__ __forceinline__ void fwht8(T v[8]) {
 #pragma unroll
   for (int b = 1; b < 8; b <<= 1)
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if (!(k & b)) {
-        const double u = v[k], w = v[k | b];
+        const T u = v[k], w = v[k | b];
         v[k] = u + w;
         v[k | b] = u - w;
       }
 }
 
 constexpr int kL1Block = 128;
+template <typename T> __device__ __forceinline__ const WhtKT<T>& wht1_const();
+template <> __device__ __forceinline__ const WhtKT<double>& wht1_const<double>() { return c_wht1; }
+template <> __device__ __forceinline__ const WhtKT<float>& wht1_const<float>() { return c_wht1f; }
+
+template <typename T>
 __global__ void __launch_bounds__(kL1Block, 3)
-k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const double* __restrict__ x,
-             double* __restrict__ Y, const DevState* st) {
+k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const T* __restrict__ x,
+             T* __restrict__ Y, const DevState* st) {
   MG_GATE(st);
   const long long nel = L.nel();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
        e += (long long)gridDim.x * blockDim.x) {
     const unsigned ee = (unsigned)e, ny = (unsigned)L.ny, nz = (unsigned)L.nz;
     const unsigned t = ee / ny, ey = ee - t * ny, ex = t / nz, ez = t - ex * nz;
-    double W[3][8], Yh[3][8], Ech[8];
+    T W[3][8], Yh[3][8], Ech[8];
 #pragma unroll
     for (int ch = 0; ch < 8; ++ch)     // child moduli first: independent loads off the compute chain
-      Ech[ch] = E[elem_idx(g, 2 * ex + (ch & 1), 2 * ey + ((ch >> 1) & 1), 2 * ez + (ch >> 2))];
+      Ech[ch] = (T)E[elem_idx(g, 2 * ex + (ch & 1), 2 * ey + ((ch >> 1) & 1), 2 * ez + (ch >> 2))];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const long long n = L.n(ex + (k & 1), ey + ((k >> 1) & 1), ez + (k >> 2));
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         W[c][k] = x[n + c * L.ncomp];
-        Yh[c][k] = 0.0;
+        Yh[c][k] = T(0);
       }
     }
 #pragma unroll
@@ -495,28 +505,28 @@ k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const double* __restr
     // and the rescaled block constants c_wht1.
 #pragma unroll 1
     for (int ch = 0; ch < 8; ++ch) {
-      double Ec = Ech[0];
+      T Ec = Ech[0];
 #pragma unroll
       for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (no local memory)
-      if (Ec == 0.0) continue;                                  // child outside the fine domain
-      double P[3][8], Q[3][8];
+      if (Ec == T(0)) continue;                                 // child outside the fine domain
+      T P[3][8], Q[3][8];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int m = 0; m < 8; ++m) P[c][m] = W[c][m];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const double hs = ((ch >> d) & 1) ? -0.5 : 0.5;
+        const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int m = 0; m < 8; ++m)
             if (!((m >> d) & 1)) P[c][m] = fma(hs, P[c][m | (1 << d)], P[c][m]);
       }
-      wht_block_k(c_wht1, P, Ec, Q);
+      wht_block_k<T>(wht1_const<T>(), P, Ec, Q);
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const double hs = ((ch >> d) & 1) ? -0.5 : 0.5;
+        const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -539,17 +549,17 @@ k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const double* __restr
 
 // phase 2: q_i = mask( sum over the <= 8 elements of i of Y[corner of i] )
 // (kScale: q_i = D^-1 mask(sum), the next power step's vector)
-template <bool kScale>
+template <bool kScale, typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict__ fix, double* __restrict__ q,
-               const DevState* st, const double* __restrict__ invd) {
+k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ q,
+               const DevState* st, const T* __restrict__ invd) {
   MG_GATE(st);
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    T a0 = T(0), a1 = T(0), a2 = T(0);
 #pragma unroll
     for (int d = 0; d < 8; ++d) {
       const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
@@ -568,9 +578,9 @@ k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict_
       a1 *= invd[i + L.ncomp];
       a2 *= invd[i + 2 * L.ncomp];
     }
-    q[i] = (fm & 1) ? 0.0 : a0;
-    q[i + L.ncomp] = (fm & 2) ? 0.0 : a1;
-    q[i + 2 * L.ncomp] = (fm & 4) ? 0.0 : a2;
+    q[i] = (fm & 1) ? T(0) : a0;
+    q[i + L.ncomp] = (fm & 2) ? T(0) : a1;
+    q[i + 2 * L.ncomp] = (fm & 4) ? T(0) : a2;
   }
 }
 
@@ -580,8 +590,9 @@ k_mg_l1_gather(LvGeo L, const double* __restrict__ Y, const uint8_t* __restrict_
 // layout index i): 243 doubles per node instead of 576 per element, and no
 // element gathers.  Out-of-domain neighbours have zero blocks; pads of x are 0.
 // ---------------------------------------------------------------------------
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_stencil(LvGeo L, const double* __restrict__ K, double* __restrict__ S) {
+k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -607,15 +618,16 @@ k_mg_stencil(LvGeo L, const double* __restrict__ K, double* __restrict__ S) {
               for (int cj = 0; cj < 3; ++cj) blk[ci * 3 + cj] += K[(long long)((3 * a + ci) * 24 + 3 * c + cj) * nel + e];
           }
 #pragma unroll
-      for (int t = 0; t < 9; ++t) S[(long long)(b * 9 + t) * L.ncomp + i] = blk[t];
+      for (int t = 0; t < 9; ++t) S[(long long)(b * 9 + t) * L.ncomp + i] = (T)blk[t];
     }
   }
 }
 
 // q = mask(A x) through the stencil; thread per node, 27 neighbour 3-vectors.
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_apply_st(LvGeo L, const double* __restrict__ S, const double* __restrict__ x,
-              const uint8_t* __restrict__ fix, double* __restrict__ q, const DevState* st) {
+k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
+              const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
   MG_GATE(st);
   const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -623,22 +635,22 @@ k_mg_apply_st(LvGeo L, const double* __restrict__ S, const double* __restrict__ 
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
     const long long i = L.n(ix, iy, iz);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    T a0 = T(0), a1 = T(0), a2 = T(0);
 #pragma unroll 3
     for (int b = 0; b < 27; ++b) {
       // b = (dx+1) + 3 (dy+1) + 9 (dz+1); layout: x -> nplane, z -> NY, y -> 1
       const long long j = i + (long long)(b % 3 - 1) * L.nplane + (long long)((b / 3) % 3 - 1) +
                           (long long)(b / 9 - 1) * L.NY;
-      const double x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
-      const double* sb = S + (long long)(b * 9) * L.ncomp + i;
+      const T x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
+      const T* sb = S + (long long)(b * 9) * L.ncomp + i;
       a0 = fma(sb[0], x0, fma(sb[L.ncomp], x1, fma(sb[2 * L.ncomp], x2, a0)));
       a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, fma(sb[5 * L.ncomp], x2, a1)));
       a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, fma(sb[8 * L.ncomp], x2, a2)));
     }
     const uint8_t fm = fix[i];
-    q[i] = (fm & 1) ? 0.0 : a0;
-    q[i + L.ncomp] = (fm & 2) ? 0.0 : a1;
-    q[i + 2 * L.ncomp] = (fm & 4) ? 0.0 : a2;
+    q[i] = (fm & 1) ? T(0) : a0;
+    q[i + L.ncomp] = (fm & 2) ? T(0) : a1;
+    q[i + 2 * L.ncomp] = (fm & 4) ? T(0) : a2;
   }
 }
 
@@ -781,18 +793,19 @@ k_mg_gj_step(const double* __restrict__ a, double* __restrict__ o, int n, int k)
 }
 
 // x[imap[r]] = sum_j Ainv[r][j] b[imap[j]]  (warp per row, fixed lane order)
+template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_coarse_solve(const double* __restrict__ Ainv, int n, int ld, const long long* __restrict__ imap,
-                  const double* __restrict__ b, double* __restrict__ x, const DevState* st) {
+                  const T* __restrict__ b, T* __restrict__ x, const DevState* st) {
   MG_GATE(st);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
   for (int r = warp; r < n; r += nwarp) {
     double s = 0.0;
-    for (int j = lane; j < n; j += 32) s = fma(Ainv[(long long)r * ld + j], b[imap[j]], s);
+    for (int j = lane; j < n; j += 32) s = fma(Ainv[(long long)r * ld + j], (double)b[imap[j]], s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) x[imap[r]] = s;
+    if (lane == 0) x[imap[r]] = (T)s;
   }
 }
 

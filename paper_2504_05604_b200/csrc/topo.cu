@@ -142,10 +142,12 @@ struct Slab {
 // One coarse multigrid level (l >= 1, M1-M6).
 struct MgLevel {
   LvGeo L{};
-  double *x = nullptr, *b = nullptr, *t = nullptr, *invd = nullptr;   // 3*ncomp each
-  double* K = nullptr;          // stored element matrices [576][nel] (stored levels)
-  double* S = nullptr;          // 27-point block stencil [243][ncomp] (stored levels that are smoothed)
-  double* Y = nullptr;          // level 1 matrix-free: per-element outputs [24][nel]
+  // vectors and level operators in the preconditioner's precision (double, or
+  // float with topo_params.mg_fp32; typed access through mgp<T>)
+  void *x = nullptr, *b = nullptr, *t = nullptr, *invd = nullptr;   // 3*ncomp each
+  double* K = nullptr;          // stored element matrices [576][nel] (fp64: setup only)
+  void* S = nullptr;            // 27-point block stencil [243][ncomp] (stored levels that are smoothed)
+  void* Y = nullptr;            // level 1 matrix-free: per-element outputs [24][nel]
   uint8_t* fixm = nullptr;      // per node: bit c = DOF c fixed
   std::vector<uint8_t> hfix;    // host copy, external node order
   bool stored = false;
@@ -161,6 +163,7 @@ struct topo_ctx {
   double kd = 0.0;
   WhtK wht{};
   WhtK wht1{};              // level-1 multigrid: block constants scaled by Lambda^-1 . Lambda^-1
+  WhtKT<float> wht1f{};
   int tz = 8;               // z extent of a matvec CTA (threads 32 x tz)
   std::vector<int4> st_off;
   std::vector<double> st_w;
@@ -201,6 +204,7 @@ struct topo_ctx {
   int sticky = TOPO_OK;
   // geometric multigrid (level 0 = the fine slab; mg[0] unused)
   bool mg_on = false, mg_ready = false;
+  bool mg_f32 = false;               // levels >= 1 in fp32 (topo_params.mg_fp32)
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
@@ -299,7 +303,10 @@ int ensure_constants(topo_ctx* ctx) {
     const WhtK& w0 = ctx->wht;
     const WhtK w1{w0.k0 / 4, w0.o0 / 4, w0.k7 / 16, w0.o7 / 16, w0.a / 16, w0.b / 16, w0.r / 4, w0.s / 64};
     ctx->wht1 = w1;
+    ctx->wht1f = WhtKT<float>{(float)w1.k0, (float)w1.o0, (float)w1.k7, (float)w1.o7, (float)w1.a, (float)w1.b,
+                              (float)w1.r, (float)w1.s};
     CU(cudaMemcpyToSymbolAsync(c_wht1, &ctx->wht1, sizeof(WhtK), 0, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyToSymbolAsync(c_wht1f, &ctx->wht1f, sizeof(WhtKT<float>), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_diag8, ctx->mg_diag8, sizeof(ctx->mg_diag8), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzA, nzA, sizeof nzA, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzW, nzW, sizeof nzW, 0, cudaMemcpyHostToDevice, ctx->stream));
@@ -850,6 +857,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   }
   if (L > 16) return set_err(ctx, TOPO_EINVAL, "multigrid: more than 16 levels");
   ctx->mg_on = true;
+  ctx->mg_f32 = P.mg_fp32 != 0;
   ctx->mg.resize(L);
   auto al = [&](void** p, size_t bytes) -> int {
     CU(cudaMalloc(p, bytes));
@@ -864,14 +872,15 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     m.L.ncomp = (long long)(h.nx + 3) * m.L.nplane;
     m.hfix = h.fix;
     m.stored = (l >= 2) || (L == 2);
-    CK(al((void**)&m.x, sizeof(double) * 3 * m.L.ncomp));
-    CK(al((void**)&m.b, sizeof(double) * 3 * m.L.ncomp));
-    CK(al((void**)&m.t, sizeof(double) * 3 * m.L.ncomp));
-    CK(al((void**)&m.invd, sizeof(double) * 3 * m.L.ncomp));
+    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    CK(al(&m.x, rs * 3 * m.L.ncomp));
+    CK(al(&m.b, rs * 3 * m.L.ncomp));
+    CK(al(&m.t, rs * 3 * m.L.ncomp));
+    CK(al(&m.invd, rs * 3 * m.L.ncomp));
     CK(al((void**)&m.fixm, m.L.ncomp));
     if (m.stored) CK(al((void**)&m.K, sizeof(double) * 576 * m.L.nel()));
-    if (m.stored && l < L - 1) CK(al((void**)&m.S, sizeof(double) * 243 * m.L.ncomp));
-    if (!m.stored) CK(al((void**)&m.Y, sizeof(double) * 24 * m.L.nel()));
+    if (m.stored && l < L - 1) CK(al(&m.S, rs * 243 * m.L.ncomp));
+    if (!m.stored) CK(al(&m.Y, rs * 24 * m.L.nel()));
     std::vector<uint8_t> lay(m.L.ncomp, 0);
     for (int iz = 0; iz <= h.nz; ++iz)
       for (int ix = 0; ix <= h.nx; ++ix)
@@ -939,21 +948,26 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 
 constexpr int kMgPowerSteps = 8;   // power steps of the smoother-weight estimate (M5)
 
+template <typename T> T* mgp(void* p) { return static_cast<T*>(p); }
+
 // level-1 phase 1 (Walsh-domain Galerkin per coarse element), 128-thread CTAs
+template <typename T>
 int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst) {
   Slab& s = ctx->slabs[0];
   const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
-  k_mg_l1_elem<<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, m.x, m.Y, gst);
+  k_mg_l1_elem<T><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, mgp<T>(m.x), mgp<T>(m.Y),
+                                                                             gst);
   ctx->launches++;
   debug_sync(ctx, "k_mg_l1_elem");
   return check_launch(ctx);
 }
 int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin);
-int mg_apply(topo_ctx* ctx, int l, int gate);
+template <typename T> int mg_apply(topo_ctx* ctx, int l, int gate);
 
 double* mg_Ainv(const topo_ctx* ctx) { return ctx->mg_A0; }
 
 // Per-design setup: level-1 diagonal, Galerkin element matrices, coarsest inverse.
+template <typename T>
 int enqueue_mg_setup(topo_ctx* ctx) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size();
@@ -961,7 +975,7 @@ int enqueue_mg_setup(topo_ctx* ctx) {
     MgLevel& m = ctx->mg[l];
     const long long nn = m.L.nodes(), ne = m.L.nel();
     if (l == 1 && !m.stored) {
-      LAUNCH(ctx, k_mg_diag_l1, grid_for(nn), s.g, m.L, s.E, m.fixm, m.invd);
+      LAUNCH(ctx, k_mg_diag_l1<T>, grid_for(nn), s.g, m.L, s.E, m.fixm, mgp<T>(m.invd));
       continue;
     }
     if (l == 1) {
@@ -975,8 +989,8 @@ int enqueue_mg_setup(topo_ctx* ctx) {
       LAUNCH(ctx, k_mg_asm_galerkin, grid_for(300 * ne), f.L, f.K, m.L, m.K);
     }
     debug_sync(ctx, "k_mg_asm");
-    LAUNCH(ctx, k_mg_diag_asm, grid_for(nn), m.L, m.K, m.fixm, m.invd);
-    if (m.S) LAUNCH(ctx, k_mg_stencil, grid_for(nn), m.L, m.K, m.S);
+    LAUNCH(ctx, k_mg_diag_asm<T>, grid_for(nn), m.L, m.K, m.fixm, mgp<T>(m.invd));
+    if (m.S) LAUNCH(ctx, k_mg_stencil<T>, grid_for(nn), m.L, m.K, mgp<T>(m.S));
   }
   // smoother weights w_l = theta / lam_l (M5): kMgPowerSteps power steps per level
   const double* one = ctx->mg_om + 16;
@@ -986,32 +1000,32 @@ int enqueue_mg_setup(topo_ctx* ctx) {
       const int gF = grid_for(F.nodes());
       // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
       // masked products K v ping-pong between q and w
-      LAUNCH(ctx, k_mg_start_vec, gF, F, s.fixm, s.z);
+      LAUNCH(ctx, k_mg_start_vec<double>, gF, F, s.fixm, s.z);
       CK((launch_mv<0, false, 3>(ctx, s, 0, s.m_z, nullptr, nullptr, s.q, 0, one)));
       for (int k = 1; k <= kMgPowerSteps; ++k) {
         const bool odd = k & 1;
         CK((launch_mv<3, false, 3>(ctx, s, 0, odd ? s.m_q : s.m_w, nullptr, s.z, odd ? s.w : s.q, 0, one)));
       }
       double* tlast = (kMgPowerSteps & 1) ? s.w : s.q;
-      LAUNCH(ctx, k_mg_rayleigh<true>, gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om, s.partials,
-             s.counter);
+      LAUNCH(ctx, (k_mg_rayleigh<true, double>), gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om,
+             s.partials, s.counter);
     } else {
       MgLevel& m = ctx->mg[l];
       const int gL = grid_for(m.L.nodes());
-      LAUNCH(ctx, k_mg_start_vec, gL, m.L, m.fixm, m.x);
+      LAUNCH(ctx, k_mg_start_vec<T>, gL, m.L, m.fixm, mgp<T>(m.x));
       for (int k = 0; k < kMgPowerSteps; ++k) {
         if (!m.stored) {   // level 1: x <- D^-1 (A x) in the gather phase
-          CK(launch_l1_elem(ctx, m, nullptr));
-          LAUNCH(ctx, k_mg_l1_gather<true>, gL, m.L, m.Y, m.fixm, m.x, nullptr, m.invd);
+          CK(launch_l1_elem<T>(ctx, m, nullptr));
+          LAUNCH(ctx, (k_mg_l1_gather<true, T>), gL, m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.x), nullptr, mgp<T>(m.invd));
           continue;
         }
-        CK(mg_apply(ctx, l, 0));
-        LAUNCH(ctx, (k_mg_jacobi<0, false>), gL, m.L, m.t, m.t, m.invd, m.fixm, one, m.x, s.st, 0, s.partials,
-               s.counter);
+        CK(mg_apply<T>(ctx, l, 0));
+        LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mgp<T>(m.t), mgp<T>(m.t), mgp<T>(m.invd), m.fixm, one,
+               mgp<T>(m.x), s.st, 0, s.partials, s.counter);
       }
-      CK(mg_apply(ctx, l, 0));
-      LAUNCH(ctx, k_mg_rayleigh<false>, gL, m.L, m.x, m.t, m.invd, m.fixm, ctx->prm.mg_omega, ctx->mg_om + l,
-             s.partials, s.counter);
+      CK(mg_apply<T>(ctx, l, 0));
+      LAUNCH(ctx, (k_mg_rayleigh<false, T>), gL, m.L, mgp<T>(m.x), mgp<T>(m.t), mgp<T>(m.invd), m.fixm,
+             ctx->prm.mg_omega, ctx->mg_om + l, s.partials, s.counter);
     }
   }
   const MgLevel& c = ctx->mg[L - 1];
@@ -1048,14 +1062,15 @@ int mg_setup(topo_ctx* ctx) {
   if (!ctx->mg_on || ctx->mg_ready) return TOPO_OK;
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
+  auto setup = [&]() { return ctx->mg_f32 ? enqueue_mg_setup<float>(ctx) : enqueue_mg_setup<double>(ctx); };
   if (ctx->debug) {
-    CK(enqueue_mg_setup(ctx));
+    CK(setup());
   } else {
     if (!ctx->mg_setup_exec) {
       cudaGraph_t graph;
       const long long l0 = ctx->launches;
       CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      int rc = enqueue_mg_setup(ctx);
+      int rc = setup();
       cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
       if (rc != TOPO_OK) return rc;
       if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "MG setup capture: %s", cudaGetErrorString(e));
@@ -1079,32 +1094,36 @@ int mg_mv0(topo_ctx* ctx, int gate, const CUtensorMap& vin) {
 }
 
 // t_l = A_l x_l on a coarse level (stored: block stencil; level 1: P^T K P matrix-free)
+template <typename T>
 int mg_apply(topo_ctx* ctx, int l, int gate) {
   Slab& s = ctx->slabs[0];
   MgLevel& m = ctx->mg[l];
   const DevState* gst = gate ? s.st : nullptr;
   if (m.stored) {
-    if (m.S) LAUNCH(ctx, k_mg_apply_st, grid_for(m.L.nodes()), m.L, m.S, m.x, m.fixm, m.t, gst);
-    else LAUNCH(ctx, k_mg_apply_asm, grid_for(m.L.nodes()), m.L, m.K, m.x, m.fixm, m.t, gst);   // coarsest (test hook)
+    if (m.S) LAUNCH(ctx, k_mg_apply_st<T>, grid_for(m.L.nodes()), m.L, mgp<T>(m.S), mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);
+    else LAUNCH(ctx, k_mg_apply_asm<T>, grid_for(m.L.nodes()), m.L, m.K, mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);   // coarsest (hook)
     return check_launch(ctx);
   }
   // level 1: P^T K(E) P matrix-free in the Walsh domain (two deterministic phases)
-  CK(launch_l1_elem(ctx, m, gst));
-  LAUNCH(ctx, k_mg_l1_gather<false>, grid_for(m.L.nodes()), m.L, m.Y, m.fixm, m.t, gst, nullptr);
+  CK(launch_l1_elem<T>(ctx, m, gst));
+  LAUNCH(ctx, (k_mg_l1_gather<false, T>), grid_for(m.L.nodes()), m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.t), gst,
+         (const T*)nullptr);
   return check_launch(ctx);
 }
 
 // One V-cycle on level l (level 0: b = r; the result lands in s.w and the last
 // fine sweep also sets rho = r.V(r) and beta for the PCG; `dot` is unused).
-int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
+// T = precision of levels >= 1 (level 0 is always fp64).
+template <typename T>
+int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size(), nu = ctx->prm.mg_nu;
   const DevState* gst = gate ? s.st : nullptr;
   const double* om = ctx->mg_om + l;
   if (l == L - 1) {
     const MgLevel& c = ctx->mg[l];
-    LAUNCH(ctx, k_mg_coarse_solve, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_npad, ctx->mg_imap, c.b,
-           c.x, gst);
+    LAUNCH(ctx, k_mg_coarse_solve<T>, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_npad, ctx->mg_imap,
+           mgp<T>(c.b), mgp<T>(c.x), gst);
     return check_launch(ctx);
   }
   MgLevel& n1 = ctx->mg[l + 1];
@@ -1118,16 +1137,19 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
-      LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+      LAUNCH(ctx, (k_mg_jacobi<1, true, double>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials,
+             s.counter);
       if (k < nu - 1) CK(mg_mv0(ctx, gate, s.m_z));
       else CK((launch_mv<0, false, 2>(ctx, s, gate, s.m_z, nullptr, nullptr, s.q, 0, om)));
     }
-    LAUNCH(ctx, k_mg_restrict<false>, grid_for(n1.L.nodes()), F, n1.L, s.q, s.q, s.fixm, n1.fixm, n1.b, gst);
-    CK(enqueue_vcycle(ctx, 1, gate, false));
-    LAUNCH(ctx, k_mg_prolong<true>, gF, F, n1.L, n1.x, s.fixm, s.z, gst);
+    LAUNCH(ctx, (k_mg_restrict<false, double, T>), grid_for(n1.L.nodes()), F, n1.L, s.q, s.q, s.fixm, n1.fixm,
+           mgp<T>(n1.b), gst);
+    CK(enqueue_vcycle_t<T>(ctx, 1, gate, false));
+    LAUNCH(ctx, (k_mg_prolong<true, T, double>), gF, F, n1.L, mgp<T>(n1.x), s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
       CK(mg_mv0(ctx, gate, s.m_z));
-      LAUNCH(ctx, (k_mg_jacobi<1, true>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials, s.counter);
+      LAUNCH(ctx, (k_mg_jacobi<1, true, double>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials,
+             s.counter);
     }
     // last sweep fused into the matvec epilogue: w = z + w D^-1 (r - K z) (the
     // V-cycle result lives in s.w), rho = r.w and beta for the PCG
@@ -1138,20 +1160,26 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
   }
   MgLevel& m = ctx->mg[l];
   const int gL = grid_for(m.L.nodes());
-  LAUNCH(ctx, (k_mg_jacobi<0, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+  T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *mi = mgp<T>(m.invd);
+  LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   for (int k = 1; k < nu; ++k) {
-    CK(mg_apply(ctx, l, gate));
-    LAUNCH(ctx, (k_mg_jacobi<1, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+    CK(mg_apply<T>(ctx, l, gate));
+    LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   }
-  CK(mg_apply(ctx, l, gate));
-  LAUNCH(ctx, k_mg_restrict<true>, grid_for(n1.L.nodes()), m.L, n1.L, m.b, m.t, m.fixm, n1.fixm, n1.b, gst);
-  CK(enqueue_vcycle(ctx, l + 1, gate, false));
-  LAUNCH(ctx, k_mg_prolong<true>, gL, m.L, n1.L, n1.x, m.fixm, m.x, gst);
+  CK(mg_apply<T>(ctx, l, gate));
+  LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b),
+         gst);
+  CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
+  LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
   for (int k = 1; k <= nu; ++k) {
-    CK(mg_apply(ctx, l, gate));
-    LAUNCH(ctx, (k_mg_jacobi<1, false>), gL, m.L, m.b, m.t, m.invd, m.fixm, om, m.x, s.st, gate, s.partials, s.counter);
+    CK(mg_apply<T>(ctx, l, gate));
+    LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   }
   return check_launch(ctx);
+}
+
+int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
+  return ctx->mg_f32 ? enqueue_vcycle_t<float>(ctx, l, gate, dot) : enqueue_vcycle_t<double>(ctx, l, gate, dot);
 }
 
 // one MG-PCG iteration: z = V(r) (rho, beta) ; p = z + beta p ; q = K p ; alpha ; u, r update
@@ -1176,30 +1204,32 @@ int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   return check_launch(ctx);
 }
 
-// host <-> level-l vectors in external numbering (test hooks)
-int mg_upload(topo_ctx* ctx, int l, const double* host, double* dev) {
+// host <-> level-l vectors in external numbering (test hooks; T = level precision)
+template <typename T>
+int mg_upload(topo_ctx* ctx, int l, const double* host, void* dev) {
   const MgLevel& m = ctx->mg[l];
   const LvGeo& L = m.L;
-  std::vector<double> lay(3 * L.ncomp, 0.0);
+  std::vector<T> lay(3 * L.ncomp, T(0));
   long long n = 0;
   for (int iz = 0; iz <= L.nz; ++iz)
     for (int ix = 0; ix <= L.nx; ++ix)
       for (int iy = 0; iy <= L.ny; ++iy, ++n)
         for (int c = 0; c < 3; ++c)
-          lay[L.n(ix, iy, iz) + c * L.ncomp] = ((m.hfix[n] >> c) & 1) ? 0.0 : host[3 * n + c];
-  CU(cudaMemcpy(dev, lay.data(), sizeof(double) * lay.size(), cudaMemcpyHostToDevice));
+          lay[L.n(ix, iy, iz) + c * L.ncomp] = ((m.hfix[n] >> c) & 1) ? T(0) : (T)host[3 * n + c];
+  CU(cudaMemcpy(dev, lay.data(), sizeof(T) * lay.size(), cudaMemcpyHostToDevice));
   return TOPO_OK;
 }
-int mg_download(topo_ctx* ctx, int l, const double* dev, double* host) {
+template <typename T>
+int mg_download(topo_ctx* ctx, int l, const void* dev, double* host) {
   const LvGeo& L = ctx->mg[l].L;
-  std::vector<double> lay(3 * L.ncomp);
+  std::vector<T> lay(3 * L.ncomp);
   CU(cudaStreamSynchronize(ctx->stream));
-  CU(cudaMemcpy(lay.data(), dev, sizeof(double) * lay.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(lay.data(), dev, sizeof(T) * lay.size(), cudaMemcpyDeviceToHost));
   long long n = 0;
   for (int iz = 0; iz <= L.nz; ++iz)
     for (int ix = 0; ix <= L.nx; ++ix)
       for (int iy = 0; iy <= L.ny; ++iy, ++n)
-        for (int c = 0; c < 3; ++c) host[3 * n + c] = lay[L.n(ix, iy, iz) + c * L.ncomp];
+        for (int c = 0; c < 3; ++c) host[3 * n + c] = (double)lay[L.n(ix, iy, iz) + c * L.ncomp];
   return TOPO_OK;
 }
 
@@ -1565,6 +1595,7 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (p->precond < 0 || p->precond > 2) return set_err(ctx, TOPO_EINVAL, "precond must be 0, 1 or 2");
   if (p->mg_nu < 1 || p->mg_nu > 8) return set_err(ctx, TOPO_EINVAL, "mg_nu must be in [1, 8]");
   if (!(p->mg_omega > 0 && p->mg_omega < 2)) return set_err(ctx, TOPO_EINVAL, "mg_omega must be in (0, 2)");
+  if (p->mg_fp32 != 0 && p->mg_fp32 != 1) return set_err(ctx, TOPO_EINVAL, "mg_fp32 must be 0 or 1");
   if (p->mg_coarse_max != 0 && (p->mg_coarse_max < 24 || p->mg_coarse_max > 8192))
     return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be 0 (auto) or in [24, 8192]");
   return TOPO_OK;
@@ -1600,6 +1631,7 @@ void topo_params_default(topo_params* p) {
   p->mg_nu = 1;
   p->mg_omega = 1.4;
   p->mg_coarse_max = 0;
+  p->mg_fp32 = 1;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }
@@ -2163,9 +2195,14 @@ int topo_mg_apply(topo_ctx* ctx, int32_t level, const double* x, double* y) {
   CK(mg_setup(ctx));
   if (level == 0) return topo_apply_K(ctx, x, y);
   MgLevel& m = ctx->mg[level];
-  CK(mg_upload(ctx, level, x, m.x));
-  CK(mg_apply(ctx, level, 0));
-  return mg_download(ctx, level, m.t, y);
+  if (ctx->mg_f32) {
+    CK(mg_upload<float>(ctx, level, x, m.x));
+    CK(mg_apply<float>(ctx, level, 0));
+    return mg_download<float>(ctx, level, m.t, y);
+  }
+  CK(mg_upload<double>(ctx, level, x, m.x));
+  CK(mg_apply<double>(ctx, level, 0));
+  return mg_download<double>(ctx, level, m.t, y);
 }
 
 int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {

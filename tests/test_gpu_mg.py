@@ -3,7 +3,10 @@ DESIGN.md readings M1-M6) against oracle/mg.py, step by step:
 
   hierarchy          level grids equal the oracle's (coarse_max rule, property Q)
   A_l (Galerkin)     y = A_l x on every level vs the oracle's P^T K P, rel 1e-12
+                     (mg_fp32 = 1: levels >= 1 in fp32, rel 1e-5 in L2: unit
+                     roundoff 6e-8 times the ~30-term sums of each row)
   V-cycle            z = V(b) vs the oracle's textbook recursion, rel 1e-9
+                     (fp32 levels: 1e-4)
   MG-PCG solve       true residual <= 1e-10, u within 1e-8 of the direct solve,
                      far fewer iterations than Jacobi-PCG
   SIMP loop          c history within 1e-6 of the oracle (MG preconditioning
@@ -63,8 +66,9 @@ def _case(dims, obst, seed=0, **over):
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst):
-    p, f, fx, pas, x, K = _case(dims, obst)
+@pytest.mark.parametrize("fp32", [0, 1])
+def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst, fp32):
+    p, f, fx, pas, x, K = _case(dims, obst, mg_fp32=fp32)
     lv = mg.hierarchy(K, fx, dims, coarse_max=1000)
     with topo.Problem(p, f, fx, pas) as pr:
         pr.set_xphys(x)
@@ -73,26 +77,31 @@ def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst):
             xv = random_vector(L["K"].shape[0], seed=10 + l)
             y = pr.mg_apply(l, xv)
             yo = oracle.matvec_free(L["K"], xv, L["fixed"])
-            assert_rel(y, yo, 1e-12, f"A_{l} {L['dims']}")
+            if fp32 and l >= 1:
+                r2, _ = rel(y, yo)
+                assert r2 <= 1e-5, f"A_{l} fp32 relL2 {r2:.2e}"
+            else:
+                assert_rel(y, yo, 1e-12, f"A_{l} {L['dims']}")
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu", [1, 2])
-def test_mg_vcycle_parity(topo, dims, obst, nu):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5)
+@pytest.mark.parametrize("nu,fp32", [(1, 0), (2, 0), (1, 1)])
+def test_mg_vcycle_parity(topo, dims, obst, nu, fp32):
+    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32)
     lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=1000), theta=1.5)
     b = np.where(fx == 0, random_vector(K.shape[0], seed=3), 0.0)
     zo = mg.vcycle(lv, b, None, nu=nu)
     with topo.Problem(p, f, fx, pas) as pr:
         pr.set_xphys(x)
         z = pr.mg_vcycle(b)
-    assert_rel(z, zo, 1e-9, f"V-cycle {dims} nu={nu}")
+    assert_rel(z, zo, 1e-4 if fp32 else 1e-9, f"V-cycle {dims} nu={nu} fp32={fp32}")
     assert np.all(z[fx != 0] == 0)
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-def test_mg_solve_parity(topo, dims, obst):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=2)
+@pytest.mark.parametrize("fp32", [0, 1])
+def test_mg_solve_parity(topo, dims, obst, fp32):
+    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32)
     uo = oracle.solve_direct(K, f, fx)
     _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.4, nu=1)
     its = {}
@@ -105,7 +114,7 @@ def test_mg_solve_parity(topo, dims, obst):
         assert oracle.true_residual(K, u, f, fx) <= 1e-10
         assert np.linalg.norm(u - uo) <= 1e-8 * np.linalg.norm(uo)
         its[pc] = info["iters"]
-    assert abs(its["mg"] - it_o) <= 2           # same algorithm as the oracle's MG-PCG
+    assert abs(its["mg"] - it_o) <= (3 if fp32 else 2)   # same algorithm as the oracle's MG-PCG
     assert its["mg"] * 5 < its["jacobi"]
 
 
