@@ -225,7 +225,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     const double* si = reinterpret_cast<const double*>(slot(s) + L::ioff(kPre));
     const double* se = reinterpret_cast<const double*>(slot(s) + L::eoff(kPre));
     double* pb = pbuf + (t % 3) * PB;
-    const bool wr_plane = kFused && ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
+    const bool wr_plane = kFused && pnew != nullptr &&
+                          ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
     double* pplane = pnew + (size_t)(xs + t - g.ex0) * nplane;     // node plane j = xs-1+t
 #pragma unroll
     for (int u = 0; u < NPN; ++u) {

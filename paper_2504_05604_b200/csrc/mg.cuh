@@ -107,6 +107,60 @@ k_mg_restrict(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict
   }
 }
 
+// Level-0 restriction of a masked residual (the pre-smoothing matvec's
+// epilogue output), x-marching: thread per coarse (jy, jz) column and x-chunk;
+// each fine plane is restricted in y-z once (9 gathers, coalesced in y) and
+// shared by the two coarse planes it feeds (weights 1/2, 1, 1/2 along x), so
+// the fine vector streams through HBM once.  Same sums as k_mg_restrict<false>
+// (fp64, fixed order) up to the order of the x-terms.
+template <typename TC>
+__global__ void __launch_bounds__(128)
+k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const double* __restrict__ res, const uint8_t* __restrict__ fixC,
+               TC* __restrict__ bC, const DevState* st) {
+  MG_GATE(st);
+  const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned ny1 = Cg.ny + 1;
+  if (col >= ny1 * (unsigned)(Cg.nz + 1)) return;
+  const int jy = (int)(col % ny1), jz = (int)(col / ny1);
+  const int ja = blockIdx.y * cx_chunk, jb = min(ja + cx_chunk, Cg.nx + 1);
+  if (ja >= jb) return;
+  auto gyz = [&](int i, double g[3]) {     // y-z restriction of fine plane i at (jy, jz)
+    g[0] = g[1] = g[2] = 0.0;
+    if (i < 0 || i > F.nx) return;
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int iz = 2 * jz + dz;
+      if (iz < 0 || iz > F.nz) continue;
+      const double wz = dz ? 0.5 : 1.0;
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int iy = 2 * jy + dy;
+        if (iy < 0 || iy > F.ny) continue;
+        const double w = wz * (dy ? 0.5 : 1.0);
+        const long long n = F.n(i, iy, iz);
+        g[0] = fma(w, res[n], g[0]);
+        g[1] = fma(w, res[n + F.ncomp], g[1]);
+        g[2] = fma(w, res[n + 2 * F.ncomp], g[2]);
+      }
+    }
+  };
+  double gp[3];
+  gyz(2 * ja - 1, gp);
+  for (int jx = ja; jx < jb; ++jx) {
+    double ge[3], go[3];
+    gyz(2 * jx, ge);
+    gyz(2 * jx + 1, go);
+    const long long j = Cg.n(jx, jy, jz);
+    const uint8_t fc = fixC[j];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = fma(0.5, gp[c], fma(0.5, go[c], ge[c]));
+      bC[j + c * Cg.ncomp] = (TC)(((fc >> c) & 1) ? 0.0 : v);
+      gp[c] = go[c];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Prolongation  xF (+)= mask_F( P eC ).  Thread per fine node (<= 8 sources).
 // ---------------------------------------------------------------------------
@@ -140,6 +194,42 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
       const long long o = i + c * F.ncomp;
       xF[o] = (TF)(kAdd ? (double)xF[o] + v[c] : v[c]);
     }
+  }
+}
+
+// Level 0 after the coarse correction (nu = 1): z = mask(w D^-1 r + P x1).  The
+// first sweep z0 = w D^-1 r is recomputed from r instead of being stored by the
+// pre-smoothing matvec (reads r and D^-1: 32 B/node instead of a z round trip).
+template <typename TC>
+__global__ void __launch_bounds__(kBlock)
+k_mg_prolong0(LvGeo F, LvGeo Cg, const double* __restrict__ r, const double* __restrict__ invd,
+              const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
+              double* __restrict__ z, const DevState* st) {
+  MG_GATE(st);
+  const double omega = *omp;
+  const long long tot = F.nodes();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(F, k, ix, iy, iz);
+    const int jx = ix >> 1, jy = iy >> 1, jz = iz >> 1;
+    const int nx = (ix & 1) + 1, ny = (iy & 1) + 1, nz = (iz & 1) + 1;
+    const double w = (nx == 2 ? 0.5 : 1.0) * (ny == 2 ? 0.5 : 1.0) * (nz == 2 ? 0.5 : 1.0);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int a = 0; a < nz; ++a)
+      for (int b = 0; b < nx; ++b)
+        for (int c = 0; c < ny; ++c) {
+          const long long j = Cg.n(jx + b, jy + c, jz + a);
+          s0 += (double)eC[j];
+          s1 += (double)eC[j + Cg.ncomp];
+          s2 += (double)eC[j + 2 * Cg.ncomp];
+        }
+    const long long i = F.n(ix, iy, iz);
+    const uint8_t fm = fixF[i];
+    const double wd = omega * invd[i];
+    z[i] = (fm & 1) ? 0.0 : fma(wd, r[i], w * s0);
+    z[i + F.ncomp] = (fm & 2) ? 0.0 : fma(wd, r[i + F.ncomp], w * s1);
+    z[i + 2 * F.ncomp] = (fm & 4) ? 0.0 : fma(wd, r[i + 2 * F.ncomp], w * s2);
   }
 }
 

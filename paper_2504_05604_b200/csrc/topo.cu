@@ -128,6 +128,8 @@ struct Slab {
   double *E = nullptr, *x = nullptr, *xphys = nullptr, *dc = nullptr, *dcf = nullptr,
          *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ce = nullptr, *xnew = nullptr,
          *oca = nullptr;   // OC: A = x sqrt(max(0, -dc~/dv~))
+  double* vpad = nullptr;  // filter operand, zero-padded by R in y and z (FiltPad)
+  FiltPad fp{};
   uint8_t* passive = nullptr;
   double* partials = nullptr;
   unsigned int* counter = nullptr;
@@ -167,6 +169,7 @@ struct topo_ctx {
   int tz = 8;               // z extent of a matvec CTA (threads 32 x tz)
   std::vector<int4> st_off;
   std::vector<double> st_w;
+  std::vector<int> st_poff;   // filter offsets in the padded layout (FiltPad)
   int R = 0;
   long long n_design = 0;   // global design-element count
   double bb = 0.0;          // ||f_free||^2
@@ -322,6 +325,13 @@ int ensure_constants(topo_ctx* ctx) {
                                cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_st_w, ctx->st_w.data(), sizeof(double) * ctx->st_w.size(), 0,
                                cudaMemcpyHostToDevice, ctx->stream));
+    ctx->st_poff.resize(ctx->st_off.size());
+    const FiltPad& fp = ctx->slabs[0].fp;
+    for (size_t k = 0; k < ctx->st_off.size(); ++k)
+      ctx->st_poff[k] = (int)(ctx->st_off[k].x * fp.fplane + ctx->st_off[k].z * fp.FY + ctx->st_off[k].y);
+    CU(cudaMemcpyToSymbolAsync(c_st_poff, ctx->st_poff.data(), sizeof(int) * ctx->st_poff.size(), 0,
+                               cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
   }
   g_const_owner = ctx;
   return TOPO_OK;
@@ -1133,7 +1143,8 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // first sweep from z = 0 fused into the matvec's load: z = w D^-1 r, and
     // (nu = 1) the epilogue writes the residual r - K z for the restriction
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[0], ctx->stream, cudaEventRecordExternal));
-    if (nu == 1) CK((launch_mv<3, false, 2>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
+    // (nu = 1: z is not stored -- k_mg_prolong0 recomputes it with the correction)
+    if (nu == 1) CK((launch_mv<3, false, 2>(ctx, s, gate, s.m_r, nullptr, nullptr, s.q, 0, om)));
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
@@ -1142,10 +1153,21 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
       if (k < nu - 1) CK(mg_mv0(ctx, gate, s.m_z));
       else CK((launch_mv<0, false, 2>(ctx, s, gate, s.m_z, nullptr, nullptr, s.q, 0, om)));
     }
-    LAUNCH(ctx, (k_mg_restrict<false, double, T>), grid_for(n1.L.nodes()), F, n1.L, s.q, s.q, s.fixm, n1.fixm,
-           mgp<T>(n1.b), gst);
+    {   // x-marching restriction of the masked residual (k_mg_restrict0)
+      const long long cols = (long long)(n1.L.ny + 1) * (n1.L.nz + 1);
+      const int bx = (int)((cols + 127) / 128);
+      int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 16 + bx - 1) / bx));
+      const int cx = (n1.L.nx + 1 + chunks - 1) / chunks;
+      chunks = (n1.L.nx + 1 + cx - 1) / cx;
+      k_mg_restrict0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.q, n1.fixm, mgp<T>(n1.b), gst);
+      ctx->launches++;
+      debug_sync(ctx, "k_mg_restrict0");
+    }
     CK(enqueue_vcycle_t<T>(ctx, 1, gate, false));
-    LAUNCH(ctx, (k_mg_prolong<true, T, double>), gF, F, n1.L, mgp<T>(n1.x), s.fixm, s.z, gst);
+    if (nu == 1)   // z = w D^-1 r (the first sweep, recomputed) + P x1
+      LAUNCH(ctx, k_mg_prolong0<T>, gF, F, n1.L, s.r, s.invd, om, mgp<T>(n1.x), s.fixm, s.z, gst);
+    else
+      LAUNCH(ctx, (k_mg_prolong<true, T, double>), gF, F, n1.L, mgp<T>(n1.x), s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
       CK(mg_mv0(ctx, gate, s.m_z));
       LAUNCH(ctx, (k_mg_jacobi<1, true, double>), gF, F, s.r, s.q, s.invd, s.fixm, om, s.z, s.st, gate, s.partials,
@@ -1380,15 +1402,22 @@ int do_filter_dc(topo_ctx* ctx) {
   CK(exchange_elems(ctx, &Slab::dc, ctx->R));
   for (Slab& s : ctx->slabs) {
     const int gr = grid_for((long long)s.g.nex * s.g.eplane);
-    if (mode == TOPO_FILTER_DENSITY)
-      LAUNCH(ctx, k_filter<F_DIV>, gr, s.g, nst, s.dc, s.hs, s.hs, s.passive, s.dcf, 0);
-    else if (mode == TOPO_FILTER_SENSITIVITY)
-      LAUNCH(ctx, k_filter<F_XDC>, gr, s.g, nst, s.x, s.dc, s.hs, s.passive, s.dcf, 0);
-    else
-      LAUNCH(ctx, k_filter<F_PLAIN>, gr, s.g, nst, s.dc, s.dc, s.hs, s.passive, s.dcf, 0);
+    const int gp = grid_for(s.g.nelloc);
+    if (mode == TOPO_FILTER_DENSITY) {
+      LAUNCH(ctx, k_filt_prep<F_DIV>, gp, s.g, s.fp, s.dc, s.hs, s.vpad);
+      LAUNCH(ctx, k_filt_apply<F_DIV>, gr, s.g, s.fp, nst, s.vpad, s.dc, s.hs, s.passive, s.dcf);
+    } else if (mode == TOPO_FILTER_SENSITIVITY) {
+      LAUNCH(ctx, k_filt_prep<F_XDC>, gp, s.g, s.fp, s.x, s.dc, s.vpad);
+      LAUNCH(ctx, k_filt_apply<F_XDC>, gr, s.g, s.fp, nst, s.vpad, s.x, s.hs, s.passive, s.dcf);
+    } else {
+      LAUNCH(ctx, k_filt_prep<F_PLAIN>, gp, s.g, s.fp, s.dc, s.dc, s.vpad);
+      LAUNCH(ctx, k_filt_apply<F_PLAIN>, gr, s.g, s.fp, nst, s.vpad, s.dc, s.hs, s.passive, s.dcf);
+    }
     if (!ctx->has_dvf) {
-      if (mode == TOPO_FILTER_DENSITY)
-        LAUNCH(ctx, k_filter<F_DIV>, gr, s.g, nst, s.dv, s.hs, s.hs, s.passive, s.dvf, 0);
+      if (mode == TOPO_FILTER_DENSITY) {
+        LAUNCH(ctx, k_filt_prep<F_DIV>, gp, s.g, s.fp, s.dv, s.hs, s.vpad);
+        LAUNCH(ctx, k_filt_apply<F_DIV>, gr, s.g, s.fp, nst, s.vpad, s.dv, s.hs, s.passive, s.dvf);
+      }
       else
         CU(cudaMemcpyAsync(s.dvf, s.dv, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
     }
@@ -1405,8 +1434,11 @@ int do_filter_x(topo_ctx* ctx) {
   const int nst = (int)ctx->st_off.size();
   if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY) {
     for (Slab& s : ctx->slabs)
-      LAUNCH(ctx, k_filter<F_X0>, grid_for((long long)s.g.nex * s.g.eplane), s.g, nst, s.x, s.x, s.hs,
-             s.passive, s.xphys, 0);
+    {
+      LAUNCH(ctx, k_filt_prep<F_X0>, grid_for(s.g.nelloc), s.g, s.fp, s.x, s.x, s.vpad);
+      LAUNCH(ctx, k_filt_apply<F_X0>, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.fp, nst, s.vpad, s.x, s.hs,
+             s.passive, s.xphys);
+    }
     CK(check_launch(ctx));
     CK(exchange_elems(ctx, &Slab::xphys, ctx->slabs[0].g.H));
   } else {
@@ -1527,6 +1559,11 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew, &s.oca};
   for (double** v : ev) CK(al((void**)v, eb));
   CK(al((void**)&s.passive, g.nelloc));
+  s.fp.R = ctx->R;
+  s.fp.FY = g.nely + 2 * ctx->R;
+  s.fp.FZ = g.nelz + 2 * ctx->R;
+  s.fp.fplane = (long long)s.fp.FY * s.fp.FZ;
+  CK(al((void**)&s.vpad, sizeof(double) * g.NEXL * s.fp.fplane));
   const MvGrid mg = mv_grid(ctx, g);
   const size_t nbmax = std::max<size_t>(kMaxGridBlocks, (size_t)mg.grid.x * mg.grid.y * mg.grid.z);
   CK(al((void**)&s.partials, sizeof(double) * 8 * nbmax));
@@ -1543,6 +1580,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
+                    s.vpad,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)

@@ -142,7 +142,7 @@ def test_fullsize_config2(topo):
     _, c_o, dc_o, dv_o = oracle.sensitivities(x0, ce_o, p["penal"], p["E0"], p["Emin"], pas)
     assert_rel(ce, ce_o, 1e-9, "ce")
     assert_rel(dc, dc_o, 1e-9, "dc")
-    assert c == pytest.approx(c_o, rel=1e-11)
+    assert c == pytest.approx(c_o, rel=1e-9)     # north_star 1e-9 (ce); WHT vs dense quadratic form
     dcf_o = oracle.apply_filter(H, Hs, 0, "dc", dc)
     dvf_o = oracle.apply_filter(H, Hs, 0, "dv", dv_o)
     assert_rel(dcf, dcf_o, 1e-9, "dc~")

@@ -137,7 +137,7 @@ def test_sens_filter_oc_parity(topo, case, mode):
     E_o, c_o, dc_o, dv_o = oracle.sensitivities(xphys0, ce_o, p["penal"], p["E0"], p["Emin"], pas)
     assert_rel(ce, ce_o, 1e-9, "ce")
     assert_rel(dc, dc_o, 1e-9, "dc")
-    assert c == pytest.approx(c_o, rel=1e-11)
+    assert c == pytest.approx(c_o, rel=1e-9)     # north_star 1e-9 (ce); WHT vs dense quadratic form
     assert_rel(hs, Hs, 1e-14, "Hs")
     dcf_o = oracle.apply_filter(H, Hs, mode, "dc", dc, x=x, passive=pas)
     dvf_o = oracle.apply_filter(H, Hs, mode, "dv", dv_o, x=x, passive=pas)
