@@ -593,12 +593,14 @@ k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const T* __restrict__
     // T_c = Lambda^-1 T''_c with T''_c = [[1, s/2], [0, 1]] per axis, so
     // T_c^T B T_c = T''_c^T (Lambda^-1 B Lambda^-1) T''_c: one FMA per pair each way
     // and the rescaled block constants c_wht1.
-#pragma unroll 1
+    // fp32: children fully unrolled (static E index, no select chain); fp64 keeps
+    // the loop rolled for register pressure.  A child outside the fine domain has
+    // E = 0 and contributes exactly 0.
+#pragma unroll (sizeof(T) == 4 ? 8 : 1)
     for (int ch = 0; ch < 8; ++ch) {
       T Ec = Ech[0];
 #pragma unroll
-      for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (no local memory)
-      if (Ec == T(0)) continue;                                 // child outside the fine domain
+      for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (folds when unrolled)
       T P[3][8], Q[3][8];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -675,10 +677,13 @@ k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix
 }
 
 // ---------------------------------------------------------------------------
-// Stored levels are applied through an assembled 27-point block stencil
-// S[(b*9 + ci*3 + cj) * ncomp + i] (b = (dx+1) + 3(dy+1) + 9(dz+1), node
-// layout index i): 243 doubles per node instead of 576 per element, and no
-// element gathers.  Out-of-domain neighbours have zero blocks; pads of x are 0.
+// Stored levels are applied through an assembled 27-point block stencil, kept
+// symmetric: with b = (dx+1) + 3(dy+1) + 9(dz+1), node i stores its self block
+// (b = 13, slot 0) and the 13 forward blocks b = 14..26 (slots 1..13) as
+// S[(slot*9 + ci*3 + cj) * ncomp + i]; the backward block A(i, i - d) is the
+// transpose of the forward block stored at node i - d.  126 values per node
+// instead of 576 per element, no element gathers.  Out-of-domain neighbours
+// have zero blocks; pads of x are 0.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
@@ -689,7 +694,7 @@ k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
     const long long i = L.n(ix, iy, iz);
-    for (int b = 0; b < 27; ++b) {
+    for (int b = 13; b < 27; ++b) {        // self + forward offsets
       const int bx = b % 3 - 1, by = (b / 3) % 3 - 1, bz = b / 9 - 1;
       double blk[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
       for (int dz = 0; dz < 2; ++dz)
@@ -708,7 +713,7 @@ k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
               for (int cj = 0; cj < 3; ++cj) blk[ci * 3 + cj] += K[(long long)((3 * a + ci) * 24 + 3 * c + cj) * nel + e];
           }
 #pragma unroll
-      for (int t = 0; t < 9; ++t) S[(long long)(b * 9 + t) * L.ncomp + i] = (T)blk[t];
+      for (int t = 0; t < 9; ++t) S[(long long)((b - 13) * 9 + t) * L.ncomp + i] = (T)blk[t];
     }
   }
 }
@@ -725,17 +730,36 @@ k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
     const long long i = L.n(ix, iy, iz);
-    T a0 = T(0), a1 = T(0), a2 = T(0);
-#pragma unroll 3
-    for (int b = 0; b < 27; ++b) {
+    T a0, a1, a2;
+    {   // self block
+      const T x0 = x[i], x1 = x[i + L.ncomp], x2 = x[i + 2 * L.ncomp];
+      const T* sb = S + i;
+      a0 = fma(sb[0], x0, fma(sb[L.ncomp], x1, sb[2 * L.ncomp] * x2));
+      a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, sb[5 * L.ncomp] * x2));
+      a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, sb[8 * L.ncomp] * x2));
+    }
+#pragma unroll 2
+    for (int b = 14; b < 27; ++b) {
       // b = (dx+1) + 3 (dy+1) + 9 (dz+1); layout: x -> nplane, z -> NY, y -> 1
-      const long long j = i + (long long)(b % 3 - 1) * L.nplane + (long long)((b / 3) % 3 - 1) +
+      const long long d = (long long)(b % 3 - 1) * L.nplane + (long long)((b / 3) % 3 - 1) +
                           (long long)(b / 9 - 1) * L.NY;
-      const T x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
-      const T* sb = S + (long long)(b * 9) * L.ncomp + i;
-      a0 = fma(sb[0], x0, fma(sb[L.ncomp], x1, fma(sb[2 * L.ncomp], x2, a0)));
-      a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, fma(sb[5 * L.ncomp], x2, a1)));
-      a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, fma(sb[8 * L.ncomp], x2, a2)));
+      const long long so = (long long)((b - 13) * 9) * L.ncomp;
+      {   // forward: A(i, i+d) x_{i+d}
+        const long long j = i + d;
+        const T x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
+        const T* sb = S + so + i;
+        a0 = fma(sb[0], x0, fma(sb[L.ncomp], x1, fma(sb[2 * L.ncomp], x2, a0)));
+        a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, fma(sb[5 * L.ncomp], x2, a1)));
+        a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, fma(sb[8 * L.ncomp], x2, a2)));
+      }
+      {   // backward: A(i, i-d) = A(i-d, i)^T, stored at node i-d
+        const long long j = i - d;
+        const T x0 = x[j], x1 = x[j + L.ncomp], x2 = x[j + 2 * L.ncomp];
+        const T* sb = S + so + j;
+        a0 = fma(sb[0], x0, fma(sb[3 * L.ncomp], x1, fma(sb[6 * L.ncomp], x2, a0)));
+        a1 = fma(sb[L.ncomp], x0, fma(sb[4 * L.ncomp], x1, fma(sb[7 * L.ncomp], x2, a1)));
+        a2 = fma(sb[2 * L.ncomp], x0, fma(sb[5 * L.ncomp], x1, fma(sb[8 * L.ncomp], x2, a2)));
+      }
     }
     const uint8_t fm = fix[i];
     q[i] = (fm & 1) ? T(0) : a0;

@@ -148,8 +148,10 @@ struct MgLevel {
   // float with topo_params.mg_fp32; typed access through mgp<T>)
   void *x = nullptr, *b = nullptr, *t = nullptr, *invd = nullptr;   // 3*ncomp each
   double* K = nullptr;          // stored element matrices [576][nel] (fp64: setup only)
-  void* S = nullptr;            // 27-point block stencil [243][ncomp] (stored levels that are smoothed)
+  void* S = nullptr;            // symmetric 27-point block stencil [126][ncomp] (stored, smoothed levels)
   void* Y = nullptr;            // level 1 matrix-free: per-element outputs [24][nel]
+  void* pw = nullptr;           // power-step vector kept for the next design's warm start
+  void* pw_b = nullptr;         // its snapshot copy
   uint8_t* fixm = nullptr;      // per node: bit c = DOF c fixed
   std::vector<uint8_t> hfix;    // host copy, external node order
   bool stored = false;
@@ -218,7 +220,11 @@ struct topo_ctx {
   int* mg_dmap = nullptr;            // coarsest: level DOF index -> dense index or -1
   long long* mg_imap = nullptr;      // coarsest: dense index -> level DOF index
   double* mg_om = nullptr;           // [17]: smoother weight per level; [16] = 1.0
-  cudaGraphExec_t mg_setup_exec = nullptr;
+  cudaGraphExec_t mg_setup_exec = nullptr;     // first design: 8 power steps from the hash vector
+  cudaGraphExec_t mg_setup_exec_w = nullptr;   // later designs: 3 steps from the previous vector
+  long long mg_setup_launches_w = 0;
+  bool mg_warm = false, mg_warm_b = false;     // power vectors valid (and in the snapshot)
+  double *mg_pw0 = nullptr, *mg_pw0_b = nullptr;   // level-0 power vector (+ snapshot)
   long long mg_setup_launches = 0;
   int mg_batch = 2;
 };
@@ -872,6 +878,9 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   auto al = [&](void** p, size_t bytes) -> int {
     CU(cudaMalloc(p, bytes));
     CU(cudaMemsetAsync(*p, 0, bytes, ctx->stream));
+    // the context's stream is non-blocking: finish the zero fill before any
+    // synchronous host upload into this buffer (legacy-stream cudaMemcpy)
+    CU(cudaStreamSynchronize(ctx->stream));
     ctx->dev_bytes += bytes;
     return TOPO_OK;
   };
@@ -889,8 +898,9 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CK(al(&m.invd, rs * 3 * m.L.ncomp));
     CK(al((void**)&m.fixm, m.L.ncomp));
     if (m.stored) CK(al((void**)&m.K, sizeof(double) * 576 * m.L.nel()));
-    if (m.stored && l < L - 1) CK(al(&m.S, rs * 243 * m.L.ncomp));
+    if (m.stored && l < L - 1) CK(al(&m.S, rs * 126 * m.L.ncomp));
     if (!m.stored) CK(al(&m.Y, rs * 24 * m.L.nel()));
+    if (l < L - 1) CK(al(&m.pw, rs * 3 * m.L.ncomp));
     std::vector<uint8_t> lay(m.L.ncomp, 0);
     for (int iz = 0; iz <= h.nz; ++iz)
       for (int ix = 0; ix <= h.nx; ++ix)
@@ -934,6 +944,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     if (g_cublas.SetWorkspace(ctx->cublas, ctx->mg_ws, ws) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetWorkspace failed");
     CU(cudaFuncSetAttribute(k_gj_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjB * kGjB * 8));
   }
+  CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
   {
     std::vector<double> om(17, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * 17));
@@ -956,7 +967,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   return TOPO_OK;
 }
 
-constexpr int kMgPowerSteps = 8;   // power steps of the smoother-weight estimate (M5)
+constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
+constexpr int kMgPowerStepsWarm = 3;   // later designs: continue from the previous design's vector
 
 template <typename T> T* mgp(void* p) { return static_cast<T*>(p); }
 
@@ -978,7 +990,7 @@ double* mg_Ainv(const topo_ctx* ctx) { return ctx->mg_A0; }
 
 // Per-design setup: level-1 diagonal, Galerkin element matrices, coarsest inverse.
 template <typename T>
-int enqueue_mg_setup(topo_ctx* ctx) {
+int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size();
   for (int l = 1; l < L; ++l) {
@@ -1003,27 +1015,35 @@ int enqueue_mg_setup(topo_ctx* ctx) {
     if (m.S) LAUNCH(ctx, k_mg_stencil<T>, grid_for(nn), m.L, m.K, mgp<T>(m.S));
   }
   // smoother weights w_l = theta / lam_l (M5): kMgPowerSteps power steps per level
+  // from the hash start vector on the first design; kMgPowerStepsWarm steps from
+  // the previous design's vector afterwards (the design changes slowly, so the
+  // Rayleigh quotient keeps improving)
   const double* one = ctx->mg_om + 16;
+  const int nsteps = warm ? kMgPowerStepsWarm : kMgPowerSteps;
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0) {
       const LvGeo F = lv0(ctx);
       const int gF = grid_for(F.nodes());
       // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
       // masked products K v ping-pong between q and w
-      LAUNCH(ctx, k_mg_start_vec<double>, gF, F, s.fixm, s.z);
+      if (warm) CU(cudaMemcpyAsync(s.z, ctx->mg_pw0, sizeof(double) * 3 * s.g.ncomp, cudaMemcpyDeviceToDevice,
+                                   ctx->stream));
+      else LAUNCH(ctx, k_mg_start_vec<double>, gF, F, s.fixm, s.z);
       CK((launch_mv<0, false, 3>(ctx, s, 0, s.m_z, nullptr, nullptr, s.q, 0, one)));
-      for (int k = 1; k <= kMgPowerSteps; ++k) {
+      for (int k = 1; k <= nsteps; ++k) {
         const bool odd = k & 1;
         CK((launch_mv<3, false, 3>(ctx, s, 0, odd ? s.m_q : s.m_w, nullptr, s.z, odd ? s.w : s.q, 0, one)));
       }
-      double* tlast = (kMgPowerSteps & 1) ? s.w : s.q;
+      double* tlast = (nsteps & 1) ? s.w : s.q;
       LAUNCH(ctx, (k_mg_rayleigh<true, double>), gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om,
              s.partials, s.counter);
+      CU(cudaMemcpyAsync(ctx->mg_pw0, s.z, sizeof(double) * 3 * s.g.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
       MgLevel& m = ctx->mg[l];
       const int gL = grid_for(m.L.nodes());
-      LAUNCH(ctx, k_mg_start_vec<T>, gL, m.L, m.fixm, mgp<T>(m.x));
-      for (int k = 0; k < kMgPowerSteps; ++k) {
+      if (warm) CU(cudaMemcpyAsync(m.x, m.pw, sizeof(T) * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
+      else LAUNCH(ctx, k_mg_start_vec<T>, gL, m.L, m.fixm, mgp<T>(m.x));
+      for (int k = 0; k < nsteps; ++k) {
         if (!m.stored) {   // level 1: x <- D^-1 (A x) in the gather phase
           CK(launch_l1_elem<T>(ctx, m, nullptr));
           LAUNCH(ctx, (k_mg_l1_gather<true, T>), gL, m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.x), nullptr, mgp<T>(m.invd));
@@ -1033,6 +1053,7 @@ int enqueue_mg_setup(topo_ctx* ctx) {
         LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mgp<T>(m.t), mgp<T>(m.t), mgp<T>(m.invd), m.fixm, one,
                mgp<T>(m.x), s.st, 0, s.partials, s.counter);
       }
+      CU(cudaMemcpyAsync(m.pw, m.x, sizeof(T) * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
       CK(mg_apply<T>(ctx, l, 0));
       LAUNCH(ctx, (k_mg_rayleigh<false, T>), gL, m.L, mgp<T>(m.x), mgp<T>(m.t), mgp<T>(m.invd), m.fixm,
              ctx->prm.mg_omega, ctx->mg_om + l, s.partials, s.counter);
@@ -1072,11 +1093,16 @@ int mg_setup(topo_ctx* ctx) {
   if (!ctx->mg_on || ctx->mg_ready) return TOPO_OK;
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
-  auto setup = [&]() { return ctx->mg_f32 ? enqueue_mg_setup<float>(ctx) : enqueue_mg_setup<double>(ctx); };
+  const bool warm = ctx->mg_warm;
+  auto setup = [&]() {
+    return ctx->mg_f32 ? enqueue_mg_setup<float>(ctx, warm) : enqueue_mg_setup<double>(ctx, warm);
+  };
   if (ctx->debug) {
     CK(setup());
   } else {
-    if (!ctx->mg_setup_exec) {
+    cudaGraphExec_t& ex = warm ? ctx->mg_setup_exec_w : ctx->mg_setup_exec;
+    long long& nl = warm ? ctx->mg_setup_launches_w : ctx->mg_setup_launches;
+    if (!ex) {
       cudaGraph_t graph;
       const long long l0 = ctx->launches;
       CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -1084,16 +1110,25 @@ int mg_setup(topo_ctx* ctx) {
       cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
       if (rc != TOPO_OK) return rc;
       if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "MG setup capture: %s", cudaGetErrorString(e));
-      e = cudaGraphInstantiate(&ctx->mg_setup_exec, graph, 0);
+      e = cudaGraphInstantiate(&ex, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "MG setup instantiate: %s", cudaGetErrorString(e));
-      ctx->mg_setup_launches = ctx->launches - l0;
+      nl = ctx->launches - l0;
       ctx->launches = l0;
     }
-    CU(cudaGraphLaunch(ctx->mg_setup_exec, ctx->stream));
-    ctx->launches += ctx->mg_setup_launches;
+    CU(cudaGraphLaunch(ex, ctx->stream));
+    ctx->launches += nl;
   }
   ctx->mg_ready = true;
+  ctx->mg_warm = true;
+  if (getenv("TOPO_MG_VERBOSE")) {   // smoother weights per level (diagnostics)
+    double om[17];
+    CU(cudaMemcpyAsync(om, ctx->mg_om, sizeof om, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    fprintf(stderr, "[topo] MG setup (%s): w =", warm ? "warm" : "cold");
+    for (size_t l = 0; l + 1 < ctx->mg.size(); ++l) fprintf(stderr, " %.4f", om[l]);
+    fprintf(stderr, "\n");
+  }
   return TOPO_OK;
 }
 
@@ -1548,6 +1583,9 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   auto al = [&](void** p, size_t bytes) -> int {
     CU(cudaMalloc(p, bytes));
     CU(cudaMemsetAsync(*p, 0, bytes, ctx->stream));
+    // the context's stream is non-blocking: finish the zero fill before any
+    // synchronous host upload into this buffer (legacy-stream cudaMemcpy)
+    CU(cudaStreamSynchronize(ctx->stream));
     ctx->dev_bytes += bytes;
     return TOPO_OK;
   };
@@ -1587,7 +1625,7 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   for (MgLevel& m : ctx->mg) {
-    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.fixm};
+    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.pw, m.pw_b, m.fixm};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -1598,7 +1636,10 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   if (ctx->mg_setup_exec) cudaGraphExecDestroy(ctx->mg_setup_exec);
+  if (ctx->mg_setup_exec_w) cudaGraphExecDestroy(ctx->mg_setup_exec_w);
   if (ctx->cublas) g_cublas.Destroy(ctx->cublas);
+  if (ctx->mg_pw0) cudaFree(ctx->mg_pw0);
+  if (ctx->mg_pw0_b) cudaFree(ctx->mg_pw0_b);
   for (cudaGraphExec_t g : ctx->cg_exec)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
@@ -1919,6 +1960,7 @@ int topo_set_stream(topo_ctx* ctx, void* stream) {
     for (cudaGraphExec_t& g : ctx->cg_exec)
       if (g) { cudaGraphExecDestroy(g); g = nullptr; }
     if (ctx->mg_setup_exec) { cudaGraphExecDestroy(ctx->mg_setup_exec); ctx->mg_setup_exec = nullptr; }
+    if (ctx->mg_setup_exec_w) { cudaGraphExecDestroy(ctx->mg_setup_exec_w); ctx->mg_setup_exec_w = nullptr; }
     if (ctx->oc_exec) { cudaGraphExecDestroy(ctx->oc_exec); ctx->oc_exec = nullptr; }
     g_const_owner = nullptr;
   }
@@ -2124,6 +2166,18 @@ int topo_snapshot(topo_ctx* ctx) {
     CU(cudaMemcpyAsync(s.x_b, s.x, eb, cudaMemcpyDeviceToDevice, ctx->stream));
     CU(cudaMemcpyAsync(s.xphys_b, s.xphys, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   }
+  if (ctx->mg_on) {   // the multigrid power vectors (warm-started smoother weights)
+    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    const size_t nb0 = sizeof(double) * 3 * ctx->slabs[0].g.ncomp;
+    if (!ctx->mg_pw0_b) CU(cudaMalloc(&ctx->mg_pw0_b, nb0));
+    CU(cudaMemcpyAsync(ctx->mg_pw0_b, ctx->mg_pw0, nb0, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (MgLevel& m : ctx->mg) {
+      if (!m.pw) continue;
+      if (!m.pw_b) CU(cudaMalloc(&m.pw_b, rs * 3 * m.L.ncomp));
+      CU(cudaMemcpyAsync(m.pw_b, m.pw, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    ctx->mg_warm_b = ctx->mg_warm;
+  }
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->snap_has_u = ctx->has_u;
   ctx->has_snap = true;
@@ -2139,6 +2193,15 @@ int topo_restore(topo_ctx* ctx) {
     CU(cudaMemcpyAsync(s.u, s.u_b, nb, cudaMemcpyDeviceToDevice, ctx->stream));
     CU(cudaMemcpyAsync(s.x, s.x_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
     CU(cudaMemcpyAsync(s.xphys, s.xphys_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  if (ctx->mg_on && ctx->mg_pw0_b) {
+    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    CU(cudaMemcpyAsync(ctx->mg_pw0, ctx->mg_pw0_b, sizeof(double) * 3 * ctx->slabs[0].g.ncomp,
+                       cudaMemcpyDeviceToDevice, ctx->stream));
+    for (MgLevel& m : ctx->mg)
+      if (m.pw && m.pw_b)
+        CU(cudaMemcpyAsync(m.pw, m.pw_b, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->mg_warm = ctx->mg_warm_b;
   }
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->has_u = ctx->snap_has_u;
