@@ -8,9 +8,13 @@ A "step" is one SIMP iteration (modulus, PCG solve,
 sensitivities, filter, OC) of BASELINE config --config (default 4: the
 512x256x256 cantilever, 101.6 M DOF, fp64) with all inputs resident in HBM.
 Steps continue the optimisation (x evolves), so W warm-up + K timed steps of
-config 4 are its 5 BASELINE iterations.  N > 1: launched by torchrun, one rank
-per GPU, x-slab decomposition with NCCL (strong scaling).  Prints ONE JSON
-line on rank 0.  See DESIGN.md "Measurement" for every number's definition.
+config 4 are its 5 BASELINE iterations.  The solve is PCG in fp64 to rtol 1e-8
+with the library's default preconditioner: geometric multigrid on one GPU
+(coarse levels in fp32 = f3); --precond jacobi times the
+north_star's Jacobi-PCG instead.  N > 1: launched by torchrun, one rank per
+GPU, x-slab decomposition with NCCL (strong scaling; Jacobi-PCG, the path that
+shards).  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for
+every number's definition.
 """
 import argparse
 import json
@@ -338,10 +342,11 @@ def main():
         # MG-PCG iteration, algorithmic bytes per launch:
         #   <2,1,0> PCG   p = V(r) + beta p, q = K p, p.q : read V(r) 24 + p_old 24, write p 24 + q 24 B/node
         #   <3,0,2> pre   z = w D^-1 r, res = r - K z    : read r 24 + D^-1 8 (TMA) + r 24 + mask 1
-        #                                                  (epilogue), write z 24 + res 24 B/node
-        #   <0,0,1> post  z + w D^-1 (r - K z), r.(..)   : read z 24 + r 24 + D^-1 8 + mask 1, write 24 B/node
+        #                                                  (epilogue), write res 24 B/node (z is not
+        #                                                  stored: k_mg_prolong0 recomputes it)
+        #   <0,0,1> post  w = z + w D^-1 (r - K z), r.w  : read z 24 + r 24 + D^-1 8 + mask 1, write w 24 B/node
         # each + E (8 B/el)
-        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 105, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
+        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 81, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
         per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
                 "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
                for n, b, t in var]

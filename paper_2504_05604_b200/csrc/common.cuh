@@ -148,15 +148,26 @@ __device__ bool grid_reduce(double (&v)[K], double* partials, unsigned int* coun
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
+  // each thread folds its partials with 4 independent accumulators so the L2
+  // loads are in flight together (a dependent chain of ~10 L2 round trips per
+  // value otherwise dominates the tail of short kernels); fixed order
   double t[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    double a = (k < K - KMAX) ? 0.0 : -1.0e300;
-    for (unsigned b = tid; b < nb; b += nth) {
-      double pv = __ldcg(&partials[(size_t)k * nb + b]);
-      a = (k < K - KMAX) ? a + pv : fmax(a, pv);
+    const bool mx = k >= K - KMAX;
+    const double id = mx ? -1.0e300 : 0.0;
+    double a4[4] = {id, id, id, id};
+    for (unsigned b = tid; b < nb; b += 4 * nth) {
+      double pv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const unsigned bj = b + j * nth;
+        pv[j] = bj < nb ? __ldcg(&partials[(size_t)k * nb + bj]) : id;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a4[j] = mx ? fmax(a4[j], pv[j]) : a4[j] + pv[j];
     }
-    t[k] = a;
+    t[k] = mx ? fmax(fmax(a4[0], a4[1]), fmax(a4[2], a4[3])) : (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
   {
     double s[K];

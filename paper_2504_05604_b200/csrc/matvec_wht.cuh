@@ -111,6 +111,8 @@ struct MvEpi {
   const double* b;          // 3 * ncomp
   const double* invd;       // per node
   const uint8_t* fixm;      // per node
+  float* out32;             // kEpi = 2: if set, the residual is written here in fp32 (the
+                            // restriction input of an fp32 multigrid hierarchy)
 };
 
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
@@ -348,7 +350,9 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double qv = S[c] + xch[buf][c][tz - 1][ty];
-          qp[c * ncomp] = ((efm >> c) & 1) ? 0.0 : (kEpi == 2 ? eb[c] - qv : qv);
+          const double o = ((efm >> c) & 1) ? 0.0 : (kEpi == 2 ? eb[c] - qv : qv);
+          if (kEpi == 2 && epi.out32) epi.out32[(qp - q) + c * ncomp] = (float)o;
+          else qp[c * ncomp] = o;
         }
       } else if (owned) {
         // damped-Jacobi sweep on the owner's node: out = v + w D^-1 (b - K v)

@@ -113,9 +113,9 @@ k_mg_restrict(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict
 // shared by the two coarse planes it feeds (weights 1/2, 1, 1/2 along x), so
 // the fine vector streams through HBM once.  Same sums as k_mg_restrict<false>
 // (fp64, fixed order) up to the order of the x-terms.
-template <typename TC>
+template <typename TF, typename TC>
 __global__ void __launch_bounds__(128)
-k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const double* __restrict__ res, const uint8_t* __restrict__ fixC,
+k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const TF* __restrict__ res, const uint8_t* __restrict__ fixC,
                TC* __restrict__ bC, const DevState* st) {
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
@@ -138,9 +138,9 @@ k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const double* __restrict__ res, 
         if (iy < 0 || iy > F.ny) continue;
         const double w = wz * (dy ? 0.5 : 1.0);
         const long long n = F.n(i, iy, iz);
-        g[0] = fma(w, res[n], g[0]);
-        g[1] = fma(w, res[n + F.ncomp], g[1]);
-        g[2] = fma(w, res[n + 2 * F.ncomp], g[2]);
+        g[0] = fma(w, (double)res[n], g[0]);
+        g[1] = fma(w, (double)res[n + F.ncomp], g[1]);
+        g[2] = fma(w, (double)res[n + 2 * F.ncomp], g[2]);
       }
     }
   };
@@ -200,36 +200,56 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
 // Level 0 after the coarse correction (nu = 1): z = mask(w D^-1 r + P x1).  The
 // first sweep z0 = w D^-1 r is recomputed from r instead of being stored by the
 // pre-smoothing matvec (reads r and D^-1: 32 B/node instead of a z round trip).
+// x-marching: thread per fine (iy, iz) column and x-chunk; the y-z
+// interpolation of a coarse plane is formed once and used by the 2-3 fine planes
+// that lie next to it; fine streams are coalesced in y.
 template <typename TC>
-__global__ void __launch_bounds__(kBlock)
-k_mg_prolong0(LvGeo F, LvGeo Cg, const double* __restrict__ r, const double* __restrict__ invd,
+__global__ void __launch_bounds__(128)
+k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, const double* __restrict__ invd,
               const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
               double* __restrict__ z, const DevState* st) {
   MG_GATE(st);
+  const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned ny1 = F.ny + 1;
+  if (col >= ny1 * (unsigned)(F.nz + 1)) return;
+  const int iy = (int)(col % ny1), iz = (int)(col / ny1);
+  const int ia = blockIdx.y * fx_chunk, ib = min(ia + fx_chunk, F.nx + 1);
+  if (ia >= ib) return;
   const double omega = *omp;
-  const long long tot = F.nodes();
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
-       k += (long long)gridDim.x * blockDim.x) {
-    int ix, iy, iz;
-    lv_decode(F, k, ix, iy, iz);
-    const int jx = ix >> 1, jy = iy >> 1, jz = iz >> 1;
-    const int nx = (ix & 1) + 1, ny = (iy & 1) + 1, nz = (iz & 1) + 1;
-    const double w = (nx == 2 ? 0.5 : 1.0) * (ny == 2 ? 0.5 : 1.0) * (nz == 2 ? 0.5 : 1.0);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int a = 0; a < nz; ++a)
-      for (int b = 0; b < nx; ++b)
-        for (int c = 0; c < ny; ++c) {
-          const long long j = Cg.n(jx + b, jy + c, jz + a);
-          s0 += (double)eC[j];
-          s1 += (double)eC[j + Cg.ncomp];
-          s2 += (double)eC[j + 2 * Cg.ncomp];
-        }
-    const long long i = F.n(ix, iy, iz);
-    const uint8_t fm = fixF[i];
-    const double wd = omega * invd[i];
-    z[i] = (fm & 1) ? 0.0 : fma(wd, r[i], w * s0);
-    z[i + F.ncomp] = (fm & 2) ? 0.0 : fma(wd, r[i + F.ncomp], w * s1);
-    z[i + 2 * F.ncomp] = (fm & 4) ? 0.0 : fma(wd, r[i + 2 * F.ncomp], w * s2);
+  const int jy = iy >> 1, jz = iz >> 1, oy = iy & 1, oz = iz & 1;
+  const double wy1 = oy ? 0.5 : 0.0, wy0 = 1.0 - wy1, wz1 = oz ? 0.5 : 0.0, wz0 = 1.0 - wz1;
+  auto gyz = [&](int cx, double g[3]) {   // y-z interpolation of coarse plane cx at (iy, iz)
+    const long long a = Cg.n(cx, jy, jz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const TC* e = eC + a + c * Cg.ncomp;
+      g[c] = fma(wz0, fma(wy0, (double)e[0], wy1 * (double)e[oy]),
+                 wz1 * fma(wy0, (double)e[oz * Cg.NY], wy1 * (double)e[oz * Cg.NY + oy]));
+    }
+  };
+  // planes in (even, odd) pairs: both read coarse plane c = i/2, the odd one also
+  // c+1; all loads of a pair are issued before its stores (two planes in flight)
+  double g0[3], g1[3];
+  gyz(ia >> 1, g0);
+  for (int i = ia; i < ib; i += 2) {
+    const int c = i >> 1;
+    const bool odd_ok = i + 1 < ib;
+    gyz(c + 1, g1);
+    const long long n0 = F.n(i, iy, iz), n1 = n0 + F.nplane;
+    double r0[3], r1[3];
+    const uint8_t f0 = fixF[n0], f1 = odd_ok ? fixF[n1] : (uint8_t)7;
+    const double d0 = invd[n0], d1 = odd_ok ? invd[n1] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      r0[k] = r[n0 + k * F.ncomp];
+      r1[k] = odd_ok ? r[n1 + k * F.ncomp] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      z[n0 + k * F.ncomp] = ((f0 >> k) & 1) ? 0.0 : fma(omega * d0, r0[k], g0[k]);
+      if (odd_ok) z[n1 + k * F.ncomp] = ((f1 >> k) & 1) ? 0.0 : fma(omega * d1, r1[k], 0.5 * (g0[k] + g1[k]));
+      g0[k] = g1[k];
+    }
   }
 }
 

@@ -122,6 +122,7 @@ struct Slab {
   // node vectors: 3*ncomp doubles each (SoA)
   double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
+  float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
   double* invd = nullptr;    // per node (1 component): 1/(kd sum E)
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
@@ -687,7 +688,7 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
-  const MvEpi epi{s.r, s.invd, s.fixm};
+  const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr};
   k_mv_wht<TZ, kPre, kDot, kEpi><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
                                                                          s.partials, s.counter, finish, scale, epi);
   ctx->launches++;
@@ -945,6 +946,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CU(cudaFuncSetAttribute(k_gj_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjB * kGjB * 8));
   }
   CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
+  if (ctx->mg_f32) CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
   {
     std::vector<double> om(17, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * 17));
@@ -1194,14 +1196,27 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
       int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 16 + bx - 1) / bx));
       const int cx = (n1.L.nx + 1 + chunks - 1) / chunks;
       chunks = (n1.L.nx + 1 + cx - 1) / cx;
-      k_mg_restrict0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.q, n1.fixm, mgp<T>(n1.b), gst);
+      if (ctx->mg_f32 && nu == 1)   // the pre-smoothing epilogue wrote the residual in fp32
+        k_mg_restrict0<float, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.res32, n1.fixm,
+                                                                            mgp<T>(n1.b), gst);
+      else
+        k_mg_restrict0<double, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.q, n1.fixm,
+                                                                             mgp<T>(n1.b), gst);
       ctx->launches++;
       debug_sync(ctx, "k_mg_restrict0");
     }
     CK(enqueue_vcycle_t<T>(ctx, 1, gate, false));
-    if (nu == 1)   // z = w D^-1 r (the first sweep, recomputed) + P x1
-      LAUNCH(ctx, k_mg_prolong0<T>, gF, F, n1.L, s.r, s.invd, om, mgp<T>(n1.x), s.fixm, s.z, gst);
-    else
+    if (nu == 1) {   // z = w D^-1 r (the first sweep, recomputed) + P x1, x-marching
+      const long long cols = (long long)(F.ny + 1) * (F.nz + 1);
+      const int bx = (int)((cols + 127) / 128);
+      int chunks = (int)std::max<long long>(1, std::min<long long>(F.nx + 1, (148LL * 16 + bx - 1) / bx));
+      const int cx = ((F.nx + 1 + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
+      chunks = (F.nx + 1 + cx - 1) / cx;
+      k_mg_prolong0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.r, s.invd, om, mgp<T>(n1.x), s.fixm,
+                                                                  s.z, gst);
+      ctx->launches++;
+      debug_sync(ctx, "k_mg_prolong0");
+    } else
       LAUNCH(ctx, (k_mg_prolong<true, T, double>), gF, F, n1.L, mgp<T>(n1.x), s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
       CK(mg_mv0(ctx, gate, s.m_z));
@@ -1618,7 +1633,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad,
+                    s.vpad, s.res32,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
