@@ -341,12 +341,13 @@ def main():
         # dominant kernel: the TMA-fed WHT matvec k_mv_wht, three variants per
         # MG-PCG iteration, algorithmic bytes per launch:
         #   <2,1,0> PCG   p = V(r) + beta p, q = K p, p.q : read V(r) 24 + p_old 24, write p 24 + q 24 B/node
-        #   <3,0,2> pre   z = w D^-1 r, res = r - K z    : read r 24 + D^-1 8 (TMA) + r 24 + mask 1
-        #                                                  (epilogue), write res 24 B/node (z is not
+        #   <3,0,2> pre   z = w D^-1 r, res = r - K z    : read r 24 + D^-1 8 + mask 1, write res
+        #                                                  12 (fp32 hierarchy) / 24 B/node (the
+        #                                                  epilogue's second r read hits L2; z is not
         #                                                  stored: k_mg_prolong0 recomputes it)
         #   <0,0,1> post  w = z + w D^-1 (r - K z), r.w  : read z 24 + r 24 + D^-1 8 + mask 1, write w 24 B/node
         # each + E (8 B/el)
-        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 81, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
+        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 45 if int(p.get("mg_fp32", 1)) else 57, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
         per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
                 "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
                for n, b, t in var]

@@ -1,6 +1,6 @@
 """Run BASELINE configs end to end on one GPU and report s/SIMP iteration,
 N_cg per iteration and the compliance history (for BASELINE.md).
-   python tools/run_configs.py 0 1 2 3      (config 4: use bench.py)"""
+   python tools/run_configs.py 0 1 2 3 [precond=jacobi|mg|auto]   (config 4: use bench.py)"""
 import json
 import os
 import sys
@@ -13,8 +13,9 @@ from workloads import make_problem  # noqa: E402
 from paper_2504_05604_b200 import topo  # noqa: E402
 
 out = []
-for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2, 3]:
-    p, f, fx, pas = make_problem(cfg)
+over = dict(a.split("=") for a in sys.argv[1:] if "=" in a)
+for cfg in [int(a) for a in sys.argv[1:] if "=" not in a] or [0, 1, 2, 3]:
+    p, f, fx, pas = make_problem(cfg, **over)
     n_iter = p["n_iter"]
     with topo.Problem(p, f, fx, pas) as pr:
         s = torch.cuda.Stream()
@@ -31,7 +32,7 @@ for cfg in [int(a) for a in sys.argv[1:]] or [0, 1, 2, 3]:
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         t = pr.timings()
-    rec = dict(config=cfg, grid=[p["nelx"], p["nely"], p["nelz"]], n_iter=n_iter,
+    rec = dict(config=cfg, precond=over.get("precond", "auto"), grid=[p["nelx"], p["nely"], p["nelz"]], n_iter=n_iter,
                s_per_iter_median=float(np.median(ms[2:] if len(ms) > 2 else ms)) / 1e3,
                s_per_iter_mean=float(np.mean(ms)) / 1e3, wall_s=wall, ncg=ncg, c=c,
                volume=t["volume"], launches=t["kernel_launches"])
