@@ -469,12 +469,26 @@ k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const 
     vol[k] = 0.0;
   }
   const unsigned b0 = (unsigned)(g.H * g.eplane), e0 = (unsigned)((g.H + g.nex) * g.eplane);
-  for (unsigned i = b0 + blockIdx.x * blockDim.x + threadIdx.x; i < e0; i += gridDim.x * blockDim.x) {
-    const double xv = x[i], av = A[i], dv = MODE0 ? dvf[i] : 1.0;
-    // lambda-independent clamp bounds: xnew = min(hi, max(lo, A s)) (= oc_xnew exactly)
-    const double lo = fmax(0.0, xv - move), hi = fmin(1.0, xv + move);
+  const unsigned stride = gridDim.x * blockDim.x;
+  // 4 elements per trip with all loads issued first (the pass is latency-bound
+  // otherwise); an out-of-range slot reads x = A = 0, which gives xnew = 0
+  for (unsigned i0 = b0 + blockIdx.x * blockDim.x + threadIdx.x; i0 < e0; i0 += 4 * stride) {
+    double xv[4], av[4], dv[4];
 #pragma unroll
-    for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv, fmin(hi, fmax(lo, av * sc[k])), vol[k]);
+    for (int j = 0; j < 4; ++j) {
+      const unsigned i = i0 + j * stride;
+      const bool ok = i < e0;
+      xv[j] = ok ? x[i] : 0.0;
+      av[j] = ok ? A[i] : 0.0;
+      dv[j] = MODE0 ? (ok ? dvf[i] : 0.0) : 1.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // lambda-independent clamp bounds: xnew = min(hi, max(lo, A s)) (= oc_xnew exactly)
+      const double lo = fmax(0.0, xv[j] - move), hi = fmin(1.0, xv[j] + move);
+#pragma unroll
+      for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv[j], fmin(hi, fmax(lo, av[j] * sc[k])), vol[k]);
+    }
   }
   __shared__ double tot[kOcCand];
   if (grid_reduce<kOcCand>(vol, partials, counter, tot) && threadIdx.x == 0) {

@@ -1193,7 +1193,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     {   // x-marching restriction of the masked residual (k_mg_restrict0)
       const long long cols = (long long)(n1.L.ny + 1) * (n1.L.nz + 1);
       const int bx = (int)((cols + 127) / 128);
-      int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 16 + bx - 1) / bx));
+      int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 64 + bx - 1) / bx));
       const int cx = (n1.L.nx + 1 + chunks - 1) / chunks;
       chunks = (n1.L.nx + 1 + cx - 1) / cx;
       if (ctx->mg_f32 && nu == 1)   // the pre-smoothing epilogue wrote the residual in fp32
@@ -1209,7 +1209,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     if (nu == 1) {   // z = w D^-1 r (the first sweep, recomputed) + P x1, x-marching
       const long long cols = (long long)(F.ny + 1) * (F.nz + 1);
       const int bx = (int)((cols + 127) / 128);
-      int chunks = (int)std::max<long long>(1, std::min<long long>(F.nx + 1, (148LL * 16 + bx - 1) / bx));
+      int chunks = (int)std::max<long long>(1, std::min<long long>((F.nx + 2) / 2, (148LL * 64 + bx - 1) / bx));
       const int cx = ((F.nx + 1 + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
       chunks = (F.nx + 1 + cx - 1) / cx;
       k_mg_prolong0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.r, s.invd, om, mgp<T>(n1.x), s.fixm,
