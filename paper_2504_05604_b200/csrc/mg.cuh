@@ -841,36 +841,41 @@ k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ d
 constexpr int kGjB = 64;
 
 // P = inverse of the b x b diagonal block at (k0, k0) by scalar Gauss-Jordan in
-// shared memory (one CTA)
-__global__ void __launch_bounds__(1024)
+// one CTA of b*b/4 threads: thread (i, j4) keeps a_{i, j4 + 16 m} (m < 4, b = 64)
+// in registers; per pivot the pivot column and row go through shared memory
+// (two barriers per step, no shared-memory round trip of the whole block).
+__global__ void __launch_bounds__(kGjB * kGjB / 4)
 k_gj_block_inv(const double* __restrict__ A, int ld, int k0, double* __restrict__ P) {
-  extern __shared__ double sb[];           // [kGjB][kGjB] column-major
+  constexpr int NJ = 4, JS = kGjB / NJ;               // columns per thread, column stride
   __shared__ double col[kGjB], row[kGjB];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int t = tid; t < kGjB * kGjB; t += nt) {
-    const int i = t % kGjB, j = t / kGjB;
-    sb[t] = A[(long long)(k0 + j) * ld + k0 + i];
-  }
-  __syncthreads();
+  const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;   // row i, columns j0 + JS m
+  double a[NJ];
+#pragma unroll
+  for (int m = 0; m < NJ; ++m) a[m] = A[(long long)(k0 + j0 + JS * m) * ld + k0 + i];
   for (int k = 0; k < kGjB; ++k) {
-    if (tid < kGjB) {
-      col[tid] = sb[k * kGjB + tid];       // a_ik
-      row[tid] = sb[tid * kGjB + k];       // a_kj
+    // publish the pivot column (owners: j0 + JS m == k) and row (owner: i == k)
+#pragma unroll
+    for (int m = 0; m < NJ; ++m) {
+      if (j0 + JS * m == k) col[i] = a[m];
+      if (i == k) row[j0 + JS * m] = a[m];
     }
     __syncthreads();
     const double ip = 1.0 / col[k];
-    for (int t = tid; t < kGjB * kGjB; t += nt) {
-      const int i = t % kGjB, j = t / kGjB;
+    const double cik = col[i];
+#pragma unroll
+    for (int m = 0; m < NJ; ++m) {
+      const int j = j0 + JS * m;
       double v;
       if (i == k && j == k) v = ip;
       else if (i == k) v = row[j] * ip;
-      else if (j == k) v = -col[i] * ip;
-      else v = sb[t] - col[i] * row[j] * ip;
-      sb[t] = v;
+      else if (j == k) v = -cik * ip;
+      else v = a[m] - cik * row[j] * ip;
+      a[m] = v;
     }
     __syncthreads();
   }
-  for (int t = tid; t < kGjB * kGjB; t += nt) P[t] = sb[t];
+#pragma unroll
+  for (int m = 0; m < NJ; ++m) P[(j0 + JS * m) * kGjB + i] = a[m];
 }
 
 // C = A_:,K with rows K zeroed (n_pad x b, column-major)

@@ -943,7 +943,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     if (!g_cublas.load(err)) return set_err(ctx, TOPO_ECUDA, "%s", err.c_str());
     if (g_cublas.Create(&ctx->cublas) != 0) return set_err(ctx, TOPO_ECUDA, "cublasCreate failed");
     if (g_cublas.SetWorkspace(ctx->cublas, ctx->mg_ws, ws) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetWorkspace failed");
-    CU(cudaFuncSetAttribute(k_gj_block_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, kGjB * kGjB * 8));
+
   }
   CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
   if (ctx->mg_f32) CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
@@ -1072,7 +1072,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
   const double d_one = 1.0, d_mone = -1.0, d_zero = 0.0;
   for (int k0 = 0; k0 < np; k0 += kGjB) {
-    k_gj_block_inv<<<1, 1024, kGjB * kGjB * 8, ctx->stream>>>(A, np, k0, ctx->mg_P);
+    k_gj_block_inv<<<1, kGjB * kGjB / 4, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
     ctx->launches++;
     // R = P A_K,:  (b x np)
     if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, kGjB, np, kGjB, &d_one, ctx->mg_P, kGjB, A + k0, np,
