@@ -41,9 +41,10 @@ template <typename T> struct WhtKT { T k0, o0, k7, o7, a, b, r, s; };
 using WhtK = WhtKT<double>;
 __constant__ WhtK c_wht;
 
-__device__ __forceinline__ void wht4(const double v[4], double G[4]) {
+template <typename T>
+__device__ __forceinline__ void wht4(const T v[4], T G[4]) {
   // G[k], k = my + 2 mz, from corners v[a], a = ay + 2 az
-  const double s0 = v[0] + v[1], d0 = v[0] - v[1], s1 = v[2] + v[3], d1 = v[2] - v[3];
+  const T s0 = v[0] + v[1], d0 = v[0] - v[1], s1 = v[2] + v[3], d1 = v[2] - v[3];
   G[0] = s0 + s1;
   G[1] = d0 + d1;
   G[2] = s0 - s1;
@@ -55,11 +56,15 @@ __device__ __forceinline__ void wht4(const double v[4], double G[4]) {
 // Lambda^-1 B Lambda^-1, Lambda = diag(2^|m|): level-1 multigrid (mg.cuh), fp64 and fp32
 __constant__ WhtK c_wht1;
 __constant__ WhtKT<float> c_wht1f;
+__constant__ WhtKT<float> c_whtf;   // c_wht in fp32: the multigrid smoothing matvecs with mg_fp32
 
 template <typename T>
 __device__ __forceinline__ void wht_block_k(const WhtKT<T>& K, const T P[3][8], T Ee, T Q[3][8]);
 __device__ __forceinline__ void wht_block(const double P[3][8], double Ee, double Q[3][8]) {
   wht_block_k<double>(c_wht, P, Ee, Q);
+}
+__device__ __forceinline__ void wht_block(const float P[3][8], float Ee, float Q[3][8]) {
+  wht_block_k<float>(c_whtf, P, Ee, Q);
 }
 template <typename T>
 __device__ __forceinline__ void wht_block_k(const WhtKT<T>& K, const T P[3][8], T Ee, T Q[3][8]) {
@@ -132,8 +137,11 @@ template <int TZ> struct MvSmem {
   __host__ __device__ static constexpr int bytes(int pre) { return kMvStages * stage(pre) + 3 * VA + 128; }
 };
 
-template <int TZ, int kPre, bool kDot, int kEpi>
-__global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? 2 : 1))
+// TC: arithmetic type of the element operator (double; float for the
+// multigrid smoothing matvecs with mg_fp32 -- the TMA operands stay fp64, the
+// p-planes and the Walsh-domain work are fp32, the epilogue finishes in fp64).
+template <int TZ, int kPre, bool kDot, int kEpi, typename TC>
+__global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? (sizeof(TC) == 4 ? 3 : 2) : 1))
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
          double* __restrict__ pnew, double* __restrict__ q,
          double* partials, unsigned int* counter, int finish, const double* __restrict__ scale, MvEpi epi) {
@@ -144,7 +152,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   const double beta = (kPre == 1 || kPre == 2) && !st->fresh ? st->beta : 0.0;
   const double wsc = (kPre == 3 || kEpi == 1) ? *scale : 1.0;
   extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ double xch[2][3][TZ][32];   // lanes contiguous: conflict-free
+  __shared__ TC xch[2][3][TZ][32];   // lanes contiguous: conflict-free
   __shared__ __align__(8) uint64_t full[kMvStages];
 
   const int ty = threadIdx.x, tz = threadIdx.y;
@@ -167,8 +175,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   double* qp = q + (size_t)(xs - g.ex0 + 1) * nplane + ob;
 
   auto slot = [&](int s) { return dsm + s * L::stage(kPre); };
-  double* pbuf = reinterpret_cast<double*>(dsm + kMvStages * L::stage(kPre));   // [3][3][TZ+1][YW]
-  constexpr int PB = L::VA / 8;                                                      // doubles per p-plane
+  TC* pbuf = reinterpret_cast<TC*>(dsm + kMvStages * L::stage(kPre));           // [3][3][TZ+1][YW]
+  constexpr int PB = L::VA / (int)sizeof(TC);                                        // entries per p-plane
   constexpr int CS = (TZ + 1) * L::YW;                                               // component stride
   auto issue = [&](int t) {                 // unit t: node plane j = xs-1+t, element plane j-1
     const int s = t % kMvStages;
@@ -219,14 +227,14 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   // tile plane into p-plane t%3 (plain variant: copy), owner nodes write p to
   // global; returns this thread's E_e for element plane j-1.  The raw stage is
   // fully consumed here.
-  auto prepass = [&](int t) -> double {
+  auto prepass = [&](int t) -> TC {
     const int s = t % kMvStages;
     mbar_wait(&full[s], (uint32_t)((t / kMvStages) & 1));
     const double* sv = reinterpret_cast<const double*>(slot(s));
     const double* sp = reinterpret_cast<const double*>(slot(s) + L::VA);
     const double* si = reinterpret_cast<const double*>(slot(s) + L::ioff(kPre));
     const double* se = reinterpret_cast<const double*>(slot(s) + L::eoff(kPre));
-    double* pb = pbuf + (t % 3) * PB;
+    TC* pb = pbuf + (t % 3) * PB;
     const bool wr_plane = kFused && pnew != nullptr &&
                           ((t >= 1 && t < nunits - 1) || (t == 0 && first_chunk) || (t == nunits - 1 && last_chunk));
     double* pplane = pnew + (size_t)(xs + t - g.ex0) * nplane;     // node plane j = xs-1+t
@@ -251,21 +259,21 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];
       }
 #pragma unroll
-      for (int c = 0; c < 3; ++c) pb[c * CS + n] = v[c];
+      for (int c = 0; c < 3; ++c) pb[c * CS + n] = (TC)v[c];
       if (wr_plane && pn_off[u] >= 0) {
         double* o = pplane + pn_off[u];
 #pragma unroll
         for (int c = 0; c < 3; ++c) o[(size_t)c * ncomp] = v[c];
       }
     }
-    return t > 0 ? se[tz * L::YW + ty + yoff] : 0.0;
+    return t > 0 ? (TC)se[tz * L::YW + ty + yoff] : TC(0);
   };
   // corners (k = ay + 2 az) of this thread's element column in p-plane t%3
-  auto corners_wht = [&](int t, double G[3][4]) {
-    const double* pb = pbuf + (t % 3) * PB;
+  auto corners_wht = [&](int t, TC G[3][4]) {
+    const TC* pb = pbuf + (t % 3) * PB;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double v[4];
+      TC v[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) v[k] = pb[c * CS + (tz + (k >> 1)) * L::YW + ty + yoff + (k & 1)];
       wht4(v, G[c]);
@@ -278,8 +286,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     }
   };
 
-  double G0[3][4], A[3][4];
-  double Ecur = 0.0;
+  TC G0[3][4], A[3][4];
+  TC Ecur = TC(0);
   // kEpi: the owner's epilogue operands (b, M^-1, mask) for the next node plane it
   // writes are loaded one x-step ahead, so the global loads overlap the compute
   double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0;
@@ -304,13 +312,13 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   for (int t = 1; t < nunits; ++t) {
     const int ex = xs - 2 + t;              // element plane of this step (node planes ex, ex+1)
     (void)ex;
-    double G1[3][4];
+    TC G1[3][4];
     corners_wht(t, G1);
-    const double Ee = Ecur;
+    const TC Ee = Ecur;
     if (t + 1 < nunits) Ecur = prepass(t + 1);
-    double Q[3][8];
+    TC Q[3][8];
     {
-      double P[3][8];
+      TC P[3][8];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -322,10 +330,11 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     }
     if (t >= 2) {                           // ex >= xs: complete node plane ex
       const int buf = t & 1;
-      double S[3], pbase[3];
+      TC S[3];
+      double pbase[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        double Ac[4], C[4];
+        TC Ac[4], C[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) Ac[k] = A[c][k] + (Q[c][2 * k] + Q[c][2 * k + 1]);
         wht4(Ac, C);
@@ -333,7 +342,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         xch[buf][c][tz][ty] = C[2] + __shfl_up_sync(0xffffffffu, C[3], 1);
         S[c] = C[0] + __shfl_up_sync(0xffffffffu, C[1], 1);
         // p at the owner's node of plane ex (p-plane (t-1)%3 is rewritten only after this barrier)
-        pbase[c] = (kDot || kEpi) ? pbuf[((t - 1) % 3) * PB + c * CS + tz * L::YW + ty + yoff] : 0.0;
+        pbase[c] = (kDot || kEpi) ? (double)pbuf[((t - 1) % 3) * PB + c * CS + tz * L::YW + ty + yoff] : 0.0;
       }
       __syncthreads();
       if (owned && kEpi == 0) {
@@ -342,14 +351,14 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         // p.q is unaffected.  Keeps a latency-bound byte load off this loop.
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          const double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
           qp[c * ncomp] = qv;
           if (kDot) dot = fma(pbase[c], qv, dot);
         }
       } else if (owned && (kEpi == 2 || kEpi == 3)) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          const double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
           const double o = ((efm >> c) & 1) ? 0.0 : (kEpi == 2 ? eb[c] - qv : qv);
           if (kEpi == 2 && epi.out32) epi.out32[(qp - q) + c * ncomp] = (float)o;
           else qp[c * ncomp] = o;
@@ -359,7 +368,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         const double wd = wsc * einv;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double qv = S[c] + xch[buf][c][tz - 1][ty];
+          const double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
           const double zn = ((efm >> c) & 1) ? 0.0 : fma(wd, eb[c] - qv, pbase[c]);
           qp[c * ncomp] = zn;
           dot = fma(eb[c], zn, dot);

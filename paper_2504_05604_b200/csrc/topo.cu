@@ -168,7 +168,7 @@ struct topo_ctx {
   double kd = 0.0;
   WhtK wht{};
   WhtK wht1{};              // level-1 multigrid: block constants scaled by Lambda^-1 . Lambda^-1
-  WhtKT<float> wht1f{};
+  WhtKT<float> wht1f{}, whtf{};
   int tz = 8;               // z extent of a matvec CTA (threads 32 x tz)
   std::vector<int4> st_off;
   std::vector<double> st_w;
@@ -317,6 +317,9 @@ int ensure_constants(topo_ctx* ctx) {
                               (float)w1.r, (float)w1.s};
     CU(cudaMemcpyToSymbolAsync(c_wht1, &ctx->wht1, sizeof(WhtK), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_wht1f, &ctx->wht1f, sizeof(WhtKT<float>), 0, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->whtf = WhtKT<float>{(float)w0.k0, (float)w0.o0, (float)w0.k7, (float)w0.o7, (float)w0.a, (float)w0.b,
+                             (float)w0.r, (float)w0.s};
+    CU(cudaMemcpyToSymbolAsync(c_whtf, &ctx->whtf, sizeof(WhtKT<float>), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_diag8, ctx->mg_diag8, sizeof(ctx->mg_diag8), 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzA, nzA, sizeof nzA, 0, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyToSymbolAsync(c_mg_nzW, nzW, sizeof nzW, 0, cudaMemcpyHostToDevice, ctx->stream));
@@ -678,26 +681,26 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   return TOPO_OK;
 }
 
-template <int TZ, int kPre, bool kDot, int kEpi>
+template <int TZ, int kPre, bool kDot, int kEpi, typename TC>
 int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish,
                 const double* scale) {
   static bool attr_set = false;
   const int smem = MvSmem<TZ>::bytes(kPre);
   if (!attr_set) {
-    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
   const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr};
-  k_mv_wht<TZ, kPre, kDot, kEpi><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
-                                                                         s.partials, s.counter, finish, scale, epi);
+  k_mv_wht<TZ, kPre, kDot, kEpi, TC><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
+                                                                             s.partials, s.counter, finish, scale, epi);
   ctx->launches++;
   debug_sync(ctx, kPre == 1 ? "k_mv_wht<jacobi-fused>" : kPre == 2 ? "k_mv_wht<mg-fused>"
                   : kPre == 3 ? "k_mv_wht<mg-presmooth>" : "k_mv_wht<plain>");
   return check_launch(ctx);
 }
 
-template <int kPre, bool kDot, int kEpi = 0>
+template <int kPre, bool kDot, int kEpi = 0, typename TC = double>
 int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CUtensorMap* pold, double* pnew,
               double* q, int finish, const double* scale = nullptr) {
   MvMaps maps;
@@ -705,8 +708,8 @@ int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CU
   maps.pold = pold ? *pold : vin;
   maps.invd = s.m_invd;
   maps.E = s.m_E;
-  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot, kEpi>(ctx, s, gate, maps, pnew, q, finish, scale);
-  return launch_mv_t<8, kPre, kDot, kEpi>(ctx, s, gate, maps, pnew, q, finish, scale);
+  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot, kEpi, TC>(ctx, s, gate, maps, pnew, q, finish, scale);
+  return launch_mv_t<8, kPre, kDot, kEpi, TC>(ctx, s, gate, maps, pnew, q, finish, scale);
 }
 
 // q = K v for every slab (v ghosts exchanged first; v must be 0 on fixed DOFs)
@@ -1181,7 +1184,8 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // (nu = 1) the epilogue writes the residual r - K z for the restriction
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[0], ctx->stream, cudaEventRecordExternal));
     // (nu = 1: z is not stored -- k_mg_prolong0 recomputes it with the correction)
-    if (nu == 1) CK((launch_mv<3, false, 2>(ctx, s, gate, s.m_r, nullptr, nullptr, s.q, 0, om)));
+    // (with mg_fp32 the smoothing matvecs compute the element operator in fp32)
+    if (nu == 1) CK((launch_mv<3, false, 2, T>(ctx, s, gate, s.m_r, nullptr, nullptr, s.q, 0, om)));
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
@@ -1226,7 +1230,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // last sweep fused into the matvec epilogue: w = z + w D^-1 (r - K z) (the
     // V-cycle result lives in s.w), rho = r.w and beta for the PCG
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[2], ctx->stream, cudaEventRecordExternal));
-    CK((launch_mv<0, false, 1>(ctx, s, gate, s.m_z, nullptr, nullptr, s.w, 0, om)));
+    CK((launch_mv<0, false, 1, T>(ctx, s, gate, s.m_z, nullptr, nullptr, s.w, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[3], ctx->stream, cudaEventRecordExternal));
     return check_launch(ctx);
   }
