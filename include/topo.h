@@ -123,8 +123,11 @@ typedef struct {
   int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (24..8192;
                                  0 = auto: min(5000, max(1000, n_dof / 2000)))                     */
   int32_t mg_fp32;            /* 1 (default): multigrid levels >= 1 (vectors, stencils, level-1 Galerkin
-                                 operator) in fp32 -- mixed precision: the fine level,
-                                 the PCG and every result stay fp64; 0: the whole V-cycle in fp64   */
+                                 operator) and the fine smoothing matvecs' element operator in fp32 --
+                                 mixed precision; the PCG, its matvec and every
+                                 result stay fp64.  A breakdown of the fp32 V-cycle (rounded coarse
+                                 operators of a high-contrast design can lose definiteness) promotes
+                                 the hierarchy to fp64 for the rest of the run.  0: fp64 throughout */
 } topo_params;
 
 #define TOPO_PRECOND_JACOBI 0
@@ -157,6 +160,8 @@ typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulativ
   int64_t cg_iters_total;     /* cumulative PCG iterations                                   */
   int32_t mg_fallbacks;       /* solves where the multigrid PCG broke down and was redone with
                                  the Jacobi preconditioner (cumulative)                        */
+  int32_t mg_promotions;      /* 1 once an fp32 hierarchy (mg_fp32) broke down and was promoted to
+                                 fp64 for the rest of the run (that solve is redone)           */
 } topo_timings;
 
 /* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,

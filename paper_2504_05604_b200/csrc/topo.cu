@@ -211,6 +211,7 @@ struct topo_ctx {
   // geometric multigrid (level 0 = the fine slab; mg[0] unused)
   bool mg_on = false, mg_ready = false;
   bool mg_f32 = false;               // levels >= 1 in fp32 (topo_params.mg_fp32)
+  bool mg_f32_b = false;             // ... in the snapshot
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
@@ -895,7 +896,9 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     m.L.ncomp = (long long)(h.nx + 3) * m.L.nplane;
     m.hfix = h.fix;
     m.stored = (l >= 2) || (L == 2);
-    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    // double-sized either way: an fp32 hierarchy can be promoted to fp64 in place
+    // (do_solve) by reinterpreting the same buffers
+    const size_t rs = sizeof(double);
     CK(al(&m.x, rs * 3 * m.L.ncomp));
     CK(al(&m.b, rs * 3 * m.L.ncomp));
     CK(al(&m.t, rs * 3 * m.L.ncomp));
@@ -949,7 +952,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 
   }
   CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
-  if (ctx->mg_f32) CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
+  CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
   {
     std::vector<double> om(17, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * 17));
@@ -1092,6 +1095,31 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
     LAUNCH(ctx, k_gj_put_row, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
   }
   return check_launch(ctx);
+}
+
+// Drop everything captured for the current multigrid precision (graphs of the
+// setup and of the MG-PCG batch; typed power vectors) so the next solve rebuilds it.
+void mg_invalidate(topo_ctx* ctx) {
+  if (ctx->mg_setup_exec) { cudaGraphExecDestroy(ctx->mg_setup_exec); ctx->mg_setup_exec = nullptr; }
+  if (ctx->mg_setup_exec_w) { cudaGraphExecDestroy(ctx->mg_setup_exec_w); ctx->mg_setup_exec_w = nullptr; }
+  if (ctx->cg_exec[1]) { cudaGraphExecDestroy(ctx->cg_exec[1]); ctx->cg_exec[1] = nullptr; }
+  ctx->mg_ready = false;
+  ctx->mg_warm = false;
+}
+
+// Zero the typed level buffers (after a precision change: the pads and unused
+// halves written in the other element type must read as 0).  The power vectors
+// are typed too; they are restarted cold (mg_invalidate).
+int mg_clear_levels(topo_ctx* ctx) {
+  for (MgLevel& m : ctx->mg) {
+    const size_t n3 = sizeof(double) * 3 * m.L.ncomp;
+    void* v3[] = {m.x, m.b, m.t, m.invd, m.pw};
+    for (void* v : v3)
+      if (v) CU(cudaMemsetAsync(v, 0, n3, ctx->stream));
+    if (m.S) CU(cudaMemsetAsync(m.S, 0, sizeof(double) * 126 * m.L.ncomp, ctx->stream));
+    if (m.Y) CU(cudaMemsetAsync(m.Y, 0, sizeof(double) * 24 * m.L.nel(), ctx->stream));
+  }
+  return TOPO_OK;
 }
 
 int mg_setup(topo_ctx* ctx) {
@@ -1397,6 +1425,18 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   long long iters = 0;
   int rc = solve_pass(ctx, mg, &replacements, &rr_true);
   iters = ctx->hstate->it;
+  if (rc == TOPO_EBREAKDOWN && mg && ctx->mg_f32) {
+    // the fp32 hierarchy lost positive definiteness (high-contrast designs late in
+    // an optimisation): promote it to fp64 for the rest of the run and redo the solve
+    ctx->tim.mg_promotions++;
+    ctx->mg_f32 = false;
+    mg_invalidate(ctx);
+    CK(mg_clear_levels(ctx));   // pads must read as 0.0 in the new element type
+    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
+    CK(mg_setup(ctx));
+    rc = solve_pass(ctx, 1, &replacements, &rr_true);
+    iters += ctx->hstate->it;
+  }
   if (rc == TOPO_EBREAKDOWN && mg) {
     // multigrid breakdown (an indefinite V-cycle): redo this solve with the
     // Jacobi preconditioner from u = 0 (both GPU paths; counted in timings)
@@ -2186,7 +2226,7 @@ int topo_snapshot(topo_ctx* ctx) {
     CU(cudaMemcpyAsync(s.xphys_b, s.xphys, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (ctx->mg_on) {   // the multigrid power vectors (warm-started smoother weights)
-    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    const size_t rs = sizeof(double);
     const size_t nb0 = sizeof(double) * 3 * ctx->slabs[0].g.ncomp;
     if (!ctx->mg_pw0_b) CU(cudaMalloc(&ctx->mg_pw0_b, nb0));
     CU(cudaMemcpyAsync(ctx->mg_pw0_b, ctx->mg_pw0, nb0, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -2196,6 +2236,7 @@ int topo_snapshot(topo_ctx* ctx) {
       CU(cudaMemcpyAsync(m.pw_b, m.pw, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     ctx->mg_warm_b = ctx->mg_warm;
+    ctx->mg_f32_b = ctx->mg_f32;
   }
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->snap_has_u = ctx->has_u;
@@ -2214,13 +2255,18 @@ int topo_restore(topo_ctx* ctx) {
     CU(cudaMemcpyAsync(s.xphys, s.xphys_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   }
   if (ctx->mg_on && ctx->mg_pw0_b) {
-    const size_t rs = ctx->mg_f32 ? sizeof(float) : sizeof(double);
+    const size_t rs = sizeof(double);
     CU(cudaMemcpyAsync(ctx->mg_pw0, ctx->mg_pw0_b, sizeof(double) * 3 * ctx->slabs[0].g.ncomp,
                        cudaMemcpyDeviceToDevice, ctx->stream));
     for (MgLevel& m : ctx->mg)
       if (m.pw && m.pw_b)
         CU(cudaMemcpyAsync(m.pw, m.pw_b, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
     ctx->mg_warm = ctx->mg_warm_b;
+    if (ctx->mg_f32 != ctx->mg_f32_b) {   // precision state of the snapshot (promotion undone)
+      ctx->mg_f32 = ctx->mg_f32_b;
+      mg_invalidate(ctx);
+      CK(mg_clear_levels(ctx));
+    }
   }
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->has_u = ctx->snap_has_u;

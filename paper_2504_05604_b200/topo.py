@@ -63,7 +63,8 @@ class topo_timings(C.Structure):
                 ("cg_iters", C.c_int64), ("oc_passes", C.c_int32), ("c", C.c_double),
                 ("fu", C.c_double), ("volume", C.c_double), ("change", C.c_double),
                 ("lambda_", C.c_double), ("kernel_launches", C.c_int64),
-                ("cg_iters_total", C.c_int64), ("mg_fallbacks", C.c_int32)]
+                ("cg_iters_total", C.c_int64), ("mg_fallbacks", C.c_int32),
+                ("mg_promotions", C.c_int32)]
 
 
 def _load():

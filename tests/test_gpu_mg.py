@@ -173,3 +173,17 @@ def test_mg_selection_rules(topo):
     with pytest.raises(topo.TopoError) as e:
         topo.Problem(dict(p, precond="mg"), f, fx1)
     assert e.value.code == topo.TOPO_EINVAL
+
+
+def test_mg_long_run_no_jacobi_fallback(topo):
+    """Config 1's full 50 iterations with the default (fp32-level) hierarchy: late,
+    high-contrast designs may promote the hierarchy to fp64 (mg_promotions), but the
+    solve never falls back to Jacobi and the c history matches the oracle."""
+    p, f, fx, pas = make_problem(1)
+    ro = oracle.run_optimization(p, f, fx, pas, n_iter=50)
+    with topo.Problem(p, f, fx, pas) as pr:
+        c, x, nd = pr.optimize(50)
+        t = pr.timings()
+    assert t["mg_fallbacks"] == 0
+    assert t["mg_promotions"] in (0, 1)
+    assert_rel(c, ro["c"], 1e-6, "c history (50 iterations, MG)")
