@@ -125,9 +125,10 @@ typedef struct {
   int32_t mg_fp32;            /* 1 (default): multigrid levels >= 1 (vectors, stencils, level-1 Galerkin
                                  operator) and the fine smoothing matvecs' element operator in fp32 --
                                  mixed precision; the PCG, its matvec and every
-                                 result stay fp64.  A breakdown of the fp32 V-cycle (rounded coarse
-                                 operators of a high-contrast design can lose definiteness) promotes
-                                 the hierarchy to fp64 for the rest of the run.  0: fp64 throughout */
+                                 result stay fp64.  Safety net: a breakdown of the fp32 V-cycle
+                                 (indefinite preconditioner) promotes the hierarchy to fp64 for the
+                                 rest of the run; none observed on the BASELINE configs or the
+                                 paper protocol.  0: fp64 throughout                               */
 } topo_params;
 
 #define TOPO_PRECOND_JACOBI 0

@@ -339,6 +339,8 @@ k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, T* __restrict__ v) {
   }
 }
 
+constexpr int kMgScaleOff = 17;   // mg_om layout: [0,16) weights, [16] = 1.0, [17,33) power-vector scales
+
 template <bool kNodeD, typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T* __restrict__ invd,
@@ -363,7 +365,22 @@ k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T
   }
   __shared__ double tot_sh[2];
   double r[2] = {vt, vdv};
-  if (grid_reduce<2>(r, partials, counter, tot_sh) && threadIdx.x == 0) *om_out = theta * tot_sh[1] / tot_sh[0];
+  if (grid_reduce<2>(r, partials, counter, tot_sh) && threadIdx.x == 0) {
+    om_out[0] = theta * tot_sh[1] / tot_sh[0];
+    // 1 / ||v||_D: the vector kept for the next design's warm start is stored
+    // normalised (unnormalised, it grows by ~lam per power step and overflows
+    // after a few dozen designs in fp32, a few hundred in fp64)
+    om_out[kMgScaleOff] = tot_sh[1] > 0.0 ? 1.0 / sqrt(tot_sh[1]) : 1.0;
+  }
+}
+
+// dst = s * src (s on the device: the power vector's 1/||v||_D)
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_mg_scale_copy(const T* __restrict__ src, T* __restrict__ dst, long long n, const double* __restrict__ sp) {
+  const double sc = *sp;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = (T)(sc * (double)src[i]);
 }
 
 // ---------------------------------------------------------------------------

@@ -221,7 +221,7 @@ struct topo_ctx {
   int mg_n = 0;                      // free DOFs of the coarsest level
   int* mg_dmap = nullptr;            // coarsest: level DOF index -> dense index or -1
   long long* mg_imap = nullptr;      // coarsest: dense index -> level DOF index
-  double* mg_om = nullptr;           // [17]: smoother weight per level; [16] = 1.0
+  double* mg_om = nullptr;           // [33]: smoother weight per level; [16] = 1.0; [17 + l] = 1/||pw_l||_D
   cudaGraphExec_t mg_setup_exec = nullptr;     // first design: 8 power steps from the hash vector
   cudaGraphExec_t mg_setup_exec_w = nullptr;   // later designs: 3 steps from the previous vector
   long long mg_setup_launches_w = 0;
@@ -954,9 +954,9 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
   CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
   {
-    std::vector<double> om(17, 1.0);
-    CK(al((void**)&ctx->mg_om, sizeof(double) * 17));
-    CU(cudaMemcpy(ctx->mg_om, om.data(), sizeof(double) * 17, cudaMemcpyHostToDevice));
+    std::vector<double> om(kMgScaleOff + 16, 1.0);
+    CK(al((void**)&ctx->mg_om, sizeof(double) * om.size()));
+    CU(cudaMemcpy(ctx->mg_om, om.data(), sizeof(double) * om.size(), cudaMemcpyHostToDevice));
   }
   // Galerkin tables
   {
@@ -1045,7 +1045,8 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       double* tlast = (nsteps & 1) ? s.w : s.q;
       LAUNCH(ctx, (k_mg_rayleigh<true, double>), gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om,
              s.partials, s.counter);
-      CU(cudaMemcpyAsync(ctx->mg_pw0, s.z, sizeof(double) * 3 * s.g.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
+      LAUNCH(ctx, k_mg_scale_copy<double>, grid_for(3 * s.g.ncomp), s.z, ctx->mg_pw0, 3 * s.g.ncomp,
+             ctx->mg_om + kMgScaleOff);
     } else {
       MgLevel& m = ctx->mg[l];
       const int gL = grid_for(m.L.nodes());
@@ -1061,10 +1062,11 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
         LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mgp<T>(m.t), mgp<T>(m.t), mgp<T>(m.invd), m.fixm, one,
                mgp<T>(m.x), s.st, 0, s.partials, s.counter);
       }
-      CU(cudaMemcpyAsync(m.pw, m.x, sizeof(T) * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
       CK(mg_apply<T>(ctx, l, 0));
       LAUNCH(ctx, (k_mg_rayleigh<false, T>), gL, m.L, mgp<T>(m.x), mgp<T>(m.t), mgp<T>(m.invd), m.fixm,
              ctx->prm.mg_omega, ctx->mg_om + l, s.partials, s.counter);
+      LAUNCH(ctx, k_mg_scale_copy<T>, grid_for(3 * m.L.ncomp), mgp<T>(m.x), mgp<T>(m.pw), 3 * m.L.ncomp,
+             ctx->mg_om + kMgScaleOff + l);
     }
   }
   const MgLevel& c = ctx->mg[L - 1];

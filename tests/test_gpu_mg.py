@@ -176,14 +176,32 @@ def test_mg_selection_rules(topo):
 
 
 def test_mg_long_run_no_jacobi_fallback(topo):
-    """Config 1's full 50 iterations with the default (fp32-level) hierarchy: late,
-    high-contrast designs may promote the hierarchy to fp64 (mg_promotions), but the
-    solve never falls back to Jacobi and the c history matches the oracle."""
+    """Config 1's full 50 iterations with the default (fp32-level) hierarchy: the
+    warm-started smoother-weight estimate stays finite (normalised power vectors),
+    so the hierarchy is never promoted to fp64, the solve never falls back to
+    Jacobi and the c history matches the oracle."""
     p, f, fx, pas = make_problem(1)
     ro = oracle.run_optimization(p, f, fx, pas, n_iter=50)
     with topo.Problem(p, f, fx, pas) as pr:
         c, x, nd = pr.optimize(50)
         t = pr.timings()
     assert t["mg_fallbacks"] == 0
-    assert t["mg_promotions"] in (0, 1)
+    assert t["mg_promotions"] == 0
     assert_rel(c, ro["c"], 1e-6, "c history (50 iterations, MG)")
+
+
+@pytest.mark.gpu
+def test_mg_paper_protocol_200_iterations(topo):
+    """The paper's 200-iteration benchmark protocol (NEXT f1) on the
+    default hierarchy: 400+ warm power steps per level over the run must neither
+    overflow the smoother-weight estimate (promotion) nor break the V-cycle
+    (Jacobi fallback); iteration counts stay multigrid-like throughout."""
+    p, f, fx, pas = make_problem("paper")
+    with topo.Problem(p, f, fx, pas) as pr:
+        ncg = []
+        for _ in range(200):
+            pr.optimize(1)
+            ncg.append(pr.timings()["cg_iters"])
+        t = pr.timings()
+    assert t["mg_fallbacks"] == 0 and t["mg_promotions"] == 0
+    assert max(ncg) <= 40, ncg

@@ -15,6 +15,6 @@ with topo.Problem(p, f, fx, pas) as pr:
     for it in range(p["n_iter"]):
         pr.optimize(1)
         t = pr.timings()
-        rows.append((t["cg_iters"], t["mg_fallbacks"]))
-print(json.dumps(dict(cfg=str(cfg), over=over, ncg=[r[0] for r in rows], fallbacks=rows[-1][1],
+        rows.append((t["cg_iters"], t["mg_fallbacks"], t["mg_promotions"]))
+print(json.dumps(dict(cfg=str(cfg), over=over, ncg=[r[0] for r in rows], fallbacks=rows[-1][1], promotions=rows[-1][2],
                       first_fallback_it=next((i for i, r in enumerate(rows) if r[1] > 0), None))))

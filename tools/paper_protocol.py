@@ -48,12 +48,15 @@ def main():
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         vol = pr.timings()["volume"]
+        tt = pr.timings()
+        mgc = dict(levels=pr.mg_levels(), fallbacks=tt["mg_fallbacks"], promotions=tt["mg_promotions"])
     tot = sum(ph.values())
     rec = {"workload": "paper protocol 32x16x16, volfrac 0.2, penal 3, rmin 4, point load, "
                        "sensitivity filter, PCG rtol 1e-10",
            "iterations": args.iters, "gpu_wall_s": wall, "gpu_phase_s": ph,
            "gpu_phase_pct": {k: 100 * v / tot for k, v in ph.items()},
-           "cg_iters_mean": float(np.mean(ncg)), "c_first": c[0], "c_last": c[-1], "volume": vol,
+           "cg_iters_mean": float(np.mean(ncg)), "cg_iters": ncg, "multigrid": mgc,
+           "c_first": c[0], "c_last": c[-1], "volume": vol,
            "paper_table1_s": PAPER_TABLE1,
            "speedup_vs_paper_total": PAPER_TABLE1["total"] / wall}
     if args.oracle_iters > 0:
