@@ -1230,7 +1230,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
       int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 64 + bx - 1) / bx));
       const int cx = (n1.L.nx + 1 + chunks - 1) / chunks;
       chunks = (n1.L.nx + 1 + cx - 1) / cx;
-      if (ctx->mg_f32 && nu == 1)   // the pre-smoothing epilogue wrote the residual in fp32
+      if (ctx->mg_f32)   // the pre-smoothing residual epilogue (kEpi = 2) wrote it in fp32
         k_mg_restrict0<float, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.res32, n1.fixm,
                                                                             mgp<T>(n1.b), gst);
       else

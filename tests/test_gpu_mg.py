@@ -85,7 +85,7 @@ def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst, fp32):
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu,fp32", [(1, 0), (2, 0), (1, 1)])
+@pytest.mark.parametrize("nu,fp32", [(1, 0), (2, 0), (1, 1), (2, 1)])
 def test_mg_vcycle_parity(topo, dims, obst, nu, fp32):
     p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32)
     lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=1000), theta=1.5)
@@ -99,11 +99,11 @@ def test_mg_vcycle_parity(topo, dims, obst, nu, fp32):
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("fp32", [0, 1])
-def test_mg_solve_parity(topo, dims, obst, fp32):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32)
+@pytest.mark.parametrize("nu,fp32", [(1, 0), (1, 1), (2, 1)])
+def test_mg_solve_parity(topo, dims, obst, nu, fp32):
+    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu)
     uo = oracle.solve_direct(K, f, fx)
-    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.4, nu=1)
+    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.4, nu=nu)
     its = {}
     for pc in ("jacobi", "mg"):
         with topo.Problem(dict(p, precond=pc), f, fx, pas) as pr:
