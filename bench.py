@@ -41,41 +41,57 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region: ONE
+    `nvidia-smi -lms 200` process (the profiling recipe's clocks line), started
+    before the timed region and stopped after it.  (Spawning nvidia-smi per sample
+    stalls the library's host-side batch polling and costs ~15 % at config 4.)"""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device):
+    def __init__(self, device, enabled=True):
         self.device = device
+        self.enabled = enabled
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
+        self._first = threading.Event()
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self._p.stdout:
+            line = line.strip()
+            if line and line[0].isdigit():
+                self.samples.append([v.strip() for v in line.split(",")])
+                self._first.set()
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
+        if not self.enabled:
+            return self
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self._p = None
+            return self
+        self._t = threading.Thread(target=self._read, daemon=True)
         self._t.start()
+        self._first.wait(5.0)          # nvidia-smi is up and sampling before timing starts
+        self.samples.clear()           # keep only samples taken during the timed region
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -217,6 +233,7 @@ def main():
     ap.add_argument("--precond", default="auto", choices=["auto", "mg", "jacobi"],
                     help="PCG preconditioner (auto: geometric multigrid on one GPU, Jacobi on x-slabs)")
     ap.add_argument("--mg-coarse-max", type=int, default=0, help="coarsest MG level DOF bound (0 = library auto)")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")
     ap.add_argument("--mg-omega", type=float, default=1.4, help="MG smoother theta (w_l = theta / lam_l)")
     args = ap.parse_args()
@@ -267,7 +284,7 @@ def main():
     # ---- warm-up SIMP iterations (untimed) ----
     cg_warm = []
     for _ in range(args.warmup):
-        pr.optimize(1)
+        pr.optimize(1, want_x=False)
         cg_warm.append(pr.timings()["cg_iters"])
 
     # ---- timed SIMP iterations (device-resident inputs) ----
@@ -277,13 +294,13 @@ def main():
     cg_timed, phase = [], []
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, not args.no_clocks) as clk:
         with torch.cuda.stream(stream):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(args.steps):
-                c_hist, _, _ = pr.optimize(1)
+                c_hist, _, _ = pr.optimize(1, want_x=False)   # device-resident: the design stays in HBM
                 t = pr.timings()
                 cg_timed.append(t["cg_iters"])
                 phase.append({k: t[k] for k in ("ms_efield", "ms_solve", "ms_sens", "ms_filter", "ms_oc")})

@@ -281,12 +281,14 @@ class Problem:
                                       C.byref(vol)), "topo_oc_step")
         return xnew, lam.value, chg.value, vol.value
 
-    def optimize(self, n_iter, change_tol=0.0, x_out=None):
+    def optimize(self, n_iter, change_tol=0.0, x_out=None, want_x=True):
+        """n_iter SIMP iterations; returns (c history, x or None, iterations done).
+        want_x=False skips the design download (x stays in HBM)."""
         c_hist = np.zeros(n_iter)
-        x = x_out if x_out is not None else np.zeros(self.n_el)
+        x = x_out if x_out is not None else (np.zeros(self.n_el) if want_x else None)
         nd = C.c_int32()
         self._check(_lib.topo_optimize(self._ctx, int(n_iter), float(change_tol), _dp(c_hist),
-                                       _dp(x), C.byref(nd)), "topo_optimize")
+                                       _dp(x) if x is not None else None, C.byref(nd)), "topo_optimize")
         return c_hist[:nd.value], x, nd.value
 
     def apply_K(self, p):
