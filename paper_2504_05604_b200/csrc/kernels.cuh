@@ -196,9 +196,22 @@ __global__ void k_finish_alpha(DevState* st) {
   if (!(pq > 0.0) || !isfinite(pq)) { st->status = 3; st->done = 1; }
   else st->alpha = st->rz / pq;
 }
+template <bool kMG = false>
 __global__ void k_finish_update(DevState* st, int even) {
   if (st->done) return;
-  cg_finish_update(st, st->sums[0], st->sums[1], even);
+  cg_finish_update<kMG>(st, st->sums[0], st->sums[1], even);
+}
+// multigrid PCG: rho = r.V(r) of the V-cycle's last sweep (allreduced) -> beta, rz
+__global__ void k_finish_rho(DevState* st) {
+  if (st->done) return;
+  const double rho = st->sums[0];
+  if (!(rho > 0.0) || !isfinite(rho)) {
+    st->status = 3;
+    st->done = 1;
+  } else {
+    st->beta = st->fresh ? 0.0 : rho / st->rz;
+    st->rz = rho;
+  }
 }
 
 // r = f - q, 0 on fixed DOFs (q arrives unmasked from the matvec); partial

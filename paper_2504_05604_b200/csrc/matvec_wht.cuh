@@ -394,7 +394,9 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     double vv[1] = {dot};
     if (grid_reduce<1>(vv, partials, counter, tot) && leader) {
       const double rho = tot[0];
-      if (!(rho > 0.0) || !isfinite(rho)) {
+      if (!finish) {                         // x-slabs: allreduced, then k_finish_rho
+        st->sums[0] = rho;
+      } else if (!(rho > 0.0) || !isfinite(rho)) {
         st->status = 3;
         st->done = 1;
       } else {

@@ -113,20 +113,28 @@ k_mg_restrict(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict
 // shared by the two coarse planes it feeds (weights 1/2, 1, 1/2 along x), so
 // the fine vector streams through HBM once.  Same sums as k_mg_restrict<false>
 // (fp64, fixed order) up to the order of the x-terms.
+//
+// x-slabs (W > 1): res holds the fine planes [xa, xb) (global x; local plane 0
+// at global x0) of one slab; planes outside contribute 0, the coarse planes
+// j0 .. j0 + gridDim.y * cx_chunk - 1 that these planes reach are written, and
+// with `accum` added to bC (zeroed first), so the sum over slabs -- in slab
+// order (loopback) or by an allreduce (NCCL) -- is the restriction of the whole
+// residual.  Single slab: x0 = 0, [xa, xb) = [0, nx], j0 = 0, accum = 0.
 template <typename TF, typename TC>
 __global__ void __launch_bounds__(128)
 k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const TF* __restrict__ res, const uint8_t* __restrict__ fixC,
-               TC* __restrict__ bC, const DevState* st) {
+               TC* __restrict__ bC, const DevState* st, int x0, int xa, int xb, int j0, int jend, int accum) {
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned ny1 = Cg.ny + 1;
   if (col >= ny1 * (unsigned)(Cg.nz + 1)) return;
   const int jy = (int)(col % ny1), jz = (int)(col / ny1);
-  const int ja = blockIdx.y * cx_chunk, jb = min(ja + cx_chunk, Cg.nx + 1);
+  const int ja = j0 + blockIdx.y * cx_chunk, jb = min(ja + cx_chunk, jend);
   if (ja >= jb) return;
   auto gyz = [&](int i, double g[3]) {     // y-z restriction of fine plane i at (jy, jz)
     g[0] = g[1] = g[2] = 0.0;
-    if (i < 0 || i > F.nx) return;
+    if (i < xa || i >= xb) return;
+    i -= x0;
 #pragma unroll
     for (int dz = -1; dz <= 1; ++dz) {
       const int iz = 2 * jz + dz;
@@ -155,7 +163,12 @@ k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const TF* __restrict__ res, cons
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double v = fma(0.5, gp[c], fma(0.5, go[c], ge[c]));
-      bC[j + c * Cg.ncomp] = (TC)(((fc >> c) & 1) ? 0.0 : v);
+      const long long o = j + c * Cg.ncomp;
+      if (accum) {
+        if (!((fc >> c) & 1)) bC[o] = (TC)((double)bC[o] + v);
+      } else {
+        bC[o] = (TC)(((fc >> c) & 1) ? 0.0 : v);
+      }
       gp[c] = go[c];
     }
   }
@@ -203,17 +216,20 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
 // x-marching: thread per fine (iy, iz) column and x-chunk; the y-z
 // interpolation of a coarse plane is formed once and used by the 2-3 fine planes
 // that lie next to it; fine streams are coalesced in y.
+// x-slabs: the fine planes [pa, pb) (global x; a slab's owned planes plus its
+// ghost planes, local plane 0 at global x0) are written; chunks start at the even
+// plane pa & ~1.  Single slab: x0 = 0, [pa, pb) = [0, nx].
 template <typename TC>
 __global__ void __launch_bounds__(128)
 k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, const double* __restrict__ invd,
               const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
-              double* __restrict__ z, const DevState* st) {
+              double* __restrict__ z, const DevState* st, int x0, int pa, int pb) {
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned ny1 = F.ny + 1;
   if (col >= ny1 * (unsigned)(F.nz + 1)) return;
   const int iy = (int)(col % ny1), iz = (int)(col / ny1);
-  const int ia = blockIdx.y * fx_chunk, ib = min(ia + fx_chunk, F.nx + 1);
+  const int ia = (pa & ~1) + blockIdx.y * fx_chunk, ib = min(ia + fx_chunk, pb);
   if (ia >= ib) return;
   const double omega = *omp;
   const int jy = iy >> 1, jz = iz >> 1, oy = iy & 1, oz = iz & 1;
@@ -233,20 +249,21 @@ k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, con
   gyz(ia >> 1, g0);
   for (int i = ia; i < ib; i += 2) {
     const int c = i >> 1;
+    const bool even_ok = i >= pa;             // only the first pair of a slab can start below pa
     const bool odd_ok = i + 1 < ib;
     gyz(c + 1, g1);
-    const long long n0 = F.n(i, iy, iz), n1 = n0 + F.nplane;
+    const long long n0 = F.n(i - x0, iy, iz), n1 = n0 + F.nplane;
     double r0[3], r1[3];
-    const uint8_t f0 = fixF[n0], f1 = odd_ok ? fixF[n1] : (uint8_t)7;
-    const double d0 = invd[n0], d1 = odd_ok ? invd[n1] : 0.0;
+    const uint8_t f0 = even_ok ? fixF[n0] : (uint8_t)7, f1 = odd_ok ? fixF[n1] : (uint8_t)7;
+    const double d0 = even_ok ? invd[n0] : 0.0, d1 = odd_ok ? invd[n1] : 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      r0[k] = r[n0 + k * F.ncomp];
+      r0[k] = even_ok ? r[n0 + k * F.ncomp] : 0.0;
       r1[k] = odd_ok ? r[n1 + k * F.ncomp] : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      z[n0 + k * F.ncomp] = ((f0 >> k) & 1) ? 0.0 : fma(omega * d0, r0[k], g0[k]);
+      if (even_ok) z[n0 + k * F.ncomp] = ((f0 >> k) & 1) ? 0.0 : fma(omega * d0, r0[k], g0[k]);
       if (odd_ok) z[n1 + k * F.ncomp] = ((f1 >> k) & 1) ? 0.0 : fma(omega * d1, r1[k], 0.5 * (g0[k] + g1[k]));
       g0[k] = g1[k];
     }
@@ -323,16 +340,22 @@ __device__ __forceinline__ double mg_hash_unit(unsigned long long k) {
   return 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
 }
 
+// Node planes [xa, xb] (global x) of a vector stored with local plane 0 at
+// global x0 (a slab: x0 = ex0, the ghost planes included; one level: x0 = 0);
+// the hash uses global coordinates (nxg = global element count in x), so every
+// slab produces the same entries as the single-slab vector.
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_mg_start_vec(LvGeo L, const uint8_t* __restrict__ fix, T* __restrict__ v) {
-  const long long tot = L.nodes();
+k_mg_start_vec(LvGeo L, int x0, int xa, int xb, int nxg, const uint8_t* __restrict__ fix, T* __restrict__ v) {
+  const long long tot = (long long)(xb - xa + 1) * (L.ny + 1) * (L.nz + 1);
+  const LvGeo D{xb - xa, L.ny, L.nz, L.NY, L.nplane, L.ncomp};   // decode range only
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     int ix, iy, iz;
-    lv_decode(L, k, ix, iy, iz);
-    const long long i = L.n(ix, iy, iz);
-    const unsigned long long ext = ((unsigned long long)iz * (L.nx + 1) + ix) * (L.ny + 1) + iy;
+    lv_decode(D, k, ix, iy, iz);
+    ix += xa;
+    const long long i = L.n(ix - x0, iy, iz);
+    const unsigned long long ext = ((unsigned long long)iz * (nxg + 1) + ix) * (L.ny + 1) + iy;
     const uint8_t fm = fix[i];
 #pragma unroll
     for (int c = 0; c < 3; ++c) v[i + c * L.ncomp] = (T)(((fm >> c) & 1) ? 0.0 : mg_hash_unit(3 * ext + c));
@@ -345,7 +368,7 @@ template <bool kNodeD, typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T* __restrict__ invd,
               const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out, double* partials,
-              unsigned int* counter) {
+              unsigned int* counter, DevState* st = nullptr) {
   const long long tot = L.nodes();
   double vt = 0.0, vdv = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -366,12 +389,22 @@ k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T
   __shared__ double tot_sh[2];
   double r[2] = {vt, vdv};
   if (grid_reduce<2>(r, partials, counter, tot_sh) && threadIdx.x == 0) {
+    if (st) {   // slab partial: (v.t, v.Dv) allreduced, then k_mg_rayleigh_finish
+      st->sums[0] = tot_sh[0];
+      st->sums[1] = tot_sh[1];
+      return;
+    }
     om_out[0] = theta * tot_sh[1] / tot_sh[0];
     // 1 / ||v||_D: the vector kept for the next design's warm start is stored
     // normalised (unnormalised, it grows by ~lam per power step and overflows
     // after a few dozen designs in fp32, a few hundred in fp64)
     om_out[kMgScaleOff] = tot_sh[1] > 0.0 ? 1.0 / sqrt(tot_sh[1]) : 1.0;
   }
+}
+
+__global__ void k_mg_rayleigh_finish(const DevState* st, double theta, double* __restrict__ om_out) {
+  om_out[0] = theta * st->sums[1] / st->sums[0];
+  om_out[kMgScaleOff] = st->sums[1] > 0.0 ? 1.0 / sqrt(st->sums[1]) : 1.0;
 }
 
 // dst = s * src (s on the device: the power vector's 1/||v||_D)

@@ -36,7 +36,7 @@ namespace {
 typedef struct ncclComm* ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { ncclFloat64 = 8 };
+enum { ncclFloat32 = 7, ncclFloat64 = 8 };
 enum { ncclSum = 0, ncclMax = 2 };
 struct NcclApi {
   void* h = nullptr;
@@ -123,6 +123,7 @@ struct Slab {
   double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
   float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
+  double *pw0 = nullptr, *pw0_b = nullptr;   // multigrid level-0 power vector (+ snapshot)
   double* invd = nullptr;    // per node (1 component): 1/(kd sum E)
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
@@ -226,7 +227,10 @@ struct topo_ctx {
   cudaGraphExec_t mg_setup_exec_w = nullptr;   // later designs: 3 steps from the previous vector
   long long mg_setup_launches_w = 0;
   bool mg_warm = false, mg_warm_b = false;     // power vectors valid (and in the snapshot)
-  double *mg_pw0 = nullptr, *mg_pw0_b = nullptr;   // level-0 power vector (+ snapshot)
+  // x-slabs (W > 1): levels >= 1 are replicated (every rank, or once in loopback
+  // mode); level 1 is formed from the whole grid's moduli, gathered per design
+  Geo mg_gG{};                       // whole-grid element geometry of mg_gE
+  double* mg_gE = nullptr;           // whole-grid E (W > 1; W = 1 uses slab 0's E)
   long long mg_setup_launches = 0;
   int mg_batch = 2;
 };
@@ -613,6 +617,7 @@ int update_modulus(topo_ctx* ctx) {
     LAUNCH(ctx, k_invdiag, grid_for((long long)s.g.nown * s.g.nplane), s.g, m, s.E, s.fixm, s.invd);
   }
   CK(check_launch(ctx));
+  CK(exchange_nodes(ctx, &Slab::invd, 1));   // ghost planes feed the fused pre-passes and the prolongation
   ctx->has_E = true;
   ctx->mg_ready = false;
   return TOPO_OK;
@@ -758,7 +763,7 @@ int enqueue_cg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   }
   if (!fin) {
     CK(allreduce(ctx, 0, 2, 0));
-    for (Slab& s : ctx->slabs) { k_finish_update<<<1, 1, 0, ctx->stream>>>(s.st, parity ? 0 : 1); ctx->launches++; }
+    for (Slab& s : ctx->slabs) { k_finish_update<false><<<1, 1, 0, ctx->stream>>>(s.st, parity ? 0 : 1); ctx->launches++; }
     CK(exchange_nodes(ctx, &Slab::r));
   }
   return check_launch(ctx);
@@ -814,6 +819,45 @@ LvGeo lv0(const topo_ctx* ctx) {
   return LvGeo{g.nelx, g.nely, g.nelz, g.NY, g.nplane, g.ncomp};
 }
 const LvGeo& lvg(const topo_ctx* ctx, int l) { return ctx->mg[l].L; }
+// level 0 of slab s: its owned node planes (local plane 0 = global ex0)
+LvGeo lv_slab(const Slab& s) { return LvGeo{s.g.nown - 1, s.g.nely, s.g.nelz, s.g.NY, s.g.nplane, s.g.ncomp}; }
+// element geometry / moduli the replicated levels >= 1 are formed from
+const Geo& mgG(const topo_ctx* ctx) { return ctx->world > 1 ? ctx->mg_gG : ctx->slabs[0].g; }
+const double* mgE(const topo_ctx* ctx) { return ctx->world > 1 ? ctx->mg_gE : ctx->slabs[0].E; }
+
+// x-slabs: all-gather of the owned element planes of E into mg_gE (per design)
+int mg_gather_E(topo_ctx* ctx) {
+  if (ctx->world == 1) return TOPO_OK;
+  const Geo& G = ctx->mg_gG;
+  auto dst = [&](int ex0) { return ctx->mg_gE + (size_t)(ex0 + G.H) * G.eplane; };
+  if (ctx->mode == TOPO_DIST_LOOPBACK) {
+    for (Slab& s : ctx->slabs)
+      CU(cudaMemcpyAsync(dst(s.g.ex0), s.E + (size_t)s.g.H * s.g.eplane, sizeof(double) * s.g.nex * s.g.eplane,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    return TOPO_OK;
+  }
+  Slab& a = ctx->slabs[0];
+  CU(cudaMemcpyAsync(dst(a.g.ex0), a.E + (size_t)a.g.H * a.g.eplane, sizeof(double) * a.g.nex * a.g.eplane,
+                     cudaMemcpyDeviceToDevice, ctx->stream));
+  NC(g_nccl.GroupStart());
+  for (int r = 0; r < ctx->world; ++r) {
+    if (r == ctx->rank) continue;
+    int b = 0, e = 0;
+    topo_partition(ctx->prm.nelx, ctx->prm.rmin, ctx->world, r, &b, &e);
+    NC(g_nccl.Send(a.E + (size_t)a.g.H * a.g.eplane, (size_t)a.g.nex * a.g.eplane, ncclFloat64, r, ctx->comm,
+                   ctx->stream));
+    NC(g_nccl.Recv(dst(b), (size_t)(e - b) * G.eplane, ncclFloat64, r, ctx->comm, ctx->stream));
+  }
+  NC(g_nccl.GroupEnd());
+  return TOPO_OK;
+}
+
+// x-slabs, NCCL: sum of the slabs' partial level-1 restrictions (in place)
+int mg_allreduce_level(topo_ctx* ctx, void* buf, size_t n, bool f32) {
+  if (ctx->world == 1 || ctx->mode == TOPO_DIST_LOOPBACK) return TOPO_OK;   // loopback: accumulated in slab order
+  NC(g_nccl.AllReduce(buf, buf, n, f32 ? ncclFloat32 : ncclFloat64, ncclSum, ctx->comm, ctx->stream));
+  return TOPO_OK;
+}
 
 // Hierarchy on the host (init): dims, coarse Dirichlet masks (M4: the node at the
 // clamped position min(2j, n) decides), property Q, allocations, coarsest maps.
@@ -821,8 +865,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   const topo_params& P = ctx->prm;
   ctx->mg_on = false;
   if (P.precond == TOPO_PRECOND_JACOBI) return TOPO_OK;
-  if (ctx->world != 1 || ctx->slabs.size() != 1) {
-    if (P.precond == TOPO_PRECOND_MG) return set_err(ctx, TOPO_EINVAL, "multigrid needs a single slab (world == 1)");
+  if (ctx->world > 1 && P.mg_nu != 1) {   // x-slabs: the fused nu = 1 level-0 path only
+    if (P.precond == TOPO_PRECOND_MG) return set_err(ctx, TOPO_EINVAL, "multigrid on x-slabs needs mg_nu == 1");
     return TOPO_OK;
   }
   struct H { int nx, ny, nz; std::vector<uint8_t> fix; };
@@ -951,8 +995,22 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     if (g_cublas.SetWorkspace(ctx->cublas, ctx->mg_ws, ws) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetWorkspace failed");
 
   }
-  CK(al((void**)&ctx->mg_pw0, sizeof(double) * 3 * ctx->slabs[0].g.ncomp));
-  CK(al((void**)&ctx->slabs[0].res32, sizeof(float) * 3 * ctx->slabs[0].g.ncomp));
+  for (Slab& s : ctx->slabs) {
+    CK(al((void**)&s.pw0, sizeof(double) * 3 * s.g.ncomp));
+    CK(al((void**)&s.res32, sizeof(float) * 3 * s.g.ncomp));
+  }
+  if (ctx->world > 1) {   // whole-grid moduli for the replicated levels >= 1
+    Geo G = ctx->slabs[0].g;
+    G.ex0 = 0;
+    G.ex1 = G.nex = P.nelx;
+    G.nown = P.nelx + 1;
+    G.NXL = G.nown + 2;
+    G.ncomp = (long long)G.NXL * G.nplane;
+    G.NEXL = G.nex + 2 * G.H;
+    G.nelloc = (long long)G.NEXL * G.eplane;
+    ctx->mg_gG = G;
+    CK(al((void**)&ctx->mg_gE, sizeof(double) * G.nelloc));
+  }
   {
     std::vector<double> om(kMgScaleOff + 16, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * om.size()));
@@ -985,8 +1043,8 @@ template <typename T>
 int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst) {
   Slab& s = ctx->slabs[0];
   const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
-  k_mg_l1_elem<T><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(s.g, m.L, s.E, mgp<T>(m.x), mgp<T>(m.Y),
-                                                                             gst);
+  k_mg_l1_elem<T><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), mgp<T>(m.x),
+                                                                             mgp<T>(m.Y), gst);
   ctx->launches++;
   debug_sync(ctx, "k_mg_l1_elem");
   return check_launch(ctx);
@@ -1001,18 +1059,19 @@ template <typename T>
 int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size();
+  CK(mg_gather_E(ctx));   // x-slabs: the replicated levels see the whole grid
   for (int l = 1; l < L; ++l) {
     MgLevel& m = ctx->mg[l];
     const long long nn = m.L.nodes(), ne = m.L.nel();
     if (l == 1 && !m.stored) {
-      LAUNCH(ctx, k_mg_diag_l1<T>, grid_for(nn), s.g, m.L, s.E, m.fixm, mgp<T>(m.invd));
+      LAUNCH(ctx, k_mg_diag_l1<T>, grid_for(nn), mgG(ctx), m.L, mgE(ctx), m.fixm, mgp<T>(m.invd));
       continue;
     }
     if (l == 1) {
-      k_mg_asm_fine<2><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(s.g, m.L, s.E, ctx->mg_tab8, m.K);
+      k_mg_asm_fine<2><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), ctx->mg_tab8, m.K);
       ctx->launches++;
     } else if (l == 2 && !ctx->mg[1].stored) {
-      k_mg_asm_fine<4><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(s.g, m.L, s.E, ctx->mg_tab64, m.K);
+      k_mg_asm_fine<4><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), ctx->mg_tab64, m.K);
       ctx->launches++;
     } else {
       const MgLevel& f = ctx->mg[l - 1];
@@ -1030,28 +1089,46 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   const int nsteps = warm ? kMgPowerStepsWarm : kMgPowerSteps;
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0) {
-      const LvGeo F = lv0(ctx);
-      const int gF = grid_for(F.nodes());
       // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
-      // masked products K v ping-pong between q and w
-      if (warm) CU(cudaMemcpyAsync(s.z, ctx->mg_pw0, sizeof(double) * 3 * s.g.ncomp, cudaMemcpyDeviceToDevice,
-                                   ctx->stream));
-      else LAUNCH(ctx, k_mg_start_vec<double>, gF, F, s.fixm, s.z);
-      CK((launch_mv<0, false, 3>(ctx, s, 0, s.m_z, nullptr, nullptr, s.q, 0, one)));
+      // masked products K v ping-pong between q and w (x-slabs: per slab, ghost
+      // planes exchanged after every product, Rayleigh sums allreduced)
+      const int W = ctx->world;
+      for (Slab& sl : ctx->slabs) {
+        if (warm) {
+          CU(cudaMemcpyAsync(sl.z, sl.pw0, sizeof(double) * 3 * sl.g.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
+        } else {   // owned + ghost planes (global hash: the same vector as one slab)
+          const int xa = std::max(0, sl.g.ex0 - 1), xb = std::min(sl.g.nelx, sl.g.ex0 + sl.g.nown);
+          LAUNCH(ctx, k_mg_start_vec<double>, grid_for((long long)(xb - xa + 1) * sl.g.NY * sl.g.NZ), lv_slab(sl),
+                 sl.g.ex0, xa, xb, sl.g.nelx, sl.fixm, sl.z);
+        }
+      }
+      for (Slab& sl : ctx->slabs) CK((launch_mv<0, false, 3>(ctx, sl, 0, sl.m_z, nullptr, nullptr, sl.q, 0, one)));
+      CK(exchange_nodes(ctx, &Slab::q));
       for (int k = 1; k <= nsteps; ++k) {
         const bool odd = k & 1;
-        CK((launch_mv<3, false, 3>(ctx, s, 0, odd ? s.m_q : s.m_w, nullptr, s.z, odd ? s.w : s.q, 0, one)));
+        for (Slab& sl : ctx->slabs)
+          CK((launch_mv<3, false, 3>(ctx, sl, 0, odd ? sl.m_q : sl.m_w, nullptr, sl.z, odd ? sl.w : sl.q, 0, one)));
+        CK(exchange_nodes(ctx, odd ? &Slab::w : &Slab::q));
       }
-      double* tlast = (nsteps & 1) ? s.w : s.q;
-      LAUNCH(ctx, (k_mg_rayleigh<true, double>), gF, F, s.z, tlast, s.invd, s.fixm, ctx->prm.mg_omega, ctx->mg_om,
-             s.partials, s.counter);
-      LAUNCH(ctx, k_mg_scale_copy<double>, grid_for(3 * s.g.ncomp), s.z, ctx->mg_pw0, 3 * s.g.ncomp,
-             ctx->mg_om + kMgScaleOff);
+      for (Slab& sl : ctx->slabs) {
+        const LvGeo F = lv_slab(sl);
+        double* tlast = (nsteps & 1) ? sl.w : sl.q;
+        LAUNCH(ctx, (k_mg_rayleigh<true, double>), grid_for(F.nodes()), F, sl.z, tlast, sl.invd, sl.fixm,
+               ctx->prm.mg_omega, ctx->mg_om, sl.partials, sl.counter, W > 1 ? sl.st : nullptr);
+      }
+      if (W > 1) {
+        CK(allreduce(ctx, 0, 2, 0));
+        k_mg_rayleigh_finish<<<1, 1, 0, ctx->stream>>>(s.st, ctx->prm.mg_omega, ctx->mg_om);
+        ctx->launches++;
+      }
+      for (Slab& sl : ctx->slabs)
+        LAUNCH(ctx, k_mg_scale_copy<double>, grid_for(3 * sl.g.ncomp), sl.z, sl.pw0, 3 * sl.g.ncomp,
+               ctx->mg_om + kMgScaleOff);
     } else {
       MgLevel& m = ctx->mg[l];
       const int gL = grid_for(m.L.nodes());
       if (warm) CU(cudaMemcpyAsync(m.x, m.pw, sizeof(T) * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
-      else LAUNCH(ctx, k_mg_start_vec<T>, gL, m.L, m.fixm, mgp<T>(m.x));
+      else LAUNCH(ctx, k_mg_start_vec<T>, gL, m.L, 0, 0, m.L.nx, m.L.nx, m.fixm, mgp<T>(m.x));
       for (int k = 0; k < nsteps; ++k) {
         if (!m.stored) {   // level 1: x <- D^-1 (A x) in the gather phase
           CK(launch_l1_elem<T>(ctx, m, nullptr));
@@ -1215,7 +1292,9 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[0], ctx->stream, cudaEventRecordExternal));
     // (nu = 1: z is not stored -- k_mg_prolong0 recomputes it with the correction)
     // (with mg_fp32 the smoothing matvecs compute the element operator in fp32)
-    if (nu == 1) CK((launch_mv<3, false, 2, T>(ctx, s, gate, s.m_r, nullptr, nullptr, s.q, 0, om)));
+    // (x-slabs: every step below runs per slab; nu = 1 only, see mg_build)
+    if (nu == 1)
+      for (Slab& sl : ctx->slabs) CK((launch_mv<3, false, 2, T>(ctx, sl, gate, sl.m_r, nullptr, nullptr, sl.q, 0, om)));
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
@@ -1224,32 +1303,45 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
       if (k < nu - 1) CK(mg_mv0(ctx, gate, s.m_z));
       else CK((launch_mv<0, false, 2>(ctx, s, gate, s.m_z, nullptr, nullptr, s.q, 0, om)));
     }
-    {   // x-marching restriction of the masked residual (k_mg_restrict0)
+    // x-marching restriction of the masked residual (k_mg_restrict0); x-slabs:
+    // each slab restricts its owned fine planes and the partial level-1 vectors
+    // are summed (slab order in loopback mode, an allreduce with NCCL)
+    const bool slabs = ctx->world > 1;
+    if (slabs) CU(cudaMemsetAsync(n1.b, 0, sizeof(T) * 3 * n1.L.ncomp, ctx->stream));
+    for (Slab& sl : ctx->slabs) {
+      const int xa = sl.g.ex0, xb = sl.g.ex0 + sl.g.nown;          // owned fine planes [xa, xb)
+      const int j0 = xa / 2, jend = std::min(n1.L.nx, xb / 2) + 1;   // coarse planes they reach
       const long long cols = (long long)(n1.L.ny + 1) * (n1.L.nz + 1);
       const int bx = (int)((cols + 127) / 128);
-      int chunks = (int)std::max<long long>(1, std::min<long long>(n1.L.nx + 1, (148LL * 64 + bx - 1) / bx));
-      const int cx = (n1.L.nx + 1 + chunks - 1) / chunks;
-      chunks = (n1.L.nx + 1 + cx - 1) / cx;
+      int chunks = (int)std::max<long long>(1, std::min<long long>(jend - j0, (148LL * 64 + bx - 1) / bx));
+      const int cx = (jend - j0 + chunks - 1) / chunks;
+      chunks = (jend - j0 + cx - 1) / cx;
+      const LvGeo Fs = lv_slab(sl);
       if (ctx->mg_f32)   // the pre-smoothing residual epilogue (kEpi = 2) wrote it in fp32
-        k_mg_restrict0<float, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.res32, n1.fixm,
-                                                                            mgp<T>(n1.b), gst);
+        k_mg_restrict0<float, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
+            Fs, n1.L, cx, sl.res32, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend, slabs ? 1 : 0);
       else
-        k_mg_restrict0<double, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.q, n1.fixm,
-                                                                             mgp<T>(n1.b), gst);
+        k_mg_restrict0<double, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
+            Fs, n1.L, cx, sl.q, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend, slabs ? 1 : 0);
       ctx->launches++;
       debug_sync(ctx, "k_mg_restrict0");
     }
+    CK(mg_allreduce_level(ctx, n1.b, 3 * n1.L.ncomp, sizeof(T) == 4));
     CK(enqueue_vcycle_t<T>(ctx, 1, gate, false));
     if (nu == 1) {   // z = w D^-1 r (the first sweep, recomputed) + P x1, x-marching
-      const long long cols = (long long)(F.ny + 1) * (F.nz + 1);
-      const int bx = (int)((cols + 127) / 128);
-      int chunks = (int)std::max<long long>(1, std::min<long long>((F.nx + 2) / 2, (148LL * 64 + bx - 1) / bx));
-      const int cx = ((F.nx + 1 + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
-      chunks = (F.nx + 1 + cx - 1) / cx;
-      k_mg_prolong0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(F, n1.L, cx, s.r, s.invd, om, mgp<T>(n1.x), s.fixm,
-                                                                  s.z, gst);
-      ctx->launches++;
-      debug_sync(ctx, "k_mg_prolong0");
+      for (Slab& sl : ctx->slabs) {   // owned + ghost planes (the post-smoothing matvec reads the ghosts)
+        const int pa = std::max(0, sl.g.ex0 - 1), pb = std::min(sl.g.nelx, sl.g.ex0 + sl.g.nown) + 1;
+        const int np = pb - (pa & ~1);
+        const long long cols = (long long)(F.ny + 1) * (F.nz + 1);
+        const int bx = (int)((cols + 127) / 128);
+        int chunks = (int)std::max<long long>(1, std::min<long long>((np + 1) / 2, (148LL * 64 + bx - 1) / bx));
+        const int cx = ((np + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
+        chunks = (np + cx - 1) / cx;
+        k_mg_prolong0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
+                                                                    mgp<T>(n1.x), sl.fixm, sl.z, gst, sl.g.ex0, pa, pb);
+        ctx->launches++;
+        debug_sync(ctx, "k_mg_prolong0");
+      }
     } else
       LAUNCH(ctx, (k_mg_prolong<true, T, double>), gF, F, n1.L, mgp<T>(n1.x), s.fixm, s.z, gst);
     for (int k = 1; k < nu; ++k) {
@@ -1259,9 +1351,17 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     }
     // last sweep fused into the matvec epilogue: w = z + w D^-1 (r - K z) (the
     // V-cycle result lives in s.w), rho = r.w and beta for the PCG
+    // (x-slabs: rho allreduced, then beta per slab; w's ghost planes exchanged
+    // for the PCG matvec's p = w + beta p pre-pass)
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[2], ctx->stream, cudaEventRecordExternal));
-    CK((launch_mv<0, false, 1, T>(ctx, s, gate, s.m_z, nullptr, nullptr, s.w, 0, om)));
+    for (Slab& sl : ctx->slabs)
+      CK((launch_mv<0, false, 1, T>(ctx, sl, gate, sl.m_z, nullptr, nullptr, sl.w, slabs ? 0 : 1, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[3], ctx->stream, cudaEventRecordExternal));
+    if (slabs) {
+      CK(allreduce(ctx, 0, 1, 0));
+      for (Slab& sl : ctx->slabs) { k_finish_rho<<<1, 1, 0, ctx->stream>>>(sl.st); ctx->launches++; }
+      CK(exchange_nodes(ctx, &Slab::w));
+    }
     return check_launch(ctx);
   }
   MgLevel& m = ctx->mg[l];
@@ -1290,23 +1390,37 @@ int enqueue_vcycle(topo_ctx* ctx, int l, int gate, bool dot) {
 
 // one MG-PCG iteration: z = V(r) (rho, beta) ; p = z + beta p ; q = K p ; alpha ; u, r update
 int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
-  Slab& s = ctx->slabs[0];
   ctx->prof_capture = prof_here;
   const int rcv = enqueue_vcycle(ctx, 0, 1, true);
   ctx->prof_capture = false;
   CK(rcv);
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
-  const CUtensorMap* pold = parity ? &s.m_p1 : &s.m_p0;
-  double* pnew = parity ? s.p0 : s.p1;
-  double* pprev = parity ? s.p1 : s.p0;
-  CK((launch_mv<2, true>(ctx, s, 1, s.m_w, pold, pnew, s.q, 1)));   // p = V(r) + beta p, V(r) in s.w
+  const int fin = ctx->world == 1 ? 1 : 0;
+  for (Slab& sl : ctx->slabs) {   // p = V(r) + beta p, V(r) in w
+    const CUtensorMap* pold = parity ? &sl.m_p1 : &sl.m_p0;
+    double* pnew = parity ? sl.p0 : sl.p1;
+    CK((launch_mv<2, true>(ctx, sl, 1, sl.m_w, pold, pnew, sl.q, fin)));
+  }
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
-  if (parity)
-    LAUNCH(ctx, (k_update<true, true>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
-           pnew, s.q, s.invd, s.fixm, s.partials, s.counter, 1);
-  else
-    LAUNCH(ctx, (k_update<false, true>), grid_for((long long)s.g.nown * s.g.nplane / 2), s.g, s.st, s.u, s.r, pprev,
-           pnew, s.q, s.invd, s.fixm, s.partials, s.counter, 1);
+  if (!fin) {
+    CK(allreduce(ctx, 0, 1, 0));
+    for (Slab& sl : ctx->slabs) { k_finish_alpha<<<1, 1, 0, ctx->stream>>>(sl.st); ctx->launches++; }
+  }
+  for (Slab& sl : ctx->slabs) {
+    double* pnew = parity ? sl.p0 : sl.p1;
+    double* pprev = parity ? sl.p1 : sl.p0;
+    if (parity)
+      LAUNCH(ctx, (k_update<true, true>), grid_for((long long)sl.g.nown * sl.g.nplane / 2), sl.g, sl.st, sl.u, sl.r,
+             pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials, sl.counter, fin);
+    else
+      LAUNCH(ctx, (k_update<false, true>), grid_for((long long)sl.g.nown * sl.g.nplane / 2), sl.g, sl.st, sl.u, sl.r,
+             pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials, sl.counter, fin);
+  }
+  if (!fin) {
+    CK(allreduce(ctx, 0, 2, 0));
+    for (Slab& sl : ctx->slabs) { k_finish_update<true><<<1, 1, 0, ctx->stream>>>(sl.st, parity ? 0 : 1); ctx->launches++; }
+    CK(exchange_nodes(ctx, &Slab::r));
+  }
   return check_launch(ctx);
 }
 
@@ -1679,7 +1793,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad, s.res32,
+                    s.vpad, s.res32, s.pw0, s.pw0_b,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
@@ -1699,8 +1813,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->mg_setup_exec) cudaGraphExecDestroy(ctx->mg_setup_exec);
   if (ctx->mg_setup_exec_w) cudaGraphExecDestroy(ctx->mg_setup_exec_w);
   if (ctx->cublas) g_cublas.Destroy(ctx->cublas);
-  if (ctx->mg_pw0) cudaFree(ctx->mg_pw0);
-  if (ctx->mg_pw0_b) cudaFree(ctx->mg_pw0_b);
+  if (ctx->mg_gE) cudaFree(ctx->mg_gE);
   for (cudaGraphExec_t g : ctx->cg_exec)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
@@ -1941,9 +2054,10 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   std::vector<double> locd;
   for (Slab& s : ctx->slabs) {
     const Geo& g = s.g;
-    // fixed-DOF bit mask on the owned node planes
+    // fixed-DOF bit mask on the owned node planes and the ghost planes (the
+    // multigrid prolongation writes z on the ghost planes too)
     loc8.assign(g.ncomp, 0);
-    for (int ix = g.ex0; ix < g.ex0 + g.nown; ++ix)
+    for (int ix = std::max(0, g.ex0 - 1); ix <= std::min(nelx, g.ex0 + g.nown); ++ix)
       for (int iz = 0; iz <= nelz; ++iz)
         for (int iy = 0; iy <= nely; ++iy) {
           const long long n = (long long)iz * (nelx + 1) * (nely + 1) + (long long)ix * (nely + 1) + iy;
@@ -2229,9 +2343,11 @@ int topo_snapshot(topo_ctx* ctx) {
   }
   if (ctx->mg_on) {   // the multigrid power vectors (warm-started smoother weights)
     const size_t rs = sizeof(double);
-    const size_t nb0 = sizeof(double) * 3 * ctx->slabs[0].g.ncomp;
-    if (!ctx->mg_pw0_b) CU(cudaMalloc(&ctx->mg_pw0_b, nb0));
-    CU(cudaMemcpyAsync(ctx->mg_pw0_b, ctx->mg_pw0, nb0, cudaMemcpyDeviceToDevice, ctx->stream));
+    for (Slab& s : ctx->slabs) {
+      const size_t nb0 = sizeof(double) * 3 * s.g.ncomp;
+      if (!s.pw0_b) CU(cudaMalloc(&s.pw0_b, nb0));
+      CU(cudaMemcpyAsync(s.pw0_b, s.pw0, nb0, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     for (MgLevel& m : ctx->mg) {
       if (!m.pw) continue;
       if (!m.pw_b) CU(cudaMalloc(&m.pw_b, rs * 3 * m.L.ncomp));
@@ -2256,10 +2372,10 @@ int topo_restore(topo_ctx* ctx) {
     CU(cudaMemcpyAsync(s.x, s.x_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
     CU(cudaMemcpyAsync(s.xphys, s.xphys_b, eb, cudaMemcpyDeviceToDevice, ctx->stream));
   }
-  if (ctx->mg_on && ctx->mg_pw0_b) {
+  if (ctx->mg_on && ctx->slabs[0].pw0_b) {
     const size_t rs = sizeof(double);
-    CU(cudaMemcpyAsync(ctx->mg_pw0, ctx->mg_pw0_b, sizeof(double) * 3 * ctx->slabs[0].g.ncomp,
-                       cudaMemcpyDeviceToDevice, ctx->stream));
+    for (Slab& s : ctx->slabs)
+      CU(cudaMemcpyAsync(s.pw0, s.pw0_b, sizeof(double) * 3 * s.g.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
     for (MgLevel& m : ctx->mg)
       if (m.pw && m.pw_b)
         CU(cudaMemcpyAsync(m.pw, m.pw_b, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -2382,6 +2498,7 @@ int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
   for (Slab& s : ctx->slabs)
     LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.r);
   CK(check_launch(ctx));
+  CK(exchange_nodes(ctx, &Slab::r));
   CK(enqueue_vcycle(ctx, 0, 0, false));
   return download_nodes(ctx, &Slab::w, z);   // the V-cycle result (last sweep fused into the matvec)
 }

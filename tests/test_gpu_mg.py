@@ -147,16 +147,24 @@ def test_mg_loop_parity_obstacle(topo):
 
 
 def test_mg_selection_rules(topo):
-    """AUTO picks MG on one slab, Jacobi on several slabs or when the grid is too
-    small; explicit MG where the hierarchy cannot be built is EINVAL."""
+    """AUTO picks MG on one slab and on x-slabs (nu = 1), Jacobi on x-slabs with
+    nu > 1 or when the grid is too small; explicit MG where the hierarchy cannot
+    be built is EINVAL."""
     p, f, fx, pas = make_problem(0)
+    lb = dict(mode=topo.TOPO_DIST_LOOPBACK, rank=0, world=2, device=0)
     with topo.Problem(p, f, fx, pas) as pr:
         assert len(pr.mg_levels()) == 2
-    with topo.Problem(p, f, fx, pas, dist=dict(mode=topo.TOPO_DIST_LOOPBACK, rank=0, world=2,
-                                               device=0)) as pr:
+    with topo.Problem(p, f, fx, pas, dist=lb) as pr:
+        assert len(pr.mg_levels()) == 2
+        _, info = pr.solve()
+        assert info["precond"] == "mg"
+    with topo.Problem(dict(p, mg_nu=2), f, fx, pas, dist=lb) as pr:
         assert pr.mg_levels() == []
         _, info = pr.solve()
         assert info["precond"] == "jacobi"
+    with pytest.raises(topo.TopoError) as e:
+        topo.Problem(dict(p, mg_nu=2, precond="mg"), f, fx, pas, dist=lb)
+    assert e.value.code == topo.TOPO_EINVAL
     tiny = config_params(dict(nelx=3, nely=2, nelz=2, volfrac=0.3, rmin=1.5, n_iter=1,
                               cg_rtol=1e-10, obstacle=None))
     ft, fxt = cantilever_load(3, 2, 2), cantilever_fixed(3, 2, 2)
@@ -205,3 +213,35 @@ def test_mg_paper_protocol_200_iterations(topo):
         t = pr.timings()
     assert t["mg_fallbacks"] == 0 and t["mg_promotions"] == 0
     assert max(ncg) <= 40, ncg
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+@pytest.mark.parametrize("fp32", [0, 1])
+def test_mg_loopback_slabs_match_single(topo, W, fp32):
+    """Multigrid on W x-slabs (in-process halo copies on one GPU; the coarse
+    levels replicated, the level-1 restriction summed over slabs): the smoother
+    weights, one V-cycle, a solve and a 5-iteration optimisation equal the single
+    slab up to rounding (slab-boundary partial sums), and the oracle."""
+    dims, obst = (37, 13, 5), (18.0, 6.0, 3.0)
+    p, f, fx, pas, x, K = _case(dims, obst, seed=4, mg_fp32=fp32)
+    b = np.where(fx == 0, random_vector(K.shape[0], seed=7), 0.0)
+    outs = []
+    for mode, world in ((topo.TOPO_DIST_SINGLE, 1), (topo.TOPO_DIST_LOOPBACK, W)):
+        with topo.Problem(p, f, fx, pas, dist=dict(mode=mode, rank=0, world=world, device=0)) as pr:
+            pr.set_xphys(x)
+            z = pr.mg_vcycle(b)
+            u, info = pr.solve()
+            assert info["precond"] == "mg"
+            pr.set_density(None)
+            c, _, _ = pr.optimize(5)
+            t = pr.timings()
+            assert t["mg_fallbacks"] == 0 and t["mg_promotions"] == 0
+            outs.append((z, u, info["iters"], c))
+    (z1, u1, it1, c1), (zW, uW, itW, cW) = outs
+    assert_rel(zW, z1, 1e-5 if fp32 else 1e-11, f"V-cycle W={W}")
+    assert abs(itW - it1) <= 1
+    assert oracle.true_residual(K, uW, f, fx) <= 1e-10
+    assert_rel(uW, u1, 1e-7, f"u W={W}")
+    assert_rel(cW, c1, 1e-9, f"c history W={W}")
+    ro = oracle.run_optimization(p, f, fx, pas, n_iter=5)
+    assert_rel(cW, ro["c"], 1e-6, "c history vs oracle")
