@@ -9,11 +9,11 @@ sensitivities, filter, OC) of BASELINE config --config (default 4: the
 512x256x256 cantilever, 101.6 M DOF, fp64) with all inputs resident in HBM.
 Steps continue the optimisation (x evolves), so W warm-up + K timed steps of
 config 4 are its 5 BASELINE iterations.  The solve is PCG in fp64 to rtol 1e-8
-with the library's default preconditioner: geometric multigrid on one GPU
-(coarse levels in fp32 = f3); --precond jacobi times the
-north_star's Jacobi-PCG instead.  N > 1: launched by torchrun, one rank per
-GPU, x-slab decomposition with NCCL (strong scaling; Jacobi-PCG, the path that
-shards).  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for
+with the library's default preconditioner: geometric multigrid (SURVEY §8(f)
+f2, coarse levels in fp32 = f3); --precond jacobi times the north_star's
+Jacobi-PCG instead.  N > 1: launched by torchrun, one rank per GPU, x-slab
+decomposition with NCCL (strong scaling): the fine level is slab-local with
+halo exchanges, the coarse multigrid levels are replicated on every rank.  Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement" for
 every number's definition.
 """
 import argparse
@@ -231,7 +231,7 @@ def main():
     ap.add_argument("--ref-ncg", type=int, default=None)
     ap.add_argument("--ref-slab", type=int, default=8)
     ap.add_argument("--precond", default="auto", choices=["auto", "mg", "jacobi"],
-                    help="PCG preconditioner (auto: geometric multigrid on one GPU, Jacobi on x-slabs)")
+                    help="PCG preconditioner (auto: geometric multigrid where the hierarchy can be built)")
     ap.add_argument("--mg-coarse-max", type=int, default=0, help="coarsest MG level DOF bound (0 = library auto)")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")

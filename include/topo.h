@@ -111,9 +111,11 @@ typedef struct {
    * TOPO_PRECOND_JACOBI: z = D^-1 r with the on-the-fly diagonal.
    * TOPO_PRECOND_MG: one V-cycle of geometric multigrid on the nested Hex8 grids
    *   (trilinear transfer, Galerkin coarse operators, damped-Jacobi smoothing,
-   *   exact coarsest solve).  Single slab only (world == 1); EINVAL at init if
-   *   the hierarchy cannot be built (fewer than 2 levels, or coarse Dirichlet
-   *   DOFs that do not cover the fine ones: property Q of reading M4).
+   *   exact coarsest solve).  On x-slabs (world > 1) the fine level is
+   *   slab-local and levels >= 1 are replicated on every rank (mg_nu == 1
+   *   only).  EINVAL at init if the hierarchy cannot be built (fewer than 2
+   *   levels, coarse Dirichlet DOFs that do not cover the fine ones: property Q
+   *   of reading M4; or x-slabs with mg_nu > 1).
    * TOPO_PRECOND_AUTO (default): MG where it can be built, else Jacobi.         */
   int32_t precond;
   int32_t mg_nu;              /* damped-Jacobi sweeps before and after the coarse correction (>= 1) */
