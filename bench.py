@@ -235,7 +235,7 @@ def main():
     ap.add_argument("--mg-coarse-max", type=int, default=0, help="coarsest MG level DOF bound (0 = library auto)")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")
-    ap.add_argument("--mg-omega", type=float, default=1.4, help="MG smoother theta (w_l = theta / lam_l)")
+    ap.add_argument("--mg-omega", type=float, default=None, help="MG smoother theta (default: the library's)")
     args = ap.parse_args()
 
     from workloads import make_problem
@@ -243,7 +243,8 @@ def main():
         args.e2e_steps = args.steps
     world, rank, local = dist_env()
     p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max,
-                                 mg_nu=args.mg_nu, mg_omega=args.mg_omega)
+                                 mg_nu=args.mg_nu,
+                                 **({} if args.mg_omega is None else {"mg_omega": args.mg_omega}))
 
     if args.impl == "reference":
         run_reference(args, p, world, rank)

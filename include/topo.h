@@ -120,8 +120,10 @@ typedef struct {
   int32_t precond;
   int32_t mg_nu;              /* damped-Jacobi sweeps before and after the coarse correction (>= 1) */
   double  mg_omega;           /* theta in (0, 2): level-l Jacobi weight w_l = theta / lam_l, lam_l the
-                                 Rayleigh quotient of D^-1 A_l after 8 power steps (default 1.4: the
-                                 8-step estimate is 0.80-0.95 of lam_max, so w lam_max <= 1.75)   */
+                                 Rayleigh quotient of D^-1 A_l after 8 power steps (default 1.6:
+                                 5-7 % fewer iterations than 1.4 on every BASELINE config; a
+                                 breakdown lowers theta by 0.2, down to 1.2, for the rest of the
+                                 run -- reading M7)                                               */
   int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (24..8192;
                                  0 = auto: min(5000, max(1000, n_dof / 2000)))                     */
   int32_t mg_fp32;            /* 1 (default): multigrid levels >= 1 (vectors, stencils, level-1 Galerkin
@@ -165,6 +167,8 @@ typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulativ
                                  the Jacobi preconditioner (cumulative)                        */
   int32_t mg_promotions;      /* 1 once an fp32 hierarchy (mg_fp32) broke down and was promoted to
                                  fp64 for the rest of the run (that solve is redone)           */
+  int32_t mg_theta_cuts;      /* breakdowns answered by lowering the smoother theta by 0.2 (down
+                                 to 1.2) for the rest of the run (that solve is redone)        */
 } topo_timings;
 
 /* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,

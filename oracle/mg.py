@@ -179,7 +179,16 @@ def lambda_estimate(lv, k=8):
     return float((v @ (A @ v)) / (v @ (d * v)))
 
 
-def smoother_weights(levels, theta=1.4, k=8):
+def jacobi_bound(KE):
+    """lam_bar = lam_max(KE) / KE_ii >= lam_max(D^-1 K) for every modulus field
+    E > 0 and every Dirichlet set (reading M5): x^T K x = sum_e E_e x_e^T KE x_e
+    <= lam_max(KE) sum_e E_e |x_e|^2 = (lam_max(KE) / KE_ii) x^T D x, because
+    KE's diagonal is constant (App. A)."""
+    KE = np.asarray(KE)
+    return float(np.linalg.eigvalsh(KE).max() / KE[0, 0])
+
+
+def smoother_weights(levels, theta=1.6, k=8):
     """w_l = theta / lam_l on every level but the coarsest (M5)."""
     for lv in levels[:-1]:
         lv["lam"] = lambda_estimate(lv, k)
@@ -220,7 +229,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
     return x
 
 
-def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.4, nu=1, coarse_max=1000,
+def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
                max_iter=10000, u0=None, power_steps=8):
     """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
     TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""

@@ -367,8 +367,8 @@ constexpr int kMgScaleOff = 17;   // mg_om layout: [0,16) weights, [16] = 1.0, [
 template <bool kNodeD, typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T* __restrict__ invd,
-              const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out, double* partials,
-              unsigned int* counter, DevState* st = nullptr) {
+              const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out,
+              double* partials, unsigned int* counter, DevState* st = nullptr) {
   const long long tot = L.nodes();
   double vt = 0.0, vdv = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;

@@ -213,6 +213,7 @@ struct topo_ctx {
   bool mg_on = false, mg_ready = false;
   bool mg_f32 = false;               // levels >= 1 in fp32 (topo_params.mg_fp32)
   bool mg_f32_b = false;             // ... in the snapshot
+  double mg_theta = 1.6, mg_theta_b = 1.6;   // smoother theta in use (cut after a breakdown) (+ snapshot)
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
@@ -923,6 +924,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   if (L > 16) return set_err(ctx, TOPO_EINVAL, "multigrid: more than 16 levels");
   ctx->mg_on = true;
   ctx->mg_f32 = P.mg_fp32 != 0;
+  ctx->mg_theta = P.mg_omega;
   ctx->mg.resize(L);
   auto al = [&](void** p, size_t bytes) -> int {
     CU(cudaMalloc(p, bytes));
@@ -1114,11 +1116,11 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
         const LvGeo F = lv_slab(sl);
         double* tlast = (nsteps & 1) ? sl.w : sl.q;
         LAUNCH(ctx, (k_mg_rayleigh<true, double>), grid_for(F.nodes()), F, sl.z, tlast, sl.invd, sl.fixm,
-               ctx->prm.mg_omega, ctx->mg_om, sl.partials, sl.counter, W > 1 ? sl.st : nullptr);
+               ctx->mg_theta, ctx->mg_om, sl.partials, sl.counter, W > 1 ? sl.st : nullptr);
       }
       if (W > 1) {
         CK(allreduce(ctx, 0, 2, 0));
-        k_mg_rayleigh_finish<<<1, 1, 0, ctx->stream>>>(s.st, ctx->prm.mg_omega, ctx->mg_om);
+        k_mg_rayleigh_finish<<<1, 1, 0, ctx->stream>>>(s.st, ctx->mg_theta, ctx->mg_om);
         ctx->launches++;
       }
       for (Slab& sl : ctx->slabs)
@@ -1141,7 +1143,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       }
       CK(mg_apply<T>(ctx, l, 0));
       LAUNCH(ctx, (k_mg_rayleigh<false, T>), gL, m.L, mgp<T>(m.x), mgp<T>(m.t), mgp<T>(m.invd), m.fixm,
-             ctx->prm.mg_omega, ctx->mg_om + l, s.partials, s.counter);
+             ctx->mg_theta, ctx->mg_om + l, s.partials, s.counter);
       LAUNCH(ctx, k_mg_scale_copy<T>, grid_for(3 * m.L.ncomp), mgp<T>(m.x), mgp<T>(m.pw), 3 * m.L.ncomp,
              ctx->mg_om + kMgScaleOff + l);
     }
@@ -1541,9 +1543,21 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   long long iters = 0;
   int rc = solve_pass(ctx, mg, &replacements, &rr_true);
   iters = ctx->hstate->it;
+  while (rc == TOPO_EBREAKDOWN && mg && ctx->mg_theta > 1.2 + 1e-12) {
+    // an indefinite V-cycle: first suspect the smoother weights (a Rayleigh
+    // estimate well below lam_max on a coarse level) -- lower theta by 0.2 for
+    // the rest of the run and redo the solve
+    ctx->tim.mg_theta_cuts++;
+    ctx->mg_theta = std::max(1.2, ctx->mg_theta - 0.2);
+    mg_invalidate(ctx);
+    for (Slab& s : ctx->slabs) CU(cudaMemsetAsync(s.u, 0, sizeof(double) * 3 * s.g.ncomp, ctx->stream));
+    CK(mg_setup(ctx));
+    rc = solve_pass(ctx, 1, &replacements, &rr_true);
+    iters += ctx->hstate->it;
+  }
   if (rc == TOPO_EBREAKDOWN && mg && ctx->mg_f32) {
-    // the fp32 hierarchy lost positive definiteness (high-contrast designs late in
-    // an optimisation): promote it to fp64 for the rest of the run and redo the solve
+    // then the precision: promote the fp32 hierarchy to fp64 for the rest of the
+    // run and redo the solve
     ctx->tim.mg_promotions++;
     ctx->mg_f32 = false;
     mg_invalidate(ctx);
@@ -1882,7 +1896,7 @@ void topo_params_default(topo_params* p) {
   p->cg_check_every = 0;
   p->precond = TOPO_PRECOND_AUTO;
   p->mg_nu = 1;
-  p->mg_omega = 1.4;
+  p->mg_omega = 1.6;
   p->mg_coarse_max = 0;
   p->mg_fp32 = 1;
 }
@@ -2355,6 +2369,7 @@ int topo_snapshot(topo_ctx* ctx) {
     }
     ctx->mg_warm_b = ctx->mg_warm;
     ctx->mg_f32_b = ctx->mg_f32;
+    ctx->mg_theta_b = ctx->mg_theta;
   }
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->snap_has_u = ctx->has_u;
@@ -2380,6 +2395,10 @@ int topo_restore(topo_ctx* ctx) {
       if (m.pw && m.pw_b)
         CU(cudaMemcpyAsync(m.pw, m.pw_b, rs * 3 * m.L.ncomp, cudaMemcpyDeviceToDevice, ctx->stream));
     ctx->mg_warm = ctx->mg_warm_b;
+    if (ctx->mg_theta != ctx->mg_theta_b) {
+      ctx->mg_theta = ctx->mg_theta_b;
+      mg_invalidate(ctx);
+    }
     if (ctx->mg_f32 != ctx->mg_f32_b) {   // precision state of the snapshot (promotion undone)
       ctx->mg_f32 = ctx->mg_f32_b;
       mg_invalidate(ctx);

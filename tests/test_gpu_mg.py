@@ -103,7 +103,7 @@ def test_mg_vcycle_parity(topo, dims, obst, nu, fp32):
 def test_mg_solve_parity(topo, dims, obst, nu, fp32):
     p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu)
     uo = oracle.solve_direct(K, f, fx)
-    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.4, nu=nu)
+    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=nu)
     its = {}
     for pc in ("jacobi", "mg"):
         with topo.Problem(dict(p, precond=pc), f, fx, pas) as pr:
@@ -245,3 +245,19 @@ def test_mg_loopback_slabs_match_single(topo, W, fp32):
     assert_rel(cW, c1, 1e-9, f"c history W={W}")
     ro = oracle.run_optimization(p, f, fx, pas, n_iter=5)
     assert_rel(cW, ro["c"], 1e-6, "c history vs oracle")
+
+
+@pytest.mark.gpu
+def test_mg_theta_cut_recovers(topo):
+    """An over-aggressive smoother theta (1.99: coarse-level weights beyond the
+    convergent range) makes the V-cycle indefinite; the solve lowers theta
+    (mg_theta_cuts) and still converges with multigrid, not Jacobi."""
+    p, f, fx, pas, x, K = _case((60, 20, 4), None, seed=9, mg_omega=1.99)
+    with topo.Problem(p, f, fx, pas) as pr:
+        pr.set_xphys(x)
+        u, info = pr.solve()
+        t = pr.timings()
+    assert oracle.true_residual(K, u, f, fx) <= 1e-10
+    assert t["mg_fallbacks"] == 0
+    assert info["precond"] == "mg"
+    print("theta cuts", t["mg_theta_cuts"], "promotions", t["mg_promotions"], "iters", info["iters"])

@@ -186,7 +186,7 @@ def test_start_vector_is_splitmix64():
 def test_lambda_estimate_bounds(seed):
     """Rayleigh quotient <= lam_max(D^-1 A) <= element bound lam_max(KE)/KE_ii
     (x^T A x = sum_e x_e^T E_e KE x_e <= lam(KE)/kd x^T D x), and the damped
-    smoother it sets is convergent: w lam_max < 2 for theta = 1.4."""
+    smoother it sets is convergent: w lam_max < 2 for the default theta (1.6)."""
     import scipy.sparse as sps
     import scipy.sparse.linalg as spla
     from workloads import random_density
@@ -195,8 +195,8 @@ def test_lambda_estimate_bounds(seed):
     KE = oracle.element_stiffness(0.3)
     E = 1e-9 + random_density(int(np.prod(dims)), seed=seed) ** 3
     K = oracle.assemble(*dims, KE, E)
+    bound = mg.jacobi_bound(KE)
     lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=200))
-    bound = np.linalg.eigvalsh(KE).max() / KE[0, 0]
     for l in lv[:-1]:
         A, d, _ = mg.level_operator(l)
         Dm = sps.diags(1.0 / np.sqrt(d))
@@ -206,3 +206,13 @@ def test_lambda_estimate_bounds(seed):
     A0, d0, _ = mg.level_operator(lv[0])
     Dm = sps.diags(1.0 / np.sqrt(d0))
     assert spla.eigsh(Dm @ A0 @ Dm, k=1, which="LA", return_eigenvectors=False)[0] <= bound + 1e-12
+
+
+def test_jacobi_bound_closed_form():
+    """lam_bar = lam_max(KE) / KE_ii at nu = 0.3: KE's largest eigenvalue 1.25
+    (SURVEY §8(c) spectrum pin) over KE_ii = (lam + 4 mu) / 9 = 0.2350427350
+    (closed form) = 5.3181818..."""
+    KE = oracle.element_stiffness(0.3)
+    lam, mu = 0.3 / (1.3 * 0.4), 1.0 / 2.6
+    assert abs(mg.jacobi_bound(KE) - 1.25 / ((lam + 4 * mu) / 9)) <= 1e-6 * 5.3
+    assert abs((lam + 4 * mu) / 9 - 0.2350427350) <= 1e-10

@@ -22,11 +22,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--oracle-iters", type=int, default=0)
+    ap.add_argument("--set", nargs="*", default=[], help="parameter overrides key=value")
     args = ap.parse_args()
+    over = {k: (int(v) if v.lstrip("-").isdigit() else float(v) if "." in v else v)
+            for k, v in (a.split("=") for a in args.set)}
     import torch
     from workloads import make_problem
     from paper_2504_05604_b200 import topo
-    p, f, fx, pas = make_problem("paper")
+    p, f, fx, pas = make_problem("paper", **over)
     ph = dict(assembly=0.0, solve=0.0, filter=0.0, update=0.0)
     ncg, c = [], []
     with topo.Problem(p, f, fx, pas) as pr:
