@@ -126,6 +126,11 @@ typedef struct {
                                  run -- reading M7)                                               */
   int32_t mg_coarse_max;      /* coarsening stops at the first level with <= this many DOFs (24..8192;
                                  0 = auto: min(5000, max(1000, n_dof / 2000)))                     */
+  int32_t mg_nu_deep;         /* sweeps on the small coarse levels (<= 150 000 nodes, level >= 1):
+                                 0 (default) = auto: 8 when the fine grid has >= 2 M nodes (those
+                                 levels cost little next to the fine level, and solving the deep
+                                 coarse problem better cuts the PCG iterations by ~30 % at config
+                                 4), else mg_nu;  >= 1: that many on those levels (reading M5)      */
   int32_t mg_fp32;            /* 1 (default): multigrid levels >= 1 (vectors, stencils, level-1 Galerkin
                                  operator) and the fine smoothing matvecs' element operator in fp32 --
                                  mixed precision; the PCG, its matvec and every

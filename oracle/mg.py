@@ -196,11 +196,30 @@ def smoother_weights(levels, theta=1.6, k=8):
     return levels
 
 
+def level_sweeps(levels, nu=1, nu_deep=0, deep_nodes=150000):
+    """Sweeps per level (M5): nu on the fine level and on coarse levels with more
+    than deep_nodes nodes; nu_deep on the smaller coarse levels (0 = auto: 8 when
+    the fine grid has >= 2 000 000 nodes, else nu)."""
+    def nodes(d):
+        return (d[0] + 1) * (d[1] + 1) * (d[2] + 1)
+    fine = nodes(levels[0]["dims"])
+    out = []
+    for l, lv in enumerate(levels):
+        if l == 0 or nodes(lv["dims"]) > deep_nodes:
+            out.append(nu)
+        elif nu_deep > 0:
+            out.append(nu_deep)
+        else:
+            out.append(8 if fine >= 2000000 else nu)
+    return out
+
+
 def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
     """One V-cycle z = V(b) for a full-length level-_l vector b (0 on fixed DOFs).
     M5/M6; textbook recursion (Briggs, Henson, McCormick, "A Multigrid Tutorial",
     V-cycle scheme), written out without fusion.  omega None -> each level's
-    lv["omega"] (smoother_weights), else one fixed weight on every level."""
+    lv["omega"] (smoother_weights), else one fixed weight on every level.
+    nu: sweeps per side, one int for every level or a per-level sequence (M5)."""
     if _ops is None:
         _ops = [level_operator(lv) for lv in levels]
         for k, lv in enumerate(levels):
@@ -213,8 +232,9 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
     if _l == len(levels) - 1:
         xf = sla.cho_solve(lv["chol"], bf)
     else:
+        nl = nu[_l] if hasattr(nu, "__len__") else nu
         xf = np.zeros_like(bf)
-        for _ in range(nu):
+        for _ in range(nl):
             xf = xf + w * (bf - A @ xf) / d
         r = np.zeros_like(b)
         r[free] = bf - A @ xf
@@ -222,7 +242,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
         rc[levels[_l + 1]["fixed"] != 0] = 0.0
         ec = vcycle(levels, rc, omega, nu, _l + 1, _ops)
         xf = xf + (lv["P"] @ ec)[free]
-        for _ in range(nu):
+        for _ in range(nl):
             xf = xf + w * (bf - A @ xf) / d
     x = np.zeros_like(b)
     x[free] = xf
@@ -230,10 +250,11 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
 
 
 def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
-               max_iter=10000, u0=None, power_steps=8):
+               max_iter=10000, u0=None, power_steps=8, nu_deep=0):
     """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
     TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""
     levels = smoother_weights(hierarchy(K, fixed, dims, coarse_max=coarse_max), theta, power_steps)
+    nu = level_sweeps(levels, nu, nu_deep)
     ops = [level_operator(lv) for lv in levels]
     levels[-1]["chol"] = sla.cho_factor(ops[-1][0].toarray())
     A, _, free = ops[0]

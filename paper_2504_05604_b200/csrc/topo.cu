@@ -1270,13 +1270,24 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   return check_launch(ctx);
 }
 
+// smoothing sweeps on level l (reading M5): mg_nu, or mg_nu_deep on the small
+// coarse levels (auto: 8 when the fine grid is large enough that they are cheap)
+constexpr long long kMgDeepNodes = 150000;
+int mg_level_nu(const topo_ctx* ctx, int l) {
+  const topo_params& P = ctx->prm;
+  if (l == 0 || ctx->mg[l].L.nodes() > kMgDeepNodes) return P.mg_nu;
+  if (P.mg_nu_deep > 0) return P.mg_nu_deep;
+  const long long fine = (long long)(P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+  return fine >= 2000000 ? 8 : P.mg_nu;
+}
+
 // One V-cycle on level l (level 0: b = r; the result lands in s.w and the last
 // fine sweep also sets rho = r.V(r) and beta for the PCG; `dot` is unused).
 // T = precision of levels >= 1 (level 0 is always fp64).
 template <typename T>
 int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   Slab& s = ctx->slabs[0];
-  const int L = (int)ctx->mg.size(), nu = ctx->prm.mg_nu;
+  const int L = (int)ctx->mg.size(), nu = mg_level_nu(ctx, l);
   const DevState* gst = gate ? s.st : nullptr;
   const double* om = ctx->mg_om + l;
   if (l == L - 1) {
@@ -1863,6 +1874,7 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (p->mg_nu < 1 || p->mg_nu > 8) return set_err(ctx, TOPO_EINVAL, "mg_nu must be in [1, 8]");
   if (!(p->mg_omega > 0 && p->mg_omega < 2)) return set_err(ctx, TOPO_EINVAL, "mg_omega must be in (0, 2)");
   if (p->mg_fp32 != 0 && p->mg_fp32 != 1) return set_err(ctx, TOPO_EINVAL, "mg_fp32 must be 0 or 1");
+  if (p->mg_nu_deep < 0 || p->mg_nu_deep > 64) return set_err(ctx, TOPO_EINVAL, "mg_nu_deep must be in [0, 64]");
   if (p->mg_coarse_max != 0 && (p->mg_coarse_max < 24 || p->mg_coarse_max > 8192))
     return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be 0 (auto) or in [24, 8192]");
   return TOPO_OK;
@@ -1899,6 +1911,7 @@ void topo_params_default(topo_params* p) {
   p->mg_omega = 1.6;
   p->mg_coarse_max = 0;
   p->mg_fp32 = 1;
+  p->mg_nu_deep = 0;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }

@@ -85,25 +85,25 @@ def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst, fp32):
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu,fp32", [(1, 0), (2, 0), (1, 1), (2, 1)])
-def test_mg_vcycle_parity(topo, dims, obst, nu, fp32):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32)
+@pytest.mark.parametrize("nu,fp32,deep", [(1, 0, 0), (2, 0, 0), (1, 1, 0), (2, 1, 0), (1, 0, 4), (1, 1, 6)])
+def test_mg_vcycle_parity(topo, dims, obst, nu, fp32, deep):
+    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32, mg_nu_deep=deep)
     lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=1000), theta=1.5)
     b = np.where(fx == 0, random_vector(K.shape[0], seed=3), 0.0)
-    zo = mg.vcycle(lv, b, None, nu=nu)
+    zo = mg.vcycle(lv, b, None, nu=mg.level_sweeps(lv, nu, deep))
     with topo.Problem(p, f, fx, pas) as pr:
         pr.set_xphys(x)
         z = pr.mg_vcycle(b)
-    assert_rel(z, zo, 1e-4 if fp32 else 1e-9, f"V-cycle {dims} nu={nu} fp32={fp32}")
+    assert_rel(z, zo, 1e-4 if fp32 else 1e-9, f"V-cycle {dims} nu={nu} fp32={fp32} deep={deep}")
     assert np.all(z[fx != 0] == 0)
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu,fp32", [(1, 0), (1, 1), (2, 1)])
-def test_mg_solve_parity(topo, dims, obst, nu, fp32):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu)
+@pytest.mark.parametrize("nu,fp32,deep", [(1, 0, 0), (1, 1, 0), (2, 1, 0), (1, 1, 8)])
+def test_mg_solve_parity(topo, dims, obst, nu, fp32, deep):
+    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu, mg_nu_deep=deep)
     uo = oracle.solve_direct(K, f, fx)
-    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=nu)
+    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=nu, nu_deep=deep)
     its = {}
     for pc in ("jacobi", "mg"):
         with topo.Problem(dict(p, precond=pc), f, fx, pas) as pr:
