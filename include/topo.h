@@ -174,6 +174,7 @@ typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulativ
                                  fp64 for the rest of the run (that solve is redone)           */
   int32_t mg_theta_cuts;      /* breakdowns answered by lowering the smoother theta by 0.2 (down
                                  to 1.2) for the rest of the run (that solve is redone)        */
+  double  ms_mg_setup;        /* multigrid setup of the last solve (part of ms_solve)          */
 } topo_timings;
 
 /* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,

@@ -202,6 +202,7 @@ struct topo_ctx {
   bool prof_capture = false;   // set while enqueueing the profiled iteration
   // phase events
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_setup[2] = {};   // brackets the multigrid setup of a solve
   topo_timings tim{};
   long long launches = 0;
   std::string err;
@@ -1380,6 +1381,32 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   MgLevel& m = ctx->mg[l];
   const int gL = grid_for(m.L.nodes());
   T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *mi = mgp<T>(m.invd);
+  if (m.S && m.L.nodes() <= kMgDeepNodes) {
+    // small stencil level: lane-parallel stencil sweeps (k_mg_sweep_st, 8 lanes
+    // per node), each damped-Jacobi sweep one fused kernel ping-ponging x and t
+    constexpr int kLpn = 8;
+    const int gS = grid_for(m.L.nodes() * kLpn);
+    T* buf[2] = {mx, mt};
+    int cur = (nu - 1) & 1;   // the last pre-smoothing sweep lands in x
+    LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, buf[cur], s.st, gate, s.partials,
+           s.counter);
+    for (int k = 1; k < nu; ++k, cur ^= 1)
+      LAUNCH(ctx, (k_mg_sweep_st<true, kLpn, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
+    LAUNCH(ctx, (k_mg_sweep_st<false, kLpn, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);   // t = A x
+    LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm,
+           mgp<T>(n1.b), gst);
+    CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
+    LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
+    int k = 0;
+    if (nu & 1) {   // odd: one in-place sweep, then pairs of fused sweeps end in x
+      LAUNCH(ctx, (k_mg_sweep_st<false, kLpn, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);
+      LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
+      k = 1;
+    }
+    for (cur = 0; k < nu; ++k, cur ^= 1)
+      LAUNCH(ctx, (k_mg_sweep_st<true, kLpn, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
+    return check_launch(ctx);
+  }
   LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   for (int k = 1; k < nu; ++k) {
     CK(mg_apply<T>(ctx, l, gate));
@@ -1544,7 +1571,9 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   CK(ensure_constants(ctx));
   if (!ctx->has_E) CK(update_modulus(ctx));
   CK(exchange_nodes(ctx, &Slab::invd, 1));   // ghost planes feed the fused p-update
+  CU(cudaEventRecord(ctx->ev_setup[0], ctx->stream));
   CK(mg_setup(ctx));                         // multigrid: smoother weights, Galerkin levels, coarsest inverse
+  CU(cudaEventRecord(ctx->ev_setup[1], ctx->stream));
   const topo_params& P = ctx->prm;
   CU(cudaEventRecord(ctx->ev[6], ctx->stream));
   if (!P.cg_warm_start || !ctx->has_u || ctx->bb == 0.0)
@@ -1592,6 +1621,10 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
   CU(cudaEventSynchronize(ctx->ev[7]));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+  {
+    float ms_setup = 0.f;
+    if (cudaEventElapsedTime(&ms_setup, ctx->ev_setup[0], ctx->ev_setup[1]) == cudaSuccess) ctx->tim.ms_mg_setup = ms_setup;
+  }
   ctx->tim.cg_iters = iters;
   ctx->tim.cg_iters_total += iters;
   if (info) {
@@ -1848,6 +1881,8 @@ void free_ctx(topo_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_setup)
+    if (e) cudaEventDestroy(e);
   if (ctx->hstate) cudaFreeHost(ctx->hstate);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -2038,6 +2073,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   cudaEventCreate(&ctx->pe1);
   for (cudaEvent_t& e : ctx->pe) cudaEventCreate(&e);
   for (cudaEvent_t& e : ctx->ev) cudaEventCreate(&e);
+  for (cudaEvent_t& e : ctx->ev_setup) cudaEventCreate(&e);
   if (ctx->mode == TOPO_DIST_NCCL && W > 1) {
     std::string err;
     if (!g_nccl.load(err)) { rc = set_err(ctx, TOPO_ENCCL, "%s", err.c_str()); free_ctx(ctx); return rc; }

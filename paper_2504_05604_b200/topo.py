@@ -64,7 +64,7 @@ class topo_timings(C.Structure):
                 ("fu", C.c_double), ("volume", C.c_double), ("change", C.c_double),
                 ("lambda_", C.c_double), ("kernel_launches", C.c_int64),
                 ("cg_iters_total", C.c_int64), ("mg_fallbacks", C.c_int32),
-                ("mg_promotions", C.c_int32), ("mg_theta_cuts", C.c_int32)]
+                ("mg_promotions", C.c_int32), ("mg_theta_cuts", C.c_int32), ("ms_mg_setup", C.c_double)]
 
 
 def _load():
