@@ -838,68 +838,70 @@ k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
   }
 }
 
-// Stencil sweep for the small (deep) levels, LPN lanes per node: the 27 block
-// tasks of a node (self, 13 forward blocks stored at the node, 13 backward
-// blocks = transposes stored at the neighbour) are spread over the lanes and
-// summed with shuffles, so a level of ~10^4 nodes is not bound by one
-// thread's 243-FMA dependency chain.
+// Warp-split stencil sweep: a 256-thread block covers 32 consecutive nodes;
+// warp w takes the block tasks w, w+8, w+16, w+24 (< 27) of all 32 nodes, so
+// every stencil / vector load of a warp is 32 consecutive nodes (coalesced, SoA),
+// and the dependency chain per thread is <= 4 tasks; the 8 warps' partial sums
+// meet in shared memory and warp 0 finishes the node (fixed order).
 //   kFused = false: dst = mask(A src)
-//   kFused = true : dst = mask(src + w D^-1 (b - A src))   (one damped-Jacobi
-//                   sweep; dst != src, the caller ping-pongs two buffers)
-template <bool kFused, int LPN, typename T>
-__global__ void __launch_bounds__(kBlock)
-k_mg_sweep_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
-              const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
-              T* __restrict__ dst, const DevState* st) {
+//   kFused = true : dst = mask(src + w D^-1 (b - A src))   (dst != src)
+template <bool kFused, typename T>
+__global__ void __launch_bounds__(256)
+k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
+               const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
+               T* __restrict__ dst, const DevState* st) {
   MG_GATE(st);
-  static_assert(LPN >= 1 && LPN <= 32 && (LPN & (LPN - 1)) == 0, "LPN: power of two <= 32");
+  __shared__ double part[8][3][32];
   const long long tot = L.nodes();
-  const int lane = threadIdx.x & (LPN - 1);
-  const long long gpb = blockDim.x / LPN;   // node groups per block
-  const long long gstride = (long long)gridDim.x * gpb;
-  // every lane of a warp runs the same trip count (the shuffles need them all)
-  const long long g0 = blockIdx.x * gpb + threadIdx.x / LPN;
-  const long long trips = (tot + gstride - 1) / gstride;
-  for (long long tr = 0; tr < trips; ++tr) {
-    const long long k = g0 + tr * gstride;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long base = (long long)blockIdx.x * 32; base < tot; base += (long long)gridDim.x * 32) {
+    const long long k = base + lane;
     const bool ok = k < tot;
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
     long long i = 0;
+    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
     if (ok) {
       int ix, iy, iz;
       lv_decode(L, k, ix, iy, iz);
       i = L.n(ix, iy, iz);
-      for (int t = lane; t < 27; t += LPN) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = w + 8 * q;
+        if (t >= 27) break;
         const int bb = t == 0 ? 13 : (t <= 13 ? 13 + t : t);
         const long long d = (long long)(bb % 3 - 1) * L.nplane + (long long)((bb / 3) % 3 - 1) +
                             (long long)(bb / 9 - 1) * L.NY;
         const bool back = t >= 14;
         const long long j = back ? i - d : i + d;
         const T* sb = S + (long long)((bb - 13) * 9) * L.ncomp + (back ? j : i);
-        const T x0 = src[j], x1 = src[j + L.ncomp], x2 = src[j + 2 * L.ncomp];
-        T m[9];
+        const double x0 = (double)src[j], x1 = (double)src[j + L.ncomp], x2 = (double)src[j + 2 * L.ncomp];
+        double m[9];
 #pragma unroll
-        for (int e = 0; e < 9; ++e) m[e] = sb[(long long)e * L.ncomp];
+        for (int e = 0; e < 9; ++e) m[e] = (double)sb[(long long)e * L.ncomp];
         if (back) {   // transpose
-          d0 = fma((double)m[0], (double)x0, fma((double)m[3], (double)x1, fma((double)m[6], (double)x2, d0)));
-          d1 = fma((double)m[1], (double)x0, fma((double)m[4], (double)x1, fma((double)m[7], (double)x2, d1)));
-          d2 = fma((double)m[2], (double)x0, fma((double)m[5], (double)x1, fma((double)m[8], (double)x2, d2)));
+          d0 = fma(m[0], x0, fma(m[3], x1, fma(m[6], x2, d0)));
+          d1 = fma(m[1], x0, fma(m[4], x1, fma(m[7], x2, d1)));
+          d2 = fma(m[2], x0, fma(m[5], x1, fma(m[8], x2, d2)));
         } else {
-          d0 = fma((double)m[0], (double)x0, fma((double)m[1], (double)x1, fma((double)m[2], (double)x2, d0)));
-          d1 = fma((double)m[3], (double)x0, fma((double)m[4], (double)x1, fma((double)m[5], (double)x2, d1)));
-          d2 = fma((double)m[6], (double)x0, fma((double)m[7], (double)x1, fma((double)m[8], (double)x2, d2)));
+          d0 = fma(m[0], x0, fma(m[1], x1, fma(m[2], x2, d0)));
+          d1 = fma(m[3], x0, fma(m[4], x1, fma(m[5], x2, d1)));
+          d2 = fma(m[6], x0, fma(m[7], x1, fma(m[8], x2, d2)));
         }
       }
     }
+    part[w][0][lane] = d0;
+    part[w][1][lane] = d1;
+    part[w][2][lane] = d2;
+    __syncthreads();
+    if (w == 0 && ok) {
+      double av[3];
 #pragma unroll
-    for (int o = LPN / 2; o >= 1; o >>= 1) {
-      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-    }
-    if (ok && lane == 0) {
+      for (int c = 0; c < 3; ++c) {
+        double a = part[0][c][lane];
+#pragma unroll
+        for (int ww = 1; ww < 8; ++ww) a += part[ww][c][lane];
+        av[c] = a;
+      }
       const uint8_t fm = fix[i];
-      const double av[3] = {d0, d1, d2};
       const double omega = kFused ? *omp : 0.0;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -909,6 +911,7 @@ k_mg_sweep_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const
         dst[o] = ((fm >> c) & 1) ? T(0) : (T)v;
       }
     }
+    __syncthreads();
   }
 }
 

@@ -1382,29 +1382,28 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   const int gL = grid_for(m.L.nodes());
   T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *mi = mgp<T>(m.invd);
   if (m.S && m.L.nodes() <= kMgDeepNodes) {
-    // small stencil level: lane-parallel stencil sweeps (k_mg_sweep_st, 8 lanes
-    // per node), each damped-Jacobi sweep one fused kernel ping-ponging x and t
-    constexpr int kLpn = 8;
-    const int gS = grid_for(m.L.nodes() * kLpn);
+    // small stencil level: each damped-Jacobi sweep is one fused warp-split
+    // stencil kernel (k_mg_sweep_st8) ping-ponging x and t
+    const int gS = (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16);   // 32 nodes per block
     T* buf[2] = {mx, mt};
     int cur = (nu - 1) & 1;   // the last pre-smoothing sweep lands in x
     LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, buf[cur], s.st, gate, s.partials,
            s.counter);
     for (int k = 1; k < nu; ++k, cur ^= 1)
-      LAUNCH(ctx, (k_mg_sweep_st<true, kLpn, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
-    LAUNCH(ctx, (k_mg_sweep_st<false, kLpn, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);   // t = A x
+      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
+    LAUNCH(ctx, (k_mg_sweep_st8<false, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);   // t = A x
     LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm,
            mgp<T>(n1.b), gst);
     CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
     LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
     int k = 0;
     if (nu & 1) {   // odd: one in-place sweep, then pairs of fused sweeps end in x
-      LAUNCH(ctx, (k_mg_sweep_st<false, kLpn, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);
       LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
       k = 1;
     }
     for (cur = 0; k < nu; ++k, cur ^= 1)
-      LAUNCH(ctx, (k_mg_sweep_st<true, kLpn, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
+      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
     return check_launch(ctx);
   }
   LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
