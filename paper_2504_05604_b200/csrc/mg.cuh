@@ -568,6 +568,24 @@ k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __rest
   }
 }
 
+// Level 2 as a GEMM: K2[rs][e] = sum_f E_f(e) tab64[f][rs] (linear in the 64
+// fine moduli of a level-2 element); this gathers Eg[e + nel * f] (column-major
+// nel x 64) for cuBLAS DGEMM.  Child f = (fx, fy, fz) = (f % 4, (f / 4) % 4, f / 16)
+// as in k_mg_asm_fine<4>; children outside the fine grid give 0.
+__global__ void __launch_bounds__(kBlock)
+k_mg_gather64(Geo g, LvGeo L, const double* __restrict__ E, double* __restrict__ Eg) {
+  const long long nel = L.nel(), tot = 64 * nel;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(t / nel);
+    const long long e = t - (long long)f * nel;
+    const int ey = (int)(e % L.ny);
+    const long long r = e / L.ny;
+    const int ez = (int)(r % L.nz), ex = (int)(r / L.nz);
+    const int fx = 4 * ex + f % 4, fy = 4 * ey + (f / 4) % 4, fz = 4 * ez + f / 16;
+    Eg[t] = (fx < g.nelx && fy < g.nely && fz < g.nelz) ? E[elem_idx(g, fx, fy, fz)] : 0.0;
+  }
+}
+
 // Element matrices of level l+1 from the stored level l (Galerkin per child):
 //   KC_e[3R+i][3S+j] = sum_c sum_{A,B} w[c][A][R] KF_child(c)[3A+i][3B+j] w[c][B][S]
 // Thread per (entry, coarse element), element fastest.
@@ -604,6 +622,80 @@ k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __re
     KC[(long long)k * nelC + e] = acc;
     KC[(long long)(s * 24 + r) * nelC + e] = acc;
   }
+}
+
+// Same product, tiled for memory efficiency: a CTA owns 8 coarse elements
+// consecutive in y (fixed ex, ez) and walks the 4 (cx, cz) child pairs; for each
+// pair the 16 fine elements (cy = 0, 1 of each coarse element, consecutive in the
+// fine y) are staged in shared memory, every entry read once and coalesced.
+// Thread (e, s) builds column s = 3S + j of its coarse element:
+//   v[(A,i)] = sum_{B} w[c][B][S] KF_c[(A,i),(B,j)],  KC[(R,i), s] += sum_A w[c][A][R] v[(A,i)].
+constexpr int kGalTile = 8;
+__global__ void __launch_bounds__(kGalTile * 24, 2)
+k_mg_asm_galerkin_t(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __restrict__ KC) {
+  extern __shared__ double sK[];                 // [576][2 * kGalTile]
+  constexpr int NF = 2 * kGalTile;
+  const int el = threadIdx.x, sc = threadIdx.y;  // coarse element in the tile, output column
+  const int tid = sc * kGalTile + el, nth = kGalTile * 24;
+  const int ey0 = blockIdx.x * kGalTile, ez = blockIdx.y, ex = blockIdx.z;
+  const int ey = ey0 + el;
+  const long long nelC = Cg.nel(), nelF = F.nel();
+  const int S = sc / 3, j = sc % 3;
+  double acc[24];
+#pragma unroll
+  for (int r = 0; r < 24; ++r) acc[r] = 0.0;
+  for (int pr = 0; pr < 4; ++pr) {
+    const int cx = pr & 1, cz = pr >> 1;
+    const int fx = 2 * ex + cx, fz = 2 * ez + cz;
+    const bool plane_ok = fx < F.nx && fz < F.nz;
+    __syncthreads();
+    if (plane_ok) {
+      const long long fbase = ((long long)fx * F.nz + fz) * F.ny + 2 * ey0;
+      for (int t = tid; t < 576 * NF; t += nth) {
+        const int q = t / NF, f = t - q * NF;
+        sK[t] = (2 * ey0 + f < F.ny) ? KF[(long long)q * nelF + fbase + f] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (!plane_ok || ey >= Cg.ny) continue;
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      const int c = cx + 2 * cy + 4 * cz;
+      const int f = 2 * el + cy;
+      double v[24];
+#pragma unroll
+      for (int r = 0; r < 24; ++r) v[r] = 0.0;
+      const int nb = c_mg_nzN[c][S];
+      for (int ib = 0; ib < nb; ++ib) {
+        const int B = c_mg_nzA[c][S][ib];
+        const double wb = c_mg_nzW[c][S][ib];
+#pragma unroll
+        for (int r = 0; r < 24; ++r) v[r] = fma(wb, sK[(r * 24 + 3 * B + j) * NF + f], v[r]);
+      }
+      // acc += W_c^T v with w[c][A][R] = prod_d (R_d ? t_d : 1 - t_d), t_d = (c_d + A_d) / 2
+      // (SPEC corner order: A_x = ((A + 1) >> 1) & 1, A_y = (A >> 1) & 1, A_z = A >> 2);
+      // fully unrolled so v and acc stay in registers
+      const int cd[3] = {cx, cy, cz};
+#pragma unroll
+      for (int A = 0; A < 8; ++A) {
+        const int ad[3] = {((A + 1) >> 1) & 1, (A >> 1) & 1, A >> 2};
+        double t[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) t[d] = 0.5 * (double)(cd[d] + ad[d]);
+#pragma unroll
+        for (int R = 0; R < 8; ++R) {
+          const int rd[3] = {((R + 1) >> 1) & 1, (R >> 1) & 1, R >> 2};
+          const double w = (rd[0] ? t[0] : 1.0 - t[0]) * (rd[1] ? t[1] : 1.0 - t[1]) * (rd[2] ? t[2] : 1.0 - t[2]);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) acc[3 * R + i] = fma(w, v[3 * A + i], acc[3 * R + i]);
+        }
+      }
+    }
+  }
+  if (ey >= Cg.ny) return;
+  const long long e = ((long long)ex * Cg.nz + ez) * Cg.ny + ey;
+#pragma unroll
+  for (int r = 0; r < 24; ++r) KC[(long long)(r * 24 + sc) * nelC + e] = acc[r];
 }
 
 // ---------------------------------------------------------------------------

@@ -106,7 +106,7 @@ struct CublasApi {
   }
 };
 CublasApi g_cublas;
-constexpr int CUBLAS_OP_N_ = 0;
+constexpr int CUBLAS_OP_N_ = 0, CUBLAS_OP_T_ = 1;
 
 struct TopoError {
   int code;
@@ -217,6 +217,7 @@ struct topo_ctx {
   double mg_theta = 1.6, mg_theta_b = 1.6;   // smoother theta in use (cut after a breakdown) (+ snapshot)
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
+  double* mg_Eg = nullptr;           // level-2 Galerkin: gathered fine moduli [64][nel_2] (DGEMM operand)
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
   int mg_npad = 0;                   // coarsest dense size rounded up to kGjB
   cublasHandle_t cublas = nullptr;
@@ -962,6 +963,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
           lay[m.L.n(ix, iy, iz)] = h.fix[(long long)iz * (h.nx + 1) * (h.ny + 1) + (long long)ix * (h.ny + 1) + iy];
     CU(cudaMemcpy(m.fixm, lay.data(), m.L.ncomp, cudaMemcpyHostToDevice));
   }
+  if (L >= 3 && !ctx->mg[1].stored)   // level-2 Galerkin DGEMM operand
+    CK(al((void**)&ctx->mg_Eg, sizeof(double) * 64 * ctx->mg[2].L.nel()));
   // coarsest dense maps
   {
     const MgLevel& m = ctx->mg[L - 1];
@@ -1074,11 +1077,27 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       k_mg_asm_fine<2><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), ctx->mg_tab8, m.K);
       ctx->launches++;
     } else if (l == 2 && !ctx->mg[1].stored) {
-      k_mg_asm_fine<4><<<(unsigned)((ne + kBlock - 1) / kBlock), kBlock, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), ctx->mg_tab64, m.K);
-      ctx->launches++;
+      // K2 = Eg tab64^T: gather the 64 fine moduli per element, then one DGEMM
+      // (nel x 64) x (64 x 576) into the entry-major [576][nel] layout
+      LAUNCH(ctx, k_mg_gather64, grid_for(64 * ne), mgG(ctx), m.L, mgE(ctx), ctx->mg_Eg);
+      if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
+      const double d1 = 1.0, d0 = 0.0;
+      if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_T_, (int)ne, 576, 64, &d1, ctx->mg_Eg, (int)ne,
+                         ctx->mg_tab64, 576, &d0, m.K, (int)ne) != 0)
+        return set_err(ctx, TOPO_ECUDA, "cublasDgemm (level-2 Galerkin) failed");
     } else {
       const MgLevel& f = ctx->mg[l - 1];
-      LAUNCH(ctx, k_mg_asm_galerkin, grid_for(300 * ne), f.L, f.K, m.L, m.K);
+      {   // tiled Galerkin product (k_mg_asm_galerkin_t), 8 coarse elements per CTA
+        const size_t smem = sizeof(double) * 576 * 2 * kGalTile;
+        static bool attr = false;
+        if (!attr) {
+          CU(cudaFuncSetAttribute(k_mg_asm_galerkin_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attr = true;
+        }
+        k_mg_asm_galerkin_t<<<dim3((m.L.ny + kGalTile - 1) / kGalTile, m.L.nz, m.L.nx), dim3(kGalTile, 24), smem,
+                              ctx->stream>>>(f.L, f.K, m.L, m.K);
+        ctx->launches++;
+      }
     }
     debug_sync(ctx, "k_mg_asm");
     LAUNCH(ctx, k_mg_diag_asm<T>, grid_for(nn), m.L, m.K, m.fixm, mgp<T>(m.invd));
@@ -1105,12 +1124,14 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
                  sl.g.ex0, xa, xb, sl.g.nelx, sl.fixm, sl.z);
         }
       }
-      for (Slab& sl : ctx->slabs) CK((launch_mv<0, false, 3>(ctx, sl, 0, sl.m_z, nullptr, nullptr, sl.q, 0, one)));
+      // (T = the hierarchy's precision: with mg_fp32 the power steps use the fp32
+      // element operator like the smoothing matvecs they calibrate)
+      for (Slab& sl : ctx->slabs) CK((launch_mv<0, false, 3, T>(ctx, sl, 0, sl.m_z, nullptr, nullptr, sl.q, 0, one)));
       CK(exchange_nodes(ctx, &Slab::q));
       for (int k = 1; k <= nsteps; ++k) {
         const bool odd = k & 1;
         for (Slab& sl : ctx->slabs)
-          CK((launch_mv<3, false, 3>(ctx, sl, 0, odd ? sl.m_q : sl.m_w, nullptr, sl.z, odd ? sl.w : sl.q, 0, one)));
+          CK((launch_mv<3, false, 3, T>(ctx, sl, 0, odd ? sl.m_q : sl.m_w, nullptr, sl.z, odd ? sl.w : sl.q, 0, one)));
         CK(exchange_nodes(ctx, odd ? &Slab::w : &Slab::q));
       }
       for (Slab& sl : ctx->slabs) {
@@ -1862,7 +1883,7 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   {
-    void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_A0, ctx->mg_C, ctx->mg_R, ctx->mg_P, ctx->mg_ws,
+    void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_Eg, ctx->mg_A0, ctx->mg_C, ctx->mg_R, ctx->mg_P, ctx->mg_ws,
                     ctx->mg_dmap, ctx->mg_imap, ctx->mg_om};
     for (void* p : ptrs)
       if (p) cudaFree(p);

@@ -11,7 +11,10 @@ res = {"_source": src}
 for r in rows[2:]:
     name = r[col["Kernel Name"]]
     m = re.match(r"void (\w+)<([^>]*)>", name) or re.match(r"(\w+)", name)
-    key = m.group(1) + ("<" + m.group(2).replace(" ", "") + ">" if m.lastindex and m.lastindex > 1 else "")
+    args = m.group(2).replace(" ", "") if m.lastindex and m.lastindex > 1 else None
+    if args is not None:   # k_mv_wht<8,3,0,2,float> -> k_mv_wht<8,3,0,2> (the element-operator type is not part of the key)
+        args = re.sub(r",(double|float)$", "", args)
+    key = m.group(1) + ("<" + args + ">" if args is not None else "")
     if key in res:
         continue
     def g(k, scale=1.0):
