@@ -271,6 +271,16 @@ int set_err(topo_ctx* c, int code, const char* fmt, ...) {
       return set_err(ctx, TOPO_ENCCL, "%s failed: %s", #call, g_nccl.GetErrorString(r_)); \
   } while (0)
 
+// grid of a grid-stride streaming kernel: at most the CTAs that are resident at
+// once (one wave: no tail of a partial last wave), at most grid_for(n)
+template <typename K>
+int grid_resident(K kern, long long n, int threads = kBlock) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+  const long long b = (n + threads - 1) / threads;
+  return (int)std::max(1LL, std::min<long long>(b, 148LL * per_sm));
+}
+
 inline int grid_for(long long n) {
   long long b = (n + kBlock - 1) / kBlock;
   if (b < 1) b = 1;
@@ -732,7 +742,7 @@ int matvec_all(topo_ctx* ctx, double* Slab::*pin, CUtensorMap Slab::*pmap, doubl
 int residual(topo_ctx* ctx, bool write_r) {
   CK(matvec_all(ctx, &Slab::u, &Slab::m_u, &Slab::q));
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_residual, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.fixm,
+    LAUNCH(ctx, k_residual, grid_resident(k_residual, (long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.fixm,
            s.r, write_r ? 1 : 0, s.partials, s.counter);
   CK(check_launch(ctx));
   if (write_r) CK(exchange_nodes(ctx, &Slab::r));
@@ -1668,7 +1678,7 @@ int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
   CK(exchange_nodes(ctx, &Slab::u));
   const Material m = material(ctx);
   for (Slab& s : ctx->slabs) {
-    LAUNCH(ctx, k_sens, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
+    LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
            s.passive, s.ce, s.dc, s.partials, s.counter);
     LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.u, 1, s.partials, s.counter);
   }
@@ -1741,7 +1751,7 @@ int enqueue_oc_batch(topo_ctx* ctx) {
   const int W = ctx->world, fin = (W == 1) ? 1 : 0;
   for (int i = 0; i < ctx->oc_batch; ++i) {
     for (Slab& s : ctx->slabs) {
-      const int gr = grid_for((long long)s.g.nex * s.g.eplane);
+      const int gr = grid_resident(k_oc_pass<1>, (long long)s.g.nex * s.g.eplane);
       if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY)
         LAUNCH(ctx, k_oc_pass<1>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
       else
@@ -1780,7 +1790,7 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   for (Slab& s : ctx->slabs) {
     k_oc_init<<<1, 1, 0, ctx->stream>>>(s.st, P.oc_lmax, P.volfrac * (double)ctx->n_design, P.oc_tol);
     ctx->launches++;
-    LAUNCH(ctx, k_oc_prep, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.x, s.dcf, s.dvf, s.passive, s.oca);
+    LAUNCH(ctx, k_oc_prep, grid_resident(k_oc_prep, (long long)s.g.nex * s.g.eplane), s.g, s.x, s.dcf, s.dvf, s.passive, s.oca);
   }
   CK(check_launch(ctx));
   if (!ctx->debug) CK(build_oc_graph(ctx));
@@ -1798,7 +1808,7 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
     if (++guard > 4096 / ctx->oc_batch) return set_err(ctx, TOPO_EBISECT, "OC bisection did not terminate");
   }
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_oc_final, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.xnew,
+    LAUNCH(ctx, k_oc_final, grid_resident(k_oc_final, (long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.xnew,
            s.partials, s.counter);
   CK(check_launch(ctx));
   CK(allreduce(ctx, 2, 2, 0x2));
