@@ -236,6 +236,7 @@ def main():
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")
     ap.add_argument("--mg-omega", type=float, default=None, help="MG smoother theta (default: the library's)")
+    ap.add_argument("--mg-nu-deep", type=int, default=0, help="MG sweeps on the small coarse levels (0 = library auto)")
     args = ap.parse_args()
 
     from workloads import make_problem
@@ -243,7 +244,7 @@ def main():
         args.e2e_steps = args.steps
     world, rank, local = dist_env()
     p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max,
-                                 mg_nu=args.mg_nu,
+                                 mg_nu=args.mg_nu, mg_nu_deep=args.mg_nu_deep,
                                  **({} if args.mg_omega is None else {"mg_omega": args.mg_omega}))
 
     if args.impl == "reference":
