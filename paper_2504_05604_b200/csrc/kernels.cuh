@@ -481,26 +481,41 @@ k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const 
     sc[k] = 1.0 / sqrt(lam[k + 1]);
     vol[k] = 0.0;
   }
+  // element pairs (double2: b0 and the plane size are even, so pairs are
+  // 16-byte aligned); 2 pairs per trip with all 6 vector loads issued before
+  // any use (the pass is latency-bound otherwise).  An out-of-range pair reads
+  // pair 0 and is weighted by 0.
   const unsigned b0 = (unsigned)(g.H * g.eplane), e0 = (unsigned)((g.H + g.nex) * g.eplane);
+  const unsigned np = (e0 - b0) / 2;        // (e0 - b0) = nex * eplane is even
   const unsigned stride = gridDim.x * blockDim.x;
-  // 4 elements per trip with all loads issued first (the pass is latency-bound
-  // otherwise); an out-of-range slot reads x = A = 0, which gives xnew = 0
-  for (unsigned i0 = b0 + blockIdx.x * blockDim.x + threadIdx.x; i0 < e0; i0 += 4 * stride) {
-    double xv[4], av[4], dv[4];
+  const double2* x2 = reinterpret_cast<const double2*>(x + b0);
+  const double2* a2 = reinterpret_cast<const double2*>(A + b0);
+  const double2* d2 = reinterpret_cast<const double2*>(dvf + b0);
+  for (unsigned p0 = blockIdx.x * blockDim.x + threadIdx.x; p0 < np; p0 += 2 * stride) {
+    double2 xv[2], av[2], dv[2];
+    double wv[2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const unsigned i = i0 + j * stride;
-      const bool ok = i < e0;
-      xv[j] = ok ? x[i] : 0.0;
-      av[j] = ok ? A[i] : 0.0;
-      dv[j] = MODE0 ? (ok ? dvf[i] : 0.0) : 1.0;
+    for (int j = 0; j < 2; ++j) {
+      const unsigned pj = p0 + j * stride;
+      const bool ok = pj < np;
+      const unsigned q = ok ? pj : 0u;
+      xv[j] = __ldg(x2 + q);
+      av[j] = __ldg(a2 + q);
+      dv[j] = MODE0 ? __ldg(d2 + q) : make_double2(1.0, 1.0);
+      wv[j] = ok ? 1.0 : 0.0;
     }
+    asm volatile("" ::: "memory");   // keep all six loads ahead of the compute (compiler barrier)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 2; ++j) {
       // lambda-independent clamp bounds: xnew = min(hi, max(lo, A s)) (= oc_xnew exactly)
-      const double lo = fmax(0.0, xv[j] - move), hi = fmin(1.0, xv[j] + move);
+      const double lo0 = fmax(0.0, xv[j].x - move), hi0 = fmin(1.0, xv[j].x + move);
+      const double lo1 = fmax(0.0, xv[j].y - move), hi1 = fmin(1.0, xv[j].y + move);
+      const double w0 = wv[j] * dv[j].x, w1 = wv[j] * dv[j].y;
 #pragma unroll
-      for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv[j], fmin(hi, fmax(lo, av[j] * sc[k])), vol[k]);
+      for (int k = 0; k < kOcCand; ++k) {
+        vol[k] = fma(w0, fmin(hi0, fmax(lo0, av[j].x * sc[k])), vol[k]);
+        vol[k] = fma(w1, fmin(hi1, fmax(lo1, av[j].y * sc[k])), vol[k]);
+      }
     }
   }
   __shared__ double tot[kOcCand];
