@@ -504,7 +504,17 @@ k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const 
       dv[j] = MODE0 ? __ldg(d2 + q) : make_double2(1.0, 1.0);
       wv[j] = ok ? 1.0 : 0.0;
     }
-    asm volatile("" ::: "memory");   // keep all six loads ahead of the compute (compiler barrier)
+    // L2 prefetch of the next trip's pairs (ptxas sinks the second pair's loads
+    // behind the first pair's compute; the prefetches keep DRAM busy meanwhile)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const unsigned pn = p0 + (2 + j) * stride;
+      if (pn < np) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(x2 + pn));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a2 + pn));
+        if (MODE0) asm volatile("prefetch.global.L2 [%0];" ::"l"(d2 + pn));
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       // lambda-independent clamp bounds: xnew = min(hi, max(lo, A s)) (= oc_xnew exactly)
