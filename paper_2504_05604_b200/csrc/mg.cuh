@@ -1063,9 +1063,10 @@ constexpr int kGjB = 64;
 // one CTA of b*b/4 threads: thread (i, j4) keeps a_{i, j4 + 16 m} (m < 4, b = 64)
 // in registers; per pivot the pivot column and row go through shared memory
 // (two barriers per step, no shared-memory round trip of the whole block).
-__global__ void __launch_bounds__(kGjB * kGjB / 4)
+constexpr int kGjInvNJ = 4;    // columns per thread: 1024 threads (16 was slower: more work per pivot step)
+__global__ void __launch_bounds__(kGjB * kGjB / kGjInvNJ)
 k_gj_block_inv(const double* __restrict__ A, int ld, int k0, double* __restrict__ P) {
-  constexpr int NJ = 4, JS = kGjB / NJ;               // columns per thread, column stride
+  constexpr int NJ = kGjInvNJ, JS = kGjB / NJ;        // columns per thread, column stride
   __shared__ double col[kGjB], row[kGjB];
   const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;   // row i, columns j0 + JS m
   double a[NJ];

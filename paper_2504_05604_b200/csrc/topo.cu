@@ -1191,7 +1191,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
   const double d_one = 1.0, d_mone = -1.0, d_zero = 0.0;
   for (int k0 = 0; k0 < np; k0 += kGjB) {
-    k_gj_block_inv<<<1, kGjB * kGjB / 4, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
+    k_gj_block_inv<<<1, kGjB * kGjB / kGjInvNJ, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
     ctx->launches++;
     // R = P A_K,:  (b x np)
     if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, kGjB, np, kGjB, &d_one, ctx->mg_P, kGjB, A + k0, np,
