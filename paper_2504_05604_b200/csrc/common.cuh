@@ -58,6 +58,9 @@ struct DevState {
   // OC bisection
   double l1, l2, lmid, target, vol, oc_tol;
   int oc_active, oc_pass;
+  double oc_frozen;    // OC after compaction: volume of the elements frozen at a clamp bound
+  double oc_lin;       // ... sum of dv~ A over the elements unclamped for every remaining lambda
+  long long oc_nact;   // ... and the number of active (compacted) elements
   // landing zone of per-slab partial sums (allreduced across slabs)
   double sums[8];
 };

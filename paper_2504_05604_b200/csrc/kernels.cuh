@@ -535,6 +535,141 @@ k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const 
       for (int k = 0; k < kOcCand; ++k) st->sums[k] = tot[k];
   }
 }
+// ---------------------------------------------------------------------------
+// OC frozen set: once the bracket [l1, l2] (l1 > 0) is narrow, s = 1/sqrt(lambda)
+// stays in [1/sqrt(l2), 1/sqrt(l1)] for every lambda the bisection can still
+// evaluate, and an element's xnew = clamp(A s, lo, hi) is either
+//   fixed at lo (A s_hi <= lo) or at hi (A s_lo >= hi): a constant, or
+//   unclamped (lo <= A s_lo, A s_hi <= hi): linear in s, dv~ A s,
+//   or crossing a bound inside the bracket (active).
+// F = sum of the constants and G = sum dv~ A over the linear class are formed
+// once; the active elements are compacted (in element order) and later passes
+// evaluate V(s) = F + s G + sum_active -- the same terms as the full sum up to
+// the order of the additions.  Applied twice (two nested brackets) with
+// ping-pong arrays.  Block b owns the contiguous chunk [b chunk, (b+1) chunk),
+// so the compaction order is deterministic.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int oc_class(double x, double A, double move, double slo, double shi) {
+  const double lo = fmax(0.0, x - move), hi = fmin(1.0, x + move);
+  if (A * shi <= lo) return 0;                   // fixed at lo
+  if (A * slo >= hi) return 1;                   // fixed at hi
+  if (lo <= A * slo && A * shi <= hi) return 2;  // unclamped: linear in s
+  return 3;                                      // crossing: active
+}
+
+template <int MODE0>
+__global__ void __launch_bounds__(kBlock)
+k_oc_freeze(long long n0, const long long* __restrict__ nptr, const double* __restrict__ x, const double* __restrict__ A,
+            const double* __restrict__ dvf, DevState* st, double move, unsigned chunk,
+            unsigned* __restrict__ counts, double* partials, unsigned int* counter) {
+  const double slo = 1.0 / sqrt(st->l2), shi = 1.0 / sqrt(st->l1);
+  const long long n = nptr ? *nptr : n0;   // stage 2 reads the stage-1 active count on the device
+  const long long c0 = (long long)blockIdx.x * chunk, c1 = min(n, c0 + (long long)chunk);
+  double fz = 0.0, lin = 0.0;
+  unsigned na = 0;
+  for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const double xv = x[i], av = A[i], dv = MODE0 ? dvf[i] : 1.0;
+    const int c = oc_class(xv, av, move, slo, shi);
+    if (c == 3) ++na;
+    else if (c == 2) lin = fma(dv, av, lin);
+    else fz = fma(dv, c == 0 ? fmax(0.0, xv - move) : fmin(1.0, xv + move), fz);
+  }
+  __shared__ unsigned cnt_sh;
+  if (threadIdx.x == 0) cnt_sh = 0;
+  __syncthreads();
+  atomicAdd(&cnt_sh, na);   // integer: order-independent
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = cnt_sh;
+  __shared__ double tot[2];
+  double v[2] = {fz, lin};
+  if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
+    st->oc_frozen += tot[0];
+    st->oc_lin += tot[1];
+  }
+}
+
+// exclusive scan of the per-block active counts (one thread; nb <= a few thousand)
+__global__ void k_oc_scan(const unsigned* __restrict__ counts, int nb, unsigned* __restrict__ offs, DevState* st) {
+  if (threadIdx.x != 0) return;
+  unsigned long long run = 0;
+  for (int b = 0; b < nb; ++b) {
+    offs[b] = (unsigned)run;
+    run += counts[b];
+  }
+  st->oc_nact = (long long)run;
+}
+
+// compaction in element order: tiles of blockDim elements, block-wide scan of the flags
+template <int MODE0>
+__global__ void __launch_bounds__(kBlock)
+k_oc_compact(long long n0, const long long* __restrict__ nptr, const double* __restrict__ x, const double* __restrict__ A,
+             const double* __restrict__ dvf, const DevState* st, double move, unsigned chunk,
+             const unsigned* __restrict__ offs, double* __restrict__ cx, double* __restrict__ cA,
+             double* __restrict__ cdv) {
+  const double slo = 1.0 / sqrt(st->l2), shi = 1.0 / sqrt(st->l1);
+  const long long n = nptr ? *nptr : n0;   // stage 2 reads the stage-1 active count on the device
+  const long long c0 = (long long)blockIdx.x * chunk, c1 = min(n, c0 + (long long)chunk);
+  __shared__ unsigned wsum[kBlock / 32];
+  unsigned base = offs[blockIdx.x];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (long long t0 = c0; t0 < c1; t0 += blockDim.x) {
+    const long long i = t0 + threadIdx.x;
+    double xv = 0.0, av = 0.0, dv = 0.0;
+    bool act = false;
+    if (i < c1) {
+      xv = x[i];
+      av = A[i];
+      dv = MODE0 ? dvf[i] : 1.0;
+      act = oc_class(xv, av, move, slo, shi) == 3;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    unsigned before = 0, total = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      if (k < w) before += wsum[k];
+      total += wsum[k];
+    }
+    if (act) {
+      const unsigned o = base + before + __popc(bal & ((1u << lane) - 1u));
+      cx[o] = xv;
+      cA[o] = av;
+      cdv[o] = dv;
+    }
+    base += total;
+    __syncthreads();
+  }
+}
+
+// a bisection pass over the compacted active elements: V(s) = F + s G + sum_active
+__global__ void __launch_bounds__(kBlock)
+k_oc_pass_c(DevState* st, double move, const double* __restrict__ cx, const double* __restrict__ cA,
+            const double* __restrict__ cdv, double* partials, unsigned int* counter, int finish) {
+  if (!st->oc_active) return;
+  double lam[kOcCand + 1], sc[kOcCand], vol[kOcCand];
+  oc_tree(st->l1, st->l2, lam);
+#pragma unroll
+  for (int k = 0; k < kOcCand; ++k) {
+    sc[k] = 1.0 / sqrt(lam[k + 1]);
+    vol[k] = 0.0;
+  }
+  const long long n = st->oc_nact;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double xv = cx[i], av = cA[i], dv = cdv[i];
+    const double lo = fmax(0.0, xv - move), hi = fmin(1.0, xv + move);
+#pragma unroll
+    for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv, fmin(hi, fmax(lo, av * sc[k])), vol[k]);
+  }
+  __shared__ double tot[kOcCand];
+  if (grid_reduce<kOcCand>(vol, partials, counter, tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kOcCand; ++k) tot[k] += fma(sc[k], st->oc_lin, st->oc_frozen);
+    if (finish) oc_walk(st, tot);
+    else
+      for (int k = 0; k < kOcCand; ++k) st->sums[k] = tot[k];
+  }
+}
+
 __global__ void k_oc_finish(DevState* st) {
   if (!st->oc_active) return;
   oc_walk(st, st->sums);
@@ -698,6 +833,9 @@ __global__ void k_oc_init(DevState* st, double lmax, double target, double tol) 
   st->oc_tol = tol;
   st->oc_pass = 0;
   st->vol = 0.0;
+  st->oc_frozen = 0.0;
+  st->oc_lin = 0.0;
+  st->oc_nact = 0;
   st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > tol) ? 1 : 0;
   st->lmid = 0.5 * (st->l2 + st->l1);
 }

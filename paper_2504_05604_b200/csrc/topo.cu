@@ -124,6 +124,11 @@ struct Slab {
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
   float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
   double *pw0 = nullptr, *pw0_b = nullptr;   // multigrid level-0 power vector (+ snapshot)
+  // OC frozen set: per-block active counts / offsets and the compacted (x, A, dv~)
+  unsigned *oc_counts = nullptr, *oc_offs = nullptr;
+  double *oc_cx = nullptr, *oc_cA = nullptr, *oc_cdv = nullptr;      // stage-1 active set
+  double *oc_cx2 = nullptr, *oc_cA2 = nullptr, *oc_cdv2 = nullptr;   // stage-2 active set
+  long long* oc_n1 = nullptr;                                          // stage-1 active count (device)
   double* invd = nullptr;    // per node (1 component): 1/(kd sum E)
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
@@ -186,8 +191,8 @@ struct topo_ctx {
   int cg_batch = 0;
   long long cg_batch_launches[2] = {0, 0};
   bool cg_profiled_graph[2] = {false, false};
-  cudaGraphExec_t oc_exec = nullptr;
-  int oc_batch = 14;                 // passes (3 bisection levels each) per OC graph launch
+  cudaGraphExec_t oc_exec = nullptr, oc_exec_c = nullptr, oc_exec_c2 = nullptr;   // full / stage-1 / stage-2 OC batches
+  int oc_batch = 4;                  // passes (3 bisection levels each) per OC graph launch
   long long oc_batch_launches = 0;
   // profiling
   bool profile = false;
@@ -1747,10 +1752,18 @@ int do_filter_x(topo_ctx* ctx) {
   return TOPO_OK;
 }
 
-int enqueue_oc_batch(topo_ctx* ctx) {
+constexpr int kOcFreezeBlocks = 148 * 4;   // blocks of the freeze / compaction kernels
+
+int enqueue_oc_batch(topo_ctx* ctx, int compact) {
   const int W = ctx->world, fin = (W == 1) ? 1 : 0;
   for (int i = 0; i < ctx->oc_batch; ++i) {
     for (Slab& s : ctx->slabs) {
+      if (compact) {
+        const bool s2 = compact == 2;
+        LAUNCH(ctx, k_oc_pass_c, 148 * 4, s.st, ctx->prm.move, s2 ? s.oc_cx2 : s.oc_cx, s2 ? s.oc_cA2 : s.oc_cA,
+               s2 ? s.oc_cdv2 : s.oc_cdv, s.partials, s.counter, fin);
+        continue;
+      }
       const int gr = grid_resident(k_oc_pass<1>, (long long)s.g.nex * s.g.eplane);
       if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY)
         LAUNCH(ctx, k_oc_pass<1>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
@@ -1765,21 +1778,56 @@ int enqueue_oc_batch(topo_ctx* ctx) {
   return check_launch(ctx);
 }
 
-int build_oc_graph(topo_ctx* ctx) {
-  if (ctx->oc_exec) return TOPO_OK;
+int build_oc_graph(topo_ctx* ctx, int compact) {
+  cudaGraphExec_t& ex = compact == 2 ? ctx->oc_exec_c2 : compact == 1 ? ctx->oc_exec_c : ctx->oc_exec;
+  if (ex) return TOPO_OK;
   cudaGraph_t graph;
   const long long l0 = ctx->launches;
   CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_oc_batch(ctx);
+  int rc = enqueue_oc_batch(ctx, compact);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
   if (rc != TOPO_OK) return rc;
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "OC graph capture: %s", cudaGetErrorString(e));
-  e = cudaGraphInstantiate(&ctx->oc_exec, graph, 0);
+  e = cudaGraphInstantiate(&ex, graph, 0);
   cudaGraphDestroy(graph);
   if (e != cudaSuccess) return set_err(ctx, TOPO_ECUDA, "OC graph instantiate: %s", cudaGetErrorString(e));
-  ctx->oc_batch_launches = ctx->launches - l0;
+  ctx->oc_batch_launches = ctx->launches - l0;   // same count for both batch kinds
   ctx->launches = l0;
   return TOPO_OK;
+}
+
+// Freeze the elements whose xnew is a constant or linear in s for the rest of
+// the bisection and compact the others (k_oc_freeze / k_oc_scan /
+// k_oc_compact); per slab.  Stage 1 reads the element arrays, stage 2 the
+// stage-1 active set (its count stays on the device).
+int oc_compact(topo_ctx* ctx, int stage) {
+  const bool dens = ctx->prm.filter_mode == TOPO_FILTER_DENSITY;
+  for (Slab& s : ctx->slabs) {
+    const long long b0 = (long long)s.g.H * s.g.eplane, n = (long long)s.g.nex * s.g.eplane;
+    const int nb = (int)std::max(1LL, std::min<long long>(kOcFreezeBlocks, (n + kBlock - 1) / kBlock));
+    const unsigned chunk = (unsigned)((n + nb - 1) / nb);
+    const double *x, *A, *dv;
+    const long long* nptr = nullptr;
+    double *ox, *oA, *odv;
+    if (stage == 1) {
+      x = s.x + b0; A = s.oca + b0; dv = s.dvf + b0;
+      ox = s.oc_cx; oA = s.oc_cA; odv = s.oc_cdv;
+    } else {
+      CU(cudaMemcpyAsync(s.oc_n1, &s.st->oc_nact, sizeof(long long), cudaMemcpyDeviceToDevice, ctx->stream));
+      x = s.oc_cx; A = s.oc_cA; dv = s.oc_cdv; nptr = s.oc_n1;
+      ox = s.oc_cx2; oA = s.oc_cA2; odv = s.oc_cdv2;
+    }
+    const bool m0 = stage == 1 ? dens : true;   // stage 2: dv~ (or 1) is stored in the active set
+    if (m0) LAUNCH(ctx, k_oc_freeze<1>, nb, n, nptr, x, A, dv, s.st, ctx->prm.move, chunk, s.oc_counts, s.partials,
+                   s.counter);
+    else LAUNCH(ctx, k_oc_freeze<0>, nb, n, nptr, x, A, dv, s.st, ctx->prm.move, chunk, s.oc_counts, s.partials,
+                s.counter);
+    k_oc_scan<<<1, 32, 0, ctx->stream>>>(s.oc_counts, nb, s.oc_offs, s.st);
+    ctx->launches++;
+    if (m0) LAUNCH(ctx, k_oc_compact<1>, nb, n, nptr, x, A, dv, s.st, ctx->prm.move, chunk, s.oc_offs, ox, oA, odv);
+    else LAUNCH(ctx, k_oc_compact<0>, nb, n, nptr, x, A, dv, s.st, ctx->prm.move, chunk, s.oc_offs, ox, oA, odv);
+  }
+  return check_launch(ctx);
 }
 
 // A7: bisection, final xnew, x <- xnew, xPhys <- filter(x)
@@ -1793,20 +1841,36 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
     LAUNCH(ctx, k_oc_prep, grid_resident(k_oc_prep, (long long)s.g.nex * s.g.eplane), s.g, s.x, s.dcf, s.dvf, s.passive, s.oca);
   }
   CK(check_launch(ctx));
-  if (!ctx->debug) CK(build_oc_graph(ctx));
+  if (!ctx->debug)
+    for (int c = 0; c < 3; ++c) CK(build_oc_graph(ctx, c));
   DevState& h = *ctx->hstate;
   CK(sync_state(ctx));
   int guard = 0;
+  int compact = 0;
   while (h.oc_active) {
+    // once the bracket is narrow (l1 > 0, l2 <= 1.5 l1, then l2 <= 1.002 l1),
+    // most elements are at a clamp bound or unclamped for every remaining
+    // lambda: fold them into F + s G and compact the rest (slab 0's bracket is
+    // every slab's bracket)
+    const int want = (h.l1 > 0.0 && h.l2 <= 1.002 * h.l1) ? 2 : (h.l1 > 0.0 && h.l2 <= 1.5 * h.l1) ? 1 : 0;
+    while (compact < want) {
+      CK(oc_compact(ctx, ++compact));
+      if (getenv("TOPO_OC_VERBOSE")) {   // diagnostics
+        CK(sync_state(ctx));
+        fprintf(stderr, "[topo] OC compaction %d after %d bisection steps: %lld active elements\n", compact,
+                h.oc_pass, (long long)h.oc_nact);
+      }
+    }
     if (ctx->debug) {
-      CK(enqueue_oc_batch(ctx));
+      CK(enqueue_oc_batch(ctx, compact));
     } else {
-      CU(cudaGraphLaunch(ctx->oc_exec, ctx->stream));
+      CU(cudaGraphLaunch(compact == 2 ? ctx->oc_exec_c2 : compact == 1 ? ctx->oc_exec_c : ctx->oc_exec, ctx->stream));
       ctx->launches += ctx->oc_batch_launches;
     }
     CK(sync_state(ctx));
     if (++guard > 4096 / ctx->oc_batch) return set_err(ctx, TOPO_EBISECT, "OC bisection did not terminate");
   }
+  if (getenv("TOPO_OC_VERBOSE")) fprintf(stderr, "[topo] OC done after %d passes (%d batches)\n", h.oc_pass, guard);
   for (Slab& s : ctx->slabs)
     LAUNCH(ctx, k_oc_final, grid_resident(k_oc_final, (long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.xnew,
            s.partials, s.counter);
@@ -1870,6 +1934,18 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   CK(al((void**)&s.partials, sizeof(double) * 8 * nbmax));
   CK(al((void**)&s.counter, sizeof(unsigned int) * 4));
   CK(al((void**)&s.st, sizeof(DevState)));
+  CK(al((void**)&s.oc_counts, sizeof(unsigned) * kOcFreezeBlocks));
+  CK(al((void**)&s.oc_offs, sizeof(unsigned) * kOcFreezeBlocks));
+  {   // compacted OC arrays: worst case every owned element active
+    const size_t ne = sizeof(double) * (size_t)g.nex * g.eplane;
+    CK(al((void**)&s.oc_cx, ne));
+    CK(al((void**)&s.oc_cA, ne));
+    CK(al((void**)&s.oc_cdv, ne));
+    CK(al((void**)&s.oc_cx2, ne));
+    CK(al((void**)&s.oc_cA2, ne));
+    CK(al((void**)&s.oc_cdv2, ne));
+    CK(al((void**)&s.oc_n1, sizeof(long long)));
+  }
   s.stage_n = std::max((size_t)3 * (g.nown) * (g.nely + 1) * (g.nelz + 1), (size_t)g.nex * g.nely * g.nelz);
   CK(al((void**)&s.stage, sizeof(double) * s.stage_n));
   return TOPO_OK;
@@ -1881,7 +1957,8 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad, s.res32, s.pw0, s.pw0_b,
+                    s.vpad, s.res32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
+                    s.oc_cx2, s.oc_cA2, s.oc_cdv2, s.oc_n1,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
@@ -1905,6 +1982,8 @@ void free_ctx(topo_ctx* ctx) {
   for (cudaGraphExec_t g : ctx->cg_exec)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
+  if (ctx->oc_exec_c) cudaGraphExecDestroy(ctx->oc_exec_c);
+  if (ctx->oc_exec_c2) cudaGraphExecDestroy(ctx->oc_exec_c2);
   if (ctx->pe0) cudaEventDestroy(ctx->pe0);
   if (ctx->pe1) cudaEventDestroy(ctx->pe1);
   for (cudaEvent_t e : ctx->pe)
@@ -2230,6 +2309,8 @@ int topo_set_stream(topo_ctx* ctx, void* stream) {
     if (ctx->mg_setup_exec) { cudaGraphExecDestroy(ctx->mg_setup_exec); ctx->mg_setup_exec = nullptr; }
     if (ctx->mg_setup_exec_w) { cudaGraphExecDestroy(ctx->mg_setup_exec_w); ctx->mg_setup_exec_w = nullptr; }
     if (ctx->oc_exec) { cudaGraphExecDestroy(ctx->oc_exec); ctx->oc_exec = nullptr; }
+    if (ctx->oc_exec_c) { cudaGraphExecDestroy(ctx->oc_exec_c); ctx->oc_exec_c = nullptr; }
+    if (ctx->oc_exec_c2) { cudaGraphExecDestroy(ctx->oc_exec_c2); ctx->oc_exec_c2 = nullptr; }
     g_const_owner = nullptr;
   }
   return TOPO_OK;
