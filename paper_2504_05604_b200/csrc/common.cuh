@@ -60,6 +60,8 @@ struct DevState {
   int oc_active, oc_pass;
   double oc_frozen;    // OC after compaction: volume of the elements frozen at a clamp bound
   double oc_lin;       // ... sum of dv~ A over the elements unclamped for every remaining lambda
+  int oc_glo, oc_ghi;  // OC phase-1 grid search: last k with V(lmax 2^-k) <= target, first known > (0: none)
+  double oc_gvhi;      // ... V at k = oc_ghi
   long long oc_nact;   // ... and the number of active (compacted) elements
   // landing zone of per-slab partial sums (allreduced across slabs)
   double sums[8];

@@ -670,6 +670,83 @@ k_oc_pass_c(DevState* st, double move, const double* __restrict__ cx, const doub
   }
 }
 
+// ---------------------------------------------------------------------------
+// OC phase 1 in two passes.  While l1 = 0 the bisection evaluates exactly
+// lmid_k = lmax 2^-k (k = 1, 2, ...) and moves l2 down until the first k* with
+// V(lmid_k*) > target (V is monotone in lambda).  Two 7-candidate passes find
+// k* (pass A: k = 8, 16, ..., 56; pass B: the 7 k's below the first hit) and the
+// state jumps to where the sequential loop would be after k* steps: l1 =
+// lmid_k*, l2 = lmid_(k*-1), lmid = lmid_k*, k* bisection steps counted.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int oc_gk(const DevState* st, int stage, int j) {
+  return stage == 0 ? 8 * (j + 1) : st->oc_glo + 1 + j;
+}
+
+__device__ __forceinline__ void oc_gwalk(DevState* st, int stage, const double* V) {
+  int hit = -1;
+  for (int j = 0; j < kOcCand; ++j)
+    if (V[j] > st->target) { hit = j; break; }
+  if (stage == 0) {
+    st->oc_glo = hit < 0 ? 8 * kOcCand : 8 * hit;
+    st->oc_ghi = hit < 0 ? 0 : 8 * (hit + 1);
+    st->oc_gvhi = hit < 0 ? 0.0 : V[hit];
+    return;
+  }
+  int ks;
+  double vs;
+  if (hit >= 0) {
+    ks = st->oc_glo + 1 + hit;
+    vs = V[hit];
+  } else if (st->oc_ghi > 0) {
+    ks = st->oc_ghi;
+    vs = st->oc_gvhi;
+  } else {   // no crossing within k <= 63: take the 63 steps that moved l2 only
+    const int k = st->oc_glo + kOcCand;
+    st->l2 = ldexp(st->l2, -k);
+    st->lmid = st->l2;
+    st->vol = V[kOcCand - 1];
+    st->oc_pass += k;
+    return;
+  }
+  const double lmax = st->l2;
+  st->l1 = ldexp(lmax, -ks);
+  st->l2 = ks == 1 ? lmax : ldexp(lmax, -(ks - 1));
+  st->lmid = st->l1;
+  st->vol = vs;
+  st->oc_pass += ks;
+  st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > st->oc_tol) ? 1 : 0;
+}
+
+template <int MODE0>
+__global__ void __launch_bounds__(kBlock)
+k_oc_gpass(Geo g, DevState* st, int stage, double move, const double* __restrict__ x, const double* __restrict__ A,
+           const double* __restrict__ dvf, double* partials, unsigned int* counter, int finish) {
+  if (!st->oc_active) return;
+  double sc[kOcCand], vol[kOcCand];
+#pragma unroll
+  for (int k = 0; k < kOcCand; ++k) {
+    sc[k] = 1.0 / sqrt(ldexp(st->l2, -oc_gk(st, stage, k)));   // l2 = lmax during phase 1
+    vol[k] = 0.0;
+  }
+  const unsigned b0 = (unsigned)(g.H * g.eplane), e0 = (unsigned)((g.H + g.nex) * g.eplane);
+  for (unsigned i = b0 + blockIdx.x * blockDim.x + threadIdx.x; i < e0; i += gridDim.x * blockDim.x) {
+    const double xv = x[i], av = A[i], dv = MODE0 ? dvf[i] : 1.0;
+    const double lo = fmax(0.0, xv - move), hi = fmin(1.0, xv + move);
+#pragma unroll
+    for (int k = 0; k < kOcCand; ++k) vol[k] = fma(dv, fmin(hi, fmax(lo, av * sc[k])), vol[k]);
+  }
+  __shared__ double tot[kOcCand];
+  if (grid_reduce<kOcCand>(vol, partials, counter, tot) && threadIdx.x == 0) {
+    if (finish) oc_gwalk(st, stage, tot);
+    else
+      for (int k = 0; k < kOcCand; ++k) st->sums[k] = tot[k];
+  }
+}
+__global__ void k_oc_gfinish(DevState* st, int stage) {
+  if (!st->oc_active) return;
+  oc_gwalk(st, stage, st->sums);
+}
+
 __global__ void k_oc_finish(DevState* st) {
   if (!st->oc_active) return;
   oc_walk(st, st->sums);
@@ -836,6 +913,8 @@ __global__ void k_oc_init(DevState* st, double lmax, double target, double tol) 
   st->oc_frozen = 0.0;
   st->oc_lin = 0.0;
   st->oc_nact = 0;
+  st->oc_glo = st->oc_ghi = 0;
+  st->oc_gvhi = 0.0;
   st->oc_active = ((st->l2 - st->l1) / (st->l1 + st->l2) > tol) ? 1 : 0;
   st->lmid = 0.5 * (st->l2 + st->l1);
 }

@@ -1843,16 +1843,34 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   CK(check_launch(ctx));
   if (!ctx->debug)
     for (int c = 0; c < 3; ++c) CK(build_oc_graph(ctx, c));
+  // phase 1 (l1 = 0) in two grid passes (k_oc_gpass): the same decisions as the
+  // sequential loop, which halves l2 from oc_lmax until V(lmid) > target
+  {
+    const int W = ctx->world, fin = (W == 1) ? 1 : 0;
+    const bool dens = P.filter_mode == TOPO_FILTER_DENSITY;
+    for (int stage = 0; stage < 2; ++stage) {
+      for (Slab& s : ctx->slabs) {
+        const int gr = grid_resident(k_oc_gpass<1>, (long long)s.g.nex * s.g.eplane);
+        if (dens) LAUNCH(ctx, k_oc_gpass<1>, gr, s.g, s.st, stage, P.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
+        else LAUNCH(ctx, k_oc_gpass<0>, gr, s.g, s.st, stage, P.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
+      }
+      if (!fin) {
+        CK(allreduce(ctx, 0, kOcCand, 0));
+        for (Slab& s : ctx->slabs) { k_oc_gfinish<<<1, 1, 0, ctx->stream>>>(s.st, stage); ctx->launches++; }
+      }
+    }
+    CK(check_launch(ctx));
+  }
   DevState& h = *ctx->hstate;
   CK(sync_state(ctx));
   int guard = 0;
   int compact = 0;
   while (h.oc_active) {
-    // once the bracket is narrow (l1 > 0, l2 <= 1.5 l1, then l2 <= 1.002 l1),
+    // once the bracket is narrow (l1 > 0, l2 <= 2 l1, then l2 <= 1.002 l1),
     // most elements are at a clamp bound or unclamped for every remaining
     // lambda: fold them into F + s G and compact the rest (slab 0's bracket is
     // every slab's bracket)
-    const int want = (h.l1 > 0.0 && h.l2 <= 1.002 * h.l1) ? 2 : (h.l1 > 0.0 && h.l2 <= 1.5 * h.l1) ? 1 : 0;
+    const int want = (h.l1 > 0.0 && h.l2 <= 1.002 * h.l1) ? 2 : (h.l1 > 0.0 && h.l2 <= 2.0 * h.l1) ? 1 : 0;
     while (compact < want) {
       CK(oc_compact(ctx, ++compact));
       if (getenv("TOPO_OC_VERBOSE")) {   // diagnostics
