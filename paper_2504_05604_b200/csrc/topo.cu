@@ -1123,7 +1123,8 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   // the previous design's vector afterwards (the design changes slowly, so the
   // Rayleigh quotient keeps improving)
   const double* one = ctx->mg_om + 16;
-  const int nsteps = warm ? kMgPowerStepsWarm : kMgPowerSteps;
+  static const int pw_env = getenv("TOPO_EXP_PW") ? atoi(getenv("TOPO_EXP_PW")) : 0;   // EXPERIMENT
+  const int nsteps = warm ? (pw_env > 0 ? pw_env : kMgPowerStepsWarm) : kMgPowerSteps;
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0) {
       // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
