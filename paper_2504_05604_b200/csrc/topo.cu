@@ -1055,7 +1055,9 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 }
 
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
-constexpr int kMgPowerStepsWarm = 3;   // later designs: continue from the previous design's vector
+constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
+                                       // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
+                                       // paper protocol, 2 ms less setup per design at config 4)
 
 template <typename T> T* mgp(void* p) { return static_cast<T*>(p); }
 
@@ -1123,8 +1125,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   // the previous design's vector afterwards (the design changes slowly, so the
   // Rayleigh quotient keeps improving)
   const double* one = ctx->mg_om + 16;
-  static const int pw_env = getenv("TOPO_EXP_PW") ? atoi(getenv("TOPO_EXP_PW")) : 0;   // EXPERIMENT
-  const int nsteps = warm ? (pw_env > 0 ? pw_env : kMgPowerStepsWarm) : kMgPowerSteps;
+  const int nsteps = warm ? kMgPowerStepsWarm : kMgPowerSteps;
   for (int l = 0; l < L - 1; ++l) {
     if (l == 0) {
       // v <- D^-1 (K v) fused into the matvec's pre-pass (kPre = 3, w = 1); the
