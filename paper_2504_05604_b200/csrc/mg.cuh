@@ -1048,32 +1048,38 @@ k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ d
 }
 
 // ---------------------------------------------------------------------------
-// Blocked Gauss-Jordan inverse of the coarsest matrix (column-major, n_pad =
-// multiple of kGjB, padding = identity).  Step k over the block K:
-//   P = A_KK^-1 ; R = P A_K,: (R_:,K = 0) ; C = A_:,K (C_K,: = 0)
-//   A -= C R (rank-kGjB update, cuBLAS DGEMM) ; A_:,K = -C P (DGEMM) ;
-//   A_K,: = R ; A_KK = P.
-// The scalar step (kGjB = 1) is a_kk = 1/p, a_kj = a_kj/p, a_ik = -a_ik/p,
-// a_ij -= a_ik a_kj / p; SPD needs no pivoting (pivots are Schur-complement
-// diagonals).
+// Coarsest dense inverse (column-major, n_pad = multiple of kGjB, padding =
+// identity) by a blocked symmetric sweep (below); SPD needs no pivoting (the
+// pivot blocks are Schur-complement blocks).
 // ---------------------------------------------------------------------------
 constexpr int kGjB = 64;
 
-// P = inverse of the b x b diagonal block at (k0, k0) by scalar Gauss-Jordan in
-// one CTA of b*b/4 threads: thread (i, j4) keeps a_{i, j4 + 16 m} (m < 4, b = 64)
-// in registers; per pivot the pivot column and row go through shared memory
-// (two barriers per step, no shared-memory round trip of the whole block).
-constexpr int kGjInvNJ = 4;    // columns per thread: 1024 threads (16 was slower: more work per pivot step)
+constexpr int kGjInvNJ = 4;    // pivot-block inverse: columns per thread, 1024 threads (16 was slower)
+// ---------------------------------------------------------------------------
+// Symmetric blocked sweep (the coarsest inverse, M6): only the lower triangle
+// of S (column-major, S(i, j) at S[j ld + i], i >= j) is kept.  Sweeping the
+// pivot block K (P = S_KK^-1, C = S_:,K with rows K zero):
+//   S_ij -= C_i P C_j^T (i, j not in K; one SYRKX on the lower triangle),
+//   S_iK = C_i P, S_KK = -P.
+// After all blocks S = -A^-1; the last kernel writes the full symmetric A^-1.
+// (Half the flops of the Gauss-Jordan rank updates.)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double sym_lo(const double* S, int ld, int i, int j) {
+  return i >= j ? S[(long long)j * ld + i] : S[(long long)i * ld + j];
+}
+
+// P = S_KK^-1 from the lower triangle: Gauss-Jordan in one CTA of b*b/kGjInvNJ threads;
+// thread (i, j0) keeps s_{i, j0 + JS m} in registers, the pivot column and row go
+// through shared memory (two barriers per pivot)
 __global__ void __launch_bounds__(kGjB * kGjB / kGjInvNJ)
-k_gj_block_inv(const double* __restrict__ A, int ld, int k0, double* __restrict__ P) {
-  constexpr int NJ = kGjInvNJ, JS = kGjB / NJ;        // columns per thread, column stride
+k_sw_block_inv(const double* __restrict__ S, int ld, int k0, double* __restrict__ P) {
+  constexpr int NJ = kGjInvNJ, JS = kGjB / NJ;
   __shared__ double col[kGjB], row[kGjB];
-  const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;   // row i, columns j0 + JS m
+  const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;
   double a[NJ];
 #pragma unroll
-  for (int m = 0; m < NJ; ++m) a[m] = A[(long long)(k0 + j0 + JS * m) * ld + k0 + i];
+  for (int m = 0; m < NJ; ++m) a[m] = sym_lo(S, ld, k0 + i, k0 + j0 + JS * m);
   for (int k = 0; k < kGjB; ++k) {
-    // publish the pivot column (owners: j0 + JS m == k) and row (owner: i == k)
 #pragma unroll
     for (int m = 0; m < NJ; ++m) {
       if (j0 + JS * m == k) col[i] = a[m];
@@ -1098,35 +1104,48 @@ k_gj_block_inv(const double* __restrict__ A, int ld, int k0, double* __restrict_
   for (int m = 0; m < NJ; ++m) P[(j0 + JS * m) * kGjB + i] = a[m];
 }
 
-// C = A_:,K with rows K zeroed (n_pad x b, column-major)
+// C = S_:,K (rows K zero), read from the lower triangle (n_pad x b, column-major)
 __global__ void __launch_bounds__(kBlock)
-k_gj_take_col(const double* __restrict__ A, int ld, int k0, double* __restrict__ C) {
+k_sw_take_col(const double* __restrict__ S, int ld, int k0, double* __restrict__ C) {
   const long long tot = (long long)ld * kGjB;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t % ld), j = (int)(t / ld);
-    C[t] = (i >= k0 && i < k0 + kGjB) ? 0.0 : A[(long long)(k0 + j) * ld + i];
+    C[t] = (i >= k0 && i < k0 + kGjB) ? 0.0 : sym_lo(S, ld, i, k0 + j);
   }
 }
 
-// R_:,K = 0 (R is b x n_pad column-major)
-__global__ void k_gj_zero_rk(double* __restrict__ R, int k0) {
-  for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < kGjB * kGjB; t += gridDim.x * blockDim.x) {
-    const int i = t % kGjB, j = t / kGjB;
-    R[(long long)(k0 + j) * kGjB + i] = 0.0;
-  }
-}
-
-// A_K,: = R, then A_KK = P
+// S_iK = (C P)_i for i not in K, S_KK = -P (lower triangle)
 __global__ void __launch_bounds__(kBlock)
-k_gj_put_row(double* __restrict__ A, int ld, int k0, const double* __restrict__ R, const double* __restrict__ P) {
+k_sw_put_panel(double* __restrict__ S, int ld, int k0, const double* __restrict__ CP, const double* __restrict__ P) {
   const long long tot = (long long)ld * kGjB;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(t % kGjB), j = (int)(t / kGjB);
-    A[(long long)j * ld + k0 + i] = (j >= k0 && j < k0 + kGjB) ? P[(j - k0) * kGjB + i] : R[t];
+    const int i = (int)(t % ld), jj = (int)(t / ld), k = k0 + jj;
+    if (i >= k0 && i < k0 + kGjB) {
+      if (i >= k) S[(long long)k * ld + i] = -P[jj * kGjB + (i - k0)];
+    } else if (i > k) {
+      S[(long long)k * ld + i] = CP[t];
+    } else {
+      S[(long long)i * ld + k] = CP[t];
+    }
   }
 }
 
-// identity on the padding rows/columns [n, n_pad)
+// A^-1 = -S, full symmetric (the coarse solve reads whole rows)
+__global__ void __launch_bounds__(kBlock)
+k_sw_finish(double* __restrict__ S, int ld) {
+  const long long tot = (long long)ld * ld;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(t % ld), j = (int)(t / ld);
+    if (i > j) {
+      const double v = -S[t];
+      S[t] = v;
+      S[(long long)i * ld + j] = v;
+    } else if (i == j) {
+      S[t] = -S[t];
+    }
+  }
+}
+
 __global__ void k_gj_pad(double* __restrict__ A, int n, int ld) {
   for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < ld - n; t += gridDim.x * blockDim.x)
     A[(long long)(n + t) * ld + n + t] = 1.0;

@@ -86,6 +86,8 @@ struct CublasApi {
   int (*SetWorkspace)(cublasHandle_t, void*, size_t) = nullptr;
   int (*Dgemm)(cublasHandle_t, int, int, int, int, int, const double*, const double*, int, const double*, int,
                const double*, double*, int) = nullptr;
+  int (*Dsyrkx)(cublasHandle_t, int, int, int, int, const double*, const double*, int, const double*, int,
+                const double*, double*, int) = nullptr;   // triangular rank-k update (symmetric result)
   bool load(std::string& err) {
     if (h) return true;
     const char* cands[] = {"libcublas.so.12", "libcublas.so",
@@ -101,6 +103,7 @@ struct CublasApi {
     LD(SetStream, "cublasSetStream_v2");
     LD(SetWorkspace, "cublasSetWorkspace_v2");
     LD(Dgemm, "cublasDgemm_v2");
+    LD(Dsyrkx, "cublasDsyrkx");
 #undef LD
     return true;
   }
@@ -1194,26 +1197,23 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   CU(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)np * np, ctx->stream));
   LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, np, A);
   if (np > n) LAUNCH(ctx, k_gj_pad, 1, A, n, np);
-  // blocked Gauss-Jordan (mg.cuh): A <- A^-1 in place
+  // A <- A^-1 in place (coarsest dense inverse, reading M6)
   if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
   const double d_one = 1.0, d_mone = -1.0, d_zero = 0.0;
+  // symmetric blocked sweep (mg.cuh): lower triangle, SYRKX rank-64 updates
   for (int k0 = 0; k0 < np; k0 += kGjB) {
-    k_gj_block_inv<<<1, kGjB * kGjB / kGjInvNJ, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
+    k_sw_block_inv<<<1, kGjB * kGjB / kGjInvNJ, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
     ctx->launches++;
-    // R = P A_K,:  (b x np)
-    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, kGjB, np, kGjB, &d_one, ctx->mg_P, kGjB, A + k0, np,
-                       &d_zero, ctx->mg_R, kGjB) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (row panel) failed");
-    k_gj_zero_rk<<<64, kBlock, 0, ctx->stream>>>(ctx->mg_R, k0);
-    ctx->launches++;
-    LAUNCH(ctx, k_gj_take_col, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_C);
-    // A -= C R  (rows/columns K untouched: C_K,: = 0, R_:,K = 0)
-    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, np, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_R, kGjB,
-                       &d_one, A, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (update) failed");
-    // A_:,K = -C P
-    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, kGjB, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_P, kGjB,
-                       &d_zero, A + (size_t)k0 * np, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (column panel) failed");
-    LAUNCH(ctx, k_gj_put_row, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
+    LAUNCH(ctx, k_sw_take_col, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_C);
+    // CP = C P  (n_pad x b)
+    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, kGjB, kGjB, &d_one, ctx->mg_C, np, ctx->mg_P, kGjB,
+                       &d_zero, ctx->mg_R, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (C P) failed");
+    // S -= C (C P)^T on the lower triangle (rows / columns K untouched: C_K,: = 0)
+    if (g_cublas.Dsyrkx(ctx->cublas, 0 /* lower */, CUBLAS_OP_N_, np, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_R, np,
+                        &d_one, A, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDsyrkx failed");
+    LAUNCH(ctx, k_sw_put_panel, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
   }
+  LAUNCH(ctx, k_sw_finish, grid_for((long long)np * np), A, np);
   return check_launch(ctx);
 }
 
