@@ -367,9 +367,12 @@ def main():
         #                                                  12 (fp32 hierarchy) / 24 B/node (the
         #                                                  epilogue's second r read hits L2; z is not
         #                                                  stored: k_mg_prolong0 recomputes it)
-        #   <0,0,1> post  w = z + w D^-1 (r - K z), r.w  : read z 24 + r 24 + D^-1 8 + mask 1, write w 24 B/node
+        #   <0,0,1> post  w = z + w D^-1 (r - K z), r.w  : read z 12 (fp32 hierarchy: z stored in fp32) /
+        #                                                  24 + r 24 + D^-1 8 + mask 1, write w 24 B/node
         # each + E (8 B/el)
-        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 45 if int(p.get("mg_fp32", 1)) else 57, kt[1]), ("k_mv_wht<8,0,0,1>", 81, kt[2])]
+        f32 = int(p.get("mg_fp32", 1)) != 0
+        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 45 if f32 else 57, kt[1]),
+               ("k_mv_wht<8,0,0,1>", 69 if f32 else 81, kt[2])]
         per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
                 "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
                for n, b, t in var]

@@ -121,16 +121,22 @@ struct MvEpi {
 };
 
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
-template <int TZ> struct MvSmem {
+// TV: element type of the vin tile (double; float for the post-smoothing
+// matvec's z, which the fp32 operator rounds to float anyway).  A float box
+// row must be a multiple of 16 B (36 values) and starts at a y multiple of 4.
+template <int TZ, typename TV = double> struct MvSmem {
   static constexpr int YW = 34;                                   // 33 nodes, box width padded to 16 B
+  static constexpr int YWV = sizeof(TV) == 8 ? 34 : 36;           // vin box width
   static constexpr int V = 3 * (TZ + 1) * YW * 8;                 // bytes of one 3-component node tile
+  static constexpr int VV = 3 * (TZ + 1) * YWV * (int)sizeof(TV); // bytes of the vin tile
   static constexpr int I = (TZ + 1) * YW * 8;                     // one scalar node tile
   static constexpr int EB = TZ * YW * 8;                          // element tile (box width 34 as well)
   static constexpr int VA = (V + 127) / 128 * 128, IA = (I + 127) / 128 * 128, EA = (EB + 127) / 128 * 128;
+  static constexpr int VAV = (VV + 127) / 128 * 128;
   // stage = [vin][p_old (pre 1,2)][M^-1 (pre 1,3)][E]
-  __host__ __device__ static constexpr int ioff(int pre) { return pre == 1 ? 2 * VA : VA; }
+  __host__ __device__ static constexpr int ioff(int pre) { return pre == 1 ? VAV + VA : VAV; }
   __host__ __device__ static constexpr int eoff(int pre) {
-    return VA + (pre == 1 || pre == 2 ? VA : 0) + (pre == 1 || pre == 3 ? IA : 0);
+    return VAV + (pre == 1 || pre == 2 ? VA : 0) + (pre == 1 || pre == 3 ? IA : 0);
   }
   __host__ __device__ static constexpr int stage(int pre) { return eoff(pre) + EA; }
   // raw stages + 3 rotating p-planes (pre-pass output) + alignment slack
@@ -140,7 +146,7 @@ template <int TZ> struct MvSmem {
 // TC: arithmetic type of the element operator (double; float for the
 // multigrid smoothing matvecs with mg_fp32 -- the TMA operands stay fp64, the
 // p-planes and the Walsh-domain work are fp32, the epilogue finishes in fp64).
-template <int TZ, int kPre, bool kDot, int kEpi, typename TC>
+template <int TZ, int kPre, bool kDot, int kEpi, typename TC, typename TV = double>
 __global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? (sizeof(TC) == 4 ? 3 : 2) : 1))
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
          double* __restrict__ pnew, double* __restrict__ q,
@@ -148,7 +154,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   if (gate && st->done) return;
   constexpr bool kFused = kPre != 0;
   constexpr bool kInvd = kPre == 1 || kPre == 3;
-  using L = MvSmem<TZ>;
+  using L = MvSmem<TZ, TV>;
+  static_assert(sizeof(TV) == 8 || kPre == 0, "a float vin tile is only used by the plain pre-pass");
   const double beta = (kPre == 1 || kPre == 2) && !st->fresh ? st->beta : 0.0;
   const double wsc = (kPre == 3 || kEpi == 1) ? *scale : 1.0;
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -160,6 +167,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   const int y0 = blockIdx.x * 31, z0 = blockIdx.y * (TZ - 1);   // stored coords of the tile's (ty,tz) = (0,0)
   // TMA boxes start at an even stored y (16-byte aligned row start); yoff in {0,1}
   const int yb = y0 & ~1, yoff = y0 - yb;
+  const int ybv = sizeof(TV) == 8 ? yb : (y0 & ~3);   // vin box start (16-byte aligned)
+  constexpr int CSV = (TZ + 1) * L::YWV;              // vin tile component stride
   const int iyb = y0 - 1 + ty, izb = z0 - 1 + tz;                 // base node of this thread
   const int chunk = blockIdx.z;
   const int xend_slab = g.ex0 + g.nown;
@@ -183,10 +192,10 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     unsigned char* b = slot(s);
     const int j = xs - 1 + t;
     const int ixl = j - g.ex0 + 1;
-    const uint32_t bytes = L::V + (kPre == 1 || kPre == 2 ? L::V : 0) + (kInvd ? L::I : 0) + (t > 0 ? L::EB : 0);
+    const uint32_t bytes = L::VV + (kPre == 1 || kPre == 2 ? L::V : 0) + (kInvd ? L::I : 0) + (t > 0 ? L::EB : 0);
     mbar_arrive_expect_tx(&full[s], bytes);
-    tma_load_4d(b, &maps.vin, &full[s], yb, z0, ixl, 0);
-    if (kPre == 1 || kPre == 2) tma_load_4d(b + L::VA, &maps.pold, &full[s], yb, z0, ixl, 0);
+    tma_load_4d(b, &maps.vin, &full[s], ybv, z0, ixl, 0);
+    if (kPre == 1 || kPre == 2) tma_load_4d(b + L::VAV, &maps.pold, &full[s], yb, z0, ixl, 0);
     if (kInvd) tma_load_3d(b + L::ioff(kPre), &maps.invd, &full[s], yb, z0, ixl);
     if (t > 0) tma_load_3d(b + L::eoff(kPre), &maps.E, &full[s], yb, z0, j - 1 - g.ex0 + g.H);
   };
@@ -231,7 +240,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     const int s = t % kMvStages;
     mbar_wait(&full[s], (uint32_t)((t / kMvStages) & 1));
     const double* sv = reinterpret_cast<const double*>(slot(s));
-    const double* sp = reinterpret_cast<const double*>(slot(s) + L::VA);
+    const TV* svv = reinterpret_cast<const TV*>(slot(s));
+    const double* sp = reinterpret_cast<const double*>(slot(s) + L::VAV);
     const double* si = reinterpret_cast<const double*>(slot(s) + L::ioff(kPre));
     const double* se = reinterpret_cast<const double*>(slot(s) + L::eoff(kPre));
     TC* pb = pbuf + (t % 3) * PB;
@@ -254,9 +264,13 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         const double iv = wsc * si[n];
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = iv * sv[c * CS + n];
-      } else {
+      } else if (sizeof(TV) == 8) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];
+      } else {   // float vin tile: row stride YWV, columns shifted by yb - ybv
+        const int row = n / L::YW, nv = row * L::YWV + (n - row * L::YW) + (yb - ybv);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = (double)svv[c * CSV + nv];
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) pb[c * CS + n] = (TC)v[c];

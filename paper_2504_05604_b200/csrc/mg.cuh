@@ -219,11 +219,14 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
 // x-slabs: the fine planes [pa, pb) (global x; a slab's owned planes plus its
 // ghost planes, local plane 0 at global x0) are written; chunks start at the even
 // plane pa & ~1.  Single slab: x0 = 0, [pa, pb) = [0, nx].
-template <typename TC>
+// TZo: type of z (float with mg_fp32: the post-smoothing matvec rounds its
+// input to the fp32 operator's precision anyway, so storing z in fp32 changes
+// no result and halves its write and its TMA read).
+template <typename TC, typename TZo = double>
 __global__ void __launch_bounds__(128)
 k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, const double* __restrict__ invd,
               const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
-              double* __restrict__ z, const DevState* st, int x0, int pa, int pb) {
+              TZo* __restrict__ z, const DevState* st, int x0, int pa, int pb) {
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned ny1 = F.ny + 1;
@@ -263,8 +266,8 @@ k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, con
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      if (even_ok) z[n0 + k * F.ncomp] = ((f0 >> k) & 1) ? 0.0 : fma(omega * d0, r0[k], g0[k]);
-      if (odd_ok) z[n1 + k * F.ncomp] = ((f1 >> k) & 1) ? 0.0 : fma(omega * d1, r1[k], 0.5 * (g0[k] + g1[k]));
+      if (even_ok) z[n0 + k * F.ncomp] = (TZo)(((f0 >> k) & 1) ? 0.0 : fma(omega * d0, r0[k], g0[k]));
+      if (odd_ok) z[n1 + k * F.ncomp] = (TZo)(((f1 >> k) & 1) ? 0.0 : fma(omega * d1, r1[k], 0.5 * (g0[k] + g1[k])));
       g0[k] = g1[k];
     }
   }

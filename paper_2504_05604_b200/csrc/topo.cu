@@ -126,6 +126,7 @@ struct Slab {
   double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
   float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
+  float* z32 = nullptr;                // fp32 multigrid: prolongation output z (post-smoothing input)
   double *pw0 = nullptr, *pw0_b = nullptr;   // multigrid level-0 power vector (+ snapshot)
   // OC frozen set: per-block active counts / offsets and the compacted (x, A, dv~)
   unsigned *oc_counts = nullptr, *oc_offs = nullptr;
@@ -149,6 +150,7 @@ struct Slab {
   double *u_b = nullptr, *x_b = nullptr, *xphys_b = nullptr;   // snapshot buffers
   // TMA descriptors of the matvec operands (built at init; pointers never change)
   CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z, m_q;
+  CUtensorMap m_z32;   // fp32 z (multigrid, mg_fp32)
 };
 
 // One coarse multigrid level (l >= 1, M1-M6).
@@ -682,6 +684,19 @@ int map_nodes(topo_ctx* ctx, CUtensorMap* m, double* ptr, const Geo& g, int ncom
   return TOPO_OK;
 }
 
+// fp32 3-component node vector (the multigrid z): box rows of 36 floats (16-byte multiple)
+int map_nodes32(topo_ctx* ctx, CUtensorMap* m, float* ptr, const Geo& g) {
+  const cuuint64_t dims[4] = {(cuuint64_t)g.NY, (cuuint64_t)g.NZ, (cuuint64_t)g.NXL, 3};
+  const cuuint64_t strides[3] = {(cuuint64_t)g.NY * 4, (cuuint64_t)g.nplane * 4, (cuuint64_t)g.ncomp * 4};
+  const cuuint32_t box[4] = {36, (cuuint32_t)ctx->tz + 1, 1, 3};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, ptr, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(ctx, TOPO_ECUDA, "cuTensorMapEncodeTiled(nodes32) failed: %d", (int)r);
+  return TOPO_OK;
+}
+
 int map_elems(topo_ctx* ctx, CUtensorMap* m, double* ptr, const Geo& g) {
   const cuuint64_t dims[3] = {(cuuint64_t)g.EY, (cuuint64_t)g.EZ, (cuuint64_t)g.NEXL};
   const cuuint64_t strides[2] = {(cuuint64_t)g.EY * 8, (cuuint64_t)g.eplane * 8};
@@ -708,26 +723,27 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   return TOPO_OK;
 }
 
-template <int TZ, int kPre, bool kDot, int kEpi, typename TC>
+template <int TZ, int kPre, bool kDot, int kEpi, typename TC, typename TV = double>
 int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish,
                 const double* scale) {
   static bool attr_set = false;
-  const int smem = MvSmem<TZ>::bytes(kPre);
+  const int smem = MvSmem<TZ, TV>::bytes(kPre);
   if (!attr_set) {
-    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
   const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr};
-  k_mv_wht<TZ, kPre, kDot, kEpi, TC><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew, q,
-                                                                             s.partials, s.counter, finish, scale, epi);
+  k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew,
+                                                                                 q, s.partials, s.counter, finish,
+                                                                                 scale, epi);
   ctx->launches++;
   debug_sync(ctx, kPre == 1 ? "k_mv_wht<jacobi-fused>" : kPre == 2 ? "k_mv_wht<mg-fused>"
                   : kPre == 3 ? "k_mv_wht<mg-presmooth>" : "k_mv_wht<plain>");
   return check_launch(ctx);
 }
 
-template <int kPre, bool kDot, int kEpi = 0, typename TC = double>
+template <int kPre, bool kDot, int kEpi = 0, typename TC = double, typename TV = double>
 int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CUtensorMap* pold, double* pnew,
               double* q, int finish, const double* scale = nullptr) {
   MvMaps maps;
@@ -735,8 +751,8 @@ int launch_mv(topo_ctx* ctx, Slab& s, int gate, const CUtensorMap& vin, const CU
   maps.pold = pold ? *pold : vin;
   maps.invd = s.m_invd;
   maps.E = s.m_E;
-  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot, kEpi, TC>(ctx, s, gate, maps, pnew, q, finish, scale);
-  return launch_mv_t<8, kPre, kDot, kEpi, TC>(ctx, s, gate, maps, pnew, q, finish, scale);
+  if (ctx->tz == 16) return launch_mv_t<16, kPre, kDot, kEpi, TC, TV>(ctx, s, gate, maps, pnew, q, finish, scale);
+  return launch_mv_t<8, kPre, kDot, kEpi, TC, TV>(ctx, s, gate, maps, pnew, q, finish, scale);
 }
 
 // q = K v for every slab (v ghosts exchanged first; v must be 0 on fixed DOFs)
@@ -1022,6 +1038,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   for (Slab& s : ctx->slabs) {
     CK(al((void**)&s.pw0, sizeof(double) * 3 * s.g.ncomp));
     CK(al((void**)&s.res32, sizeof(float) * 3 * s.g.ncomp));
+    CK(al((void**)&s.z32, sizeof(float) * 3 * s.g.ncomp));
+    CK(map_nodes32(ctx, &s.m_z32, s.z32, s.g));
   }
   if (ctx->world > 1) {   // whole-grid moduli for the replicated levels >= 1
     Geo G = ctx->slabs[0].g;
@@ -1389,8 +1407,14 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
         int chunks = (int)std::max<long long>(1, std::min<long long>((np + 1) / 2, (148LL * 64 + bx - 1) / bx));
         const int cx = ((np + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
         chunks = (np + cx - 1) / cx;
-        k_mg_prolong0<T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
-                                                                    mgp<T>(n1.x), sl.fixm, sl.z, gst, sl.g.ex0, pa, pb);
+        if (sizeof(T) == 4)   // fp32 hierarchy: z in fp32 (read by the fp32-operator post-smoothing)
+          k_mg_prolong0<T, float><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
+                                                                             mgp<T>(n1.x), sl.fixm, sl.z32, gst,
+                                                                             sl.g.ex0, pa, pb);
+        else
+          k_mg_prolong0<T, double><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
+                                                                              mgp<T>(n1.x), sl.fixm, sl.z, gst,
+                                                                              sl.g.ex0, pa, pb);
         ctx->launches++;
         debug_sync(ctx, "k_mg_prolong0");
       }
@@ -1407,7 +1431,10 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // for the PCG matvec's p = w + beta p pre-pass)
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[2], ctx->stream, cudaEventRecordExternal));
     for (Slab& sl : ctx->slabs)
-      CK((launch_mv<0, false, 1, T>(ctx, sl, gate, sl.m_z, nullptr, nullptr, sl.w, slabs ? 0 : 1, om)));
+      if (nu == 1 && sizeof(T) == 4)   // z in fp32 (k_mg_prolong0<T, float>)
+        CK((launch_mv<0, false, 1, T, float>(ctx, sl, gate, sl.m_z32, nullptr, nullptr, sl.w, slabs ? 0 : 1, om)));
+      else
+        CK((launch_mv<0, false, 1, T, double>(ctx, sl, gate, sl.m_z, nullptr, nullptr, sl.w, slabs ? 0 : 1, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[3], ctx->stream, cudaEventRecordExternal));
     if (slabs) {
       CK(allreduce(ctx, 0, 1, 0));
@@ -1977,7 +2004,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad, s.res32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
+                    s.vpad, s.res32, s.z32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
                     s.oc_cx2, s.oc_cA2, s.oc_cdv2, s.oc_n1,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
