@@ -16,7 +16,7 @@ K=0
 # "regex::launch-skip" (prof_mg.py runs two designs; skip into the second one)
 for spec in "k_mv_wht<.int.8, .int.2, .bool.1, .int.0,::2" "k_mv_wht<.int.8, .int.3, .bool.0, .int.2,::2" \
             "k_mv_wht<.int.8, .int.0, .bool.0, .int.1,::2" "k_mg_l1_elem<float>::4" "k_mg_restrict0<float::2" \
-            "k_mg_prolong0<float>::2" "k_update<.bool.1, .bool.1>::2" "k_oc_pass<.int.1>::6" \
+            "k_mg_prolong0<float::2" "k_update<.bool.1, .bool.1>::2" "k_oc_pass<.int.1>::6" \
             "k_mg_sweep_st8<.bool.1, float>::40" "k_mg_asm_galerkin_t::3" "k_sw_block_inv::61" \
             "k_mg_apply_st<float>::20" "k_sens::1"; do
   re="${spec%%::*}"; skip="${spec##*::}"

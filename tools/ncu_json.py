@@ -13,7 +13,7 @@ for r in rows[2:]:
     m = re.match(r"void (\w+)<([^>]*)>", name) or re.match(r"(\w+)", name)
     args = m.group(2).replace(" ", "") if m.lastindex and m.lastindex > 1 else None
     if args is not None:   # k_mv_wht<8,3,0,2,float> -> k_mv_wht<8,3,0,2> (the element-operator type is not part of the key)
-        args = re.sub(r",(double|float)$", "", args)
+        args = re.sub(r"(,(double|float))+$", "", args)
     key = m.group(1) + ("<" + args + ">" if args is not None else "")
     if key in res:
         continue
