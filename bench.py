@@ -427,9 +427,11 @@ def main():
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_total / args.steps, "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(workload_config(args, p, world),
-                               precond="multigrid" if use_mg else "jacobi",
-                               mg_levels=[list(d) for d in mg_levels] if use_mg else None),
+                # config = the workload only (identical to the reference arm's); the
+                # solver this arm used is reported beside it
+                "config": workload_config(args, p, world),
+                "solver": {"precond": "multigrid" if use_mg else "jacobi",
+                           "mg_levels": [list(d) for d in mg_levels] if use_mg else None},
                 "matvec_gdofs": gdofs, "matvec_ms": mv_standalone_ms,
                 "cg_iters_per_step": cg_timed, "cg_iters_warmup": cg_warm,
                 "ms_per_cg_iter": [ph["ms_solve"] / max(1, n) for ph, n in zip(phase, cg_timed)],
