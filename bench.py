@@ -42,7 +42,7 @@ def load_peaks():
 
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region: ONE
-    `nvidia-smi -lms 200` process (the profiling recipe's clocks line), started
+    `nvidia-smi -lms 50` process (the profiling recipe's clocks line at 50 ms), started
     before the timed region and stopped after it.  (Spawning nvidia-smi per sample
     stalls the library's host-side batch polling and costs ~15 % at config 4.)"""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -69,7 +69,7 @@ class ClockSampler:
             return self
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                                        "--format=csv,noheader,nounits", "-lms", "200"],
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self._p = None
@@ -199,7 +199,7 @@ def run_reference(args, cfg_p, world, rank):
     v = float(np.mean(vals))
     line = {"impl": "reference", "metric": "s per SIMP iteration", "value": v,
             "unit": "s/iteration", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
+            "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, cfg_p, world),
             "cpu_baseline": {"value": v, "unit": "s/iteration", "cores": cores_used(),
@@ -211,7 +211,8 @@ def run_reference(args, cfg_p, world, rank):
 
 def workload_config(args, p, world):
     n_nd = (p["nelx"] + 1) * (p["nely"] + 1) * (p["nelz"] + 1)
-    return {"workload": f"BASELINE config {args.config}: cantilever {p['nelx']}x{p['nely']}x{p['nelz']} "
+    tag = f"{args.config}w (weak, 128 element planes per GPU)" if getattr(args, "weak", False) else f"{args.config}"
+    return {"workload": f"BASELINE config {tag}: cantilever {p['nelx']}x{p['nely']}x{p['nelz']} "
                         f"Hex8, fp64, volfrac {p['volfrac']}, rmin {p['rmin']}, PCG rtol {p['cg_rtol']}",
             "nelx": p["nelx"], "nely": p["nely"], "nelz": p["nelz"], "n_dof": 3 * n_nd,
             "filter": "density (mode 0)", "parallelism": f"x-slab{world}",
@@ -234,6 +235,8 @@ def main():
                     help="PCG preconditioner (auto: geometric multigrid where the hierarchy can be built)")
     ap.add_argument("--mg-coarse-max", type=int, default=0, help="coarsest MG level DOF bound (0 = library auto)")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling (SURVEY §8(d) config 4w): 128 x N element planes, 128x256x256 per GPU")
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")
     ap.add_argument("--mg-omega", type=float, default=None, help="MG smoother theta (default: the library's)")
     ap.add_argument("--mg-nu-deep", type=int, default=0, help="MG sweeps on the small coarse levels (0 = library auto)")
@@ -243,7 +246,8 @@ def main():
     if args.e2e_steps is None:
         args.e2e_steps = args.steps
     world, rank, local = dist_env()
-    p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max,
+    weak_over = {"nelx": 128 * world} if args.weak else {}
+    p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max, **weak_over,
                                  mg_nu=args.mg_nu, mg_nu_deep=args.mg_nu_deep,
                                  **({} if args.mg_omega is None else {"mg_omega": args.mg_omega}))
 
@@ -379,7 +383,7 @@ def main():
         tot_b = sum(v["bytes_per_launch"] for v in per)
         tot_ms = sum(v["mean_ms"] for v in per)
         achieved = tot_b / (tot_ms * 1e-3) / 1e9 if tot_ms > 0 else None
-        tr = ncu_traffic(args.config, world, [v["kernel"] for v in per])
+        tr = None if args.weak else ncu_traffic(args.config, world, [v["kernel"] for v in per])
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": tr[0] if tr else None,
                 "traffic_source": (f"profiles/{tr[1]} (ncu --set full, one launch of each variant)" if tr else None),
@@ -391,7 +395,7 @@ def main():
         # E (8 B/el); write p_new (24 B/node), q (24 B/node)  -> 105 B/node + 8 B/el
         mv_bytes = 105 * own_nd + 8 * own_el
         achieved = mv_bytes / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None
-        tr = ncu_traffic(args.config, world, ["k_mv_wht<8,1,1>"])
+        tr = None if args.weak else ncu_traffic(args.config, world, ["k_mv_wht<8,1,1>"])
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": tr[0] if tr else None,
                 "traffic_source": f"profiles/{tr[1]} (ncu --set full, one launch)" if tr else None,
@@ -426,7 +430,8 @@ def main():
         line = {"metric": "s per SIMP iteration", "value": s_per_iter, "unit": "s/iteration",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_total / args.steps, "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
                 # config = the workload only (identical to the reference arm's); the
                 # solver this arm used is reported beside it
                 "config": workload_config(args, p, world),
