@@ -74,9 +74,10 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-// Minimal cuBLAS binding (dlopen): only DGEMM, for the rank-kGjB updates of the
-// blocked Gauss-Jordan inverse of the coarsest multigrid matrix (a plain
-// library GEMM; every other step runs in this library's kernels).
+// Minimal cuBLAS binding (dlopen): DGEMM and DSYRKX (a triangular GEMM) for the
+// rank-kGjB updates of the blocked symmetric-sweep inverse of the coarsest
+// multigrid matrix and the level-2 Galerkin product (plain library GEMMs; every
+// other step runs in this library's kernels).
 typedef struct cublasContext* cublasHandle_t;
 struct CublasApi {
   void* h = nullptr;
@@ -228,7 +229,7 @@ struct topo_ctx {
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
   double* mg_Eg = nullptr;           // level-2 Galerkin: gathered fine moduli [64][nel_2] (DGEMM operand)
-  double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // blocked Gauss-Jordan scratch
+  double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // symmetric-sweep scratch (C, C P, P)
   int mg_npad = 0;                   // coarsest dense size rounded up to kGjB
   cublasHandle_t cublas = nullptr;
   double mg_diag8[8 * 24];
