@@ -730,9 +730,9 @@ template <typename T> __device__ __forceinline__ const WhtKT<T>& wht1_const();
 template <> __device__ __forceinline__ const WhtKT<double>& wht1_const<double>() { return c_wht1; }
 template <> __device__ __forceinline__ const WhtKT<float>& wht1_const<float>() { return c_wht1f; }
 
-template <typename T>
+template <typename T, typename TE = double>
 __global__ void __launch_bounds__(kL1Block, 3)
-k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const T* __restrict__ x,
+k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
              T* __restrict__ Y, const DevState* st) {
   MG_GATE(st);
   const long long nel = L.nel();
@@ -802,6 +802,14 @@ k_mg_l1_elem(Geo g, LvGeo L, const double* __restrict__ E, const T* __restrict__
       for (int k = 0; k < 8; ++k) Y[(long long)(3 * k + c) * nel + e] = Yh[c][k];
     }
   }
+}
+
+// fp32 copy of the moduli for the fp32 level-1 operator (k_mg_l1_elem<float, float>
+// reads half the bytes; (float)E is what it used anyway, so results are unchanged)
+__global__ void __launch_bounds__(kBlock)
+k_mg_e32(long long n, const double* __restrict__ E, float* __restrict__ E32) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    E32[i] = (float)E[i];
 }
 
 // phase 2: q_i = mask( sum over the <= 8 elements of i of Y[corner of i] )

@@ -245,6 +245,7 @@ struct topo_ctx {
   // mode); level 1 is formed from the whole grid's moduli, gathered per design
   Geo mg_gG{};                       // whole-grid element geometry of mg_gE
   double* mg_gE = nullptr;           // whole-grid E (W > 1; W = 1 uses slab 0's E)
+  float* mg_E32 = nullptr;           // fp32 copy of mgE for the fp32 level-1 operator
   long long mg_setup_launches = 0;
   int mg_batch = 2;
 };
@@ -1054,6 +1055,8 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     ctx->mg_gG = G;
     CK(al((void**)&ctx->mg_gE, sizeof(double) * G.nelloc));
   }
+  if (!ctx->mg[1].stored)   // fp32 moduli of the matrix-free level-1 operator
+    CK(al((void**)&ctx->mg_E32, sizeof(float) * mgG(ctx).nelloc));
   {
     std::vector<double> om(kMgScaleOff + 16, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * om.size()));
@@ -1088,8 +1091,12 @@ template <typename T>
 int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst) {
   Slab& s = ctx->slabs[0];
   const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
-  k_mg_l1_elem<T><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx), mgp<T>(m.x),
-                                                                             mgp<T>(m.Y), gst);
+  if (sizeof(T) == 4)   // fp32 moduli (k_mg_e32 at setup)
+    k_mg_l1_elem<T, float><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, ctx->mg_E32,
+                                                                                   mgp<T>(m.x), mgp<T>(m.Y), gst);
+  else
+    k_mg_l1_elem<T, double><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx),
+                                                                                    mgp<T>(m.x), mgp<T>(m.Y), gst);
   ctx->launches++;
   debug_sync(ctx, "k_mg_l1_elem");
   return check_launch(ctx);
@@ -1105,6 +1112,8 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   Slab& s = ctx->slabs[0];
   const int L = (int)ctx->mg.size();
   CK(mg_gather_E(ctx));   // x-slabs: the replicated levels see the whole grid
+  if (sizeof(T) == 4 && ctx->mg_E32)
+    LAUNCH(ctx, k_mg_e32, grid_for(mgG(ctx).nelloc), mgG(ctx).nelloc, mgE(ctx), ctx->mg_E32);
   for (int l = 1; l < L; ++l) {
     MgLevel& m = ctx->mg[l];
     const long long nn = m.L.nodes(), ne = m.L.nel();
@@ -2027,6 +2036,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->mg_setup_exec_w) cudaGraphExecDestroy(ctx->mg_setup_exec_w);
   if (ctx->cublas) g_cublas.Destroy(ctx->cublas);
   if (ctx->mg_gE) cudaFree(ctx->mg_gE);
+  if (ctx->mg_E32) cudaFree(ctx->mg_E32);
   for (cudaGraphExec_t g : ctx->cg_exec)
     if (g) cudaGraphExecDestroy(g);
   if (ctx->oc_exec) cudaGraphExecDestroy(ctx->oc_exec);
