@@ -274,7 +274,7 @@ k_dot(Geo g, DevState* st, const double* __restrict__ a, const double* __restric
 // A5  ce = u_e^T KE u_e ; dc = -p xPhys^(p-1)(E0-Emin) ce (0 on passive);
 //     partial c = sum E ce.                                     (§2.3)
 // ===========================================================================
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 3)
 k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
        const double* __restrict__ E, const double* __restrict__ xphys,
        const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
