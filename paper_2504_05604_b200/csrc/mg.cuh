@@ -949,7 +949,7 @@ k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
 //   kFused = false: dst = mask(A src)
 //   kFused = true : dst = mask(src + w D^-1 (b - A src))   (dst != src)
 template <bool kFused, typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
                const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
                T* __restrict__ dst, const DevState* st) {
