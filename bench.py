@@ -240,6 +240,7 @@ def main():
     ap.add_argument("--mg-nu", type=int, default=1, help="MG smoothing sweeps per level and side")
     ap.add_argument("--mg-omega", type=float, default=None, help="MG smoother theta (default: the library's)")
     ap.add_argument("--mg-nu-deep", type=int, default=0, help="MG sweeps on the small coarse levels (0 = library auto)")
+    ap.add_argument("--cg-check-every", type=int, default=0, help="PCG iterations per CUDA-graph batch (0 = library auto)")
     args = ap.parse_args()
 
     from workloads import make_problem
@@ -248,7 +249,7 @@ def main():
     world, rank, local = dist_env()
     weak_over = {"nelx": 128 * world} if args.weak else {}
     p, f, fx, pas = make_problem(args.config, precond=args.precond, mg_coarse_max=args.mg_coarse_max, **weak_over,
-                                 mg_nu=args.mg_nu, mg_nu_deep=args.mg_nu_deep,
+                                 mg_nu=args.mg_nu, mg_nu_deep=args.mg_nu_deep, cg_check_every=args.cg_check_every,
                                  **({} if args.mg_omega is None else {"mg_omega": args.mg_omega}))
 
     if args.impl == "reference":
