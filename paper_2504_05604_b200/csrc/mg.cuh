@@ -814,6 +814,43 @@ k_mg_e32(long long n, const double* __restrict__ E, float* __restrict__ E32) {
 
 // phase 2: q_i = mask( sum over the <= 8 elements of i of Y[corner of i] )
 // (kScale: q_i = D^-1 mask(sum), the next power step's vector)
+// level-1 damped-Jacobi sweep fused into the gather: x += w D^-1 (b - mask(A x)),
+// the same arithmetic as k_mg_l1_gather<false> followed by k_mg_jacobi<1>
+// (the sum is rounded to T as it would be stored), without the t round trip
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_mg_l1_gather_jac(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ x,
+                   const T* __restrict__ b, const T* __restrict__ invd, const double* __restrict__ omp,
+                   const DevState* st) {
+  MG_GATE(st);
+  const double omega = *omp;
+  const long long tot = L.nodes(), nel = L.nel();
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
+       k += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    T a[3] = {T(0), T(0), T(0)};
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+      const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+      const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+      if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+      const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+      const int kc = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a[c] += Y[(long long)(3 * kc + c) * nel + e];
+    }
+    const long long i = L.n(ix, iy, iz);
+    const uint8_t fm = fix[i];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long o = i + c * L.ncomp;
+      const double q = ((fm >> c) & 1) ? 0.0 : (double)a[c];
+      x[o] = ((fm >> c) & 1) ? T(0) : (T)fma(omega * (double)invd[o], (double)b[o] - q, (double)x[o]);
+    }
+  }
+}
+
 template <bool kScale, typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ q,

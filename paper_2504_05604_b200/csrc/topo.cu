@@ -1492,6 +1492,11 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
   LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
   for (int k = 1; k <= nu; ++k) {
+    if (!m.stored) {   // level 1: the sweep fused into the gather phase
+      CK(launch_l1_elem<T>(ctx, m, gst));
+      LAUNCH(ctx, k_mg_l1_gather_jac<T>, gL, m.L, mgp<T>(m.Y), m.fixm, mx, mb, mi, om, gst);
+      continue;
+    }
     CK(mg_apply<T>(ctx, l, gate));
     LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   }
