@@ -591,42 +591,6 @@ k_mg_gather64(Geo g, LvGeo L, const double* __restrict__ E, double* __restrict__
 
 // Element matrices of level l+1 from the stored level l (Galerkin per child):
 //   KC_e[3R+i][3S+j] = sum_c sum_{A,B} w[c][A][R] KF_child(c)[3A+i][3B+j] w[c][B][S]
-// Thread per (entry, coarse element), element fastest.
-__global__ void __launch_bounds__(kBlock)
-k_mg_asm_galerkin(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __restrict__ KC) {
-  const long long nelC = Cg.nel(), nelF = F.nel();
-  const long long tot = 300 * nelC;      // symmetric: upper triangle, mirrored on write
-  for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < tot;
-       id += (long long)gridDim.x * blockDim.x) {
-    const int u = (int)(id / nelC);
-    const long long e = id - (long long)u * nelC;
-    const int k = c_mg_upair[u];
-    const int r = k / 24, s = k % 24, R = r / 3, i = r % 3, Sn = s / 3, j = s % 3;
-    const int ey = (int)(e % Cg.ny);
-    const long long t = e / Cg.ny;
-    const int ez = (int)(t % Cg.nz), ex = (int)(t / Cg.nz);
-    double acc = 0.0;
-    for (int c = 0; c < 8; ++c) {
-      const int fx = 2 * ex + (c & 1), fy = 2 * ey + ((c >> 1) & 1), fz = 2 * ez + (c >> 2);
-      if (fx >= F.nx || fy >= F.ny || fz >= F.nz) continue;
-      const long long fe = ((long long)fx * F.nz + fz) * F.ny + fy;
-      const int na = c_mg_nzN[c][R], nb = c_mg_nzN[c][Sn];
-      for (int ia = 0; ia < na; ++ia) {
-        const int A = c_mg_nzA[c][R][ia];
-        const double wa = c_mg_nzW[c][R][ia];
-        double sb = 0.0;
-        for (int ib = 0; ib < nb; ++ib) {
-          const int B = c_mg_nzA[c][Sn][ib];
-          sb = fma(c_mg_nzW[c][Sn][ib], KF[(long long)((3 * A + i) * 24 + 3 * B + j) * nelF + fe], sb);
-        }
-        acc = fma(wa, sb, acc);
-      }
-    }
-    KC[(long long)k * nelC + e] = acc;
-    KC[(long long)(s * 24 + r) * nelC + e] = acc;
-  }
-}
-
 // Same product, tiled for memory efficiency: a CTA owns 8 coarse elements
 // consecutive in y (fixed ex, ez) and walks the 4 (cx, cz) child pairs; for each
 // pair the 16 fine elements (cy = 0, 1 of each coarse element, consecutive in the

@@ -857,7 +857,6 @@ LvGeo lv0(const topo_ctx* ctx) {
   const Geo& g = ctx->slabs[0].g;
   return LvGeo{g.nelx, g.nely, g.nelz, g.NY, g.nplane, g.ncomp};
 }
-const LvGeo& lvg(const topo_ctx* ctx, int l) { return ctx->mg[l].L; }
 // level 0 of slab s: its owned node planes (local plane 0 = global ex0)
 LvGeo lv_slab(const Slab& s) { return LvGeo{s.g.nown - 1, s.g.nely, s.g.nelz, s.g.NY, s.g.nplane, s.g.ncomp}; }
 // element geometry / moduli the replicated levels >= 1 are formed from
