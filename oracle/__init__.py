@@ -13,6 +13,7 @@ It follows the paper's own CPU pipeline (PAPER.md = P:line):
   sens       ce = u_e^T KE u_e, dc                   P:45-47 §2.3; S:272
   filt       cone filter H, Hs (brute force)         P:50 §2.4
   oc         OC bisection with move limits, passive  P:47 §2.3; S:282
+             void (0) / solid (1) regions            S:252, S:283 (reading R27)
   loop       top3d loop                              P:53 §2.5; S:292
   mg         geometric multigrid preconditioner      SURVEY §8(f) f2 (P:104, P:115);
              (Galerkin, damped Jacobi, V-cycle)      readings M1-M6 in DESIGN.md
@@ -30,6 +31,6 @@ from .fem import (assemble, solve, solve_direct, solve_jacobi_cg, compliance_fu,
                   element_energies, matvec_free, matvec_elementwise, matvec_rows, diag_K,
                   true_residual)
 from .filt import filter_matrix, filter_matrix_allpairs, apply_filter, filter_rows  # noqa: F401
-from .oc import oc_update, oc_xnew, sensitivities  # noqa: F401
+from .oc import oc_update, oc_xnew, sensitivities, BisectionFailure, passive_value  # noqa: F401
 from .loop import run_optimization  # noqa: F401
 from . import mg  # noqa: F401

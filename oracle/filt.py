@@ -5,7 +5,8 @@ by sparse matrix multiplication.  SPEC S:183-216.
 H_ij = max(0, rmin - ||c_i - c_j||) for ||c_i - c_j|| < rmin (R#12), centroids
 (ex+.5, ey+.5, ez+.5); Hs_i = sum_j H_ij over in-domain j (R#13, truncated at
 the boundary).  Modes (R#10, R#11):
-  0 density filter      xPhys = (H x)/Hs (passive forced 0); dc~ = H(dc/Hs); dv~ = H(dv/Hs)
+  0 density filter      xPhys = (H x)/Hs (passive forced to 0 void / 1 solid, R27);
+                        dc~ = H(dc/Hs); dv~ = H(dv/Hs)
   1 sensitivity filter  dc~_i = sum_j H_ij x_j dc_j / (Hs_i max(gamma, x_i)), gamma = 1e-3
   2 plain               dc~ = (H dc)/Hs
 """
@@ -58,8 +59,10 @@ def apply_filter(H, Hs, mode, what, v, x=None, passive=None):
         if mode != 0:
             return v.copy()
         out = (H @ v) / Hs
-        if passive is not None:
-            out[np.asarray(passive) != 0] = 0.0
+        if passive is not None:                     # R14, R27: passive value after filtering
+            P = np.asarray(passive)
+            out[P == 1] = 0.0
+            out[P == 2] = 1.0
         return out
     if mode == 0:
         return H @ (v / Hs)

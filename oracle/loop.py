@@ -2,7 +2,7 @@
 involving FEM analysis, sensitivity computation, sensitivity filtering, design
 variable update using OC"; SURVEY §8(a) A8.
 
-x0 = volfrac on D, 0 on P; xPhys0 = x0 (R#18).  Fixed n_iter (R#19).
+x0 = volfrac on D, 0 on passive void, 1 on passive solid; xPhys0 = x0 (R#18, R27).  Fixed n_iter (R#19).
 Per iteration: E(xPhys) -> K -> u -> ce, c = sum E ce -> dc, dv -> filter ->
 OC -> x, xPhys.  c_hist[it] is the compliance of the design entering it.
 """
@@ -25,7 +25,15 @@ def run_optimization(p, f, fixed, passive=None, n_iter=None, solver="auto", x0=N
     H, Hs = filter_matrix(nelx, nely, nelz, p["rmin"])
     n_el = nelx * nely * nelz
     D = np.ones(n_el, dtype=bool) if passive is None else (np.asarray(passive) == 0)
-    x = np.where(D, p["volfrac"], 0.0) if x0 is None else np.asarray(x0, dtype=np.float64).copy()
+    if x0 is None:
+        x = np.where(D, p["volfrac"], 0.0)
+        if passive is not None:
+            x[np.asarray(passive) == 2] = 1.0       # R27: passive solid holds 1
+    else:
+        x = np.asarray(x0, dtype=np.float64).copy()
+        if passive is not None:
+            x[np.asarray(passive) == 1] = 0.0
+            x[np.asarray(passive) == 2] = 1.0
     xPhys = x.copy()
     dv_f = None
     hist = dict(c=[], fu=[], change=[], lam=[], vol=[], n_oc=[])

@@ -4,13 +4,34 @@ SIMP: E_e = Emin + xPhys_e^p (E0 - Emin)                        P:45
 dc_e  = -p xPhys_e^(p-1) (E0 - Emin) ce_e on design elements, 0 on passive
 dv_e  = 1 on design elements, 0 on passive                        S:272, R#9
 OC:   xnew_j(l) = max(0, x_j - m, min(1, x_j + m, x_j sqrt(max(0, -dc~_j/(dv~_j l)))))
-      on design elements, 0 on passive; bisection on l in [0, lmax]:
+      on design elements; passive elements hold their passive value (0 void,
+      1 solid, reading R27); bisection on l in [0, lmax]:
       lmid = (l1+l2)/2; V(lmid) > volfrac |D| -> l1 = lmid else l2 = lmid;
       repeat while (l2-l1)/(l1+l2) > tol; xnew from the last lmid.   P:47; R#15-17
 Volume (mode 0): V = sum_{i in D} (H xnew / Hs)_i, computed literally.
 Volume (mode 1, 2): V = sum_{i in D} xnew_i.
+Passive mask values (R27): 0 design, 1 void (x = 0, "obstacle"),
+2 solid (x = 1, "mandatory-solid").  If the bracket's upper end never
+moves (V(lmid) > target for every lmid tried, e.g. the filtered passive-solid
+volume alone exceeds the target), the update fails with BisectionFailure.
 """
 import numpy as np
+
+VOID, SOLID = 1, 2
+
+
+class BisectionFailure(RuntimeError):
+    """the volume target cannot be met in [0, lmax]."""
+
+
+def passive_value(passive, n):
+    """Density forced on each element: NaN on design elements, 0 void, 1 solid."""
+    v = np.full(n, np.nan)
+    if passive is not None:
+        P = np.asarray(passive)
+        v[P == VOID] = 0.0
+        v[P == SOLID] = 1.0
+    return v
 
 
 def sensitivities(xPhys, ce, penal, E0, Emin, passive=None):
@@ -27,9 +48,11 @@ def sensitivities(xPhys, ce, penal, E0, Emin, passive=None):
 
 
 def oc_xnew(x, dc_f, dv_f, lmid, move, passive=None):
-    """xnew(lmid) on design elements, 0 on passive (R15-R17)."""
+    """xnew(lmid) on design elements, the passive value elsewhere (R15-R17, R27)."""
     D = np.ones(x.shape, dtype=bool) if passive is None else (np.asarray(passive) == 0)
     xs = np.zeros_like(x)
+    if passive is not None:
+        xs[np.asarray(passive) == SOLID] = 1.0
     xd, dcd, dvd = x[D], dc_f[D], dv_f[D]
     cand = xd * np.sqrt(np.maximum(0.0, -dcd / (dvd * lmid)))
     xs[D] = np.maximum(0.0, np.maximum(xd - move, np.minimum(1.0, np.minimum(xd + move, cand))))
@@ -58,4 +81,6 @@ def oc_update(x, dc_f, dv_f, volfrac, move, tol, lmax, mode, H=None, Hs=None, pa
         else:
             l2 = lmid
         n += 1
+    if n > 0 and l2 == float(lmax):
+        raise BisectionFailure(f"volume {V:.6g} > target {target:.6g} at lambda = {lmid:.6g}")
     return xnew, lmid, V, n

@@ -13,6 +13,6 @@ Numbering (external, SPEC S:45 [mesh/build_mesh]):
 """
 from .cantilever import (  # noqa: F401
     CONFIGS, COMMON, PAPER_PROTOCOL, config_params, point_load, n_nodes, n_elems, node_id, elem_id,
-    cantilever_load, cantilever_fixed, roller_patch_problem, cylinder_passive,
+    cantilever_load, cantilever_fixed, roller_patch_problem, cylinder_passive, solid_block_passive,
     random_density, random_vector, make_problem,
 )

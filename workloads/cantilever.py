@@ -116,6 +116,19 @@ def cylinder_passive(nelx, nely, nelz, cx, cy, r):
     return inside.ravel().astype(np.uint8)  # ravel order = (ez, ex, ey) = external numbering
 
 
+def solid_block_passive(nelx, nely, nelz, xr, yr, zr, base=None):
+    """Passive mask with values 0 design, 1 void, 2 solid (reading R27): elements
+    with ex in [xr), ey in [yr), ez in [zr) are passive SOLID (2); if `base` =
+    (cx, cy, r) is given, the z-cylinder of cylinder_passive is passive VOID (1)."""
+    pas = np.zeros(n_elems(nelx, nely, nelz), dtype=np.uint8)
+    if base is not None:
+        pas[cylinder_passive(nelx, nely, nelz, *base) != 0] = 1
+    ez, ex, ey = np.meshgrid(np.arange(nelz), np.arange(nelx), np.arange(nely), indexing="ij")
+    box = ((ex >= xr[0]) & (ex < xr[1]) & (ey >= yr[0]) & (ey < yr[1]) & (ez >= zr[0]) & (ez < zr[1]))
+    pas[box.ravel()] = 2
+    return pas
+
+
 def random_density(n_el, seed=0, lo=0.01, hi=1.0):
     return np.random.default_rng(seed).uniform(lo, hi, n_el)
 
