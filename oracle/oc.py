@@ -11,9 +11,13 @@ OC:   xnew_j(l) = max(0, x_j - m, min(1, x_j + m, x_j sqrt(max(0, -dc~_j/(dv~_j 
 Volume (mode 0): V = sum_{i in D} (H xnew / Hs)_i, computed literally.
 Volume (mode 1, 2): V = sum_{i in D} xnew_i.
 Passive mask values (R27): 0 design, 1 void (x = 0, "obstacle"),
-2 solid (x = 1, "mandatory-solid").  If the bracket's upper end never
-moves (V(lmid) > target for every lmid tried, e.g. the filtered passive-solid
-volume alone exceeds the target), the update fails with BisectionFailure.
+2 solid (x = 1, "mandatory-solid").  If the target is unreachable for
+every lambda even without move limits -- the volume with every design element
+at 0 and the passive values held (mode 0: the filtered passive-solid spill into
+design elements; modes 1/2: 0) already exceeds it -- the update fails with
+BisectionFailure (S:283 "e.g., passive-solid volume already exceeds the target").
+A target that only the move limits keep out of reach in this step is not a
+failure: the bisection then ends at the lower clamps (l1 -> lmax), as in top3d.
 """
 import numpy as np
 
@@ -64,6 +68,12 @@ def oc_update(x, dc_f, dv_f, volfrac, move, tol, lmax, mode, H=None, Hs=None, pa
     """Returns (xnew, lmid_last, V_last, n_passes).  Literal bisection loop."""
     D = np.ones(x.shape, dtype=bool) if passive is None else (np.asarray(passive) == 0)
     target = volfrac * float(np.count_nonzero(D))
+    if mode == 0 and passive is not None:          # S:283: volume at xnew = 0 on every design element
+        floor = np.zeros_like(x)
+        floor[np.asarray(passive) == SOLID] = 1.0
+        V0 = float(np.sum(((H @ floor) / Hs)[D]))
+        if V0 > target:
+            raise BisectionFailure(f"passive-solid volume {V0:.6g} > target {target:.6g}")
     l1, l2 = 0.0, float(lmax)
     xnew, lmid, V, n = x.copy(), None, None, 0
     while (l2 - l1) / (l1 + l2) > tol:
@@ -81,6 +91,4 @@ def oc_update(x, dc_f, dv_f, volfrac, move, tol, lmax, mode, H=None, Hs=None, pa
         else:
             l2 = lmid
         n += 1
-    if n > 0 and l2 == float(lmax):
-        raise BisectionFailure(f"volume {V:.6g} > target {target:.6g} at lambda = {lmid:.6g}")
     return xnew, lmid, V, n

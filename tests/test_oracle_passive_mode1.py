@@ -211,3 +211,22 @@ def test_loop_with_solid_block(mode):
     assert r["c"][-1] < r["c"][0]
     xp = r["xPhys"].reshape(nelz, nelx, nely)
     assert np.max(np.abs(xp - xp[::-1])) <= 1e-6
+
+
+def test_paper_obstacle_bruteforce_count():
+    """S:376 shape of the paper's section-3 obstacle: y-axis cylinder,
+    radius 0.15, normalised coordinates; count = brute-force centroid loop."""
+    from workloads import paper_obstacle, make_problem
+    nelx, nely, nelz = 32, 16, 16
+    pas = paper_obstacle(nelx, nely, nelz)
+    n = 0
+    for ez in range(nelz):
+        for ex in range(nelx):
+            for ey in range(nely):
+                xc, zc = (ex + 0.5) / nelx, (ez + 0.5) / nelz
+                inside = (xc - 0.5) ** 2 + (zc - 0.5) ** 2 < 0.15 ** 2
+                n += inside
+                assert pas[ez * nelx * nely + ex * nely + ey] == inside
+    assert n == pas.sum() == 576
+    p, f, fx, pas2 = make_problem("paper_obstacle")
+    assert np.array_equal(pas, pas2) and p["rmin"] == 4.0 and p["filter_mode"] == 1
