@@ -175,6 +175,8 @@ typedef struct {              /* last SIMP iteration (CUDA-event ms) + cumulativ
   int32_t mg_theta_cuts;      /* breakdowns answered by lowering the smoother theta by 0.2 (down
                                  to 1.2) for the rest of the run (that solve is redone)        */
   double  ms_mg_setup;        /* multigrid setup of the last solve (part of ms_solve)          */
+  int64_t host_bytes;         /* cumulative bytes of field arrays the library copied between host
+                                 and device (host-pointer calls; the _d calls add nothing)     */
 } topo_timings;
 
 /* Fill defaults: BASELINE common values (E0 1, Emin 1e-9, nu 0.3, penal 3,
@@ -183,7 +185,15 @@ void topo_params_default(topo_params *p);
 
 /* Create a context.  load: [3*n_nd] nodal forces (must be 0 on fixed DOFs).
  * fixed: [3*n_nd] 0/1 Dirichlet mask (u = 0 where 1, elimination).
- * passive: [n_el] 0/1 non-design (void) mask or NULL.
+ * passive: [n_el] non-design mask or NULL (reading R27):
+ *   0 design element; 1 passive VOID ("obstacle": x = xPhys = 0, E = Emin);
+ *   2 passive SOLID ("mandatory-solid region": x = xPhys = 1, E = E0).
+ *   Passive elements stay in the FE mesh and the filter, are excluded from the
+ *   update, from dv and from the volume (target = volfrac * #design elements);
+ *   with the density filter the solid elements' filtered spill into design
+ *   elements counts towards the design volume, so a solid region can make the
+ *   target unreachable: topo_oc_step then returns TOPO_EBISECT.
+ *   Any other value: EINVAL.
  * dist: NULL -> one GPU (current device).  Errors: EINVAL, EUNCONSTRAINED,
  * EALLPASSIVE, ENOMEM, ECUDA, ENCCL.  On error *out is NULL.              */
 int topo_init(const topo_params *p, const double *load, const uint8_t *fixed,
@@ -204,12 +214,12 @@ int topo_partition(int32_t nelx, double rmin, int32_t world, int32_t rank, int32
 /* Owned element range along x of this rank: [ex_begin, ex_end).           */
 int topo_owned_range(const topo_ctx *ctx, int32_t *ex_begin, int32_t *ex_end);
 
-/* Design variables x [n_el] (host).  NULL -> volfrac on design, 0 on passive.
- * Passive entries are forced to 0.  Sets xPhys = x (reading R#18: the first
+/* Design variables x [n_el] (host).  NULL -> volfrac on design elements.
+ * Passive entries are forced to their value (0 void, 1 solid).  Sets xPhys = x (reading R#18: the first
  * iteration is unfiltered).                                                 */
 int topo_set_density(topo_ctx *ctx, const double *x);
 
-/* Set physical densities directly (xPhys, [n_el]); passive forced to 0.    */
+/* Set physical densities directly (xPhys, [n_el]); passive forced to 0 / 1. */
 int topo_set_xphys(topo_ctx *ctx, const double *xphys);
 
 /* Solve K(xPhys) u = f on free DOFs (PCG, matrix-free; preconditioner per
@@ -233,7 +243,11 @@ int topo_filter(topo_ctx *ctx, int32_t what, const double *in, double *out);
  * xnew: [n_el] or NULL.  Scalars: final lambda (last lmid), change =
  * max |xnew - x| over design elements, volume = mean design xPhys(xnew)
  * (mode 0) / mean design xnew (modes 1, 2).  Then x <- xnew and
- * xPhys <- filter(x).  Errors: EBISECT.                                      */
+ * xPhys <- filter(x).  Errors: EBISECT when no lambda can meet the target --
+ * the volume with every design element at 0 (the filtered passive-solid
+ * spill, density filter) already exceeds it; x is then unchanged.
+ * A target that only the move limit keeps out of reach in this step is not an
+ * error: xnew ends at the lower move limits (top3d behaviour).               */
 int topo_oc_step(topo_ctx *ctx, double *xnew, double *lambda, double *change, double *volume);
 
 /* The loop: n_iter x (solve, sensitivity, filter, oc).  c_hist [n_iter]
@@ -311,6 +325,38 @@ int64_t topo_count(const topo_ctx *ctx, int32_t what);
  * broadcasts the bytes, e.g. with torch.distributed).  ENCCL if libnccl.so.2
  * cannot be loaded.                                                          */
 int topo_nccl_unique_id(uint8_t *out128);
+
+/* ---- _d variants: device pointers + CUDA stream (§4.1.3
+ * "Python API ... as a library within larger Python projects") --------------
+ * Same semantics as the host calls above, except:
+ *  - every array argument is a CUDA DEVICE pointer (on the context's device) to
+ *    the WHOLE external array (S:45 numbering, same lengths); multi-GPU
+ *    (NCCL) ranks write only their owned planes, as with host arrays;
+ *  - `stream` (a cudaStream_t as void*; NULL = the stream already bound) is
+ *    bound to the context like topo_set_stream, and all work -- including the
+ *    reads of inputs and the writes of outputs -- is ordered on it: a _d call
+ *    can return before its outputs are written (use them in stream order), and
+ *    inputs must stay valid until the stream reaches the call's work;
+ *  - no field array passes through host memory (topo_timings.host_bytes does
+ *    not grow); scalar results (c, lambda, change, volume, c_hist, solve info)
+ *    are still host outputs, because the PCG and OC drivers poll device state;
+ *  - topo_init_d copies load / fixed / passive to the host once (the partition,
+ *    multigrid hierarchy and masks are set up on the host at init).
+ * Errors: as the host calls, plus EINVAL for a pointer that is not device
+ * memory of the context's device.                                           */
+int topo_init_d(const topo_params *p, const double *load_d, const uint8_t *fixed_d,
+                const uint8_t *passive_d, const topo_dist *dist, void *stream, topo_ctx **out);
+int topo_set_density_d(topo_ctx *ctx, const double *x_d, void *stream);
+int topo_set_xphys_d(topo_ctx *ctx, const double *xphys_d, void *stream);
+int topo_solve_d(topo_ctx *ctx, double *u_d, topo_solve_info *info, void *stream);
+int topo_sensitivity_d(topo_ctx *ctx, double *c, double *ce_d, double *dc_d, void *stream);
+int topo_filter_d(topo_ctx *ctx, int32_t what, const double *in_d, double *out_d, void *stream);
+int topo_oc_step_d(topo_ctx *ctx, double *xnew_d, double *lambda, double *change, double *volume,
+                   void *stream);
+int topo_optimize_d(topo_ctx *ctx, int32_t n_iter, double change_tol, double *c_hist,
+                    double *x_out_d, int32_t *n_done, void *stream);
+int topo_apply_K_d(topo_ctx *ctx, const double *p_d, double *q_d, void *stream);
+int topo_get_d(topo_ctx *ctx, int32_t field, double *out_d, void *stream);
 
 const char *topo_last_error(const topo_ctx *ctx);
 const char *topo_strerror(int code);

@@ -68,6 +68,7 @@ struct DevState {
 };
 
 constexpr int kBlock = 256;          // threads per block of the streaming kernels
+constexpr unsigned char kVoid = 1, kSolid = 2;   // passive mask values (topo.h; reading R27)
 constexpr int kMaxGridBlocks = 148 * 16;
 
 // ---------------------------------------------------------------------------

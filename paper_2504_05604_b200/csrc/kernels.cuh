@@ -328,7 +328,7 @@ k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
 // ===========================================================================
 enum FiltMode { F_HS = 0, F_X0 = 1, F_DIV = 2, F_XDC = 3, F_PLAIN = 4 };
 //  F_HS   : out = sum H                                  (row sums Hs)
-//  F_X0   : out = (sum H a)/Hs, passive -> 0             (density filter of x)
+//  F_X0   : out = (sum H a)/Hs, passive -> 0 void, 1 solid (density filter of x; R27)
 //  F_DIV  : out = sum H (a/b)                             (H(dc/Hs), H(dv/Hs))
 //  F_XDC  : out = (sum H a b)/(Hs max(1e-3, a_i))         (sensitivity filter, a=x, b=dc)
 //  F_PLAIN: out = (sum H a)/Hs                            (plain)
@@ -361,7 +361,7 @@ k_filter(Geo g, int nst, const double* __restrict__ a, const double* __restrict_
     if (MODE == F_HS || MODE == F_DIV) r = s;
     else if (MODE == F_XDC) r = s / (hs[i] * fmax(1e-3, a[i]));
     else r = s / hs[i];
-    if (MODE == F_X0 && passive[i]) r = 0.0;
+    if (MODE == F_X0 && passive[i]) r = passive[i] == kSolid ? 1.0 : 0.0;   // R14, R27
     out[i] = r;
   }
 }
@@ -407,7 +407,7 @@ k_filt_apply(Geo g, FiltPad fp, int nst, const double* __restrict__ vpad, const 
     if (MODE == F_DIV) r = s;
     else if (MODE == F_XDC) r = s / (hs[i] * fmax(1e-3, a[i]));
     else r = s / hs[i];
-    if (MODE == F_X0 && passive[i]) r = 0.0;
+    if (MODE == F_X0 && passive[i]) r = passive[i] == kSolid ? 1.0 : 0.0;   // R14, R27
     out[i] = r;
   }
 }
@@ -474,8 +474,12 @@ k_oc_prep(Geo g, const double* __restrict__ x, const double* __restrict__ dcf, c
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
        i += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
-    const bool ok = decode_elem(g, i, ex, ey, ez) && !passive[i];
-    A[i] = ok ? x[i] * sqrt(fmax(0.0, -dcf[i] / dvf[i])) : 0.0;
+    const bool in = decode_elem(g, i, ex, ey, ez);
+    const uint8_t pv = in ? passive[i] : 0;
+    // passive solid (R27): A = +inf makes every candidate clamp(A s, lo, hi) = 1
+    // (s = 1/sqrt(lambda) > 0, hi = min(1, 1 + m) = 1), in the full, frozen and
+    // compacted passes alike; void / pads: x = A = 0 gives xnew = 0
+    A[i] = !in ? 0.0 : pv == kSolid ? (double)INFINITY : pv ? 0.0 : x[i] * sqrt(fmax(0.0, -dcf[i] / dvf[i]));
   }
 }
 
@@ -763,10 +767,10 @@ __global__ void k_oc_finish(DevState* st) {
 }
 
 // final: xnew at the last evaluated lmid, change = max |xnew - x| over design
-// elements, design-volume sum of xnew (passive elements and pads give 0).
+// elements, design-volume sum of xnew (passive elements skipped; pads give 0).
 __global__ void __launch_bounds__(kBlock)
 k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const double* __restrict__ A,
-           double* __restrict__ xnew, double* partials, unsigned int* counter) {
+           const uint8_t* __restrict__ passive, double* __restrict__ xnew, double* partials, unsigned int* counter) {
   const double lmid = st->lmid;   // the last evaluated midpoint
   const int any = st->oc_pass > 0;
   const double sc = any ? 1.0 / sqrt(lmid) : 0.0;
@@ -776,6 +780,7 @@ k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const
     const double xo = x[i];
     const double xn = any ? oc_xnew(xo, A[i], sc, move) : xo;
     xnew[i] = xn;
+    if (passive[i]) continue;   // design elements only (passive solid holds 1, R27)
     chg = fmax(chg, fabs(xn - xo));
     vsum += xn;
   }
@@ -787,16 +792,17 @@ k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const
   }
 }
 
-// sum over owned design elements of a field (volume of xPhys)
+// sum over owned elements of class `want` (0 design, kSolid ...) of a field
+// (design volume of xPhys; the passive-solid volume floor sum dv~ over solid)
 __global__ void __launch_bounds__(kBlock)
 k_design_sum(Geo g, DevState* st, const double* __restrict__ a, const uint8_t* __restrict__ passive,
-             int slot, double* partials, unsigned int* counter) {
+             int slot, double* partials, unsigned int* counter, int want = 0) {
   const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
   double s = 0.0;
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
        i += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
-    if (!decode_elem(g, i, ex, ey, ez) || passive[i]) continue;
+    if (!decode_elem(g, i, ex, ey, ez) || passive[i] != want) continue;
     s += a[i];
   }
   __shared__ double tot[1];
@@ -807,9 +813,16 @@ k_design_sum(Geo g, DevState* st, const double* __restrict__ a, const uint8_t* _
 // ---------------------------------------------------------------------------
 // Layout kernels: external (host order) <-> internal, for the owned range.
 // ---------------------------------------------------------------------------
-// nodes: ext[3*n + c] (n over owned node planes) <-> SoA internal
+// nodes: ext[3*n + c] <-> SoA internal, for the owned node planes [ix0, ix0+nix).
+// ext_global = 0: ext holds only that sub-block in external order (iz, ix, iy)
+// (host staging); 1: ext is the whole external array (S:45 numbering, device
+// pointer of a _d call) and n is the node's global external index.
+__device__ __forceinline__ long long ext_node(const Geo& g, long long k, int ixr, int iy, int iz, int ix0,
+                                              int ext_global) {
+  return ext_global ? (long long)iz * (g.nelx + 1) * (g.nely + 1) + (long long)(ix0 + ixr) * (g.nely + 1) + iy : k;
+}
 __global__ void k_nodes_in(Geo g, const double* __restrict__ ext, double* __restrict__ in, int ix0,
-                           int nix) {
+                           int nix, int ext_global) {
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -817,58 +830,62 @@ __global__ void k_nodes_in(Geo g, const double* __restrict__ ext, double* __rest
     const int iy = (int)(k % (g.nely + 1));
     const long long t = k / (g.nely + 1);
     const int ixr = (int)(t % nix), iz = (int)(t / nix);
-    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz), e = ext_node(g, k, ixr, iy, iz, ix0, ext_global);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) in[i + c * g.ncomp] = ext[3 * k + c];
+    for (int c = 0; c < 3; ++c) in[i + c * g.ncomp] = ext[3 * e + c];
   }
 }
 __global__ void k_nodes_out(Geo g, const double* __restrict__ in, double* __restrict__ ext, int ix0,
-                            int nix) {
+                            int nix, int ext_global) {
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     const int iy = (int)(k % (g.nely + 1));
     const long long t = k / (g.nely + 1);
     const int ixr = (int)(t % nix), iz = (int)(t / nix);
-    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz), e = ext_node(g, k, ixr, iy, iz, ix0, ext_global);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) ext[3 * k + c] = in[i + c * g.ncomp];
+    for (int c = 0; c < 3; ++c) ext[3 * e + c] = in[i + c * g.ncomp];
   }
 }
-// elements: ext[(ez*nex + exr)*nely + ey] for the owned x range
 // per-node scalar (Jacobi inverse diagonal) -> per-DOF external array, 0 on fixed DOFs
 __global__ void k_invd_out(Geo g, const double* __restrict__ in, const uint8_t* __restrict__ fixm,
-                           double* __restrict__ ext, int ix0, int nix) {
+                           double* __restrict__ ext, int ix0, int nix, int ext_global) {
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     const int iy = (int)(k % (g.nely + 1));
     const long long t = k / (g.nely + 1);
     const int ixr = (int)(t % nix), iz = (int)(t / nix);
-    const long long i = node_idx(g, ix0 + ixr, iy, iz);
+    const long long i = node_idx(g, ix0 + ixr, iy, iz), e = ext_node(g, k, ixr, iy, iz, ix0, ext_global);
     const uint8_t fm = fixm[i];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) ext[3 * k + c] = (fm >> c) & 1 ? 0.0 : in[i];
+    for (int c = 0; c < 3; ++c) ext[3 * e + c] = (fm >> c) & 1 ? 0.0 : in[i];
   }
 }
-__global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __restrict__ in) {
+// elements: ext[(ez*nex + exr)*nely + ey] (owned sub-block, ext_global = 0) or
+// ext[ez*nelx*nely + ex*nely + ey] (whole external array, ext_global = 1)
+__device__ __forceinline__ long long ext_elem(const Geo& g, long long k, int exr, int ey, int ez, int ext_global) {
+  return ext_global ? (long long)ez * g.nelx * g.nely + (long long)(g.ex0 + exr) * g.nely + ey : k;
+}
+__global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __restrict__ in, int ext_global) {
   const long long tot = (long long)g.nex * g.nelz * g.nely;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     const int ey = (int)(k % g.nely);
     const long long t = k / g.nely;
     const int exr = (int)(t % g.nex), ez = (int)(t / g.nex);
-    in[elem_idx(g, g.ex0 + exr, ey, ez)] = ext[k];
+    in[elem_idx(g, g.ex0 + exr, ey, ez)] = ext[ext_elem(g, k, exr, ey, ez, ext_global)];
   }
 }
-__global__ void k_elems_out(Geo g, const double* __restrict__ in, double* __restrict__ ext) {
+__global__ void k_elems_out(Geo g, const double* __restrict__ in, double* __restrict__ ext, int ext_global) {
   const long long tot = (long long)g.nex * g.nelz * g.nely;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     const int ey = (int)(k % g.nely);
     const long long t = k / g.nely;
     const int exr = (int)(t % g.nex), ez = (int)(t / g.nex);
-    ext[k] = in[elem_idx(g, g.ex0 + exr, ey, ez)];
+    ext[ext_elem(g, k, exr, ey, ez, ext_global)] = in[elem_idx(g, g.ex0 + exr, ey, ez)];
   }
 }
 
@@ -940,10 +957,16 @@ __global__ void k_mask_fixed(Geo g, const uint8_t* __restrict__ fixm, double* __
       if ((fm >> c) & 1) v[i + c * g.ncomp] = 0.0;
   }
 }
-// force passive elements to 0 over the whole local element array
+// a = v * dv over the whole local element array (x0 = volfrac on design elements)
+__global__ void k_fill_design(Geo g, const double* __restrict__ dv, double v, double* __restrict__ a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = v * dv[i];
+}
+// force passive elements to their value (0 void, 1 solid; R27) over the whole local element array
 __global__ void k_apply_passive(Geo g, const uint8_t* __restrict__ passive, double* __restrict__ a) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
        i += (long long)gridDim.x * blockDim.x)
-    if (passive[i]) a[i] = 0.0;
+    if (passive[i]) a[i] = passive[i] == kSolid ? 1.0 : 0.0;
 }
 }  // namespace topo

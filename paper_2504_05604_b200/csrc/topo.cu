@@ -189,6 +189,7 @@ struct topo_ctx {
   long long n_design = 0;   // global design-element count
   double bb = 0.0;          // ||f_free||^2
   // state flags
+  bool has_solid = false;   // some element is passive solid (mask value 2, R27)
   bool has_E = false, has_u = false, has_sens = false, has_dcf = false, has_dvf = false;
   // pinned mirror of slab 0's DevState
   DevState* hstate = nullptr;
@@ -216,6 +217,7 @@ struct topo_ctx {
   cudaEvent_t ev_setup[2] = {};   // brackets the multigrid setup of a solve
   topo_timings tim{};
   long long launches = 0;
+  long long host_bytes = 0;   // field bytes copied host <-> device by the library (host-pointer calls)
   std::string err;
   size_t dev_bytes = 0;
   bool debug = false;        // TOPO_DEBUG_SYNC=1: no graphs, sync + check after every kernel
@@ -519,7 +521,8 @@ int upload_nodes(topo_ctx* ctx, const double* host, double* Slab::*field) {
       src = tmp.data();
     }
     CU(cudaMemcpyAsync(s.stage, src, sizeof(double) * row * (nelz + 1), cudaMemcpyHostToDevice, ctx->stream));
-    LAUNCH(ctx, k_nodes_in, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.stage, s.*field, ix0, nix);
+    ctx->host_bytes += sizeof(double) * row * (nelz + 1);
+    LAUNCH(ctx, k_nodes_in, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.stage, s.*field, ix0, nix, 0);
     CK(check_launch(ctx));
     if (ctx->world > 1) CU(cudaStreamSynchronize(ctx->stream));   // tmp reuse
   }
@@ -533,8 +536,9 @@ int download_nodes(topo_ctx* ctx, double* Slab::*field, double* host) {
     int ix0, nix;
     slab_node_range(s, ix0, nix);
     const size_t row = (size_t)nix * (nely + 1) * 3;
-    LAUNCH(ctx, k_nodes_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.*field, s.stage, ix0, nix);
+    LAUNCH(ctx, k_nodes_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.*field, s.stage, ix0, nix, 0);
     CK(check_launch(ctx));
+    ctx->host_bytes += sizeof(double) * row * (nelz + 1);
     if (ctx->world == 1) {
       CU(cudaMemcpyAsync(host, s.stage, sizeof(double) * row * (nelz + 1), cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
@@ -557,8 +561,9 @@ int download_invd(topo_ctx* ctx, double* host) {
     int ix0, nix;
     slab_node_range(s, ix0, nix);
     const size_t row = (size_t)nix * (nely + 1) * 3;
-    LAUNCH(ctx, k_invd_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.invd, s.fixm, s.stage, ix0, nix);
+    LAUNCH(ctx, k_invd_out, grid_for((long long)nix * (nelz + 1) * (nely + 1)), s.g, s.invd, s.fixm, s.stage, ix0, nix, 0);
     CK(check_launch(ctx));
+    ctx->host_bytes += sizeof(double) * row * (nelz + 1);
     tmp.resize(row * (nelz + 1));
     CU(cudaMemcpyAsync(tmp.data(), s.stage, sizeof(double) * tmp.size(), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -584,7 +589,8 @@ int upload_elems(topo_ctx* ctx, const double* host, double* Slab::*field) {
       src = tmp.data();
     }
     CU(cudaMemcpyAsync(s.stage, src, sizeof(double) * row * nelz, cudaMemcpyHostToDevice, ctx->stream));
-    LAUNCH(ctx, k_elems_in, grid_for((long long)row * nelz), s.g, s.stage, s.*field);
+    ctx->host_bytes += sizeof(double) * row * nelz;
+    LAUNCH(ctx, k_elems_in, grid_for((long long)row * nelz), s.g, s.stage, s.*field, 0);
     CK(check_launch(ctx));
     if (ctx->world > 1) CU(cudaStreamSynchronize(ctx->stream));
   }
@@ -596,8 +602,9 @@ int download_elems(topo_ctx* ctx, double* Slab::*field, double* host) {
   std::vector<double> tmp;
   for (Slab& s : ctx->slabs) {
     const size_t row = (size_t)s.g.nex * nely;
-    LAUNCH(ctx, k_elems_out, grid_for((long long)row * nelz), s.g, s.*field, s.stage);
+    LAUNCH(ctx, k_elems_out, grid_for((long long)row * nelz), s.g, s.*field, s.stage, 0);
     CK(check_launch(ctx));
+    ctx->host_bytes += sizeof(double) * row * nelz;
     if (ctx->world == 1) {
       CU(cudaMemcpyAsync(host, s.stage, sizeof(double) * row * nelz, cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
@@ -610,6 +617,38 @@ int download_elems(topo_ctx* ctx, double* Slab::*field, double* host) {
     }
   }
   return TOPO_OK;
+}
+
+// Device-pointer variants (the _d calls): `dev` is the caller's WHOLE external
+// array in device memory (S:45 numbering); each slab reads / writes its owned
+// part in place on the bound stream -- no staging, no host copy, no host sync.
+int upload_nodes_dev(topo_ctx* ctx, const double* dev, double* Slab::*field) {
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_nodes_in, grid_for((long long)s.g.nown * (s.g.nelz + 1) * (s.g.nely + 1)), s.g, dev, s.*field,
+           s.g.ex0, s.g.nown, 1);
+  return check_launch(ctx);
+}
+int download_nodes_dev(topo_ctx* ctx, double* Slab::*field, double* dev) {
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_nodes_out, grid_for((long long)s.g.nown * (s.g.nelz + 1) * (s.g.nely + 1)), s.g, s.*field, dev,
+           s.g.ex0, s.g.nown, 1);
+  return check_launch(ctx);
+}
+int download_invd_dev(topo_ctx* ctx, double* dev) {
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_invd_out, grid_for((long long)s.g.nown * (s.g.nelz + 1) * (s.g.nely + 1)), s.g, s.invd, s.fixm, dev,
+           s.g.ex0, s.g.nown, 1);
+  return check_launch(ctx);
+}
+int upload_elems_dev(topo_ctx* ctx, const double* dev, double* Slab::*field) {
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_elems_in, grid_for((long long)s.g.nex * s.g.nely * s.g.nelz), s.g, dev, s.*field, 1);
+  return check_launch(ctx);
+}
+int download_elems_dev(topo_ctx* ctx, double* Slab::*field, double* dev) {
+  for (Slab& s : ctx->slabs)
+    LAUNCH(ctx, k_elems_out, grid_for((long long)s.g.nex * s.g.nely * s.g.nelz), s.g, s.*field, dev, 1);
+  return check_launch(ctx);
 }
 
 // Fill a local element array (incl. halos) from a global host array of bytes.
@@ -1797,6 +1836,11 @@ int do_filter_x(topo_ctx* ctx) {
 
 constexpr int kOcFreezeBlocks = 148 * 4;   // blocks of the freeze / compaction kernels
 
+// OC volume weights: mode 0 sums dv~_j xnew_j (R26); modes 1/2 sum xnew over design
+// elements -- unweighted passes unless passive-solid elements exist (their xnew = 1
+// must not count: then the dv = 1_D copy in dvf weights them out, R27)
+bool oc_weighted(const topo_ctx* ctx) { return ctx->prm.filter_mode == TOPO_FILTER_DENSITY || ctx->has_solid; }
+
 int enqueue_oc_batch(topo_ctx* ctx, int compact) {
   const int W = ctx->world, fin = (W == 1) ? 1 : 0;
   for (int i = 0; i < ctx->oc_batch; ++i) {
@@ -1808,7 +1852,7 @@ int enqueue_oc_batch(topo_ctx* ctx, int compact) {
         continue;
       }
       const int gr = grid_resident(k_oc_pass<1>, (long long)s.g.nex * s.g.eplane);
-      if (ctx->prm.filter_mode == TOPO_FILTER_DENSITY)
+      if (oc_weighted(ctx))
         LAUNCH(ctx, k_oc_pass<1>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
       else
         LAUNCH(ctx, k_oc_pass<0>, gr, s.g, s.st, ctx->prm.move, s.x, s.oca, s.dvf, s.partials, s.counter, fin);
@@ -1844,7 +1888,7 @@ int build_oc_graph(topo_ctx* ctx, int compact) {
 // k_oc_compact); per slab.  Stage 1 reads the element arrays, stage 2 the
 // stage-1 active set (its count stays on the device).
 int oc_compact(topo_ctx* ctx, int stage) {
-  const bool dens = ctx->prm.filter_mode == TOPO_FILTER_DENSITY;
+  const bool dens = oc_weighted(ctx);
   for (Slab& s : ctx->slabs) {
     const long long b0 = (long long)s.g.H * s.g.eplane, n = (long long)s.g.nex * s.g.eplane;
     const int nb = (int)std::max(1LL, std::min<long long>(kOcFreezeBlocks, (n + kBlock - 1) / kBlock));
@@ -1878,6 +1922,19 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   if (!ctx->has_dcf) return set_err(ctx, TOPO_ESTATE, "topo_oc_step before topo_filter(DC)");
   CK(ensure_constants(ctx));
   const topo_params& P = ctx->prm;
+  if (ctx->has_solid && P.filter_mode == TOPO_FILTER_DENSITY) {
+    // with every design element at 0 the volume is the passive-solid
+    // spill sum_{j solid} dv~_j; above the target no lambda can meet it
+    for (Slab& s : ctx->slabs)
+      LAUNCH(ctx, k_design_sum, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.st, s.dvf, s.passive, 4,
+             s.partials, s.counter, (int)kSolid);
+    CK(check_launch(ctx));
+    CK(allreduce(ctx, 4, 1, 0));
+    CK(sync_state(ctx));
+    const double v0 = ctx->hstate->sums[4], target = P.volfrac * (double)ctx->n_design;
+    if (v0 > target)
+      return set_err(ctx, TOPO_EBISECT, "OC: the passive-solid volume %.6g alone exceeds the target %.6g", v0, target);
+  }
   for (Slab& s : ctx->slabs) {
     k_oc_init<<<1, 1, 0, ctx->stream>>>(s.st, P.oc_lmax, P.volfrac * (double)ctx->n_design, P.oc_tol);
     ctx->launches++;
@@ -1890,7 +1947,7 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   // sequential loop, which halves l2 from oc_lmax until V(lmid) > target
   {
     const int W = ctx->world, fin = (W == 1) ? 1 : 0;
-    const bool dens = P.filter_mode == TOPO_FILTER_DENSITY;
+    const bool dens = oc_weighted(ctx);
     for (int stage = 0; stage < 2; ++stage) {
       for (Slab& s : ctx->slabs) {
         const int gr = grid_resident(k_oc_gpass<1>, (long long)s.g.nex * s.g.eplane);
@@ -1933,7 +1990,7 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   }
   if (getenv("TOPO_OC_VERBOSE")) fprintf(stderr, "[topo] OC done after %d passes (%d batches)\n", h.oc_pass, guard);
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_oc_final, grid_resident(k_oc_final, (long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.xnew,
+    LAUNCH(ctx, k_oc_final, grid_resident(k_oc_final, (long long)s.g.nex * s.g.eplane), s.g, s.st, P.move, s.x, s.oca, s.passive, s.xnew,
            s.partials, s.counter);
   CK(check_launch(ctx));
   CK(allreduce(ctx, 2, 2, 0x2));
@@ -1964,6 +2021,45 @@ int do_oc(topo_ctx* ctx, double* lambda, double* change, double* volume) {
   ctx->tim.oc_passes = h.oc_pass;
   ctx->has_sens = ctx->has_dcf = false;
   return TOPO_OK;
+}
+
+// A8: the SIMP loop (§2.5) -- n_iter x (modulus, solve, sensitivity, filter, OC)
+int optimize_loop(topo_ctx* ctx, int n_iter, double change_tol, double* c_hist, int32_t* n_done) {
+  if (n_done) *n_done = 0;
+  int rc = TOPO_OK;
+  for (int it = 0; it < n_iter; ++it) {
+    cudaEvent_t* ev = ctx->ev;
+    CU(cudaEventRecord(ev[0], ctx->stream));
+    CK(update_modulus(ctx));
+    CU(cudaEventRecord(ev[1], ctx->stream));
+    rc = do_solve(ctx, nullptr);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[2], ctx->stream));
+    double c = 0.0, fu = 0.0;
+    rc = do_sensitivity(ctx, &c, &fu);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[3], ctx->stream));
+    rc = do_filter_dc(ctx);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[4], ctx->stream));
+    double lam, chg, vol;
+    rc = do_oc(ctx, &lam, &chg, &vol);
+    if (rc != TOPO_OK) break;
+    CU(cudaEventRecord(ev[5], ctx->stream));
+    CU(cudaEventSynchronize(ev[5]));
+    float t[5];
+    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
+    ctx->tim.ms_efield = t[0];
+    ctx->tim.ms_solve = t[1];
+    ctx->tim.ms_sens = t[2];
+    ctx->tim.ms_filter = t[3];   // dc filter; the x filter is inside ms_oc
+    ctx->tim.ms_oc = t[4];
+    ctx->tim.ms_total = t[0] + t[1] + t[2] + t[3] + t[4];
+    if (c_hist) c_hist[it] = c;
+    if (n_done) *n_done = it + 1;
+    if (change_tol > 0 && chg < change_tol) break;
+  }
+  return rc;
 }
 
 int alloc_slab(topo_ctx* ctx, Slab& s) {
@@ -2183,7 +2279,14 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   long long nd = ne;
   if (passive) {
     nd = 0;
-    for (long long e = 0; e < ne; ++e) nd += passive[e] ? 0 : 1;
+    for (long long e = 0; e < ne; ++e) {
+      if (passive[e] > kSolid) {
+        if (rc == TOPO_OK) rc = set_err(ctx, TOPO_EINVAL, "passive[%lld] = %d (0 design, 1 void, 2 solid)", e, (int)passive[e]);
+        break;
+      }
+      nd += passive[e] ? 0 : 1;
+      if (passive[e] == kSolid) ctx->has_solid = true;
+    }
   }
   if (rc == TOPO_OK && nd == 0) rc = set_err(ctx, TOPO_EALLPASSIVE, "every element is passive");
   ctx->n_design = nd;
@@ -2311,7 +2414,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
           const long long i = elem_idx(g, ex, ey, ez);
           const bool des = !loc8[i];
           locd[i] = des ? 1.0 : 0.0;
-          locx[i] = des ? p->volfrac : 0.0;
+          locx[i] = des ? p->volfrac : loc8[i] == kSolid ? 1.0 : 0.0;   // R27
         }
     }
     if (cudaMemcpy(s.dv, locd.data(), sizeof(double) * g.nelloc, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -2385,17 +2488,12 @@ int topo_owned_range(const topo_ctx* ctx, int32_t* ex_begin, int32_t* ex_end) {
   return TOPO_OK;
 }
 
-static int set_x_common(topo_ctx* ctx, const double* x, bool also_xphys) {
+static int set_x_common(topo_ctx* ctx, const double* x, bool also_xphys, bool dev = false) {
   if (x) {
-    CK(upload_elems(ctx, x, &Slab::x));
+    CK(dev ? upload_elems_dev(ctx, x, &Slab::x) : upload_elems(ctx, x, &Slab::x));
   } else {
-    for (Slab& s : ctx->slabs) {
-      // x = volfrac * dv  (dv = 1 on design, 0 elsewhere)
-      std::vector<double> h(s.g.nelloc);
-      CU(cudaMemcpy(h.data(), s.dv, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToHost));
-      for (double& v : h) v *= ctx->prm.volfrac;
-      CU(cudaMemcpy(s.x, h.data(), sizeof(double) * s.g.nelloc, cudaMemcpyHostToDevice));
-    }
+    // x = volfrac * dv  (dv = 1 on design, 0 elsewhere)
+    for (Slab& s : ctx->slabs) LAUNCH(ctx, k_fill_design, grid_for(s.g.nelloc), s.g, s.dv, ctx->prm.volfrac, s.x);
   }
   for (Slab& s : ctx->slabs) LAUNCH(ctx, k_apply_passive, grid_for(s.g.nelloc), s.g, s.passive, s.x);
   CK(check_launch(ctx));
@@ -2491,40 +2589,7 @@ int topo_optimize(topo_ctx* ctx, int32_t n_iter, double change_tol, double* c_hi
                   int32_t* n_done) {
   if (!ctx) return TOPO_EINVAL;
   cudaSetDevice(ctx->device);
-  if (n_done) *n_done = 0;
-  int rc = TOPO_OK;
-  for (int it = 0; it < n_iter; ++it) {
-    cudaEvent_t* ev = ctx->ev;
-    CU(cudaEventRecord(ev[0], ctx->stream));
-    CK(update_modulus(ctx));
-    CU(cudaEventRecord(ev[1], ctx->stream));
-    rc = do_solve(ctx, nullptr);
-    if (rc != TOPO_OK) break;
-    CU(cudaEventRecord(ev[2], ctx->stream));
-    double c = 0.0, fu = 0.0;
-    rc = do_sensitivity(ctx, &c, &fu);
-    if (rc != TOPO_OK) break;
-    CU(cudaEventRecord(ev[3], ctx->stream));
-    rc = do_filter_dc(ctx);
-    if (rc != TOPO_OK) break;
-    CU(cudaEventRecord(ev[4], ctx->stream));
-    double lam, chg, vol;
-    rc = do_oc(ctx, &lam, &chg, &vol);
-    if (rc != TOPO_OK) break;
-    CU(cudaEventRecord(ev[5], ctx->stream));
-    CU(cudaEventSynchronize(ev[5]));
-    float t[5];
-    for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]);
-    ctx->tim.ms_efield = t[0];
-    ctx->tim.ms_solve = t[1];
-    ctx->tim.ms_sens = t[2];
-    ctx->tim.ms_filter = t[3];   // dc filter; the x filter is inside ms_oc
-    ctx->tim.ms_oc = t[4];
-    ctx->tim.ms_total = t[0] + t[1] + t[2] + t[3] + t[4];
-    if (c_hist) c_hist[it] = c;
-    if (n_done) *n_done = it + 1;
-    if (change_tol > 0 && chg < change_tol) break;
-  }
+  int rc = optimize_loop(ctx, n_iter, change_tol, c_hist, n_done);
   if (x_out) CK(download_elems(ctx, &Slab::x, x_out));
   return rc;
 }
@@ -2657,6 +2722,7 @@ int topo_get_timings(const topo_ctx* ctx, topo_timings* t) {
   if (!ctx || !t) return TOPO_EINVAL;
   *t = ctx->tim;
   t->kernel_launches = ctx->launches;
+  t->host_bytes = ctx->host_bytes;
   return TOPO_OK;
 }
 
@@ -2745,5 +2811,174 @@ int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
 }
 
 void topo_destroy(topo_ctx* ctx) { free_ctx(ctx); }
+
+// ---------------------------------------------------------------------------
+// _d variants: CUDA device pointers (whole external arrays, S:45 numbering) and
+// the caller's cudaStream_t.  Field data never passes through the host; work is
+// stream-ordered (outputs are complete in `stream` order).  Scalars (c, lambda,
+// ...) are still returned on the host: the PCG / OC drivers poll device state.
+// ---------------------------------------------------------------------------
+static int bind_stream(topo_ctx* ctx, void* stream) {
+  cudaSetDevice(ctx->device);
+  if (stream && (cudaStream_t)stream != ctx->stream) return topo_set_stream(ctx, stream);
+  return TOPO_OK;
+}
+
+static int dev_pointer_ok(topo_ctx* ctx, const void* p, const char* what) {
+  if (!p) return TOPO_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess || (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)) {
+    cudaGetLastError();
+    return set_err(ctx, TOPO_EINVAL, "%s: not a CUDA device pointer", what);
+  }
+  if (a.type == cudaMemoryTypeDevice && a.device != ctx->device)
+    return set_err(ctx, TOPO_EINVAL, "%s: device pointer of device %d, context on device %d", what, a.device, ctx->device);
+  return TOPO_OK;
+}
+#define DEVPTR(p) CK(dev_pointer_ok(ctx, (p), #p))
+
+int topo_init_d(const topo_params* p, const double* load_d, const uint8_t* fixed_d, const uint8_t* passive_d,
+                const topo_dist* dist, void* stream, topo_ctx** out) {
+  if (!out || !p || !load_d || !fixed_d) return TOPO_EINVAL;
+  *out = nullptr;
+  if (p->nelx < 1 || p->nely < 1 || p->nelz < 1) return TOPO_EINVAL;
+  // one-time problem statement: the host-side setup (partition, multigrid
+  // hierarchy, Dirichlet / passive masks) reads these once; copied here
+  const size_t nn = (size_t)(p->nelx + 1) * (p->nely + 1) * (p->nelz + 1), ne = (size_t)p->nelx * p->nely * p->nelz;
+  std::vector<double> load(3 * nn);
+  std::vector<uint8_t> fixed(3 * nn), passive(passive_d ? ne : 0);
+  if (cudaMemcpy(load.data(), load_d, sizeof(double) * 3 * nn, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(fixed.data(), fixed_d, 3 * nn, cudaMemcpyDeviceToHost) != cudaSuccess ||
+      (passive_d && cudaMemcpy(passive.data(), passive_d, ne, cudaMemcpyDeviceToHost) != cudaSuccess)) {
+    cudaGetLastError();
+    return TOPO_EINVAL;
+  }
+  int rc = topo_init(p, load.data(), fixed.data(), passive_d ? passive.data() : nullptr, dist, out);
+  if (rc == TOPO_OK && stream) rc = topo_set_stream(*out, stream);
+  return rc;
+}
+
+int topo_set_density_d(topo_ctx* ctx, const double* x_d, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(x_d);
+  return set_x_common(ctx, x_d, true, true);
+}
+
+int topo_set_xphys_d(topo_ctx* ctx, const double* xphys_d, void* stream) {
+  if (!ctx || !xphys_d) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(xphys_d);
+  CK(upload_elems_dev(ctx, xphys_d, &Slab::xphys));
+  for (Slab& s : ctx->slabs) LAUNCH(ctx, k_apply_passive, grid_for(s.g.nelloc), s.g, s.passive, s.xphys);
+  CK(check_launch(ctx));
+  CK(exchange_elems(ctx, &Slab::xphys, ctx->slabs[0].g.H));
+  ctx->has_E = false;
+  return TOPO_OK;
+}
+
+int topo_solve_d(topo_ctx* ctx, double* u_d, topo_solve_info* info, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(u_d);
+  CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  CK(update_modulus(ctx));
+  CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  int rc = do_solve(ctx, info);
+  if (u_d) CK(download_nodes_dev(ctx, &Slab::u, u_d));
+  return rc;
+}
+
+int topo_sensitivity_d(topo_ctx* ctx, double* c, double* ce_d, double* dc_d, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(ce_d);
+  DEVPTR(dc_d);
+  CK(do_sensitivity(ctx, c, nullptr));
+  if (ce_d) CK(download_elems_dev(ctx, &Slab::ce, ce_d));
+  if (dc_d) CK(download_elems_dev(ctx, &Slab::dc, dc_d));
+  return TOPO_OK;
+}
+
+int topo_filter_d(topo_ctx* ctx, int32_t what, const double* in_d, double* out_d, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(in_d);
+  DEVPTR(out_d);
+  if (what == TOPO_FILTER_DC) {
+    if (in_d) {
+      CK(upload_elems_dev(ctx, in_d, &Slab::dc));
+      ctx->has_sens = true;
+    }
+    if (!ctx->has_sens) return set_err(ctx, TOPO_ESTATE, "topo_filter_d(DC) before topo_sensitivity");
+    CK(do_filter_dc(ctx));
+    if (out_d) CK(download_elems_dev(ctx, &Slab::dcf, out_d));
+    return TOPO_OK;
+  }
+  if (what == TOPO_FILTER_X) {
+    if (in_d) CK(set_x_common(ctx, in_d, false, true));
+    CK(do_filter_x(ctx));
+    if (out_d) CK(download_elems_dev(ctx, &Slab::xphys, out_d));
+    return TOPO_OK;
+  }
+  return set_err(ctx, TOPO_EINVAL, "topo_filter_d: bad `what`");
+}
+
+int topo_oc_step_d(topo_ctx* ctx, double* xnew_d, double* lambda, double* change, double* volume, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(xnew_d);
+  CK(do_oc(ctx, lambda, change, volume));
+  if (xnew_d) CK(download_elems_dev(ctx, &Slab::x, xnew_d));
+  return TOPO_OK;
+}
+
+int topo_optimize_d(topo_ctx* ctx, int32_t n_iter, double change_tol, double* c_hist, double* x_out_d,
+                    int32_t* n_done, void* stream) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(x_out_d);
+  int rc = optimize_loop(ctx, n_iter, change_tol, c_hist, n_done);
+  if (x_out_d) CK(download_elems_dev(ctx, &Slab::x, x_out_d));
+  return rc;
+}
+
+int topo_apply_K_d(topo_ctx* ctx, const double* p_d, double* q_d, void* stream) {
+  if (!ctx || !p_d) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(p_d);
+  DEVPTR(q_d);
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));
+  CK(upload_nodes_dev(ctx, p_d, &Slab::w));
+  for (Slab& s : ctx->slabs) LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.w);
+  CK(check_launch(ctx));
+  CK(matvec_all(ctx, &Slab::w, &Slab::m_w, &Slab::q));
+  for (Slab& s : ctx->slabs) LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.q);
+  CK(check_launch(ctx));
+  if (q_d) CK(download_nodes_dev(ctx, &Slab::q, q_d));
+  return TOPO_OK;
+}
+
+int topo_get_d(topo_ctx* ctx, int32_t field, double* out_d, void* stream) {
+  if (!ctx || !out_d) return TOPO_EINVAL;
+  CK(bind_stream(ctx, stream));
+  DEVPTR(out_d);
+  switch (field) {
+    case TOPO_FIELD_U: return download_nodes_dev(ctx, &Slab::u, out_d);
+    case TOPO_FIELD_X: return download_elems_dev(ctx, &Slab::x, out_d);
+    case TOPO_FIELD_XPHYS: return download_elems_dev(ctx, &Slab::xphys, out_d);
+    case TOPO_FIELD_E: return download_elems_dev(ctx, &Slab::E, out_d);
+    case TOPO_FIELD_CE: return download_elems_dev(ctx, &Slab::ce, out_d);
+    case TOPO_FIELD_DC: return download_elems_dev(ctx, &Slab::dc, out_d);
+    case TOPO_FIELD_DCF: return download_elems_dev(ctx, &Slab::dcf, out_d);
+    case TOPO_FIELD_DVF: return download_elems_dev(ctx, &Slab::dvf, out_d);
+    case TOPO_FIELD_XNEW: return download_elems_dev(ctx, &Slab::xnew, out_d);
+    case TOPO_FIELD_HS: return download_elems_dev(ctx, &Slab::hs, out_d);
+    case TOPO_FIELD_INVDIAG: return download_invd_dev(ctx, out_d);
+    case TOPO_FIELD_R: return download_nodes_dev(ctx, &Slab::r, out_d);
+    default: return set_err(ctx, TOPO_EINVAL, "unknown field %d", field);
+  }
+}
 
 }  // extern "C"

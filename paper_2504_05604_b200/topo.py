@@ -32,7 +32,11 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            "topo_matvec_load", "topo_matvec_run", "topo_get", "topo_get_timings", "topo_profile",
            "topo_kernel_time", "topo_element_stiffness", "topo_count", "topo_last_error",
            "topo_strerror", "topo_version", "topo_destroy", "topo_nccl_unique_id", "topo_partition", "topo_snapshot", "topo_restore",
-           "topo_mg_levels", "topo_mg_apply", "topo_mg_vcycle", "topo_kernel_time_k"]
+           "topo_mg_levels", "topo_mg_apply", "topo_mg_vcycle", "topo_kernel_time_k",
+           # _d variants: device pointers + cudaStream_t
+           "topo_init_d", "topo_set_density_d", "topo_set_xphys_d", "topo_solve_d",
+           "topo_sensitivity_d", "topo_filter_d", "topo_oc_step_d", "topo_optimize_d",
+           "topo_apply_K_d", "topo_get_d"]
 
 
 class topo_params(C.Structure):
@@ -64,7 +68,8 @@ class topo_timings(C.Structure):
                 ("fu", C.c_double), ("volume", C.c_double), ("change", C.c_double),
                 ("lambda_", C.c_double), ("kernel_launches", C.c_int64),
                 ("cg_iters_total", C.c_int64), ("mg_fallbacks", C.c_int32),
-                ("mg_promotions", C.c_int32), ("mg_theta_cuts", C.c_int32), ("ms_mg_setup", C.c_double)]
+                ("mg_promotions", C.c_int32), ("mg_theta_cuts", C.c_int32), ("ms_mg_setup", C.c_double),
+                ("host_bytes", C.c_int64)]
 
 
 def _load():
@@ -110,6 +115,16 @@ def _load():
         "topo_mg_apply": (I, [ctxp, C.c_int32, D, D]),
         "topo_mg_vcycle": (I, [ctxp, D, D]),
         "topo_kernel_time_k": (I, [ctxp, C.c_int32, D, P(C.c_int64)]),
+        "topo_init_d": (I, [P(topo_params), VP, VP, VP, P(topo_dist), VP, P(ctxp)]),
+        "topo_set_density_d": (I, [ctxp, VP, VP]),
+        "topo_set_xphys_d": (I, [ctxp, VP, VP]),
+        "topo_solve_d": (I, [ctxp, VP, P(topo_solve_info), VP]),
+        "topo_sensitivity_d": (I, [ctxp, D, VP, VP, VP]),
+        "topo_filter_d": (I, [ctxp, C.c_int32, VP, VP, VP]),
+        "topo_oc_step_d": (I, [ctxp, VP, D, D, D, VP]),
+        "topo_optimize_d": (I, [ctxp, C.c_int32, C.c_double, D, VP, P(C.c_int32), VP]),
+        "topo_apply_K_d": (I, [ctxp, VP, VP, VP]),
+        "topo_get_d": (I, [ctxp, C.c_int32, VP, VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -134,6 +149,27 @@ def _dp(a):
 
 def _u8(a):
     return None if a is None else a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def _devptr(t, n, dtype="float64", what="array"):
+    """Device pointer of a CUDA tensor-like object (torch.Tensor: .data_ptr(),
+    .is_cuda, .dtype, .numel(), .is_contiguous()); None -> NULL.  Marshalling
+    only: checks that the buffer is a contiguous CUDA array of n elements."""
+    if t is None:
+        return None
+    if not getattr(t, "is_cuda", False):
+        raise TopoError(TOPO_EINVAL, f"{what}: expected a CUDA tensor")
+    if str(t.dtype).split(".")[-1] != dtype or t.numel() != n or not t.is_contiguous():
+        raise TopoError(TOPO_EINVAL, f"{what}: expected a contiguous {dtype} CUDA tensor of {n} elements, got "
+                                     f"{t.dtype} {tuple(t.shape)}")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    """cudaStream_t from a torch.cuda.Stream, an int handle or None (bound stream)."""
+    if stream is None:
+        return None
+    return C.c_void_p(int(getattr(stream, "cuda_stream", stream)))
 
 
 def element_stiffness(nu):
@@ -183,16 +219,19 @@ def make_params(p):
 class Problem:
     """One topo context.  Host arrays in external numbering (topo.h)."""
 
-    def __init__(self, params, load, fixed, passive=None, dist=None):
+    def __init__(self, params, load, fixed, passive=None, dist=None, stream=None):
+        """load/fixed/passive: host arrays (numpy), or CUDA tensors -> topo_init_d."""
         self.p = dict(params)
         self.prm = make_params(self.p)
         self.nelx, self.nely, self.nelz = self.prm.nelx, self.prm.nely, self.prm.nelz
         self.n_el = self.nelx * self.nely * self.nelz
         self.n_nd = (self.nelx + 1) * (self.nely + 1) * (self.nelz + 1)
-        load = np.ascontiguousarray(load, dtype=np.float64)
-        fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
-        passive = None if passive is None else np.ascontiguousarray(passive, dtype=np.uint8)
-        if min(self.nelx, self.nely, self.nelz) >= 1 and (
+        on_dev = getattr(load, "is_cuda", False)
+        if not on_dev:
+            load = np.ascontiguousarray(load, dtype=np.float64)
+            fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+            passive = None if passive is None else np.ascontiguousarray(passive, dtype=np.uint8)
+        if not on_dev and min(self.nelx, self.nely, self.nelz) >= 1 and (
                 load.size != 3 * self.n_nd or fixed.size != 3 * self.n_nd
                 or (passive is not None and passive.size != self.n_el)):
             raise TopoError(TOPO_EINVAL, "array sizes do not match the grid")
@@ -207,8 +246,14 @@ class Problem:
                 self._id = np.frombuffer(bytes(dist["nccl_id"]), dtype=np.uint8).copy()
                 d.nccl_id = _u8(self._id)
             dptr = C.byref(d)
-        rc = _lib.topo_init(C.byref(self.prm), _dp(load), _u8(fixed), _u8(passive), dptr,
-                            C.byref(self._ctx))
+        if on_dev:
+            rc = _lib.topo_init_d(C.byref(self.prm), _devptr(load, 3 * self.n_nd, what="load"),
+                                  _devptr(fixed, 3 * self.n_nd, "uint8", "fixed"),
+                                  _devptr(passive, self.n_el, "uint8", "passive"), dptr, _stream(stream),
+                                  C.byref(self._ctx))
+        else:
+            rc = _lib.topo_init(C.byref(self.prm), _dp(load), _u8(fixed), _u8(passive), dptr,
+                                C.byref(self._ctx))
         if rc:
             raise TopoError(rc, "topo_init")
 
@@ -365,3 +410,56 @@ class Problem:
 
     def count(self, what):
         return int(_lib.topo_count(self._ctx, COUNTS[what]))
+
+    # -- _d variants: CUDA tensors in / out (external numbering, whole arrays),
+    #    work ordered on `stream` (torch.cuda.Stream, handle or None = bound) --
+    def set_density_d(self, x=None, stream=None):
+        self._check(_lib.topo_set_density_d(self._ctx, _devptr(x, self.n_el, what="x"), _stream(stream)),
+                    "topo_set_density_d")
+
+    def set_xphys_d(self, xphys, stream=None):
+        self._check(_lib.topo_set_xphys_d(self._ctx, _devptr(xphys, self.n_el, what="xphys"), _stream(stream)),
+                    "topo_set_xphys_d")
+
+    def solve_d(self, u=None, stream=None):
+        info = topo_solve_info()
+        self._check(_lib.topo_solve_d(self._ctx, _devptr(u, 3 * self.n_nd, what="u"), C.byref(info),
+                                      _stream(stream)), "topo_solve_d")
+        return dict(iters=info.iters, rel_res=info.rel_res, true_rel_res=info.true_rel_res, ms=info.ms,
+                    replacements=info.replacements, precond={0: "jacobi", 1: "mg"}[info.precond],
+                    mg_levels=info.mg_levels)
+
+    def sensitivity_d(self, ce=None, dc=None, stream=None):
+        c = C.c_double()
+        self._check(_lib.topo_sensitivity_d(self._ctx, C.byref(c), _devptr(ce, self.n_el, what="ce"),
+                                            _devptr(dc, self.n_el, what="dc"), _stream(stream)),
+                    "topo_sensitivity_d")
+        return c.value
+
+    def filter_d(self, what, inp=None, out=None, stream=None):
+        w = TOPO_FILTER_DC if what in ("dc", TOPO_FILTER_DC) else TOPO_FILTER_X
+        self._check(_lib.topo_filter_d(self._ctx, w, _devptr(inp, self.n_el, what="in"),
+                                       _devptr(out, self.n_el, what="out"), _stream(stream)), "topo_filter_d")
+
+    def oc_step_d(self, xnew=None, stream=None):
+        lam, chg, vol = C.c_double(), C.c_double(), C.c_double()
+        self._check(_lib.topo_oc_step_d(self._ctx, _devptr(xnew, self.n_el, what="xnew"), C.byref(lam),
+                                        C.byref(chg), C.byref(vol), _stream(stream)), "topo_oc_step_d")
+        return lam.value, chg.value, vol.value
+
+    def optimize_d(self, n_iter, x_out=None, change_tol=0.0, stream=None):
+        c_hist = np.zeros(n_iter)
+        nd = C.c_int32()
+        self._check(_lib.topo_optimize_d(self._ctx, int(n_iter), float(change_tol), _dp(c_hist),
+                                         _devptr(x_out, self.n_el, what="x_out"), C.byref(nd),
+                                         _stream(stream)), "topo_optimize_d")
+        return c_hist[:nd.value], nd.value
+
+    def apply_K_d(self, p, q, stream=None):
+        self._check(_lib.topo_apply_K_d(self._ctx, _devptr(p, 3 * self.n_nd, what="p"),
+                                        _devptr(q, 3 * self.n_nd, what="q"), _stream(stream)), "topo_apply_K_d")
+
+    def get_d(self, field, out, stream=None):
+        n = 3 * self.n_nd if field in NODE_FIELDS else self.n_el
+        self._check(_lib.topo_get_d(self._ctx, FIELDS[field], _devptr(out, n, what=field), _stream(stream)),
+                    f"topo_get_d({field})")

@@ -12,7 +12,7 @@ Numbering (external, SPEC S:45 [mesh/build_mesh]):
   DOFs of node n: 3n, 3n+1, 3n+2 = (ux, uy, uz)
 """
 from .cantilever import (  # noqa: F401
-    CONFIGS, COMMON, PAPER_PROTOCOL, config_params, point_load, n_nodes, n_elems, node_id, elem_id,
+    CONFIGS, COMMON, PAPER_PROTOCOL, PAPER_PROTOCOL_OBSTACLE, paper_obstacle, config_params, point_load, n_nodes, n_elems, node_id, elem_id,
     cantilever_load, cantilever_fixed, roller_patch_problem, cylinder_passive, solid_block_passive,
     random_density, random_vector, make_problem,
 )

@@ -35,6 +35,8 @@ CONFIGS = {
 # solve tolerance stands in for the paper's direct solver.
 PAPER_PROTOCOL = dict(nelx=32, nely=16, nelz=16, volfrac=0.2, rmin=4.0, n_iter=200, cg_rtol=1e-10,
                       obstacle=None, filter_mode=1, load="point")
+# ... with the section-3 cylinder obstacle (paper_obstacle below)
+PAPER_PROTOCOL_OBSTACLE = dict(PAPER_PROTOCOL, obstacle="paper")
 
 
 def config_params(cfg, **over):
@@ -129,6 +131,18 @@ def solid_block_passive(nelx, nely, nelz, xr, yr, zr, base=None):
     return pas
 
 
+def paper_obstacle(nelx, nely, nelz, radius=0.15):
+    """The paper's section-3 obstacle ("A cylindrical obstacle region is
+    defined within the domain where material is disallowed"), in the shape of
+    SPEC's example: a cylinder with its axis along y through the domain
+    centre, radius 0.15 and full height, in coordinates normalised per axis to
+    [0, 1]; element passive VOID (1) iff its normalised centroid satisfies
+    (xc - 0.5)^2 + (zc - 0.5)^2 < radius^2."""
+    ez, ex, ey = np.meshgrid(np.arange(nelz), np.arange(nelx), np.arange(nely), indexing="ij")
+    xc, zc = (ex + 0.5) / nelx, (ez + 0.5) / nelz
+    return ((xc - 0.5) ** 2 + (zc - 0.5) ** 2 < radius * radius).ravel().astype(np.uint8)
+
+
 def random_density(n_el, seed=0, lo=0.01, hi=1.0):
     return np.random.default_rng(seed).uniform(lo, hi, n_el)
 
@@ -148,15 +162,20 @@ def point_load(nelx, nely, nelz):
 
 def make_problem(cfg, **over):
     """(params, f, fixed, passive-or-None) for a BASELINE config index, "paper"
-    (the paper's benchmark protocol) or a dict."""
+    (the paper's benchmark protocol), "paper_obstacle" (the same with the
+    section-3 cylinder) or a dict."""
     if cfg == "paper":
         cfg = PAPER_PROTOCOL
+    elif cfg == "paper_obstacle":
+        cfg = PAPER_PROTOCOL_OBSTACLE
     p = config_params(cfg, **over)
     nelx, nely, nelz = p["nelx"], p["nely"], p["nelz"]
     f = point_load(nelx, nely, nelz) if p.get("load") == "point" else cantilever_load(nelx, nely, nelz)
     fixed = cantilever_fixed(nelx, nely, nelz)
     passive = None
-    if p.get("obstacle"):
+    if p.get("obstacle") == "paper":
+        passive = paper_obstacle(nelx, nely, nelz)
+    elif p.get("obstacle"):
         cx, cy, r = p["obstacle"]
         passive = cylinder_passive(nelx, nely, nelz, cx, cy, r)
     return p, f, fixed, passive
