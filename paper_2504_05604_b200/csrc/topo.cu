@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "matvec_wht.cuh"
 #include "mg.cuh"
+#include "filter25.cuh"
 
 namespace topo {
 void build_element_stiffness(double nu, double* ke);  // ke_host.cpp
@@ -152,6 +153,7 @@ struct Slab {
   // TMA descriptors of the matvec operands (built at init; pointers never change)
   CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z, m_q;
   CUtensorMap m_z32;   // fp32 z (multigrid, mg_fp32)
+  CUtensorMap m_vpad;  // padded filter operand (k_filt25), box (32+2R) x (32+2R) x 1
 };
 
 // One coarse multigrid level (l >= 1, M1-M6).
@@ -186,6 +188,7 @@ struct topo_ctx {
   std::vector<double> st_w;
   std::vector<int> st_poff;   // filter offsets in the padded layout (FiltPad)
   int R = 0;
+  unsigned f25_attr_mask = 0;   // k_filt25 dynamic-smem opt-in done (bit per device x mode)
   long long n_design = 0;   // global design-element count
   double bb = 0.0;          // ||f_free||^2
   // state flags
@@ -373,6 +376,15 @@ int ensure_constants(topo_ctx* ctx) {
       ctx->st_poff[k] = (int)(ctx->st_off[k].x * fp.fplane + ctx->st_off[k].z * fp.FY + ctx->st_off[k].y);
     CU(cudaMemcpyToSymbolAsync(c_st_poff, ctx->st_poff.data(), sizeof(int) * ctx->st_poff.size(), 0,
                                cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->R >= 1 && ctx->R <= 3) {   // k_filt25 weights on the (2R+1)^3 box, [dx+R][dz+R][dy+R]
+      static double fw[343];
+      std::fill(fw, fw + 343, 0.0);
+      for (size_t k = 0; k < ctx->st_off.size(); ++k) {
+        const int4 o = ctx->st_off[k];
+        fw[((o.x + ctx->R) * 7 + (o.z + ctx->R)) * 7 + (o.y + ctx->R)] = ctx->st_w[k];
+      }
+      CU(cudaMemcpyToSymbolAsync(c_fw, fw, sizeof fw, 0, cudaMemcpyHostToDevice, ctx->stream));
+    }
     CU(cudaStreamSynchronize(ctx->stream));
   }
   g_const_owner = ctx;
@@ -761,7 +773,53 @@ int build_maps(topo_ctx* ctx, Slab& s) {
   CK(map_elems(ctx, &s.m_E, s.E, s.g));
   CK(map_nodes(ctx, &s.m_z, s.z, s.g, 3));
   CK(map_nodes(ctx, &s.m_q, s.q, s.g, 3));
+  if (ctx->R >= 1 && ctx->R <= 3) {   // k_filt25 operand: {FY, FZ, NEXL}, zero fill beyond the array
+    const cuuint64_t dims[3] = {(cuuint64_t)s.fp.FY, (cuuint64_t)s.fp.FZ, (cuuint64_t)s.g.NEXL};
+    const cuuint64_t strides[2] = {(cuuint64_t)s.fp.FY * 8, (cuuint64_t)s.fp.fplane * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)(kF25Y + 2 * ctx->R), (cuuint32_t)(kF25Z + 2 * ctx->R), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_encode(&s.m_vpad, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, s.vpad, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(ctx, TOPO_ECUDA, "cuTensorMapEncodeTiled(vpad) failed: %d", (int)r);
+  }
   return TOPO_OK;
+}
+
+// A6 apply step: the x-marching TMA stencil (k_filt25) for R = 1..3, else the
+// per-output gather (k_filt_apply).  TOPO_FILT25=0 selects the gather (A/B).
+template <int R, int MODE>
+int launch_filt25_r(topo_ctx* ctx, Slab& s, const double* a, double* out) {
+  using L = F25Smem<R>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(ctx->f25_attr_mask & (1u << (dev * 4 + MODE % 4)))) {   // opt-in per device
+    CU(cudaFuncSetAttribute(k_filt25<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    ctx->f25_attr_mask |= 1u << (dev * 4 + MODE % 4);
+  }
+  const int gy = (s.g.nely + kF25Y - 1) / kF25Y, gz = (s.g.nelz + kF25Z - 1) / kF25Z;
+  const long long tiles = (long long)gy * gz;
+  long long gx = std::max(1LL, (148LL * 6 + tiles - 1) / tiles);
+  gx = std::min<long long>(gx, std::max(1, s.g.nex / 8));   // >= 8 output planes per chunk
+  const int CX = (int)((s.g.nex + gx - 1) / gx);
+  gx = (s.g.nex + CX - 1) / CX;
+  k_filt25<R, MODE><<<dim3(gy, gz, (unsigned)gx), dim3(kF25Y, kF25Z / kF25TZ), L::BYTES, ctx->stream>>>(
+      s.m_vpad, s.g, s.fp, CX, a, s.hs, s.passive, out);
+  ctx->launches++;
+  debug_sync(ctx, "k_filt25");
+  return check_launch(ctx);
+}
+template <int MODE>
+int launch_filt_apply(topo_ctx* ctx, Slab& s, const double* a, double* out) {
+  static const bool use25 = !getenv("TOPO_FILT25") || atoi(getenv("TOPO_FILT25")) != 0;
+  if (use25) {
+    if (ctx->R == 1) return launch_filt25_r<1, MODE>(ctx, s, a, out);
+    if (ctx->R == 2) return launch_filt25_r<2, MODE>(ctx, s, a, out);
+    if (ctx->R == 3) return launch_filt25_r<3, MODE>(ctx, s, a, out);
+  }
+  LAUNCH(ctx, k_filt_apply<MODE>, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.fp, (int)ctx->st_off.size(),
+         s.vpad, a, s.hs, s.passive, out);
+  return check_launch(ctx);
 }
 
 template <int TZ, int kPre, bool kDot, int kEpi, typename TC, typename TV = double>
@@ -1783,25 +1841,24 @@ int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
 // A6 on dc: dc~ (and dv~ once)
 int do_filter_dc(topo_ctx* ctx) {
   CK(ensure_constants(ctx));
-  const int mode = ctx->prm.filter_mode, nst = (int)ctx->st_off.size();
+  const int mode = ctx->prm.filter_mode;
   CK(exchange_elems(ctx, &Slab::dc, ctx->R));
   for (Slab& s : ctx->slabs) {
-    const int gr = grid_for((long long)s.g.nex * s.g.eplane);
     const int gp = grid_for(s.g.nelloc);
     if (mode == TOPO_FILTER_DENSITY) {
       LAUNCH(ctx, k_filt_prep<F_DIV>, gp, s.g, s.fp, s.dc, s.hs, s.vpad);
-      LAUNCH(ctx, k_filt_apply<F_DIV>, gr, s.g, s.fp, nst, s.vpad, s.dc, s.hs, s.passive, s.dcf);
+      CK(launch_filt_apply<F_DIV>(ctx, s, s.dc, s.dcf));
     } else if (mode == TOPO_FILTER_SENSITIVITY) {
       LAUNCH(ctx, k_filt_prep<F_XDC>, gp, s.g, s.fp, s.x, s.dc, s.vpad);
-      LAUNCH(ctx, k_filt_apply<F_XDC>, gr, s.g, s.fp, nst, s.vpad, s.x, s.hs, s.passive, s.dcf);
+      CK(launch_filt_apply<F_XDC>(ctx, s, s.x, s.dcf));
     } else {
       LAUNCH(ctx, k_filt_prep<F_PLAIN>, gp, s.g, s.fp, s.dc, s.dc, s.vpad);
-      LAUNCH(ctx, k_filt_apply<F_PLAIN>, gr, s.g, s.fp, nst, s.vpad, s.dc, s.hs, s.passive, s.dcf);
+      CK(launch_filt_apply<F_PLAIN>(ctx, s, s.dc, s.dcf));
     }
     if (!ctx->has_dvf) {
       if (mode == TOPO_FILTER_DENSITY) {
         LAUNCH(ctx, k_filt_prep<F_DIV>, gp, s.g, s.fp, s.dv, s.hs, s.vpad);
-        LAUNCH(ctx, k_filt_apply<F_DIV>, gr, s.g, s.fp, nst, s.vpad, s.dv, s.hs, s.passive, s.dvf);
+        CK(launch_filt_apply<F_DIV>(ctx, s, s.dv, s.dvf));
       }
       else
         CU(cudaMemcpyAsync(s.dvf, s.dv, sizeof(double) * s.g.nelloc, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1821,8 +1878,7 @@ int do_filter_x(topo_ctx* ctx) {
     for (Slab& s : ctx->slabs)
     {
       LAUNCH(ctx, k_filt_prep<F_X0>, grid_for(s.g.nelloc), s.g, s.fp, s.x, s.x, s.vpad);
-      LAUNCH(ctx, k_filt_apply<F_X0>, grid_for((long long)s.g.nex * s.g.eplane), s.g, s.fp, nst, s.vpad, s.x, s.hs,
-             s.passive, s.xphys);
+      CK(launch_filt_apply<F_X0>(ctx, s, s.x, s.xphys));
     }
     CK(check_launch(ctx));
     CK(exchange_elems(ctx, &Slab::xphys, ctx->slabs[0].g.H));
@@ -2082,7 +2138,7 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   for (double** v : ev) CK(al((void**)v, eb));
   CK(al((void**)&s.passive, g.nelloc));
   s.fp.R = ctx->R;
-  s.fp.FY = g.nely + 2 * ctx->R;
+  s.fp.FY = (g.nely + 2 * ctx->R + 1) / 2 * 2;   // even: 16-byte TMA row pitch (k_filt25)
   s.fp.FZ = g.nelz + 2 * ctx->R;
   s.fp.fplane = (long long)s.fp.FY * s.fp.FZ;
   CK(al((void**)&s.vpad, sizeof(double) * g.NEXL * s.fp.fplane));
