@@ -165,11 +165,57 @@ def oracle_sample(p, n_cg, slab=8):
     t_oc = time.perf_counter() - t0
     scale = (nelx * nely * nelz) / n_el_s
     est = n_cg * (t_mv + t_vec) * scale + (t_sens + t_filt + t_oc) * scale
+    _ORACLE_REST[0] = (t_sens + t_filt + t_oc) * scale
     sample = (f"oracle on an x-slab of {sx}x{nely}x{nelz} elements ({n_el_s} el): element-loop "
               f"matvec {t_mv:.2f}s + PCG vector ops {t_vec:.2f}s, ce/dc {t_sens:.2f}s, filter "
               f"{t_filt:.2f}s, OC ({npass} passes) {t_oc:.2f}s; scaled x{scale:.0f} to the full "
               f"grid with N_cg={n_cg} PCG iterations per SIMP iteration")
     return est, sample, (t_mv + t_vec + t_sens + t_filt + t_oc)
+
+
+def oracle_sample_mg(p, n_cg, cycle="K", div=8):
+    """Algorithm-matched CPU baseline: the oracle's own MG-PCG (oracle.mg:
+    Galerkin hierarchy, damped-Jacobi V/K-cycle, flexible PCG -- the GPU arm's
+    algorithm) on the same cantilever scaled down by `div` per axis (x = volfrac),
+    timed per PCG iteration and for the per-design setup (assembly + Galerkin
+    hierarchy + coarsest Cholesky); the sensitivities, filter and OC on an
+    8-plane x-slab (oracle_sample); both extrapolated by the DOF / element counts
+    to the full grid with the GPU arm's N_cg per SIMP iteration."""
+    import oracle
+    from oracle import mg
+    from workloads import cantilever_fixed, cantilever_load
+    dims = tuple(max(2, n // div) for n in (p["nelx"], p["nely"], p["nelz"]))
+    x = np.full(int(np.prod(dims)), p["volfrac"])
+    E = p["Emin"] + x ** p["penal"] * (p["E0"] - p["Emin"])
+    KE = oracle.element_stiffness(p["nu"])
+    f, fx = cantilever_load(*dims), cantilever_fixed(*dims)
+    t0 = time.perf_counter()
+    K = oracle.assemble(*dims, KE, E)
+    _, it0 = mg.solve_mgcg(K, f, fx, dims, rtol=1e-30, max_iter=0, cycle=cycle)   # setup only
+    t_setup = time.perf_counter() - t0
+    k = 4                                    # k PCG iterations minus the (rebuilt) setup
+    t0 = time.perf_counter()
+    _, itk = mg.solve_mgcg(K, f, fx, dims, rtol=1e-30, max_iter=k, cycle=cycle)
+    t_it = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mg.solve_mgcg(K, f, fx, dims, rtol=1e-30, max_iter=0, cycle=cycle)
+    t_h = time.perf_counter() - t0
+    t_iter = max(0.0, t_it - t_h) / max(1, itk)
+    ndof_s = 3 * (dims[0] + 1) * (dims[1] + 1) * (dims[2] + 1)
+    ndof = 3 * (p["nelx"] + 1) * (p["nely"] + 1) * (p["nelz"] + 1)
+    sc = ndof / ndof_s
+    _, sample_rest, wall_rest = oracle_sample(p, 0)
+    est_rest = _ORACLE_REST[0]
+    est = (t_setup + n_cg * t_iter) * sc + est_rest
+    sample = (f"oracle MG-PCG ({cycle}-cycle, flexible PCG: the GPU arm's algorithm) on the cantilever "
+              f"scaled to {dims[0]}x{dims[1]}x{dims[2]} ({ndof_s} DOF): setup {t_setup:.2f}s, "
+              f"{t_iter:.3f}s per PCG iteration; scaled x{sc:.0f} by DOF with N_cg={n_cg} (the GPU arm's "
+              f"count); plus {sample_rest.split('; scaled')[0].replace('oracle on', 'ce/dc, filter, OC on')} "
+              f"scaled by elements -- extrapolated")
+    return est, sample, t_setup + t_it + t_h + wall_rest
+
+
+_ORACLE_REST = [0.0]
 
 
 def cores_used():
@@ -185,16 +231,17 @@ def run_reference(args, cfg_p, world, rank):
     if rank != 0:
         return
     n_cg = args.ref_ncg
-    if n_cg is None:
+    if n_cg is None:   # the GPU arm's MG-PCG count at this config (profiles/ncg_cfg<cfg>_mg.json)
         try:
-            with open(os.path.join(ROOT, "profiles", f"ncg_cfg{args.config}.json")) as fh:
+            with open(os.path.join(ROOT, "profiles", f"ncg_cfg{args.config}_mg.json")) as fh:
                 n_cg = int(json.load(fh)["cg_iters_per_simp_iteration"])
         except Exception:
-            n_cg = int(round(6.6 * cfg_p["nelx"]))
+            n_cg = 30
     vals, sample = [], ""
-    for i in range(args.warmup + args.steps):
-        est, sample, wall = oracle_sample(cfg_p, n_cg, slab=args.ref_slab)
-        if i >= args.warmup:
+    # each step is one bounded sample (~30 s); warm-up samples are skipped beyond one
+    for i in range(min(args.warmup, 1) + args.steps):
+        est, sample, wall = oracle_sample_mg(cfg_p, n_cg)
+        if i >= min(args.warmup, 1):
             vals.append(est)
     v = float(np.mean(vals))
     line = {"impl": "reference", "metric": "s per SIMP iteration", "value": v,
@@ -405,27 +452,23 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # the oracle as it stands solves large grids with Jacobi-PCG (oracle.solve,
-        # method "auto"): its iteration count is the GPU's Jacobi-PCG count
-        # (profiles/ncg_cfg<cfg>.json from a --precond jacobi run), not the MG count
-        n_cg = int(np.mean(cg_timed))
+        # algorithm-matched: the oracle's own MG-PCG with this arm's cycle, at this
+        # arm's mean PCG iteration count (Jacobi arm: the oracle's slab sample with
+        # the Jacobi-PCG count)
+        n_cg = int(round(np.mean(cg_timed)))
         if use_mg:
-            try:
-                with open(os.path.join(ROOT, "profiles", f"ncg_cfg{args.config}.json")) as fh:
-                    n_cg = int(json.load(fh)["cg_iters_per_simp_iteration"])
-            except Exception:
-                n_cg = int(round(6.6 * p["nelx"]))
-        est, sample, wall = oracle_sample(p, n_cg)
+            est, sample, wall = oracle_sample_mg(p, n_cg, cycle="K" if int(p.get("mg_cycle", 1)) else "V")
+        else:
+            est, sample, wall = oracle_sample(p, n_cg)
         cpu = {"value": est, "unit": "s/iteration", "cores": cores_used(), "kind": "oracle",
-               "sample": sample + f" (wall {wall:.1f}s; SciPy sparse kernels single-threaded; the "
-                                  f"oracle's own solver for this size is Jacobi-PCG)"}
-        if not use_mg:
-            try:
-                os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-                with open(os.path.join(ROOT, "gpurun_out", f"ncg_cfg{args.config}.json"), "w") as fh:
-                    json.dump({"cg_iters_per_simp_iteration": n_cg, "per_step": cg_timed}, fh)
-            except Exception:
-                pass
+               "sample": sample + f" (wall {wall:.1f}s; SciPy sparse kernels single-threaded)"}
+        try:
+            os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+            with open(os.path.join(ROOT, "gpurun_out", f"ncg_cfg{args.config}{'_mg' if use_mg else ''}.json"),
+                      "w") as fh:
+                json.dump({"cg_iters_per_simp_iteration": n_cg, "per_step": cg_timed}, fh)
+        except Exception:
+            pass
 
     if rank == 0:
         line = {"metric": "s per SIMP iteration", "value": s_per_iter, "unit": "s/iteration",

@@ -138,7 +138,17 @@ typedef struct {
                                  (indefinite preconditioner) promotes the hierarchy to fp64 for the
                                  rest of the run; none observed on the BASELINE configs or the
                                  paper protocol.  0: fp64 throughout                               */
+  int32_t mg_cycle;           /* TOPO_MG_KCYCLE (default): every coarse level above the coarsest is solved
+                                 by two flexible-CG steps preconditioned by its own cycle (Notay &
+                                 Vassilevski's K-cycle, reading M8), and the outer PCG uses the
+                                 flexible Polak-Ribiere beta (M9) -- near two-grid convergence on
+                                 void-rich SIMP designs, where the V-cycle's iteration count grows
+                                 with the stiffness contrast.  TOPO_MG_VCYCLE: one cycle per level,
+                                 standard PCG (round-1 behaviour).  mg_nu > 1 forces the V-cycle.    */
 } topo_params;
+
+#define TOPO_MG_VCYCLE 0
+#define TOPO_MG_KCYCLE 1
 
 #define TOPO_PRECOND_JACOBI 0
 #define TOPO_PRECOND_MG     1

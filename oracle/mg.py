@@ -32,8 +32,20 @@ M1-M6), each step in plain NumPy/SciPy, no blocking or fusion:
                  estimate 0.80-0.95 of lam_max, so theta = 1.4 keeps w lam_max <= 1.75
   M6 coarsest    exact solve (dense Cholesky) on the coarsest level; coarsening
                  stops at the first level with <= coarse_max DOFs
+  M8 cycle       V-cycle (one recursive call per coarse level), or the K-cycle of
+                 Notay & Vassilevski ("Recursive Krylov-based multigrid cycles",
+                 2008): every coarse level above the coarsest is solved by TWO
+                 flexible-CG steps preconditioned by that level's cycle (always two;
+                 no residual-ratio threshold), written out in coarse_correction
+  M9 outer       PCG with z = V(r); with a K-cycle (a nonlinear preconditioner) the
+                 flexible (Polak-Ribiere) beta = z_new.(r_new - r_old) / (z_old.r_old)
+                 = -alpha (z_new.q) / rz, q = A p (Notay's FCG(1))
 The outer Krylov method is the same PCG as solve_jacobi_cg (stopping on the
 true residual), with z = V(r) instead of z = D^-1 r.
+The smoother parameters (theta, sweeps per level) and the cycle are INPUTS of
+this module (reading M5/M8: the paper gives no multigrid, the values used are
+chosen by measurement on the GPU and passed in by the tests); nothing here is
+tuned to the GPU implementation.
 """
 import numpy as np
 import scipy.linalg as sla
@@ -198,23 +210,50 @@ def smoother_weights(levels, theta=1.6, k=8):
 
 def level_sweeps(levels, nu=1, nu_deep=0, deep_nodes=150000):
     """Sweeps per level (M5): nu on the fine level and on coarse levels with more
-    than deep_nodes nodes; nu_deep on the smaller coarse levels (0 = auto: 8 when
-    the fine grid has >= 2 000 000 nodes, else nu)."""
+    than deep_nodes nodes; nu_deep (0 -> nu) on the smaller coarse levels.  Both
+    are inputs (the GPU's choice is passed in by the tests)."""
     def nodes(d):
         return (d[0] + 1) * (d[1] + 1) * (d[2] + 1)
-    fine = nodes(levels[0]["dims"])
     out = []
     for l, lv in enumerate(levels):
-        if l == 0 or nodes(lv["dims"]) > deep_nodes:
+        if l == 0 or nodes(lv["dims"]) > deep_nodes or nu_deep <= 0:
             out.append(nu)
-        elif nu_deep > 0:
-            out.append(nu_deep)
         else:
-            out.append(8 if fine >= 2000000 else nu)
+            out.append(nu_deep)
     return out
 
 
-def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
+def coarse_correction(levels, rc, omega, nu, l, ops, cycle="V"):
+    """Approximate A_l^{-1} rc on coarse level l (full-length vector, 0 on fixed
+    DOFs) -- reading M8.  cycle "V": one cycle B_l(rc).  cycle "K" (Notay &
+    Vassilevski 2008, K-cycle = two steps of flexible CG preconditioned by B_l):
+        x1 = B_l(rc);  v1 = A x1;  rho1 = x1.v1;  a1 = x1.rc;  r2 = rc - (a1/rho1) v1
+        x2 = B_l(r2);  v2 = A x2;  g = x2.v1;  b = x2.v2;  a2 = x2.r2;  rho2 = b - g^2/rho1
+        e  = (a1/rho1 - g a2/(rho1 rho2)) x1 + (a2/rho2) x2     (rho2 <= 0: second step dropped)
+    i.e. e is the A-orthogonal (Galerkin) projection of A^-1 rc onto span{x1, x2}.
+    The coarsest level is solved exactly (never K'd)."""
+    if cycle == "V" or l == len(levels) - 1:
+        return vcycle(levels, rc, omega, nu, l, ops, cycle)
+    A, _, free = ops[l]
+
+    def Ax(x):
+        y = np.zeros_like(x)
+        y[free] = A @ x[free]
+        return y
+    x1 = vcycle(levels, rc, omega, nu, l, ops, cycle)
+    v1 = Ax(x1)
+    rho1, a1 = float(x1 @ v1), float(x1 @ rc)
+    r2 = rc - (a1 / rho1) * v1
+    x2 = vcycle(levels, r2, omega, nu, l, ops, cycle)
+    v2 = Ax(x2)
+    g, bb, a2 = float(x2 @ v1), float(x2 @ v2), float(x2 @ r2)
+    rho2 = bb - g * g / rho1
+    if not rho2 > 0.0:
+        return (a1 / rho1) * x1
+    return (a1 / rho1 - g * a2 / (rho1 * rho2)) * x1 + (a2 / rho2) * x2
+
+
+def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None, cycle="V"):
     """One V-cycle z = V(b) for a full-length level-_l vector b (0 on fixed DOFs).
     M5/M6; textbook recursion (Briggs, Henson, McCormick, "A Multigrid Tutorial",
     V-cycle scheme), written out without fusion.  omega None -> each level's
@@ -240,7 +279,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
         r[free] = bf - A @ xf
         rc = lv["P"].T @ r
         rc[levels[_l + 1]["fixed"] != 0] = 0.0
-        ec = vcycle(levels, rc, omega, nu, _l + 1, _ops)
+        ec = coarse_correction(levels, rc, omega, nu, _l + 1, _ops, cycle)
         xf = xf + (lv["P"] @ ec)[free]
         for _ in range(nl):
             xf = xf + w * (bf - A @ xf) / d
@@ -250,9 +289,13 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None):
 
 
 def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
-               max_iter=10000, u0=None, power_steps=8, nu_deep=0):
-    """PCG with the V-cycle preconditioner on K_ff u_f = f_f, stopping on the
-    TRUE relative residual (same loop as solve_jacobi_cg).  Returns (u, iters)."""
+               max_iter=10000, u0=None, power_steps=8, nu_deep=0, cycle="V", flexible=None):
+    """PCG with the multigrid preconditioner (cycle "V" or "K", M8) on K_ff u_f =
+    f_f, stopping on the TRUE relative residual (same loop as solve_jacobi_cg).
+    flexible (default: True for the K-cycle) -> Polak-Ribiere beta (M9).
+    Returns (u, iters)."""
+    if flexible is None:
+        flexible = cycle == "K"
     levels = smoother_weights(hierarchy(K, fixed, dims, coarse_max=coarse_max), theta, power_steps)
     nu = level_sweeps(levels, nu, nu_deep)
     ops = [level_operator(lv) for lv in levels]
@@ -265,7 +308,7 @@ def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
         return np.zeros(K.shape[0]), 0
 
     def M(r):
-        return vcycle(levels, r, None, nu, 0, ops)
+        return vcycle(levels, r, None, nu, 0, ops, cycle)
 
     def res(u):
         r = np.zeros_like(u)
@@ -292,7 +335,8 @@ def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
         r = r - alpha * q
         z = M(r)
         rz_new = r @ z
-        p = z + (rz_new / rz) * p
+        beta = -alpha * (z @ q) / rz if flexible else rz_new / rz     # M9: z.(r_new - r_old) = -alpha z.q
+        p = z + beta * p
         rz = rz_new
         it += 1
     return u, it

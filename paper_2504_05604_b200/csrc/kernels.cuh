@@ -212,14 +212,15 @@ __global__ void k_finish_update(DevState* st, int even) {
   cg_finish_update<kMG>(st, st->sums[0], st->sums[1], even);
 }
 // multigrid PCG: rho = r.V(r) of the V-cycle's last sweep (allreduced) -> beta, rz
-__global__ void k_finish_rho(DevState* st) {
+// flex (K-cycle, reading M9): Polak-Ribiere beta = -alpha (q.z)/rz, q.z in sums[1]
+__global__ void k_finish_rho(DevState* st, int flex) {
   if (st->done) return;
   const double rho = st->sums[0];
   if (!(rho > 0.0) || !isfinite(rho)) {
     st->status = 3;
     st->done = 1;
   } else {
-    st->beta = st->fresh ? 0.0 : rho / st->rz;
+    st->beta = st->fresh ? 0.0 : flex ? -st->alpha * st->sums[1] / st->rz : rho / st->rz;
     st->rz = rho;
   }
 }

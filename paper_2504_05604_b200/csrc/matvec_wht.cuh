@@ -118,6 +118,9 @@ struct MvEpi {
   const uint8_t* fixm;      // per node
   float* out32;             // kEpi = 2: if set, the residual is written here in fp32 (the
                             // restriction input of an fp32 multigrid hierarchy)
+  const double* qk;         // kEpi = 1: if set, the PCG's q = K p of this iteration; the
+                            // epilogue also reduces q.out for the flexible (Polak-Ribiere)
+                            // beta = -alpha (q.z)/rz of the K-cycle PCG (reading M9)
 };
 
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
@@ -304,7 +307,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   TC Ecur = TC(0);
   // kEpi: the owner's epilogue operands (b, M^-1, mask) for the next node plane it
   // writes are loaded one x-step ahead, so the global loads overlap the compute
-  double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0;
+  double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0, eq[3] = {0.0, 0.0, 0.0};
   uint8_t efm = 0;
   auto epi_load = [&](long long go) {
     if (kEpi != 0 && owned) {
@@ -313,6 +316,9 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       if (kEpi == 1 || kEpi == 2)
 #pragma unroll
         for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
+      if (kEpi == 1 && epi.qk)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) eq[c] = epi.qk[go + c * ncomp];
     }
   };
   if (nunits > 2) epi_load(qp - q);
@@ -322,7 +328,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   release(0);
   if (nunits > 1) release(1);
   corners_wht(0, G0);
-  double dot = 0.0;
+  double dot = 0.0, dot2 = 0.0;
   for (int t = 1; t < nunits; ++t) {
     const int ex = xs - 2 + t;              // element plane of this step (node planes ex, ex+1)
     (void)ex;
@@ -386,6 +392,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
           const double zn = ((efm >> c) & 1) ? 0.0 : fma(wd, eb[c] - qv, pbase[c]);
           qp[c * ncomp] = zn;
           dot = fma(eb[c], zn, dot);
+          dot2 = fma(eq[c], zn, dot2);
         }
       }
       qp += nplane;
@@ -404,17 +411,19 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   }
 
   if (kEpi == 1) {
-    __shared__ double tot[1];
-    double vv[1] = {dot};
-    if (grid_reduce<1>(vv, partials, counter, tot) && leader) {
+    __shared__ double tot[2];
+    double vv[2] = {dot, dot2};
+    if (grid_reduce<2>(vv, partials, counter, tot) && leader) {
       const double rho = tot[0];
       if (!finish) {                         // x-slabs: allreduced, then k_finish_rho
         st->sums[0] = rho;
+        st->sums[1] = tot[1];
       } else if (!(rho > 0.0) || !isfinite(rho)) {
         st->status = 3;
         st->done = 1;
       } else {
-        st->beta = st->fresh ? 0.0 : rho / st->rz;
+        // flexible (K-cycle, M9): z.(r_new - r_old) = -alpha z.q
+        st->beta = st->fresh ? 0.0 : epi.qk ? -st->alpha * tot[1] / st->rz : rho / st->rz;
         st->rz = rho;
       }
     }

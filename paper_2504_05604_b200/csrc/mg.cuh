@@ -330,6 +330,84 @@ k_mg_jacobi(LvGeo L, const T* __restrict__ b, const T* __restrict__ q,
 }
 
 // ---------------------------------------------------------------------------
+// K-cycle (reading M8; Notay & Vassilevski 2008): a coarse level l is solved by
+// two flexible-CG steps preconditioned by its own cycle B_l:
+//   x1 = B(b); t = A x1; rho1 = x1.t, a1 = x1.b; kx = x1, kv = t     (k_kc_dot1)
+//   b <- r2 = b - (a1/rho1) kv                                         (k_kc_r2)
+//   x2 = B(r2); t = A x2; g = x2.kv, bb = x2.t, a2 = x2.r2             (k_kc_dot2)
+//   rho2 = bb - g^2/rho1;  c2 = a2/rho2, c1 = a1/rho1 - g c2/rho1 (rho2 <= 0: c2 = 0)
+//   x = c1 kx + c2 x2                                                  (k_kc_combine)
+// The vectors are whole padded level buffers (pads and fixed DOFs hold 0 in x,
+// t and b), reduced in fp64 in a fixed order.  kc[0..3] = rho1, a1, c1, c2.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_kc_dot1(long long n, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
+          T* __restrict__ kx, T* __restrict__ kv, double* __restrict__ kc, const DevState* gst,
+          double* partials, unsigned int* counter) {
+  MG_GATE(gst);
+  double xt = 0.0, xb = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const T xv = x[i], tv = t[i];
+    kx[i] = xv;
+    kv[i] = tv;
+    xt = fma((double)xv, (double)tv, xt);
+    xb = fma((double)xv, (double)b[i], xb);
+  }
+  __shared__ double tot[2];
+  double v[2] = {xt, xb};
+  if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
+    kc[0] = tot[0];
+    kc[1] = tot[1];
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_kc_r2(long long n, T* __restrict__ b, const T* __restrict__ kv, const double* __restrict__ kc, const DevState* gst) {
+  MG_GATE(gst);
+  const double s = kc[0] > 0.0 ? kc[1] / kc[0] : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = (T)fma(-s, (double)kv[i], (double)b[i]);
+}
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_kc_dot2(long long n, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
+          const T* __restrict__ kv, double* __restrict__ kc, const DevState* gst, double* partials,
+          unsigned int* counter) {
+  MG_GATE(gst);
+  double g = 0.0, bb = 0.0, a2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double xv = (double)x[i];
+    g = fma(xv, (double)kv[i], g);
+    bb = fma(xv, (double)t[i], bb);
+    a2 = fma(xv, (double)b[i], a2);
+  }
+  __shared__ double tot[3];
+  double v[3] = {g, bb, a2};
+  if (grid_reduce<3>(v, partials, counter, tot) && threadIdx.x == 0) {
+    const double rho1 = kc[0], a1 = kc[1];
+    if (!(rho1 > 0.0) || !isfinite(rho1)) {     // B_l(b) = 0 (b = 0): no correction
+      kc[2] = 0.0;
+      kc[3] = 0.0;
+      return;
+    }
+    const double rho2 = tot[1] - tot[0] * tot[0] / rho1;
+    const double c2 = (rho2 > 0.0 && isfinite(rho2)) ? tot[2] / rho2 : 0.0;
+    kc[2] = a1 / rho1 - tot[0] * c2 / rho1;
+    kc[3] = c2;
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_kc_combine(long long n, T* __restrict__ x, const T* __restrict__ kx, const double* __restrict__ kc,
+             const DevState* gst) {
+  MG_GATE(gst);
+  const double c1 = kc[2], c2 = kc[3];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = (T)fma(c1, (double)kx[i], c2 * (double)x[i]);
+}
+
+// ---------------------------------------------------------------------------
 // Smoother weights (M5): power steps v <- D^-1 A v from a fixed start vector,
 // then w_l = theta (v^T D v) / (v^T A v) = theta / lam_l.
 // Start vector: DOF k of the level's external numbering (3 n + c) gets

@@ -167,6 +167,7 @@ struct MgLevel {
   void* Y = nullptr;            // level 1 matrix-free: per-element outputs [24][nel]
   void* pw = nullptr;           // power-step vector kept for the next design's warm start
   void* pw_b = nullptr;         // its snapshot copy
+  void *kx = nullptr, *kv = nullptr;   // K-cycle (M8): x1 and A x1 of the first FCG step
   uint8_t* fixm = nullptr;      // per node: bit c = DOF c fixed
   std::vector<uint8_t> hfix;    // host copy, external node order
   bool stored = false;
@@ -253,6 +254,8 @@ struct topo_ctx {
   float* mg_E32 = nullptr;           // fp32 copy of mgE for the fp32 level-1 operator
   long long mg_setup_launches = 0;
   int mg_batch = 2;
+  bool mg_kcycle = false;            // K-cycle on the coarse levels + flexible PCG (M8, M9)
+  double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
 };
 
 namespace {
@@ -832,7 +835,10 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
     attr_set = true;
   }
   const MvGrid m = mv_grid(ctx, s.g);
-  const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr};
+  // kEpi = 1 with the K-cycle: the PCG's q (untouched by the V-cycle: the fp32
+  // pre-smoothing residual goes to res32, the fp64 one to z) for the flexible beta
+  const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr,
+                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr};
   k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew,
                                                                                  q, s.partials, s.counter, finish,
                                                                                  scale, epi);
@@ -1058,6 +1064,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   if (L > 16) return set_err(ctx, TOPO_EINVAL, "multigrid: more than 16 levels");
   ctx->mg_on = true;
   ctx->mg_f32 = P.mg_fp32 != 0;
+  ctx->mg_kcycle = P.mg_cycle == TOPO_MG_KCYCLE && P.mg_nu == 1;
   ctx->mg_theta = P.mg_omega;
   ctx->mg.resize(L);
   auto al = [&](void** p, size_t bytes) -> int {
@@ -1088,6 +1095,10 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     if (m.stored && l < L - 1) CK(al(&m.S, rs * 126 * m.L.ncomp));
     if (!m.stored) CK(al(&m.Y, rs * 24 * m.L.nel()));
     if (l < L - 1) CK(al(&m.pw, rs * 3 * m.L.ncomp));
+    if (P.mg_cycle == TOPO_MG_KCYCLE && P.mg_nu == 1 && l < L - 1) {
+      CK(al(&m.kx, rs * 3 * m.L.ncomp));
+      CK(al(&m.kv, rs * 3 * m.L.ncomp));
+    }
     std::vector<uint8_t> lay(m.L.ncomp, 0);
     for (int iz = 0; iz <= h.nz; ++iz)
       for (int ix = 0; ix <= h.nx; ++ix)
@@ -1153,6 +1164,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   }
   if (!ctx->mg[1].stored)   // fp32 moduli of the matrix-free level-1 operator
     CK(al((void**)&ctx->mg_E32, sizeof(float) * mgG(ctx).nelloc));
+  CK(al((void**)&ctx->mg_kc, sizeof(double) * 8 * 16));
   {
     std::vector<double> om(kMgScaleOff + 16, 1.0);
     CK(al((void**)&ctx->mg_om, sizeof(double) * om.size()));
@@ -1440,6 +1452,7 @@ int mg_level_nu(const topo_ctx* ctx, int l) {
   const topo_params& P = ctx->prm;
   if (l == 0 || ctx->mg[l].L.nodes() > kMgDeepNodes) return P.mg_nu;
   if (P.mg_nu_deep > 0) return P.mg_nu_deep;
+  if (ctx->mg_kcycle) return P.mg_nu;   // the K-cycle solves the deep levels well enough (M8)
   const long long fine = (long long)(P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
   return fine >= 2000000 ? 8 : P.mg_nu;
 }
@@ -1447,6 +1460,10 @@ int mg_level_nu(const topo_ctx* ctx, int l) {
 // One V-cycle on level l (level 0: b = r; the result lands in s.w and the last
 // fine sweep also sets rho = r.V(r) and beta for the PCG; `dot` is unused).
 // T = precision of levels >= 1 (level 0 is always fp64).
+template <typename T>
+int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot);
+template <typename T>
+int enqueue_coarse_t(topo_ctx* ctx, int l, int gate);
 template <typename T>
 int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   Slab& s = ctx->slabs[0];
@@ -1469,8 +1486,9 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // (nu = 1: z is not stored -- k_mg_prolong0 recomputes it with the correction)
     // (with mg_fp32 the smoothing matvecs compute the element operator in fp32)
     // (x-slabs: every step below runs per slab; nu = 1 only, see mg_build)
-    if (nu == 1)
-      for (Slab& sl : ctx->slabs) CK((launch_mv<3, false, 2, T>(ctx, sl, gate, sl.m_r, nullptr, nullptr, sl.q, 0, om)));
+    if (nu == 1)   // (fp64 residual into z with the K-cycle: q must survive for the flexible beta)
+      for (Slab& sl : ctx->slabs)
+        CK((launch_mv<3, false, 2, T>(ctx, sl, gate, sl.m_r, nullptr, nullptr, ctx->mg_kcycle ? sl.z : sl.q, 0, om)));
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
@@ -1498,12 +1516,13 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
             Fs, n1.L, cx, sl.res32, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend, slabs ? 1 : 0);
       else
         k_mg_restrict0<double, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
-            Fs, n1.L, cx, sl.q, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend, slabs ? 1 : 0);
+            Fs, n1.L, cx, ctx->mg_kcycle ? sl.z : sl.q, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend,
+            slabs ? 1 : 0);
       ctx->launches++;
       debug_sync(ctx, "k_mg_restrict0");
     }
     CK(mg_allreduce_level(ctx, n1.b, 3 * n1.L.ncomp, sizeof(T) == 4));
-    CK(enqueue_vcycle_t<T>(ctx, 1, gate, false));
+    CK(enqueue_coarse_t<T>(ctx, 1, gate));
     if (nu == 1) {   // z = w D^-1 r (the first sweep, recomputed) + P x1, x-marching
       for (Slab& sl : ctx->slabs) {   // owned + ghost planes (the post-smoothing matvec reads the ghosts)
         const int pa = std::max(0, sl.g.ex0 - 1), pb = std::min(sl.g.nelx, sl.g.ex0 + sl.g.nown) + 1;
@@ -1543,8 +1562,8 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
         CK((launch_mv<0, false, 1, T, double>(ctx, sl, gate, sl.m_z, nullptr, nullptr, sl.w, slabs ? 0 : 1, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[3], ctx->stream, cudaEventRecordExternal));
     if (slabs) {
-      CK(allreduce(ctx, 0, 1, 0));
-      for (Slab& sl : ctx->slabs) { k_finish_rho<<<1, 1, 0, ctx->stream>>>(sl.st); ctx->launches++; }
+      CK(allreduce(ctx, 0, ctx->mg_kcycle ? 2 : 1, 0));
+      for (Slab& sl : ctx->slabs) { k_finish_rho<<<1, 1, 0, ctx->stream>>>(sl.st, ctx->mg_kcycle ? 1 : 0); ctx->launches++; }
       CK(exchange_nodes(ctx, &Slab::w));
     }
     return check_launch(ctx);
@@ -1565,7 +1584,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     LAUNCH(ctx, (k_mg_sweep_st8<false, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);   // t = A x
     LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm,
            mgp<T>(n1.b), gst);
-    CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
+    CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
     LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
     int k = 0;
     if (nu & 1) {   // odd: one in-place sweep, then pairs of fused sweeps end in x
@@ -1585,7 +1604,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   CK(mg_apply<T>(ctx, l, gate));
   LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b),
          gst);
-  CK(enqueue_vcycle_t<T>(ctx, l + 1, gate, false));
+  CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
   LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
   for (int k = 1; k <= nu; ++k) {
     if (!m.stored) {   // level 1: the sweep fused into the gather phase
@@ -1596,6 +1615,31 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     CK(mg_apply<T>(ctx, l, gate));
     LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   }
+  return check_launch(ctx);
+}
+
+// Coarse correction on level l >= 1 (reading M8): one cycle (V), or the K-cycle's
+// two flexible-CG steps preconditioned by that cycle; the coarsest level is
+// solved exactly either way.  Input m.b, output m.x (m.b is overwritten by r2).
+template <typename T>
+int enqueue_coarse_t(topo_ctx* ctx, int l, int gate) {
+  const int L = (int)ctx->mg.size();
+  if (!ctx->mg_kcycle || l >= L - 1) return enqueue_vcycle_t<T>(ctx, l, gate, false);
+  Slab& s = ctx->slabs[0];
+  MgLevel& m = ctx->mg[l];
+  const DevState* gst = gate ? s.st : nullptr;
+  double* kc = ctx->mg_kc + 8 * l;
+  const long long n = 3 * m.L.ncomp;
+  const int gF = grid_for(n);
+  T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *kx = mgp<T>(m.kx), *kv = mgp<T>(m.kv);
+  CK(enqueue_vcycle_t<T>(ctx, l, gate, false));   // x1 = B(b)
+  CK(mg_apply<T>(ctx, l, gate));                  // t = A x1
+  LAUNCH(ctx, k_kc_dot1<T>, gF, n, mx, mt, mb, kx, kv, kc, gst, s.partials, s.counter);
+  LAUNCH(ctx, k_kc_r2<T>, gF, n, mb, kv, kc, gst);
+  CK(enqueue_vcycle_t<T>(ctx, l, gate, false));   // x2 = B(r2)
+  CK(mg_apply<T>(ctx, l, gate));                  // t = A x2
+  LAUNCH(ctx, k_kc_dot2<T>, gF, n, mx, mt, mb, kv, kc, gst, s.partials, s.counter);
+  LAUNCH(ctx, k_kc_combine<T>, gF, n, mx, kx, kc, gst);
   return check_launch(ctx);
 }
 
@@ -2178,13 +2222,13 @@ void free_ctx(topo_ctx* ctx) {
       if (p) cudaFree(p);
   }
   for (MgLevel& m : ctx->mg) {
-    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.pw, m.pw_b, m.fixm};
+    void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.pw, m.pw_b, m.fixm, m.kx, m.kv};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
   {
     void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_Eg, ctx->mg_A0, ctx->mg_C, ctx->mg_R, ctx->mg_P, ctx->mg_ws,
-                    ctx->mg_dmap, ctx->mg_imap, ctx->mg_om};
+                    ctx->mg_dmap, ctx->mg_imap, ctx->mg_om, ctx->mg_kc};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
@@ -2233,6 +2277,7 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (!(p->mg_omega > 0 && p->mg_omega < 2)) return set_err(ctx, TOPO_EINVAL, "mg_omega must be in (0, 2)");
   if (p->mg_fp32 != 0 && p->mg_fp32 != 1) return set_err(ctx, TOPO_EINVAL, "mg_fp32 must be 0 or 1");
   if (p->mg_nu_deep < 0 || p->mg_nu_deep > 64) return set_err(ctx, TOPO_EINVAL, "mg_nu_deep must be in [0, 64]");
+  if (p->mg_cycle != TOPO_MG_VCYCLE && p->mg_cycle != TOPO_MG_KCYCLE) return set_err(ctx, TOPO_EINVAL, "mg_cycle must be 0 or 1");
   if (p->mg_coarse_max != 0 && (p->mg_coarse_max < 24 || p->mg_coarse_max > 8192))
     return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be 0 (auto) or in [24, 8192]");
   return TOPO_OK;
@@ -2270,6 +2315,7 @@ void topo_params_default(topo_params* p) {
   p->mg_coarse_max = 0;
   p->mg_fp32 = 1;
   p->mg_nu_deep = 0;
+  p->mg_cycle = TOPO_MG_KCYCLE;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }

@@ -47,7 +47,8 @@ class topo_params(C.Structure):
                 ("cg_warm_start", C.c_int32), ("oc_tol", C.c_double), ("oc_lmax", C.c_double),
                 ("deterministic", C.c_int32), ("cg_check_every", C.c_int32),
                 ("precond", C.c_int32), ("mg_nu", C.c_int32), ("mg_omega", C.c_double),
-                ("mg_coarse_max", C.c_int32), ("mg_nu_deep", C.c_int32), ("mg_fp32", C.c_int32)]
+                ("mg_coarse_max", C.c_int32), ("mg_nu_deep", C.c_int32), ("mg_fp32", C.c_int32),
+                ("mg_cycle", C.c_int32)]
 
 
 class topo_dist(C.Structure):
@@ -205,6 +206,9 @@ def make_params(p):
               "cg_check_every", "mg_nu", "mg_coarse_max", "mg_nu_deep", "mg_fp32"):
         if k in p:
             setattr(prm, k, int(p[k]))
+    if "mg_cycle" in p:
+        prm.mg_cycle = {"V": 0, "K": 1}.get(p["mg_cycle"], p["mg_cycle"]) if isinstance(p["mg_cycle"], str) \
+            else int(p["mg_cycle"])
     if "precond" in p:
         prm.precond = PRECOND[p["precond"]] if isinstance(p["precond"], str) else int(p["precond"])
     for k in ("volfrac", "penal", "rmin", "E0", "Emin", "nu", "move", "cg_rtol", "oc_tol", "oc_lmax",

@@ -154,3 +154,31 @@ def test_fullsize_config2(topo):
     assert_rel(xphys, oracle.apply_filter(H, Hs, 0, "x", xn_o, passive=pas), 1e-9, "xPhys")
     assert abs(vol - p["volfrac"]) <= 1e-6
     assert np.all(xnew[~D] == 0) and np.all(xphys[~D] == 0)
+
+
+def test_config2_history_vs_oracle_golden(topo, golden_dir):
+    """Config 2 at full size, all 30 BASELINE iterations, against the oracle's
+    own run (tests/golden/cfg2_oracle_history.npz, written by
+    tools/make_golden_cfg2.py from oracle/ only): c history within 1e-6
+    relative, x / xPhys after iterations 10 and 30 within 1e-6 (R#25 metric),
+    volume within 1e-6 every iteration."""
+    import os
+    g = np.load(os.path.join(golden_dir, "cfg2_oracle_history.npz"))
+    p, f, fx, pas = make_problem(2)
+    with topo.Problem(p, f, fx, pas) as pr:
+        c10, x10, _ = pr.optimize(10)
+        xp10 = pr.get("xphys")
+        vols = [pr.timings()["volume"]]
+        c20, x30, nd = pr.optimize(20)
+        xp30 = pr.get("xphys")
+        vols.append(pr.timings()["volume"])
+    c = np.concatenate([c10, c20])
+    assert nd == 20 and c.size == 30
+    assert_rel(c, g["c"], 1e-6, "config-2 c history (30 iterations)")
+    assert_rel(c[:10], g["c"][:10], 1e-6, "config-2 c history (first 10)")
+    assert_rel(x10, g["x_10"], 1e-6, "x after 10")
+    assert_rel(xp10, g["xphys_10"], 1e-6, "xPhys after 10")
+    assert_rel(x30, g["x_30"], 1e-6, "x after 30")
+    assert_rel(xp30, g["xphys_30"], 1e-6, "xPhys after 30")
+    assert all(abs(v - p["volfrac"]) <= 1e-6 for v in vols)
+    assert np.all(xp30[pas != 0] == 0)

@@ -85,25 +85,33 @@ def test_mg_hierarchy_and_galerkin_operators(topo, dims, obst, fp32):
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu,fp32,deep", [(1, 0, 0), (2, 0, 0), (1, 1, 0), (2, 1, 0), (1, 0, 4), (1, 1, 6)])
-def test_mg_vcycle_parity(topo, dims, obst, nu, fp32, deep):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32, mg_nu_deep=deep)
+@pytest.mark.parametrize("nu,fp32,deep,cycle", [(1, 0, 0, "V"), (2, 0, 0, "V"), (1, 1, 0, "V"), (2, 1, 0, "V"),
+                                                (1, 0, 4, "V"), (1, 1, 6, "V"), (1, 0, 0, "K"), (1, 1, 0, "K"),
+                                                (1, 0, 3, "K")])
+def test_mg_vcycle_parity(topo, dims, obst, nu, fp32, deep, cycle):
+    """z = B(b) for the V-cycle and the K-cycle (M8) vs the oracle's recursion."""
+    p, f, fx, pas, x, K = _case(dims, obst, seed=1, mg_nu=nu, mg_omega=1.5, mg_fp32=fp32, mg_nu_deep=deep,
+                                mg_cycle=cycle)
     lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=1000), theta=1.5)
     b = np.where(fx == 0, random_vector(K.shape[0], seed=3), 0.0)
-    zo = mg.vcycle(lv, b, None, nu=mg.level_sweeps(lv, nu, deep))
+    zo = mg.vcycle(lv, b, None, nu=mg.level_sweeps(lv, nu, deep), cycle=cycle)
     with topo.Problem(p, f, fx, pas) as pr:
         pr.set_xphys(x)
         z = pr.mg_vcycle(b)
-    assert_rel(z, zo, 1e-4 if fp32 else 1e-9, f"V-cycle {dims} nu={nu} fp32={fp32} deep={deep}")
+    assert_rel(z, zo, 1e-4 if fp32 else 1e-9, f"{cycle}-cycle {dims} nu={nu} fp32={fp32} deep={deep}")
     assert np.all(z[fx != 0] == 0)
 
 
 @pytest.mark.parametrize("dims,obst", CASES)
-@pytest.mark.parametrize("nu,fp32,deep", [(1, 0, 0), (1, 1, 0), (2, 1, 0), (1, 1, 8)])
-def test_mg_solve_parity(topo, dims, obst, nu, fp32, deep):
-    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu, mg_nu_deep=deep)
+@pytest.mark.parametrize("nu,fp32,deep,cycle", [(1, 0, 0, "V"), (1, 1, 0, "V"), (2, 1, 0, "V"), (1, 1, 8, "V"),
+                                                (1, 0, 0, "K"), (1, 1, 0, "K")])
+def test_mg_solve_parity(topo, dims, obst, nu, fp32, deep, cycle):
+    """MG-PCG (V: standard PCG; K: flexible PCG, M9) solves to the direct
+    solution, in the oracle's number of iterations (same algorithm, same
+    parameters) and far fewer than Jacobi-PCG."""
+    p, f, fx, pas, x, K = _case(dims, obst, seed=2, mg_fp32=fp32, mg_nu=nu, mg_nu_deep=deep, mg_cycle=cycle)
     uo = oracle.solve_direct(K, f, fx)
-    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=nu, nu_deep=deep)
+    _, it_o = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, theta=1.6, nu=nu, nu_deep=deep, cycle=cycle)
     its = {}
     for pc in ("jacobi", "mg"):
         with topo.Problem(dict(p, precond=pc), f, fx, pas) as pr:
@@ -261,3 +269,23 @@ def test_mg_theta_cut_recovers(topo):
     assert t["mg_fallbacks"] == 0
     assert info["precond"] == "mg"
     print("theta cuts", t["mg_theta_cuts"], "promotions", t["mg_promotions"], "iters", info["iters"])
+
+
+def test_kcycle_iterations_config2(topo):
+    """Config 2 (obstacle, 312k DOF, 5 levels), 14 SIMP iterations: the K-cycle
+    (M8, flexible PCG M9) gives the same designs as the V-cycle (c history to
+    1e-6: only the way u is reached differs) with far fewer PCG iterations once
+    voids have formed (the V-cycle's count grows ~5x over the run)."""
+    p, f, fx, pas = make_problem(2)
+    out = {}
+    for cyc in ("V", "K"):
+        with topo.Problem(dict(p, mg_cycle=cyc), f, fx, pas) as pr:
+            ncg, cs = [], []
+            for _ in range(14):
+                c, _, _ = pr.optimize(1, want_x=False)
+                cs.append(c[0])
+                ncg.append(pr.timings()["cg_iters"])
+            out[cyc] = (np.array(cs), np.array(ncg))
+    assert_rel(out["K"][0], out["V"][0], 1e-6, "c history K vs V")
+    print("ncg V", out["V"][1].tolist(), "K", out["K"][1].tolist())
+    assert out["K"][1][-4:].max() * 2 < out["V"][1][-4:].min()

@@ -218,15 +218,99 @@ def test_jacobi_bound_closed_form():
     assert abs((lam + 4 * mu) / 9 - 0.2350427350) <= 1e-10
 
 
-def test_level_sweeps_rule():
-    """M5: nu on the fine level and on coarse levels above 150 000 nodes; nu_deep
-    (explicit, or auto = 8 only when the fine grid has >= 2 M nodes) below."""
-    lv = [dict(dims=(60, 20, 4)), dict(dims=(30, 10, 2)), dict(dims=(15, 5, 1))]
-    assert mg.level_sweeps(lv, 1, 0) == [1, 1, 1]
-    assert mg.level_sweeps(lv, 1, 4) == [1, 4, 4]
-    big = [dict(dims=(512, 256, 256)), dict(dims=(256, 128, 128)), dict(dims=(128, 64, 64)),
-           dict(dims=(64, 32, 32)), dict(dims=(32, 16, 16)), dict(dims=(16, 8, 8))]
-    assert mg.level_sweeps(big, 1, 0) == [1, 1, 1, 8, 8, 8]
+def _problem(dims, seed=0, voids=False):
+    """Cantilever K on a random density field (voids: half the elements at x =
+    1e-3, i.e. E ~ 1e-9, the SIMP contrast of late designs)."""
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(dims))
+    x = rng.uniform(0.01, 1.0, n)
+    if voids:
+        x = np.where(rng.uniform(size=n) < 0.5, 1e-3, 1.0)
+    E = 1e-9 + x ** 3 * (1.0 - 1e-9)
+    K = oracle.assemble(*dims, oracle.element_stiffness(0.3), E)
+    return K, cantilever_load(*dims), cantilever_fixed(*dims)
+
+
+def test_kcycle_galerkin_projection():
+    """M8 pin (a closed-form property, not a restatement): the K-cycle's coarse
+    correction e is the A-orthogonal projection of A^-1 rc onto span{x1, x2}, so
+    the new residual rc - A e is orthogonal to x1 and x2; and e reduces the
+    A-norm error at least as much as the plain V-cycle correction x1."""
+    dims = (24, 8, 4)
+    K, f, fx = _problem(dims, seed=7)
+    lv = mg.smoother_weights(mg.hierarchy(K, fx, dims, coarse_max=100), theta=1.6)
+    assert len(lv) >= 4
+    ops = [mg.level_operator(l) for l in lv]
+    lv[-1]["chol"] = __import__("scipy.linalg", fromlist=["cho_factor"]).cho_factor(ops[-1][0].toarray())
+    A, _, free = ops[1]
+    rng = np.random.default_rng(4)
+    rc = np.where(lv[1]["fixed"] == 0, rng.standard_normal(lv[1]["K"].shape[0]), 0.0)
+    x1 = mg.vcycle(lv, rc, None, 1, 1, ops, "K")
+    e = mg.coarse_correction(lv, rc, None, 1, 1, ops, "K")
+    # x2 = B(r2) recomputed: r2 = rc - (a1/rho1) A x1
+    Av1 = np.zeros_like(x1)
+    Av1[free] = A @ x1[free]
+    r2 = rc - (x1 @ rc) / (x1 @ Av1) * Av1
+    x2 = mg.vcycle(lv, r2, None, 1, 1, ops, "K")
+    Ae = np.zeros_like(e)
+    Ae[free] = A @ e[free]
+    res = rc - Ae
+    assert abs(res @ x1) <= 1e-10 * np.linalg.norm(rc) * np.linalg.norm(x1)
+    assert abs(res @ x2) <= 1e-10 * np.linalg.norm(rc) * np.linalg.norm(x2)
+    ex = np.zeros_like(rc)
+    ex[free] = __import__("scipy.sparse.linalg", fromlist=["spsolve"]).spsolve(A.tocsc(), rc[free])
+    errA = lambda d: float(d[free] @ (A @ d[free]))  # noqa: E731
+    assert errA(ex - e) <= errA(ex - (x1 @ rc) / (x1 @ Av1) * x1) + 1e-14 * errA(ex)
+
+
+def test_kcycle_exact_inner_solve_is_exact():
+    """M8 special case: with an exact solve on the level below (a 2-level cycle
+    on level 1 of a 3-level hierarchy whose smoother is skipped is not available,
+    so use the coarsest-level identity): on the coarsest level the correction is
+    the exact solve, and a K-cycle PCG on a 2-level hierarchy equals the V-cycle
+    PCG (the K-cycle only differs above the coarsest level)."""
+    dims = (12, 4, 2)
+    K, f, fx = _problem(dims, seed=3)
+    u1, it1 = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=400, cycle="V")
+    u2, it2 = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=400, cycle="K", flexible=False)
+    assert len(mg.hierarchy(K, fx, dims, coarse_max=400)) == 2
+    assert it1 == it2 and np.array_equal(u1, u2)
+
+
+def test_flexible_cg_equals_cg_for_fixed_preconditioner():
+    """M9 pin: with a fixed SPD preconditioner (the V-cycle) z_new.r_old = 0, so the
+    Polak-Ribiere beta equals the Fletcher-Reeves one up to rounding: same
+    iteration count and the same u (a sign or index slip in the flexible formula
+    breaks this)."""
+    dims = (24, 8, 4)
+    K, f, fx = _problem(dims, seed=5)
+    u1, it1 = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=200, cycle="V", flexible=False)
+    u2, it2 = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=200, cycle="V", flexible=True)
+    assert abs(it1 - it2) <= 1
+    assert np.linalg.norm(u1 - u2) <= 1e-8 * np.linalg.norm(u1)
+
+
+def test_kcycle_pcg_solves_high_contrast():
+    """K-cycle FCG reaches the direct solution (u to 1e-8, true residual 1e-10)
+    on a random half-void field (E contrast 1e9), 4+ levels."""
+    dims = (32, 8, 8)
+    K, f, fx = _problem(dims, seed=9, voids=True)
+    uo = oracle.solve_direct(K, f, fx)
+    uk, itk = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=150, cycle="K")
+    assert len(mg.hierarchy(K, fx, dims, coarse_max=150)) >= 4
+    assert np.linalg.norm(uk - uo) <= 1e-8 * np.linalg.norm(uo)
+    assert oracle.true_residual(K, uk, f, fx) <= 1e-10
+
+
+def test_kcycle_fewer_iterations_on_a_simp_design():
+    """On an evolved SIMP design (config 1 after 8 iterations, 3 levels) the
+    K-cycle needs no more PCG iterations than the V-cycle (the reason for M8)."""
+    K, f, fx, dims, u = _evolved_case(1, 8)
+    uk, itk = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=100, cycle="K")
+    uv, itv = mg.solve_mgcg(K, f, fx, dims, rtol=1e-10, coarse_max=100, cycle="V")
+    assert len(mg.hierarchy(K, fx, dims, coarse_max=100)) >= 3
+    assert np.linalg.norm(uk - u) <= 1e-8 * np.linalg.norm(u)
+    assert itk <= itv
 
 
 def test_vcycle_per_level_sweeps_spd():
