@@ -173,7 +173,7 @@ def oracle_sample(p, n_cg, slab=8):
     return est, sample, (t_mv + t_vec + t_sens + t_filt + t_oc)
 
 
-def oracle_sample_mg(p, n_cg, cycle="K", div=8):
+def oracle_sample_mg(p, n_cg, cycle="K", div=None):
     """Algorithm-matched CPU baseline: the oracle's own MG-PCG (oracle.mg:
     Galerkin hierarchy, damped-Jacobi V/K-cycle, flexible PCG -- the GPU arm's
     algorithm) on the same cantilever scaled down by `div` per axis (x = volfrac),
@@ -184,6 +184,9 @@ def oracle_sample_mg(p, n_cg, cycle="K", div=8):
     import oracle
     from oracle import mg
     from workloads import cantilever_fixed, cantilever_load
+    if div is None:   # a sample of ~2e5 DOF (config 4: 1/8 per axis; config 2: the full grid)
+        ndof_full = 3 * (p["nelx"] + 1) * (p["nely"] + 1) * (p["nelz"] + 1)
+        div = max(1, int(round((ndof_full / 2.0e5) ** (1.0 / 3.0))))
     dims = tuple(max(2, n // div) for n in (p["nelx"], p["nely"], p["nelz"]))
     x = np.full(int(np.prod(dims)), p["volfrac"])
     E = p["Emin"] + x ** p["penal"] * (p["E0"] - p["Emin"])
