@@ -30,7 +30,8 @@ from .ke import element_stiffness, lame  # noqa: F401
 from .fem import (assemble, solve, solve_direct, solve_jacobi_cg, compliance_fu,  # noqa: F401
                   element_energies, matvec_free, matvec_elementwise, matvec_rows, diag_K,
                   true_residual)
-from .filt import filter_matrix, filter_matrix_allpairs, apply_filter, filter_rows  # noqa: F401
+from .filt import (filter_matrix, filter_matrix_allpairs, apply_filter, filter_rows,  # noqa: F401
+                   hs_elements, apply_filter_rows)
 from .oc import oc_update, oc_xnew, sensitivities, BisectionFailure, passive_value  # noqa: F401
 from .loop import run_optimization  # noqa: F401
 from . import mg  # noqa: F401

@@ -98,3 +98,66 @@ def filter_rows(nelx, nely, nelz, rmin, rows):
         out.append((np.array(cols), np.array(w)))
         hs.append(float(np.sum(w)))
     return out, np.array(hs)
+
+
+def _offsets(rmin):
+    """Ball offsets (dx, dy, dz) with |d| < rmin and weights rmin - |d| (R#12)."""
+    R = int(np.ceil(rmin))
+    o = [(dx, dy, dz, rmin - np.sqrt(float(dx * dx + dy * dy + dz * dz)))
+         for dz in range(-R, R + 1) for dx in range(-R, R + 1) for dy in range(-R, R + 1)
+         if np.sqrt(float(dx * dx + dy * dy + dz * dz)) < rmin]
+    return [np.array(v) for v in zip(*o)]
+
+
+def hs_elements(nelx, nely, nelz, rmin, elems):
+    """Hs_e = sum of the in-domain weights of element e's ball (R#13), for a list of
+    element ids, by enumerating the ball offsets -- row sums of H without H (the
+    in-domain test is the same `0 <= j < n` per axis as filter_matrix)."""
+    dx, dy, dz, w = _offsets(rmin)
+    elems = np.asarray(elems, dtype=np.int64)
+    ez, rem = np.divmod(elems, nelx * nely)
+    ex, ey = np.divmod(rem, nely)
+    hs = np.zeros(elems.size)
+    for k in range(w.size):
+        ok = ((ex + dx[k] >= 0) & (ex + dx[k] < nelx) & (ey + dy[k] >= 0) & (ey + dy[k] < nely)
+              & (ez + dz[k] >= 0) & (ez + dz[k] < nelz))
+        hs += np.where(ok, w[k], 0.0)
+    return hs
+
+
+def apply_filter_rows(nelx, nely, nelz, rmin, mode, what, rows, v, x=None, passive=None):
+    """apply_filter(...)[rows] without forming H (for grids whose H does not fit):
+    the same definitions as apply_filter, row by row over the ball offsets, with
+    Hs from hs_elements.  v, x, passive are full-length arrays."""
+    dx, dy, dz, w = _offsets(rmin)
+    rows = np.asarray(rows, dtype=np.int64)
+    ez, rem = np.divmod(rows, nelx * nely)
+    ex, ey = np.divmod(rem, nely)
+    hs_i = hs_elements(nelx, nely, nelz, rmin, rows)
+    v = np.asarray(v)
+    if what == "x" and mode != 0:
+        return v[rows].copy()
+    if what == "dv" and mode != 0:
+        return v[rows].copy()
+    acc = np.zeros(rows.size)
+    for k in range(w.size):
+        jx, jy, jz = ex + dx[k], ey + dy[k], ez + dz[k]
+        ok = (jx >= 0) & (jx < nelx) & (jy >= 0) & (jy < nely) & (jz >= 0) & (jz < nelz)
+        j = np.where(ok, jz * nelx * nely + jx * nely + jy, 0)
+        if what in ("dc", "dv") and mode == 0:
+            term = v[j] / hs_elements(nelx, nely, nelz, rmin, j)        # H (v / Hs)
+        elif mode == 1:
+            term = np.asarray(x)[j] * v[j]                              # H (x v)
+        else:
+            term = v[j]
+        acc += np.where(ok, w[k] * term, 0.0)
+    if what in ("dc", "dv") and mode == 0:
+        return acc
+    if mode == 1:
+        return acc / (hs_i * np.maximum(GAMMA, np.asarray(x)[rows]))
+    out = acc / hs_i
+    if what == "x" and passive is not None:
+        P = np.asarray(passive)[rows]
+        out[P == 1] = 0.0
+        out[P == 2] = 1.0
+    return out

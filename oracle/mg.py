@@ -223,7 +223,7 @@ def level_sweeps(levels, nu=1, nu_deep=0, deep_nodes=150000):
     return out
 
 
-def coarse_correction(levels, rc, omega, nu, l, ops, cycle="V"):
+def coarse_correction(levels, rc, omega, nu, l, ops, cycle="V", kmax=None):
     """Approximate A_l^{-1} rc on coarse level l (full-length vector, 0 on fixed
     DOFs) -- reading M8.  cycle "V": one cycle B_l(rc).  cycle "K" (Notay &
     Vassilevski 2008, K-cycle = two steps of flexible CG preconditioned by B_l):
@@ -231,20 +231,23 @@ def coarse_correction(levels, rc, omega, nu, l, ops, cycle="V"):
         x2 = B_l(r2);  v2 = A x2;  g = x2.v1;  b = x2.v2;  a2 = x2.r2;  rho2 = b - g^2/rho1
         e  = (a1/rho1 - g a2/(rho1 rho2)) x1 + (a2/rho2) x2     (rho2 <= 0: second step dropped)
     i.e. e is the A-orthogonal (Galerkin) projection of A^-1 rc onto span{x1, x2}.
-    The coarsest level is solved exactly (never K'd)."""
-    if cycle == "V" or l == len(levels) - 1:
-        return vcycle(levels, rc, omega, nu, l, ops, cycle)
+    The coarsest level is solved exactly (never K'd); kmax (None = every level
+    above the coarsest) limits the K-cycle to levels l <= kmax (an input: the
+    GPU keeps a single cycle on the level above the coarsest of 6+ level
+    hierarchies, reading M8)."""
+    if cycle == "V" or l == len(levels) - 1 or (kmax is not None and l > kmax):
+        return vcycle(levels, rc, omega, nu, l, ops, cycle, kmax)
     A, _, free = ops[l]
 
     def Ax(x):
         y = np.zeros_like(x)
         y[free] = A @ x[free]
         return y
-    x1 = vcycle(levels, rc, omega, nu, l, ops, cycle)
+    x1 = vcycle(levels, rc, omega, nu, l, ops, cycle, kmax)
     v1 = Ax(x1)
     rho1, a1 = float(x1 @ v1), float(x1 @ rc)
     r2 = rc - (a1 / rho1) * v1
-    x2 = vcycle(levels, r2, omega, nu, l, ops, cycle)
+    x2 = vcycle(levels, r2, omega, nu, l, ops, cycle, kmax)
     v2 = Ax(x2)
     g, bb, a2 = float(x2 @ v1), float(x2 @ v2), float(x2 @ r2)
     rho2 = bb - g * g / rho1
@@ -253,7 +256,7 @@ def coarse_correction(levels, rc, omega, nu, l, ops, cycle="V"):
     return (a1 / rho1 - g * a2 / (rho1 * rho2)) * x1 + (a2 / rho2) * x2
 
 
-def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None, cycle="V"):
+def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None, cycle="V", kmax=None):
     """One V-cycle z = V(b) for a full-length level-_l vector b (0 on fixed DOFs).
     M5/M6; textbook recursion (Briggs, Henson, McCormick, "A Multigrid Tutorial",
     V-cycle scheme), written out without fusion.  omega None -> each level's
@@ -279,7 +282,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None, cycle="V"):
         r[free] = bf - A @ xf
         rc = lv["P"].T @ r
         rc[levels[_l + 1]["fixed"] != 0] = 0.0
-        ec = coarse_correction(levels, rc, omega, nu, _l + 1, _ops, cycle)
+        ec = coarse_correction(levels, rc, omega, nu, _l + 1, _ops, cycle, kmax)
         xf = xf + (lv["P"] @ ec)[free]
         for _ in range(nl):
             xf = xf + w * (bf - A @ xf) / d
@@ -289,7 +292,7 @@ def vcycle(levels, b, omega=None, nu=1, _l=0, _ops=None, cycle="V"):
 
 
 def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
-               max_iter=10000, u0=None, power_steps=8, nu_deep=0, cycle="V", flexible=None):
+               max_iter=10000, u0=None, power_steps=8, nu_deep=0, cycle="V", flexible=None, kmax=None):
     """PCG with the multigrid preconditioner (cycle "V" or "K", M8) on K_ff u_f =
     f_f, stopping on the TRUE relative residual (same loop as solve_jacobi_cg).
     flexible (default: True for the K-cycle) -> Polak-Ribiere beta (M9).
@@ -308,7 +311,7 @@ def solve_mgcg(K, f, fixed, dims, rtol=1e-10, theta=1.6, nu=1, coarse_max=1000,
         return np.zeros(K.shape[0]), 0
 
     def M(r):
-        return vcycle(levels, r, None, nu, 0, ops, cycle)
+        return vcycle(levels, r, None, nu, 0, ops, cycle, kmax)
 
     def res(u):
         r = np.zeros_like(u)

@@ -1277,4 +1277,36 @@ k_mg_coarse_solve(const double* __restrict__ Ainv, int n, int ld, const long lon
   }
 }
 
+// fp32 hierarchy: the coarsest inverse rounded to fp32 (half the bytes: 60 MB at
+// config 4, L2-resident across the K-cycle's repeated coarsest solves); b is
+// gathered once per block into shared memory; fp64 accumulation.
+__global__ void k_mg_inv_to32(const double* __restrict__ A, float* __restrict__ A32, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    A32[i] = (float)A[i];
+}
+__global__ void __launch_bounds__(kBlock)
+k_mg_coarse_solve32(const float* __restrict__ Ainv, int n, int ld, const long long* __restrict__ imap,
+                    const float* __restrict__ b, float* __restrict__ x, const DevState* st) {
+  MG_GATE(st);
+  extern __shared__ float bsh[];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) bsh[j] = b[imap[j]];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < n; r += nwarp) {
+    const float* row = Ainv + (long long)r * ld;
+    double s = 0.0;
+    for (int j = lane * 4; j < n; j += 128) {   // ld is a multiple of 64: 16-byte row chunks
+      const float4 a = *reinterpret_cast<const float4*>(row + j);
+      s = fma((double)a.x, (double)bsh[j], s);
+      if (j + 1 < n) s = fma((double)a.y, (double)bsh[j + 1], s);
+      if (j + 2 < n) s = fma((double)a.z, (double)bsh[j + 2], s);
+      if (j + 3 < n) s = fma((double)a.w, (double)bsh[j + 3], s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[imap[r]] = (float)s;
+  }
+}
+
 }  // namespace topo

@@ -234,6 +234,7 @@ struct topo_ctx {
   double mg_theta = 1.6, mg_theta_b = 1.6;   // smoother theta in use (cut after a breakdown) (+ snapshot)
   std::vector<MgLevel> mg;
   double *mg_tab8 = nullptr, *mg_tab64 = nullptr, *mg_A0 = nullptr;
+  float* mg_A32 = nullptr;           // fp32 copy of the coarsest inverse (fp32 hierarchy)
   double* mg_Eg = nullptr;           // level-2 Galerkin: gathered fine moduli [64][nel_2] (DGEMM operand)
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // symmetric-sweep scratch (C, C P, P)
   int mg_npad = 0;                   // coarsest dense size rounded up to kGjB
@@ -255,6 +256,7 @@ struct topo_ctx {
   long long mg_setup_launches = 0;
   int mg_batch = 2;
   bool mg_kcycle = false;            // K-cycle on the coarse levels + flexible PCG (M8, M9)
+  int mg_kmin = 1, mg_kmax = 99;     // K-cycle levels [kmin, kmax] (TOPO_KMIN / TOPO_KMAX: experiments)
   double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
 };
 
@@ -1016,8 +1018,12 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   // (a larger exact coarse solve cuts MG-PCG iterations; its dense inverse is
   // only worth it on large grids)
   const long long ndof0 = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
+  // (K-cycle: 1000 -- the deep levels are solved well by the K-cycle, and a small
+  // coarsest inverse keeps the per-design setup cheap; V-cycle: a larger exact
+  // coarse solve cuts iterations on large grids)
+  const bool kc = P.mg_cycle == TOPO_MG_KCYCLE && P.mg_nu == 1;
   const long long coarse_max = P.mg_coarse_max > 0 ? P.mg_coarse_max
-                                                   : std::min<long long>(5000, std::max<long long>(1000, ndof0 / 2000));
+                               : kc ? 1000 : std::min<long long>(5000, std::max<long long>(1000, ndof0 / 2000));
   {
     H h{P.nelx, P.nely, P.nelz, {}};
     const long long nn = (long long)(h.nx + 1) * (h.ny + 1) * (h.nz + 1);
@@ -1065,6 +1071,12 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   ctx->mg_on = true;
   ctx->mg_f32 = P.mg_fp32 != 0;
   ctx->mg_kcycle = P.mg_cycle == TOPO_MG_KCYCLE && P.mg_nu == 1;
+  // K-cycle levels (M8): 1 .. L-2, except that on hierarchies of 6+ levels the
+  // level just above the coarsest keeps a single cycle (measured at config 4:
+  // same PCG iteration counts, 0.8 ms less per iteration)
+  ctx->mg_kmax = L >= 6 ? L - 3 : L - 2;
+  if (const char* e = getenv("TOPO_KMIN")) ctx->mg_kmin = atoi(e);
+  if (const char* e = getenv("TOPO_KMAX")) ctx->mg_kmax = atoi(e);
   ctx->mg_theta = P.mg_omega;
   ctx->mg.resize(L);
   auto al = [&](void** p, size_t bytes) -> int {
@@ -1133,6 +1145,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     ctx->mg_npad = (ctx->mg_n + kGjB - 1) / kGjB * kGjB;
     const size_t np = (size_t)ctx->mg_npad;
     CK(al((void**)&ctx->mg_A0, sizeof(double) * np * np));
+    CK(al((void**)&ctx->mg_A32, sizeof(float) * np * np));
     CK(al((void**)&ctx->mg_C, sizeof(double) * np * kGjB));
     CK(al((void**)&ctx->mg_R, sizeof(double) * np * kGjB));
     CK(al((void**)&ctx->mg_P, sizeof(double) * kGjB * kGjB));
@@ -1187,6 +1200,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   return TOPO_OK;
 }
 
+constexpr long long kMgDeepNodes = 150000;   // "small" coarse levels (deep sweeps, warp-split stencil kernel)
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
 constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
                                        // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
@@ -1350,6 +1364,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
     LAUNCH(ctx, k_sw_put_panel, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
   }
   LAUNCH(ctx, k_sw_finish, grid_for((long long)np * np), A, np);
+  if (sizeof(T) == 4) LAUNCH(ctx, k_mg_inv_to32, grid_for((long long)np * np), A, ctx->mg_A32, (long long)np * np);
   return check_launch(ctx);
 }
 
@@ -1434,7 +1449,12 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   MgLevel& m = ctx->mg[l];
   const DevState* gst = gate ? s.st : nullptr;
   if (m.stored) {
-    if (m.S) LAUNCH(ctx, k_mg_apply_st<T>, grid_for(m.L.nodes()), m.L, mgp<T>(m.S), mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);
+    static const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
+                                                                          : kMgDeepNodes;
+    if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16), m.L,
+             mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
+    else if (m.S) LAUNCH(ctx, k_mg_apply_st<T>, grid_for(m.L.nodes()), m.L, mgp<T>(m.S), mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);
     else LAUNCH(ctx, k_mg_apply_asm<T>, grid_for(m.L.nodes()), m.L, m.K, mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);   // coarsest (hook)
     return check_launch(ctx);
   }
@@ -1447,7 +1467,6 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
 
 // smoothing sweeps on level l (reading M5): mg_nu, or mg_nu_deep on the small
 // coarse levels (auto: 8 when the fine grid is large enough that they are cheap)
-constexpr long long kMgDeepNodes = 150000;
 int mg_level_nu(const topo_ctx* ctx, int l) {
   const topo_params& P = ctx->prm;
   if (l == 0 || ctx->mg[l].L.nodes() > kMgDeepNodes) return P.mg_nu;
@@ -1472,8 +1491,16 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   const double* om = ctx->mg_om + l;
   if (l == L - 1) {
     const MgLevel& c = ctx->mg[l];
-    LAUNCH(ctx, k_mg_coarse_solve<T>, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_npad, ctx->mg_imap,
-           mgp<T>(c.b), mgp<T>(c.x), gst);
+    static const bool c32 = !getenv("TOPO_COARSE32") || atoi(getenv("TOPO_COARSE32")) != 0;
+    if (sizeof(T) == 4 && c32) {
+      const int nb = (int)std::min<long long>(148LL * 2, (32LL * ctx->mg_n + kBlock - 1) / kBlock);
+      k_mg_coarse_solve32<<<nb, kBlock, sizeof(float) * ctx->mg_n, ctx->stream>>>(
+          ctx->mg_A32, ctx->mg_n, ctx->mg_npad, ctx->mg_imap, (const float*)c.b, (float*)c.x, gst);
+      ctx->launches++;
+      debug_sync(ctx, "k_mg_coarse_solve32");
+    } else
+      LAUNCH(ctx, k_mg_coarse_solve<T>, grid_for(32LL * ctx->mg_n), mg_Ainv(ctx), ctx->mg_n, ctx->mg_npad,
+             ctx->mg_imap, mgp<T>(c.b), mgp<T>(c.x), gst);
     return check_launch(ctx);
   }
   MgLevel& n1 = ctx->mg[l + 1];
@@ -1624,7 +1651,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
 template <typename T>
 int enqueue_coarse_t(topo_ctx* ctx, int l, int gate) {
   const int L = (int)ctx->mg.size();
-  if (!ctx->mg_kcycle || l >= L - 1) return enqueue_vcycle_t<T>(ctx, l, gate, false);
+  if (!ctx->mg_kcycle || l >= L - 1 || l < ctx->mg_kmin || l > ctx->mg_kmax) return enqueue_vcycle_t<T>(ctx, l, gate, false);
   Slab& s = ctx->slabs[0];
   MgLevel& m = ctx->mg[l];
   const DevState* gst = gate ? s.st : nullptr;
@@ -2228,7 +2255,7 @@ void free_ctx(topo_ctx* ctx) {
   }
   {
     void* ptrs[] = {ctx->mg_tab8, ctx->mg_tab64, ctx->mg_Eg, ctx->mg_A0, ctx->mg_C, ctx->mg_R, ctx->mg_P, ctx->mg_ws,
-                    ctx->mg_dmap, ctx->mg_imap, ctx->mg_om, ctx->mg_kc};
+                    ctx->mg_dmap, ctx->mg_imap, ctx->mg_om, ctx->mg_kc, ctx->mg_A32};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }

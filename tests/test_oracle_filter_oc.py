@@ -167,3 +167,23 @@ def test_filter_rows_equal_matrix():
         row = H.getrow(i)
         assert dict(zip(cols.tolist(), w.tolist())) == pytest.approx(dict(zip(row.indices.tolist(), row.data.tolist())))
     assert np.allclose(hs, Hs[rows], rtol=1e-15)
+
+
+@pytest.mark.parametrize("dims,rmin", [((7, 6, 5), 2.5), ((9, 4, 3), 4.0), ((8, 5, 4), 3.0), ((6, 4, 3), 1.5)])
+def test_apply_filter_rows_equals_matrix_filter(dims, rmin):
+    """The row-wise (H-free) filter used at full size equals the sparse-H filter,
+    every mode and operand, on every row; hs_elements equals H's row sums."""
+    from oracle import apply_filter_rows, hs_elements
+    from workloads import solid_block_passive
+    H, Hs = filter_matrix(*dims, rmin)
+    n = H.shape[0]
+    rows = np.arange(n)
+    assert np.allclose(hs_elements(*dims, rmin, rows), Hs, rtol=1e-14, atol=0)
+    pas = solid_block_passive(*dims, (0, 2), (0, 2), (0, dims[2]), base=(dims[0] - 1.0, dims[1] - 1.0, 1.2))
+    x = random_density(n, seed=21, lo=1e-4, hi=1.0)
+    v = -random_density(n, seed=22, lo=0.1, hi=3.0)
+    for mode in (0, 1, 2):
+        for what in ("dc", "dv", "x"):
+            ref = apply_filter(H, Hs, mode, what, v if what != "x" else x, x=x, passive=pas)
+            got = apply_filter_rows(*dims, rmin, mode, what, rows, v if what != "x" else x, x=x, passive=pas)
+            assert np.allclose(got, ref, rtol=1e-13, atol=1e-15), (mode, what)

@@ -63,8 +63,12 @@ def make_vcycle(levels, ops, lams, spec):
     def coarse(rc, l):
         """approximate A_{l}^{-1} rc for a coarse level l >= 1 (full-length vector)."""
         A, d, free = ops[l]
-        kmax = int(CYCLE[1:]) if CYCLE.startswith("K") and len(CYCLE) > 1 else 99
-        if l == L - 1 or CYCLE == "V" or l > kmax:
+        kmin, kmax = 1, 99
+        if CYCLE.startswith("K") and "-" in CYCLE:
+            kmin, kmax = (int(v) for v in CYCLE[1:].split("-"))
+        elif CYCLE.startswith("K") and len(CYCLE) > 1:
+            kmax = int(CYCLE[1:])
+        if l == L - 1 or CYCLE == "V" or l > kmax or l < kmin:
             return V(rc, l)
         if CYCLE == "W":
             x = V(rc, l)
