@@ -28,7 +28,7 @@ differences).  Parity unpinned: absolute agreement with the paper's own runs
 from .mesh import edof_matrix, edof_matrix_loops, element_centroids  # noqa: F401
 from .ke import element_stiffness, lame  # noqa: F401
 from .fem import (assemble, solve, solve_direct, solve_jacobi_cg, compliance_fu,  # noqa: F401
-                  element_energies, matvec_free, matvec_elementwise, matvec_rows, diag_K,
+                  element_energies, element_energies_strain, matvec_free, matvec_elementwise, matvec_rows, diag_K,
                   true_residual)
 from .filt import (filter_matrix, filter_matrix_allpairs, apply_filter, filter_rows,  # noqa: F401
                    hs_elements, apply_filter_rows)

@@ -94,6 +94,26 @@ def element_energies(u, KE, edof):
     return np.einsum("ei,ij,ej->e", ue, KE, ue)
 
 
+def element_energies_strain(ue, nu):
+    """ce_e = sum over the 2x2x2 Gauss points of (1/8) eps^T D eps with eps = B u_e
+    -- the element strain energy from its definition (§2.3: ce = u_e^T KE u_e,
+    KE = sum_gp (1/8) B^T D B, oracle.ke), evaluated through the strains.  Equal
+    to element_energies in exact arithmetic; better conditioned when u_e is
+    nearly rigid (B annihilates translations exactly: the shape-gradient rows
+    cancel pairwise), which is how large displacements with little strain look
+    on a cantilever.  ue: [n, 24] element DOF vectors."""
+    from .ke import constitutive, strain_displacement
+    D = constitutive(1.0, nu)
+    pts = (0.5 - 0.5 / np.sqrt(3.0), 0.5 + 0.5 / np.sqrt(3.0))
+    ce = np.zeros(ue.shape[0])
+    for xi in pts:
+        for eta in pts:
+            for zeta in pts:
+                eps = ue @ strain_displacement(xi, eta, zeta).T          # [n, 6]
+                ce += 0.125 * np.einsum("ei,ij,ej->e", eps, D, eps)
+    return ce
+
+
 def matvec_free(K, p, fixed):
     """q = K p with the Dirichlet mask: q_f = K_ff p_f, q = 0 on fixed DOFs."""
     fx = np.asarray(fixed) != 0

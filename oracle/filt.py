@@ -140,12 +140,22 @@ def apply_filter_rows(nelx, nely, nelz, rmin, mode, what, rows, v, x=None, passi
     if what == "dv" and mode != 0:
         return v[rows].copy()
     acc = np.zeros(rows.size)
+    hs_of = None
+    if what in ("dc", "dv") and mode == 0:       # Hs of every neighbour, computed once per distinct element
+        allj = []
+        for k in range(w.size):
+            jx, jy, jz = ex + dx[k], ey + dy[k], ez + dz[k]
+            ok = (jx >= 0) & (jx < nelx) & (jy >= 0) & (jy < nely) & (jz >= 0) & (jz < nelz)
+            allj.append((jz * nelx * nely + jx * nely + jy)[ok])
+        uj = np.unique(np.concatenate(allj))
+        hs_u = hs_elements(nelx, nely, nelz, rmin, uj)
+        hs_of = lambda j: hs_u[np.searchsorted(uj, j)]  # noqa: E731
     for k in range(w.size):
         jx, jy, jz = ex + dx[k], ey + dy[k], ez + dz[k]
         ok = (jx >= 0) & (jx < nelx) & (jy >= 0) & (jy < nely) & (jz >= 0) & (jz < nelz)
         j = np.where(ok, jz * nelx * nely + jx * nely + jy, 0)
         if what in ("dc", "dv") and mode == 0:
-            term = v[j] / hs_elements(nelx, nely, nelz, rmin, j)        # H (v / Hs)
+            term = np.where(ok, v[j] / np.where(ok, hs_of(np.where(ok, j, uj[0])), 1.0), 0.0)   # H (v / Hs)
         elif mode == 1:
             term = np.asarray(x)[j] * v[j]                              # H (x v)
         else:

@@ -1309,4 +1309,58 @@ k_mg_coarse_solve32(const float* __restrict__ Ainv, int n, int ld, const long lo
   }
 }
 
+// ---------------------------------------------------------------------------
+// Dense fp64 "NT" product with an inner dimension of 64 (hand-written; replaces
+// the cuBLAS DGEMM / DSYRKX calls of round 1):
+//   Cm[i + j ldc] = beta Cm[..] + alpha sum_{t < 64} A[i + t lda] B[j + t ldb]
+// for i < M, j < N (lower = 1: only i >= j).  Column-major like BLAS.  Uses:
+//   level-2 Galerkin   K2 = Eg tab64^T            (M = nel_2, N = 576)
+//   symmetric sweep    CP = C P  (P symmetric)    (M = n_pad, N = 64)
+//                      S -= C (CP)^T, lower       (M = N = n_pad)
+// A 64 x 64 output tile per 256-thread block, 4 x 4 outputs per thread, the
+// 64-deep operands staged in shared memory in two halves.
+// ---------------------------------------------------------------------------
+constexpr int kNtTile = 64;
+__global__ void __launch_bounds__(256)
+k_dgemm_nt64(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
+             double* __restrict__ Cm, long long ldc, int M, int N, double alpha, double beta, int lower) {
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (lower && bj > bi) return;
+  __shared__ double As[32][kNtTile + 1], Bs[32][kNtTile + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int i0 = bi * kNtTile, j0 = bj * kNtTile;
+  double acc[4][4] = {};
+  for (int h = 0; h < 2; ++h) {
+    for (int q = tid; q < 32 * kNtTile; q += 256) {   // q = t * 64 + r: r fastest (coalesced)
+      const int r = q & (kNtTile - 1), t = q >> 6;
+      const int ia = i0 + r, jb = j0 + r;
+      As[t][r] = ia < M ? A[ia + (long long)(h * 32 + t) * lda] : 0.0;
+      Bs[t][r] = jb < N ? B[jb + (long long)(h * 32 + t) * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[t][ty * 4 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[t][tx * 4 + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty * 4 + a, j = j0 + tx * 4 + b;
+      if (i >= M || j >= N || (lower && i < j)) continue;
+      double* c = Cm + i + (long long)j * ldc;
+      *c = beta == 0.0 ? alpha * acc[a][b] : fma(alpha, acc[a][b], beta * *c);
+    }
+}
+
 }  // namespace topo

@@ -75,43 +75,6 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
-// Minimal cuBLAS binding (dlopen): DGEMM and DSYRKX (a triangular GEMM) for the
-// rank-kGjB updates of the blocked symmetric-sweep inverse of the coarsest
-// multigrid matrix and the level-2 Galerkin product (plain library GEMMs; every
-// other step runs in this library's kernels).
-typedef struct cublasContext* cublasHandle_t;
-struct CublasApi {
-  void* h = nullptr;
-  int (*Create)(cublasHandle_t*) = nullptr;
-  int (*Destroy)(cublasHandle_t) = nullptr;
-  int (*SetStream)(cublasHandle_t, cudaStream_t) = nullptr;
-  int (*SetWorkspace)(cublasHandle_t, void*, size_t) = nullptr;
-  int (*Dgemm)(cublasHandle_t, int, int, int, int, int, const double*, const double*, int, const double*, int,
-               const double*, double*, int) = nullptr;
-  int (*Dsyrkx)(cublasHandle_t, int, int, int, int, const double*, const double*, int, const double*, int,
-                const double*, double*, int) = nullptr;   // triangular rank-k update (symmetric result)
-  bool load(std::string& err) {
-    if (h) return true;
-    const char* cands[] = {"libcublas.so.12", "libcublas.so",
-                           "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib/libcublas.so.12"};
-    for (const char* c : cands) {
-      h = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
-      if (h) break;
-    }
-    if (!h) { err = "cannot dlopen libcublas.so.12"; return false; }
-#define LD(name, sym) name = reinterpret_cast<decltype(name)>(dlsym(h, sym)); if (!name) { err = "missing " sym; return false; }
-    LD(Create, "cublasCreate_v2");
-    LD(Destroy, "cublasDestroy_v2");
-    LD(SetStream, "cublasSetStream_v2");
-    LD(SetWorkspace, "cublasSetWorkspace_v2");
-    LD(Dgemm, "cublasDgemm_v2");
-    LD(Dsyrkx, "cublasDsyrkx");
-#undef LD
-    return true;
-  }
-};
-CublasApi g_cublas;
-constexpr int CUBLAS_OP_N_ = 0, CUBLAS_OP_T_ = 1;
 
 struct TopoError {
   int code;
@@ -238,7 +201,6 @@ struct topo_ctx {
   double* mg_Eg = nullptr;           // level-2 Galerkin: gathered fine moduli [64][nel_2] (DGEMM operand)
   double *mg_C = nullptr, *mg_R = nullptr, *mg_P = nullptr, *mg_ws = nullptr;   // symmetric-sweep scratch (C, C P, P)
   int mg_npad = 0;                   // coarsest dense size rounded up to kGjB
-  cublasHandle_t cublas = nullptr;
   double mg_diag8[8 * 24];
   int mg_n = 0;                      // free DOFs of the coarsest level
   int* mg_dmap = nullptr;            // coarsest: level DOF index -> dense index or -1
@@ -1149,12 +1111,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CK(al((void**)&ctx->mg_C, sizeof(double) * np * kGjB));
     CK(al((void**)&ctx->mg_R, sizeof(double) * np * kGjB));
     CK(al((void**)&ctx->mg_P, sizeof(double) * kGjB * kGjB));
-    const size_t ws = 32u << 20;
-    CK(al((void**)&ctx->mg_ws, ws));
-    std::string err;
-    if (!g_cublas.load(err)) return set_err(ctx, TOPO_ECUDA, "%s", err.c_str());
-    if (g_cublas.Create(&ctx->cublas) != 0) return set_err(ctx, TOPO_ECUDA, "cublasCreate failed");
-    if (g_cublas.SetWorkspace(ctx->cublas, ctx->mg_ws, ws) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetWorkspace failed");
+
 
   }
   for (Slab& s : ctx->slabs) {
@@ -1250,11 +1207,10 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       // K2 = Eg tab64^T: gather the 64 fine moduli per element, then one DGEMM
       // (nel x 64) x (64 x 576) into the entry-major [576][nel] layout
       LAUNCH(ctx, k_mg_gather64, grid_for(64 * ne), mgG(ctx), m.L, mgE(ctx), ctx->mg_Eg);
-      if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
-      const double d1 = 1.0, d0 = 0.0;
-      if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_T_, (int)ne, 576, 64, &d1, ctx->mg_Eg, (int)ne,
-                         ctx->mg_tab64, 576, &d0, m.K, (int)ne) != 0)
-        return set_err(ctx, TOPO_ECUDA, "cublasDgemm (level-2 Galerkin) failed");
+      k_dgemm_nt64<<<dim3(576 / kNtTile, (unsigned)((ne + kNtTile - 1) / kNtTile)), 256, 0, ctx->stream>>>(
+          ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0, 0.0, 0);
+      ctx->launches++;
+      debug_sync(ctx, "k_dgemm_nt64(level-2 Galerkin)");
     } else {
       const MgLevel& f = ctx->mg[l - 1];
       {   // tiled Galerkin product (k_mg_asm_galerkin_t), 8 coarse elements per CTA
@@ -1347,20 +1303,20 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   CU(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)np * np, ctx->stream));
   LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, np, A);
   if (np > n) LAUNCH(ctx, k_gj_pad, 1, A, n, np);
-  // A <- A^-1 in place (coarsest dense inverse, reading M6)
-  if (g_cublas.SetStream(ctx->cublas, ctx->stream) != 0) return set_err(ctx, TOPO_ECUDA, "cublasSetStream failed");
-  const double d_one = 1.0, d_mone = -1.0, d_zero = 0.0;
-  // symmetric blocked sweep (mg.cuh): lower triangle, SYRKX rank-64 updates
+  // A <- A^-1 in place (coarsest dense inverse, reading M6): symmetric blocked
+  // sweep (mg.cuh), lower triangle, rank-64 updates by k_dgemm_nt64
+  const unsigned nT = (unsigned)((np + kNtTile - 1) / kNtTile);
   for (int k0 = 0; k0 < np; k0 += kGjB) {
     k_sw_block_inv<<<1, kGjB * kGjB / kGjInvNJ, 0, ctx->stream>>>(A, np, k0, ctx->mg_P);
     ctx->launches++;
     LAUNCH(ctx, k_sw_take_col, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_C);
-    // CP = C P  (n_pad x b)
-    if (g_cublas.Dgemm(ctx->cublas, CUBLAS_OP_N_, CUBLAS_OP_N_, np, kGjB, kGjB, &d_one, ctx->mg_C, np, ctx->mg_P, kGjB,
-                       &d_zero, ctx->mg_R, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDgemm (C P) failed");
+    // CP = C P  (n_pad x b; P symmetric, so C P = C P^T)
+    k_dgemm_nt64<<<dim3(1, nT), 256, 0, ctx->stream>>>(ctx->mg_C, np, ctx->mg_P, kGjB, ctx->mg_R, np, np, kGjB, 1.0,
+                                                      0.0, 0);
     // S -= C (C P)^T on the lower triangle (rows / columns K untouched: C_K,: = 0)
-    if (g_cublas.Dsyrkx(ctx->cublas, 0 /* lower */, CUBLAS_OP_N_, np, kGjB, &d_mone, ctx->mg_C, np, ctx->mg_R, np,
-                        &d_one, A, np) != 0) return set_err(ctx, TOPO_ECUDA, "cublasDsyrkx failed");
+    k_dgemm_nt64<<<dim3(nT, nT), 256, 0, ctx->stream>>>(ctx->mg_C, np, ctx->mg_R, np, A, np, np, np, -1.0, 1.0, 1);
+    ctx->launches += 2;
+    debug_sync(ctx, "k_dgemm_nt64(sweep)");
     LAUNCH(ctx, k_sw_put_panel, grid_for((long long)np * kGjB), A, np, k0, ctx->mg_R, ctx->mg_P);
   }
   LAUNCH(ctx, k_sw_finish, grid_for((long long)np * np), A, np);
@@ -2261,7 +2217,6 @@ void free_ctx(topo_ctx* ctx) {
   }
   if (ctx->mg_setup_exec) cudaGraphExecDestroy(ctx->mg_setup_exec);
   if (ctx->mg_setup_exec_w) cudaGraphExecDestroy(ctx->mg_setup_exec_w);
-  if (ctx->cublas) g_cublas.Destroy(ctx->cublas);
   if (ctx->mg_gE) cudaFree(ctx->mg_gE);
   if (ctx->mg_E32) cudaFree(ctx->mg_E32);
   for (cudaGraphExec_t g : ctx->cg_exec)

@@ -169,3 +169,25 @@ def test_matvec_rows_equals_csr():
     from oracle import matvec_rows
     nodes = np.arange(0, K.shape[0] // 3, 7)
     assert np.allclose(matvec_rows(*dims, KE, E, p, fixed, nodes), q.reshape(-1, 3)[nodes], rtol=0, atol=1e-14)
+
+
+def test_element_energies_strain_form():
+    """The strain form of ce (sum_gp eps^T D eps / 8) equals u_e^T KE u_e, and a
+    rigid translation has zero energy in it to rounding (closed form)."""
+    import oracle
+    from oracle import element_energies_strain
+    KE = oracle.element_stiffness(0.3)
+    rng = np.random.default_rng(8)
+    ue = rng.standard_normal((500, 24))
+    ce1 = np.einsum("ei,ij,ej->e", ue, KE, ue)
+    ce2 = element_energies_strain(ue, 0.3)
+    assert np.allclose(ce2, ce1, rtol=1e-12, atol=0)
+    t = np.tile([3.7, -1.1, 250.0], 8)[None, :]
+    assert element_energies_strain(t, 0.3)[0] <= 1e-30 * float(t @ t.T)      # zero up to rounding
+    # uniform strain u = (x, 0, 0): energy lambda + 2 mu (closed form, unit cube)
+    from oracle.mesh import LOCAL_NODES
+    lam, mu = oracle.lame(1.0, 0.3)
+    u = np.zeros((1, 24))
+    for a, (ax, ay, az) in enumerate(LOCAL_NODES):
+        u[0, 3 * a] = ax
+    assert element_energies_strain(u, 0.3)[0] == pytest.approx(lam + 2 * mu, rel=1e-14)
