@@ -32,6 +32,7 @@
  *    entries of other ranks are left untouched (gathering is the caller's job).
  *    TOPO_DIST_LOOPBACK runs `world` slabs in ONE process on one GPU (tests
  *    the partition and halo logic); outputs are then complete.
+ *    TOPO_DIST_HOST: like NCCL (one process per slab), host-staged transport.
  *  - Threading: one context per thread; distinct contexts are independent.
  *  - Call order: init -> [set_density] -> solve -> sensitivity -> filter(dc)
  *    -> oc_step.  A call whose inputs are not ready returns TOPO_ESTATE.
@@ -87,6 +88,7 @@ extern "C" {
 #define TOPO_DIST_SINGLE   0
 #define TOPO_DIST_NCCL     1
 #define TOPO_DIST_LOOPBACK 2
+#define TOPO_DIST_HOST     3   /* one process per slab, host-staged shared-memory transport (tests) */
 
 typedef struct topo_ctx topo_ctx;    /* opaque; owns all device state */
 
@@ -158,7 +160,9 @@ typedef struct {
   int32_t mode;               /* TOPO_DIST_SINGLE / _NCCL / _LOOPBACK                       */
   int32_t rank, world;        /* NCCL: this rank, #ranks; LOOPBACK: world = #slabs          */
   int32_t device;             /* CUDA device ordinal of this rank                            */
-  const uint8_t *nccl_id;     /* NCCL: 128-byte ncclUniqueId broadcast by the caller         */
+  const uint8_t *nccl_id;     /* NCCL: 128-byte ncclUniqueId broadcast by the caller;
+                                 HOST: the 128-byte id of topo_host_transport_id (same on
+                                 every rank)                                                 */
 } topo_dist;
 
 typedef struct {
@@ -330,6 +334,16 @@ int64_t topo_count(const topo_ctx *ctx, int32_t what);
 #define TOPO_COUNT_DESIGN      3
 #define TOPO_COUNT_STENCIL     4   /* filter stencil points                   */
 #define TOPO_COUNT_DEVICE_BYTES 5  /* device memory held by the context        */
+
+/* TOPO_DIST_HOST helper: a fresh 128-byte transport id (a POSIX shared-memory
+ * name) that rank 0 creates and broadcasts to the other ranks.  The host
+ * transport runs the same per-rank control flow as NCCL (one slab per process,
+ * only owned planes) with every exchange staged through pinned host memory and
+ * a process-shared barrier: stream-ordered and CUDA-graph capturable, for
+ * testing the x-slab path with several processes on one GPU.  Timeouts (and
+ * NCCL asynchronous errors) surface as TOPO_ENCCL after TOPO_COMM_TIMEOUT
+ * seconds (env, default 300) instead of hanging.                            */
+int topo_host_transport_id(uint8_t *out128);
 
 /* NCCL mode helper: fill a 128-byte ncclUniqueId (rank 0 calls it and
  * broadcasts the bytes, e.g. with torch.distributed).  ENCCL if libnccl.so.2

@@ -1363,4 +1363,58 @@ k_dgemm_nt64(const double* __restrict__ A, long long lda, const double* __restri
     }
 }
 
+// Same product on the fp64 tensor cores (DMMA, mma.sync m8n8k4 .f64) for the
+// large level-2 Galerkin product (M = nel_2 = 524 288 at config 4, N = 576):
+// block tile 128 (M) x 64 (N), 8 warps of 32 x 32 (4 x 4 m8n8 tiles, 32
+// accumulators per thread), the whole 64-deep operands in shared memory.
+// N must be a multiple of 64 (576 is); beta = 0, no triangle.
+constexpr int kTcM = 128, kTcN = 64, kTcK = 64, kTcPadA = kTcM + 1, kTcPadB = kTcN + 1;
+constexpr int kTcSmem = (kTcK * kTcPadA + kTcK * kTcPadB) * 8;
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256)
+k_dgemm_nt64_tc(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
+                double* __restrict__ Cm, long long ldc, int M, int N, double alpha) {
+  extern __shared__ double tsm[];
+  double* As = tsm;                       // [t][i], pitch kTcPadA
+  double* Bs = tsm + kTcK * kTcPadA;      // [t][j], pitch kTcPadB
+  const int i0 = blockIdx.y * kTcM, j0 = blockIdx.x * kTcN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int q = tid; q < kTcK * kTcM; q += 256) {
+    const int r = q & (kTcM - 1), t = q / kTcM;
+    As[t * kTcPadA + r] = (i0 + r) < M ? A[(i0 + r) + (long long)t * lda] : 0.0;
+  }
+  for (int q = tid; q < kTcK * kTcN; q += 256) {
+    const int r = q & (kTcN - 1), t = q / kTcN;
+    Bs[t * kTcPadB + r] = (j0 + r) < N ? B[(j0 + r) + (long long)t * ldb] : 0.0;
+  }
+  __syncthreads();
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;   // 4 x 2 warps
+  const int g = lane >> 2, tg = lane & 3;
+  double acc[4][4][2] = {};
+  for (int k0 = 0; k0 < kTcK; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = As[(k0 + tg) * kTcPadA + wm + mi * 8 + g];   // A(row g, col tg)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k0 + tg) * kTcPadB + wn + ni * 8 + g];   // B(row tg, col g)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni], a[mi], b[ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + wm + mi * 8 + g, j = j0 + wn + ni * 8 + tg * 2 + e;   // C(row g, col 2 tg + e)
+        if (i < M && j < N) Cm[i + (long long)j * ldc] = alpha * acc[mi][ni][e];
+      }
+}
+
 }  // namespace topo

@@ -20,6 +20,8 @@
 #include "matvec_wht.cuh"
 #include "mg.cuh"
 #include "filter25.cuh"
+#include "host_transport.h"
+#include <chrono>
 
 namespace topo {
 void build_element_stiffness(double nu, double* ke);  // ke_host.cpp
@@ -50,6 +52,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;   // optional
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                          // optional
   bool load(std::string& err) {
     if (h) return true;
     const char* cands[] = {"libnccl.so.2", "libnccl.so",
@@ -70,6 +74,8 @@ struct NcclApi {
     LD(GroupEnd, "ncclGroupEnd");
     LD(GetErrorString, "ncclGetErrorString");
 #undef LD
+    CommGetAsyncError = reinterpret_cast<decltype(CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    CommAbort = reinterpret_cast<decltype(CommAbort)>(dlsym(h, "ncclCommAbort"));
     return true;
   }
 };
@@ -142,6 +148,9 @@ struct topo_ctx {
   std::vector<Slab> slabs;
   cudaStream_t stream = nullptr, own_stream = nullptr;
   ncclComm_t comm = nullptr;
+  HostTransport* ht = nullptr;          // TOPO_DIST_HOST: shared-memory transport
+  std::deque<HostOp> hops;              // host nodes' userData (alive as long as the graphs)
+  double comm_timeout_s = 300.0;        // NCCL / host transport: give up (TOPO_ENCCL) after this long
   double ke[576];
   double kd = 0.0;
   WhtK wht{};
@@ -153,6 +162,7 @@ struct topo_ctx {
   std::vector<int> st_poff;   // filter offsets in the padded layout (FiltPad)
   int R = 0;
   unsigned f25_attr_mask = 0;   // k_filt25 dynamic-smem opt-in done (bit per device x mode)
+  bool tc_attr_set = false;     // k_dgemm_nt64_tc dynamic-smem opt-in done (this context's device)
   long long n_design = 0;   // global design-element count
   double bb = 0.0;          // ||f_free||^2
   // state flags
@@ -365,9 +375,29 @@ Material material(const topo_ctx* ctx) {
 // ---------------------------------------------------------------------------
 // Communication across slabs (loopback: in-process copies; NCCL: send/recv)
 // ---------------------------------------------------------------------------
+void CUDART_CB host_op_cb(void* p) { host_op_run(static_cast<HostOp*>(p)); }
+
+int host_launch(topo_ctx* ctx, const HostOp& op) {
+  ctx->hops.push_back(op);
+  CU(cudaLaunchHostFunc(ctx->stream, host_op_cb, &ctx->hops.back()));
+  return TOPO_OK;
+}
+
 int allreduce(topo_ctx* ctx, int k0, int nk, int maxmask) {
   const int W = ctx->world;
   if (W == 1) return TOPO_OK;
+  if (ctx->mode == TOPO_DIST_HOST) {
+    DevState* st = ctx->slabs[0].st;
+    CU(cudaMemcpyAsync(ctx->ht->hsend, st->sums + k0, sizeof(double) * nk, cudaMemcpyDeviceToHost, ctx->stream));
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 1;
+    op.n = nk;
+    op.maxmask = (unsigned)maxmask;
+    CK(host_launch(ctx, op));
+    CU(cudaMemcpyAsync(st->sums + k0, ctx->ht->hrecv, sizeof(double) * nk, cudaMemcpyHostToDevice, ctx->stream));
+    return TOPO_OK;
+  }
   if (ctx->mode == TOPO_DIST_LOOPBACK) {
     StatePtrs sp{};
     for (int s = 0; s < W; ++s) sp.s[s] = ctx->slabs[s].st;
@@ -415,6 +445,29 @@ int exchange_nodes(topo_ctx* ctx, double* Slab::*field, int ncomp = 3) {
   }
   Slab& a = ctx->slabs[0];
   const size_t n = a.g.nplane;
+  if (ctx->mode == TOPO_DIST_HOST) {
+    double *hs = ctx->ht->hsend, *hr = ctx->ht->hrecv;
+    const size_t b = sizeof(double) * n;
+    for (int c = 0; c < ncomp; ++c) {
+      double* v = a.*field + c * a.g.ncomp;
+      if (ctx->rank > 0) CU(cudaMemcpyAsync(hs + (2 * c) * n, v + a.g.nplane, b, cudaMemcpyDeviceToHost, ctx->stream));
+      if (ctx->rank < W - 1)
+        CU(cudaMemcpyAsync(hs + (2 * c + 1) * n, v + a.g.nown * a.g.nplane, b, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 0;
+    op.len = (long long)n;
+    op.nblk = ncomp;
+    CK(host_launch(ctx, op));
+    for (int c = 0; c < ncomp; ++c) {
+      double* v = a.*field + c * a.g.ncomp;
+      if (ctx->rank > 0) CU(cudaMemcpyAsync(v, hr + (2 * c) * n, b, cudaMemcpyHostToDevice, ctx->stream));
+      if (ctx->rank < W - 1)
+        CU(cudaMemcpyAsync(v + (a.g.nown + 1) * a.g.nplane, hr + (2 * c + 1) * n, b, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return TOPO_OK;
+  }
   NC(g_nccl.GroupStart());
   for (int c = 0; c < ncomp; ++c) {
     double* v = a.*field + c * a.g.ncomp;
@@ -458,6 +511,23 @@ int exchange_elems(topo_ctx* ctx, double* Slab::*field, int k) {
   Slab& a = ctx->slabs[0];
   const size_t n = a.g.eplane * k;
   double* v = a.*field;
+  if (ctx->mode == TOPO_DIST_HOST) {
+    double *hs = ctx->ht->hsend, *hr = ctx->ht->hrecv;
+    const size_t b = sizeof(double) * n;
+    if (ctx->rank > 0) CU(cudaMemcpyAsync(hs, v + a.g.H * a.g.eplane, b, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->rank < W - 1)
+      CU(cudaMemcpyAsync(hs + n, v + (a.g.H + a.g.nex - k) * a.g.eplane, b, cudaMemcpyDeviceToHost, ctx->stream));
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 0;
+    op.len = (long long)n;
+    op.nblk = 1;
+    CK(host_launch(ctx, op));
+    if (ctx->rank > 0) CU(cudaMemcpyAsync(v + (a.g.H - k) * a.g.eplane, hr, b, cudaMemcpyHostToDevice, ctx->stream));
+    if (ctx->rank < W - 1)
+      CU(cudaMemcpyAsync(v + (a.g.H + a.g.nex) * a.g.eplane, hr + n, b, cudaMemcpyHostToDevice, ctx->stream));
+    return TOPO_OK;
+  }
   NC(g_nccl.GroupStart());
   if (ctx->rank > 0) {
     NC(g_nccl.Send(v + a.g.H * a.g.eplane, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream));
@@ -643,10 +713,47 @@ void fill_local_elems_u8(const topo_ctx* ctx, const Slab& s, const uint8_t* glob
   }
 }
 
+// Wait for the bound stream.  Multi-process transports poll instead of blocking:
+// NCCL's asynchronous error state (ncclCommGetAsyncError; the communicator is
+// aborted on an error) and a timeout, so a dead peer becomes TOPO_ENCCL instead
+// of a hang; the host transport reports a peer timeout the same way.
+int wait_stream(topo_ctx* ctx) {
+  const bool nccl = ctx->mode == TOPO_DIST_NCCL && ctx->comm;
+  if (!nccl && !ctx->ht) {
+    CU(cudaStreamSynchronize(ctx->stream));
+    return TOPO_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  long long spins = 0;
+  while (true) {
+    const cudaError_t e = cudaStreamQuery(ctx->stream);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return set_err(ctx, TOPO_ECUDA, "stream: %s", cudaGetErrorString(e));
+    if (nccl && g_nccl.CommGetAsyncError) {
+      ncclResult_t ar = 0;
+      if (g_nccl.CommGetAsyncError(ctx->comm, &ar) == 0 && ar != 0 && ar != 7 /* ncclInProgress */) {
+        if (g_nccl.CommAbort) g_nccl.CommAbort(ctx->comm);
+        ctx->comm = nullptr;
+        return set_err(ctx, TOPO_ENCCL, "NCCL asynchronous error: %s", g_nccl.GetErrorString(ar));
+      }
+    }
+    if (ctx->ht && ctx->ht->failed.load()) return set_err(ctx, TOPO_ENCCL, "host transport: a peer timed out");
+    if (++spins > 256) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > ctx->comm_timeout_s) {
+        if (nccl && g_nccl.CommAbort) { g_nccl.CommAbort(ctx->comm); ctx->comm = nullptr; }
+        return set_err(ctx, TOPO_ENCCL, "collective timeout after %.0f s (dead peer?)", el);
+      }
+      sched_yield();
+    }
+  }
+  if (ctx->ht && ctx->ht->failed.load()) return set_err(ctx, TOPO_ENCCL, "host transport: a peer timed out");
+  return TOPO_OK;
+}
+
 int sync_state(topo_ctx* ctx) {
   CU(cudaMemcpyAsync(ctx->hstate, ctx->slabs[0].st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  return TOPO_OK;
+  return wait_stream(ctx);
 }
 
 // ---------------------------------------------------------------------------
@@ -942,6 +1049,23 @@ int mg_gather_E(topo_ctx* ctx) {
     return TOPO_OK;
   }
   Slab& a = ctx->slabs[0];
+  if (ctx->mode == TOPO_DIST_HOST) {   // all-gather of the owned planes through the shared segment
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 3;
+    for (int r = 0; r < ctx->world; ++r) {
+      int b = 0, e = 0;
+      topo_partition(ctx->prm.nelx, ctx->prm.rmin, ctx->world, r, &b, &e);
+      op.cnt[r] = (long long)(e - b) * G.eplane;
+      op.off[r] = (long long)b * G.eplane;
+    }
+    CU(cudaMemcpyAsync(ctx->ht->hsend, a.E + (size_t)a.g.H * a.g.eplane, sizeof(double) * a.g.nex * a.g.eplane,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(host_launch(ctx, op));
+    CU(cudaMemcpyAsync(dst(0), ctx->ht->hrecv, sizeof(double) * (size_t)G.nex * G.eplane, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    return TOPO_OK;
+  }
   CU(cudaMemcpyAsync(dst(a.g.ex0), a.E + (size_t)a.g.H * a.g.eplane, sizeof(double) * a.g.nex * a.g.eplane,
                      cudaMemcpyDeviceToDevice, ctx->stream));
   NC(g_nccl.GroupStart());
@@ -960,6 +1084,17 @@ int mg_gather_E(topo_ctx* ctx) {
 // x-slabs, NCCL: sum of the slabs' partial level-1 restrictions (in place)
 int mg_allreduce_level(topo_ctx* ctx, void* buf, size_t n, bool f32) {
   if (ctx->world == 1 || ctx->mode == TOPO_DIST_LOOPBACK) return TOPO_OK;   // loopback: accumulated in slab order
+  if (ctx->mode == TOPO_DIST_HOST) {
+    const size_t es = f32 ? sizeof(float) : sizeof(double);
+    CU(cudaMemcpyAsync(ctx->ht->hsend, buf, es * n, cudaMemcpyDeviceToHost, ctx->stream));
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = f32 ? 2 : 1;
+    op.n = (long long)n;
+    CK(host_launch(ctx, op));
+    CU(cudaMemcpyAsync(buf, ctx->ht->hrecv, es * n, cudaMemcpyHostToDevice, ctx->stream));
+    return TOPO_OK;
+  }
   NC(g_nccl.AllReduce(buf, buf, n, f32 ? ncclFloat32 : ncclFloat64, ncclSum, ctx->comm, ctx->stream));
   return TOPO_OK;
 }
@@ -1207,10 +1342,14 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       // K2 = Eg tab64^T: gather the 64 fine moduli per element, then one DGEMM
       // (nel x 64) x (64 x 576) into the entry-major [576][nel] layout
       LAUNCH(ctx, k_mg_gather64, grid_for(64 * ne), mgG(ctx), m.L, mgE(ctx), ctx->mg_Eg);
-      k_dgemm_nt64<<<dim3(576 / kNtTile, (unsigned)((ne + kNtTile - 1) / kNtTile)), 256, 0, ctx->stream>>>(
-          ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0, 0.0, 0);
+      if (!ctx->tc_attr_set) {
+        CU(cudaFuncSetAttribute(k_dgemm_nt64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+        ctx->tc_attr_set = true;
+      }
+      k_dgemm_nt64_tc<<<dim3(576 / kTcN, (unsigned)((ne + kTcM - 1) / kTcM)), 256, kTcSmem, ctx->stream>>>(
+          ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0);
       ctx->launches++;
-      debug_sync(ctx, "k_dgemm_nt64(level-2 Galerkin)");
+      debug_sync(ctx, "k_dgemm_nt64_tc(level-2 Galerkin)");
     } else {
       const MgLevel& f = ctx->mg[l - 1];
       {   // tiled Galerkin product (k_mg_asm_galerkin_t), 8 coarse elements per CTA
@@ -2145,6 +2284,32 @@ int optimize_loop(topo_ctx* ctx, int n_iter, double change_tol, double* c_hist, 
   return rc;
 }
 
+// TOPO_DIST_HOST: mailbox = the largest message any step sends (all ranks agree:
+// global sizes only), pinned staging of the same size
+int open_host_transport(topo_ctx* ctx, const topo_dist* dist) {
+  const Slab& a = ctx->slabs[0];
+  long long mb = 32 * 8;                                             // scalar allreduces
+  mb = std::max<long long>(mb, 8LL * 6 * a.g.nplane);                // node halo, 3 components
+  mb = std::max<long long>(mb, 8LL * 2 * a.g.H * a.g.eplane);        // element halo
+  for (int r = 0; r < ctx->world; ++r) {                             // moduli all-gather / planes
+    int b = 0, e = 0;
+    topo_partition(ctx->prm.nelx, ctx->prm.rmin, ctx->world, r, &b, &e);
+    mb = std::max<long long>(mb, 8LL * (e - b) * a.g.eplane);
+  }
+  mb = std::max<long long>(mb, 8LL * ctx->prm.nelx * a.g.eplane);   // the gathered whole-grid moduli (recv side)
+  if (ctx->mg_on && ctx->mg.size() > 1) mb = std::max<long long>(mb, 8LL * 3 * ctx->mg[1].L.ncomp);   // level-1 allreduce
+  char name[129];
+  memcpy(name, dist->nccl_id, 128);
+  name[128] = 0;
+  ctx->ht = new HostTransport();
+  ctx->ht->timeout_s = ctx->comm_timeout_s;
+  std::string err;
+  if (!ctx->ht->open(name, ctx->rank, ctx->world, mb, err)) return set_err(ctx, TOPO_ENCCL, "%s", err.c_str());
+  CU(cudaMallocHost(&ctx->ht->hsend, (size_t)ctx->ht->mbox));
+  CU(cudaMallocHost(&ctx->ht->hrecv, (size_t)ctx->ht->mbox));
+  return TOPO_OK;
+}
+
 int alloc_slab(topo_ctx* ctx, Slab& s) {
   const Geo& g = s.g;
   auto al = [&](void** p, size_t bytes) -> int {
@@ -2234,6 +2399,12 @@ void free_ctx(topo_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->hstate) cudaFreeHost(ctx->hstate);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->ht) {
+    if (ctx->ht->hsend) cudaFreeHost(ctx->ht->hsend);
+    if (ctx->ht->hrecv) cudaFreeHost(ctx->ht->hrecv);
+    ctx->ht->close_all();
+    delete ctx->ht;
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (g_const_owner == ctx) g_const_owner = nullptr;
   delete ctx;
@@ -2336,6 +2507,14 @@ int topo_nccl_unique_id(uint8_t* out128) {
   return TOPO_OK;
 }
 
+int topo_host_transport_id(uint8_t* out128) {
+  if (!out128) return TOPO_EINVAL;
+  memset(out128, 0, 128);
+  const unsigned long long t = (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count();
+  snprintf(reinterpret_cast<char*>(out128), 128, "/topo_%d_%llx", (int)getpid(), t);
+  return TOPO_OK;
+}
+
 int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, const uint8_t* passive,
               const topo_dist* dist, topo_ctx** out) {
   if (!out) return TOPO_EINVAL;
@@ -2385,6 +2564,11 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   }
   if (rc == TOPO_OK && (ctx->world < 1 || ctx->world > 16 || ctx->rank < 0 || ctx->rank >= ctx->world))
     rc = set_err(ctx, TOPO_EINVAL, "bad rank/world");
+  if (const char* e = getenv("TOPO_COMM_TIMEOUT")) ctx->comm_timeout_s = atof(e);
+  if (rc == TOPO_OK && ctx->mode == TOPO_DIST_HOST && (!dist || !dist->nccl_id))
+    rc = set_err(ctx, TOPO_EINVAL, "TOPO_DIST_HOST needs the transport id (topo_host_transport_id) in nccl_id");
+  if (rc == TOPO_OK && (ctx->mode < TOPO_DIST_SINGLE || ctx->mode > TOPO_DIST_HOST))
+    rc = set_err(ctx, TOPO_EINVAL, "bad dist mode %d", ctx->mode);
   if (rc == TOPO_OK && ctx->mode == TOPO_DIST_SINGLE && ctx->world != 1)
     rc = set_err(ctx, TOPO_EINVAL, "TOPO_DIST_SINGLE needs world == 1");
   // --- KE and filter stencil (host precompute) ---
@@ -2442,8 +2626,9 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
     if (r != 0) { rc = set_err(ctx, TOPO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); free_ctx(ctx); return rc; }
   }
   // local slabs
-  const int s_begin = (ctx->mode == TOPO_DIST_NCCL) ? ctx->rank : 0;
-  const int s_end = (ctx->mode == TOPO_DIST_NCCL) ? ctx->rank + 1 : W;
+  const bool own_only = ctx->mode == TOPO_DIST_NCCL || ctx->mode == TOPO_DIST_HOST;   // one slab per process
+  const int s_begin = own_only ? ctx->rank : 0;
+  const int s_end = own_only ? ctx->rank + 1 : W;
   for (int s = s_begin; s < s_end; ++s) {
     Slab sl;
     Geo& g = sl.g;
@@ -2510,6 +2695,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   }
   rc = upload_nodes(ctx, load, &Slab::f);
   if (rc == TOPO_OK) rc = mg_build(ctx, fixed);
+  if (rc == TOPO_OK && ctx->mode == TOPO_DIST_HOST && W > 1) rc = open_host_transport(ctx, dist);
   if (rc == TOPO_OK) rc = ensure_constants(ctx);
   if (rc == TOPO_OK) {
     // ||f_free||^2 and filter row sums Hs (all local in-domain elements)

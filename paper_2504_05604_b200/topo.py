@@ -20,7 +20,7 @@ TOPO_FILTER_DENSITY, TOPO_FILTER_SENSITIVITY, TOPO_FILTER_PLAIN = 0, 1, 2
 TOPO_FILTER_X, TOPO_FILTER_DC = 0, 1
 FIELDS = dict(u=0, x=1, xphys=2, E=3, ce=4, dc=5, dcf=6, dvf=7, xnew=8, hs=9, invdiag=10, r=11)
 NODE_FIELDS = {"u", "invdiag", "r"}
-TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK = 0, 1, 2
+TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK, TOPO_DIST_HOST = 0, 1, 2, 3
 TOPO_PRECOND_JACOBI, TOPO_PRECOND_MG, TOPO_PRECOND_AUTO = 0, 1, 2
 PRECOND = dict(jacobi=0, mg=1, auto=2)
 COUNTS = dict(ndof=0, nel=1, nodes=2, design=3, stencil=4, device_bytes=5)
@@ -36,7 +36,7 @@ EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_ra
            # _d variants: device pointers + cudaStream_t
            "topo_init_d", "topo_set_density_d", "topo_set_xphys_d", "topo_solve_d",
            "topo_sensitivity_d", "topo_filter_d", "topo_oc_step_d", "topo_optimize_d",
-           "topo_apply_K_d", "topo_get_d"]
+           "topo_apply_K_d", "topo_get_d", "topo_host_transport_id"]
 
 
 class topo_params(C.Structure):
@@ -109,6 +109,7 @@ def _load():
         "topo_version": (C.c_char_p, []),
         "topo_destroy": (None, [ctxp]),
         "topo_nccl_unique_id": (I, [U8]),
+        "topo_host_transport_id": (I, [U8]),
         "topo_snapshot": (I, [ctxp]),
         "topo_restore": (I, [ctxp]),
         "topo_partition": (I, [C.c_int32, C.c_double, C.c_int32, C.c_int32, P(C.c_int32), P(C.c_int32)]),
@@ -186,6 +187,16 @@ def nccl_unique_id():
     rc = _lib.topo_nccl_unique_id(_u8(buf))
     if rc:
         raise TopoError(rc, "topo_nccl_unique_id")
+    return bytes(buf)
+
+
+def host_transport_id():
+    """128-byte id of a fresh host-staged transport (TOPO_DIST_HOST); rank 0
+    creates it and passes it to every rank as dist["nccl_id"]."""
+    buf = np.zeros(128, dtype=np.uint8)
+    rc = _lib.topo_host_transport_id(_u8(buf))
+    if rc:
+        raise TopoError(rc, "topo_host_transport_id")
     return bytes(buf)
 
 
