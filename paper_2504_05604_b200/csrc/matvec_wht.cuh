@@ -121,7 +121,16 @@ struct MvEpi {
   const double* qk;         // kEpi = 1: if set, the PCG's q = K p of this iteration; the
                             // epilogue also reduces q.out for the flexible (Polak-Ribiere)
                             // beta = -alpha (q.z)/rz of the K-cycle PCG (reading M9)
+  // kEpi = 4 (A5 sensitivities, vin = u): per owned element ce = u_e^T KE u_e =
+  // P^T B P in the Walsh basis, dc = -p xPhys^(p-1) (E0 - Emin) ce (0 on passive),
+  // and c = sum E ce reduced into st->sums[0]; no node output
+  double* ce;
+  double* dc;
+  const double* xphys;
+  const uint8_t* passive;
+  double penal, dE;         // p, E0 - Emin
 };
+__device__ __forceinline__ double simp_pow(double x, double p);   // kernels.cuh
 
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
 // TV: element type of the vin tile (double; float for the post-smoothing
@@ -310,7 +319,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0, eq[3] = {0.0, 0.0, 0.0};
   uint8_t efm = 0;
   auto epi_load = [&](long long go) {
-    if (kEpi != 0 && owned) {
+    if (kEpi != 0 && kEpi != 4 && owned) {
       efm = epi.fixm[go];
       if (kEpi == 1) einv = epi.invd[go];
       if (kEpi == 1 || kEpi == 2)
@@ -337,6 +346,37 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     const TC Ee = Ecur;
     if (t + 1 < nunits) Ecur = prepass(t + 1);
     TC Q[3][8];
+    if (kEpi == 4) {   // element energy of element plane ex (owned elements only)
+      TC P[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          P[c][2 * k] = G0[c][k] + G1[c][k];
+          P[c][2 * k + 1] = G0[c][k] - G1[c][k];
+        }
+      wht_block(P, TC(1), Q);
+      const int exe = xs - 2 + t;
+      if (ty >= 1 && tz >= 1 && iyb < g.nely && izb < g.nelz && exe >= xs && exe < g.ex0 + g.nex) {
+        double sce = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) sce = fma((double)P[c][k], (double)Q[c][k], sce);
+        const long long ie = (long long)(exe - g.ex0 + g.H) * g.eplane + (long long)(izb + 1) * g.EY + (iyb + 1);
+        epi.ce[ie] = sce;
+        const double xp = epi.xphys[ie];
+        epi.dc[ie] = epi.passive[ie] ? 0.0 : -epi.penal * simp_pow(xp, epi.penal - 1.0) * epi.dE * sce;
+        dot = fma((double)Ee, sce, dot);
+      }
+      __syncthreads();
+      if (t + 1 < nunits) release(t + 1);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) G0[c][k] = G1[c][k];
+      continue;
+    }
     {
       TC P[3][8];
 #pragma unroll
@@ -410,7 +450,11 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       }
   }
 
-  if (kEpi == 1) {
+  if (kEpi == 4) {
+    __shared__ double tot4[1];
+    double vv[1] = {dot};
+    if (grid_reduce<1>(vv, partials, counter, tot4) && leader) st->sums[0] = tot4[0];
+  } else if (kEpi == 1) {
     __shared__ double tot[2];
     double vv[2] = {dot, dot2};
     if (grid_reduce<2>(vv, partials, counter, tot) && leader) {

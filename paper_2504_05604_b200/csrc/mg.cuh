@@ -177,10 +177,11 @@ k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const TF* __restrict__ res, cons
 // ---------------------------------------------------------------------------
 // Prolongation  xF (+)= mask_F( P eC ).  Thread per fine node (<= 8 sources).
 // ---------------------------------------------------------------------------
+// (xin != nullptr: out of place, xF = xin + P eC)
 template <bool kAdd, typename TC, typename TF>
 __global__ void __launch_bounds__(kBlock)
 k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
-             TF* __restrict__ xF, const DevState* st) {
+             TF* __restrict__ xF, const DevState* st, const TF* __restrict__ xin = nullptr) {
   MG_GATE(st);
   const long long tot = F.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -205,7 +206,7 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const long long o = i + c * F.ncomp;
-      xF[o] = (TF)(kAdd ? (double)xF[o] + v[c] : v[c]);
+      xF[o] = (TF)(kAdd ? (double)(xin ? xin[o] : xF[o]) + v[c] : v[c]);
     }
   }
 }
@@ -325,6 +326,56 @@ k_mg_jacobi(LvGeo L, const T* __restrict__ b, const T* __restrict__ q,
         st->beta = st->fresh ? 0.0 : rho / st->rz;
         st->rz = rho;
       }
+    }
+  }
+}
+
+// Small coarse levels: the same restriction with a WARP per coarse node (lane
+// d < 27 takes fine neighbour d of the 3x3x3 box), partial sums combined by a
+// fixed shuffle tree -- the thread-per-node loop is a 27-step latency chain
+// with a handful of blocks on the deep levels (9-11 us per launch).
+template <bool kResid, typename TF, typename TC>
+__global__ void __launch_bounds__(kBlock)
+k_mg_restrict_w(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict__ qF,
+                const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, TC* __restrict__ bC,
+                const DevState* st) {
+  MG_GATE(st);
+  const long long tot = Cg.nodes();
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int dx = lane < 27 ? lane / 9 - 1 : 0, dz = lane < 27 ? (lane / 3) % 3 - 1 : 0, dy = lane < 27 ? lane % 3 - 1 : 0;
+  const double w = lane < 27 ? (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0) * (dz ? 0.5 : 1.0) : 0.0;
+  for (long long k = w0; k < tot; k += nw) {
+    int jx, jy, jz;
+    lv_decode(Cg, k, jx, jy, jz);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const int ix = 2 * jx + dx, iy = 2 * jy + dy, iz = 2 * jz + dz;
+    if (lane < 27 && ix >= 0 && ix <= F.nx && iy >= 0 && iy <= F.ny && iz >= 0 && iz <= F.nz) {
+      const long long i = F.n(ix, iy, iz);
+      const uint8_t fm = fixF[i];
+      double v0 = (double)bF[i], v1 = (double)bF[i + F.ncomp], v2 = (double)bF[i + 2 * F.ncomp];
+      if (kResid) {
+        v0 -= qF[i];
+        v1 -= qF[i + F.ncomp];
+        v2 -= qF[i + 2 * F.ncomp];
+      }
+      s0 = (fm & 1) ? 0.0 : w * v0;
+      s1 = (fm & 2) ? 0.0 : w * v1;
+      s2 = (fm & 4) ? 0.0 : w * v2;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane == 0) {
+      const long long j = Cg.n(jx, jy, jz);
+      const uint8_t fc = fixC[j];
+      bC[j] = (TC)((fc & 1) ? 0.0 : s0);
+      bC[j + Cg.ncomp] = (TC)((fc & 2) ? 0.0 : s1);
+      bC[j + 2 * Cg.ncomp] = (TC)((fc & 4) ? 0.0 : s2);
     }
   }
 }
@@ -1027,11 +1078,14 @@ k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
 // meet in shared memory and warp 0 finishes the node (fixed order).
 //   kFused = false: dst = mask(A src)
 //   kFused = true : dst = mask(src + w D^-1 (b - A src))   (dst != src)
-template <bool kFused, typename T>
+//   kFromB (with kFused = false): src is the first sweep from 0, x = w D^-1 b, formed
+//     on the fly from b and D^-1 (0 on fixed DOFs); xout = x, dst = mask(A x) --
+//     one launch instead of a Jacobi kernel plus the stencil apply
+template <bool kFused, typename T, bool kFromB = false>
 __global__ void __launch_bounds__(256, 4)
 k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
                const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
-               T* __restrict__ dst, const DevState* st) {
+               T* __restrict__ dst, const DevState* st, T* __restrict__ xout = nullptr) {
   MG_GATE(st);
   __shared__ double part[8][3][32];
   const long long tot = L.nodes();
@@ -1055,7 +1109,17 @@ k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, cons
         const bool back = t >= 14;
         const long long j = back ? i - d : i + d;
         const T* sb = S + (long long)((bb - 13) * 9) * L.ncomp + (back ? j : i);
-        const double x0 = (double)src[j], x1 = (double)src[j + L.ncomp], x2 = (double)src[j + 2 * L.ncomp];
+        double x0, x1, x2;
+        if (kFromB) {   // x = w D^-1 b rounded to T, as the Jacobi kernel would store it
+          const double om = *omp;
+          x0 = (double)(T)(om * (double)invd[j] * (double)b[j]);
+          x1 = (double)(T)(om * (double)invd[j + L.ncomp] * (double)b[j + L.ncomp]);
+          x2 = (double)(T)(om * (double)invd[j + 2 * L.ncomp] * (double)b[j + 2 * L.ncomp]);
+        } else {
+          x0 = (double)src[j];
+          x1 = (double)src[j + L.ncomp];
+          x2 = (double)src[j + 2 * L.ncomp];
+        }
         double m[9];
 #pragma unroll
         for (int e = 0; e < 9; ++e) m[e] = (double)sb[(long long)e * L.ncomp];
@@ -1091,6 +1155,7 @@ k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, cons
         double v = av[c];
         if (kFused) v = fma(omega * (double)invd[o], (double)b[o] - v, (double)src[o]);
         dst[o] = ((fm >> c) & 1) ? T(0) : (T)v;
+        if (kFromB) xout[o] = ((fm >> c) & 1) ? T(0) : (T)(*omp * (double)invd[o] * (double)b[o]);
       }
     }
     __syncthreads();

@@ -909,7 +909,8 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
   // kEpi = 1 with the K-cycle: the PCG's q (untouched by the V-cycle: the fp32
   // pre-smoothing residual goes to res32, the fp64 one to z) for the flexible beta
   const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr,
-                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr};
+                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr, s.ce, s.dc, s.xphys, s.passive, ctx->prm.penal,
+                  ctx->prm.E0 - ctx->prm.Emin};
   k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew,
                                                                                  q, s.partials, s.counter, finish,
                                                                                  scale, epi);
@@ -1560,6 +1561,19 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   return check_launch(ctx);
 }
 
+// b_{l+1} = P^T (b - t) on a coarse level: warp per coarse node on small levels
+template <typename T>
+int launch_restrict(topo_ctx* ctx, const LvGeo& F, const LvGeo& C, const T* b, const T* t, const uint8_t* ff,
+                    const uint8_t* fc, T* bc, const DevState* gst) {
+  if (C.nodes() <= 20000) {
+    const int nb = (int)std::min<long long>((C.nodes() * 32 + kBlock - 1) / kBlock, 148LL * 8);
+    LAUNCH(ctx, (k_mg_restrict_w<true, T, T>), nb, F, C, b, t, ff, fc, bc, gst);
+  } else {
+    LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(C.nodes()), F, C, b, t, ff, fc, bc, gst);
+  }
+  return check_launch(ctx);
+}
+
 // smoothing sweeps on level l (reading M5): mg_nu, or mg_nu_deep on the small
 // coarse levels (auto: 8 when the fine grid is large enough that they are cheap)
 int mg_level_nu(const topo_ctx* ctx, int l) {
@@ -1697,6 +1711,16 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // small stencil level: each damped-Jacobi sweep is one fused warp-split
     // stencil kernel (k_mg_sweep_st8) ping-ponging x and t
     const int gS = (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16);   // 32 nodes per block
+    if (nu == 1) {
+      // x = w D^-1 b and t = A x in one launch; restrict; correct; t = x + P e
+      // (out of place) and the sweep x = t + w D^-1 (b - A t) in one launch
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
+      CK(launch_restrict<T>(ctx, m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b), gst));
+      CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
+      LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mt, gst, (const T*)mx);
+      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
+      return check_launch(ctx);
+    }
     T* buf[2] = {mx, mt};
     int cur = (nu - 1) & 1;   // the last pre-smoothing sweep lands in x
     LAUNCH(ctx, (k_mg_jacobi<0, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, buf[cur], s.st, gate, s.partials,
@@ -1704,8 +1728,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     for (int k = 1; k < nu; ++k, cur ^= 1)
       LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), buf[cur], mb, mi, m.fixm, om, buf[cur ^ 1], gst);
     LAUNCH(ctx, (k_mg_sweep_st8<false, T>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst);   // t = A x
-    LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm,
-           mgp<T>(n1.b), gst);
+    CK(launch_restrict<T>(ctx, m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b), gst));
     CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
     LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
     int k = 0;
@@ -1724,8 +1747,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     LAUNCH(ctx, (k_mg_jacobi<1, false, T>), gL, m.L, mb, mt, mi, m.fixm, om, mx, s.st, gate, s.partials, s.counter);
   }
   CK(mg_apply<T>(ctx, l, gate));
-  LAUNCH(ctx, (k_mg_restrict<true, T, T>), grid_for(n1.L.nodes()), m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b),
-         gst);
+  CK(launch_restrict<T>(ctx, m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b), gst));
   CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
   LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mx, gst);
   for (int k = 1; k <= nu; ++k) {
@@ -1988,9 +2010,13 @@ int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
   CK(ensure_constants(ctx));
   CK(exchange_nodes(ctx, &Slab::u));
   const Material m = material(ctx);
+  static const bool sens_mv = !getenv("TOPO_SENS_MV") || atoi(getenv("TOPO_SENS_MV")) != 0;
   for (Slab& s : ctx->slabs) {
-    LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
-           s.passive, s.ce, s.dc, s.partials, s.counter);
+    if (sens_mv)   // the matvec's x-marching TMA structure with the energy epilogue (kEpi = 4)
+      CK((launch_mv<0, false, 4>(ctx, s, 0, s.m_u, nullptr, nullptr, nullptr, 0)));
+    else
+      LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
+             s.passive, s.ce, s.dc, s.partials, s.counter);
     LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.u, 1, s.partials, s.counter);
   }
   CK(check_launch(ctx));
