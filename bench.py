@@ -425,9 +425,14 @@ def main():
         #   <0,0,1> post  w = z + w D^-1 (r - K z), r.w  : read z 12 (fp32 hierarchy: z stored in fp32) /
         #                                                  24 + r 24 + D^-1 8 + mask 1, write w 24 B/node
         # each + E (8 B/el)
+        #   (round 2: with the fp32 hierarchy on one slab the V-cycle output w is stored in
+        #   fp32 -- PCG reads w 12 B/node, post writes it 12 B/node -- and the K-cycle's
+        #   flexible beta reads q (24 B/node) in the post-smoothing epilogue)
         f32 = int(p.get("mg_fp32", 1)) != 0
-        var = [("k_mv_wht<8,2,1,0>", 96, kt[0]), ("k_mv_wht<8,3,0,2>", 45 if f32 else 57, kt[1]),
-               ("k_mv_wht<8,0,0,1>", 69 if f32 else 81, kt[2])]
+        w32 = f32 and world == 1
+        kc = int(p.get("mg_cycle", 1)) != 0
+        var = [("k_mv_wht<8,2,1,0>", 84 if w32 else 96, kt[0]), ("k_mv_wht<8,3,0,2>", 45 if f32 else 57, kt[1]),
+               ("k_mv_wht<8,0,0,1>", (57 if w32 else 69 if f32 else 81) + (24 if kc else 0), kt[2])]
         per = [{"kernel": n, "bytes_per_launch": b * own_nd + 8 * own_el, "mean_ms": t[0], "samples": t[1],
                 "achieved": (b * own_nd + 8 * own_el) / (t[0] * 1e-3) / 1e9 if t[0] > 0 else None}
                for n, b, t in var]

@@ -118,12 +118,18 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
 // r is 0 on fixed DOFs (q comes unmasked from the matvec); partial
 // (r M^{-1} r, r r).  double2 over pairs of nodes of the owned planes (pads
 // are zero and stay zero).  Saves one read+write of u every second iteration.
-template <bool kU, bool kMG>
+// TK: type of r and q (double; float for the fp32 Krylov vectors of the
+// multigrid PCG, SURVEY f3 -- the true residual is always fp64, so the fp32
+// recursion only decides when to check it)
+template <typename TK> struct Vec2T { using t = double2; };
+template <> struct Vec2T<float> { using t = float2; };
+template <bool kU, bool kMG, typename TK = double>
 __global__ void __launch_bounds__(kBlock, 2)
-k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
-         const double* __restrict__ pprev, const double* __restrict__ p, const double* __restrict__ q,
+k_update(Geo g, DevState* st, double* __restrict__ u, TK* __restrict__ r,
+         const double* __restrict__ pprev, const double* __restrict__ p, const TK* __restrict__ q,
          const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* partials,
          unsigned int* counter, int finish) {
+  using V2 = typename Vec2T<TK>::t;
   if (st->done) return;
   const double alpha = st->alpha, alpha_prev = kU ? st->alpha_prev : 0.0;
   const long long b0 = g.nplane, npair = (long long)g.nown * g.nplane / 2;
@@ -132,7 +138,8 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
   constexpr int UN = kU ? 1 : 2;            // pairs per thread per trip: all loads issued first
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long j0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; j0 < npair; j0 += UN * stride) {
-    double2 rv[UN][3], qq[UN][3], uu[UN][3], p0[UN][3], pp[UN][3], iv[UN];
+    V2 rv[UN][3], qq[UN][3];
+    double2 uu[UN][3], p0[UN][3], pp[UN][3], iv[UN];
     uchar2 fm[UN];
     bool ok[UN];
 #pragma unroll
@@ -145,8 +152,8 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const long long k = i + c * nc;
-        rv[w][c] = *reinterpret_cast<const double2*>(r + k);
-        qq[w][c] = *reinterpret_cast<const double2*>(q + k);
+        rv[w][c] = *reinterpret_cast<const V2*>(r + k);
+        qq[w][c] = *reinterpret_cast<const V2*>(q + k);
         if (kU) {
           uu[w][c] = *reinterpret_cast<const double2*>(u + k);
           p0[w][c] = *reinterpret_cast<const double2*>(pprev + k);
@@ -168,12 +175,12 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
           un.y = fma(alpha, pp[w][c].y, fma(alpha_prev, p0[w][c].y, uu[w][c].y));
           *reinterpret_cast<double2*>(u + k) = un;
         }
-        double2 rn;
-        rn.x = (fm[w].x >> c) & 1 ? 0.0 : fma(-alpha, qq[w][c].x, rv[w][c].x);
-        rn.y = (fm[w].y >> c) & 1 ? 0.0 : fma(-alpha, qq[w][c].y, rv[w][c].y);
-        *reinterpret_cast<double2*>(r + k) = rn;
-        s0 = fma(rn.x, rn.x, s0);
-        s1 = fma(rn.y, rn.y, s1);
+        V2 rn;
+        rn.x = (TK)((fm[w].x >> c) & 1 ? 0.0 : fma(-alpha, (double)qq[w][c].x, (double)rv[w][c].x));
+        rn.y = (TK)((fm[w].y >> c) & 1 ? 0.0 : fma(-alpha, (double)qq[w][c].y, (double)rv[w][c].y));
+        *reinterpret_cast<V2*>(r + k) = rn;
+        s0 = fma((double)rn.x, (double)rn.x, s0);
+        s1 = fma((double)rn.y, (double)rn.y, s1);
       }
       if (!kMG) rz = fma(s0, iv[w].x, fma(s1, iv[w].y, rz));
       rr += s0 + s1;
@@ -185,6 +192,12 @@ k_update(Geo g, DevState* st, double* __restrict__ u, double* __restrict__ r,
     if (finish) cg_finish_update<kMG>(st, tot[0], tot[1], kU ? 0 : 1);
     else { st->sums[0] = tot[0]; st->sums[1] = tot[1]; }
   }
+}
+
+// dst = (double) src over a whole buffer (the fp32 Krylov residual back into r after a solve)
+__global__ void k_f2d(long long n, const float* __restrict__ src, double* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = (double)src[i];
 }
 
 // u += alpha_prev p (the deferred half-step) when the solve stops after an even slot
@@ -227,9 +240,10 @@ __global__ void k_finish_rho(DevState* st, int flex) {
 
 // r = f - q, 0 on fixed DOFs (q arrives unmasked from the matvec); partial
 // (r M^{-1} r, r r).  Used at PCG start and for the true-residual check.
+template <typename TK = double>
 __global__ void __launch_bounds__(kBlock)
 k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __restrict__ q,
-           const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* __restrict__ r,
+           const double* __restrict__ invd, const uint8_t* __restrict__ fixm, TK* __restrict__ r,
            int write_r, double* partials, unsigned int* counter) {
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   double rz = 0.0, rr = 0.0;
@@ -240,8 +254,11 @@ k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __re
     double s = 0.0;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const double rv = (fm >> c) & 1 ? 0.0 : f[i + c * g.ncomp] - q[i + c * g.ncomp];
-      if (write_r) r[i + c * g.ncomp] = rv;
+      double rv = (fm >> c) & 1 ? 0.0 : f[i + c * g.ncomp] - q[i + c * g.ncomp];
+      if (write_r) {
+        r[i + c * g.ncomp] = (TK)rv;
+        rv = (double)(TK)rv;   // the sums of the vector the recursion continues from
+      }
       s = fma(rv, rv, s);
     }
     rz = fma(s, invd[i], rz);

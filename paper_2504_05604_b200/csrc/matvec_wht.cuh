@@ -118,19 +118,18 @@ struct MvEpi {
   const uint8_t* fixm;      // per node
   float* out32;             // kEpi = 2: if set, the residual is written here in fp32 (the
                             // restriction input of an fp32 multigrid hierarchy)
+  float* w32;               // kEpi = 1: if set, the result is written here in fp32 (the
+                            // fp32 multigrid's V-cycle output, read by the PCG matvec as a
+                            // float TMA tile) instead of the double `q` output
   const double* qk;         // kEpi = 1: if set, the PCG's q = K p of this iteration; the
                             // epilogue also reduces q.out for the flexible (Polak-Ribiere)
                             // beta = -alpha (q.z)/rz of the K-cycle PCG (reading M9)
-  // kEpi = 4 (A5 sensitivities, vin = u): per owned element ce = u_e^T KE u_e =
-  // P^T B P in the Walsh basis, dc = -p xPhys^(p-1) (E0 - Emin) ce (0 on passive),
-  // and c = sum E ce reduced into st->sums[0]; no node output
-  double* ce;
-  double* dc;
-  const double* xphys;
-  const uint8_t* passive;
-  double penal, dE;         // p, E0 - Emin
+  // fp32 Krylov vectors: if set, b is read from b32 (r in fp32), the
+  // flexible beta's q from qk32, and the PCG matvec (kEpi = 0) writes q to q32
+  const float* b32;
+  const float* qk32;
+  float* q32;
 };
-__device__ __forceinline__ double simp_pow(double x, double p);   // kernels.cuh
 
 constexpr int kMvStages = 3;   // raw TMA stages in flight ahead of the pre-pass
 // TV: element type of the vin tile (double; float for the post-smoothing
@@ -167,7 +166,8 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   constexpr bool kFused = kPre != 0;
   constexpr bool kInvd = kPre == 1 || kPre == 3;
   using L = MvSmem<TZ, TV>;
-  static_assert(sizeof(TV) == 8 || kPre == 0, "a float vin tile is only used by the plain pre-pass");
+  static_assert(sizeof(TV) == 8 || kPre == 0 || kPre == 2 || kPre == 3,
+                "a float vin tile is not used by the Jacobi pre-pass");
   const double beta = (kPre == 1 || kPre == 2) && !st->fresh ? st->beta : 0.0;
   const double wsc = (kPre == 3 || kEpi == 1) ? *scale : 1.0;
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -269,13 +269,22 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         const double iv = si[n];
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], iv * sv[c * CS + n]);
-      } else if (kPre == 2) {
+      } else if (kPre == 2 && sizeof(TV) == 8) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], sv[c * CS + n]);
-      } else if (kPre == 3) {
+      } else if (kPre == 2) {   // V-cycle output w in fp32 (float vin tile, row stride YWV)
+        const int row = n / L::YW, nv = row * L::YWV + (n - row * L::YW) + (yb - ybv);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = fma(beta, sp[c * CS + n], (double)svv[c * CSV + nv]);
+      } else if (kPre == 3 && sizeof(TV) == 8) {
         const double iv = wsc * si[n];
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = iv * sv[c * CS + n];
+      } else if (kPre == 3) {   // fp32 Krylov residual r (float vin tile)
+        const double iv = wsc * si[n];
+        const int row = n / L::YW, nv = row * L::YWV + (n - row * L::YW) + (yb - ybv);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = iv * (double)svv[c * CSV + nv];
       } else if (sizeof(TV) == 8) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[c] = sv[c * CS + n];
@@ -319,13 +328,16 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
   double eb[3] = {0.0, 0.0, 0.0}, einv = 0.0, eq[3] = {0.0, 0.0, 0.0};
   uint8_t efm = 0;
   auto epi_load = [&](long long go) {
-    if (kEpi != 0 && kEpi != 4 && owned) {
+    if (kEpi != 0 && owned) {
       efm = epi.fixm[go];
       if (kEpi == 1) einv = epi.invd[go];
       if (kEpi == 1 || kEpi == 2)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) eb[c] = epi.b[go + c * ncomp];
-      if (kEpi == 1 && epi.qk)
+        for (int c = 0; c < 3; ++c) eb[c] = epi.b32 ? (double)epi.b32[go + c * ncomp] : epi.b[go + c * ncomp];
+      if (kEpi == 1 && epi.qk32)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) eq[c] = (double)epi.qk32[go + c * ncomp];
+      else if (kEpi == 1 && epi.qk)
 #pragma unroll
         for (int c = 0; c < 3; ++c) eq[c] = epi.qk[go + c * ncomp];
     }
@@ -346,37 +358,6 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
     const TC Ee = Ecur;
     if (t + 1 < nunits) Ecur = prepass(t + 1);
     TC Q[3][8];
-    if (kEpi == 4) {   // element energy of element plane ex (owned elements only)
-      TC P[3][8];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          P[c][2 * k] = G0[c][k] + G1[c][k];
-          P[c][2 * k + 1] = G0[c][k] - G1[c][k];
-        }
-      wht_block(P, TC(1), Q);
-      const int exe = xs - 2 + t;
-      if (ty >= 1 && tz >= 1 && iyb < g.nely && izb < g.nelz && exe >= xs && exe < g.ex0 + g.nex) {
-        double sce = 0.0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) sce = fma((double)P[c][k], (double)Q[c][k], sce);
-        const long long ie = (long long)(exe - g.ex0 + g.H) * g.eplane + (long long)(izb + 1) * g.EY + (iyb + 1);
-        epi.ce[ie] = sce;
-        const double xp = epi.xphys[ie];
-        epi.dc[ie] = epi.passive[ie] ? 0.0 : -epi.penal * simp_pow(xp, epi.penal - 1.0) * epi.dE * sce;
-        dot = fma((double)Ee, sce, dot);
-      }
-      __syncthreads();
-      if (t + 1 < nunits) release(t + 1);
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) G0[c][k] = G1[c][k];
-      continue;
-    }
     {
       TC P[3][8];
 #pragma unroll
@@ -411,8 +392,14 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
         // p.q is unaffected.  Keeps a latency-bound byte load off this loop.
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
-          qp[c * ncomp] = qv;
+          double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
+          if (epi.q32) {   // fp32 Krylov q: p.q of exactly the rounded q the update uses
+            const float qf = (float)qv;
+            epi.q32[(qp - q) + c * ncomp] = qf;
+            qv = (double)qf;
+          } else {
+            qp[c * ncomp] = qv;
+          }
           if (kDot) dot = fma(pbase[c], qv, dot);
         }
       } else if (owned && (kEpi == 2 || kEpi == 3)) {
@@ -429,8 +416,14 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double qv = (double)(S[c] + xch[buf][c][tz - 1][ty]);
-          const double zn = ((efm >> c) & 1) ? 0.0 : fma(wd, eb[c] - qv, pbase[c]);
-          qp[c * ncomp] = zn;
+          double zn = ((efm >> c) & 1) ? 0.0 : fma(wd, eb[c] - qv, pbase[c]);
+          if (epi.w32) {   // the V-cycle output stored in fp32 (its precision is the fp32 hierarchy's)
+            const float zf = (float)zn;
+            epi.w32[(qp - q) + c * ncomp] = zf;
+            zn = (double)zf;   // rho and q.w of exactly what the PCG will read
+          } else {
+            qp[c * ncomp] = zn;
+          }
           dot = fma(eb[c], zn, dot);
           dot2 = fma(eq[c], zn, dot2);
         }
@@ -450,11 +443,7 @@ k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int
       }
   }
 
-  if (kEpi == 4) {
-    __shared__ double tot4[1];
-    double vv[1] = {dot};
-    if (grid_reduce<1>(vv, partials, counter, tot4) && leader) st->sums[0] = tot4[0];
-  } else if (kEpi == 1) {
+  if (kEpi == 1) {
     __shared__ double tot[2];
     double vv[2] = {dot, dot2};
     if (grid_reduce<2>(vv, partials, counter, tot) && leader) {

@@ -223,9 +223,9 @@ k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __rest
 // TZo: type of z (float with mg_fp32: the post-smoothing matvec rounds its
 // input to the fp32 operator's precision anyway, so storing z in fp32 changes
 // no result and halves its write and its TMA read).
-template <typename TC, typename TZo = double>
+template <typename TC, typename TZo = double, typename TR = double>
 __global__ void __launch_bounds__(128)
-k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, const double* __restrict__ invd,
+k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const TR* __restrict__ r, const double* __restrict__ invd,
               const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
               TZo* __restrict__ z, const DevState* st, int x0, int pa, int pb) {
   MG_GATE(st);
@@ -262,8 +262,8 @@ k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const double* __restrict__ r, con
     const double d0 = even_ok ? invd[n0] : 0.0, d1 = odd_ok ? invd[n1] : 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      r0[k] = even_ok ? r[n0 + k * F.ncomp] : 0.0;
-      r1[k] = odd_ok ? r[n1 + k * F.ncomp] : 0.0;
+      r0[k] = even_ok ? (double)r[n0 + k * F.ncomp] : 0.0;
+      r1[k] = odd_ok ? (double)r[n1 + k * F.ncomp] : 0.0;
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {

@@ -98,6 +98,7 @@ struct Slab {
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
   float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
   float* z32 = nullptr;                // fp32 multigrid: prolongation output z (post-smoothing input)
+  float* w32 = nullptr;                // fp32 multigrid (one slab): the V-cycle output w (PCG matvec input)
   double *pw0 = nullptr, *pw0_b = nullptr;   // multigrid level-0 power vector (+ snapshot)
   // OC frozen set: per-block active counts / offsets and the compacted (x, A, dv~)
   unsigned *oc_counts = nullptr, *oc_offs = nullptr;
@@ -122,6 +123,7 @@ struct Slab {
   // TMA descriptors of the matvec operands (built at init; pointers never change)
   CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z, m_q;
   CUtensorMap m_z32;   // fp32 z (multigrid, mg_fp32)
+  CUtensorMap m_w32;   // fp32 w (multigrid, mg_fp32, one slab)
   CUtensorMap m_vpad;  // padded filter operand (k_filt25), box (32+2R) x (32+2R) x 1
 };
 
@@ -228,6 +230,7 @@ struct topo_ctx {
   long long mg_setup_launches = 0;
   int mg_batch = 2;
   bool mg_kcycle = false;            // K-cycle on the coarse levels + flexible PCG (M8, M9)
+  bool w32_off = false;              // the V-cycle output stays double (test hook)
   int mg_kmin = 1, mg_kmax = 99;     // K-cycle levels [kmin, kmax] (TOPO_KMIN / TOPO_KMAX: experiments)
   double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
 };
@@ -759,6 +762,11 @@ int sync_state(topo_ctx* ctx) {
 // ---------------------------------------------------------------------------
 // Phase pieces
 // ---------------------------------------------------------------------------
+// The V-cycle output w in fp32: with the fp32 hierarchy on one slab (its
+// precision is the fp32 levels' anyway; the PCG's own vectors stay fp64).
+// Off inside the topo_mg_vcycle test hook (it downloads the double w).
+bool w32_active(const topo_ctx* ctx) { return ctx->mg_f32 && ctx->world == 1 && !ctx->w32_off && ctx->slabs[0].w32; }
+
 int update_modulus(topo_ctx* ctx) {
   CK(ensure_constants(ctx));
   const Material m = material(ctx);
@@ -909,8 +917,8 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
   // kEpi = 1 with the K-cycle: the PCG's q (untouched by the V-cycle: the fp32
   // pre-smoothing residual goes to res32, the fp64 one to z) for the flexible beta
   const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr,
-                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr, s.ce, s.dc, s.xphys, s.passive, ctx->prm.penal,
-                  ctx->prm.E0 - ctx->prm.Emin};
+                  (kEpi == 1 && w32_active(ctx)) ? s.w32 : nullptr,
+                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr};
   k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew,
                                                                                  q, s.partials, s.counter, finish,
                                                                                  scale, epi);
@@ -1255,6 +1263,10 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     CK(al((void**)&s.res32, sizeof(float) * 3 * s.g.ncomp));
     CK(al((void**)&s.z32, sizeof(float) * 3 * s.g.ncomp));
     CK(map_nodes32(ctx, &s.m_z32, s.z32, s.g));
+    if (ctx->world == 1) {
+      CK(al((void**)&s.w32, sizeof(float) * 3 * s.g.ncomp));
+      CK(map_nodes32(ctx, &s.m_w32, s.w32, s.g));
+    }
   }
   if (ctx->world > 1) {   // whole-grid moduli for the replicated levels >= 1
     Geo G = ctx->slabs[0].g;
@@ -1799,10 +1811,11 @@ int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   CK(rcv);
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe0, ctx->stream, cudaEventRecordExternal));
   const int fin = ctx->world == 1 ? 1 : 0;
-  for (Slab& sl : ctx->slabs) {   // p = V(r) + beta p, V(r) in w
+  for (Slab& sl : ctx->slabs) {   // p = V(r) + beta p, V(r) in w (fp32 with w32_active)
     const CUtensorMap* pold = parity ? &sl.m_p1 : &sl.m_p0;
     double* pnew = parity ? sl.p0 : sl.p1;
-    CK((launch_mv<2, true>(ctx, sl, 1, sl.m_w, pold, pnew, sl.q, fin)));
+    if (w32_active(ctx)) CK((launch_mv<2, true, 0, double, float>(ctx, sl, 1, sl.m_w32, pold, pnew, sl.q, fin)));
+    else CK((launch_mv<2, true>(ctx, sl, 1, sl.m_w, pold, pnew, sl.q, fin)));
   }
   if (prof_here) CU(cudaEventRecordWithFlags(ctx->pe1, ctx->stream, cudaEventRecordExternal));
   if (!fin) {
@@ -2010,13 +2023,9 @@ int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
   CK(ensure_constants(ctx));
   CK(exchange_nodes(ctx, &Slab::u));
   const Material m = material(ctx);
-  static const bool sens_mv = !getenv("TOPO_SENS_MV") || atoi(getenv("TOPO_SENS_MV")) != 0;
   for (Slab& s : ctx->slabs) {
-    if (sens_mv)   // the matvec's x-marching TMA structure with the energy epilogue (kEpi = 4)
-      CK((launch_mv<0, false, 4>(ctx, s, 0, s.m_u, nullptr, nullptr, nullptr, 0)));
-    else
-      LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
-             s.passive, s.ce, s.dc, s.partials, s.counter);
+    LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
+           s.passive, s.ce, s.dc, s.partials, s.counter);
     LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.u, 1, s.partials, s.counter);
   }
   CK(check_launch(ctx));
@@ -2388,7 +2397,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad, s.res32, s.z32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
+                    s.vpad, s.res32, s.z32, s.w32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
                     s.oc_cx2, s.oc_cA2, s.oc_cdv2, s.oc_n1,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
@@ -3102,7 +3111,10 @@ int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
     LAUNCH(ctx, k_mask_fixed, grid_for((long long)s.g.nown * s.g.nplane), s.g, s.fixm, s.r);
   CK(check_launch(ctx));
   CK(exchange_nodes(ctx, &Slab::r));
-  CK(enqueue_vcycle(ctx, 0, 0, false));
+  ctx->w32_off = true;
+  const int rc = enqueue_vcycle(ctx, 0, 0, false);
+  ctx->w32_off = false;
+  CK(rc);
   return download_nodes(ctx, &Slab::w, z);   // the V-cycle result (last sweep fused into the matvec)
 }
 

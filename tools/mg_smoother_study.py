@@ -54,7 +54,9 @@ def smooth(A, d, b, x, kind, lam, nu, theta, alpha, deg):
     return x
 
 
-CYCLE = os.environ.get("CYCLE", "V")        # V, W (gamma = 2 below level 0), K (Notay K-cycle), K1 (K at level 1 only)
+CYCLE = os.environ.get("CYCLE", "V")
+KTHR = float(os.environ.get("KTHR", "0"))   # Notay's threshold: skip the second FCG step when ||r2|| <= t ||r||
+SKIPS, CALLS = {}, {}        # V, W (gamma = 2 below level 0), K (Notay K-cycle), K1 (K at level 1 only)
 
 
 def make_vcycle(levels, ops, lams, spec):
@@ -81,6 +83,10 @@ def make_vcycle(levels, ops, lams, spec):
         v1[free] = A @ x1[free]
         rho1, a1 = x1 @ v1, x1 @ rc
         r2 = rc - (a1 / rho1) * v1
+        if KTHR > 0 and np.linalg.norm(r2) <= KTHR * np.linalg.norm(rc):
+            SKIPS[l] = SKIPS.get(l, 0) + 1
+            return (a1 / rho1) * x1
+        CALLS[l] = CALLS.get(l, 0) + 1
         x2 = V(r2, l)
         v2 = np.zeros_like(rc)
         v2[free] = A @ x2[free]
@@ -179,7 +185,10 @@ def main():
             t0 = time.time()
             it = pcg(A0, f, V, free, p["cg_rtol"])
             k0, n0, d0 = spec(0)
-            print(f"{v:16s} iters {it:4d}  fine matvecs/iter {2 * n0 * d0 + 1}  ({time.time() - t0:.1f} s)", flush=True)
+            print(f"{v:16s} iters {it:4d}  fine matvecs/iter {2 * n0 * d0 + 1}  ({time.time() - t0:.1f} s)"
+                  f"  skips {SKIPS} second steps {CALLS}", flush=True)
+            SKIPS.clear()
+            CALLS.clear()
             continue
         kind, nu, deg = v.split(":")
         nu, deg = int(nu), int(deg)
