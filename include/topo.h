@@ -147,6 +147,15 @@ typedef struct {
                                  void-rich SIMP designs, where the V-cycle's iteration count grows
                                  with the stiffness contrast.  TOPO_MG_VCYCLE: one cycle per level,
                                  standard PCG (round-1 behaviour).  mg_nu > 1 forces the V-cycle.    */
+  int32_t krylov_fp32;        /* 1: with the fp32 hierarchy on one slab, the multigrid PCG keeps its
+                                 residual r and q = K p in fp32 (SURVEY §8(f) f3 "fp32 storage inside
+                                 fp64 iterative refinement"): u, p and the matvec stay fp64, and the
+                                 fp64 TRUE residual f - K u decides convergence -- when the fp32
+                                 recursion meets cg_rtol, the true residual is checked and, if it has
+                                 not, r is replaced by it and PCG restarts (iterative refinement).
+                                 0 (default): fp64 r and q -- measured faster on the B200 (config 4:
+                                 0.160 vs 0.167 s per SIMP iteration): the fine matvecs are issue-
+                                 bound, not byte-bound, and the fp32 recursion costs restarts      */
 } topo_params;
 
 #define TOPO_MG_VCYCLE 0

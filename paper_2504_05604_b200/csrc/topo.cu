@@ -99,6 +99,7 @@ struct Slab {
   float* res32 = nullptr;              // fp32 multigrid: fine residual for the restriction
   float* z32 = nullptr;                // fp32 multigrid: prolongation output z (post-smoothing input)
   float* w32 = nullptr;                // fp32 multigrid (one slab): the V-cycle output w (PCG matvec input)
+  float *r32 = nullptr, *q32 = nullptr;  // fp32 Krylov residual and q = K p of the MG-PCG
   double *pw0 = nullptr, *pw0_b = nullptr;   // multigrid level-0 power vector (+ snapshot)
   // OC frozen set: per-block active counts / offsets and the compacted (x, A, dv~)
   unsigned *oc_counts = nullptr, *oc_offs = nullptr;
@@ -124,6 +125,7 @@ struct Slab {
   CUtensorMap m_r, m_u, m_w, m_p0, m_p1, m_invd, m_E, m_z, m_q;
   CUtensorMap m_z32;   // fp32 z (multigrid, mg_fp32)
   CUtensorMap m_w32;   // fp32 w (multigrid, mg_fp32, one slab)
+  CUtensorMap m_r32;   // fp32 r (fp32 Krylov vectors)
   CUtensorMap m_vpad;  // padded filter operand (k_filt25), box (32+2R) x (32+2R) x 1
 };
 
@@ -231,6 +233,8 @@ struct topo_ctx {
   int mg_batch = 2;
   bool mg_kcycle = false;            // K-cycle on the coarse levels + flexible PCG (M8, M9)
   bool w32_off = false;              // the V-cycle output stays double (test hook)
+  bool k32_on = false;               // fp32 Krylov r, q allocated (topo_params.krylov_fp32, one slab)
+  bool k32_pass = false;             // ... in use by the running MG-PCG pass
   int mg_kmin = 1, mg_kmax = 99;     // K-cycle levels [kmin, kmax] (TOPO_KMIN / TOPO_KMAX: experiments)
   double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
 };
@@ -766,6 +770,9 @@ int sync_state(topo_ctx* ctx) {
 // precision is the fp32 levels' anyway; the PCG's own vectors stay fp64).
 // Off inside the topo_mg_vcycle test hook (it downloads the double w).
 bool w32_active(const topo_ctx* ctx) { return ctx->mg_f32 && ctx->world == 1 && !ctx->w32_off && ctx->slabs[0].w32; }
+// fp32 Krylov residual / q in the running MG-PCG pass: with the fp32
+// hierarchy on one slab; the true residual f - K u stays fp64 and decides.
+bool k32_active(const topo_ctx* ctx) { return ctx->k32_pass && ctx->k32_on && ctx->mg_f32; }
 
 int update_modulus(topo_ctx* ctx) {
   CK(ensure_constants(ctx));
@@ -916,9 +923,13 @@ int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pn
   const MvGrid m = mv_grid(ctx, s.g);
   // kEpi = 1 with the K-cycle: the PCG's q (untouched by the V-cycle: the fp32
   // pre-smoothing residual goes to res32, the fp64 one to z) for the flexible beta
+  const bool k32 = k32_active(ctx);
   const MvEpi epi{s.r, s.invd, s.fixm, (kEpi == 2 && ctx->mg_f32) ? s.res32 : nullptr,
                   (kEpi == 1 && w32_active(ctx)) ? s.w32 : nullptr,
-                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr};
+                  (kEpi == 1 && ctx->mg_kcycle) ? s.q : nullptr,
+                  (k32 && (kEpi == 1 || kEpi == 2)) ? s.r32 : nullptr,
+                  (k32 && kEpi == 1 && ctx->mg_kcycle) ? s.q32 : nullptr,
+                  (k32 && kEpi == 0 && kPre == 2) ? s.q32 : nullptr};
   k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV><<<m.grid, m.block, smem, ctx->stream>>>(maps, s.g, s.st, gate, m.CX, pnew,
                                                                                  q, s.partials, s.counter, finish,
                                                                                  scale, epi);
@@ -951,8 +962,12 @@ int matvec_all(topo_ctx* ctx, double* Slab::*pin, CUtensorMap Slab::*pmap, doubl
 int residual(topo_ctx* ctx, bool write_r) {
   CK(matvec_all(ctx, &Slab::u, &Slab::m_u, &Slab::q));
   for (Slab& s : ctx->slabs)
-    LAUNCH(ctx, k_residual, grid_resident(k_residual, (long long)s.g.nown * s.g.nplane), s.g, s.st, s.f, s.q, s.invd, s.fixm,
-           s.r, write_r ? 1 : 0, s.partials, s.counter);
+    if (write_r && k32_active(ctx))
+      LAUNCH(ctx, k_residual<float>, grid_resident(k_residual<float>, (long long)s.g.nown * s.g.nplane), s.g, s.st, s.f,
+             s.q, s.invd, s.fixm, s.r32, 1, s.partials, s.counter);
+    else
+      LAUNCH(ctx, k_residual<double>, grid_resident(k_residual<double>, (long long)s.g.nown * s.g.nplane), s.g, s.st,
+             s.f, s.q, s.invd, s.fixm, s.r, write_r ? 1 : 0, s.partials, s.counter);
   CK(check_launch(ctx));
   if (write_r) CK(exchange_nodes(ctx, &Slab::r));
   return allreduce(ctx, 0, 2, 0);
@@ -1266,6 +1281,12 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
     if (ctx->world == 1) {
       CK(al((void**)&s.w32, sizeof(float) * 3 * s.g.ncomp));
       CK(map_nodes32(ctx, &s.m_w32, s.w32, s.g));
+      if (P.krylov_fp32) {
+        CK(al((void**)&s.r32, sizeof(float) * 3 * s.g.ncomp));
+        CK(al((void**)&s.q32, sizeof(float) * 3 * s.g.ncomp));
+        CK(map_nodes32(ctx, &s.m_r32, s.r32, s.g));
+        ctx->k32_on = true;
+      }
     }
   }
   if (ctx->world > 1) {   // whole-grid moduli for the replicated levels >= 1
@@ -1306,6 +1327,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 }
 
 constexpr long long kMgDeepNodes = 150000;   // "small" coarse levels (deep sweeps, warp-split stencil kernel)
+static const long long kMgTinyNodes = getenv("TOPO_TINY_NODES") ? atoll(getenv("TOPO_TINY_NODES")) : 12000;   // warp per node
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
 constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
                                        // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
@@ -1559,7 +1581,10 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   if (m.stored) {
     static const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
                                                                           : kMgDeepNodes;
-    if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
+    if (m.S && m.L.nodes() <= kMgTinyNodes)   // tiny levels: warp per node
+      LAUNCH(ctx, (k_mg_sweep_wn<false, T>), (int)std::min<long long>((m.L.nodes() * 32 + kBlock - 1) / kBlock, 148LL * 8),
+             m.L, mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
+    else if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
       LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16), m.L,
              mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
     else if (m.S) LAUNCH(ctx, k_mg_apply_st<T>, grid_for(m.L.nodes()), m.L, mgp<T>(m.S), mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);
@@ -1636,7 +1661,10 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // (x-slabs: every step below runs per slab; nu = 1 only, see mg_build)
     if (nu == 1)   // (fp64 residual into z with the K-cycle: q must survive for the flexible beta)
       for (Slab& sl : ctx->slabs)
-        CK((launch_mv<3, false, 2, T>(ctx, sl, gate, sl.m_r, nullptr, nullptr, ctx->mg_kcycle ? sl.z : sl.q, 0, om)));
+        if (k32_active(ctx))   // fp32 Krylov residual: float vin tile
+          CK((launch_mv<3, false, 2, T, float>(ctx, sl, gate, sl.m_r32, nullptr, nullptr, sl.z, 0, om)));
+        else
+          CK((launch_mv<3, false, 2, T>(ctx, sl, gate, sl.m_r, nullptr, nullptr, ctx->mg_kcycle ? sl.z : sl.q, 0, om)));
     else CK((launch_mv<3, false>(ctx, s, gate, s.m_r, nullptr, s.z, s.q, 0, om)));
     if (ctx->prof_capture) CU(cudaEventRecordWithFlags(ctx->pe[1], ctx->stream, cudaEventRecordExternal));
     for (int k = 1; k < nu; ++k) {
@@ -1680,7 +1708,10 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
         int chunks = (int)std::max<long long>(1, std::min<long long>((np + 1) / 2, (148LL * 64 + bx - 1) / bx));
         const int cx = ((np + chunks - 1) / chunks + 1) / 2 * 2;   // even: chunks start on coarse planes
         chunks = (np + cx - 1) / cx;
-        if (sizeof(T) == 4)   // fp32 hierarchy: z in fp32 (read by the fp32-operator post-smoothing)
+        if (sizeof(T) == 4 && k32_active(ctx))   // fp32 Krylov residual
+          k_mg_prolong0<T, float, float><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
+              lv_slab(sl), n1.L, cx, sl.r32, sl.invd, om, mgp<T>(n1.x), sl.fixm, sl.z32, gst, sl.g.ex0, pa, pb);
+        else if (sizeof(T) == 4)   // fp32 hierarchy: z in fp32 (read by the fp32-operator post-smoothing)
           k_mg_prolong0<T, float><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
                                                                              mgp<T>(n1.x), sl.fixm, sl.z32, gst,
                                                                              sl.g.ex0, pa, pb);
@@ -1726,11 +1757,15 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     if (nu == 1) {
       // x = w D^-1 b and t = A x in one launch; restrict; correct; t = x + P e
       // (out of place) and the sweep x = t + w D^-1 (b - A t) in one launch
-      LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
+      const bool tiny = m.L.nodes() <= kMgTinyNodes;
+      const int gW = (int)std::min<long long>((m.L.nodes() * 32 + kBlock - 1) / kBlock, 148LL * 8);
+      if (tiny) LAUNCH(ctx, (k_mg_sweep_wn<false, T, true>), gW, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
+      else LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
       CK(launch_restrict<T>(ctx, m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b), gst));
       CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
       LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mt, gst, (const T*)mx);
-      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
+      if (tiny) LAUNCH(ctx, (k_mg_sweep_wn<true, T>), gW, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
+      else LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
       return check_launch(ctx);
     }
     T* buf[2] = {mx, mt};
@@ -1825,12 +1860,20 @@ int enqueue_mg_iter(topo_ctx* ctx, bool prof_here, int parity) {
   for (Slab& sl : ctx->slabs) {
     double* pnew = parity ? sl.p0 : sl.p1;
     double* pprev = parity ? sl.p1 : sl.p0;
-    if (parity)
-      LAUNCH(ctx, (k_update<true, true>), grid_for((long long)sl.g.nown * sl.g.nplane / 2), sl.g, sl.st, sl.u, sl.r,
-             pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials, sl.counter, fin);
+    const int gU = grid_for((long long)sl.g.nown * sl.g.nplane / 2);
+    if (k32_active(ctx)) {   // fp32 Krylov r, q
+      if (parity)
+        LAUNCH(ctx, (k_update<true, true, float>), gU, sl.g, sl.st, sl.u, sl.r32, pprev, pnew, sl.q32, sl.invd, sl.fixm,
+               sl.partials, sl.counter, fin);
+      else
+        LAUNCH(ctx, (k_update<false, true, float>), gU, sl.g, sl.st, sl.u, sl.r32, pprev, pnew, sl.q32, sl.invd,
+               sl.fixm, sl.partials, sl.counter, fin);
+    } else if (parity)
+      LAUNCH(ctx, (k_update<true, true>), gU, sl.g, sl.st, sl.u, sl.r, pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials,
+             sl.counter, fin);
     else
-      LAUNCH(ctx, (k_update<false, true>), grid_for((long long)sl.g.nown * sl.g.nplane / 2), sl.g, sl.st, sl.u, sl.r,
-             pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials, sl.counter, fin);
+      LAUNCH(ctx, (k_update<false, true>), gU, sl.g, sl.st, sl.u, sl.r, pprev, pnew, sl.q, sl.invd, sl.fixm, sl.partials,
+             sl.counter, fin);
   }
   if (!fin) {
     CK(allreduce(ctx, 0, 2, 0));
@@ -1880,6 +1923,7 @@ int mg_download(topo_ctx* ctx, int l, const void* dev, double* host) {
 // One PCG pass (Jacobi or multigrid preconditioner) from the current u.
 int solve_pass(topo_ctx* ctx, int mg, int* replacements_out, double* rr_true_out) {
   const topo_params& P = ctx->prm;
+  ctx->k32_pass = mg && ctx->k32_on;   // fp32 Krylov r, q (the graphs of each path are captured with it)
   const long long n_dof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
   const long long maxit = P.cg_max_iter > 0 ? P.cg_max_iter : 10 * n_dof;
   for (Slab& s : ctx->slabs) {
@@ -1992,6 +2036,9 @@ int do_solve(topo_ctx* ctx, topo_solve_info* info) {
     rc = solve_pass(ctx, 0, &replacements, &rr_true);
     iters += ctx->hstate->it;
   }
+  if (k32_active(ctx))   // keep the fp64 r (TOPO_FIELD_R) consistent with the fp32 recursion
+    for (Slab& s : ctx->slabs) LAUNCH(ctx, k_f2d, grid_for(3 * s.g.ncomp), 3 * s.g.ncomp, s.r32, s.r);
+  ctx->k32_pass = false;
   DevState& h = *ctx->hstate;
   CU(cudaEventRecord(ctx->ev[7], ctx->stream));
   CU(cudaEventSynchronize(ctx->ev[7]));
@@ -2397,7 +2444,7 @@ void free_ctx(topo_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (Slab& s : ctx->slabs) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
-                    s.vpad, s.res32, s.z32, s.w32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
+                    s.vpad, s.res32, s.z32, s.w32, s.r32, s.q32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
                     s.oc_cx2, s.oc_cA2, s.oc_cdv2, s.oc_n1,
                     s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
@@ -2466,6 +2513,7 @@ int validate(topo_ctx* ctx, const topo_params* p) {
   if (p->mg_fp32 != 0 && p->mg_fp32 != 1) return set_err(ctx, TOPO_EINVAL, "mg_fp32 must be 0 or 1");
   if (p->mg_nu_deep < 0 || p->mg_nu_deep > 64) return set_err(ctx, TOPO_EINVAL, "mg_nu_deep must be in [0, 64]");
   if (p->mg_cycle != TOPO_MG_VCYCLE && p->mg_cycle != TOPO_MG_KCYCLE) return set_err(ctx, TOPO_EINVAL, "mg_cycle must be 0 or 1");
+  if (p->krylov_fp32 != 0 && p->krylov_fp32 != 1) return set_err(ctx, TOPO_EINVAL, "krylov_fp32 must be 0 or 1");
   if (p->mg_coarse_max != 0 && (p->mg_coarse_max < 24 || p->mg_coarse_max > 8192))
     return set_err(ctx, TOPO_EINVAL, "mg_coarse_max must be 0 (auto) or in [24, 8192]");
   return TOPO_OK;
@@ -2504,6 +2552,7 @@ void topo_params_default(topo_params* p) {
   p->mg_fp32 = 1;
   p->mg_nu_deep = 0;
   p->mg_cycle = TOPO_MG_KCYCLE;
+  p->krylov_fp32 = 0;
 }
 
 const char* topo_version(void) { return "topo-b200 0.1 (sm_100a, fp64 matrix-free EbE PCG)"; }

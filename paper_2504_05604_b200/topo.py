@@ -48,7 +48,7 @@ class topo_params(C.Structure):
                 ("deterministic", C.c_int32), ("cg_check_every", C.c_int32),
                 ("precond", C.c_int32), ("mg_nu", C.c_int32), ("mg_omega", C.c_double),
                 ("mg_coarse_max", C.c_int32), ("mg_nu_deep", C.c_int32), ("mg_fp32", C.c_int32),
-                ("mg_cycle", C.c_int32)]
+                ("mg_cycle", C.c_int32), ("krylov_fp32", C.c_int32)]
 
 
 class topo_dist(C.Structure):
@@ -214,7 +214,7 @@ def make_params(p):
     prm = topo_params()
     _lib.topo_params_default(C.byref(prm))
     for k in ("nelx", "nely", "nelz", "filter_mode", "cg_warm_start", "deterministic",
-              "cg_check_every", "mg_nu", "mg_coarse_max", "mg_nu_deep", "mg_fp32"):
+              "cg_check_every", "mg_nu", "mg_coarse_max", "mg_nu_deep", "mg_fp32", "krylov_fp32"):
         if k in p:
             setattr(prm, k, int(p[k]))
     if "mg_cycle" in p:

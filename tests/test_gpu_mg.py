@@ -289,3 +289,23 @@ def test_kcycle_iterations_config2(topo):
     assert_rel(out["K"][0], out["V"][0], 1e-6, "c history K vs V")
     print("ncg V", out["V"][1].tolist(), "K", out["K"][1].tolist())
     assert out["K"][1][-4:].max() * 2 < out["V"][1][-4:].min()
+
+
+@pytest.mark.parametrize("dims,obst", CASES[:4])
+def test_krylov_fp32_refinement(topo, dims, obst):
+    """SURVEY f3 as scoped (topo_params.krylov_fp32): the MG-PCG keeps r and q in
+    fp32 inside fp64 iterative refinement (the fp64 true residual decides, with
+    residual replacement): the solve still reaches the direct solution (u to
+    1e-8, true residual 1e-10) -- only the route differs."""
+    p, f, fx, pas, x, K = _case(dims, obst, seed=2, krylov_fp32=1)
+    uo = oracle.solve_direct(K, f, fx)
+    with topo.Problem(p, f, fx, pas) as pr:
+        pr.set_xphys(x)
+        u, info = pr.solve()
+        r = pr.get("r")
+    assert info["precond"] == "mg"
+    assert info["true_rel_res"] <= 1e-10
+    assert oracle.true_residual(K, u, f, fx) <= 1e-10
+    assert np.linalg.norm(u - uo) <= 1e-8 * np.linalg.norm(uo)
+    rt = np.where(fx != 0, 0.0, f - oracle.matvec_free(K, u, fx))
+    assert np.linalg.norm(r - rt) <= 1e-6 * np.linalg.norm(f)    # the fp32 recursion tracks the true residual
