@@ -380,76 +380,6 @@ k_mg_restrict_w(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restri
   }
 }
 
-// Tiny coarse levels (<= ~12 k nodes): the stencil sweep with a WARP per node --
-// lane t < 27 takes stencil block t (forward blocks 13.. from this node, backward
-// blocks transposed from the neighbour), the 3 partial sums meet in a fixed
-// shuffle tree.  One L2 round trip per node instead of the warp-split kernel's
-// four (k_mg_sweep_st8 spends 6-7 us per launch on these levels).  Modes as
-// k_mg_sweep_st8 (kFused, kFromB).
-template <bool kFused, typename T, bool kFromB = false>
-__global__ void __launch_bounds__(kBlock)
-k_mg_sweep_wn(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
-              const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
-              T* __restrict__ dst, const DevState* st, T* __restrict__ xout = nullptr) {
-  MG_GATE(st);
-  const long long tot = L.nodes();
-  const int lane = threadIdx.x & 31;
-  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  const double om = (kFused || kFromB) ? *omp : 0.0;
-  const int t = lane;
-  const int bb = t == 0 ? 13 : (t <= 13 ? 13 + t : t);      // same block order as k_mg_sweep_st8
-  const bool back = t >= 14 && t < 27;
-  const long long d = (long long)(bb % 3 - 1) * L.nplane + (long long)((bb / 3) % 3 - 1) + (long long)(bb / 9 - 1) * L.NY;
-  for (long long k = w0; k < tot; k += nw) {
-    int ix, iy, iz;
-    lv_decode(L, k, ix, iy, iz);
-    const long long i = L.n(ix, iy, iz);
-    double d0 = 0.0, d1 = 0.0, d2 = 0.0;
-    if (t < 27) {
-      const long long j = back ? i - d : i + d;
-      const T* sb = S + (long long)((bb - 13) * 9) * L.ncomp + (back ? j : i);
-      double x0, x1, x2;
-      if (kFromB) {
-        x0 = (double)(T)(om * (double)invd[j] * (double)b[j]);
-        x1 = (double)(T)(om * (double)invd[j + L.ncomp] * (double)b[j + L.ncomp]);
-        x2 = (double)(T)(om * (double)invd[j + 2 * L.ncomp] * (double)b[j + 2 * L.ncomp]);
-      } else {
-        x0 = (double)src[j];
-        x1 = (double)src[j + L.ncomp];
-        x2 = (double)src[j + 2 * L.ncomp];
-      }
-      double m[9];
-#pragma unroll
-      for (int e = 0; e < 9; ++e) m[e] = (double)sb[(long long)e * L.ncomp];
-      if (back) {
-        d0 = fma(m[0], x0, fma(m[3], x1, m[6] * x2));
-        d1 = fma(m[1], x0, fma(m[4], x1, m[7] * x2));
-        d2 = fma(m[2], x0, fma(m[5], x1, m[8] * x2));
-      } else {
-        d0 = fma(m[0], x0, fma(m[1], x1, m[2] * x2));
-        d1 = fma(m[3], x0, fma(m[4], x1, m[5] * x2));
-        d2 = fma(m[6], x0, fma(m[7], x1, m[8] * x2));
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-    }
-    if (lane < 3) {   // lane c finishes component c
-      const double a = lane == 0 ? d0 : lane == 1 ? d1 : d2;
-      const long long o = i + lane * L.ncomp;
-      const uint8_t fm = fix[i];
-      double v = a;
-      if (kFused) v = fma(om * (double)invd[o], (double)b[o] - a, (double)src[o]);
-      dst[o] = ((fm >> lane) & 1) ? T(0) : (T)v;
-      if (kFromB) xout[o] = ((fm >> lane) & 1) ? T(0) : (T)(om * (double)invd[o] * (double)b[o]);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // K-cycle (reading M8; Notay & Vassilevski 2008): a coarse level l is solved by
 // two flexible-CG steps preconditioned by its own cycle B_l:

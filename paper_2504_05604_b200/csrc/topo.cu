@@ -1327,7 +1327,6 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
 }
 
 constexpr long long kMgDeepNodes = 150000;   // "small" coarse levels (deep sweeps, warp-split stencil kernel)
-static const long long kMgTinyNodes = getenv("TOPO_TINY_NODES") ? atoll(getenv("TOPO_TINY_NODES")) : 12000;   // warp per node
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
 constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
                                        // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
@@ -1581,10 +1580,7 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   if (m.stored) {
     static const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
                                                                           : kMgDeepNodes;
-    if (m.S && m.L.nodes() <= kMgTinyNodes)   // tiny levels: warp per node
-      LAUNCH(ctx, (k_mg_sweep_wn<false, T>), (int)std::min<long long>((m.L.nodes() * 32 + kBlock - 1) / kBlock, 148LL * 8),
-             m.L, mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
-    else if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
+    if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
       LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16), m.L,
              mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
     else if (m.S) LAUNCH(ctx, k_mg_apply_st<T>, grid_for(m.L.nodes()), m.L, mgp<T>(m.S), mgp<T>(m.x), m.fixm, mgp<T>(m.t), gst);
@@ -1757,15 +1753,11 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     if (nu == 1) {
       // x = w D^-1 b and t = A x in one launch; restrict; correct; t = x + P e
       // (out of place) and the sweep x = t + w D^-1 (b - A t) in one launch
-      const bool tiny = m.L.nodes() <= kMgTinyNodes;
-      const int gW = (int)std::min<long long>((m.L.nodes() * 32 + kBlock - 1) / kBlock, 148LL * 8);
-      if (tiny) LAUNCH(ctx, (k_mg_sweep_wn<false, T, true>), gW, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
-      else LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), gS, m.L, mgp<T>(m.S), mx, mb, mi, m.fixm, om, mt, gst, mx);
       CK(launch_restrict<T>(ctx, m.L, n1.L, mb, mt, m.fixm, n1.fixm, mgp<T>(n1.b), gst));
       CK(enqueue_coarse_t<T>(ctx, l + 1, gate));
       LAUNCH(ctx, (k_mg_prolong<true, T, T>), gL, m.L, n1.L, mgp<T>(n1.x), m.fixm, mt, gst, (const T*)mx);
-      if (tiny) LAUNCH(ctx, (k_mg_sweep_wn<true, T>), gW, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
-      else LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
+      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), gS, m.L, mgp<T>(m.S), mt, mb, mi, m.fixm, om, mx, gst);
       return check_launch(ctx);
     }
     T* buf[2] = {mx, mt};
