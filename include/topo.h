@@ -33,7 +33,12 @@
  *    TOPO_DIST_LOOPBACK runs `world` slabs in ONE process on one GPU (tests
  *    the partition and halo logic); outputs are then complete.
  *    TOPO_DIST_HOST: like NCCL (one process per slab), host-staged transport.
- *  - Threading: one context per thread; distinct contexts are independent.
+ *  - Threading: one context per thread; distinct contexts are independent,
+ *    except that the element stiffness, filter weights and multigrid tables
+ *    live in __constant__ memory of the device: a context re-uploads its
+ *    tables whenever another context on the same device ran since its last
+ *    call, so contexts on one device must not run CONCURRENTLY (interleaved
+ *    calls are fine).
  *  - Call order: init -> [set_density] -> solve -> sensitivity -> filter(dc)
  *    -> oc_step.  A call whose inputs are not ready returns TOPO_ESTATE.
  */

@@ -914,11 +914,12 @@ int launch_filt_apply(topo_ctx* ctx, Slab& s, const double* a, double* out) {
 template <int TZ, int kPre, bool kDot, int kEpi, typename TC, typename TV = double>
 int launch_mv_t(topo_ctx* ctx, Slab& s, int gate, const MvMaps& maps, double* pnew, double* q, int finish,
                 const double* scale) {
-  static bool attr_set = false;
+  // the dynamic-smem opt-in is per device: remember it per device
+  static unsigned attr_set = 0;
   const int smem = MvSmem<TZ, TV>::bytes(kPre);
-  if (!attr_set) {
+  if (!(attr_set & (1u << (ctx->device & 31)))) {
     CU(cudaFuncSetAttribute(k_mv_wht<TZ, kPre, kDot, kEpi, TC, TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = true;
+    attr_set |= 1u << (ctx->device & 31);
   }
   const MvGrid m = mv_grid(ctx, s.g);
   // kEpi = 1 with the K-cycle: the PCG's q (untouched by the V-cycle: the fp32
@@ -1388,10 +1389,10 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       const MgLevel& f = ctx->mg[l - 1];
       {   // tiled Galerkin product (k_mg_asm_galerkin_t), 8 coarse elements per CTA
         const size_t smem = sizeof(double) * 576 * 2 * kGalTile;
-        static bool attr = false;
-        if (!attr) {
+        static unsigned attr = 0;   // per device
+        if (!(attr & (1u << (ctx->device & 31)))) {
           CU(cudaFuncSetAttribute(k_mg_asm_galerkin_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attr = true;
+          attr |= 1u << (ctx->device & 31);
         }
         k_mg_asm_galerkin_t<<<dim3((m.L.ny + kGalTile - 1) / kGalTile, m.L.nz, m.L.nx), dim3(kGalTile, 24), smem,
                               ctx->stream>>>(f.L, f.K, m.L, m.K);

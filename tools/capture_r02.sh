@@ -3,7 +3,14 @@
 # the bench launch list, ncu --set full of the hot kernels, the paper protocol
 # (both variants, oracle timed beside).  Output under gpurun_out/$TAG*.
 TAG=${1:-r02}
+if [ -z "$NO_TESTS" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${TAG}_gpu_tests.log 2>&1
+  tail -2 gpurun_out/${TAG}_gpu_tests.log
+  python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; tail -1 gpurun_out/${TAG}_smoke.log
+  timeout 600 python tools/run_configs.py 0 1 2 3 > gpurun_out/${TAG}_configs.jsonl 2>&1
+fi
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench.jsonl 2> gpurun_out/${TAG}_bench.err
+timeout 900 python bench.py > gpurun_out/${TAG}_bench_default.jsonl 2> gpurun_out/${TAG}_bench_default.err
 tail -c 600 gpurun_out/${TAG}_bench.jsonl
 timeout 600 python tools/paper_protocol.py --variant both --oracle-iters 2 > gpurun_out/${TAG}_paper_protocol.jsonl 2>&1
 tail -c 300 gpurun_out/${TAG}_paper_protocol.jsonl
@@ -15,8 +22,9 @@ python tools/ncu_agg_grid.py gpurun_out/${TAG}_launches_bench.csv 60 > gpurun_ou
 gzip -f gpurun_out/${TAG}_launches_bench.csv
 K=0
 for spec in "k_mv_wht<.int.8, .int.2, .bool.1, .int.0,::2" "k_mv_wht<.int.8, .int.3, .bool.0, .int.2,::2" \
-            "k_mv_wht<.int.8, .int.0, .bool.0, .int.1,::2" "k_mg_l1_elem<float::4" "k_filt25<2, 2>::0" \
-            "k_sens::1" "k_update<.bool.1, .bool.1>::2" "k_mg_apply_st<float>::4" "k_mg_coarse_solve32::4"; do
+            "k_mv_wht<.int.8, .int.0, .bool.0, .int.1,::2" "k_mg_l1_elem<float::4" "k_filt25::1" \
+            "k_sens::1" "k_update<.bool.1, .bool.1>::2" "k_mg_apply_st<float>::4" "k_dgemm_nt64_tc::0" \
+            "k_mg_sweep_st8::40"; do
   re="${spec%%::*}"; skip="${spec##*::}"
   K=$((K+1))
   timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
