@@ -1022,7 +1022,10 @@ k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
 }
 
 // q = mask(A x) through the stencil; thread per node, 27 neighbour 3-vectors.
-template <typename T>
+// (kU: unroll of the 13 neighbour pairs; fully unrolled (13) the loads of all
+// 27 blocks are in flight together: 79 vs 91 us per level-2 apply at config 4,
+// the kernel is long-scoreboard bound on its L2/HBM gathers)
+template <typename T, int kU = 13>
 __global__ void __launch_bounds__(kBlock)
 k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
               const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
@@ -1041,7 +1044,7 @@ k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
       a1 = fma(sb[3 * L.ncomp], x0, fma(sb[4 * L.ncomp], x1, sb[5 * L.ncomp] * x2));
       a2 = fma(sb[6 * L.ncomp], x0, fma(sb[7 * L.ncomp], x1, sb[8 * L.ncomp] * x2));
     }
-#pragma unroll 2
+#pragma unroll (kU)
     for (int b = 14; b < 27; ++b) {
       // b = (dx+1) + 3 (dy+1) + 9 (dz+1); layout: x -> nplane, z -> NY, y -> 1
       const long long d = (long long)(b % 3 - 1) * L.nplane + (long long)((b / 3) % 3 - 1) +
