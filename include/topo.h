@@ -348,6 +348,8 @@ int64_t topo_count(const topo_ctx *ctx, int32_t what);
 #define TOPO_COUNT_DESIGN      3
 #define TOPO_COUNT_STENCIL     4   /* filter stencil points                   */
 #define TOPO_COUNT_DEVICE_BYTES 5  /* device memory held by the context        */
+#define TOPO_COUNT_MG_DIST     6   /* x-slabs: multigrid levels 1..k cycled on
+                                      each slab's owned planes (0: replicated) */
 
 /* TOPO_DIST_HOST helper: a fresh 128-byte transport id (a POSIX shared-memory
  * name) that rank 0 creates and broadcasts to the other ranks.  The host

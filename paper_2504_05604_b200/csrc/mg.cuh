@@ -24,22 +24,42 @@ struct LvGeo {
   int NY;                 // y pitch (nodes)
   long long nplane;       // NY * NZ
   long long ncomp;        // component stride
+  // node planes [xa, xb] a launch computes (distributed levels, x-slabs: a rank's
+  // owned planes; default: all, xb = -1 -> nx).  nodes() counts the range and
+  // lv_decode offsets into it, so every node-parallel kernel is range-aware;
+  // the layout (n(), ncomp, nel()) stays the whole level's.
+  int xa = 0, xb = -1;
   __host__ __device__ long long n(int ix, int iy, int iz) const {
     return (long long)(ix + 1) * nplane + (long long)(iz + 1) * NY + (iy + 1);
   }
-  __host__ __device__ long long nodes() const { return (long long)(nx + 1) * (ny + 1) * (nz + 1); }
+  __host__ __device__ int xlast() const { return xb < 0 ? nx : xb; }
+  __host__ __device__ bool full() const { return xa == 0 && xlast() == nx; }
+  __host__ __device__ long long nodes() const { return (long long)(xlast() - xa + 1) * (ny + 1) * (nz + 1); }
   __host__ __device__ long long nel() const { return (long long)nx * ny * nz; }
+  // element planes adjacent to the node range: [max(xa - 1, 0), min(xlast, nx - 1)]
+  __host__ __device__ long long el_lo() const { return (long long)(xa > 0 ? xa - 1 : 0) * ny * nz; }
+  __host__ __device__ long long el_hi() const { return (long long)(xlast() < nx ? xlast() + 1 : nx) * ny * nz; }
+  // per-component index range of the node planes (the whole component, pads
+  // included, for the full range)
+  __host__ __device__ long long v_lo() const { return full() ? 0 : (long long)(xa + 1) * nplane; }
+  __host__ __device__ long long v_hi() const { return full() ? ncomp : (long long)(xlast() + 2) * nplane; }
 };
 
-// node k of the (nx+1)(ny+1)(nz+1) enumeration, iy fastest (coalesced); 32-bit
-// arithmetic (init validates node counts < 2^31)
+// node k of the (nx+1)(ny+1)(nz+1) enumeration (of the range [xa, xb]), iy
+// fastest (coalesced); 32-bit arithmetic (init validates node counts < 2^31)
 __device__ __forceinline__ void lv_decode(const LvGeo& L, long long k, int& ix, int& iy, int& iz) {
   const unsigned kk = (unsigned)k, ny1 = (unsigned)(L.ny + 1), nz1 = (unsigned)(L.nz + 1);
   const unsigned t = kk / ny1;
   iy = (int)(kk - t * ny1);
   const unsigned u = t / nz1;
   iz = (int)(t - u * nz1);
-  ix = (int)u;
+  ix = (int)u + L.xa;
+}
+// element e of a vector-range loop over 3 components: index of the k-th entry
+__device__ __forceinline__ long long lv_vidx(const LvGeo& L, long long k) {
+  const long long w = L.v_hi() - L.v_lo();
+  const long long c = k / w;
+  return c * L.ncomp + L.v_lo() + (k - c * w);
 }
 
 __constant__ double c_mg_diag8[8 * 24];       // diag of M_c (level-1 Galerkin from fine E)
@@ -393,12 +413,14 @@ k_mg_restrict_w(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restri
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_kc_dot1(long long n, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
+k_kc_dot1(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
           T* __restrict__ kx, T* __restrict__ kv, double* __restrict__ kc, const DevState* gst,
-          double* partials, unsigned int* counter) {
+          double* partials, unsigned int* counter, DevState* slab_out = nullptr) {
   MG_GATE(gst);
   double xt = 0.0, xb = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long n = 3 * (L.v_hi() - L.v_lo());
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long i = lv_vidx(L, k);
     const T xv = x[i], tv = t[i];
     kx[i] = xv;
     kv[i] = tv;
@@ -408,26 +430,53 @@ k_kc_dot1(long long n, const T* __restrict__ x, const T* __restrict__ t, const T
   __shared__ double tot[2];
   double v[2] = {xt, xb};
   if (grid_reduce<2>(v, partials, counter, tot) && threadIdx.x == 0) {
+    if (slab_out) {   // x-slab partial: allreduced, then k_kc_finish1
+      slab_out->sums[0] = tot[0];
+      slab_out->sums[1] = tot[1];
+      return;
+    }
     kc[0] = tot[0];
     kc[1] = tot[1];
   }
 }
-template <typename T>
-__global__ void __launch_bounds__(kBlock)
-k_kc_r2(long long n, T* __restrict__ b, const T* __restrict__ kv, const double* __restrict__ kc, const DevState* gst) {
+__global__ void k_kc_finish1(const DevState* st, double* __restrict__ kc, const DevState* gst) {
   MG_GATE(gst);
-  const double s = kc[0] > 0.0 ? kc[1] / kc[0] : 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    b[i] = (T)fma(-s, (double)kv[i], (double)b[i]);
+  kc[0] = st->sums[0];
+  kc[1] = st->sums[1];
 }
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_kc_dot2(long long n, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
+k_kc_r2(LvGeo L, T* __restrict__ b, const T* __restrict__ kv, const double* __restrict__ kc, const DevState* gst) {
+  MG_GATE(gst);
+  const double s = kc[0] > 0.0 ? kc[1] / kc[0] : 0.0;
+  const long long n = 3 * (L.v_hi() - L.v_lo());
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long i = lv_vidx(L, k);
+    b[i] = (T)fma(-s, (double)kv[i], (double)b[i]);
+  }
+}
+__device__ __forceinline__ void kc_coeffs(double* kc, double g, double bb, double a2) {
+  const double rho1 = kc[0], a1 = kc[1];
+  if (!(rho1 > 0.0) || !isfinite(rho1)) {     // B_l(b) = 0 (b = 0): no correction
+    kc[2] = 0.0;
+    kc[3] = 0.0;
+    return;
+  }
+  const double rho2 = bb - g * g / rho1;
+  const double c2 = (rho2 > 0.0 && isfinite(rho2)) ? a2 / rho2 : 0.0;
+  kc[2] = a1 / rho1 - g * c2 / rho1;
+  kc[3] = c2;
+}
+template <typename T>
+__global__ void __launch_bounds__(kBlock)
+k_kc_dot2(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
           const T* __restrict__ kv, double* __restrict__ kc, const DevState* gst, double* partials,
-          unsigned int* counter) {
+          unsigned int* counter, DevState* slab_out = nullptr) {
   MG_GATE(gst);
   double g = 0.0, bb = 0.0, a2 = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long n = 3 * (L.v_hi() - L.v_lo());
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long i = lv_vidx(L, k);
     const double xv = (double)x[i];
     g = fma(xv, (double)kv[i], g);
     bb = fma(xv, (double)t[i], bb);
@@ -436,26 +485,30 @@ k_kc_dot2(long long n, const T* __restrict__ x, const T* __restrict__ t, const T
   __shared__ double tot[3];
   double v[3] = {g, bb, a2};
   if (grid_reduce<3>(v, partials, counter, tot) && threadIdx.x == 0) {
-    const double rho1 = kc[0], a1 = kc[1];
-    if (!(rho1 > 0.0) || !isfinite(rho1)) {     // B_l(b) = 0 (b = 0): no correction
-      kc[2] = 0.0;
-      kc[3] = 0.0;
+    if (slab_out) {
+      slab_out->sums[0] = tot[0];
+      slab_out->sums[1] = tot[1];
+      slab_out->sums[2] = tot[2];
       return;
     }
-    const double rho2 = tot[1] - tot[0] * tot[0] / rho1;
-    const double c2 = (rho2 > 0.0 && isfinite(rho2)) ? tot[2] / rho2 : 0.0;
-    kc[2] = a1 / rho1 - tot[0] * c2 / rho1;
-    kc[3] = c2;
+    kc_coeffs(kc, tot[0], tot[1], tot[2]);
   }
+}
+__global__ void k_kc_finish2(const DevState* st, double* __restrict__ kc, const DevState* gst) {
+  MG_GATE(gst);
+  kc_coeffs(kc, st->sums[0], st->sums[1], st->sums[2]);
 }
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
-k_kc_combine(long long n, T* __restrict__ x, const T* __restrict__ kx, const double* __restrict__ kc,
+k_kc_combine(LvGeo L, T* __restrict__ x, const T* __restrict__ kx, const double* __restrict__ kc,
              const DevState* gst) {
   MG_GATE(gst);
   const double c1 = kc[2], c2 = kc[3];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+  const long long n = 3 * (L.v_hi() - L.v_lo());
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+    const long long i = lv_vidx(L, k);
     x[i] = (T)fma(c1, (double)kx[i], c2 * (double)x[i]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -828,8 +881,8 @@ __global__ void __launch_bounds__(kL1Block, 3)
 k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
              T* __restrict__ Y, const DevState* st) {
   MG_GATE(st);
-  const long long nel = L.nel();
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nel;
+  const long long nel = L.nel(), ehi = L.el_hi();   // (x-slabs: the element planes next to the node range)
+  for (long long e = L.el_lo() + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ehi;
        e += (long long)gridDim.x * blockDim.x) {
     const unsigned ee = (unsigned)e, ny = (unsigned)L.ny, nz = (unsigned)L.nz;
     const unsigned t = ee / ny, ey = ee - t * ny, ex = t / nz, ez = t - ex * nz;

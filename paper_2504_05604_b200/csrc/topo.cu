@@ -91,8 +91,23 @@ struct TopoError {
 // ---------------------------------------------------------------------------
 // Context
 // ---------------------------------------------------------------------------
+// One distributed coarse level of a slab (x-slabs, levels 1 .. mg_dl; DESIGN.md
+// §6): the level's vectors in the WHOLE level's layout (a node plane has the same
+// offset on every rank), of which this slab computes its owned node planes
+// [oa, ob) and keeps the ghost planes oa - 1 and ob current by exchanges.  Slab 0
+// (every slab with one slab per process) aliases ctx->mg[l]'s buffers; the other
+// slabs of a loopback context own theirs.  The level operators (D^-1, stencil,
+// masks, the fine moduli of level 1) are the replicated setup's.
+struct DLv {
+  void *x = nullptr, *b = nullptr, *t = nullptr, *kx = nullptr, *kv = nullptr, *Y = nullptr;
+  double* kc = nullptr;   // K-cycle scalars of this slab (8)
+  int oa = 0, ob = 0;
+  bool own = false;       // buffers allocated here (freed with the context)
+};
+
 struct Slab {
   Geo g{};
+  std::vector<DLv> dlv;   // [0, mg_dl]: distributed levels (index 0 unused)
   // node vectors: 3*ncomp doubles each (SoA)
   double *u = nullptr, *r = nullptr, *p0 = nullptr, *p1 = nullptr, *q = nullptr, *f = nullptr,
          *w = nullptr, *z = nullptr;   // z: multigrid preconditioned residual V(r)
@@ -237,6 +252,7 @@ struct topo_ctx {
   bool k32_pass = false;             // ... in use by the running MG-PCG pass
   int mg_kmin = 1, mg_kmax = 99;     // K-cycle levels [kmin, kmax] (TOPO_KMIN / TOPO_KMAX: experiments)
   double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
+  int mg_dl = 0;                     // x-slabs: levels 1 .. mg_dl distributed over the slabs (0: replicated)
 };
 
 namespace {
@@ -1126,6 +1142,7 @@ int mg_allreduce_level(topo_ctx* ctx, void* buf, size_t n, bool f32) {
 
 // Hierarchy on the host (init): dims, coarse Dirichlet masks (M4: the node at the
 // clamped position min(2j, n) decides), property Q, allocations, coarsest maps.
+int mg_dist_plan(topo_ctx* ctx);
 int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   const topo_params& P = ctx->prm;
   ctx->mg_on = false;
@@ -1327,7 +1344,12 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   return TOPO_OK;
 }
 
-constexpr long long kMgDeepNodes = 150000;   // "small" coarse levels (deep sweeps, warp-split stencil kernel)
+constexpr long long kMgDeepNodesDefault = 150000;   // "small" coarse levels (deep sweeps, warp-split stencil kernel)
+// (TOPO_DEEP_NODES overrides it: tests run the large-level code paths on small grids)
+long long mg_deep_nodes() {
+  const char* e = getenv("TOPO_DEEP_NODES");
+  return e ? atoll(e) : kMgDeepNodesDefault;
+}
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
 constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
                                        // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
@@ -1335,17 +1357,254 @@ constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previ
 
 template <typename T> T* mgp(void* p) { return static_cast<T*>(p); }
 
+// ---------------------------------------------------------------------------
+// Distributed coarse levels on x-slabs (W > 1, reading M10).
+// Rank r owns element planes [ex0 >> l, ex1 >> l) of level l and the node
+// planes [ex0 >> l, ex1 >> l) (the last rank also the last plane); levels
+// 1 .. mg_dl are cycled on the owned planes only (ghost planes exchanged, the
+// K-cycle's dots allreduced), level mg_dl + 1 and below stay replicated (their
+// restricted right-hand side is all-gathered plane-wise).  The per-design setup
+// stays replicated (operators from the all-gathered moduli).
+// ---------------------------------------------------------------------------
+void dl_owned(const topo_ctx* ctx, int r, int l, int& oa, int& ob) {
+  int b = 0, e = 0;
+  topo_partition(ctx->prm.nelx, ctx->prm.rmin, ctx->world, r, &b, &e);
+  oa = b >> l;
+  ob = (e >> l) + (r == ctx->world - 1 ? 1 : 0);
+}
+int slab_rank(const topo_ctx* ctx, const Slab& sl) {
+  return ctx->mode == TOPO_DIST_LOOPBACK ? (int)(&sl - &ctx->slabs[0]) : ctx->rank;
+}
+LvGeo dl_geo(const topo_ctx* ctx, const Slab& sl, int l) {
+  LvGeo L = ctx->mg[l].L;
+  L.xa = sl.dlv[l].oa;
+  L.xb = sl.dlv[l].ob - 1;
+  return L;
+}
+
+int mg_dist_plan(topo_ctx* ctx) {
+  ctx->mg_dl = 0;
+  const int W = ctx->world, L = (int)ctx->mg.size();
+  const bool force1 = getenv("TOPO_DIST_FORCE1") && atoi(getenv("TOPO_DIST_FORCE1")) != 0;   // (debug: W = 1)
+  if ((W == 1 && !force1) || !ctx->mg_on || L < 3) return TOPO_OK;
+  const int maxl = getenv("TOPO_DIST_LEVELS") ? atoi(getenv("TOPO_DIST_LEVELS")) : 16;
+  const long long min_nodes = getenv("TOPO_DIST_MIN_NODES") ? atoll(getenv("TOPO_DIST_MIN_NODES")) : mg_deep_nodes();
+  int lD = 0;
+  for (int l = 1; l <= L - 2 && l <= maxl; ++l) {
+    if (ctx->mg[l].L.nodes() <= min_nodes || (l == 1 && ctx->mg[1].stored)) break;
+    // every slab boundary (and nelx) on an even plane of level l (the owned
+    // coarse planes of level l + 1 are then the coarsened owned planes), >= 2
+    // owned element planes per slab
+    const int q = 1 << (l + 1);
+    bool ok = ctx->prm.nelx % q == 0;
+    for (int r = 0; r < W && ok; ++r) {
+      int b = 0, e = 0;
+      topo_partition(ctx->prm.nelx, ctx->prm.rmin, W, r, &b, &e);
+      ok = b % q == 0 && ((e - b) >> l) >= 2;
+    }
+    if (!ok) break;
+    lD = l;
+  }
+  if (!lD) return TOPO_OK;
+  for (Slab& sl : ctx->slabs) {
+    sl.dlv.assign(lD + 1, DLv{});
+    const bool alias = &sl == &ctx->slabs[0];
+    for (int l = 1; l <= lD; ++l) {
+      MgLevel& m = ctx->mg[l];
+      DLv& d = sl.dlv[l];
+      dl_owned(ctx, slab_rank(ctx, sl), l, d.oa, d.ob);
+      if (alias) {
+        d.x = m.x; d.b = m.b; d.t = m.t; d.kx = m.kx; d.kv = m.kv; d.Y = m.Y;
+        d.kc = ctx->mg_kc + 8 * l;
+        continue;
+      }
+      d.own = true;
+      const size_t v = sizeof(double) * 3 * m.L.ncomp;
+      void** bufs[] = {&d.x, &d.b, &d.t, &d.kx, &d.kv};
+      for (void** p : bufs) {
+        CU(cudaMalloc(p, v));
+        CU(cudaMemsetAsync(*p, 0, v, ctx->stream));
+        ctx->dev_bytes += v;
+      }
+      if (m.Y) {
+        CU(cudaMalloc(&d.Y, sizeof(double) * 24 * m.L.nel()));
+        CU(cudaMemsetAsync(d.Y, 0, sizeof(double) * 24 * m.L.nel(), ctx->stream));
+        ctx->dev_bytes += sizeof(double) * 24 * m.L.nel();
+      }
+      CU(cudaMalloc((void**)&d.kc, sizeof(double) * 8));
+      CU(cudaMemsetAsync(d.kc, 0, sizeof(double) * 8, ctx->stream));
+    }
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->mg_dl = lD;
+  return TOPO_OK;
+}
+
+// Ghost planes of a node vector between neighbouring slabs.  get(slab) ->
+// {base pointer, b0, oa, ob}: global node plane P sits at index (P - b0 + 1) *
+// nplane of each component (stride ncomp), the slab owns planes [oa, ob).
+// dirs & 1: the left ghost (oa - 1) from the left neighbour's last owned plane;
+// dirs & 2: the right ghost (ob) from the right neighbour's first owned plane.
+struct PlaneSet {
+  char* v;
+  long long b0, oa, ob;
+  long long ncomp;   // component stride (slab vectors: differs for the last slab)
+};
+template <typename Get>
+int exchange_planes(topo_ctx* ctx, Get get, size_t es, long long nplane, int dirs) {
+  const int W = ctx->world;
+  if (W == 1) return TOPO_OK;
+  const size_t pb = es * nplane;
+  auto at = [&](const PlaneSet& p, long long P, int c) { return p.v + es * (c * p.ncomp + (P - p.b0 + 1) * nplane); };
+  if (ctx->mode == TOPO_DIST_LOOPBACK) {
+    for (int s = 0; s < W; ++s) {
+      const PlaneSet a = get(ctx->slabs[s]);
+      for (int c = 0; c < 3; ++c) {
+        if ((dirs & 1) && s > 0) {
+          const PlaneSet l = get(ctx->slabs[s - 1]);
+          CU(cudaMemcpyAsync(at(a, a.oa - 1, c), at(l, a.oa - 1, c), pb, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        if ((dirs & 2) && s < W - 1) {
+          const PlaneSet r = get(ctx->slabs[s + 1]);
+          CU(cudaMemcpyAsync(at(a, a.ob, c), at(r, a.ob, c), pb, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+      }
+    }
+    return TOPO_OK;
+  }
+  const PlaneSet a = get(ctx->slabs[0]);
+  const int rk = ctx->rank;
+  if (ctx->mode == TOPO_DIST_HOST) {   // blocks [c][0] to the left (plane oa), [c][1] to the right (plane ob - 1)
+    const long long len = (long long)((pb + 7) / 8);
+    char *hs = reinterpret_cast<char*>(ctx->ht->hsend), *hr = reinterpret_cast<char*>(ctx->ht->hrecv);
+    for (int c = 0; c < 3; ++c) {
+      if (rk > 0 && (dirs & 2))
+        CU(cudaMemcpyAsync(hs + 8 * (2 * c) * len, at(a, a.oa, c), pb, cudaMemcpyDeviceToHost, ctx->stream));
+      if (rk < W - 1 && (dirs & 1))
+        CU(cudaMemcpyAsync(hs + 8 * (2 * c + 1) * len, at(a, a.ob - 1, c), pb, cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 0;
+    op.len = len;
+    op.nblk = 3;
+    CK(host_launch(ctx, op));
+    for (int c = 0; c < 3; ++c) {
+      if (rk > 0 && (dirs & 1))
+        CU(cudaMemcpyAsync(at(a, a.oa - 1, c), hr + 8 * (2 * c) * len, pb, cudaMemcpyHostToDevice, ctx->stream));
+      if (rk < W - 1 && (dirs & 2))
+        CU(cudaMemcpyAsync(at(a, a.ob, c), hr + 8 * (2 * c + 1) * len, pb, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return TOPO_OK;
+  }
+  const int dt = es == 4 ? ncclFloat32 : ncclFloat64;
+  NC(g_nccl.GroupStart());
+  for (int c = 0; c < 3; ++c) {
+    if (dirs & 1) {
+      if (rk < W - 1) NC(g_nccl.Send(at(a, a.ob - 1, c), (size_t)nplane, dt, rk + 1, ctx->comm, ctx->stream));
+      if (rk > 0) NC(g_nccl.Recv(at(a, a.oa - 1, c), (size_t)nplane, dt, rk - 1, ctx->comm, ctx->stream));
+    }
+    if (dirs & 2) {
+      if (rk > 0) NC(g_nccl.Send(at(a, a.oa, c), (size_t)nplane, dt, rk - 1, ctx->comm, ctx->stream));
+      if (rk < W - 1) NC(g_nccl.Recv(at(a, a.ob, c), (size_t)nplane, dt, rk + 1, ctx->comm, ctx->stream));
+    }
+  }
+  NC(g_nccl.GroupEnd());
+  return TOPO_OK;
+}
+// a distributed level's vector (field of DLv), elements of es bytes
+int exchange_lv(topo_ctx* ctx, int l, void* DLv::*field, size_t es, int dirs) {
+  const LvGeo& L = ctx->mg[l].L;
+  return exchange_planes(
+      ctx,
+      [&](Slab& sl) {
+        const DLv& d = sl.dlv[l];
+        return PlaneSet{static_cast<char*>(d.*field), 0, d.oa, d.ob, L.ncomp};
+      },
+      es, L.nplane, dirs);
+}
+// a fine-level slab vector (slab layout: local plane 0 = global ex0)
+int exchange_fine(topo_ctx* ctx, void* (*field)(Slab&), size_t es, int dirs) {
+  const Geo& g = ctx->slabs[0].g;
+  return exchange_planes(
+      ctx,
+      [&](Slab& sl) {
+        return PlaneSet{static_cast<char*>(field(sl)), sl.g.ex0, sl.g.ex0, sl.g.ex0 + sl.g.nown, sl.g.ncomp};
+      },
+      es, g.nplane, dirs);
+}
+
+// Replicated level l (the first level below the distributed ones): every rank
+// computed the restriction on its owned planes of buf; all-gather them (loopback:
+// the slabs wrote one shared buffer -- nothing to do).
+int gather_level(topo_ctx* ctx, int l, void* buf, size_t es) {
+  const int W = ctx->world;
+  if (W == 1 || ctx->mode == TOPO_DIST_LOOPBACK) return TOPO_OK;
+  const LvGeo& L = ctx->mg[l].L;
+  char* v = static_cast<char*>(buf);
+  auto at = [&](long long P, int c) { return v + es * (c * L.ncomp + (P + 1) * L.nplane); };
+  const int rk = ctx->rank;
+  if (ctx->mode == TOPO_DIST_HOST) {   // pack the 3 components' owned planes, all-gather, unpack
+    HostOp op;
+    op.t = ctx->ht;
+    op.kind = 3;
+    long long off = 0;
+    for (int r = 0; r < W; ++r) {
+      int oa = 0, ob = 0;
+      dl_owned(ctx, r, l, oa, ob);
+      op.cnt[r] = (long long)((3 * es * (ob - oa) * L.nplane + 7) / 8);
+      op.off[r] = off;
+      off += op.cnt[r];
+    }
+    int oa = 0, ob = 0;
+    dl_owned(ctx, rk, l, oa, ob);
+    const size_t cb = es * (ob - oa) * L.nplane;
+    char* hs = reinterpret_cast<char*>(ctx->ht->hsend);
+    for (int c = 0; c < 3; ++c) CU(cudaMemcpyAsync(hs + c * cb, at(oa, c), cb, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(host_launch(ctx, op));
+    for (int r = 0; r < W; ++r) {
+      if (r == rk) continue;
+      int pa = 0, pbn = 0;
+      dl_owned(ctx, r, l, pa, pbn);
+      const size_t rb = es * (pbn - pa) * L.nplane;
+      const char* src = reinterpret_cast<const char*>(ctx->ht->hrecv + op.off[r]);
+      for (int c = 0; c < 3; ++c) CU(cudaMemcpyAsync(at(pa, c), src + c * rb, rb, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return TOPO_OK;
+  }
+  const int dt = es == 4 ? ncclFloat32 : ncclFloat64;
+  int oa = 0, ob = 0;
+  dl_owned(ctx, rk, l, oa, ob);
+  NC(g_nccl.GroupStart());
+  for (int r = 0; r < W; ++r) {
+    if (r == rk) continue;
+    int pa = 0, pbn = 0;
+    dl_owned(ctx, r, l, pa, pbn);
+    for (int c = 0; c < 3; ++c) {
+      NC(g_nccl.Send(at(oa, c), (size_t)((ob - oa) * L.nplane), dt, r, ctx->comm, ctx->stream));
+      NC(g_nccl.Recv(at(pa, c), (size_t)((pbn - pa) * L.nplane), dt, r, ctx->comm, ctx->stream));
+    }
+  }
+  NC(g_nccl.GroupEnd());
+  return TOPO_OK;
+}
+
 // level-1 phase 1 (Walsh-domain Galerkin per coarse element), 128-thread CTAs
+// (x-slabs: Lr = the slab's owned node planes -- the element planes next to
+// them are computed -- and the slab's x and Y)
 template <typename T>
-int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst) {
-  Slab& s = ctx->slabs[0];
-  const long long nb = std::min<long long>((m.L.nel() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
+int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst, const LvGeo* Lr = nullptr, void* xv = nullptr,
+                   void* Yv = nullptr) {
+  const LvGeo L = Lr ? *Lr : m.L;
+  T* x = mgp<T>(xv ? xv : m.x);
+  T* Y = mgp<T>(Yv ? Yv : m.Y);
+  const long long nb = std::min<long long>((L.el_hi() - L.el_lo() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
   if (sizeof(T) == 4)   // fp32 moduli (k_mg_e32 at setup)
-    k_mg_l1_elem<T, float><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, ctx->mg_E32,
-                                                                                   mgp<T>(m.x), mgp<T>(m.Y), gst);
+    k_mg_l1_elem<T, float><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y,
+                                                                                   gst);
   else
-    k_mg_l1_elem<T, double><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), m.L, mgE(ctx),
-                                                                                    mgp<T>(m.x), mgp<T>(m.Y), gst);
+    k_mg_l1_elem<T, double><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), L, mgE(ctx), x, Y,
+                                                                                    gst);
   ctx->launches++;
   debug_sync(ctx, "k_mg_l1_elem");
   return check_launch(ctx);
@@ -1520,6 +1779,16 @@ int mg_clear_levels(topo_ctx* ctx) {
     if (m.S) CU(cudaMemsetAsync(m.S, 0, sizeof(double) * 126 * m.L.ncomp, ctx->stream));
     if (m.Y) CU(cudaMemsetAsync(m.Y, 0, sizeof(double) * 24 * m.L.nel(), ctx->stream));
   }
+  for (Slab& s : ctx->slabs)   // distributed levels' own buffers (loopback slabs >= 1)
+    for (size_t l = 1; l < s.dlv.size(); ++l) {
+      DLv& d = s.dlv[l];
+      if (!d.own) continue;
+      const size_t n3 = sizeof(double) * 3 * ctx->mg[l].L.ncomp;
+      void* v3[] = {d.x, d.b, d.t, d.kx, d.kv};
+      for (void* v : v3)
+        if (v) CU(cudaMemsetAsync(v, 0, n3, ctx->stream));
+      if (d.Y) CU(cudaMemsetAsync(d.Y, 0, sizeof(double) * 24 * ctx->mg[l].L.nel(), ctx->stream));
+    }
   return TOPO_OK;
 }
 
@@ -1579,8 +1848,8 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   MgLevel& m = ctx->mg[l];
   const DevState* gst = gate ? s.st : nullptr;
   if (m.stored) {
-    static const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
-                                                                          : kMgDeepNodes;
+    const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
+                                                                   : mg_deep_nodes();
     if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
       LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16), m.L,
              mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
@@ -1612,7 +1881,7 @@ int launch_restrict(topo_ctx* ctx, const LvGeo& F, const LvGeo& C, const T* b, c
 // coarse levels (auto: 8 when the fine grid is large enough that they are cheap)
 int mg_level_nu(const topo_ctx* ctx, int l) {
   const topo_params& P = ctx->prm;
-  if (l == 0 || ctx->mg[l].L.nodes() > kMgDeepNodes) return P.mg_nu;
+  if (l == 0 || ctx->mg[l].L.nodes() > mg_deep_nodes()) return P.mg_nu;
   if (P.mg_nu_deep > 0) return P.mg_nu_deep;
   if (ctx->mg_kcycle) return P.mg_nu;   // the K-cycle solves the deep levels well enough (M8)
   const long long fine = (long long)(P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
@@ -1626,6 +1895,8 @@ template <typename T>
 int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot);
 template <typename T>
 int enqueue_coarse_t(topo_ctx* ctx, int l, int gate);
+template <typename T>
+int dist_coarse(topo_ctx* ctx, int l, int gate);
 template <typename T>
 int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   Slab& s = ctx->slabs[0];
@@ -1673,31 +1944,47 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
     // x-marching restriction of the masked residual (k_mg_restrict0); x-slabs:
     // each slab restricts its owned fine planes and the partial level-1 vectors
     // are summed (slab order in loopback mode, an allreduce with NCCL)
-    const bool slabs = ctx->world > 1;
-    if (slabs) CU(cudaMemsetAsync(n1.b, 0, sizeof(T) * 3 * n1.L.ncomp, ctx->stream));
+    // (distributed level 1, mg_dl >= 1: each slab restricts into ITS owned coarse
+    // planes, reading the residual's left ghost plane -- no level-1 allreduce)
+    const bool slabs = ctx->world > 1, dl = ctx->mg_dl >= 1;
+    if (slabs && !dl) CU(cudaMemsetAsync(n1.b, 0, sizeof(T) * 3 * n1.L.ncomp, ctx->stream));
+    if (dl) {
+      if (ctx->mg_f32) CK(exchange_fine(ctx, [](Slab& q) -> void* { return q.res32; }, sizeof(float), 1));
+      else if (ctx->mg_kcycle) CK(exchange_fine(ctx, [](Slab& q) -> void* { return q.z; }, sizeof(double), 1));
+      else CK(exchange_fine(ctx, [](Slab& q) -> void* { return q.q; }, sizeof(double), 1));
+    }
     for (Slab& sl : ctx->slabs) {
-      const int xa = sl.g.ex0, xb = sl.g.ex0 + sl.g.nown;          // owned fine planes [xa, xb)
-      const int j0 = xa / 2, jend = std::min(n1.L.nx, xb / 2) + 1;   // coarse planes they reach
+      const int xa = dl ? std::max(0, sl.g.ex0 - 1) : sl.g.ex0, xb = sl.g.ex0 + sl.g.nown;   // fine planes [xa, xb)
+      const int j0 = dl ? sl.dlv[1].oa : xa / 2;                                              // coarse planes written
+      const int jend = dl ? sl.dlv[1].ob : std::min(n1.L.nx, xb / 2) + 1;
+      T* b1 = mgp<T>(dl ? sl.dlv[1].b : n1.b);
       const long long cols = (long long)(n1.L.ny + 1) * (n1.L.nz + 1);
       const int bx = (int)((cols + 127) / 128);
       int chunks = (int)std::max<long long>(1, std::min<long long>(jend - j0, (148LL * 64 + bx - 1) / bx));
       const int cx = (jend - j0 + chunks - 1) / chunks;
       chunks = (jend - j0 + cx - 1) / cx;
       const LvGeo Fs = lv_slab(sl);
+      const DevState* sgst = gate ? sl.st : nullptr;
+      const int acc = slabs && !dl ? 1 : 0;
       if (ctx->mg_f32)   // the pre-smoothing residual epilogue (kEpi = 2) wrote it in fp32
         k_mg_restrict0<float, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
-            Fs, n1.L, cx, sl.res32, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend, slabs ? 1 : 0);
+            Fs, n1.L, cx, sl.res32, n1.fixm, b1, sgst, sl.g.ex0, xa, xb, j0, jend, acc);
       else
         k_mg_restrict0<double, T><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
-            Fs, n1.L, cx, ctx->mg_kcycle ? sl.z : sl.q, n1.fixm, mgp<T>(n1.b), gst, sl.g.ex0, xa, xb, j0, jend,
-            slabs ? 1 : 0);
+            Fs, n1.L, cx, ctx->mg_kcycle ? sl.z : sl.q, n1.fixm, b1, sgst, sl.g.ex0, xa, xb, j0, jend, acc);
       ctx->launches++;
       debug_sync(ctx, "k_mg_restrict0");
     }
-    CK(mg_allreduce_level(ctx, n1.b, 3 * n1.L.ncomp, sizeof(T) == 4));
-    CK(enqueue_coarse_t<T>(ctx, 1, gate));
+    if (dl) {
+      CK(dist_coarse<T>(ctx, 1, gate));
+      CK(exchange_lv(ctx, 1, &DLv::x, sizeof(T), 3));   // the prolongation reads coarse planes oa - 1 .. ob
+    } else {
+      CK(mg_allreduce_level(ctx, n1.b, 3 * n1.L.ncomp, sizeof(T) == 4));
+      CK(enqueue_coarse_t<T>(ctx, 1, gate));
+    }
     if (nu == 1) {   // z = w D^-1 r (the first sweep, recomputed) + P x1, x-marching
       for (Slab& sl : ctx->slabs) {   // owned + ghost planes (the post-smoothing matvec reads the ghosts)
+        const T* x1 = mgp<T>(dl ? sl.dlv[1].x : n1.x);
         const int pa = std::max(0, sl.g.ex0 - 1), pb = std::min(sl.g.nelx, sl.g.ex0 + sl.g.nown) + 1;
         const int np = pb - (pa & ~1);
         const long long cols = (long long)(F.ny + 1) * (F.nz + 1);
@@ -1707,14 +1994,14 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
         chunks = (np + cx - 1) / cx;
         if (sizeof(T) == 4 && k32_active(ctx))   // fp32 Krylov residual
           k_mg_prolong0<T, float, float><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(
-              lv_slab(sl), n1.L, cx, sl.r32, sl.invd, om, mgp<T>(n1.x), sl.fixm, sl.z32, gst, sl.g.ex0, pa, pb);
+              lv_slab(sl), n1.L, cx, sl.r32, sl.invd, om, x1, sl.fixm, sl.z32, gst, sl.g.ex0, pa, pb);
         else if (sizeof(T) == 4)   // fp32 hierarchy: z in fp32 (read by the fp32-operator post-smoothing)
           k_mg_prolong0<T, float><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
-                                                                             mgp<T>(n1.x), sl.fixm, sl.z32, gst,
+                                                                             x1, sl.fixm, sl.z32, gst,
                                                                              sl.g.ex0, pa, pb);
         else
           k_mg_prolong0<T, double><<<dim3(bx, chunks), 128, 0, ctx->stream>>>(lv_slab(sl), n1.L, cx, sl.r, sl.invd, om,
-                                                                              mgp<T>(n1.x), sl.fixm, sl.z, gst,
+                                                                              x1, sl.fixm, sl.z, gst,
                                                                               sl.g.ex0, pa, pb);
         ctx->launches++;
         debug_sync(ctx, "k_mg_prolong0");
@@ -1747,7 +2034,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   MgLevel& m = ctx->mg[l];
   const int gL = grid_for(m.L.nodes());
   T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *mi = mgp<T>(m.invd);
-  if (m.S && m.L.nodes() <= kMgDeepNodes) {
+  if (m.S && m.L.nodes() <= mg_deep_nodes()) {
     // small stencil level: each damped-Jacobi sweep is one fused warp-split
     // stencil kernel (k_mg_sweep_st8) ping-ponging x and t
     const int gS = (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16);   // 32 nodes per block
@@ -1818,12 +2105,195 @@ int enqueue_coarse_t(topo_ctx* ctx, int l, int gate) {
   T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *kx = mgp<T>(m.kx), *kv = mgp<T>(m.kv);
   CK(enqueue_vcycle_t<T>(ctx, l, gate, false));   // x1 = B(b)
   CK(mg_apply<T>(ctx, l, gate));                  // t = A x1
-  LAUNCH(ctx, k_kc_dot1<T>, gF, n, mx, mt, mb, kx, kv, kc, gst, s.partials, s.counter);
-  LAUNCH(ctx, k_kc_r2<T>, gF, n, mb, kv, kc, gst);
+  LAUNCH(ctx, k_kc_dot1<T>, gF, m.L, mx, mt, mb, kx, kv, kc, gst, s.partials, s.counter);
+  LAUNCH(ctx, k_kc_r2<T>, gF, m.L, mb, kv, kc, gst);
   CK(enqueue_vcycle_t<T>(ctx, l, gate, false));   // x2 = B(r2)
   CK(mg_apply<T>(ctx, l, gate));                  // t = A x2
-  LAUNCH(ctx, k_kc_dot2<T>, gF, n, mx, mt, mb, kv, kc, gst, s.partials, s.counter);
-  LAUNCH(ctx, k_kc_combine<T>, gF, n, mx, kx, kc, gst);
+  LAUNCH(ctx, k_kc_dot2<T>, gF, m.L, mx, mt, mb, kv, kc, gst, s.partials, s.counter);
+  LAUNCH(ctx, k_kc_combine<T>, gF, m.L, mx, kx, kc, gst);
+  return check_launch(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// Distributed levels (x-slabs, levels 1 .. mg_dl; see mg_dist_plan): the cycle
+// of enqueue_vcycle_t / enqueue_coarse_t (nu = 1) on each slab's owned node
+// planes.  Ghost planes are exchanged where a step reads a neighbour's planes:
+// the operator apply reads x at oa - 1 and ob, the restriction reads b - t at
+// oa - 1, the prolongation reads the coarse plane ob / 2 (the right ghost of the
+// next level).  Dots of the K-cycle: owned planes, allreduced.
+// ---------------------------------------------------------------------------
+bool kc_level(const topo_ctx* ctx, int l) {
+  return ctx->mg_kcycle && l < (int)ctx->mg.size() - 1 && l >= ctx->mg_kmin && l <= ctx->mg_kmax;
+}
+bool dl_deep(const topo_ctx* ctx, int l) {
+  const MgLevel& m = ctx->mg[l];
+  return m.S && m.L.nodes() <= mg_deep_nodes();
+}
+// t = A x on the owned planes of every slab (x ghosts current)
+template <typename T>
+int dl_apply(topo_ctx* ctx, int l, int gate) {
+  MgLevel& m = ctx->mg[l];
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    const DevState* gst = gate ? sl.st : nullptr;
+    if (!m.stored) {   // level 1: P^T K(E) P matrix-free, element planes next to the owned nodes
+      CK(launch_l1_elem<T>(ctx, m, gst, &Ls, d.x, d.Y));
+      LAUNCH(ctx, (k_mg_l1_gather<false, T>), grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.t), gst,
+             (const T*)nullptr);
+    } else if (dl_deep(ctx, l)) {
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((Ls.nodes() + 31) / 32, 148LL * 8 * 16), Ls,
+             mgp<T>(m.S), mgp<T>(d.x), mgp<T>(d.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(d.t), gst);
+    } else {
+      LAUNCH(ctx, k_mg_apply_st<T>, grid_for(Ls.nodes()), Ls, mgp<T>(m.S), mgp<T>(d.x), m.fixm, mgp<T>(d.t), gst);
+    }
+  }
+  return check_launch(ctx);
+}
+
+template <typename T>
+int dist_coarse(topo_ctx* ctx, int l, int gate);
+
+template <typename T>
+int dist_vcycle(topo_ctx* ctx, int l, int gate) {
+  MgLevel& m = ctx->mg[l];
+  MgLevel& n1 = ctx->mg[l + 1];
+  const double* om = ctx->mg_om + l;
+  const bool deep = dl_deep(ctx, l), cdist = l + 1 <= ctx->mg_dl;
+  const size_t es = sizeof(T);
+  // pre-smoothing from 0 and t = A x
+  if (deep) {   // x = w D^-1 b formed on the fly at the neighbours: b ghosts
+    CK(exchange_lv(ctx, l, &DLv::b, es, 3));
+    for (Slab& sl : ctx->slabs) {
+      DLv& d = sl.dlv[l];
+      const LvGeo Ls = dl_geo(ctx, sl, l);
+      LAUNCH(ctx, (k_mg_sweep_st8<false, T, true>), (int)std::min<long long>((Ls.nodes() + 31) / 32, 148LL * 8 * 16),
+             Ls, mgp<T>(m.S), mgp<T>(d.x), mgp<T>(d.b), mgp<T>(m.invd), m.fixm, om, mgp<T>(d.t), gate ? sl.st : nullptr,
+             mgp<T>(d.x));
+    }
+  } else {
+    for (Slab& sl : ctx->slabs) {
+      DLv& d = sl.dlv[l];
+      const LvGeo Ls = dl_geo(ctx, sl, l);
+      LAUNCH(ctx, (k_mg_jacobi<0, false, T>), grid_for(Ls.nodes()), Ls, mgp<T>(d.b), mgp<T>(d.t), mgp<T>(m.invd),
+             m.fixm, om, mgp<T>(d.x), sl.st, gate, sl.partials, sl.counter);
+    }
+    CK(exchange_lv(ctx, l, &DLv::x, es, 3));
+    CK(dl_apply<T>(ctx, l, gate));
+    CK(exchange_lv(ctx, l, &DLv::b, es, 1));
+  }
+  // restriction of b - t into the owned coarse planes (read at oa - 1: left ghosts)
+  CK(exchange_lv(ctx, l, &DLv::t, es, 1));
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    LvGeo C = n1.L;
+    void* bc = n1.b;
+    if (cdist) {
+      C = dl_geo(ctx, sl, l + 1);
+      bc = sl.dlv[l + 1].b;
+    } else {
+      int oa = 0, ob = 0;
+      dl_owned(ctx, slab_rank(ctx, sl), l + 1, oa, ob);
+      C.xa = oa;
+      C.xb = ob - 1;
+    }
+    CK(launch_restrict<T>(ctx, m.L, C, mgp<T>(d.b), mgp<T>(d.t), m.fixm, n1.fixm, mgp<T>(bc), gate ? sl.st : nullptr));
+  }
+  if (cdist) {
+    CK(dist_coarse<T>(ctx, l + 1, gate));
+    CK(exchange_lv(ctx, l + 1, &DLv::x, es, 2));   // the prolongation reads coarse plane ob / 2
+  } else {
+    CK(gather_level(ctx, l + 1, n1.b, es));
+    CK(enqueue_coarse_t<T>(ctx, l + 1, gate));      // replicated below (slab 0's state gates it)
+  }
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    const T* xc = mgp<T>(cdist ? sl.dlv[l + 1].x : n1.x);
+    const DevState* gst = gate ? sl.st : nullptr;
+    if (deep)   // t = x + P e (out of place)
+      LAUNCH(ctx, (k_mg_prolong<true, T, T>), grid_for(Ls.nodes()), Ls, n1.L, xc, m.fixm, mgp<T>(d.t), gst,
+             (const T*)mgp<T>(d.x));
+    else
+      LAUNCH(ctx, (k_mg_prolong<true, T, T>), grid_for(Ls.nodes()), Ls, n1.L, xc, m.fixm, mgp<T>(d.x), gst);
+  }
+  // post-smoothing
+  if (deep) {
+    CK(exchange_lv(ctx, l, &DLv::t, es, 3));
+    for (Slab& sl : ctx->slabs) {
+      DLv& d = sl.dlv[l];
+      const LvGeo Ls = dl_geo(ctx, sl, l);
+      LAUNCH(ctx, (k_mg_sweep_st8<true, T>), (int)std::min<long long>((Ls.nodes() + 31) / 32, 148LL * 8 * 16), Ls,
+             mgp<T>(m.S), mgp<T>(d.t), mgp<T>(d.b), mgp<T>(m.invd), m.fixm, om, mgp<T>(d.x), gate ? sl.st : nullptr);
+    }
+    return check_launch(ctx);
+  }
+  CK(exchange_lv(ctx, l, &DLv::x, es, 3));
+  if (!m.stored) {   // level 1: the sweep fused into the gather phase
+    for (Slab& sl : ctx->slabs) {
+      DLv& d = sl.dlv[l];
+      const LvGeo Ls = dl_geo(ctx, sl, l);
+      const DevState* gst = gate ? sl.st : nullptr;
+      CK(launch_l1_elem<T>(ctx, m, gst, &Ls, d.x, d.Y));
+      LAUNCH(ctx, k_mg_l1_gather_jac<T>, grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.x), mgp<T>(d.b),
+             mgp<T>(m.invd), om, gst);
+    }
+    return check_launch(ctx);
+  }
+  CK(dl_apply<T>(ctx, l, gate));
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    LAUNCH(ctx, (k_mg_jacobi<1, false, T>), grid_for(Ls.nodes()), Ls, mgp<T>(d.b), mgp<T>(d.t), mgp<T>(m.invd), m.fixm,
+           om, mgp<T>(d.x), sl.st, gate, sl.partials, sl.counter);
+  }
+  return check_launch(ctx);
+}
+
+template <typename T>
+int dist_coarse(topo_ctx* ctx, int l, int gate) {
+  if (!kc_level(ctx, l)) return dist_vcycle<T>(ctx, l, gate);
+  const size_t es = sizeof(T);
+  CK(dist_vcycle<T>(ctx, l, gate));   // x1 = B(b)
+  CK(exchange_lv(ctx, l, &DLv::x, es, 3));
+  CK(dl_apply<T>(ctx, l, gate));      // t = A x1
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    LAUNCH(ctx, k_kc_dot1<T>, grid_for(3 * (Ls.v_hi() - Ls.v_lo())), Ls, mgp<T>(d.x), mgp<T>(d.t), mgp<T>(d.b),
+           mgp<T>(d.kx), mgp<T>(d.kv), d.kc, gate ? sl.st : nullptr, sl.partials, sl.counter, sl.st);
+  }
+  CK(allreduce(ctx, 0, 2, 0));
+  for (Slab& sl : ctx->slabs) {
+    k_kc_finish1<<<1, 1, 0, ctx->stream>>>(sl.st, sl.dlv[l].kc, gate ? sl.st : nullptr);
+    ctx->launches++;
+  }
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    LAUNCH(ctx, k_kc_r2<T>, grid_for(3 * (Ls.v_hi() - Ls.v_lo())), Ls, mgp<T>(d.b), mgp<T>(d.kv), d.kc,
+           gate ? sl.st : nullptr);
+  }
+  CK(dist_vcycle<T>(ctx, l, gate));   // x2 = B(r2)
+  CK(exchange_lv(ctx, l, &DLv::x, es, 3));
+  CK(dl_apply<T>(ctx, l, gate));      // t = A x2
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    LAUNCH(ctx, k_kc_dot2<T>, grid_for(3 * (Ls.v_hi() - Ls.v_lo())), Ls, mgp<T>(d.x), mgp<T>(d.t), mgp<T>(d.b),
+           mgp<T>(d.kv), d.kc, gate ? sl.st : nullptr, sl.partials, sl.counter, sl.st);
+  }
+  CK(allreduce(ctx, 0, 3, 0));
+  for (Slab& sl : ctx->slabs) {
+    k_kc_finish2<<<1, 1, 0, ctx->stream>>>(sl.st, sl.dlv[l].kc, gate ? sl.st : nullptr);
+    ctx->launches++;
+  }
+  for (Slab& sl : ctx->slabs) {
+    DLv& d = sl.dlv[l];
+    const LvGeo Ls = dl_geo(ctx, sl, l);
+    LAUNCH(ctx, k_kc_combine<T>, grid_for(3 * (Ls.v_hi() - Ls.v_lo())), Ls, mgp<T>(d.x), mgp<T>(d.kx), d.kc,
+           gate ? sl.st : nullptr);
+  }
   return check_launch(ctx);
 }
 
@@ -2444,6 +2914,13 @@ void free_ctx(topo_ctx* ctx) {
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }
+  for (Slab& s : ctx->slabs)
+    for (DLv& d : s.dlv)
+      if (d.own) {
+        void* ptrs[] = {d.x, d.b, d.t, d.kx, d.kv, d.Y, d.kc};
+        for (void* p : ptrs)
+          if (p) cudaFree(p);
+      }
   for (MgLevel& m : ctx->mg) {
     void* ptrs[] = {m.x, m.b, m.t, m.invd, m.K, m.S, m.Y, m.pw, m.pw_b, m.fixm, m.kx, m.kv};
     for (void* p : ptrs)
@@ -2772,6 +3249,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   }
   rc = upload_nodes(ctx, load, &Slab::f);
   if (rc == TOPO_OK) rc = mg_build(ctx, fixed);
+  if (rc == TOPO_OK) rc = mg_dist_plan(ctx);
   if (rc == TOPO_OK && ctx->mode == TOPO_DIST_HOST && W > 1) rc = open_host_transport(ctx, dist);
   if (rc == TOPO_OK) rc = ensure_constants(ctx);
   if (rc == TOPO_OK) {
@@ -3107,6 +3585,7 @@ int64_t topo_count(const topo_ctx* ctx, int32_t what) {
     case TOPO_COUNT_DESIGN: return ctx->n_design;
     case TOPO_COUNT_STENCIL: return (long long)ctx->st_off.size();
     case TOPO_COUNT_DEVICE_BYTES: return (long long)ctx->dev_bytes;
+    case TOPO_COUNT_MG_DIST: return ctx->mg_dl;
     default: return -1;
   }
 }

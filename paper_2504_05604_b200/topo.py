@@ -23,7 +23,7 @@ NODE_FIELDS = {"u", "invdiag", "r"}
 TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK, TOPO_DIST_HOST = 0, 1, 2, 3
 TOPO_PRECOND_JACOBI, TOPO_PRECOND_MG, TOPO_PRECOND_AUTO = 0, 1, 2
 PRECOND = dict(jacobi=0, mg=1, auto=2)
-COUNTS = dict(ndof=0, nel=1, nodes=2, design=3, stencil=4, device_bytes=5)
+COUNTS = dict(ndof=0, nel=1, nodes=2, design=3, stencil=4, device_bytes=5, mg_dist=6)
 
 # Every symbol include/topo.h declares (checked by tests/test_abi.py).
 EXPORTS = ["topo_params_default", "topo_init", "topo_set_stream", "topo_owned_range",

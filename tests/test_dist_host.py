@@ -22,6 +22,11 @@ def _problem(kind, **over):
     from workloads import config_params, cantilever_load, cantilever_fixed, solid_block_passive, make_problem
     if kind == "cfg1":
         return make_problem(1, **over)
+    if kind == "dist":   # 4 levels: levels 1-2 distributed over the slabs (TOPO_DIST_MIN_NODES=0)
+        dims = (128, 32, 16)
+        p = config_params(dict(nelx=dims[0], nely=dims[1], nelz=dims[2], volfrac=0.2, rmin=1.5, n_iter=3,
+                               cg_rtol=1e-10, obstacle=None), **over)
+        return p, cantilever_load(*dims), cantilever_fixed(*dims), None
     dims = (36, 12, 6)
     p = config_params(dict(nelx=dims[0], nely=dims[1], nelz=dims[2], volfrac=0.25, rmin=2.5, n_iter=5,
                            cg_rtol=1e-10, obstacle=None), **over)
@@ -29,8 +34,9 @@ def _problem(kind, **over):
     return p, cantilever_load(*dims), cantilever_fixed(*dims), pas
 
 
-def _worker(rank, world, tid, kind, over, n_iter, q, die_after_init=False, timeout=None):
+def _worker(rank, world, tid, kind, over, n_iter, q, die_after_init=False, timeout=None, env=None):
     try:
+        os.environ.update(env or {})
         if timeout is not None:
             os.environ["TOPO_COMM_TIMEOUT"] = str(timeout)
         import torch
@@ -42,6 +48,8 @@ def _worker(rank, world, tid, kind, over, n_iter, q, die_after_init=False, timeo
             if die_after_init:
                 os._exit(0)
             a, b = pr.owned_range()
+            if env and "TOPO_DIST_MIN_NODES" in env:
+                assert pr.count("mg_dist") == 2
             try:
                 c, x, nd = pr.optimize(n_iter)
                 q.put((rank, "ok", c.tolist(), (a, b), x, pr.timings()["cg_iters_total"]))
@@ -52,13 +60,13 @@ def _worker(rank, world, tid, kind, over, n_iter, q, die_after_init=False, timeo
         q.put((rank, "exc", code, repr(e), None, None))
 
 
-def _run(world, kind, over, n_iter=5, **kw):
+def _run(world, kind, over, n_iter=5, env=None, **kw):
     from paper_2504_05604_b200 import topo
     tid = topo.host_transport_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, tid, kind, over, n_iter, q),
-                         kwargs=kw.get("per_rank", {}).get(r, {})) for r in range(world)]
+                         kwargs=dict(kw.get("per_rank", {}).get(r, {}), env=env)) for r in range(world)]
     for pr in procs:
         pr.start()
     out = {}
@@ -116,6 +124,34 @@ def test_host_transport_matches_loopback_and_oracle(gpu, world, kind, precond):
     np.testing.assert_allclose(x.ravel(), xl, rtol=0, atol=1e-12)
     ro = oracle.run_optimization(p, f, fx, pas, n_iter=5)
     assert np.max(np.abs(c0 - ro["c"]) / ro["c"]) <= 1e-6
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_host_transport_distributed_levels(gpu, monkeypatch, world):
+    """Multigrid levels 1-2 distributed over one process per slab (ghost-plane
+    exchanges, K-cycle dot allreduces and the level-3 all-gather through the
+    host transport): c history and design equal the loopback slabs (same
+    partition) to 1e-12 and the single slab to 1e-9."""
+    from paper_2504_05604_b200 import topo
+    env = {"TOPO_DIST_MIN_NODES": "0"}
+    over = dict(precond="mg")
+    out = _run(world, "dist", over, n_iter=3, env=env)
+    assert sorted(out) == list(range(world)), out
+    for r in range(world):
+        assert out[r][1] == "ok", out[r]
+    c0 = np.array(out[0][2])
+    p, f, fx, pas = _problem("dist", **over)
+    x = np.zeros(p["nelx"] * p["nely"] * p["nelz"]).reshape(p["nelz"], p["nelx"], p["nely"])
+    for r in range(world):
+        a, b = out[r][3]
+        x[:, a:b, :] = out[r][4].reshape(p["nelz"], p["nelx"], p["nely"])[:, a:b, :]
+    monkeypatch.setenv("TOPO_DIST_MIN_NODES", "0")
+    cl, xl = _loopback(world, "dist", over, n_iter=3)
+    np.testing.assert_allclose(c0, cl, rtol=1e-12, atol=0)
+    np.testing.assert_allclose(x.ravel(), xl, rtol=0, atol=1e-12)
+    with topo.Problem(p, f, fx, pas) as pr:
+        c1, x1, _ = pr.optimize(3)
+    assert np.max(np.abs(c0 - c1) / c1) <= 1e-9
 
 
 def test_host_transport_peer_never_joins(gpu):
