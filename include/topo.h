@@ -94,6 +94,12 @@ extern "C" {
 #define TOPO_DIST_NCCL     1
 #define TOPO_DIST_LOOPBACK 2
 #define TOPO_DIST_HOST     3   /* one process per slab, host-staged shared-memory transport (tests) */
+#define TOPO_DIST_SOLO     4   /* measurement only: rank `rank`'s slab of a `world`-slab run, alone on
+                                  this GPU, every exchange / allreduce / all-gather omitted (the
+                                  other ranks' moduli are this slab's, tiled).  The kernel sequence
+                                  and sizes are one rank's of the NCCL run; the numbers are NOT a
+                                  solution of the problem (the coupling is dropped) -- for per-rank
+                                  compute time of a strong-scaling run (tools/solo_scale.py)      */
 
 typedef struct topo_ctx topo_ctx;    /* opaque; owns all device state */
 
@@ -171,7 +177,7 @@ typedef struct {
 #define TOPO_PRECOND_AUTO   2
 
 typedef struct {
-  int32_t mode;               /* TOPO_DIST_SINGLE / _NCCL / _LOOPBACK                       */
+  int32_t mode;               /* TOPO_DIST_SINGLE / _NCCL / _LOOPBACK / _HOST / _SOLO       */
   int32_t rank, world;        /* NCCL: this rank, #ranks; LOOPBACK: world = #slabs          */
   int32_t device;             /* CUDA device ordinal of this rank                            */
   const uint8_t *nccl_id;     /* NCCL: 128-byte ncclUniqueId broadcast by the caller;

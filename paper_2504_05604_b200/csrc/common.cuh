@@ -54,6 +54,7 @@ struct DevState {
   int status;       // 0 ok, 2 ENOCONV, 3 EBREAKDOWN
   int fresh;        // 1 -> next p-update uses beta = 0 (start / restart)
   int pending;      // 1 -> u lacks alpha_prev * p (applied by the next odd update or a flush)
+  int solo;         // TOPO_DIST_SOLO timing runs: no convergence / breakdown exit (max_it iterations)
   double alpha_prev;
   // OC bisection
   double l1, l2, lmid, target, vol, oc_tol;

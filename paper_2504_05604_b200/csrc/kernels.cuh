@@ -101,10 +101,10 @@ __device__ __forceinline__ void cg_finish_update(DevState* st, double rz_new, do
   st->rr = rr;
   st->it += 1;
   st->fresh = 0;
-  if (!isfinite(rr) || !isfinite(rz_new)) {
+  if ((!isfinite(rr) || !isfinite(rz_new)) && !st->solo) {
     st->status = 3;
     st->done = 1;
-  } else if (rr <= st->tol2 * st->bb) {
+  } else if (!st->solo && rr <= st->tol2 * st->bb) {
     st->done = 1;
   } else if (st->it >= st->max_it) {
     st->status = 2;
@@ -216,8 +216,10 @@ __global__ void k_finish_alpha(DevState* st) {
   if (st->done) return;
   const double pq = st->sums[0];
   st->pq = pq;
-  if (!(pq > 0.0) || !isfinite(pq)) { st->status = 3; st->done = 1; }
-  else st->alpha = st->rz / pq;
+  if (!(pq > 0.0) || !isfinite(pq)) {
+    if (st->solo) st->alpha = 0.0;
+    else { st->status = 3; st->done = 1; }
+  } else st->alpha = st->rz / pq;
 }
 template <bool kMG = false>
 __global__ void k_finish_update(DevState* st, int even) {
@@ -229,7 +231,9 @@ __global__ void k_finish_update(DevState* st, int even) {
 __global__ void k_finish_rho(DevState* st, int flex) {
   if (st->done) return;
   const double rho = st->sums[0];
-  if (!(rho > 0.0) || !isfinite(rho)) {
+  if ((!(rho > 0.0) || !isfinite(rho)) && st->solo) {
+    st->beta = 0.0;
+  } else if (!(rho > 0.0) || !isfinite(rho)) {
     st->status = 3;
     st->done = 1;
   } else {
@@ -292,7 +296,7 @@ k_dot(Geo g, DevState* st, const double* __restrict__ a, const double* __restric
 // A5  ce = u_e^T KE u_e ; dc = -p xPhys^(p-1)(E0-Emin) ce (0 on passive);
 //     partial c = sum E ce.                                     (§2.3)
 // ===========================================================================
-__global__ void __launch_bounds__(kBlock, 3)
+__global__ void __launch_bounds__(kBlock)
 k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
        const double* __restrict__ E, const double* __restrict__ xphys,
        const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
@@ -334,6 +338,87 @@ k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
     const double xp = xphys[i];
     dc[i] = passive[i] ? 0.0 : -m.penal * simp_pow(xp, m.penal - 1.0) * (m.E0 - m.Emin) * s;
     csum = fma(E[i], s, csum);
+  }
+  __shared__ double tot[1];
+  double v[1] = {csum};
+  if (grid_reduce<1>(v, partials, counter, tot) && threadIdx.x == 0) st->sums[0] = tot[0];
+}
+
+// A5 x-marching: a thread owns one (ey, ez) element column and walks kSensCX
+// elements along x; the 4 corners x 3 components of each node plane are loaded
+// once and shared by the two elements left and right of it (12 instead of 24
+// loads per element; the next plane's loads are issued before the current
+// element's arithmetic).  Same per-element arithmetic as k_sens.
+constexpr int kSensCX = 16;
+__global__ void __launch_bounds__(kBlock)
+k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
+         const double* __restrict__ E, const double* __restrict__ xphys,
+         const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
+         double* partials, unsigned int* counter) {
+  const long long ncol = (long long)g.nely * g.nelz;
+  const int nchunk = (g.nex + kSensCX - 1) / kSensCX;
+  double csum = 0.0;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncol * nchunk;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int chunk = (int)(t / ncol);
+    const long long col = t - (long long)chunk * ncol;
+    const int ez = (int)(col / g.nely), ey = (int)(col - (long long)ez * g.nely);
+    const int xa = g.ex0 + chunk * kSensCX, xb = min(xa + kSensCX, g.ex0 + g.nex);
+    // corners of a node plane, j = ay + 2 az
+    const long long n0 = node_idx(g, xa, ey, ez);
+    long long o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = (long long)(j >> 1) * g.NY + (j & 1);
+    double A[3][4], B[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) A[c][j] = u[n0 + o[j] + c * g.ncomp];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) B[c][j] = u[n0 + g.nplane + o[j] + c * g.ncomp];
+    long long e = elem_idx(g, xa, ey, ez);
+    for (int ex = xa; ex < xb; ++ex, e += g.eplane) {
+      double P[3][8], Q[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {   // natural corner index k = ax + 2 ay + 4 az = ax + 2 j
+          P[c][2 * j] = A[c][j];
+          P[c][2 * j + 1] = B[c][j];
+          A[c][j] = B[c][j];
+        }
+      if (ex + 1 < xb) {                // next plane's corners, in flight during the arithmetic
+        const long long nn = n0 + (long long)(ex + 2 - xa) * g.nplane;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) B[c][j] = u[nn + o[j] + c * g.ncomp];
+      }
+      const double Ee = E[e], xp = xphys[e];
+      const uint8_t pv = passive[e];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int bb = 1; bb < 8; bb <<= 1)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (!(k & bb)) {
+              const double x0 = P[c][k], x1 = P[c][k | bb];
+              P[c][k] = x0 + x1;
+              P[c][k | bb] = x0 - x1;
+            }
+      wht_block(P, 1.0, Q);
+      double sv = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sv = fma(P[c][k], Q[c][k], sv);
+      ce[e] = sv;
+      dc[e] = pv ? 0.0 : -m.penal * simp_pow(xp, m.penal - 1.0) * (m.E0 - m.Emin) * sv;
+      csum = fma(Ee, sv, csum);
+    }
   }
   __shared__ double tot[1];
   double v[1] = {csum};
@@ -931,6 +1016,7 @@ namespace topo {
 __global__ void k_cg_init(DevState* st, double tol2, double bb, long long max_it) {
   st->pending = 0;
   st->alpha_prev = 0.0;
+  st->solo = tol2 < 0.0;   // TOPO_DIST_SOLO: a fixed iteration count, never a breakdown exit
   st->tol2 = tol2;
   st->bb = bb;
   st->max_it = max_it;
@@ -946,7 +1032,7 @@ __global__ void k_cg_start(DevState* st) {
   st->rr = st->sums[1];
   st->fresh = 1;
   st->status = 0;
-  st->done = (st->rr <= st->tol2 * st->bb) ? 1 : 0;
+  st->done = (!st->solo && st->rr <= st->tol2 * st->bb) ? 1 : 0;
 }
 __global__ void k_oc_init(DevState* st, double lmax, double target, double tol) {
   st->l1 = 0.0;

@@ -384,6 +384,27 @@ int ensure_constants(topo_ctx* ctx) {
         fw[((o.x + ctx->R) * 7 + (o.z + ctx->R)) * 7 + (o.y + ctx->R)] = ctx->st_w[k];
       }
       CU(cudaMemcpyToSymbolAsync(c_fw, fw, sizeof fw, 0, cudaMemcpyHostToDevice, ctx->stream));
+      // by class (|dx|, a <= b): the stencil is a function of |d| (checked here)
+      static double fw2[64];
+      std::fill(fw2, fw2 + 64, 0.0);
+      const int R = ctx->R;
+      for (int dx = -R; dx <= R; ++dx)
+        for (int dz = -R; dz <= R; ++dz)
+          for (int dy = -R; dy <= R; ++dy) {
+            const int a = std::min(std::abs(dy), std::abs(dz)), b = std::max(std::abs(dy), std::abs(dz));
+            const double w = fw[((dx + R) * 7 + (dz + R)) * 7 + (dy + R)];
+            double& c = fw2[(std::abs(dx) * 4 + a) * 4 + b];
+            if (dx >= 0 && dy >= 0 && dz >= 0 && dy <= dz) c = w;
+          }
+      for (int dx = -R; dx <= R; ++dx)
+        for (int dz = -R; dz <= R; ++dz)
+          for (int dy = -R; dy <= R; ++dy) {
+            const int a = std::min(std::abs(dy), std::abs(dz)), b = std::max(std::abs(dy), std::abs(dz));
+            if (fw[((dx + R) * 7 + (dz + R)) * 7 + (dy + R)] != fw2[(std::abs(dx) * 4 + a) * 4 + b] ||
+                (fw2[(std::abs(dx) * 4 + a) * 4 + b] != 0.0 && dx * dx + a * a + b * b >= (R + 1) * (R + 1)))
+              return set_err(ctx, TOPO_EINVAL, "filter stencil is not a function of |d|");
+          }
+      CU(cudaMemcpyToSymbolAsync(c_fw2, fw2, sizeof fw2, 0, cudaMemcpyHostToDevice, ctx->stream));
     }
     CU(cudaStreamSynchronize(ctx->stream));
   }
@@ -408,7 +429,7 @@ int host_launch(topo_ctx* ctx, const HostOp& op) {
 
 int allreduce(topo_ctx* ctx, int k0, int nk, int maxmask) {
   const int W = ctx->world;
-  if (W == 1) return TOPO_OK;
+  if (W == 1 || ctx->mode == TOPO_DIST_SOLO) return TOPO_OK;
   if (ctx->mode == TOPO_DIST_HOST) {
     DevState* st = ctx->slabs[0].st;
     CU(cudaMemcpyAsync(ctx->ht->hsend, st->sums + k0, sizeof(double) * nk, cudaMemcpyDeviceToHost, ctx->stream));
@@ -445,7 +466,7 @@ int allreduce(topo_ctx* ctx, int k0, int nk, int maxmask) {
 // node planes of a 3-component vector: owned boundary planes -> neighbours' ghosts
 int exchange_nodes(topo_ctx* ctx, double* Slab::*field, int ncomp = 3) {
   const int W = ctx->world;
-  if (W == 1) return TOPO_OK;
+  if (W == 1 || ctx->mode == TOPO_DIST_SOLO) return TOPO_OK;
   if (ctx->mode == TOPO_DIST_LOOPBACK) {
     for (int s = 0; s < W; ++s) {
       Slab& a = ctx->slabs[s];
@@ -511,7 +532,7 @@ int exchange_nodes(topo_ctx* ctx, double* Slab::*field, int ncomp = 3) {
 // k element planes each side: owned boundary planes -> neighbours' halos
 int exchange_elems(topo_ctx* ctx, double* Slab::*field, int k) {
   const int W = ctx->world;
-  if (W == 1 || k <= 0) return TOPO_OK;
+  if (W == 1 || k <= 0 || ctx->mode == TOPO_DIST_SOLO) return TOPO_OK;
   if (ctx->mode == TOPO_DIST_LOOPBACK) {
     for (int s = 0; s < W; ++s) {
       Slab& a = ctx->slabs[s];
@@ -896,10 +917,12 @@ int build_maps(topo_ctx* ctx, Slab& s) {
 template <int R, int MODE>
 int launch_filt25_r(topo_ctx* ctx, Slab& s, const double* a, double* out) {
   using L = F25Smem<R>;
+  static const bool sym = !getenv("TOPO_FILT_SYM") || atoi(getenv("TOPO_FILT_SYM")) != 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(ctx->f25_attr_mask & (1u << (dev * 4 + MODE % 4)))) {   // opt-in per device
-    CU(cudaFuncSetAttribute(k_filt25<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    CU(cudaFuncSetAttribute(k_filt25<R, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
+    CU(cudaFuncSetAttribute(k_filt25<R, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES));
     ctx->f25_attr_mask |= 1u << (dev * 4 + MODE % 4);
   }
   const int gy = (s.g.nely + kF25Y - 1) / kF25Y, gz = (s.g.nelz + kF25Z - 1) / kF25Z;
@@ -908,7 +931,8 @@ int launch_filt25_r(topo_ctx* ctx, Slab& s, const double* a, double* out) {
   gx = std::min<long long>(gx, std::max(1, s.g.nex / 8));   // >= 8 output planes per chunk
   const int CX = (int)((s.g.nex + gx - 1) / gx);
   gx = (s.g.nex + CX - 1) / CX;
-  k_filt25<R, MODE><<<dim3(gy, gz, (unsigned)gx), dim3(kF25Y, kF25Z / kF25TZ), L::BYTES, ctx->stream>>>(
+  auto kern = sym ? k_filt25<R, MODE, true> : k_filt25<R, MODE, false>;
+  kern<<<dim3(gy, gz, (unsigned)gx), dim3(kF25Y, kF25Z / kF25TZ), L::BYTES, ctx->stream>>>(
       s.m_vpad, s.g, s.fp, CX, a, s.hs, s.passive, out);
   ctx->launches++;
   debug_sync(ctx, "k_filt25");
@@ -1090,6 +1114,18 @@ int mg_gather_E(topo_ctx* ctx) {
     return TOPO_OK;
   }
   Slab& a = ctx->slabs[0];
+  if (ctx->mode == TOPO_DIST_SOLO) {   // no peers: own planes tiled over every rank's range (same bytes land)
+    for (int r = 0; r < ctx->world; ++r) {
+      int b = 0, e = 0;
+      topo_partition(ctx->prm.nelx, ctx->prm.rmin, ctx->world, r, &b, &e);
+      for (int P = b; P < e; P += a.g.nex) {
+        const int n = std::min(e - P, a.g.nex);
+        CU(cudaMemcpyAsync(dst(P), a.E + (size_t)a.g.H * a.g.eplane, sizeof(double) * n * a.g.eplane,
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    return TOPO_OK;
+  }
   if (ctx->mode == TOPO_DIST_HOST) {   // all-gather of the owned planes through the shared segment
     HostOp op;
     op.t = ctx->ht;
@@ -1124,7 +1160,8 @@ int mg_gather_E(topo_ctx* ctx) {
 
 // x-slabs, NCCL: sum of the slabs' partial level-1 restrictions (in place)
 int mg_allreduce_level(topo_ctx* ctx, void* buf, size_t n, bool f32) {
-  if (ctx->world == 1 || ctx->mode == TOPO_DIST_LOOPBACK) return TOPO_OK;   // loopback: accumulated in slab order
+  if (ctx->world == 1 || ctx->mode == TOPO_DIST_LOOPBACK || ctx->mode == TOPO_DIST_SOLO)
+    return TOPO_OK;   // loopback: accumulated in slab order
   if (ctx->mode == TOPO_DIST_HOST) {
     const size_t es = f32 ? sizeof(float) : sizeof(double);
     CU(cudaMemcpyAsync(ctx->ht->hsend, buf, es * n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1453,7 +1490,7 @@ struct PlaneSet {
 template <typename Get>
 int exchange_planes(topo_ctx* ctx, Get get, size_t es, long long nplane, int dirs) {
   const int W = ctx->world;
-  if (W == 1) return TOPO_OK;
+  if (W == 1 || ctx->mode == TOPO_DIST_SOLO) return TOPO_OK;
   const size_t pb = es * nplane;
   auto at = [&](const PlaneSet& p, long long P, int c) { return p.v + es * (c * p.ncomp + (P - p.b0 + 1) * nplane); };
   if (ctx->mode == TOPO_DIST_LOOPBACK) {
@@ -1539,7 +1576,7 @@ int exchange_fine(topo_ctx* ctx, void* (*field)(Slab&), size_t es, int dirs) {
 // the slabs wrote one shared buffer -- nothing to do).
 int gather_level(topo_ctx* ctx, int l, void* buf, size_t es) {
   const int W = ctx->world;
-  if (W == 1 || ctx->mode == TOPO_DIST_LOOPBACK) return TOPO_OK;
+  if (W == 1 || ctx->mode == TOPO_DIST_LOOPBACK || ctx->mode == TOPO_DIST_SOLO) return TOPO_OK;
   const LvGeo& L = ctx->mg[l].L;
   char* v = static_cast<char*>(buf);
   auto at = [&](long long P, int c) { return v + es * (c * L.ncomp + (P + 1) * L.nplane); };
@@ -2390,7 +2427,8 @@ int solve_pass(topo_ctx* ctx, int mg, int* replacements_out, double* rr_true_out
   const long long n_dof = 3LL * (P.nelx + 1) * (P.nely + 1) * (P.nelz + 1);
   const long long maxit = P.cg_max_iter > 0 ? P.cg_max_iter : 10 * n_dof;
   for (Slab& s : ctx->slabs) {
-    k_cg_init<<<1, 1, 0, ctx->stream>>>(s.st, P.cg_rtol * P.cg_rtol, ctx->bb, maxit);
+    k_cg_init<<<1, 1, 0, ctx->stream>>>(s.st, ctx->mode == TOPO_DIST_SOLO ? -1.0 : P.cg_rtol * P.cg_rtol, ctx->bb,
+                                        maxit);
     ctx->launches++;
   }
   CK(residual(ctx, true));
@@ -2429,6 +2467,7 @@ int solve_pass(topo_ctx* ctx, int mg, int* replacements_out, double* rr_true_out
       continue;
     }
     CK(flush_u(ctx));
+    if (ctx->mode == TOPO_DIST_SOLO) break;   // timing run: exactly cg_max_iter iterations, no residual check
     if (h.status == 2) { rc = set_err(ctx, TOPO_ENOCONV, "PCG: no convergence in %lld iterations", h.it); break; }
     if (h.status == 3) { rc = set_err(ctx, TOPO_EBREAKDOWN, "PCG breakdown at iteration %lld", h.it); break; }
     CK(residual(ctx, false));
@@ -2534,8 +2573,14 @@ int do_sensitivity(topo_ctx* ctx, double* c_out, double* fu_out) {
   CK(exchange_nodes(ctx, &Slab::u));
   const Material m = material(ctx);
   for (Slab& s : ctx->slabs) {
-    LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
-           s.passive, s.ce, s.dc, s.partials, s.counter);
+    static const bool sens_x = !getenv("TOPO_SENS_X") || atoi(getenv("TOPO_SENS_X")) != 0;
+    if (sens_x)
+      LAUNCH(ctx, k_sens_x,
+             grid_resident(k_sens_x, (long long)s.g.nely * s.g.nelz * ((s.g.nex + kSensCX - 1) / kSensCX)), s.g, s.st,
+             m, s.u, s.E, s.xphys, s.passive, s.ce, s.dc, s.partials, s.counter);
+    else
+      LAUNCH(ctx, k_sens, grid_resident(k_sens, (long long)s.g.nex * s.g.eplane), s.g, s.st, m, s.u, s.E, s.xphys,
+             s.passive, s.ce, s.dc, s.partials, s.counter);
     LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.u, 1, s.partials, s.counter);
   }
   CK(check_launch(ctx));
@@ -3121,7 +3166,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
   if (const char* e = getenv("TOPO_COMM_TIMEOUT")) ctx->comm_timeout_s = atof(e);
   if (rc == TOPO_OK && ctx->mode == TOPO_DIST_HOST && (!dist || !dist->nccl_id))
     rc = set_err(ctx, TOPO_EINVAL, "TOPO_DIST_HOST needs the transport id (topo_host_transport_id) in nccl_id");
-  if (rc == TOPO_OK && (ctx->mode < TOPO_DIST_SINGLE || ctx->mode > TOPO_DIST_HOST))
+  if (rc == TOPO_OK && (ctx->mode < TOPO_DIST_SINGLE || ctx->mode > TOPO_DIST_SOLO))
     rc = set_err(ctx, TOPO_EINVAL, "bad dist mode %d", ctx->mode);
   if (rc == TOPO_OK && ctx->mode == TOPO_DIST_SINGLE && ctx->world != 1)
     rc = set_err(ctx, TOPO_EINVAL, "TOPO_DIST_SINGLE needs world == 1");
@@ -3180,7 +3225,8 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
     if (r != 0) { rc = set_err(ctx, TOPO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); free_ctx(ctx); return rc; }
   }
   // local slabs
-  const bool own_only = ctx->mode == TOPO_DIST_NCCL || ctx->mode == TOPO_DIST_HOST;   // one slab per process
+  const bool own_only = ctx->mode == TOPO_DIST_NCCL || ctx->mode == TOPO_DIST_HOST ||
+                        ctx->mode == TOPO_DIST_SOLO;   // one slab per process
   const int s_begin = own_only ? ctx->rank : 0;
   const int s_end = own_only ? ctx->rank + 1 : W;
   for (int s = s_begin; s < s_end; ++s) {

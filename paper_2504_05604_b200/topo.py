@@ -20,7 +20,7 @@ TOPO_FILTER_DENSITY, TOPO_FILTER_SENSITIVITY, TOPO_FILTER_PLAIN = 0, 1, 2
 TOPO_FILTER_X, TOPO_FILTER_DC = 0, 1
 FIELDS = dict(u=0, x=1, xphys=2, E=3, ce=4, dc=5, dcf=6, dvf=7, xnew=8, hs=9, invdiag=10, r=11)
 NODE_FIELDS = {"u", "invdiag", "r"}
-TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK, TOPO_DIST_HOST = 0, 1, 2, 3
+TOPO_DIST_SINGLE, TOPO_DIST_NCCL, TOPO_DIST_LOOPBACK, TOPO_DIST_HOST, TOPO_DIST_SOLO = 0, 1, 2, 3, 4
 TOPO_PRECOND_JACOBI, TOPO_PRECOND_MG, TOPO_PRECOND_AUTO = 0, 1, 2
 PRECOND = dict(jacobi=0, mg=1, auto=2)
 COUNTS = dict(ndof=0, nel=1, nodes=2, design=3, stencil=4, device_bytes=5, mg_dist=6)

@@ -117,3 +117,21 @@ def test_dist_code_path_one_slab(topo, monkeypatch, fp32):
     assert_rel(zF, z1, 1e-6 if fp32 else 1e-12, "V-cycle")
     assert itF == it1
     assert_rel(cF, c1, 1e-10, "c history")
+
+
+@pytest.mark.parametrize("W,r", [(2, 1), (4, 2)])
+def test_solo_timing_mode_runs_fixed_iterations(topo, monkeypatch, W, r):
+    """TOPO_DIST_SOLO (tools/solo_scale.py): rank r's slab alone, no transport;
+    every solve runs exactly cg_max_iter PCG iterations with no breakdown exit and
+    no Jacobi fallback, so the kernel sequence per iteration is the NCCL rank's."""
+    monkeypatch.setenv("TOPO_DIST_MIN_NODES", "0")
+    p, f, fx, pas, x = _case(1)
+    p = dict(p, cg_max_iter=7)
+    with topo.Problem(p, f, fx, pas, dist=dict(mode=topo.TOPO_DIST_SOLO, rank=r, world=W, device=0)) as pr:
+        assert pr.count("mg_dist") == 2
+        lo, hi = pr.owned_range()
+        assert (lo, hi) == topo.partition(DIMS[0], p["rmin"], W, r)
+        pr.optimize(2, want_x=False)
+        t = pr.timings()
+        assert t["cg_iters"] == 7 and t["cg_iters_total"] == 14
+        assert t["mg_fallbacks"] == 0 and t["mg_promotions"] == 0 and t["mg_theta_cuts"] == 0
