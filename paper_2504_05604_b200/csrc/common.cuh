@@ -40,6 +40,17 @@ __host__ __device__ inline long long elem_idx(const Geo& g, int ex, int ey, int 
 }
 
 // Device-resident scalar state of one slab (PCG + OC + scratch sums).
+// Programmatic dependent launch (sm_90+): every kernel of this library starts with
+// pdl_enter().  launch_dependents lets a kernel launched after it with the
+// programmatic-serialization attribute (LAUNCH: TOPO_PDL) be scheduled as soon
+// as every CTA of this one has started; wait blocks until the preceding grid has
+// completed and its memory is visible -- so reads of its outputs stay ordered.
+// Both are no-ops when the kernel was not launched that way.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 struct DevState {
   // PCG
   double rz;        // r^T M^{-1} r of the current residual

@@ -56,6 +56,7 @@ template <int R, int MODE, bool kSym>
 __global__ void __launch_bounds__(kF25Y * (kF25Z / kF25TZ), R == 3 ? 1 : 2)
 k_filt25(const __grid_constant__ CUtensorMap vmap, Geo g, FiltPad fp, int CX, const double* __restrict__ a,
          const double* __restrict__ hs, const uint8_t* __restrict__ passive, double* __restrict__ out) {
+  pdl_enter();
   constexpr int P = 2 * R + 1;
   using L = F25Smem<R>;
   extern __shared__ __align__(128) unsigned char dsm[];

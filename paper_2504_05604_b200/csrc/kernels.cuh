@@ -53,6 +53,7 @@ __device__ __forceinline__ double simp_pow(double x, double p) {
 
 __global__ void k_efield(Geo g, Material m, const double* __restrict__ xphys,
                          double* __restrict__ E) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
        i += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
@@ -65,6 +66,7 @@ __global__ void k_efield(Geo g, Material m, const double* __restrict__ xphys,
 // diag(K) is one scalar per node because every KE_ii = (lambda+4mu)/9.
 __global__ void k_invdiag(Geo g, Material m, const double* __restrict__ E,
                           const uint8_t* __restrict__ fixm, double* __restrict__ invd) {
+  pdl_enter();
   const long long b = g.nplane, e = (long long)(g.nown + 1) * g.nplane;
   for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
        i += (long long)gridDim.x * blockDim.x) {
@@ -129,6 +131,7 @@ k_update(Geo g, DevState* st, double* __restrict__ u, TK* __restrict__ r,
          const double* __restrict__ pprev, const double* __restrict__ p, const TK* __restrict__ q,
          const double* __restrict__ invd, const uint8_t* __restrict__ fixm, double* partials,
          unsigned int* counter, int finish) {
+  pdl_enter();
   using V2 = typename Vec2T<TK>::t;
   if (st->done) return;
   const double alpha = st->alpha, alpha_prev = kU ? st->alpha_prev : 0.0;
@@ -196,12 +199,14 @@ k_update(Geo g, DevState* st, double* __restrict__ u, TK* __restrict__ r,
 
 // dst = (double) src over a whole buffer (the fp32 Krylov residual back into r after a solve)
 __global__ void k_f2d(long long n, const float* __restrict__ src, double* __restrict__ dst) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = (double)src[i];
 }
 
 // u += alpha_prev p (the deferred half-step) when the solve stops after an even slot
 __global__ void k_flush_u(Geo g, double alpha_prev, double* __restrict__ u, const double* __restrict__ p) {
+  pdl_enter();
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
        k += (long long)gridDim.x * blockDim.x) {
@@ -209,10 +214,12 @@ __global__ void k_flush_u(Geo g, double alpha_prev, double* __restrict__ u, cons
     u[i] = fma(alpha_prev, p[i], u[i]);
   }
 }
-__global__ void k_clear_pending(DevState* st) { st->pending = 0; }
+__global__ void k_clear_pending(DevState* st) {
+  pdl_enter(); st->pending = 0; }
 
 // Multi-slab finish kernels (after the allreduce of st->sums).
 __global__ void k_finish_alpha(DevState* st) {
+  pdl_enter();
   if (st->done) return;
   const double pq = st->sums[0];
   st->pq = pq;
@@ -223,12 +230,14 @@ __global__ void k_finish_alpha(DevState* st) {
 }
 template <bool kMG = false>
 __global__ void k_finish_update(DevState* st, int even) {
+  pdl_enter();
   if (st->done) return;
   cg_finish_update<kMG>(st, st->sums[0], st->sums[1], even);
 }
 // multigrid PCG: rho = r.V(r) of the V-cycle's last sweep (allreduced) -> beta, rz
 // flex (K-cycle, reading M9): Polak-Ribiere beta = -alpha (q.z)/rz, q.z in sums[1]
 __global__ void k_finish_rho(DevState* st, int flex) {
+  pdl_enter();
   if (st->done) return;
   const double rho = st->sums[0];
   if ((!(rho > 0.0) || !isfinite(rho)) && st->solo) {
@@ -249,6 +258,7 @@ __global__ void __launch_bounds__(kBlock)
 k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __restrict__ q,
            const double* __restrict__ invd, const uint8_t* __restrict__ fixm, TK* __restrict__ r,
            int write_r, double* partials, unsigned int* counter) {
+  pdl_enter();
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   double rz = 0.0, rr = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
@@ -280,6 +290,7 @@ k_residual(Geo g, DevState* st, const double* __restrict__ f, const double* __re
 __global__ void __launch_bounds__(kBlock)
 k_dot(Geo g, DevState* st, const double* __restrict__ a, const double* __restrict__ b,
       int slot, double* partials, unsigned int* counter) {
+  pdl_enter();
   const long long b0 = g.nplane, n = (long long)g.nown * g.nplane;
   double s = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < 3 * n;
@@ -301,6 +312,7 @@ k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
        const double* __restrict__ E, const double* __restrict__ xphys,
        const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
        double* partials, unsigned int* counter) {
+  pdl_enter();
   // ce = u_e^T KE u_e = P^T B P with P = H u_e (KE = H^T B H, B block-diagonal in
   // the Walsh basis, matvec_wht.cuh): ~140 fp64 ops instead of the 576-FMA
   // dense quadratic form (SURVEY App. A "The same factorisation gives ce")
@@ -355,6 +367,7 @@ k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
          const double* __restrict__ E, const double* __restrict__ xphys,
          const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
          double* partials, unsigned int* counter) {
+  pdl_enter();
   const long long ncol = (long long)g.nely * g.nelz;
   const int nchunk = (g.nex + kSensCX - 1) / kSensCX;
   double csum = 0.0;
@@ -440,6 +453,7 @@ __global__ void __launch_bounds__(kBlock)
 k_filter(Geo g, int nst, const double* __restrict__ a, const double* __restrict__ b,
          const double* __restrict__ hs, const uint8_t* __restrict__ passive,
          double* __restrict__ out, int all_local) {
+  pdl_enter();
   // all_local: evaluate on every in-domain local element (Hs incl. halos), else owned only
   const long long b0 = all_local ? 0 : (long long)g.H * g.eplane;
   const long long e0 = all_local ? g.nelloc : (long long)(g.H + g.nex) * g.eplane;
@@ -481,6 +495,7 @@ struct FiltPad { int FY, FZ, R; long long fplane; };   // padded layout: (exl*FZ
 template <int MODE>
 __global__ void __launch_bounds__(kBlock)
 k_filt_prep(Geo g, FiltPad fp, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ vpad) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
        i += (long long)gridDim.x * blockDim.x) {
     int ex, ey, ez;
@@ -498,6 +513,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kBlock)
 k_filt_apply(Geo g, FiltPad fp, int nst, const double* __restrict__ vpad, const double* __restrict__ a,
              const double* __restrict__ hs, const uint8_t* __restrict__ passive, double* __restrict__ out) {
+  pdl_enter();
   const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
        i += (long long)gridDim.x * blockDim.x) {
@@ -573,6 +589,7 @@ __device__ __forceinline__ void oc_walk(DevState* st, const double* V) {
 __global__ void __launch_bounds__(kBlock)
 k_oc_prep(Geo g, const double* __restrict__ x, const double* __restrict__ dcf, const double* __restrict__ dvf,
           const uint8_t* __restrict__ passive, double* __restrict__ A) {
+  pdl_enter();
   const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
        i += (long long)gridDim.x * blockDim.x) {
@@ -590,6 +607,7 @@ template <int MODE0>
 __global__ void __launch_bounds__(kBlock)
 k_oc_pass(Geo g, DevState* st, double move, const double* __restrict__ x, const double* __restrict__ A,
           const double* __restrict__ dvf, double* partials, unsigned int* counter, int finish) {
+  pdl_enter();
   if (!st->oc_active) return;
   double lam[kOcCand + 1], sc[kOcCand], vol[kOcCand];
   oc_tree(st->l1, st->l2, lam);
@@ -679,6 +697,7 @@ __global__ void __launch_bounds__(kBlock)
 k_oc_freeze(long long n0, const long long* __restrict__ nptr, const double* __restrict__ x, const double* __restrict__ A,
             const double* __restrict__ dvf, DevState* st, double move, unsigned chunk,
             unsigned* __restrict__ counts, double* partials, unsigned int* counter) {
+  pdl_enter();
   const double slo = 1.0 / sqrt(st->l2), shi = 1.0 / sqrt(st->l1);
   const long long n = nptr ? *nptr : n0;   // stage 2 reads the stage-1 active count on the device
   const long long c0 = (long long)blockIdx.x * chunk, c1 = min(n, c0 + (long long)chunk);
@@ -707,6 +726,7 @@ k_oc_freeze(long long n0, const long long* __restrict__ nptr, const double* __re
 
 // exclusive scan of the per-block active counts (one thread; nb <= a few thousand)
 __global__ void k_oc_scan(const unsigned* __restrict__ counts, int nb, unsigned* __restrict__ offs, DevState* st) {
+  pdl_enter();
   if (threadIdx.x != 0) return;
   unsigned long long run = 0;
   for (int b = 0; b < nb; ++b) {
@@ -723,6 +743,7 @@ k_oc_compact(long long n0, const long long* __restrict__ nptr, const double* __r
              const double* __restrict__ dvf, const DevState* st, double move, unsigned chunk,
              const unsigned* __restrict__ offs, double* __restrict__ cx, double* __restrict__ cA,
              double* __restrict__ cdv) {
+  pdl_enter();
   const double slo = 1.0 / sqrt(st->l2), shi = 1.0 / sqrt(st->l1);
   const long long n = nptr ? *nptr : n0;   // stage 2 reads the stage-1 active count on the device
   const long long c0 = (long long)blockIdx.x * chunk, c1 = min(n, c0 + (long long)chunk);
@@ -762,6 +783,7 @@ k_oc_compact(long long n0, const long long* __restrict__ nptr, const double* __r
 __global__ void __launch_bounds__(kBlock)
 k_oc_pass_c(DevState* st, double move, const double* __restrict__ cx, const double* __restrict__ cA,
             const double* __restrict__ cdv, double* partials, unsigned int* counter, int finish) {
+  pdl_enter();
   if (!st->oc_active) return;
   double lam[kOcCand + 1], sc[kOcCand], vol[kOcCand];
   oc_tree(st->l1, st->l2, lam);
@@ -838,6 +860,7 @@ template <int MODE0>
 __global__ void __launch_bounds__(kBlock)
 k_oc_gpass(Geo g, DevState* st, int stage, double move, const double* __restrict__ x, const double* __restrict__ A,
            const double* __restrict__ dvf, double* partials, unsigned int* counter, int finish) {
+  pdl_enter();
   if (!st->oc_active) return;
   double sc[kOcCand], vol[kOcCand];
 #pragma unroll
@@ -860,11 +883,13 @@ k_oc_gpass(Geo g, DevState* st, int stage, double move, const double* __restrict
   }
 }
 __global__ void k_oc_gfinish(DevState* st, int stage) {
+  pdl_enter();
   if (!st->oc_active) return;
   oc_gwalk(st, stage, st->sums);
 }
 
 __global__ void k_oc_finish(DevState* st) {
+  pdl_enter();
   if (!st->oc_active) return;
   oc_walk(st, st->sums);
 }
@@ -874,6 +899,7 @@ __global__ void k_oc_finish(DevState* st) {
 __global__ void __launch_bounds__(kBlock)
 k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const double* __restrict__ A,
            const uint8_t* __restrict__ passive, double* __restrict__ xnew, double* partials, unsigned int* counter) {
+  pdl_enter();
   const double lmid = st->lmid;   // the last evaluated midpoint
   const int any = st->oc_pass > 0;
   const double sc = any ? 1.0 / sqrt(lmid) : 0.0;
@@ -900,6 +926,7 @@ k_oc_final(Geo g, DevState* st, double move, const double* __restrict__ x, const
 __global__ void __launch_bounds__(kBlock)
 k_design_sum(Geo g, DevState* st, const double* __restrict__ a, const uint8_t* __restrict__ passive,
              int slot, double* partials, unsigned int* counter, int want = 0) {
+  pdl_enter();
   const long long b0 = (long long)g.H * g.eplane, e0 = (long long)(g.H + g.nex) * g.eplane;
   double s = 0.0;
   for (long long i = b0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e0;
@@ -926,6 +953,7 @@ __device__ __forceinline__ long long ext_node(const Geo& g, long long k, int ixr
 }
 __global__ void k_nodes_in(Geo g, const double* __restrict__ ext, double* __restrict__ in, int ix0,
                            int nix, int ext_global) {
+  pdl_enter();
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -940,6 +968,7 @@ __global__ void k_nodes_in(Geo g, const double* __restrict__ ext, double* __rest
 }
 __global__ void k_nodes_out(Geo g, const double* __restrict__ in, double* __restrict__ ext, int ix0,
                             int nix, int ext_global) {
+  pdl_enter();
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -954,6 +983,7 @@ __global__ void k_nodes_out(Geo g, const double* __restrict__ in, double* __rest
 // per-node scalar (Jacobi inverse diagonal) -> per-DOF external array, 0 on fixed DOFs
 __global__ void k_invd_out(Geo g, const double* __restrict__ in, const uint8_t* __restrict__ fixm,
                            double* __restrict__ ext, int ix0, int nix, int ext_global) {
+  pdl_enter();
   const long long tot = (long long)nix * (g.nelz + 1) * (g.nely + 1);
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -972,6 +1002,7 @@ __device__ __forceinline__ long long ext_elem(const Geo& g, long long k, int exr
   return ext_global ? (long long)ez * g.nelx * g.nely + (long long)(g.ex0 + exr) * g.nely + ey : k;
 }
 __global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __restrict__ in, int ext_global) {
+  pdl_enter();
   const long long tot = (long long)g.nex * g.nelz * g.nely;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -982,6 +1013,7 @@ __global__ void k_elems_in(Geo g, const double* __restrict__ ext, double* __rest
   }
 }
 __global__ void k_elems_out(Geo g, const double* __restrict__ in, double* __restrict__ ext, int ext_global) {
+  pdl_enter();
   const long long tot = (long long)g.nex * g.nelz * g.nely;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -995,6 +1027,7 @@ __global__ void k_elems_out(Geo g, const double* __restrict__ in, double* __rest
 // loopback allreduce: dst[g]->sums[k] = sum_g src ... (fixed slab order)
 struct StatePtrs { DevState* s[16]; };
 __global__ void k_slab_allreduce(StatePtrs sp, int nslab, int k0, int nk, int maxmask) {
+  pdl_enter();
   // thread t owns slot k0+t: reads it on every slab, then writes it back
   const int k = k0 + threadIdx.x;
   if (threadIdx.x >= nk) return;
@@ -1014,6 +1047,7 @@ namespace topo {
 // small state / utility kernels
 // ---------------------------------------------------------------------------
 __global__ void k_cg_init(DevState* st, double tol2, double bb, long long max_it) {
+  pdl_enter();
   st->pending = 0;
   st->alpha_prev = 0.0;
   st->solo = tol2 < 0.0;   // TOPO_DIST_SOLO: a fixed iteration count, never a breakdown exit
@@ -1028,6 +1062,7 @@ __global__ void k_cg_init(DevState* st, double tol2, double bb, long long max_it
 }
 // after k_residual(write_r) + allreduce: rz, rr from sums; restart semantics
 __global__ void k_cg_start(DevState* st) {
+  pdl_enter();
   st->rz = st->sums[0];
   st->rr = st->sums[1];
   st->fresh = 1;
@@ -1035,6 +1070,7 @@ __global__ void k_cg_start(DevState* st) {
   st->done = (!st->solo && st->rr <= st->tol2 * st->bb) ? 1 : 0;
 }
 __global__ void k_oc_init(DevState* st, double lmax, double target, double tol) {
+  pdl_enter();
   st->l1 = 0.0;
   st->l2 = lmax;
   st->target = target;
@@ -1051,6 +1087,7 @@ __global__ void k_oc_init(DevState* st, double lmax, double target, double tol) 
 }
 // zero the fixed DOFs of a node vector (owned planes)
 __global__ void k_mask_fixed(Geo g, const uint8_t* __restrict__ fixm, double* __restrict__ v) {
+  pdl_enter();
   const long long b = g.nplane, e = (long long)(g.nown + 1) * g.nplane;
   for (long long i = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < e;
        i += (long long)gridDim.x * blockDim.x) {
@@ -1063,12 +1100,14 @@ __global__ void k_mask_fixed(Geo g, const uint8_t* __restrict__ fixm, double* __
 }
 // a = v * dv over the whole local element array (x0 = volfrac on design elements)
 __global__ void k_fill_design(Geo g, const double* __restrict__ dv, double v, double* __restrict__ a) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
        i += (long long)gridDim.x * blockDim.x)
     a[i] = v * dv[i];
 }
 // force passive elements to their value (0 void, 1 solid; R27) over the whole local element array
 __global__ void k_apply_passive(Geo g, const uint8_t* __restrict__ passive, double* __restrict__ a) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.nelloc;
        i += (long long)gridDim.x * blockDim.x)
     if (passive[i]) a[i] = passive[i] == kSolid ? 1.0 : 0.0;

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(32 * TZ, (TZ <= 8 ? (sizeof(TC) == 4 ? 3 : 2) 
 k_mv_wht(const __grid_constant__ MvMaps maps, Geo g, DevState* st, int gate, int CX,
          double* __restrict__ pnew, double* __restrict__ q,
          double* partials, unsigned int* counter, int finish, const double* __restrict__ scale, MvEpi epi) {
+  pdl_enter();
   if (gate && st->done) return;
   constexpr bool kFused = kPre != 0;
   constexpr bool kInvd = kPre == 1 || kPre == 3;

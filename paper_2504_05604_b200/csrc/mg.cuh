@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(kBlock)
 k_mg_restrict(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict__ qF,
               const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, TC* __restrict__ bC,
               const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = Cg.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -144,6 +145,7 @@ template <typename TF, typename TC>
 __global__ void __launch_bounds__(128)
 k_mg_restrict0(LvGeo F, LvGeo Cg, int cx_chunk, const TF* __restrict__ res, const uint8_t* __restrict__ fixC,
                TC* __restrict__ bC, const DevState* st, int x0, int xa, int xb, int j0, int jend, int accum) {
+  pdl_enter();
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned ny1 = Cg.ny + 1;
@@ -202,6 +204,7 @@ template <bool kAdd, typename TC, typename TF>
 __global__ void __launch_bounds__(kBlock)
 k_mg_prolong(LvGeo F, LvGeo Cg, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
              TF* __restrict__ xF, const DevState* st, const TF* __restrict__ xin = nullptr) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = F.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -248,6 +251,7 @@ __global__ void __launch_bounds__(128)
 k_mg_prolong0(LvGeo F, LvGeo Cg, int fx_chunk, const TR* __restrict__ r, const double* __restrict__ invd,
               const double* __restrict__ omp, const TC* __restrict__ eC, const uint8_t* __restrict__ fixF,
               TZo* __restrict__ z, const DevState* st, int x0, int pa, int pb) {
+  pdl_enter();
   MG_GATE(st);
   const unsigned col = blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned ny1 = F.ny + 1;
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(kBlock)
 k_mg_jacobi(LvGeo L, const T* __restrict__ b, const T* __restrict__ q,
             const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
             T* __restrict__ x, DevState* st, int gate, double* partials, unsigned int* counter) {
+  pdl_enter();
   if (gate && st->done) return;
   const double omega = *omp;
   const long long tot = L.nodes();
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(kBlock)
 k_mg_restrict_w(LvGeo F, LvGeo Cg, const TF* __restrict__ bF, const TF* __restrict__ qF,
                 const uint8_t* __restrict__ fixF, const uint8_t* __restrict__ fixC, TC* __restrict__ bC,
                 const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = Cg.nodes();
   const int lane = threadIdx.x & 31;
@@ -416,6 +422,7 @@ __global__ void __launch_bounds__(kBlock)
 k_kc_dot1(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
           T* __restrict__ kx, T* __restrict__ kv, double* __restrict__ kc, const DevState* gst,
           double* partials, unsigned int* counter, DevState* slab_out = nullptr) {
+  pdl_enter();
   MG_GATE(gst);
   double xt = 0.0, xb = 0.0;
   const long long n = 3 * (L.v_hi() - L.v_lo());
@@ -440,6 +447,7 @@ k_kc_dot1(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __
   }
 }
 __global__ void k_kc_finish1(const DevState* st, double* __restrict__ kc, const DevState* gst) {
+  pdl_enter();
   MG_GATE(gst);
   kc[0] = st->sums[0];
   kc[1] = st->sums[1];
@@ -447,6 +455,7 @@ __global__ void k_kc_finish1(const DevState* st, double* __restrict__ kc, const 
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_kc_r2(LvGeo L, T* __restrict__ b, const T* __restrict__ kv, const double* __restrict__ kc, const DevState* gst) {
+  pdl_enter();
   MG_GATE(gst);
   const double s = kc[0] > 0.0 ? kc[1] / kc[0] : 0.0;
   const long long n = 3 * (L.v_hi() - L.v_lo());
@@ -472,6 +481,7 @@ __global__ void __launch_bounds__(kBlock)
 k_kc_dot2(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __restrict__ b,
           const T* __restrict__ kv, double* __restrict__ kc, const DevState* gst, double* partials,
           unsigned int* counter, DevState* slab_out = nullptr) {
+  pdl_enter();
   MG_GATE(gst);
   double g = 0.0, bb = 0.0, a2 = 0.0;
   const long long n = 3 * (L.v_hi() - L.v_lo());
@@ -495,6 +505,7 @@ k_kc_dot2(LvGeo L, const T* __restrict__ x, const T* __restrict__ t, const T* __
   }
 }
 __global__ void k_kc_finish2(const DevState* st, double* __restrict__ kc, const DevState* gst) {
+  pdl_enter();
   MG_GATE(gst);
   kc_coeffs(kc, st->sums[0], st->sums[1], st->sums[2]);
 }
@@ -502,6 +513,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_kc_combine(LvGeo L, T* __restrict__ x, const T* __restrict__ kx, const double* __restrict__ kc,
              const DevState* gst) {
+  pdl_enter();
   MG_GATE(gst);
   const double c1 = kc[2], c2 = kc[3];
   const long long n = 3 * (L.v_hi() - L.v_lo());
@@ -532,6 +544,7 @@ __device__ __forceinline__ double mg_hash_unit(unsigned long long k) {
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_start_vec(LvGeo L, int x0, int xa, int xb, int nxg, const uint8_t* __restrict__ fix, T* __restrict__ v) {
+  pdl_enter();
   const long long tot = (long long)(xb - xa + 1) * (L.ny + 1) * (L.nz + 1);
   const LvGeo D{xb - xa, L.ny, L.nz, L.NY, L.nplane, L.ncomp};   // decode range only
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -554,6 +567,7 @@ __global__ void __launch_bounds__(kBlock)
 k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T* __restrict__ invd,
               const uint8_t* __restrict__ fix, double theta, double* __restrict__ om_out,
               double* partials, unsigned int* counter, DevState* st = nullptr) {
+  pdl_enter();
   const long long tot = L.nodes();
   double vt = 0.0, vdv = 0.0;
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -588,6 +602,7 @@ k_mg_rayleigh(LvGeo L, const T* __restrict__ v, const T* __restrict__ t, const T
 }
 
 __global__ void k_mg_rayleigh_finish(const DevState* st, double theta, double* __restrict__ om_out) {
+  pdl_enter();
   om_out[0] = theta * st->sums[1] / st->sums[0];
   om_out[kMgScaleOff] = st->sums[1] > 0.0 ? 1.0 / sqrt(st->sums[1]) : 1.0;
 }
@@ -596,6 +611,7 @@ __global__ void k_mg_rayleigh_finish(const DevState* st, double theta, double* _
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_scale_copy(const T* __restrict__ src, T* __restrict__ dst, long long n, const double* __restrict__ sp) {
+  pdl_enter();
   const double sc = *sp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     dst[i] = (T)(sc * (double)src[i]);
@@ -609,6 +625,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const T* __restrict__ x,
                const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -650,6 +667,7 @@ k_mg_apply_asm(LvGeo L, const double* __restrict__ K, const T* __restrict__ x,
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_diag_asm(LvGeo L, const double* __restrict__ K, const uint8_t* __restrict__ fix, T* __restrict__ invd) {
+  pdl_enter();
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -679,6 +697,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_diag_l1(Geo g, LvGeo L, const double* __restrict__ E, const uint8_t* __restrict__ fix,
              T* __restrict__ invd) {
+  pdl_enter();
   const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -717,6 +736,7 @@ template <int S>
 __global__ void __launch_bounds__(kBlock)
 k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __restrict__ tab,
               double* __restrict__ K) {
+  pdl_enter();
   constexpr int NT = S * S * S, kCh = 32;
   __shared__ double tb[NT][kCh];
   const long long nel = L.nel();
@@ -759,6 +779,7 @@ k_mg_asm_fine(Geo g, LvGeo L, const double* __restrict__ E, const double* __rest
 // as in k_mg_asm_fine<4>; children outside the fine grid give 0.
 __global__ void __launch_bounds__(kBlock)
 k_mg_gather64(Geo g, LvGeo L, const double* __restrict__ E, double* __restrict__ Eg) {
+  pdl_enter();
   const long long nel = L.nel(), tot = 64 * nel;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     const int f = (int)(t / nel);
@@ -782,6 +803,7 @@ k_mg_gather64(Geo g, LvGeo L, const double* __restrict__ E, double* __restrict__
 constexpr int kGalTile = 8;
 __global__ void __launch_bounds__(kGalTile * 24, 2)
 k_mg_asm_galerkin_t(LvGeo F, const double* __restrict__ KF, LvGeo Cg, double* __restrict__ KC) {
+  pdl_enter();
   extern __shared__ double sK[];                 // [576][2 * kGalTile]
   constexpr int NF = 2 * kGalTile;
   const int el = threadIdx.x, sc = threadIdx.y;  // coarse element in the tile, output column
@@ -880,6 +902,7 @@ template <typename T, typename TE = double>
 __global__ void __launch_bounds__(kL1Block, 3)
 k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
              T* __restrict__ Y, const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const long long nel = L.nel(), ehi = L.el_hi();   // (x-slabs: the element planes next to the node range)
   for (long long e = L.el_lo() + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ehi;
@@ -954,6 +977,7 @@ k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
 // reads half the bytes; (float)E is what it used anyway, so results are unchanged)
 __global__ void __launch_bounds__(kBlock)
 k_mg_e32(long long n, const double* __restrict__ E, float* __restrict__ E32) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     E32[i] = (float)E[i];
 }
@@ -968,6 +992,7 @@ __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather_jac(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ x,
                    const T* __restrict__ b, const T* __restrict__ invd, const double* __restrict__ omp,
                    const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const double omega = *omp;
   const long long tot = L.nodes(), nel = L.nel();
@@ -1001,6 +1026,7 @@ template <bool kScale, typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ q,
                const DevState* st, const T* __restrict__ invd) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -1044,6 +1070,7 @@ k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix
 template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
+  pdl_enter();
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -1082,6 +1109,7 @@ template <typename T, int kU = 13>
 __global__ void __launch_bounds__(kBlock)
 k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
               const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
@@ -1142,6 +1170,7 @@ __global__ void __launch_bounds__(256, 4)
 k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, const T* __restrict__ b,
                const T* __restrict__ invd, const uint8_t* __restrict__ fix, const double* __restrict__ omp,
                T* __restrict__ dst, const DevState* st, T* __restrict__ xout = nullptr) {
+  pdl_enter();
   MG_GATE(st);
   __shared__ double part[8][3][32];
   const long long tot = L.nodes();
@@ -1227,6 +1256,7 @@ k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, cons
 __global__ void __launch_bounds__(kBlock)
 k_mg_dense_fill(LvGeo L, const double* __restrict__ K, const int* __restrict__ dmap, int ld,
                 double* __restrict__ A) {
+  pdl_enter();
   const long long tot = L.nodes(), nel = L.nel();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
@@ -1284,6 +1314,7 @@ __device__ __forceinline__ double sym_lo(const double* S, int ld, int i, int j) 
 // through shared memory (two barriers per pivot)
 __global__ void __launch_bounds__(kGjB * kGjB / kGjInvNJ)
 k_sw_block_inv(const double* __restrict__ S, int ld, int k0, double* __restrict__ P) {
+  pdl_enter();
   constexpr int NJ = kGjInvNJ, JS = kGjB / NJ;
   __shared__ double col[kGjB], row[kGjB];
   const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;
@@ -1318,6 +1349,7 @@ k_sw_block_inv(const double* __restrict__ S, int ld, int k0, double* __restrict_
 // C = S_:,K (rows K zero), read from the lower triangle (n_pad x b, column-major)
 __global__ void __launch_bounds__(kBlock)
 k_sw_take_col(const double* __restrict__ S, int ld, int k0, double* __restrict__ C) {
+  pdl_enter();
   const long long tot = (long long)ld * kGjB;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t % ld), j = (int)(t / ld);
@@ -1328,6 +1360,7 @@ k_sw_take_col(const double* __restrict__ S, int ld, int k0, double* __restrict__
 // S_iK = (C P)_i for i not in K, S_KK = -P (lower triangle)
 __global__ void __launch_bounds__(kBlock)
 k_sw_put_panel(double* __restrict__ S, int ld, int k0, const double* __restrict__ CP, const double* __restrict__ P) {
+  pdl_enter();
   const long long tot = (long long)ld * kGjB;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t % ld), jj = (int)(t / ld), k = k0 + jj;
@@ -1344,6 +1377,7 @@ k_sw_put_panel(double* __restrict__ S, int ld, int k0, const double* __restrict_
 // A^-1 = -S, full symmetric (the coarse solve reads whole rows)
 __global__ void __launch_bounds__(kBlock)
 k_sw_finish(double* __restrict__ S, int ld) {
+  pdl_enter();
   const long long tot = (long long)ld * ld;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(t % ld), j = (int)(t / ld);
@@ -1358,6 +1392,7 @@ k_sw_finish(double* __restrict__ S, int ld) {
 }
 
 __global__ void k_gj_pad(double* __restrict__ A, int n, int ld) {
+  pdl_enter();
   for (int t = threadIdx.x + blockIdx.x * blockDim.x; t < ld - n; t += gridDim.x * blockDim.x)
     A[(long long)(n + t) * ld + n + t] = 1.0;
 }
@@ -1367,6 +1402,7 @@ __global__ void k_gj_pad(double* __restrict__ A, int n, int ld) {
 // After steps k = 0..n-1 the buffer holds A^-1.
 __global__ void __launch_bounds__(kBlock)
 k_mg_gj_step(const double* __restrict__ a, double* __restrict__ o, int n, int k) {
+  pdl_enter();
   const long long tot = (long long)n * n;
   const double p = a[(long long)k * n + k], ip = 1.0 / p;
   for (long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x; id < tot;
@@ -1386,6 +1422,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBlock)
 k_mg_coarse_solve(const double* __restrict__ Ainv, int n, int ld, const long long* __restrict__ imap,
                   const T* __restrict__ b, T* __restrict__ x, const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
@@ -1402,12 +1439,14 @@ k_mg_coarse_solve(const double* __restrict__ Ainv, int n, int ld, const long lon
 // config 4, L2-resident across the K-cycle's repeated coarsest solves); b is
 // gathered once per block into shared memory; fp64 accumulation.
 __global__ void k_mg_inv_to32(const double* __restrict__ A, float* __restrict__ A32, long long n) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     A32[i] = (float)A[i];
 }
 __global__ void __launch_bounds__(kBlock)
 k_mg_coarse_solve32(const float* __restrict__ Ainv, int n, int ld, const long long* __restrict__ imap,
                     const float* __restrict__ b, float* __restrict__ x, const DevState* st) {
+  pdl_enter();
   MG_GATE(st);
   extern __shared__ float bsh[];
   for (int j = threadIdx.x; j < n; j += blockDim.x) bsh[j] = b[imap[j]];
@@ -1445,6 +1484,7 @@ constexpr int kNtTile = 64;
 __global__ void __launch_bounds__(256)
 k_dgemm_nt64(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
              double* __restrict__ Cm, long long ldc, int M, int N, double alpha, double beta, int lower) {
+  pdl_enter();
   const int bi = blockIdx.y, bj = blockIdx.x;
   if (lower && bj > bi) return;
   __shared__ double As[32][kNtTile + 1], Bs[32][kNtTile + 1];
@@ -1499,6 +1539,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 __global__ void __launch_bounds__(256)
 k_dgemm_nt64_tc(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
                 double* __restrict__ Cm, long long ldc, int M, int N, double alpha) {
+  pdl_enter();
   extern __shared__ double tsm[];
   double* As = tsm;                       // [t][i], pitch kTcPadA
   double* Bs = tsm + kTcK * kTcPadA;      // [t][j], pitch kTcPadB

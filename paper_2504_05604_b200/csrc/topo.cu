@@ -13,6 +13,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <tuple>
+#include <utility>
 
 #include "../../include/topo.h"
 #include "common.cuh"
@@ -313,9 +315,48 @@ void debug_sync(topo_ctx* ctx, const char* name) {
   if (e != cudaSuccess) ctx->sticky = set_err(ctx, TOPO_ECUDA, "kernel %s: %s", name, cudaGetErrorString(e));
 }
 
+// Kernel launch on the bound stream.  With TOPO_PDL (default on) the launch
+// carries the programmatic-stream-serialization attribute: the kernel may be
+// scheduled while the previous one drains and waits for it in pdl_enter()
+// (common.cuh) -- the launch latency of the chains of small multigrid kernels
+// overlaps the previous kernel instead of following it.
+inline bool pdl_on() {
+  static const bool on = !getenv("TOPO_PDL") || atoi(getenv("TOPO_PDL")) != 0;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_k(cudaStream_t stream, void (*kern)(KArgs...), int grid, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  // the kernel's parameter types; trailing defaulted parameters (all 0 / nullptr) value-initialised
+  using Tup = std::tuple<std::decay_t<KArgs>...>;
+  static_assert(sizeof...(Args) <= sizeof...(KArgs), "kernel argument count");
+  auto in = std::forward_as_tuple(std::forward<Args>(args)...);
+  Tup conv = [&]<size_t... I>(std::index_sequence<I...>) {
+    auto pick = [&]<size_t J>(std::integral_constant<size_t, J>) -> std::tuple_element_t<J, Tup> {
+      if constexpr (J < sizeof...(Args)) return std::get<J>(in);
+      else return std::tuple_element_t<J, Tup>{};
+    };
+    return Tup{pick(std::integral_constant<size_t, I>{})...};
+  }(std::index_sequence_for<KArgs...>{});
+  std::apply(
+      [&](auto&... a) {
+        void* ptrs[] = {static_cast<void*>(&a)...};
+        cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(kern), ptrs);
+      },
+      conv);
+}
 #define LAUNCH(ctx, kern, grid, ...)                                      \
   do {                                                                    \
-    kern<<<(grid), kBlock, 0, (ctx)->stream>>>(__VA_ARGS__);              \
+    launch_k((ctx)->stream, kern, (grid), __VA_ARGS__);                   \
     (ctx)->launches++;                                                    \
     debug_sync((ctx), #kern);                                             \
   } while (0)
