@@ -898,8 +898,11 @@ template <typename T> __device__ __forceinline__ const WhtKT<T>& wht1_const();
 template <> __device__ __forceinline__ const WhtKT<double>& wht1_const<double>() { return c_wht1; }
 template <> __device__ __forceinline__ const WhtKT<float>& wht1_const<float>() { return c_wht1f; }
 
+#ifndef TOPO_L1_MINB
+#define TOPO_L1_MINB 4   // fp32: 4 CTAs / SM at 128 registers, no spills (measured 0.08 ms less per MG-PCG iteration than 3)
+#endif
 template <typename T, typename TE = double>
-__global__ void __launch_bounds__(kL1Block, 3)
+__global__ void __launch_bounds__(kL1Block, (sizeof(T) == 4 ? TOPO_L1_MINB : 3))
 k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
              T* __restrict__ Y, const DevState* st) {
   pdl_enter();
