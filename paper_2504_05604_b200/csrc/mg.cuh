@@ -901,6 +901,61 @@ template <> __device__ __forceinline__ const WhtKT<float>& wht1_const<float>() {
 #ifndef TOPO_L1_MINB
 #define TOPO_L1_MINB 4   // fp32: 4 CTAs / SM at 128 registers, no spills (measured 0.08 ms less per MG-PCG iteration than 3)
 #endif
+// Level-1 element operator: W[c][k] = the corner values (natural corner index
+// k = ax + 2 ay + 4 az, overwritten), Ech the 8 child moduli -> Yh[c][k] = the
+// element's outputs at its corners (K1_e applied matrix-free, see above).
+template <typename T>
+__device__ __forceinline__ void l1_elem_core(T W[3][8], const T Ech[8], T Yh[3][8]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) Yh[c][k] = T(0);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) fwht8(W[c]);
+  // T_c = Lambda^-1 T''_c with T''_c = [[1, s/2], [0, 1]] per axis, so
+  // T_c^T B T_c = T''_c^T (Lambda^-1 B Lambda^-1) T''_c: one FMA per pair each way
+  // and the rescaled block constants c_wht1.
+  // fp32: children fully unrolled (static E index, no select chain); fp64 keeps
+  // the loop rolled for register pressure.  A child outside the fine domain has
+  // E = 0 and contributes exactly 0.
+#pragma unroll (sizeof(T) == 4 ? 8 : 1)
+  for (int ch = 0; ch < 8; ++ch) {
+    T Ec = Ech[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (folds when unrolled)
+    T P[3][8], Q[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) P[c][m] = W[c][m];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          if (!((m >> d) & 1)) P[c][m] = fma(hs, P[c][m | (1 << d)], P[c][m]);
+    }
+    wht_block_k<T>(wht1_const<T>(), P, Ec, Q);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          if (!((m >> d) & 1)) Q[c][m | (1 << d)] = fma(hs, Q[c][m], Q[c][m | (1 << d)]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) Yh[c][m] += Q[c][m];
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) fwht8(Yh[c]);
+}
+
 template <typename T, typename TE = double>
 __global__ void __launch_bounds__(kL1Block, (sizeof(T) == 4 ? TOPO_L1_MINB : 3))
 k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
@@ -920,59 +975,127 @@ k_mg_l1_elem(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x,
     for (int k = 0; k < 8; ++k) {
       const long long n = L.n(ex + (k & 1), ey + ((k >> 1) & 1), ez + (k >> 2));
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        W[c][k] = x[n + c * L.ncomp];
-        Yh[c][k] = T(0);
-      }
+      for (int c = 0; c < 3; ++c) W[c][k] = x[n + c * L.ncomp];
     }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) fwht8(W[c]);
-    // T_c = Lambda^-1 T''_c with T''_c = [[1, s/2], [0, 1]] per axis, so
-    // T_c^T B T_c = T''_c^T (Lambda^-1 B Lambda^-1) T''_c: one FMA per pair each way
-    // and the rescaled block constants c_wht1.
-    // fp32: children fully unrolled (static E index, no select chain); fp64 keeps
-    // the loop rolled for register pressure.  A child outside the fine domain has
-    // E = 0 and contributes exactly 0.
-#pragma unroll (sizeof(T) == 4 ? 8 : 1)
-    for (int ch = 0; ch < 8; ++ch) {
-      T Ec = Ech[0];
-#pragma unroll
-      for (int k = 1; k < 8; ++k) Ec = ch == k ? Ech[k] : Ec;   // register select (folds when unrolled)
-      T P[3][8], Q[3][8];
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int m = 0; m < 8; ++m) P[c][m] = W[c][m];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int m = 0; m < 8; ++m)
-            if (!((m >> d) & 1)) P[c][m] = fma(hs, P[c][m | (1 << d)], P[c][m]);
-      }
-      wht_block_k<T>(wht1_const<T>(), P, Ec, Q);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const T hs = ((ch >> d) & 1) ? T(-0.5) : T(0.5);
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int m = 0; m < 8; ++m)
-            if (!((m >> d) & 1)) Q[c][m | (1 << d)] = fma(hs, Q[c][m], Q[c][m | (1 << d)]);
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int m = 0; m < 8; ++m) Yh[c][m] += Q[c][m];
-    }
+    l1_elem_core<T>(W, Ech, Yh);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      fwht8(Yh[c]);
 #pragma unroll
       for (int k = 0; k < 8; ++k) Y[(long long)(3 * k + c) * nel + e] = Yh[c][k];
     }
+  }
+}
+
+
+// Face-accumulating variant (TOPO_L1_FACE, default): a thread owns one (ey, ez)
+// element column and walks kL1CX node planes of it along x; node plane x's
+// 4 corners x 3 components are loaded once and shared by elements x - 1 and x,
+// and the thread writes the x-complete FACE sums
+//   F[x][j][c][col] = (element x-1's ax = 1 corner j) + (element x's ax = 0 corner j),
+// j = ay + 2 az, col = ez ny + ey -- 12 values per node plane and column instead
+// of 24 per element (half the bytes of the Y round trip), and the gather sums 4
+// faces instead of 8 element corners.  The element before a chunk is recomputed
+// (1 in kL1CX).  x-slab ranges: node planes [xa, xlast] only.
+constexpr int kL1CX = 16;
+#ifndef TOPO_L1F_MINB
+#define TOPO_L1F_MINB 3
+#endif
+template <typename T, typename TE = double>
+__global__ void __launch_bounds__(kL1Block, (sizeof(T) == 4 ? TOPO_L1F_MINB : 3))
+k_mg_l1_face(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x, T* __restrict__ F,
+             const DevState* st) {
+  pdl_enter();
+  MG_GATE(st);
+  const int nx = L.nx, ny = L.ny;
+  const long long ncol = (long long)L.ny * L.nz;
+  const int plo = L.xa, phi = L.xlast() + 1;              // node planes [plo, phi)
+  const int nchunk = (phi - plo + kL1CX - 1) / kL1CX;
+  __shared__ T sA[12][kL1Block], sacc[12][kL1Block];
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < ncol * nchunk;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int chunk = (int)(t / ncol);
+    const long long col = t - (long long)chunk * ncol;
+    const int ez = (int)(col / ny), ey = (int)(col - (long long)ez * ny);
+    const int p0 = plo + chunk * kL1CX, p1 = min(p0 + kL1CX, phi);
+    // running pointers (advanced one plane per step) and 32-bit in-plane offsets
+    const int NY = L.NY;
+    const T* xp = x + L.n(p0 - 1, ey, ez);                   // node plane ex (corner j = 0)
+    const int onp = (int)L.nplane;
+    const long long ebase = elem_idx(g, 2 * (p0 - 1), 2 * ey, 2 * ez);
+    const int eplane2 = (int)(2 * g.eplane), EY = g.EY;
+    T* fp = F + (long long)(p0 - 1) * 12 * ncol + col;
+    const long long fstep = 12 * ncol;
+    // per-thread carries in shared memory (slot [c*4+j][thread]): the previous node
+    // plane's corners and the running face sum -- kept out of the registers of the
+    // element arithmetic
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sacc[c * 4 + j][threadIdx.x] = T(0);
+        sA[c * 4 + j][threadIdx.x] = p0 - 1 >= 0 ? xp[(j >> 1) * NY + (j & 1) + c * L.ncomp] : T(0);
+      }
+    const TE* ep = E + ebase;
+    for (int ex = p0 - 1; ex < p1; ++ex, xp += onp, ep += eplane2, fp += fstep) {
+      T Yh[3][8];
+      if (ex >= 0 && ex < nx) {
+        T W[3][8], Ech[8];
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) Ech[ch] = (T)ep[(ch & 1) * (eplane2 / 2) + (ch >> 2) * EY + ((ch >> 1) & 1)];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const T bn = xp[onp + (j >> 1) * NY + (j & 1) + c * L.ncomp];
+            W[c][2 * j] = sA[c * 4 + j][threadIdx.x];
+            W[c][2 * j + 1] = bn;
+            sA[c * 4 + j][threadIdx.x] = bn;
+          }
+        l1_elem_core<T>(W, Ech, Yh);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) Yh[c][k] = T(0);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (ex >= p0) fp[(j * 3 + c) * ncol] = sacc[c * 4 + j][threadIdx.x] + Yh[c][2 * j];
+          sacc[c * 4 + j][threadIdx.x] = Yh[c][2 * j + 1];
+        }
+    }
+  }
+}
+
+// sum of the level-1 element outputs at node (ix, iy, iz): kFace -> the 4 face sums
+// of k_mg_l1_face, else the 8 element corners of k_mg_l1_elem (fixed order)
+template <bool kFace, typename T>
+__device__ __forceinline__ void l1_node_sum(const LvGeo& L, const T* __restrict__ Y, int ix, int iy, int iz, T a[3]) {
+  a[0] = a[1] = a[2] = T(0);
+  if (kFace) {
+    const long long ncol = (long long)L.ny * L.nz;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ey = iy - (j & 1), ez = iz - (j >> 1);
+      if (ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+      const long long col = (long long)ez * L.ny + ey;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) a[c] += Y[((long long)(ix * 4 + j) * 3 + c) * ncol + col];
+    }
+    return;
+  }
+  const long long nel = L.nel();
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
+    const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+    if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+    const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+    const int kc = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a[c] += Y[(long long)(3 * kc + c) * nel + e];
   }
 }
 
@@ -990,7 +1113,7 @@ k_mg_e32(long long n, const double* __restrict__ E, float* __restrict__ E32) {
 // level-1 damped-Jacobi sweep fused into the gather: x += w D^-1 (b - mask(A x)),
 // the same arithmetic as k_mg_l1_gather<false> followed by k_mg_jacobi<1>
 // (the sum is rounded to T as it would be stored), without the t round trip
-template <typename T>
+template <typename T, bool kFace = true>
 __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather_jac(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ x,
                    const T* __restrict__ b, const T* __restrict__ invd, const double* __restrict__ omp,
@@ -1003,17 +1126,8 @@ k_mg_l1_gather_jac(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__
        k += (long long)gridDim.x * blockDim.x) {
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
-    T a[3] = {T(0), T(0), T(0)};
-#pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
-      const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
-      if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
-      const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
-      const int kc = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) a[c] += Y[(long long)(3 * kc + c) * nel + e];
-    }
+    T a[3];
+    l1_node_sum<kFace, T>(L, Y, ix, iy, iz, a);
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
 #pragma unroll
@@ -1025,29 +1139,20 @@ k_mg_l1_gather_jac(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__
   }
 }
 
-template <bool kScale, typename T>
+template <bool kScale, typename T, bool kFace = true>
 __global__ void __launch_bounds__(kBlock)
 k_mg_l1_gather(LvGeo L, const T* __restrict__ Y, const uint8_t* __restrict__ fix, T* __restrict__ q,
                const DevState* st, const T* __restrict__ invd) {
   pdl_enter();
   MG_GATE(st);
-  const long long tot = L.nodes(), nel = L.nel();
+  const long long tot = L.nodes();
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < tot;
        k += (long long)gridDim.x * blockDim.x) {
     int ix, iy, iz;
     lv_decode(L, k, ix, iy, iz);
-    T a0 = T(0), a1 = T(0), a2 = T(0);
-#pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const int dx = d & 1, dy = (d >> 1) & 1, dz = d >> 2;
-      const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
-      if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
-      const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
-      const int kc = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
-      a0 += Y[(long long)(3 * kc) * nel + e];
-      a1 += Y[(long long)(3 * kc + 1) * nel + e];
-      a2 += Y[(long long)(3 * kc + 2) * nel + e];
-    }
+    T a[3];
+    l1_node_sum<kFace, T>(L, Y, ix, iy, iz, a);
+    T a0 = a[0], a1 = a[1], a2 = a[2];
     const long long i = L.n(ix, iy, iz);
     const uint8_t fm = fix[i];
     if (kScale) {   // invd is 0 on fixed DOFs

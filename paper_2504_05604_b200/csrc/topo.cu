@@ -253,6 +253,7 @@ struct topo_ctx {
   bool k32_on = false;               // fp32 Krylov r, q allocated (topo_params.krylov_fp32, one slab)
   bool k32_pass = false;             // ... in use by the running MG-PCG pass
   int mg_kmin = 1, mg_kmax = 99;     // K-cycle levels [kmin, kmax] (TOPO_KMIN / TOPO_KMAX: experiments)
+  bool l1_face = true;               // level-1 operator: face-accumulating k_mg_l1_face (TOPO_L1_FACE=0: k_mg_l1_elem)
   double* mg_kc = nullptr;           // K-cycle scalars, 8 per level
   int mg_dl = 0;                     // x-slabs: levels 1 .. mg_dl distributed over the slabs (0: replicated)
 };
@@ -1293,6 +1294,7 @@ int mg_build(topo_ctx* ctx, const uint8_t* fixed) {
   // same PCG iteration counts, 0.8 ms less per iteration)
   ctx->mg_kmax = L >= 6 ? L - 3 : L - 2;
   if (const char* e = getenv("TOPO_KMIN")) ctx->mg_kmin = atoi(e);
+  if (const char* e = getenv("TOPO_L1_FACE")) ctx->l1_face = atoi(e) != 0;
   if (const char* e = getenv("TOPO_KMAX")) ctx->mg_kmax = atoi(e);
   ctx->mg_theta = P.mg_omega;
   ctx->mg.resize(L);
@@ -1670,6 +1672,17 @@ int gather_level(topo_ctx* ctx, int l, void* buf, size_t es) {
 // level-1 phase 1 (Walsh-domain Galerkin per coarse element), 128-thread CTAs
 // (x-slabs: Lr = the slab's owned node planes -- the element planes next to
 // them are computed -- and the slab's x and Y)
+// level-1 gather phase matching the element phase's output layout (ctx->l1_face)
+#define L1_GATHER(ctx, kScale, T, grid, ...)                                        \
+  do {                                                                              \
+    if ((ctx)->l1_face) LAUNCH(ctx, (k_mg_l1_gather<kScale, T, true>), grid, __VA_ARGS__);  \
+    else LAUNCH(ctx, (k_mg_l1_gather<kScale, T, false>), grid, __VA_ARGS__);               \
+  } while (0)
+#define L1_GATHER_JAC(ctx, T, grid, ...)                                            \
+  do {                                                                              \
+    if ((ctx)->l1_face) LAUNCH(ctx, (k_mg_l1_gather_jac<T, true>), grid, __VA_ARGS__);       \
+    else LAUNCH(ctx, (k_mg_l1_gather_jac<T, false>), grid, __VA_ARGS__);                    \
+  } while (0)
 template <typename T>
 int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst, const LvGeo* Lr = nullptr, void* xv = nullptr,
                    void* Yv = nullptr) {
@@ -1677,7 +1690,14 @@ int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst, const LvGeo* 
   T* x = mgp<T>(xv ? xv : m.x);
   T* Y = mgp<T>(Yv ? Yv : m.Y);
   const long long nb = std::min<long long>((L.el_hi() - L.el_lo() + kL1Block - 1) / kL1Block, 148LL * 3 * 16);
-  if (sizeof(T) == 4)   // fp32 moduli (k_mg_e32 at setup)
+  if (ctx->l1_face) {   // face sums (k_mg_l1_face): one thread per (column, chunk of kL1CX node planes)
+    const long long nt = (long long)L.ny * L.nz * ((L.xlast() - L.xa + 1 + kL1CX - 1) / kL1CX);
+    const unsigned nbf = (unsigned)std::max(1LL, std::min<long long>((nt + kL1Block - 1) / kL1Block, 148LL * 3 * 16));
+    if (sizeof(T) == 4)
+      k_mg_l1_face<T, float><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y, gst);
+    else
+      k_mg_l1_face<T, double><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, mgE(ctx), x, Y, gst);
+  } else if (sizeof(T) == 4)   // fp32 moduli (k_mg_e32 at setup)
     k_mg_l1_elem<T, float><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y,
                                                                                    gst);
   else
@@ -1793,7 +1813,7 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       for (int k = 0; k < nsteps; ++k) {
         if (!m.stored) {   // level 1: x <- D^-1 (A x) in the gather phase
           CK(launch_l1_elem<T>(ctx, m, nullptr));
-          LAUNCH(ctx, (k_mg_l1_gather<true, T>), gL, m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.x), nullptr, mgp<T>(m.invd));
+          L1_GATHER(ctx, true, T, gL, m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.x), nullptr, mgp<T>(m.invd));
           continue;
         }
         CK(mg_apply<T>(ctx, l, 0));
@@ -1937,8 +1957,7 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   }
   // level 1: P^T K(E) P matrix-free in the Walsh domain (two deterministic phases)
   CK(launch_l1_elem<T>(ctx, m, gst));
-  LAUNCH(ctx, (k_mg_l1_gather<false, T>), grid_for(m.L.nodes()), m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.t), gst,
-         (const T*)nullptr);
+  L1_GATHER(ctx, false, T, grid_for(m.L.nodes()), m.L, mgp<T>(m.Y), m.fixm, mgp<T>(m.t), gst, (const T*)nullptr);
   return check_launch(ctx);
 }
 
@@ -2158,7 +2177,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   for (int k = 1; k <= nu; ++k) {
     if (!m.stored) {   // level 1: the sweep fused into the gather phase
       CK(launch_l1_elem<T>(ctx, m, gst));
-      LAUNCH(ctx, k_mg_l1_gather_jac<T>, gL, m.L, mgp<T>(m.Y), m.fixm, mx, mb, mi, om, gst);
+      L1_GATHER_JAC(ctx, T, gL, m.L, mgp<T>(m.Y), m.fixm, mx, mb, mi, om, gst);
       continue;
     }
     CK(mg_apply<T>(ctx, l, gate));
@@ -2217,8 +2236,7 @@ int dl_apply(topo_ctx* ctx, int l, int gate) {
     const DevState* gst = gate ? sl.st : nullptr;
     if (!m.stored) {   // level 1: P^T K(E) P matrix-free, element planes next to the owned nodes
       CK(launch_l1_elem<T>(ctx, m, gst, &Ls, d.x, d.Y));
-      LAUNCH(ctx, (k_mg_l1_gather<false, T>), grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.t), gst,
-             (const T*)nullptr);
+      L1_GATHER(ctx, false, T, grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.t), gst, (const T*)nullptr);
     } else if (dl_deep(ctx, l)) {
       LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((Ls.nodes() + 31) / 32, 148LL * 8 * 16), Ls,
              mgp<T>(m.S), mgp<T>(d.x), mgp<T>(d.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(d.t), gst);
@@ -2313,8 +2331,8 @@ int dist_vcycle(topo_ctx* ctx, int l, int gate) {
       const LvGeo Ls = dl_geo(ctx, sl, l);
       const DevState* gst = gate ? sl.st : nullptr;
       CK(launch_l1_elem<T>(ctx, m, gst, &Ls, d.x, d.Y));
-      LAUNCH(ctx, k_mg_l1_gather_jac<T>, grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.x), mgp<T>(d.b),
-             mgp<T>(m.invd), om, gst);
+      L1_GATHER_JAC(ctx, T, grid_for(Ls.nodes()), Ls, mgp<T>(d.Y), m.fixm, mgp<T>(d.x), mgp<T>(d.b), mgp<T>(m.invd),
+                    om, gst);
     }
     return check_launch(ctx);
   }
