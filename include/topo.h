@@ -125,8 +125,10 @@ typedef struct {
    * TOPO_PRECOND_MG: one V-cycle of geometric multigrid on the nested Hex8 grids
    *   (trilinear transfer, Galerkin coarse operators, damped-Jacobi smoothing,
    *   exact coarsest solve).  On x-slabs (world > 1) the fine level is
-   *   slab-local and levels >= 1 are replicated on every rank (mg_nu == 1
-   *   only).  EINVAL at init if the hierarchy cannot be built (fewer than 2
+   *   slab-local, the coarse levels with > 150 k nodes are distributed over
+   *   the slabs by coarsened plane ranges (ghost-plane exchanges, allreduced
+   *   K-cycle dots) and the smaller ones are replicated on every rank (mg_nu
+   *   == 1 only, reading M10).  EINVAL at init if the hierarchy cannot be built (fewer than 2
    *   levels, coarse Dirichlet DOFs that do not cover the fine ones: property Q
    *   of reading M4; or x-slabs with mg_nu > 1).
    * TOPO_PRECOND_AUTO (default): MG where it can be built, else Jacobi.         */
