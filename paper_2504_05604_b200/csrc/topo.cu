@@ -2459,7 +2459,11 @@ int mg_upload(topo_ctx* ctx, int l, const double* host, void* dev) {
       for (int iy = 0; iy <= L.ny; ++iy, ++n)
         for (int c = 0; c < 3; ++c)
           lay[L.n(ix, iy, iz) + c * L.ncomp] = ((m.hfix[n] >> c) & 1) ? T(0) : (T)host[3 * n + c];
-  CU(cudaMemcpy(dev, lay.data(), sizeof(T) * lay.size(), cudaMemcpyHostToDevice));
+  // stream-ordered: the context's stream is non-blocking, and a legacy-stream copy
+  // could land while a just-launched multigrid setup (its power steps use the
+  // level vectors) is still running
+  CU(cudaMemcpyAsync(dev, lay.data(), sizeof(T) * lay.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
   return TOPO_OK;
 }
 template <typename T>
@@ -3719,6 +3723,8 @@ int topo_mg_apply(topo_ctx* ctx, int32_t level, const double* x, double* y) {
   if (!ctx->mg_on) return set_err(ctx, TOPO_ESTATE, "topo_mg_apply: context has no multigrid hierarchy");
   if (level < 0 || level >= (int)ctx->mg.size()) return set_err(ctx, TOPO_EINVAL, "topo_mg_apply: bad level %d", level);
   cudaSetDevice(ctx->device);
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));   // the hierarchy is formed from E(xPhys)
   CK(mg_setup(ctx));
   if (level == 0) return topo_apply_K(ctx, x, y);
   MgLevel& m = ctx->mg[level];
@@ -3736,6 +3742,8 @@ int topo_mg_vcycle(topo_ctx* ctx, const double* b, double* z) {
   if (!ctx || !b || !z) return TOPO_EINVAL;
   if (!ctx->mg_on) return set_err(ctx, TOPO_ESTATE, "topo_mg_vcycle: context has no multigrid hierarchy");
   cudaSetDevice(ctx->device);
+  CK(ensure_constants(ctx));
+  if (!ctx->has_E) CK(update_modulus(ctx));   // the hierarchy is formed from E(xPhys)
   CK(mg_setup(ctx));
   CK(upload_nodes(ctx, b, &Slab::r));
   for (Slab& s : ctx->slabs)

@@ -135,3 +135,19 @@ def test_solo_timing_mode_runs_fixed_iterations(topo, monkeypatch, W, r):
         t = pr.timings()
         assert t["cg_iters"] == 7 and t["cg_iters_total"] == 14
         assert t["mg_fallbacks"] == 0 and t["mg_promotions"] == 0 and t["mg_theta_cuts"] == 0
+
+
+@pytest.mark.parametrize("W", [2, 4])
+def test_dist_levels_face_layout_loopback(topo, monkeypatch, W):
+    """Distributed level 1 with the face layout (forced): each slab writes the face
+    sums of its own node planes only; loopback slabs reproduce one slab."""
+    monkeypatch.setenv("TOPO_DIST_MIN_NODES", "0")
+    monkeypatch.setenv("TOPO_L1_FACE", "1")
+    p, f, fx, pas, x = _case(1)
+    b = np.where(fx == 0, random_vector(fx.size, seed=9), 0.0)
+    n1, z1, u1, it1, c1, x1 = _run(topo, p, f, fx, pas, x, b, topo.TOPO_DIST_SINGLE, 1)
+    nW, zW, uW, itW, cW, xW = _run(topo, p, f, fx, pas, x, b, topo.TOPO_DIST_LOOPBACK, W)
+    assert nW == 2
+    assert_rel(zW, z1, 1e-5, f"V-cycle W={W}")
+    assert abs(itW - it1) <= 1
+    assert_rel(cW, c1, 1e-9, f"c history W={W}")

@@ -309,3 +309,37 @@ def test_krylov_fp32_refinement(topo, dims, obst):
     assert np.linalg.norm(u - uo) <= 1e-8 * np.linalg.norm(uo)
     rt = np.where(fx != 0, 0.0, f - oracle.matvec_free(K, u, fx))
     assert np.linalg.norm(r - rt) <= 1e-6 * np.linalg.norm(f)    # the fp32 recursion tracks the true residual
+
+
+@pytest.mark.parametrize("dims,obst", [((48, 16, 8), (24.0, 8.0, 3.2)), ((37, 13, 5), (18.0, 6.0, 3.0)),
+                                       ((60, 20, 4), None)])
+@pytest.mark.parametrize("fp32", [0, 1])
+def test_l1_face_layout_matches_oracle(topo, monkeypatch, dims, obst, fp32):
+    """The face-accumulating level-1 operator (k_mg_l1_face: x-complete face sums
+    per node plane and element column, gathered from 4 faces; the default on
+    grids with >= 1 M level-1 elements) forced on small grids: A_1 x against the
+    oracle's Galerkin operator, and the V-cycle and K-cycle PCG solve against
+    the element-corner layout (same sums, another order)."""
+    p, f, fx, pas, x, K = _case(dims, obst, seed=4, mg_fp32=fp32)
+    lv = mg.hierarchy(K, fx, dims, coarse_max=1000)
+    assert len(lv) >= 3
+    xv = random_vector(lv[1]["K"].shape[0], seed=11)
+    yo = oracle.matvec_free(lv[1]["K"], xv, lv[1]["fixed"])
+    b = np.where(fx == 0, random_vector(K.shape[0], seed=12), 0.0)
+    out = {}
+    for face in ("1", "0"):
+        monkeypatch.setenv("TOPO_L1_FACE", face)
+        with topo.Problem(p, f, fx, pas) as pr:
+            pr.set_xphys(x)
+            y = pr.mg_apply(1, xv)
+            if fp32:
+                assert rel(y, yo)[0] <= 1e-5, f"A_1 fp32 face={face}"
+            else:
+                assert_rel(y, yo, 1e-12, f"A_1 face={face}")
+            z = pr.mg_vcycle(b)
+            u, info = pr.solve()
+            assert info["true_rel_res"] <= 1e-10
+            out[face] = (z, u, info["iters"])
+    assert_rel(out["1"][0], out["0"][0], 1e-5 if fp32 else 1e-11, "V-cycle face vs corners")
+    assert_rel(out["1"][1], out["0"][1], 1e-8, "u face vs corners")
+    assert abs(out["1"][2] - out["0"][2]) <= 1
