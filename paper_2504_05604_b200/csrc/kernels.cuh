@@ -197,6 +197,13 @@ k_update(Geo g, DevState* st, double* __restrict__ u, TK* __restrict__ r,
   }
 }
 
+// out = 1/v (0 where v = 0: padding elements): the filter's 1/Hs
+__global__ void k_recip(long long n, const double* __restrict__ v, double* __restrict__ out) {
+  pdl_enter();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = v[i] != 0.0 ? 1.0 / v[i] : 0.0;
+}
+
 // dst = (double) src over a whole buffer (the fp32 Krylov residual back into r after a solve)
 __global__ void k_f2d(long long n, const float* __restrict__ src, double* __restrict__ dst) {
   pdl_enter();

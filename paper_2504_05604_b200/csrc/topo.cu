@@ -127,7 +127,7 @@ struct Slab {
   uint8_t* fixm = nullptr;   // per node: bit c = DOF c fixed
   // element arrays: nelloc each
   double *E = nullptr, *x = nullptr, *xphys = nullptr, *dc = nullptr, *dcf = nullptr,
-         *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ce = nullptr, *xnew = nullptr,
+         *dvf = nullptr, *dv = nullptr, *hs = nullptr, *ihs = nullptr, *ce = nullptr, *xnew = nullptr,
          *oca = nullptr;   // OC: A = x sqrt(max(0, -dc~/dv~))
   double* vpad = nullptr;  // filter operand, zero-padded by R in y and z (FiltPad)
   FiltPad fp{};
@@ -975,7 +975,7 @@ int launch_filt25_r(topo_ctx* ctx, Slab& s, const double* a, double* out) {
   gx = (s.g.nex + CX - 1) / CX;
   auto kern = sym ? k_filt25<R, MODE, true> : k_filt25<R, MODE, false>;
   kern<<<dim3(gy, gz, (unsigned)gx), dim3(kF25Y, kF25Z / kF25TZ), L::BYTES, ctx->stream>>>(
-      s.m_vpad, s.g, s.fp, CX, a, s.hs, s.passive, out);
+      s.m_vpad, s.g, s.fp, CX, a, (MODE == F_X0 || MODE == F_PLAIN) ? s.ihs : s.hs, s.passive, out);
   ctx->launches++;
   debug_sync(ctx, "k_filt25");
   return check_launch(ctx);
@@ -2984,7 +2984,7 @@ int alloc_slab(topo_ctx* ctx, Slab& s) {
   for (double** v : nv) CK(al((void**)v, nb));
   CK(al((void**)&s.invd, sizeof(double) * g.ncomp));
   CK(al((void**)&s.fixm, g.ncomp));
-  double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ce, &s.xnew, &s.oca};
+  double** ev[] = {&s.E, &s.x, &s.xphys, &s.dc, &s.dcf, &s.dvf, &s.dv, &s.hs, &s.ihs, &s.ce, &s.xnew, &s.oca};
   for (double** v : ev) CK(al((void**)v, eb));
   CK(al((void**)&s.passive, g.nelloc));
   s.fp.R = ctx->R;
@@ -3022,7 +3022,7 @@ void free_ctx(topo_ctx* ctx) {
     void* ptrs[] = {s.u, s.r, s.p0, s.p1, s.q, s.f, s.invd, s.w, s.z, s.fixm, s.E, s.x, s.xphys, s.dc, s.dcf, s.oca,
                     s.vpad, s.res32, s.z32, s.w32, s.r32, s.q32, s.pw0, s.pw0_b, s.oc_counts, s.oc_offs, s.oc_cx, s.oc_cA, s.oc_cdv,
                     s.oc_cx2, s.oc_cA2, s.oc_cdv2, s.oc_n1,
-                    s.dvf, s.dv, s.hs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
+                    s.dvf, s.dv, s.hs, s.ihs, s.ce, s.xnew, s.passive, s.partials, s.counter, s.st, s.stage,
                     s.u_b, s.x_b, s.xphys_b};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -3372,6 +3372,7 @@ int topo_init(const topo_params* p, const double* load, const uint8_t* fixed, co
       LAUNCH(ctx, k_dot, grid_for(3LL * s.g.nown * s.g.nplane), s.g, s.st, s.f, s.f, 0, s.partials, s.counter);
       LAUNCH(ctx, k_filter<F_HS>, grid_for(s.g.nelloc), s.g, (int)ctx->st_off.size(), s.hs, s.hs, s.hs,
              s.passive, s.hs, 1);
+      LAUNCH(ctx, k_recip, grid_for(s.g.nelloc), s.g.nelloc, s.hs, s.ihs);
     }
     rc = check_launch(ctx);
   }
