@@ -369,7 +369,7 @@ k_sens(Geo g, DevState* st, Material m, const double* __restrict__ u,
 // loads per element; the next plane's loads are issued before the current
 // element's arithmetic).  Same per-element arithmetic as k_sens.
 constexpr int kSensCX = 16;
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 2)
 k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
          const double* __restrict__ E, const double* __restrict__ xphys,
          const uint8_t* __restrict__ passive, double* __restrict__ ce, double* __restrict__ dc,
@@ -399,6 +399,8 @@ k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
 #pragma unroll
       for (int j = 0; j < 4; ++j) B[c][j] = u[n0 + g.nplane + o[j] + c * g.ncomp];
     long long e = elem_idx(g, xa, ey, ez);
+    double Ee = E[e], xp = xphys[e];   // this element's scalars; the next element's are loaded one step ahead
+    uint8_t pv = passive[e];
     for (int ex = xa; ex < xb; ++ex, e += g.eplane) {
       double P[3][8], Q[3][8];
 #pragma unroll
@@ -416,8 +418,13 @@ k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
 #pragma unroll
           for (int j = 0; j < 4; ++j) B[c][j] = u[nn + o[j] + c * g.ncomp];
       }
-      const double Ee = E[e], xp = xphys[e];
-      const uint8_t pv = passive[e];
+      const double Ec = Ee, xc = xp;
+      const uint8_t pc = pv;
+      if (ex + 1 < xb) {
+        Ee = E[e + g.eplane];
+        xp = xphys[e + g.eplane];
+        pv = passive[e + g.eplane];
+      }
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -436,8 +443,8 @@ k_sens_x(Geo g, DevState* st, Material m, const double* __restrict__ u,
 #pragma unroll
         for (int k = 0; k < 8; ++k) sv = fma(P[c][k], Q[c][k], sv);
       ce[e] = sv;
-      dc[e] = pv ? 0.0 : -m.penal * simp_pow(xp, m.penal - 1.0) * (m.E0 - m.Emin) * sv;
-      csum = fma(Ee, sv, csum);
+      dc[e] = pc ? 0.0 : -m.penal * simp_pow(xc, m.penal - 1.0) * (m.E0 - m.Emin) * sv;
+      csum = fma(Ec, sv, csum);
     }
   }
   __shared__ double tot[1];
