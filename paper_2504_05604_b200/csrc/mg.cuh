@@ -1213,8 +1213,11 @@ k_mg_stencil(LvGeo L, const double* __restrict__ K, T* __restrict__ S) {
 // (kU: unroll of the 13 neighbour pairs; fully unrolled (13) the loads of all
 // 27 blocks are in flight together: 79 vs 91 us per level-2 apply at config 4,
 // the kernel is long-scoreboard bound on its L2/HBM gathers)
+#ifndef TOPO_ST_MINB
+#define TOPO_ST_MINB 3   // 80 registers, 3 CTAs/SM: 8.82 vs 8.92 ms per MG-PCG iteration at 125 registers, 2 CTAs/SM (same box)
+#endif
 template <typename T, int kU = 13>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, TOPO_ST_MINB)
 k_mg_apply_st(LvGeo L, const T* __restrict__ S, const T* __restrict__ x,
               const uint8_t* __restrict__ fix, T* __restrict__ q, const DevState* st) {
   pdl_enter();
