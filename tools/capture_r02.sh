@@ -23,7 +23,7 @@ gzip -f gpurun_out/${TAG}_launches_bench.csv
 K=0
 for spec in "k_mv_wht<.int.8, .int.2, .bool.1, .int.0,::2" "k_mv_wht<.int.8, .int.3, .bool.0, .int.2,::2" \
             "k_mv_wht<.int.8, .int.0, .bool.0, .int.1,::2" "k_mg_l1_face<float::4" "k_filt25::1" \
-            "k_sens_x::1" "k_update<.bool.1, .bool.1>::2" "k_mg_apply_st<float::4" "k_dgemm_nt64_tc::0" \
+            "k_sens_x::1" "k_update<.bool.1, .bool.1::2" "k_mg_apply_st<float::4" "k_dgemm_nt64_tc::0" \
             "k_mg_sweep_st8::40"; do
   re="${spec%%::*}"; skip="${spec##*::}"
   K=$((K+1))
