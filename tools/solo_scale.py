@@ -12,7 +12,9 @@ NVLink is NOT in it (one GPU per gpurun call; DESIGN.md §6 states the bytes).
 In SOLO mode the PCG runs exactly cg_max_iter = 20 iterations per solve (no
 convergence or breakdown exit: the decoupled slab is not the problem).
 
-   python tools/solo_scale.py [cfg=4] [W list=1,2,4,8] [iters=3]"""
+   python tools/solo_scale.py [cfg=4] [W list=1,2,4,8] [iters=3] [--weak]
+--weak: SURVEY config 4w, 128 x W element planes (128 x 256 x 256 per rank).
+"""
 import json
 import os
 import statistics as st
@@ -24,11 +26,14 @@ from workloads import make_problem  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 Ws = [int(w) for w in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4,8").split(",")]
-iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+iters = int(sys.argv[3]) if len(sys.argv) > 3 and not sys.argv[3].startswith("-") else 3
+weak = "--weak" in sys.argv
+out = {"cfg": f"{cfg}w" if weak else cfg, "scaling": "weak" if weak else "strong",
+       "what": "rank W//2's slab alone on one B200 (TOPO_DIST_SOLO), SIMP iterations 3.. of the run", "runs": {}}
 p, f, fx, pas = make_problem(cfg)
-out = {"cfg": cfg, "what": "rank W//2's slab alone on one B200 (TOPO_DIST_SOLO), SIMP iterations 3.. of the run",
-       "runs": {}}
 for W in Ws:
+    if weak:
+        p, f, fx, pas = make_problem(cfg, nelx=128 * W)
     r = W // 2
     dist = None if W == 1 else dict(mode=topo.TOPO_DIST_SOLO, rank=r, world=W, device=0)
     kw = {"dist": dist} if dist else {}
