@@ -35,19 +35,10 @@ template <int R> struct F25Smem {
   static constexpr int BYTES = kF25Stages * STAGE + 128;
 };
 
-// post-op of one output (k_filt_apply's arithmetic; modes X0 / PLAIN multiply by the
-// precomputed 1/Hs -- within 1 ulp of the division, which inlined its slow path
-// into the march loop: 665 vs ~150 us at config 4)
-template <int MODE>
-__device__ __forceinline__ double f25_post(double s, long long i, const double* __restrict__ a,
-                                           const double* __restrict__ hs, const uint8_t* __restrict__ passive) {
-  double r;
-  if (MODE == F_DIV) r = s;
-  else if (MODE == F_XDC) r = s / (hs[i] * fmax(1e-3, a[i]));
-  else r = s * hs[i];   // F_X0 / F_PLAIN: hs = 1/Hs (k_recip at init): no fp64 division in the march loop
-  if (MODE == F_X0 && passive[i]) r = passive[i] == kSolid ? 1.0 : 0.0;
-  return r;
-}
+// Post-op of an output (k_filt_apply's arithmetic): X0 / PLAIN multiply by the
+// precomputed 1/Hs (within 1 ulp of the division, whose inlined slow path in the
+// march loop made the x filter 665 vs ~150 us at config 4); its operands are
+// loaded before the step's TMA wait.
 
 // kSym: the cone weights depend on |d| only, so per input plane a thread first sums
 // its 4 z-outputs' inputs by (y, z) offset class {|dy|, |dz|} = {a, b} (1D y-pair
@@ -99,6 +90,23 @@ k_filt25(const __grid_constant__ CUtensorMap vmap, Geo g, FiltPad fp, int CX, co
     for (int j = 0; j < P; ++j) {
       const int t = tb + j;
       if (t >= nin) break;
+      // post-op operands of the output plane this step completes (t - 2R), loaded
+      // before the TMA wait and the arithmetic so their latency is hidden
+      double ph[kF25TZ];
+      uint8_t pp[kF25TZ];
+      if (MODE == F_X0 || MODE == F_PLAIN || MODE == F_XDC) {
+        const int to0 = t - 2 * R;
+#pragma unroll
+        for (int k = 0; k < kF25TZ; ++k) {
+          ph[k] = 1.0;
+          pp[k] = 0;
+          if (to0 >= 0 && col_ok && ez0 + k < g.nelz) {
+            const long long i = elem_idx(g, x0 + to0, ey, ez0 + k);
+            ph[k] = hs[i];
+            if (MODE == F_X0) pp[k] = passive[i];
+          }
+        }
+      }
       mbar_wait(&full[t % kF25Stages], (uint32_t)((t / kF25Stages) & 1));
       const double* sv = stage(t);
       if (kSym) {
@@ -175,7 +183,11 @@ k_filt25(const __grid_constant__ CUtensorMap vmap, Geo g, FiltPad fp, int CX, co
           const int ez = ez0 + k;
           if (col_ok && ez < g.nelz) {
             const long long i = elem_idx(g, xo, ey, ez);
-            out[i] = f25_post<MODE>(acc[es][k], i, a, hs, passive);
+            double r = acc[es][k];
+            if (MODE == F_XDC) r = r / (ph[k] * fmax(1e-3, a[i]));
+            else if (MODE != F_DIV) r = r * ph[k];   // X0 / PLAIN: hs = 1/Hs
+            if (MODE == F_X0 && pp[k]) r = pp[k] == kSolid ? 1.0 : 0.0;
+            out[i] = r;
           }
         }
       }
