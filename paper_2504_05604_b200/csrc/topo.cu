@@ -1435,6 +1435,16 @@ long long mg_deep_nodes() {
   const char* e = getenv("TOPO_DEEP_NODES");
   return e ? atoll(e) : kMgDeepNodesDefault;
 }
+// Stored levels up to this size run the fused warp-split sweeps (k_mg_sweep_st8);
+// larger ones the thread-per-node stencil apply + Jacobi kernels.  At config 4
+// level 3 (70.8 k nodes) is faster on the latter since the apply runs at 3 CTAs/SM
+// (8.73 vs 8.82 ms per MG-PCG iteration); level 4 (9.5 k) on the former (8.87 ms
+// with every stored level on the apply).  TOPO_SWEEP_NODES overrides it; never
+// above mg_deep_nodes() (tests set TOPO_DEEP_NODES=0 for the large-level paths).
+long long mg_sweep_nodes() {
+  const char* e = getenv("TOPO_SWEEP_NODES");
+  return std::min<long long>(e ? atoll(e) : 60000, mg_deep_nodes());
+}
 constexpr int kMgPowerSteps = 8;       // power steps of the smoother-weight estimate (M5)
 constexpr int kMgPowerStepsWarm = 1;   // later designs: continue from the previous design's vector
                                        // (1 vs 3 steps: same PCG iterations on configs 1-4 and the
@@ -1952,7 +1962,7 @@ int mg_apply(topo_ctx* ctx, int l, int gate) {
   const DevState* gst = gate ? s.st : nullptr;
   if (m.stored) {
     const long long sweep_nodes = getenv("TOPO_SWEEP_APPLY_NODES") ? atoll(getenv("TOPO_SWEEP_APPLY_NODES"))
-                                                                   : mg_deep_nodes();
+                                                                   : mg_sweep_nodes();
     if (m.S && m.L.nodes() <= sweep_nodes)   // small levels: the coalesced warp-split stencil kernel
       LAUNCH(ctx, (k_mg_sweep_st8<false, T>), (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16), m.L,
              mgp<T>(m.S), mgp<T>(m.x), mgp<T>(m.b), mgp<T>(m.invd), m.fixm, ctx->mg_om + l, mgp<T>(m.t), gst);
@@ -2136,7 +2146,7 @@ int enqueue_vcycle_t(topo_ctx* ctx, int l, int gate, bool dot) {
   MgLevel& m = ctx->mg[l];
   const int gL = grid_for(m.L.nodes());
   T *mx = mgp<T>(m.x), *mb = mgp<T>(m.b), *mt = mgp<T>(m.t), *mi = mgp<T>(m.invd);
-  if (m.S && m.L.nodes() <= mg_deep_nodes()) {
+  if (m.S && m.L.nodes() <= mg_sweep_nodes()) {
     // small stencil level: each damped-Jacobi sweep is one fused warp-split
     // stencil kernel (k_mg_sweep_st8) ping-ponging x and t
     const int gS = (int)std::min<long long>((m.L.nodes() + 31) / 32, 148LL * 8 * 16);   // 32 nodes per block
@@ -2229,7 +2239,7 @@ bool kc_level(const topo_ctx* ctx, int l) {
 }
 bool dl_deep(const topo_ctx* ctx, int l) {
   const MgLevel& m = ctx->mg[l];
-  return m.S && m.L.nodes() <= mg_deep_nodes();
+  return m.S && m.L.nodes() <= mg_sweep_nodes();
 }
 // t = A x on the owned planes of every slab (x ghosts current)
 template <typename T>
