@@ -91,7 +91,9 @@ extern "C" {
 
 /* distribution modes */
 #define TOPO_DIST_SINGLE   0
-#define TOPO_DIST_NCCL     1
+#define TOPO_DIST_NCCL     1   /* EXPERIMENTAL: the NCCL data plane has never run (every GPU box of
+                                  this build has one GPU); its control flow is the HOST mode's,
+                                  which is tested with 2-4 processes on one GPU                   */
 #define TOPO_DIST_LOOPBACK 2
 #define TOPO_DIST_HOST     3   /* one process per slab, host-staged shared-memory transport (tests) */
 #define TOPO_DIST_SOLO     4   /* measurement only: rank `rank`'s slab of a `world`-slab run, alone on
