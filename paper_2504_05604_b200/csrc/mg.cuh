@@ -1690,4 +1690,92 @@ k_dgemm_nt64_tc(const double* __restrict__ A, long long lda, const double* __res
       }
 }
 
+// Persistent, pipelined form of k_dgemm_nt64_tc (the level-2 Galerkin product):
+// one CTA per SM walks its M tiles; a tile's 128 x 64 A block is loaded ONCE and
+// kept for all N / 64 output blocks (the one-shot kernel re-read it per block);
+// the next stage's B block (64 x 64, L2-resident) and, at a tile boundary, the
+// next A block are in flight (cp.async, 8-byte, zero-filled past M) while the
+// current stage runs on the DMMA pipe.  Stage s = (tile s / nb, N block s % nb).
+// Row pitches 132 / 68 doubles: the m8n8k4 operand reads (lane = 4 g + tg,
+// address (k0 + tg) pitch + g) hit distinct banks.  Same k order as the one-shot
+// kernel (4-deep DMMA steps, k ascending): bitwise the same C.
+constexpr int kT2PA = 132, kT2PB = 68;
+constexpr int kT2Smem = (2 * kTcK * kT2PA + 2 * kTcK * kT2PB) * 8;   // 204 800 B: 1 CTA/SM
+__device__ __forceinline__ void cp_async8(double* s, const double* g, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(g), "r"(pred ? 8 : 0) : "memory");
+}
+__global__ void __launch_bounds__(256, 1)
+k_dgemm_nt64_tc2(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
+                 double* __restrict__ Cm, long long ldc, int M, int N, double alpha) {
+  pdl_enter();
+  extern __shared__ double tsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nb = N / kTcN;
+  const long long ntile = (M + kTcM - 1) / kTcM;
+  const long long my_tiles = ntile > blockIdx.x ? (ntile - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const long long S = my_tiles * nb;
+  auto bufA = [&](long long k) { return tsm + (k & 1) * (kTcK * kT2PA); };
+  auto bufB = [&](long long s) { return tsm + 2 * kTcK * kT2PA + (s & 1) * (kTcK * kT2PB); };
+  auto issue = [&](long long s) {   // stage s's B block, and its A block if s starts a tile
+    const long long k = s / nb;
+    const int jb = (int)(s - k * nb);
+    if (jb == 0) {
+      const long long i0 = (blockIdx.x + k * gridDim.x) * kTcM;
+      double* As = bufA(k);
+      for (int q = tid; q < kTcK * kTcM; q += 256) {
+        const int r = q & (kTcM - 1), t = q / kTcM;
+        const bool ok = i0 + r < M;
+        cp_async8(As + t * kT2PA + r, ok ? A + (i0 + r) + (long long)t * lda : A, ok);
+      }
+    }
+    double* Bs = bufB(s);
+    for (int q = tid; q < kTcK * kTcN; q += 256) {
+      const int r = q & (kTcN - 1), t = q / kTcN;
+      cp_async8(Bs + t * kT2PB + r, B + (jb * kTcN + r) + (long long)t * ldb, true);
+    }
+  };
+  if (S > 0) issue(0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;   // 4 x 2 warps
+  const int g = lane >> 2, tg = lane & 3;
+  for (long long s = 0; s < S; ++s) {
+    if (s + 1 < S) issue(s + 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const long long k = s / nb;
+    const int jb = (int)(s - k * nb);
+    const double* As = bufA(k);
+    const double* Bs = bufB(s);
+    double acc[4][4][2] = {};
+#pragma unroll 4
+    for (int k0 = 0; k0 < kTcK; k0 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = As[(k0 + tg) * kT2PA + wm + mi * 8 + g];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(k0 + tg) * kT2PB + wn + ni * 8 + g];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni], a[mi], b[ni]);
+    }
+    const long long i0 = (blockIdx.x + k * gridDim.x) * kTcM;
+    const int j0 = jb * kTcN;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const long long i = i0 + wm + mi * 8 + g;
+          const int j = j0 + wn + ni * 8 + tg * 2 + e;
+          if (i < M) Cm[i + (long long)j * ldc] = alpha * acc[mi][ni][e];
+        }
+    __syncthreads();   // stage s's buffers are refilled by issue(s + 2)
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 }  // namespace topo

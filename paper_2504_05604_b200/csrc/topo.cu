@@ -1749,12 +1749,19 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
       // K2 = Eg tab64^T: gather the 64 fine moduli per element, then one DGEMM
       // (nel x 64) x (64 x 576) into the entry-major [576][nel] layout
       LAUNCH(ctx, k_mg_gather64, grid_for(64 * ne), mgG(ctx), m.L, mgE(ctx), ctx->mg_Eg);
+      static const bool tc2 = !getenv("TOPO_TC2") || atoi(getenv("TOPO_TC2")) != 0;
       if (!ctx->tc_attr_set) {
         CU(cudaFuncSetAttribute(k_dgemm_nt64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+        CU(cudaFuncSetAttribute(k_dgemm_nt64_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, kT2Smem));
         ctx->tc_attr_set = true;
       }
-      k_dgemm_nt64_tc<<<dim3(576 / kTcN, (unsigned)((ne + kTcM - 1) / kTcM)), 256, kTcSmem, ctx->stream>>>(
-          ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0);
+      const long long ntile = (ne + kTcM - 1) / kTcM;
+      if (tc2)   // persistent: one CTA per SM, A tile kept across the 9 N blocks
+        k_dgemm_nt64_tc2<<<(unsigned)std::min<long long>(ntile, 148LL), 256, kT2Smem, ctx->stream>>>(
+            ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0);
+      else
+        k_dgemm_nt64_tc<<<dim3(576 / kTcN, (unsigned)ntile), 256, kTcSmem, ctx->stream>>>(
+            ctx->mg_Eg, ne, ctx->mg_tab64, 576, m.K, ne, (int)ne, 576, 1.0);
       ctx->launches++;
       debug_sync(ctx, "k_dgemm_nt64_tc(level-2 Galerkin)");
     } else {
