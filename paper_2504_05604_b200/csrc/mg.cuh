@@ -1362,6 +1362,48 @@ k_mg_sweep_st8(LvGeo L, const T* __restrict__ S, const T* __restrict__ src, cons
 // Coarsest level (M6): dense matrix over free DOFs, Gauss-Jordan inverse,
 // dense solve.
 // ---------------------------------------------------------------------------
+// Thread per (row DOF, neighbour node): A[row][3 neighbour columns] = the sum
+// over the elements that hold both nodes, in k_mg_dense_fill's element order
+// (dz, dx, dy) -- bitwise its result -- but 81 threads per node instead of one
+// (the thread-per-node form ran the whole 225-node coarsest level of config 4
+// in one CTA: 330 us of serial, strided read-modify-writes).  A is zeroed
+// beforehand; every written entry has exactly one owner.
+__global__ void __launch_bounds__(kBlock)
+k_mg_dense_fill27(LvGeo L, const double* __restrict__ K, const int* __restrict__ dmap, int ld,
+                  double* __restrict__ A) {
+  pdl_enter();
+  const long long tot = L.nodes() * 81, nel = L.nel();
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long k = t / 81;
+    const int rem = (int)(t - k * 81), ci = rem / 27, o = rem - ci * 27;
+    int ix, iy, iz;
+    lv_decode(L, k, ix, iy, iz);
+    const int row = dmap[L.n(ix, iy, iz) + ci * L.ncomp];
+    const int jx = ix + o % 3 - 1, jy = iy + (o / 3) % 3 - 1, jz = iz + o / 9 - 1;
+    if (row < 0 || jx < 0 || jx > L.nx || jy < 0 || jy > L.ny || jz < 0 || jz > L.nz) continue;
+    const long long nb = L.n(jx, jy, jz);
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dx = 0; dx < 2; ++dx)
+        for (int dy = 0; dy < 2; ++dy) {
+          const int ex = ix - 1 + dx, ey = iy - 1 + dy, ez = iz - 1 + dz;
+          if (ex < 0 || ex >= L.nx || ey < 0 || ey >= L.ny || ez < 0 || ez >= L.nz) continue;
+          const int cx = jx - ex, cy = jy - ey, cz = jz - ez;
+          if (cx < 0 || cx > 1 || cy < 0 || cy > 1 || cz < 0 || cz > 1) continue;
+          const long long e = ((long long)ex * L.nz + ez) * L.ny + ey;
+          const int a = mg_lidx(1 - dx, 1 - dy, 1 - dz), bb = mg_lidx(cx, cy, cz);
+#pragma unroll
+          for (int cj = 0; cj < 3; ++cj) s[cj] += K[(long long)((3 * a + ci) * 24 + 3 * bb + cj) * nel + e];
+        }
+#pragma unroll
+    for (int cj = 0; cj < 3; ++cj) {
+      const int col = dmap[nb + cj * L.ncomp];
+      if (col >= 0) A[(long long)row * ld + col] = s[cj];
+    }
+  }
+}
+
 // dmap[level idx of DOF] = dense index or -1 (fixed / pad).  Thread per node:
 // it owns (zeroes and fills) its rows; no atomics.
 __global__ void __launch_bounds__(kBlock)
@@ -1427,7 +1469,7 @@ __global__ void __launch_bounds__(kGjB * kGjB / kGjInvNJ)
 k_sw_block_inv(const double* __restrict__ S, int ld, int k0, double* __restrict__ P) {
   pdl_enter();
   constexpr int NJ = kGjInvNJ, JS = kGjB / NJ;
-  __shared__ double col[kGjB], row[kGjB];
+  __shared__ double col[kGjB], row[kGjB], pinv;
   const int i = threadIdx.x % kGjB, j0 = threadIdx.x / kGjB;
   double a[NJ];
 #pragma unroll
@@ -1437,9 +1479,10 @@ k_sw_block_inv(const double* __restrict__ S, int ld, int k0, double* __restrict_
     for (int m = 0; m < NJ; ++m) {
       if (j0 + JS * m == k) col[i] = a[m];
       if (i == k) row[j0 + JS * m] = a[m];
+      if (i == k && j0 + JS * m == k) pinv = 1.0 / a[m];   // one fp64 division per pivot, not one per thread
     }
     __syncthreads();
-    const double ip = 1.0 / col[k];
+    const double ip = pinv;
     const double cik = col[i];
 #pragma unroll
     for (int m = 0; m < NJ; ++m) {

@@ -1854,7 +1854,9 @@ int enqueue_mg_setup(topo_ctx* ctx, bool warm) {
   const int np = ctx->mg_npad;
   double* A = ctx->mg_A0;
   CU(cudaMemsetAsync(A, 0, sizeof(double) * (size_t)np * np, ctx->stream));
-  LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, np, A);
+  static const bool fill27 = !getenv("TOPO_FILL27") || atoi(getenv("TOPO_FILL27")) != 0;
+  if (fill27) LAUNCH(ctx, k_mg_dense_fill27, grid_for(c.L.nodes() * 81), c.L, c.K, ctx->mg_dmap, np, A);
+  else LAUNCH(ctx, k_mg_dense_fill, grid_for(c.L.nodes()), c.L, c.K, ctx->mg_dmap, np, A);
   if (np > n) LAUNCH(ctx, k_gj_pad, 1, A, n, np);
   // A <- A^-1 in place (coarsest dense inverse, reading M6): symmetric blocked
   // sweep (mg.cuh), lower triangle, rank-64 updates by k_dgemm_nt64
