@@ -1000,12 +1000,24 @@ constexpr int kL1CX = 16;
 #ifndef TOPO_L1F_MINB
 #define TOPO_L1F_MINB 3
 #endif
-template <typename T, typename TE = double>
+// kAsync (TOPO_L1F_ASYNC, default): the NEXT step's 12 node values and 8 child
+// moduli travel global -> shared by per-thread cp.async (4 / 8 bytes, the thread's
+// own slots, two buffers in turn) while this step's element arithmetic runs, so a
+// warp no longer waits out the DRAM latency at the top of every step (ncu r02s:
+// 38 % long-scoreboard stalls at 12 warps/SM).  Same values, same arithmetic.
+template <int B>
+__device__ __forceinline__ void cp_async_own(void* s, const void* gp) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(sa), "l"(gp), "n"(B) : "memory");
+}
+template <typename T, typename TE = double, bool kAsync = false>
 __global__ void __launch_bounds__(kL1Block, (sizeof(T) == 4 ? TOPO_L1F_MINB : 3))
 k_mg_l1_face(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x, T* __restrict__ F,
              const DevState* st) {
   pdl_enter();
   MG_GATE(st);
+  __shared__ T sB[kAsync ? 2 : 1][kAsync ? 12 : 1][kAsync ? kL1Block : 1];
+  __shared__ TE sE[kAsync ? 2 : 1][kAsync ? 8 : 1][kAsync ? kL1Block : 1];
   const int nx = L.nx, ny = L.ny;
   const long long ncol = (long long)L.ny * L.nz;
   const int plo = L.xa, phi = L.xlast() + 1;              // node planes [plo, phi)
@@ -1036,17 +1048,39 @@ k_mg_l1_face(Geo g, LvGeo L, const TE* __restrict__ E, const T* __restrict__ x, 
         sA[c * 4 + j][threadIdx.x] = p0 - 1 >= 0 ? xp[(j >> 1) * NY + (j & 1) + c * L.ncomp] : T(0);
       }
     const TE* ep = E + ebase;
+    // step ex's operands -> buffer b (only where the step itself would load them)
+    auto prefetch = [&](int ex, const T* xq, const TE* eq, int b) {
+      if (ex >= 0 && ex < nx && ex < p1) {
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch)
+          cp_async_own<sizeof(TE)>(&sE[b][ch][threadIdx.x], eq + (ch & 1) * (eplane2 / 2) + (ch >> 2) * EY + ((ch >> 1) & 1));
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            cp_async_own<sizeof(T)>(&sB[b][c * 4 + j][threadIdx.x], xq + onp + (j >> 1) * NY + (j & 1) + c * L.ncomp);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (kAsync) prefetch(p0 - 1, xp, ep, 0);
     for (int ex = p0 - 1; ex < p1; ++ex, xp += onp, ep += eplane2, fp += fstep) {
       T Yh[3][8];
+      const int b = kAsync ? ((ex - (p0 - 1)) & 1) : 0;
+      if constexpr (kAsync) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        prefetch(ex + 1, xp + onp, ep + eplane2, b ^ 1);
+      }
       if (ex >= 0 && ex < nx) {
         T W[3][8], Ech[8];
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) Ech[ch] = (T)ep[(ch & 1) * (eplane2 / 2) + (ch >> 2) * EY + ((ch >> 1) & 1)];
+        for (int ch = 0; ch < 8; ++ch)
+          Ech[ch] = kAsync ? (T)sE[b][ch][threadIdx.x]
+                           : (T)ep[(ch & 1) * (eplane2 / 2) + (ch >> 2) * EY + ((ch >> 1) & 1)];
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            const T bn = xp[onp + (j >> 1) * NY + (j & 1) + c * L.ncomp];
+            const T bn = kAsync ? sB[b][c * 4 + j][threadIdx.x] : xp[onp + (j >> 1) * NY + (j & 1) + c * L.ncomp];
             W[c][2 * j] = sA[c * 4 + j][threadIdx.x];
             W[c][2 * j + 1] = bn;
             sA[c * 4 + j][threadIdx.x] = bn;

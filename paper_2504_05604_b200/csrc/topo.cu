@@ -1708,9 +1708,13 @@ int launch_l1_elem(topo_ctx* ctx, MgLevel& m, const DevState* gst, const LvGeo* 
   if (ctx->l1_face) {   // face sums (k_mg_l1_face): one thread per (column, chunk of kL1CX node planes)
     const long long nt = (long long)L.ny * L.nz * ((L.xlast() - L.xa + 1 + kL1CX - 1) / kL1CX);
     const unsigned nbf = (unsigned)std::max(1LL, std::min<long long>((nt + kL1Block - 1) / kL1Block, 148LL * 3 * 16));
-    if (sizeof(T) == 4)
-      k_mg_l1_face<T, float><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y, gst);
-    else
+    static const bool l1f_async = !getenv("TOPO_L1F_ASYNC") || atoi(getenv("TOPO_L1F_ASYNC")) != 0;
+    if constexpr (sizeof(T) == 4) {
+      if (l1f_async)
+        k_mg_l1_face<T, float, true><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y, gst);
+      else
+        k_mg_l1_face<T, float, false><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y, gst);
+    } else
       k_mg_l1_face<T, double><<<nbf, kL1Block, 0, ctx->stream>>>(mgG(ctx), L, mgE(ctx), x, Y, gst);
   } else if (sizeof(T) == 4)   // fp32 moduli (k_mg_e32 at setup)
     k_mg_l1_elem<T, float><<<(unsigned)std::max(1LL, nb), kL1Block, 0, ctx->stream>>>(mgG(ctx), L, ctx->mg_E32, x, Y,
